@@ -1,0 +1,267 @@
+/*
+ * relaykv_b200.h -- C ABI of the B200-native RelayCaching relay-prefill engine.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (BASELINE.json north_star). The reference exposes a
+ * C++ API only (/root/reference/proj/include/relaykv/relay_engine.hpp:142-163,
+ * model.hpp:116-152); every entry point below replaces one reference function
+ * and is cited next to it. Plain pointers and sizes only: no torch or CUDA
+ * types cross this boundary. The C++ drop-in (namespace relaykv, same headers
+ * as the reference) and the Python host mirror both sit on top of it.
+ *
+ * Conventions
+ *  - Every call returns an rk_status. A non-zero status maps 1:1 to the
+ *    exception type the reference throws on the same condition (see
+ *    rk_status); rk_last_error() returns the message (thread-local).
+ *  - Host output pointers are optional: NULL means "do not copy back". With all
+ *    output pointers NULL a call is device-resident end to end.
+ *  - Layouts are the reference's: row-major fp32, x.W convention,
+ *    KVContext rows [layer][pos][kv_dim] with head h at [h*d_head,(h+1)*d_head),
+ *    SegmentMarks origin layer-major [L x n] (relay_engine.hpp:26-35).
+ */
+#ifndef RELAYKV_B200_H_
+#define RELAYKV_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RK_ABI_VERSION 1
+
+/* Status codes, one per reference exception type on this path
+ * (SURVEY.md 8(b) "Errors"). */
+typedef enum rk_status {
+  RK_OK = 0,
+  RK_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument (shapes, capacity, snapshot, alpha) */
+  RK_ERR_SCHEMA = 2,           /* relaykv::SchemaError (profile window, profiler.cpp:28-35) */
+  RK_ERR_LOGIC = 3,            /* std::logic_error (accounting, relay_engine.cpp:57-66) */
+  RK_ERR_NONFINITE = 4,        /* std::runtime_error "<what>: non-finite value" (tensor.cpp:58-64) */
+  RK_ERR_RUNTIME = 5           /* other std::runtime_error: CUDA failure, out of memory */
+} rk_status;
+
+/* Numerics of a weights object (and of everything computed with it).
+ *  RK_FP32_EXACT: fp32 storage; every kernel replays the reference's
+ *    operation order (sequential-k matmul without FMA, glibc-identical expf,
+ *    double RoPE from a host cos/sin table) so results are bit-identical to
+ *    the reference CPU path.
+ *  RK_BF16: bf16 weights and KV context, tcgen05 tensor-core GEMMs with fp32
+ *    accumulation, flash attention; throughput mode, reports its own error. */
+typedef enum rk_precision { RK_FP32_EXACT = 0, RK_BF16 = 1 } rk_precision;
+
+/* RelayMode (relay_engine.hpp:17-22). */
+typedef enum rk_relay_mode {
+  RK_MODE_FULL = 0,
+  RK_MODE_ZERO = 1,
+  RK_MODE_RELAY = 2,
+  RK_MODE_BLEND = 3
+} rk_relay_mode;
+
+/* SelectionTag bits (selector.hpp:21-26). */
+enum {
+  RK_SEL_DEVIATION = 1u << 0,
+  RK_SEL_INFLUENCE_SCORE = 1u << 1,
+  RK_SEL_INFLUENCE_SUFFIX = 1u << 2,
+  RK_SEL_BLEND_TOPK = 1u << 3
+};
+
+/* ModelSpec (model.hpp:21-38). */
+typedef struct rk_model_spec {
+  uint64_t num_layers;
+  uint64_t d_model;
+  uint64_t num_heads;
+  uint64_t num_kv_heads;
+  uint64_t d_head;
+  uint64_t d_ff;
+  uint64_t vocab_size;
+  float theta_base;
+  uint64_t max_positions;
+  float norm_eps;
+} rk_model_spec;
+
+/* LayerProfile's window (profiler.hpp:30-43): l_start <= l_det <= l_end < L. */
+typedef struct rk_layer_profile {
+  uint64_t l_start;
+  uint64_t l_det;
+  uint64_t l_end;
+} rk_layer_profile;
+
+/* RelayOptions + SelectionThresholds (relay_engine.hpp:119-126, selector.hpp:13-19). */
+typedef struct rk_relay_options {
+  int32_t mode;              /* rk_relay_mode */
+  double tau_dev;            /* 1.5 */
+  double tau_inf;            /* 1.45 */
+  uint64_t suffix_k;         /* 10 */
+  double blend_alpha;        /* 0.2, BLEND only: recompute ratio */
+  int32_t rectify_above_end; /* ablation flag */
+} rk_relay_options;
+
+/* Host view of a RelayCache (relay_cache.hpp:23-46); all arrays fp32 / int32. */
+typedef struct rk_relay_cache_view {
+  uint64_t num_layers;
+  uint64_t num_kv_heads;
+  uint64_t d_head;
+  uint64_t d_model;
+  float theta_base;
+  uint64_t max_positions;
+  uint64_t segment_len;
+  const int32_t* segment_tokens; /* [n] */
+  uint64_t source_base_position;
+  uint64_t snapshot_layer;
+  uint64_t decode_steps_observed;
+  const float* const* k_pre;    /* [L] -> [n x kv_dim], keys BEFORE rotation */
+  const float* const* v;        /* [L] -> [n x kv_dim] */
+  const float* hidden_snapshot; /* [n x d_model], input to snapshot_layer */
+  const float* influence;       /* [n], >= 0 */
+} rk_relay_cache_view;
+
+/* PhaseTimings (relay_engine.hpp:42-49). Device phases are CUDA-event times. */
+typedef struct rk_phase_timings {
+  double fresh_ms, realign_ms, recompute_ms, selection_ms, rectify_ms, total_ms;
+} rk_phase_timings;
+
+/* ReuseStats (relay_engine.hpp:53-71). */
+typedef struct rk_reuse_stats {
+  uint64_t total_entries;
+  uint64_t recomputed_entries;
+  double reuse_rate;
+  uint64_t selected_count;
+  uint64_t selected_deviation;
+  uint64_t selected_influence_score;
+  uint64_t selected_influence_suffix;
+  uint64_t selected_blend;
+  double flops_cost;
+  double flops_selection;
+  double flops_realign;
+  double flops_full_equiv;
+  rk_phase_timings wall;
+} rk_reuse_stats;
+
+/* RelayOutput (relay_engine.hpp:128-137) + SegmentMarks of the new segment.
+ * Caller-owned host buffers sized for the segment length n; any may be NULL. */
+typedef struct rk_relay_output {
+  uint64_t* selection_indices; /* [n] sorted ascending */
+  uint32_t* selection_tags;    /* [n] RK_SEL_* bits */
+  double* s_dev;               /* [n] value deviation at l_det (RELAY only) */
+  double* s_key_dev;           /* [n] key deviation at l_det (RELAY only) */
+  float* segment_hidden;       /* [n x d_model] */
+  uint64_t* hidden_depth;      /* [n] */
+  uint8_t* origin;             /* [L x n] layer-major, 0 reused / 1 recomputed */
+  /* filled by the call */
+  uint64_t segment_base;
+  uint64_t segment_len;
+  uint64_t selection_count;
+  uint64_t s_dev_len;          /* n in RELAY mode, else 0 (reference leaves them empty) */
+  double dev_threshold;        /* tau_dev * mean(s_dev), or 0 */
+  double min_dev_margin;       /* min_j |s_dev[j]-thr|/thr: selection certification margin */
+  rk_reuse_stats stats;
+} rk_relay_output;
+
+typedef struct rk_engine rk_engine;
+typedef struct rk_weights rk_weights;
+typedef struct rk_cache rk_cache;
+typedef struct rk_context rk_context;
+
+/* ---- engine ------------------------------------------------------------ */
+int rk_abi_version(void);
+const char* rk_last_error(void);
+/* One engine per device: owns a stream, scratch arena, RoPE cos/sin tables. */
+int rk_engine_create(int device, rk_engine** out);
+void rk_engine_destroy(rk_engine* e);
+int rk_engine_synchronize(rk_engine* e);
+/* Opaque cudaStream_t of the engine (for external event timing). */
+void* rk_engine_stream(rk_engine* e);
+/* Number of engine kernel launches issued so far (instrumentation). */
+uint64_t rk_engine_launch_count(rk_engine* e);
+/* CUDA-graph replay of repeated identical rk_agent_prefill calls (0/1). */
+int rk_engine_set_graphs(rk_engine* e, int enable);
+
+/* ---- weights (model.hpp:42-58) ----------------------------------------- */
+/* == init_weights(spec, seed) (model.cpp:81-114) computed on the device,
+ * without spec.validate() (model.cpp:82) so 2-layer specs are accepted. */
+int rk_weights_init(rk_engine* e, const rk_model_spec* spec, uint64_t seed, int precision,
+                    rk_weights** out);
+/* Upload host tensors in weights_io.cpp tensor_table order (weights_io.cpp:21-38). */
+int rk_weights_upload(rk_engine* e, const rk_model_spec* spec, const float* const* tensors,
+                      uint64_t n_tensors, int precision, rk_weights** out);
+uint64_t rk_weights_num_tensors(const rk_model_spec* spec);
+/* Copy tensor #index (tensor_table order) back to host as fp32. */
+int rk_weights_export(rk_weights* w, uint64_t index, float* out, uint64_t count);
+void rk_weights_destroy(rk_weights* w);
+
+/* ---- relay cache (relay_cache.hpp:23-46) ------------------------------- */
+/* Validates like RelayCache::validate (relay_cache.cpp:18-41), then uploads. */
+int rk_cache_upload(rk_engine* e, rk_weights* w, const rk_relay_cache_view* view,
+                    rk_cache** out);
+/* Decode-time capture on the device (relay_cache.cpp:68-136 via
+ * model.cpp:372-389): greedy-decodes n tokens after ctx, recording pre-RoPE
+ * K, V, the hidden input of snapshot_layer and influence. first_logits: the
+ * prompt-end logits row [V] on the host, or NULL to use the context's last
+ * computed row. */
+int rk_cache_capture_decode(rk_engine* e, rk_weights* w, rk_context* ctx,
+                            const float* first_logits, uint64_t n, uint64_t snapshot_layer,
+                            int include_self, rk_cache** out);
+/* Capture by chunked prefill of given segment tokens (prefill == decode, test_model.cpp:78-101). */
+int rk_cache_capture_prefill(rk_engine* e, rk_weights* w, rk_context* ctx,
+                             const int32_t* segment_tokens, uint64_t n, uint64_t snapshot_layer,
+                             int include_self, rk_cache** out);
+uint64_t rk_cache_segment_len(const rk_cache* c);
+/* Copy a cache back to host (fp32). Any pointer may be NULL. k_pre/v: [L] arrays of [n x kv]. */
+int rk_cache_export(rk_cache* c, int32_t* tokens, float* const* k_pre, float* const* v,
+                    float* hidden_snapshot, float* influence, uint64_t* source_base,
+                    uint64_t* snapshot_layer);
+void rk_cache_destroy(rk_cache* c);
+
+/* ---- merged KV context (model.hpp:68-87, relay_engine.hpp:37-40) ------- */
+int rk_context_create(rk_engine* e, rk_weights* w, rk_context** out);
+int rk_context_clone(rk_context* src, rk_context** out);
+uint64_t rk_context_size(const rk_context* c);
+uint64_t rk_context_num_segments(const rk_context* c);
+int rk_context_segment(rk_context* c, uint64_t index, uint64_t* base, uint64_t* len,
+                       uint8_t* origin /* [L x len] or NULL */);
+/* Rows [pos_begin, pos_begin+count) of one layer, fp32. */
+int rk_context_export(rk_context* c, uint64_t layer, uint64_t pos_begin, uint64_t count,
+                      float* k, float* v);
+void rk_context_destroy(rk_context* c);
+
+/* ---- hot path ------------------------------------------------------------ */
+/* prefill (model.cpp:305-331): fresh rows at base_position == ctx size.
+ * last_logits: logits of the last row [V] (NULL = not computed). */
+int rk_prefill(rk_engine* e, rk_weights* w, rk_context* ctx, const int32_t* tokens, uint64_t n,
+               uint64_t base_position, float* last_logits);
+/* relay_extend (relay_engine.cpp:183-361): appends one relayed segment at ctx size. */
+int rk_relay_extend(rk_engine* e, rk_weights* w, rk_context* ctx, rk_cache* cache,
+                    const rk_layer_profile* profile, const rk_relay_options* opts,
+                    rk_relay_output* out);
+/* relay_prefill (relay_engine.cpp:363-395): fresh prefix prefill into an empty
+ * ctx, relay_extend, then the segment-end logits (row_logits_from_layer,
+ * model.cpp:339-362). */
+int rk_relay_prefill(rk_engine* e, rk_weights* w, rk_context* ctx, const int32_t* prefix,
+                     uint64_t n_prefix, rk_cache* cache, const rk_layer_profile* profile,
+                     const rk_relay_options* opts, rk_relay_output* out,
+                     float* segment_end_logits);
+/* The downstream agent's TTFT sequence of run_workflow's relay branch
+ * (workflow.cpp:316-369): prefix prefill, relay_extend per upstream cache in
+ * order, then the suffix prefill's last-row logits (or, with no suffix, the
+ * last segment row as a pure query), then argmax (model.cpp:364-370).
+ * mode RK_MODE_FULL prefills prefix ++ segments ++ suffix from scratch
+ * (workflow.cpp:301-315). outs: [n_upstream] or NULL. */
+int rk_agent_prefill(rk_engine* e, rk_weights* w, rk_context* ctx, const int32_t* prefix,
+                     uint64_t n_prefix, rk_cache* const* upstream, uint64_t n_upstream,
+                     const int32_t* suffix, uint64_t n_suffix, const rk_layer_profile* profile,
+                     const rk_relay_options* opts, rk_relay_output* outs, float* end_logits,
+                     int32_t* first_token);
+
+/* ---- analytic FLOP model (relay_engine.cpp:72-128) ---------------------- */
+double rk_flops_span_full(const rk_model_spec* s, uint64_t base, uint64_t n);
+double rk_flops_segment_schedule(const rk_model_spec* s, uint64_t base, uint64_t n,
+                                 uint64_t band_lo, uint64_t band_hi, uint64_t sparse_hi,
+                                 uint64_t selected);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* RELAYKV_B200_H_ */
