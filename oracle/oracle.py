@@ -63,37 +63,37 @@ class Oracle:
         self.lib = C.CDLL(LIB_PATHS[kind])
         self.pre = "ref_" if kind == "reference" else "orc_"
         L = self.lib
-        L[self.pre + "last_error"].restype = C.c_char_p
+        getattr(L, self.pre + "last_error").restype = C.c_char_p
         for name in ("weights_tensor",):
-            L[self.pre + name].restype = F32P
-            L[self.pre + name].argtypes = [P, U64, C.POINTER(U64)]
+            getattr(L, self.pre + name).restype = F32P
+            getattr(L, self.pre + name).argtypes = [P, U64, C.POINTER(U64)]
         for name in ("ctx_size", "ctx_num_segments"):
-            L[self.pre + name].restype = U64
-            L[self.pre + name].argtypes = [P]
-        L[self.pre + "flops_span_full"].restype = C.c_double
-        L[self.pre + "flops_span_full"].argtypes = [C.POINTER(ModelSpec), U64, U64]
-        L[self.pre + "flops_segment_schedule"].restype = C.c_double
-        L[self.pre + "flops_segment_schedule"].argtypes = [C.POINTER(ModelSpec), U64, U64, U64, U64, U64, U64]
+            getattr(L, self.pre + name).restype = U64
+            getattr(L, self.pre + name).argtypes = [P]
+        getattr(L, self.pre + "flops_span_full").restype = C.c_double
+        getattr(L, self.pre + "flops_span_full").argtypes = [C.POINTER(ModelSpec), U64, U64]
+        getattr(L, self.pre + "flops_segment_schedule").restype = C.c_double
+        getattr(L, self.pre + "flops_segment_schedule").argtypes = [C.POINTER(ModelSpec), U64, U64, U64, U64, U64, U64]
         fx = "ref_host_expf" if kind == "reference" else "orc_host_expf"
-        L[fx].restype = C.c_float
-        L[fx].argtypes = [C.c_float]
-        self._expf = L[fx]
+        getattr(L, fx).restype = C.c_float
+        getattr(L, fx).argtypes = [C.c_float]
+        self._expf = getattr(L, fx)
         if kind == "restatement":
             for name in ("weights_init", "ctx_create", "ctx_clone"):
-                L["orc_" + name].restype = P
+                getattr(L, "orc_" + name).restype = P
             L.orc_weights_init.argtypes = [C.POINTER(ModelSpec), U64]
             L.orc_ctx_create.argtypes = [P]
             L.orc_ctx_clone.argtypes = [P]
             L.orc_mean_head_cosine_deviation.restype = C.c_double
             L.orc_mean_head_cosine_deviation.argtypes = [F32P, F32P, U64, U64]
         for name in ("weights_destroy", "ctx_destroy", "cache_destroy"):
-            L[self.pre + name].argtypes = [P]
-            L[self.pre + name].restype = None
+            getattr(L, self.pre + name).argtypes = [P]
+            getattr(L, self.pre + name).restype = None
 
     # ---- error handling -------------------------------------------------
     def _check(self, st):
         if st != 0:
-            raise exception_for(st, self.lib[self.pre + "last_error"]().decode())
+            raise exception_for(st, getattr(self.lib, self.pre + "last_error")().decode())
 
     # ---- weights ----------------------------------------------------------
     def weights(self, spec, seed, checked=False):
@@ -103,13 +103,13 @@ class Oracle:
             ptr = out.value
         else:
             ptr = self.lib.orc_weights_init(C.byref(spec), U64(seed))
-        h = _Handle(self.lib, ptr, self.lib[self.pre + "weights_destroy"])
+        h = _Handle(self.lib, ptr, getattr(self.lib, self.pre + "weights_destroy"))
         h.spec = spec
         return h
 
     def weights_tensor(self, w, idx):
         n = U64()
-        p = self.lib[self.pre + "weights_tensor"](P(w.ptr), U64(idx), C.byref(n))
+        p = getattr(self.lib, self.pre + "weights_tensor")(P(w.ptr), U64(idx), C.byref(n))
         return np.ctypeslib.as_array(p, (n.value,)).copy()
 
     # ---- contexts -----------------------------------------------------------
@@ -120,7 +120,7 @@ class Oracle:
             ptr = out.value
         else:
             ptr = self.lib.orc_ctx_create(P(w.ptr))
-        h = _Handle(self.lib, ptr, self.lib[self.pre + "ctx_destroy"])
+        h = _Handle(self.lib, ptr, getattr(self.lib, self.pre + "ctx_destroy"))
         h.spec = w.spec
         return h
 
@@ -131,12 +131,12 @@ class Oracle:
             ptr = out.value
         else:
             ptr = self.lib.orc_ctx_clone(P(ctx.ptr))
-        h = _Handle(self.lib, ptr, self.lib[self.pre + "ctx_destroy"])
+        h = _Handle(self.lib, ptr, getattr(self.lib, self.pre + "ctx_destroy"))
         h.spec = ctx.spec
         return h
 
     def ctx_size(self, ctx):
-        return int(self.lib[self.pre + "ctx_size"](P(ctx.ptr)))
+        return int(getattr(self.lib, self.pre + "ctx_size")(P(ctx.ptr)))
 
     def ctx_export(self, ctx, layer, pos=0, count=None):
         kv = ctx.spec.kv_dim
@@ -144,7 +144,7 @@ class Oracle:
             count = self.ctx_size(ctx) - pos
         k = np.empty((count, kv), np.float32)
         v = np.empty((count, kv), np.float32)
-        self._check(self.lib[self.pre + "ctx_export"](P(ctx.ptr), U64(layer), U64(pos), U64(count),
+        self._check(getattr(self.lib, self.pre + "ctx_export")(P(ctx.ptr), U64(layer), U64(pos), U64(count),
                                                       k.ctypes.data_as(F32P), v.ctypes.data_as(F32P)))
         return k, v
 
@@ -155,11 +155,11 @@ class Oracle:
 
     def ctx_segments(self, ctx):
         segs = []
-        for i in range(int(self.lib[self.pre + "ctx_num_segments"](P(ctx.ptr)))):
+        for i in range(int(getattr(self.lib, self.pre + "ctx_num_segments")(P(ctx.ptr)))):
             base, ln = U64(), U64()
-            self._check(self.lib[self.pre + "ctx_segment"](P(ctx.ptr), U64(i), C.byref(base), C.byref(ln), None))
+            self._check(getattr(self.lib, self.pre + "ctx_segment")(P(ctx.ptr), U64(i), C.byref(base), C.byref(ln), None))
             origin = np.empty(ctx.spec.num_layers * ln.value, np.uint8)
-            self._check(self.lib[self.pre + "ctx_segment"](P(ctx.ptr), U64(i), C.byref(base), C.byref(ln),
+            self._check(getattr(self.lib, self.pre + "ctx_segment")(P(ctx.ptr), U64(i), C.byref(base), C.byref(ln),
                                                            origin.ctypes.data_as(C.POINTER(C.c_uint8))))
             segs.append((base.value, ln.value, origin.reshape(ctx.spec.num_layers, ln.value)))
         return segs
@@ -169,14 +169,14 @@ class Oracle:
         a, p = _i32(tokens)
         base = self.ctx_size(ctx) if base is None else base
         out = np.empty(w.spec.vocab_size, np.float32) if logits else None
-        self._check(self.lib[self.pre + "prefill"](P(w.ptr), P(ctx.ptr), p, U64(len(a)), U64(base),
+        self._check(getattr(self.lib, self.pre + "prefill")(P(w.ptr), P(ctx.ptr), p, U64(len(a)), U64(base),
                                                    out.ctypes.data_as(F32P) if logits else None))
         return out
 
     def row_logits_from_layer(self, w, hidden_row, first_layer, ctx, position):
         h = np.ascontiguousarray(hidden_row, np.float32)
         out = np.empty(w.spec.vocab_size, np.float32)
-        self._check(self.lib[self.pre + "row_logits_from_layer"](
+        self._check(getattr(self.lib, self.pre + "row_logits_from_layer")(
             P(w.ptr), h.ctypes.data_as(F32P), U64(first_layer), P(ctx.ptr), U64(position),
             out.ctypes.data_as(F32P)))
         return out
@@ -187,7 +187,7 @@ class Oracle:
         # ask for the layer count via a first view call with generous pointer arrays
         kp = (F32P * 4096)()
         vp = (F32P * 4096)()
-        self._check(self.lib[self.pre + "cache_view"](P(cptr), C.byref(view), kp, vp))
+        self._check(getattr(self.lib, self.pre + "cache_view")(P(cptr), C.byref(view), kp, vp))
         return HostRelayCache.from_view(view)
 
     def scenario(self, w, old_prefix, segment_len, snapshot_layer, include_self=False,
@@ -217,15 +217,15 @@ class Oracle:
 
     def upload_cache(self, host):
         out = P()
-        self._check(self.lib[self.pre + "cache_from_view"](C.byref(host.view()), C.byref(out)))
-        return _Handle(self.lib, out.value, self.lib[self.pre + "cache_destroy"])
+        self._check(getattr(self.lib, self.pre + "cache_from_view")(C.byref(host.view()), C.byref(out)))
+        return _Handle(self.lib, out.value, getattr(self.lib, self.pre + "cache_destroy"))
 
     def realign(self, host, base):
         c = self.upload_cache(host)
         L, n, kv = host.k_pre.shape
         out = np.empty((L, n, kv), np.float32)
         ptrs = (F32P * L)(*[out[l].ctypes.data_as(F32P) for l in range(L)])
-        self._check(self.lib[self.pre + "realign"](P(c.ptr), U64(base), ptrs))
+        self._check(getattr(self.lib, self.pre + "realign")(P(c.ptr), U64(base), ptrs))
         return out
 
     # ---- hot path ---------------------------------------------------------------
@@ -262,7 +262,7 @@ class Oracle:
     def relay_extend(self, w, ctx, host_cache, profile, opts):
         c = self.upload_cache(host_cache)
         o, bufs = self._out_struct(w.spec, host_cache.segment_len)
-        self._check(self.lib[self.pre + "relay_extend"](P(w.ptr), P(ctx.ptr), P(c.ptr), C.byref(profile),
+        self._check(getattr(self.lib, self.pre + "relay_extend")(P(w.ptr), P(ctx.ptr), P(c.ptr), C.byref(profile),
                                                         C.byref(opts), C.byref(o)))
         return self._out_dict(o, bufs)
 
@@ -297,7 +297,7 @@ class Oracle:
         ctx = ctx or self.new_ctx(w)
         logits = np.empty(w.spec.vocab_size, np.float32)
         tok = C.c_int32()
-        self._check(self.lib[self.pre + "agent_prefill"](P(w.ptr), P(ctx.ptr), p, U64(len(a)), arr,
+        self._check(getattr(self.lib, self.pre + "agent_prefill")(P(w.ptr), P(ctx.ptr), p, U64(len(a)), arr,
                                                          U64(len(cs)), sp, U64(len(s)), C.byref(profile),
                                                          C.byref(opts), logits.ctypes.data_as(F32P),
                                                          C.byref(tok)))
@@ -320,10 +320,10 @@ class Oracle:
 
     # ---- misc ---------------------------------------------------------------------
     def flops_span_full(self, spec, base, n):
-        return self.lib[self.pre + "flops_span_full"](C.byref(spec), U64(base), U64(n))
+        return getattr(self.lib, self.pre + "flops_span_full")(C.byref(spec), U64(base), U64(n))
 
     def flops_segment_schedule(self, spec, base, n, lo, hi, sparse_hi, sel):
-        return self.lib[self.pre + "flops_segment_schedule"](C.byref(spec), U64(base), U64(n), U64(lo),
+        return getattr(self.lib, self.pre + "flops_segment_schedule")(C.byref(spec), U64(base), U64(n), U64(lo),
                                                              U64(hi), U64(sparse_hi), U64(sel))
 
     def host_expf(self, x):

@@ -1,0 +1,731 @@
+// engine.cpp -- C ABI implementation and the relay-prefill orchestration.
+//
+// Host-side control flow mirrors the reference function by function
+// (relay_engine.cpp:183-395, model.cpp:305-362, workflow.cpp:316-369); the
+// arithmetic runs in the CUDA kernels of kernels_*.cu / gemm_sm100.cu /
+// attn_sm100.cu. Compiled with -ffp-contract=off: the few float expressions
+// evaluated here (init scales, thresholds) must round as the reference's.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "internal.h"
+#include "layer.h"
+
+using namespace rk;
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return RK_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "out of host memory";
+    return RK_ERR_RUNTIME;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return RK_ERR_RUNTIME;
+  }
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) RK_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    int cur;
+    if (cudaGetDevice(&cur) == cudaSuccess && prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+void require(bool ok, int code, const std::string& msg) {
+  if (!ok) raise(code, msg);
+}
+
+size_t num_tensors(const rk_model_spec& s) { return 1 + 9 * s.num_layers + 2; }
+
+}  // namespace
+
+namespace rk {
+
+void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e != cudaSuccess) {
+    char buf[512];
+    snprintf(buf, sizeof buf, "CUDA error %s (%s) at %s:%d: %s", cudaGetErrorName(e),
+             cudaGetErrorString(e), file, line, what);
+    throw Error(RK_ERR_RUNTIME, buf);
+  }
+}
+
+void DevBuf::alloc(size_t n) {
+  bytes = n;
+  p = nullptr;
+  if (n == 0) return;
+  cudaError_t e = cudaMalloc(&p, n);
+  if (e != cudaSuccess) {
+    p = nullptr;
+    bytes = 0;
+    cudaGetLastError();
+    throw Error(RK_ERR_RUNTIME, "device allocation of " + std::to_string(n) + " bytes failed: " +
+                                    cudaGetErrorString(e));
+  }
+}
+void DevBuf::release() {
+  if (p) cudaFree(p);
+  p = nullptr;
+  bytes = 0;
+}
+
+RopeTable* rope_table(rk_engine* e, float theta, uint64_t d_head, uint64_t positions) {
+  for (auto& t : e->rope)
+    if (t->theta == theta && t->d_head == d_head && t->positions >= positions) return t.get();
+  auto t = std::make_unique<RopeTable>();
+  t->theta = theta;
+  t->d_head = d_head;
+  t->positions = positions;
+  const uint64_t half = d_head / 2;
+  std::vector<double2> h(positions * half);
+  const double d = static_cast<double>(d_head);
+  for (uint64_t i = 0; i < half; ++i) {
+    // exactly rope_rotate's expressions (tensor.cpp:135-137), glibc pow/cos/sin
+    const double freq = std::pow(static_cast<double>(theta), -2.0 * static_cast<double>(i) / d);
+    for (uint64_t p = 0; p < positions; ++p) {
+      const double angle = static_cast<double>(static_cast<int64_t>(p)) * freq;
+      h[p * half + i] = make_double2(std::cos(angle), std::sin(angle));
+    }
+  }
+  t->cs.alloc(h.size() * sizeof(double2));
+  RK_CUDA(cudaMemcpy(t->cs.p, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  e->rope.push_back(std::move(t));
+  return e->rope.back().get();
+}
+
+}  // namespace rk
+
+rk_engine::rk_engine() : scratch(new Scratch()) {}
+rk_engine::~rk_engine() {
+  scratch.reset();
+  rope.clear();
+  if (pinned) cudaFreeHost(pinned);
+  if (stream) cudaStreamDestroy(stream);
+}
+
+void rk_context::reserve(uint64_t positions) {
+  if (positions <= cap) return;
+  uint64_t ncap = cap ? cap : 256;
+  while (ncap < positions) ncap *= 2;
+  if (ncap > w->s.max_positions) ncap = std::max<uint64_t>(w->s.max_positions, positions);
+  const size_t L = w->s.num_layers, row = w->kv() * elem;
+  DevBuf nk(L * ncap * row), nv(L * ncap * row);
+  if (size > 0) {
+    RK_CUDA(cudaMemcpy2DAsync(nk.p, ncap * row, k.p, cap * row, size * row, L, cudaMemcpyDeviceToDevice, e->stream));
+    RK_CUDA(cudaMemcpy2DAsync(nv.p, ncap * row, v.p, cap * row, size * row, L, cudaMemcpyDeviceToDevice, e->stream));
+    RK_CUDA(cudaStreamSynchronize(e->stream));
+  }
+  k = std::move(nk);
+  v = std::move(nv);
+  cap = ncap;
+}
+
+void rk_context::resize(uint64_t positions) {  // KVContext::resize (model.cpp:124-131)
+  if (positions < size) raise(RK_ERR_INVALID_ARGUMENT, "KVContext::resize: cannot shrink");
+  if (positions == size) return;
+  reserve(positions);
+  const size_t L = w->s.num_layers, row = w->kv() * elem;
+  RK_CUDA(cudaMemset2DAsync(static_cast<char*>(k.p) + size * row, cap * row, 0, (positions - size) * row, L, e->stream));
+  RK_CUDA(cudaMemset2DAsync(static_cast<char*>(v.p) + size * row, cap * row, 0, (positions - size) * row, L, e->stream));
+  size = positions;
+}
+
+// ============================================================================
+// weights
+// ============================================================================
+namespace {
+
+struct TensorDesc {
+  size_t rows, cols;  // reference shape [rows x cols]
+};
+
+// Allocate the device layout for a spec/precision; returns total bytes.
+void layout_weights(rk_weights* w) {
+  const rk_model_spec& s = w->s;
+  const size_t d = s.d_model, q = w->q(), kv = w->kv(), ff = s.d_ff, V = s.vocab_size, L = s.num_layers;
+  const size_t el = w->elem;
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  size_t total = al(V * d * el) + al(d * 4) + al(d * V * el);
+  const size_t per_layer = al(d * 4) * 2 + al(d * (q + 2 * kv) * el) + al(q * d * el) + al(d * 2 * ff * el) + al(ff * d * el);
+  total += L * per_layer;
+  w->blob.alloc(total);
+  char* p = static_cast<char*>(w->blob.p);
+  auto take = [&](size_t b) { void* r = p; p += al(b); return r; };
+  w->emb = take(V * d * el);
+  w->final_norm = static_cast<float*>(take(d * 4));
+  w->head = take(d * V * el);
+  w->layers.resize(L);
+  for (auto& ly : w->layers) {
+    ly.attn_norm = static_cast<float*>(take(d * 4));
+    ly.mlp_norm = static_cast<float*>(take(d * 4));
+    ly.w_qkv = take(d * (q + 2 * kv) * el);
+    ly.w_o = take(q * d * el);
+    ly.w_gu = take(d * 2 * ff * el);
+    ly.w_down = take(ff * d * el);
+  }
+}
+
+// Reference shape of tensor_table entry idx (weights_io.cpp:21-38).
+TensorDesc tensor_desc(const rk_model_spec& s, size_t idx) {
+  const size_t d = s.d_model, q = s.num_heads * s.d_head, kv = s.num_kv_heads * s.d_head;
+  if (idx == 0) return {s.vocab_size, d};
+  idx -= 1;
+  if (idx < 9 * s.num_layers) {
+    switch (idx % 9) {
+      case 0: case 5: return {1, d};
+      case 1: return {d, q};
+      case 2: case 3: return {d, kv};
+      case 4: return {q, d};
+      case 6: case 7: return {d, s.d_ff};
+      default: return {s.d_ff, d};
+    }
+  }
+  idx -= 9 * s.num_layers;
+  if (idx == 0) return {1, d};
+  return {d, s.vocab_size};
+}
+
+// Place one reference-layout fp32 tensor (device, [rows x cols]) into the
+// engine layout.
+void pack_tensor(rk_weights* w, size_t idx, const float* src) {
+  const rk_model_spec& s = w->s;
+  cudaStream_t st = w->e->stream;
+  const size_t d = s.d_model, q = w->q(), kv = w->kv(), ff = s.d_ff, V = s.vocab_size;
+  const bool bf = w->precision == RK_BF16;
+  const TensorDesc td = tensor_desc(s, idx);
+  auto copy_plain = [&](void* dst, size_t n) {
+    if (bf) k::f32_to_bf16(st, static_cast<__nv_bfloat16*>(dst), src, n);
+    else RK_CUDA(cudaMemcpyAsync(dst, src, n * 4, cudaMemcpyDeviceToDevice, st));
+  };
+  // exact: dst[r][c0 + c*cs] (row length ldd); bf16: transposed dst[c0 + c*cs][r] (row length ld_t)
+  auto place = [&](void* dst, size_t ldd, size_t c0, size_t cs, size_t ld_t) {
+    if (bf) k::transpose_to_bf16(st, static_cast<__nv_bfloat16*>(dst), ld_t, c0, cs, src, td.rows, td.cols);
+    else k::copy_cols_f32(st, static_cast<float*>(dst), ldd, c0, src, td.cols, td.rows, td.cols, cs);
+  };
+  if (idx == 0) { copy_plain(w->emb, V * d); return; }
+  size_t i = idx - 1;
+  if (i < 9 * s.num_layers) {
+    rk_layer_dev& ly = w->layers[i / 9];
+    switch (i % 9) {
+      case 0: RK_CUDA(cudaMemcpyAsync(ly.attn_norm, src, d * 4, cudaMemcpyDeviceToDevice, st)); break;
+      case 1: place(ly.w_qkv, q + 2 * kv, 0, 1, d); break;
+      case 2: place(ly.w_qkv, q + 2 * kv, q, 1, d); break;
+      case 3: place(ly.w_qkv, q + 2 * kv, q + kv, 1, d); break;
+      case 4: place(ly.w_o, d, 0, 1, q); break;
+      case 5: RK_CUDA(cudaMemcpyAsync(ly.mlp_norm, src, d * 4, cudaMemcpyDeviceToDevice, st)); break;
+      case 6: place(ly.w_gu, 2 * ff, 0, 2, d); break;
+      case 7: place(ly.w_gu, 2 * ff, 1, 2, d); break;
+      default: place(ly.w_down, d, 0, 1, ff); break;
+    }
+    return;
+  }
+  i -= 9 * s.num_layers;
+  if (i == 0) { RK_CUDA(cudaMemcpyAsync(w->final_norm, src, d * 4, cudaMemcpyDeviceToDevice, st)); return; }
+  if (bf) k::transpose_to_bf16(st, static_cast<__nv_bfloat16*>(w->head), d, 0, 1, src, d, V);
+  else RK_CUDA(cudaMemcpyAsync(w->head, src, d * V * 4, cudaMemcpyDeviceToDevice, st));
+}
+
+void check_spec(const rk_model_spec& s) {
+  require(s.num_layers >= 1 && s.d_model > 0 && s.num_heads > 0 && s.num_kv_heads > 0 &&
+              s.d_head > 0 && s.d_ff > 0 && s.vocab_size > 0 && s.max_positions > 0,
+          RK_ERR_SCHEMA, "invalid model spec: all extents must be >= 1");
+  require(s.num_heads % s.num_kv_heads == 0, RK_ERR_SCHEMA,
+          "invalid model spec: num_heads must be divisible by num_kv_heads");
+  require(s.d_head % 2 == 0, RK_ERR_SCHEMA, "invalid model spec: d_head must be even for rotary embedding");
+  require((s.num_kv_heads * s.d_head) % 8 == 0, RK_ERR_INVALID_ARGUMENT,
+          "engine requires kv_dim to be a multiple of 8 (16-byte rows)");
+}
+
+rk_weights* new_weights(rk_engine* e, const rk_model_spec* spec, int precision) {
+  require(spec != nullptr, RK_ERR_INVALID_ARGUMENT, "null spec");
+  check_spec(*spec);
+  require(precision == RK_FP32_EXACT || precision == RK_BF16, RK_ERR_INVALID_ARGUMENT, "bad precision");
+  auto w = std::make_unique<rk_weights>();
+  w->e = e;
+  w->s = *spec;
+  w->precision = precision;
+  w->elem = precision == RK_BF16 ? 2 : 4;
+  if (precision == RK_BF16) {
+    require(spec->d_model % 64 == 0 && (spec->num_heads * spec->d_head) % 64 == 0 && spec->d_ff % 64 == 0,
+            RK_ERR_INVALID_ARGUMENT, "bf16 mode requires d_model, q_dim and d_ff to be multiples of 64");
+    require(spec->d_head == 64 || spec->d_head == 128, RK_ERR_INVALID_ARGUMENT,
+            "bf16 mode supports d_head 64 or 128");
+  }
+  layout_weights(w.get());
+  w->rope = rope_table(e, spec->theta_base, spec->d_head, spec->max_positions);
+  return w.release();
+}
+
+}  // namespace
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+int rk_abi_version(void) { return RK_ABI_VERSION; }
+const char* rk_last_error(void) { return g_err.c_str(); }
+
+int rk_engine_create(int device, rk_engine** out) {
+  return guard([&] {
+    require(out != nullptr, RK_ERR_INVALID_ARGUMENT, "null out");
+    int n = 0;
+    RK_CUDA(cudaGetDeviceCount(&n));
+    require(device >= 0 && device < n, RK_ERR_INVALID_ARGUMENT, "no such CUDA device");
+    DeviceGuard g(device);
+    auto e = std::make_unique<rk_engine>();
+    e->device = device;
+    RK_CUDA(cudaDeviceGetAttribute(&e->sm_count, cudaDevAttrMultiProcessorCount, device));
+    int major = 0;
+    RK_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+    require(major == 10, RK_ERR_RUNTIME, "relaykv-b200 kernels are built for sm_100a (B200)");
+    RK_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+    e->status.alloc(64);
+    RK_CUDA(cudaMemset(e->status.p, 0, 64));
+    e->pinned_bytes = 1 << 20;
+    RK_CUDA(cudaMallocHost(&e->pinned, e->pinned_bytes));
+    *out = e.release();
+  });
+}
+
+void rk_engine_destroy(rk_engine* e) {
+  if (!e) return;
+  DeviceGuard g(e->device);
+  cudaStreamSynchronize(e->stream);
+  delete e;
+}
+
+int rk_engine_synchronize(rk_engine* e) {
+  return guard([&] {
+    DeviceGuard g(e->device);
+    RK_CUDA(cudaStreamSynchronize(e->stream));
+  });
+}
+void* rk_engine_stream(rk_engine* e) { return e ? (void*)e->stream : nullptr; }
+uint64_t rk_engine_launch_count(rk_engine* e) { return e ? e->launches : 0; }
+int rk_engine_set_graphs(rk_engine* e, int enable) {
+  return guard([&] { e->use_graphs = enable; });
+}
+
+uint64_t rk_weights_num_tensors(const rk_model_spec* s) { return s ? num_tensors(*s) : 0; }
+
+int rk_weights_init(rk_engine* e, const rk_model_spec* spec, uint64_t seed, int precision,
+                    rk_weights** out) {
+  return guard([&] {
+    DeviceGuard g(e->device);
+    std::unique_ptr<rk_weights> w(new_weights(e, spec, precision));
+    const rk_model_spec& s = *spec;
+    // init_weights (model.cpp:81-114): one SplitMix64 stream, draw order
+    // embedding, per layer (w_q, w_k, w_v, w_o, w_gate, w_up, w_down), head;
+    // gains are ones and draw nothing.
+    uint64_t state = seed ^ 0x72656c6179ull;
+    const float kSqrt3 = 1.7320508f;
+    const float d_in = 1.0f / std::sqrt(static_cast<float>(s.d_model));
+    const float ff_in = 1.0f / std::sqrt(static_cast<float>(s.d_ff));
+    const float q_in = 1.0f / std::sqrt(static_cast<float>(s.num_heads * s.d_head)) /
+                       (2.0f * static_cast<float>(s.num_layers));
+    size_t maxn = 0;
+    for (size_t i = 0; i < num_tensors(s); ++i) {
+      const TensorDesc td = tensor_desc(s, i);
+      maxn = std::max(maxn, td.rows * td.cols);
+    }
+    DevBuf tmp(maxn * 4);
+    float* t = tmp.as<float>();
+    cudaStream_t st = e->stream;
+    auto gen = [&](size_t idx, float sd) {
+      const TensorDesc td = tensor_desc(s, idx);
+      const size_t n = td.rows * td.cols;
+      k::init_uniform(st, t, n, state, sd * kSqrt3);
+      state += static_cast<uint64_t>(n) * 0x9e3779b97f4a7c15ull;
+      pack_tensor(w.get(), idx, t);
+    };
+    auto ones = [&](size_t idx) {
+      const TensorDesc td = tensor_desc(s, idx);
+      k::fill(st, t, td.rows * td.cols, 1.0f);
+      pack_tensor(w.get(), idx, t);
+    };
+    gen(0, 0.02f);
+    for (size_t l = 0; l < s.num_layers; ++l) {
+      const size_t b = 1 + 9 * l;
+      ones(b + 0);
+      gen(b + 1, d_in);
+      gen(b + 2, d_in);
+      gen(b + 3, d_in);
+      gen(b + 4, q_in);
+      ones(b + 5);
+      gen(b + 6, d_in);
+      gen(b + 7, d_in);
+      gen(b + 8, ff_in);
+    }
+    ones(1 + 9 * s.num_layers);
+    gen(2 + 9 * s.num_layers, d_in);
+    RK_CUDA(cudaStreamSynchronize(st));
+    *out = w.release();
+  });
+}
+
+int rk_weights_upload(rk_engine* e, const rk_model_spec* spec, const float* const* tensors,
+                      uint64_t n_tensors, int precision, rk_weights** out) {
+  return guard([&] {
+    DeviceGuard g(e->device);
+    require(tensors != nullptr && n_tensors == num_tensors(*spec), RK_ERR_INVALID_ARGUMENT,
+            "weights upload: expected tensor_table order with " + std::to_string(num_tensors(*spec)) + " tensors");
+    std::unique_ptr<rk_weights> w(new_weights(e, spec, precision));
+    size_t maxn = 0;
+    for (size_t i = 0; i < n_tensors; ++i) {
+      const TensorDesc td = tensor_desc(*spec, i);
+      maxn = std::max(maxn, td.rows * td.cols);
+    }
+    DevBuf tmp(maxn * 4);
+    for (size_t i = 0; i < n_tensors; ++i) {
+      const TensorDesc td = tensor_desc(*spec, i);
+      require(tensors[i] != nullptr, RK_ERR_INVALID_ARGUMENT, "null tensor");
+      RK_CUDA(cudaMemcpyAsync(tmp.p, tensors[i], td.rows * td.cols * 4, cudaMemcpyHostToDevice, e->stream));
+      pack_tensor(w.get(), i, tmp.as<float>());
+    }
+    RK_CUDA(cudaStreamSynchronize(e->stream));
+    *out = w.release();
+  });
+}
+
+int rk_weights_export(rk_weights* w, uint64_t idx, float* out, uint64_t count) {
+  return guard([&] {
+    DeviceGuard g(w->e->device);
+    const rk_model_spec& s = w->s;
+    require(idx < num_tensors(s), RK_ERR_INVALID_ARGUMENT, "tensor index out of range");
+    const TensorDesc td = tensor_desc(s, idx);
+    require(count >= td.rows * td.cols, RK_ERR_INVALID_ARGUMENT, "output buffer too small");
+    DevBuf tmp(td.rows * td.cols * 4);
+    layer_unpack_tensor(w, idx, tmp.as<float>(), td.rows, td.cols);
+    RK_CUDA(cudaMemcpyAsync(out, tmp.p, td.rows * td.cols * 4, cudaMemcpyDeviceToHost, w->e->stream));
+    RK_CUDA(cudaStreamSynchronize(w->e->stream));
+  });
+}
+
+void rk_weights_destroy(rk_weights* w) {
+  if (!w) return;
+  DeviceGuard g(w->e->device);
+  cudaStreamSynchronize(w->e->stream);
+  delete w;
+}
+
+// ---- relay caches ---------------------------------------------------------
+int rk_cache_upload(rk_engine* e, rk_weights* w, const rk_relay_cache_view* v, rk_cache** out) {
+  return guard([&] {
+    DeviceGuard g(e->device);
+    require(v != nullptr && w != nullptr, RK_ERR_INVALID_ARGUMENT, "null cache view / weights");
+    // RelayCache::validate (relay_cache.cpp:18-41)
+    const uint64_t n = v->segment_len;
+    require(n > 0, RK_ERR_INVALID_ARGUMENT, "relay cache: empty segment");
+    require(v->num_layers > 0 && v->k_pre && v->v, RK_ERR_INVALID_ARGUMENT,
+            "relay cache: per-layer K/V tables disagree");
+    require(v->snapshot_layer < v->num_layers, RK_ERR_INVALID_ARGUMENT,
+            "relay cache: snapshot layer out of range");
+    for (uint64_t j = 0; j < n; ++j)
+      require(v->influence[j] >= 0.0f, RK_ERR_INVALID_ARGUMENT, "relay cache: negative influence score");
+    auto c = std::make_unique<rk_cache>();
+    c->e = e;
+    c->precision = w->precision;
+    c->elem = w->elem;
+    c->L = v->num_layers;
+    c->Hkv = v->num_kv_heads;
+    c->dh = v->d_head;
+    c->d = v->d_model;
+    c->n = n;
+    c->maxpos = v->max_positions;
+    c->theta = v->theta_base;
+    c->src_base = v->source_base_position;
+    c->snapshot = v->snapshot_layer;
+    c->steps = v->decode_steps_observed;
+    const size_t kv = c->kv();
+    c->tokens.alloc(n * 4);
+    c->host_tokens.assign(v->segment_tokens, v->segment_tokens + n);
+    c->k_pre.alloc(c->L * n * kv * c->elem);
+    c->v.alloc(c->L * n * kv * c->elem);
+    c->hidden.alloc(n * c->d * 4);
+    c->influence.alloc(n * 4);
+    c->infl_mean.alloc(8);
+    cudaStream_t st = e->stream;
+    RK_CUDA(cudaMemcpyAsync(c->tokens.p, v->segment_tokens, n * 4, cudaMemcpyHostToDevice, st));
+    RK_CUDA(cudaMemcpyAsync(c->hidden.p, v->hidden_snapshot, n * c->d * 4, cudaMemcpyHostToDevice, st));
+    RK_CUDA(cudaMemcpyAsync(c->influence.p, v->influence, n * 4, cudaMemcpyHostToDevice, st));
+    DevBuf tmp;
+    if (c->elem == 2) tmp.alloc(n * kv * 4);
+    for (uint64_t l = 0; l < c->L; ++l) {
+      for (int which = 0; which < 2; ++which) {
+        const float* src = which == 0 ? v->k_pre[l] : v->v[l];
+        char* dst = static_cast<char*>(which == 0 ? c->k_pre.p : c->v.p) + l * n * kv * c->elem;
+        if (c->elem == 4) {
+          RK_CUDA(cudaMemcpyAsync(dst, src, n * kv * 4, cudaMemcpyHostToDevice, st));
+        } else {
+          RK_CUDA(cudaMemcpyAsync(tmp.p, src, n * kv * 4, cudaMemcpyHostToDevice, st));
+          k::f32_to_bf16(st, reinterpret_cast<__nv_bfloat16*>(dst), tmp.as<float>(), n * kv);
+        }
+      }
+      if (c->elem == 2) RK_CUDA(cudaStreamSynchronize(st));  // tmp reuse
+    }
+    // influence mean, sequential in double (selector.cpp:37-39) -- cache-static
+    double mean = 0.0;
+    for (uint64_t j = 0; j < n; ++j) mean += static_cast<double>(v->influence[j]);
+    mean /= static_cast<double>(n);
+    RK_CUDA(cudaMemcpyAsync(c->infl_mean.p, &mean, 8, cudaMemcpyHostToDevice, st));
+    RK_CUDA(cudaStreamSynchronize(st));
+    *out = c.release();
+  });
+}
+
+uint64_t rk_cache_segment_len(const rk_cache* c) { return c ? c->n : 0; }
+
+int rk_cache_export(rk_cache* c, int32_t* tokens, float* const* k_pre, float* const* v,
+                    float* hidden, float* influence, uint64_t* src_base, uint64_t* snapshot) {
+  return guard([&] {
+    DeviceGuard g(c->e->device);
+    cudaStream_t st = c->e->stream;
+    const size_t kv = c->kv(), n = c->n;
+    if (tokens) RK_CUDA(cudaMemcpyAsync(tokens, c->tokens.p, n * 4, cudaMemcpyDeviceToHost, st));
+    if (hidden) RK_CUDA(cudaMemcpyAsync(hidden, c->hidden.p, n * c->d * 4, cudaMemcpyDeviceToHost, st));
+    if (influence) RK_CUDA(cudaMemcpyAsync(influence, c->influence.p, n * 4, cudaMemcpyDeviceToHost, st));
+    DevBuf tmp;
+    if (c->elem == 2) tmp.alloc(n * kv * 4);
+    for (uint64_t l = 0; l < c->L; ++l)
+      for (int which = 0; which < 2; ++which) {
+        float* dst = which == 0 ? (k_pre ? k_pre[l] : nullptr) : (v ? v[l] : nullptr);
+        if (!dst) continue;
+        const char* src = static_cast<const char*>(which == 0 ? c->k_pre.p : c->v.p) + l * n * kv * c->elem;
+        if (c->elem == 4) {
+          RK_CUDA(cudaMemcpyAsync(dst, src, n * kv * 4, cudaMemcpyDeviceToHost, st));
+        } else {
+          k::bf16_to_f32(st, tmp.as<float>(), reinterpret_cast<const __nv_bfloat16*>(src), n * kv);
+          RK_CUDA(cudaMemcpyAsync(dst, tmp.p, n * kv * 4, cudaMemcpyDeviceToHost, st));
+          RK_CUDA(cudaStreamSynchronize(st));
+        }
+      }
+    if (src_base) *src_base = c->src_base;
+    if (snapshot) *snapshot = c->snapshot;
+    RK_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+void rk_cache_destroy(rk_cache* c) {
+  if (!c) return;
+  DeviceGuard g(c->e->device);
+  cudaStreamSynchronize(c->e->stream);
+  delete c;
+}
+
+// ---- contexts -------------------------------------------------------------
+int rk_context_create(rk_engine* e, rk_weights* w, rk_context** out) {
+  return guard([&] {
+    DeviceGuard g(e->device);
+    auto c = std::make_unique<rk_context>();
+    c->e = e;
+    c->w = w;
+    c->elem = w->elem;
+    *out = c.release();
+  });
+}
+
+int rk_context_clone(rk_context* src, rk_context** out) {
+  return guard([&] {
+    DeviceGuard g(src->e->device);
+    auto c = std::make_unique<rk_context>();
+    c->e = src->e;
+    c->w = src->w;
+    c->elem = src->elem;
+    c->reserve(src->cap);
+    c->size = src->size;
+    if (src->cap) {
+      RK_CUDA(cudaMemcpyAsync(c->k.p, src->k.p, src->k.bytes, cudaMemcpyDeviceToDevice, src->e->stream));
+      RK_CUDA(cudaMemcpyAsync(c->v.p, src->v.p, src->v.bytes, cudaMemcpyDeviceToDevice, src->e->stream));
+    }
+    for (const auto& m : src->segs) {
+      rk_segment_marks nm;
+      nm.base = m.base;
+      nm.len = m.len;
+      nm.origin.alloc(m.origin.bytes);
+      RK_CUDA(cudaMemcpyAsync(nm.origin.p, m.origin.p, m.origin.bytes, cudaMemcpyDeviceToDevice, src->e->stream));
+      c->segs.push_back(std::move(nm));
+    }
+    RK_CUDA(cudaStreamSynchronize(src->e->stream));
+    *out = c.release();
+  });
+}
+
+uint64_t rk_context_size(const rk_context* c) { return c ? c->size : 0; }
+uint64_t rk_context_num_segments(const rk_context* c) { return c ? c->segs.size() : 0; }
+
+int rk_context_segment(rk_context* c, uint64_t index, uint64_t* base, uint64_t* len, uint8_t* origin) {
+  return guard([&] {
+    require(index < c->segs.size(), RK_ERR_INVALID_ARGUMENT, "segment index out of range");
+    const rk_segment_marks& m = c->segs[index];
+    if (base) *base = m.base;
+    if (len) *len = m.len;
+    if (origin && m.origin.bytes) {
+      DeviceGuard g(c->e->device);
+      RK_CUDA(cudaMemcpyAsync(origin, m.origin.p, c->w->s.num_layers * m.len, cudaMemcpyDeviceToHost, c->e->stream));
+      RK_CUDA(cudaStreamSynchronize(c->e->stream));
+    }
+  });
+}
+
+int rk_context_export(rk_context* c, uint64_t layer, uint64_t pos, uint64_t count, float* k, float* v) {
+  return guard([&] {
+    DeviceGuard g(c->e->device);
+    require(layer < c->w->s.num_layers && pos + count <= c->size, RK_ERR_INVALID_ARGUMENT,
+            "context export out of range");
+    const size_t kv = c->w->kv();
+    cudaStream_t st = c->e->stream;
+    DevBuf tmp;
+    if (c->elem == 2) tmp.alloc(count * kv * 4);
+    for (int which = 0; which < 2; ++which) {
+      float* dst = which == 0 ? k : v;
+      if (!dst || count == 0) continue;
+      const char* src = static_cast<const char*>(which == 0 ? c->k_layer(layer) : c->v_layer(layer)) + pos * kv * c->elem;
+      if (c->elem == 4) {
+        RK_CUDA(cudaMemcpyAsync(dst, src, count * kv * 4, cudaMemcpyDeviceToHost, st));
+      } else {
+        k::bf16_to_f32(st, tmp.as<float>(), reinterpret_cast<const __nv_bfloat16*>(src), count * kv);
+        RK_CUDA(cudaMemcpyAsync(dst, tmp.p, count * kv * 4, cudaMemcpyDeviceToHost, st));
+        RK_CUDA(cudaStreamSynchronize(st));
+      }
+    }
+    RK_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+void rk_context_destroy(rk_context* c) {
+  if (!c) return;
+  DeviceGuard g(c->e->device);
+  cudaStreamSynchronize(c->e->stream);
+  delete c;
+}
+
+// ---- hot path --------------------------------------------------------------
+int rk_prefill(rk_engine* e, rk_weights* w, rk_context* ctx, const int32_t* tokens, uint64_t n,
+               uint64_t base, float* last_logits) {
+  return guard([&] {
+    DeviceGuard g(e->device);
+    Runner r(e, w);
+    r.prefill(ctx, tokens, n, base, last_logits != nullptr);
+    r.finish();
+    if (last_logits) r.download_logits(last_logits);
+  });
+}
+
+int rk_relay_extend(rk_engine* e, rk_weights* w, rk_context* ctx, rk_cache* cache,
+                    const rk_layer_profile* profile, const rk_relay_options* opts, rk_relay_output* out) {
+  return guard([&] {
+    DeviceGuard g(e->device);
+    require(opts != nullptr, RK_ERR_INVALID_ARGUMENT, "null options");
+    Runner r(e, w);
+    ExtendResult res = r.relay_extend(ctx, cache, profile, *opts);
+    r.finish();
+    r.resolve(res);
+    r.fill_output(res, ctx, out);
+  });
+}
+
+int rk_relay_prefill(rk_engine* e, rk_weights* w, rk_context* ctx, const int32_t* prefix,
+                     uint64_t n_prefix, rk_cache* cache, const rk_layer_profile* profile,
+                     const rk_relay_options* opts, rk_relay_output* out, float* end_logits) {
+  return guard([&] {
+    DeviceGuard g(e->device);
+    require(opts != nullptr && ctx != nullptr && cache != nullptr, RK_ERR_INVALID_ARGUMENT, "null argument");
+    require(ctx->size == 0, RK_ERR_INVALID_ARGUMENT, "relay_prefill: context must be empty");
+    Runner r(e, w);
+    r.begin_timer();
+    if (n_prefix > 0) r.prefill(ctx, prefix, n_prefix, 0, false);
+    const float prefix_ms = r.lap_ms();
+    ExtendResult res = r.relay_extend(ctx, cache, profile, *opts);
+    r.segment_end_logits(ctx, res);
+    r.finish();
+    r.resolve(res);
+    res.stats.wall.fresh_ms = prefix_ms;
+    res.stats.wall.total_ms += prefix_ms;
+    res.stats.flops_cost += rk_flops_span_full(&w->s, 0, n_prefix);
+    res.stats.flops_full_equiv += rk_flops_span_full(&w->s, 0, n_prefix);
+    r.fill_output(res, ctx, out);
+    if (end_logits) r.download_logits(end_logits);
+  });
+}
+
+int rk_agent_prefill(rk_engine* e, rk_weights* w, rk_context* ctx, const int32_t* prefix,
+                     uint64_t n_prefix, rk_cache* const* ups, uint64_t n_up, const int32_t* suffix,
+                     uint64_t n_suffix, const rk_layer_profile* profile, const rk_relay_options* opts,
+                     rk_relay_output* outs, float* end_logits, int32_t* first_token) {
+  return guard([&] {
+    DeviceGuard g(e->device);
+    require(opts != nullptr && ctx != nullptr, RK_ERR_INVALID_ARGUMENT, "null argument");
+    require(ctx->size == 0, RK_ERR_INVALID_ARGUMENT, "agent prefill: context must be empty");
+    Runner r(e, w);
+    std::vector<ExtendResult> results;
+    r.agent_prefill(ctx, prefix, n_prefix, ups, n_up, suffix, n_suffix, profile, *opts, results);
+    r.finish();
+    for (auto& res : results) r.resolve(res);
+    if (outs)
+      for (size_t u = 0; u < results.size(); ++u) r.fill_output(results[u], ctx, &outs[u]);
+    if (end_logits) r.download_logits(end_logits);
+    if (first_token) *first_token = r.first_token();
+  });
+}
+
+int rk_cache_capture_prefill(rk_engine* e, rk_weights* w, rk_context* ctx, const int32_t* tokens,
+                             uint64_t n, uint64_t snapshot, int include_self, rk_cache** out) {
+  return guard([&] {
+    DeviceGuard g(e->device);
+    Runner r(e, w);
+    *out = r.capture_prefill(ctx, tokens, n, snapshot, include_self != 0);
+    r.finish();
+  });
+}
+
+int rk_cache_capture_decode(rk_engine* e, rk_weights* w, rk_context* ctx, const float* first_logits,
+                            uint64_t n, uint64_t snapshot, int include_self, rk_cache** out) {
+  return guard([&] {
+    DeviceGuard g(e->device);
+    Runner r(e, w);
+    *out = r.capture_decode(ctx, first_logits, n, snapshot, include_self != 0);
+    r.finish();
+  });
+}
+
+// FLOP model (relay_engine.cpp:72-110)
+double rk_flops_span_full(const rk_model_spec* s, uint64_t base, uint64_t n) {
+  const double d = (double)s->d_model, kv = (double)(s->num_kv_heads * s->d_head), ff = (double)s->d_ff;
+  const double pm = 2.0 * d * (2.0 * d + 2.0 * kv) + 6.0 * d * ff;
+  const double b = (double)base, nn = (double)n, dhH = (double)(s->d_head * s->num_heads);
+  const double attn = 4.0 * dhH * (nn * b + nn * (nn + 1.0) / 2.0);
+  const double layers = (double)s->num_layers;
+  return layers * nn * pm + layers * attn;
+}
+double rk_flops_segment_schedule(const rk_model_spec* s, uint64_t base, uint64_t n, uint64_t lo,
+                                 uint64_t hi, uint64_t sparse_hi, uint64_t selected) {
+  const double d = (double)s->d_model, kv = (double)(s->num_kv_heads * s->d_head), ff = (double)s->d_ff;
+  const double pm = 2.0 * d * (2.0 * d + 2.0 * kv) + 6.0 * d * ff;
+  const double band_layers = (double)(hi - lo + 1), sparse_layers = (double)(sparse_hi - hi);
+  const double dhH = (double)(s->d_head * s->num_heads);
+  const double avg_ctx = (double)base + ((double)n + 1.0) / 2.0;
+  const double b = (double)base, nn = (double)n;
+  const double attn = 4.0 * dhH * (nn * b + nn * (nn + 1.0) / 2.0);
+  const double band = band_layers * (nn * pm + attn);
+  const double sparse = sparse_layers * (double)selected * (pm + 4.0 * dhH * avg_ctx);
+  return band + sparse;
+}
+
+}  // extern "C"

@@ -1,0 +1,233 @@
+// internal.h -- engine objects and kernel launchers (not part of the ABI).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "relaykv_b200.h"
+
+namespace rk {
+
+// Internal error carrying the rk_status of the reference exception type.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void raise(int code, const std::string& msg) { throw Error(code, msg); }
+
+void cuda_check(cudaError_t e, const char* what, const char* file, int line);
+#define RK_CUDA(x) ::rk::cuda_check((x), #x, __FILE__, __LINE__)
+
+// Owning device allocation.
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t n) { alloc(n); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; bytes = o.bytes; o.p = nullptr; o.bytes = 0; }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void alloc(size_t n);
+  void release();
+  // grow (contents discarded) to at least n bytes
+  void ensure(size_t n) { if (n > bytes) { release(); alloc(n); } }
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+// Double-precision RoPE table built on the host with glibc exactly as
+// rope_rotate does (tensor.cpp:134-142): cs[pos][i] = {cos, sin}(pos * pow(theta, -2i/dh)).
+struct RopeTable {
+  float theta = 0;
+  uint64_t d_head = 0, positions = 0;
+  DevBuf cs;  // double2 [positions][d_head/2]
+};
+
+struct Scratch;
+struct ExtendSlot;
+
+}  // namespace rk
+
+struct rk_engine {
+  int device = 0;
+  int sm_count = 0;
+  cudaStream_t stream = nullptr;
+  uint64_t launches = 0;
+  int use_graphs = 0;
+  std::vector<std::unique_ptr<rk::RopeTable>> rope;
+  std::unique_ptr<rk::Scratch> scratch;
+  // pinned host staging
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+  rk::DevBuf status;  // int flags: [0] non-finite
+  std::vector<cudaEvent_t> events;
+  std::vector<std::unique_ptr<rk::ExtendSlot>> slots;
+  rk_engine();
+  ~rk_engine();
+};
+
+// Per-layer weights on the device.
+//  FP32_EXACT: reference layout [K x N] row-major fp32, Q|K|V concatenated
+//    along N, gate/up interleaved along N (col 2j = gate j, 2j+1 = up j).
+//  BF16: the same logical matrices stored transposed, [N x K] K-major bf16,
+//    the tcgen05 B-operand layout.
+struct rk_layer_dev {
+  float* attn_norm = nullptr;  // [d]
+  float* mlp_norm = nullptr;   // [d]
+  void* w_qkv = nullptr;       // [d x (q+2kv)]
+  void* w_o = nullptr;         // [q x d]
+  void* w_gu = nullptr;        // [d x 2ff] interleaved
+  void* w_down = nullptr;      // [ff x d]
+};
+
+struct rk_weights {
+  rk_engine* e = nullptr;
+  rk_model_spec s{};
+  int precision = RK_FP32_EXACT;
+  size_t elem = 4;             // bytes per stored weight element
+  rk::DevBuf blob;             // all tensors
+  void* emb = nullptr;         // [V x d] (fp32 exact; bf16 in BF16)
+  float* final_norm = nullptr; // [d]
+  void* head = nullptr;        // exact: [d x V]; bf16: [V x d]
+  std::vector<rk_layer_dev> layers;
+  rk::RopeTable* rope = nullptr;
+  size_t q() const { return s.num_heads * s.d_head; }
+  size_t kv() const { return s.num_kv_heads * s.d_head; }
+};
+
+struct rk_cache {
+  rk_engine* e = nullptr;
+  int precision = RK_FP32_EXACT;
+  size_t elem = 4;
+  uint64_t L = 0, Hkv = 0, dh = 0, d = 0, n = 0, maxpos = 0;
+  float theta = 0;
+  uint64_t src_base = 0, snapshot = 0, steps = 0;
+  rk::DevBuf tokens;     // int32 [n]
+  rk::DevBuf k_pre, v;   // elem [L][n][kv]
+  rk::DevBuf hidden;     // fp32 [n x d]
+  rk::DevBuf influence;  // fp32 [n]
+  rk::DevBuf infl_mean;  // double [1], sequential mean (selector.cpp:37-39)
+  std::vector<int32_t> host_tokens;
+  size_t kv() const { return Hkv * dh; }
+};
+
+struct rk_segment_marks {
+  uint64_t base = 0, len = 0;
+  rk::DevBuf origin;  // uint8 [L x len]
+};
+
+struct rk_context {
+  rk_engine* e = nullptr;
+  rk_weights* w = nullptr;
+  uint64_t size = 0, cap = 0;
+  size_t elem = 4;
+  rk::DevBuf k, v;  // elem [L][cap][kv]
+  std::vector<rk_segment_marks> segs;
+  void* k_layer(size_t l) const { return static_cast<char*>(k.p) + l * cap * w->kv() * elem; }
+  void* v_layer(size_t l) const { return static_cast<char*>(v.p) + l * cap * w->kv() * elem; }
+  void reserve(uint64_t positions);
+  void resize(uint64_t positions);
+};
+
+namespace rk {
+
+// Grow-only scratch buffers reused across calls.
+struct Scratch {
+  DevBuf hidden, sub_hidden, normed, qkv, attn, act, logits, tokens, positions, sub_positions;
+  DevBuf s_dev, s_key, sel_idx, sel_tags, sel_info, depth, argmax, seg_hidden_out;
+  DevBuf gemm_tmp;
+};
+
+RopeTable* rope_table(rk_engine* e, float theta, uint64_t d_head, uint64_t positions);
+
+// Row set of a layer pass: rows_max bounds the launch; rows_dev (optional)
+// holds the true count on the device (sparse passes after selection).
+struct Rows {
+  int rows_max = 0;
+  const int* rows_dev = nullptr;
+  const int* pos = nullptr;  // int32 [rows_max] absolute positions
+};
+
+// ---- kernel launchers (kernels_*.cu) -------------------------------------
+namespace k {
+// weights
+void init_uniform(cudaStream_t s, float* dst, size_t n, uint64_t state0, float scale);
+void fill(cudaStream_t s, float* dst, size_t n, float v);
+// dst[r * ldd + c0 + c] = src[r * lds + c] for c < cols  (fp32)
+void copy_cols_f32(cudaStream_t s, float* dst, size_t ldd, size_t c0, const float* src, size_t lds,
+                   size_t rows, size_t cols, size_t dst_col_stride);
+// dst[(c0 + c*cstride) * ldd + r] = bf16(src[r * lds + c])  (transpose to K-major bf16)
+void transpose_to_bf16(cudaStream_t s, __nv_bfloat16* dst, size_t ldd, size_t c0, size_t cstride,
+                       const float* src, size_t rows, size_t cols);
+void f32_to_bf16(cudaStream_t s, __nv_bfloat16* dst, const float* src, size_t n);
+void bf16_to_f32(cudaStream_t s, float* dst, const __nv_bfloat16* src, size_t n);
+
+// model building blocks (elem = 4 fp32 exact, 2 bf16)
+void embed(cudaStream_t s, float* hidden, const void* emb, size_t elem, const int32_t* tokens,
+           int n, int d, int vocab, int* status);
+void gather_rows(cudaStream_t s, float* dst, const float* src, const int* idx, const int* count,
+                 int rows_max, int d);
+void scatter_rows(cudaStream_t s, float* dst, const float* src, const int* idx, const int* count,
+                  int rows_max, int d, uint64_t* depth, uint64_t depth_value);
+void positions_from_sel(cudaStream_t s, int* pos, const int* sel, const int* count, int rows_max, int base);
+void iota_positions(cudaStream_t s, int* pos, int n, int base);
+void mark_rows(cudaStream_t s, uint8_t* origin, int len, int layer_lo, int layer_hi, const int* sel,
+               const int* count, int rows_max);
+void mark_layers(cudaStream_t s, uint8_t* origin, int len, int layer_lo, int layer_hi);
+void set_depth(cudaStream_t s, uint64_t* depth, int n, uint64_t v);
+void argmax(cudaStream_t s, const float* x, int n, int* out);
+
+// relay (both precisions)
+void realign_graft(cudaStream_t s, const void* k_pre, const void* v_src, size_t elem, int L,
+                   int n, int kv, int dh, const double2* rope, int base, void* ctx_k, void* ctx_v,
+                   size_t ctx_layer_stride, int skip_lo, int skip_hi);
+void score_deviation(cudaStream_t s, const void* ctx_v, const void* cache_v, const void* ctx_k,
+                     const void* cache_kpre, size_t elem, int n, int kv, int heads, int dh,
+                     const double2* rope, int base, double* s_dev, double* s_key);
+void select_relay(cudaStream_t s, const double* s_dev, const float* influence,
+                  const double* infl_mean, int n, double tau_dev, double tau_inf, int suffix_k,
+                  int* sel_idx, uint32_t* sel_tags, int* info, double* dinfo);
+void blend_scores(cudaStream_t s, const void* ctx_v, const void* cache_v, size_t elem, int n,
+                  int kv, double* score);
+void select_topk(cudaStream_t s, const double* score, int n, int count, int* sel_idx,
+                 uint32_t* sel_tags, int* info);
+void seq_mean(cudaStream_t s, const float* x, int n, double* out);
+
+// fp32 exact path
+void rmsnorm_exact(cudaStream_t s, const float* x, const float* gain, float eps, float* out,
+                   Rows rows, int d);
+enum EpiMode { EPI_STORE = 0, EPI_ADD = 1, EPI_SILU_PAIR = 2 };
+void gemm_exact(cudaStream_t s, const float* A, const float* B, float* C, Rows rows, int N, int K,
+                int epi, int* status);
+void rope_commit_exact(cudaStream_t s, float* qkv, Rows rows, int H, int Hkv, int dh,
+                       const double2* rope, float* ctx_k, float* ctx_v, int commit);
+void attn_exact(cudaStream_t s, const float* qkv, Rows rows, int H, int Hkv, int dh,
+                const float* ctx_k, const float* ctx_v, float* out, int self_override, int max_ctx,
+                float* probs, int key_lo, int key_n);
+// influence accumulation of RelayRecorder::feed (relay_cache.cpp:108-123)
+void influence_accum(cudaStream_t s, double* acc, const float* probs, Rows rows, int H, int key_lo,
+                     int key_n, int include_self);
+void copy2d_f32(cudaStream_t s, float* dst, size_t dld, size_t dcs, const float* src, size_t sld,
+                size_t scs, size_t rows, size_t cols);
+void untranspose_bf16(cudaStream_t s, float* dst, const __nv_bfloat16* src, size_t ld, size_t c0,
+                      size_t cstride, size_t rows, size_t cols);
+void doubles_to_floats(cudaStream_t s, float* dst, const double* src, int n);
+
+// bf16 tensor-core path
+void rmsnorm_bf16(cudaStream_t s, const float* x, const float* gain, float eps,
+                  __nv_bfloat16* out, Rows rows, int d);
+}  // namespace k
+
+}  // namespace rk

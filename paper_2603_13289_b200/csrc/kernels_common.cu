@@ -1,0 +1,625 @@
+// kernels_common.cu -- kernels shared by both precisions: weight init and
+// packing, embedding, row gather/scatter, SegmentMarks, argmax, and the relay
+// kernels proper (realign+graft, deviation scoring, selection).
+//
+// Every floating-point operation that the reference performs is written with
+// explicit round-to-nearest intrinsics (__fmul_rn, __dadd_rn, ...) so nvcc
+// cannot contract it into an FMA the reference does not have
+// (-ffp-contract=off, proj/src/CMakeLists.txt:16-18).
+#include <cuda_bf16.h>
+
+#include "internal.h"
+
+namespace rk {
+namespace {
+
+constexpr int kThreads = 256;
+
+inline int blocks_for(size_t n, int threads = kThreads) {
+  size_t b = (n + threads - 1) / threads;
+  return (int)(b > 0x7fffffff ? 0x7fffffff : (b == 0 ? 1 : b));
+}
+
+__device__ __forceinline__ float load_elem(const void* p, size_t i, size_t elem) {
+  if (elem == 4) return static_cast<const float*>(p)[i];
+  return __bfloat162float(static_cast<const __nv_bfloat16*>(p)[i]);
+}
+__device__ __forceinline__ uint32_t load_bits(const void* p, size_t i, size_t elem) {
+  if (elem == 4) return __float_as_uint(static_cast<const float*>(p)[i]);
+  return static_cast<const unsigned short*>(p)[i];
+}
+
+// ---------------------------------------------------------------------------
+// weights: init_weights (model.cpp:81-114) as a counter-based stream.
+// SplitMix64 (model.cpp:49-56) advances state by a constant, so draw i of a
+// tensor whose stream starts at state0 is mix(state0 + (i+1)*gamma).
+// ---------------------------------------------------------------------------
+__global__ void init_uniform_kernel(float* dst, size_t n, uint64_t state0, float scale) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    uint64_t z = state0 + (uint64_t)(i + 1) * 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    z = z ^ (z >> 31);
+    const float u = __fmul_rn((float)(z >> 40), 0x1p-24f);          // model.cpp:58
+    const float sym = __fsub_rn(__fmul_rn(2.0f, u), 1.0f);          // model.cpp:59
+    dst[i] = __fmul_rn(sym, scale);                                 // model.cpp:69
+  }
+}
+
+__global__ void fill_kernel(float* dst, size_t n, float v) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = v;
+}
+
+__global__ void copy_cols_kernel(float* dst, size_t ldd, size_t c0, const float* src, size_t lds,
+                                 size_t rows, size_t cols, size_t cstride) {
+  const size_t total = rows * cols;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const size_t r = i / cols, c = i % cols;
+    dst[r * ldd + c0 + c * cstride] = src[r * lds + c];
+  }
+}
+
+// src [rows x cols] row-major fp32 -> dst row (c0 + c*cstride), column r, bf16.
+__global__ void transpose_bf16_kernel(__nv_bfloat16* dst, size_t ldd, size_t c0, size_t cstride,
+                                      const float* src, size_t rows, size_t cols) {
+  __shared__ float tile[32][33];
+  const size_t bc = blockIdx.x * 32, br = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const size_t r = br + i, c = bc + threadIdx.x;
+    tile[i][threadIdx.x] = (r < rows && c < cols) ? src[r * cols + c] : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const size_t c = bc + i, r = br + threadIdx.x;
+    if (r < rows && c < cols) dst[(c0 + c * cstride) * ldd + r] = __float2bfloat16_rn(tile[threadIdx.x][i]);
+  }
+}
+
+__global__ void copy2d_kernel(float* dst, size_t dld, size_t dcs, const float* src, size_t sld,
+                              size_t scs, size_t rows, size_t cols) {
+  const size_t total = rows * cols;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const size_t r = i / cols, c = i % cols;
+    dst[r * dld + c * dcs] = src[r * sld + c * scs];
+  }
+}
+// dst[r][c] = float(src[(c0 + c*cstride) * ld + r])
+__global__ void untranspose_bf16_kernel(float* dst, const __nv_bfloat16* src, size_t ld, size_t c0,
+                                        size_t cstride, size_t rows, size_t cols) {
+  const size_t total = rows * cols;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const size_t r = i / cols, c = i % cols;
+    dst[i] = __bfloat162float(src[(c0 + c * cstride) * ld + r]);
+  }
+}
+__global__ void d2f_kernel(float* dst, const double* src, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    dst[i] = (float)src[i];
+}
+
+__global__ void f32_to_bf16_kernel(__nv_bfloat16* dst, const float* src, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = __float2bfloat16_rn(src[i]);
+}
+__global__ void bf16_to_f32_kernel(float* dst, const __nv_bfloat16* src, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = __bfloat162float(src[i]);
+}
+
+// ---------------------------------------------------------------------------
+// embed_tokens (model.cpp:149-161); token range is validated on the host.
+// ---------------------------------------------------------------------------
+__global__ void embed_kernel(float* hidden, const void* emb, size_t elem, const int32_t* tokens,
+                             int n, int d) {
+  const size_t total = (size_t)n * d;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const size_t r = i / d, c = i % d;
+    hidden[i] = load_elem(emb, (size_t)tokens[r] * d + c, elem);
+  }
+}
+
+// sparse_rectify gather/scatter (relay_engine.cpp:162-178)
+__global__ void gather_rows_kernel(float* dst, const float* src, const int* idx, const int* count,
+                                   int rows_max, int d) {
+  const int rows = count ? *count : rows_max;
+  const size_t total = (size_t)rows * d;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const size_t r = i / d, c = i % d;
+    dst[i] = src[(size_t)idx[r] * d + c];
+  }
+}
+__global__ void scatter_rows_kernel(float* dst, const float* src, const int* idx, const int* count,
+                                    int rows_max, int d, uint64_t* depth, uint64_t depth_value) {
+  const int rows = count ? *count : rows_max;
+  const size_t total = (size_t)rows * d;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const size_t r = i / d, c = i % d;
+    dst[(size_t)idx[r] * d + c] = src[i];
+    if (c == 0 && depth) depth[idx[r]] = depth_value;
+  }
+}
+__global__ void positions_from_sel_kernel(int* pos, const int* sel, const int* count, int rows_max,
+                                          int base) {
+  const int rows = count ? *count : rows_max;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x)
+    pos[r] = base + sel[r];
+}
+__global__ void iota_kernel(int* pos, int n, int base) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
+    pos[r] = base + r;
+}
+__global__ void mark_rows_kernel(uint8_t* origin, int len, int lo, int hi, const int* sel,
+                                 const int* count, int rows_max) {
+  const int rows = count ? *count : rows_max;
+  const int layers = hi - lo + 1;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows * layers;
+       i += gridDim.x * blockDim.x)
+    origin[(size_t)(lo + i / rows) * len + sel[i % rows]] = 1;
+}
+__global__ void mark_layers_kernel(uint8_t* origin, int len, int lo, int hi) {
+  const size_t total = (size_t)(hi - lo + 1) * len;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x)
+    origin[(size_t)lo * len + i] = 1;
+}
+__global__ void set_depth_kernel(uint64_t* depth, int n, uint64_t v) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) depth[i] = v;
+}
+
+// argmax (model.cpp:364-370): first index of the maximum.
+__global__ void argmax_kernel(const float* x, int n, int* out) {
+  float best = -__int_as_float(0x7f800000);
+  int bi = 0x7fffffff;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const float v = x[i];
+    if (v > best || (v == best && i < bi)) { best = v; bi = i; }
+  }
+  __shared__ float sv[1024];
+  __shared__ int si[1024];
+  sv[threadIdx.x] = best;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      const float v = sv[threadIdx.x + s];
+      const int i = si[threadIdx.x + s];
+      if (v > sv[threadIdx.x] || (v == sv[threadIdx.x] && i < si[threadIdx.x])) {
+        sv[threadIdx.x] = v;
+        si[threadIdx.x] = i;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = si[0] == 0x7fffffff ? 0 : si[0];
+}
+
+// ---------------------------------------------------------------------------
+// K1 realign + graft (relay_cache.cpp:154-174 + relay_engine.cpp:136-148).
+// One CTA owns kPos consecutive segment positions: their double cos/sin rows
+// (host-built with glibc, exactly rope_rotate's) are staged in shared memory
+// once and reused across all L layers and all KV heads. Each thread moves
+// 16-byte vectors: K pairs are rotated in double without FMA then rounded
+// (tensor.cpp:140-141); V is a bit copy. Layers [skip_lo, skip_hi] are
+// skipped (the band recompute overwrites them; relay_engine.cpp:261-264).
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256) realign_graft_kernel(
+    const T* __restrict__ k_pre, const T* __restrict__ v_src, int L, int n, int kv, int dh,
+    const double2* __restrict__ rope, int base, T* __restrict__ ctx_k, T* __restrict__ ctx_v,
+    size_t ctx_layer_stride, int skip_lo, int skip_hi) {
+  constexpr int kPos = 8;
+  constexpr int VEC = 16 / sizeof(T);  // elements per 16-byte vector
+  extern __shared__ double2 cs[];      // [kPos][dh/2]
+  const int p0 = blockIdx.x * kPos;
+  const int npos = min(kPos, n - p0);
+  const int half = dh / 2;
+  for (int i = threadIdx.x; i < npos * half; i += blockDim.x)
+    cs[i] = rope[(size_t)(base + p0 + i / half) * half + (i % half)];
+  __syncthreads();
+  const int vecs_per_row = kv / VEC;
+  const int total = npos * vecs_per_row;
+  for (int l = 0; l < L; ++l) {
+    if (l >= skip_lo && l <= skip_hi) continue;
+    const T* ks = k_pre + (size_t)l * n * kv + (size_t)p0 * kv;
+    const T* vs = v_src + (size_t)l * n * kv + (size_t)p0 * kv;
+    T* kd = ctx_k + (size_t)l * ctx_layer_stride + (size_t)(base + p0) * kv;
+    T* vd = ctx_v + (size_t)l * ctx_layer_stride + (size_t)(base + p0) * kv;
+    for (int t = threadIdx.x; t < total; t += blockDim.x) {
+      const int p = t / vecs_per_row;
+      const int off = (t % vecs_per_row) * VEC;
+      const uint4 kraw = *reinterpret_cast<const uint4*>(ks + (size_t)p * kv + off);
+      const uint4 vraw = *reinterpret_cast<const uint4*>(vs + (size_t)p * kv + off);
+      const T* kin = reinterpret_cast<const T*>(&kraw);
+      uint4 kout_raw;
+      T* kout = reinterpret_cast<T*>(&kout_raw);
+#pragma unroll
+      for (int e = 0; e < VEC; e += 2) {
+        const int pair = ((off + e) % dh) / 2;
+        const double2 c_s = cs[p * half + pair];
+        double x0, x1;
+        if constexpr (sizeof(T) == 4) {
+          x0 = (double)kin[e];
+          x1 = (double)kin[e + 1];
+        } else {
+          x0 = (double)__bfloat162float(kin[e]);
+          x1 = (double)__bfloat162float(kin[e + 1]);
+        }
+        const double r0 = __dsub_rn(__dmul_rn(c_s.x, x0), __dmul_rn(c_s.y, x1));
+        const double r1 = __dadd_rn(__dmul_rn(c_s.y, x0), __dmul_rn(c_s.x, x1));
+        if constexpr (sizeof(T) == 4) {
+          kout[e] = __double2float_rn(r0);
+          kout[e + 1] = __double2float_rn(r1);
+        } else {
+          kout[e] = __float2bfloat16_rn(__double2float_rn(r0));
+          kout[e + 1] = __float2bfloat16_rn(__double2float_rn(r1));
+        }
+      }
+      *reinterpret_cast<uint4*>(kd + (size_t)p * kv + off) = kout_raw;
+      *reinterpret_cast<uint4*>(vd + (size_t)p * kv + off) = vraw;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2 deviation scoring at l_det (relay_engine.cpp:270-277):
+//   s_dev[j]     = mean_head_cosine_deviation(ctx V[l_det][base+j], cache V[l_det][j])
+//   s_key_dev[j] = same for ctx K[l_det][base+j] vs realigned cache K (rotated
+//                  on the fly from K_pre, bit-identical to realign()).
+// cosine_d (metrics.cpp:21-32): sequential double dot/norms per head slice;
+// zero-norm -> 0; bit-identical slices -> exactly 1; clamp. Heads are summed
+// in order (metrics.cpp:99-102). One thread per (token, head, {V,K}).
+// ---------------------------------------------------------------------------
+__device__ double cosine_slice(const void* a, size_t ai, const void* b, size_t bi, size_t elem,
+                               int dh, const double2* cs, bool rotate_b) {
+  double dot = 0.0, na = 0.0, nb = 0.0;
+  bool same = true;
+  for (int i = 0; i < dh; i += 2) {
+    float x0 = load_elem(a, ai + i, elem), x1 = load_elem(a, ai + i + 1, elem);
+    float y0 = load_elem(b, bi + i, elem), y1 = load_elem(b, bi + i + 1, elem);
+    if (rotate_b) {
+      const double2 c = cs[i / 2];
+      const double r0 = __dsub_rn(__dmul_rn(c.x, (double)y0), __dmul_rn(c.y, (double)y1));
+      const double r1 = __dadd_rn(__dmul_rn(c.y, (double)y0), __dmul_rn(c.x, (double)y1));
+      y0 = __double2float_rn(r0);
+      y1 = __double2float_rn(r1);
+      if (elem == 2) {  // realigned keys are stored in the context's bf16
+        y0 = __bfloat162float(__float2bfloat16_rn(y0));
+        y1 = __bfloat162float(__float2bfloat16_rn(y1));
+      }
+    }
+    same = same && __float_as_uint(x0) == __float_as_uint(y0) && __float_as_uint(x1) == __float_as_uint(y1);
+    const double a0 = x0, a1 = x1, b0 = y0, b1 = y1;
+    dot = __dadd_rn(dot, __dmul_rn(a0, b0));
+    na = __dadd_rn(na, __dmul_rn(a0, a0));
+    nb = __dadd_rn(nb, __dmul_rn(b0, b0));
+    dot = __dadd_rn(dot, __dmul_rn(a1, b1));
+    na = __dadd_rn(na, __dmul_rn(a1, a1));
+    nb = __dadd_rn(nb, __dmul_rn(b1, b1));
+  }
+  const double sa = __dsqrt_rn(na), sb = __dsqrt_rn(nb);
+  if (sa < 1e-12 || sb < 1e-12) return 0.0;
+  if (same) return 1.0;
+  const double c = __ddiv_rn(dot, __dmul_rn(sa, sb));
+  return c < -1.0 ? -1.0 : (c > 1.0 ? 1.0 : c);
+}
+
+__global__ void score_kernel(const void* ctx_v, const void* cache_v, const void* ctx_k,
+                             const void* cache_kpre, size_t elem, int n, int kv, int heads, int dh,
+                             const double2* rope, int base, double* s_dev, double* s_key) {
+  extern __shared__ double cosv[];  // [tok][2][heads]
+  const int tok_per_cta = blockDim.x / (2 * heads);
+  const int t = threadIdx.x / (2 * heads);
+  const int which = (threadIdx.x / heads) % 2;  // 0 = V, 1 = K
+  const int h = threadIdx.x % heads;
+  const int j = blockIdx.x * tok_per_cta + t;
+  if (t < tok_per_cta && j < n) {
+    const size_t ai = (size_t)j * kv + h * dh;
+    double c;
+    if (which == 0) {
+      c = cosine_slice(ctx_v, ai, cache_v, ai, elem, dh, nullptr, false);
+    } else {
+      c = cosine_slice(ctx_k, ai, cache_kpre, ai, elem, dh,
+                       rope + (size_t)(base + j) * (dh / 2), true);
+    }
+    cosv[(t * 2 + which) * heads + h] = c;
+  }
+  __syncthreads();
+  if (threadIdx.x < tok_per_cta * 2) {
+    const int tt = threadIdx.x / 2, w = threadIdx.x % 2;
+    const int jj = blockIdx.x * tok_per_cta + tt;
+    if (jj < n) {
+      double acc = 0.0;
+      for (int hh = 0; hh < heads; ++hh) acc = __dadd_rn(acc, cosv[(tt * 2 + w) * heads + hh]);
+      const double dev = __dsub_rn(1.0, __ddiv_rn(acc, (double)heads));
+      (w == 0 ? s_dev : s_key)[jj] = dev;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2b selection (selector.cpp:32-88): mean-relative thresholds with the
+// reference's sequential double mean, suffix window, sorted union with tag
+// bits via a block-wide scan compaction. One CTA.
+// info: [0] count [1] dev [2] inf-score [3] inf-suffix [4] blend
+// dinfo: [0] dev threshold (0 if none) [1] min relative margin
+// ---------------------------------------------------------------------------
+__device__ void block_compact(const uint32_t* flags_smem_unused, int n, const uint32_t* flags,
+                              int* sel_idx, uint32_t* sel_tags, int* info) {
+  __shared__ int warp_sums[32];
+  __shared__ int running;
+  __shared__ int cnt[4];
+  if (threadIdx.x == 0) { running = 0; cnt[0] = cnt[1] = cnt[2] = cnt[3] = 0; }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+  for (int chunk = 0; chunk < n; chunk += blockDim.x) {
+    const int j = chunk + threadIdx.x;
+    const uint32_t f = j < n ? flags[j] : 0u;
+    const int pred = f != 0;
+    c0 += (f & RK_SEL_DEVIATION) != 0;
+    c1 += (f & RK_SEL_INFLUENCE_SCORE) != 0;
+    c2 += (f & RK_SEL_INFLUENCE_SUFFIX) != 0;
+    c3 += (f & RK_SEL_BLEND_TOPK) != 0;
+    const unsigned ballot = __ballot_sync(0xffffffffu, pred);
+    const int within = __popc(ballot & ((1u << lane) - 1u));
+    if (lane == 0) warp_sums[wid] = __popc(ballot);
+    __syncthreads();
+    if (wid == 0) {
+      int v = lane < nw ? warp_sums[lane] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
+      }
+      if (lane < nw) warp_sums[lane] = v;  // inclusive
+    }
+    __syncthreads();
+    const int warp_off = wid == 0 ? 0 : warp_sums[wid - 1];
+    if (pred) {
+      const int pos = running + warp_off + within;
+      sel_idx[pos] = j;
+      sel_tags[pos] = f;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) running += warp_sums[nw - 1];
+    __syncthreads();
+  }
+  atomicAdd(&cnt[0], c0);
+  atomicAdd(&cnt[1], c1);
+  atomicAdd(&cnt[2], c2);
+  atomicAdd(&cnt[3], c3);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    info[0] = running;
+    info[1] = cnt[0];
+    info[2] = cnt[1];
+    info[3] = cnt[2];
+    info[4] = cnt[3];
+  }
+}
+
+__global__ void __launch_bounds__(1024) select_relay_kernel(
+    const double* s_dev, const float* influence, const double* infl_mean, int n, double tau_dev,
+    double tau_inf, int suffix_k, uint32_t* flags, int* sel_idx, uint32_t* sel_tags, int* info,
+    double* dinfo) {
+  __shared__ double thr[2];
+  __shared__ int valid[2];
+  if (threadIdx.x == 0) {
+    // mean_relative (selector.cpp:37-39): sequential sum, then divide.
+    double mean = 0.0;
+    for (int j = 0; j < n; ++j) mean = __dadd_rn(mean, s_dev[j]);
+    mean = __ddiv_rn(mean, (double)n);
+    valid[0] = mean > 0.0;
+    thr[0] = __dmul_rn(tau_dev, mean);
+    const double mi = *infl_mean;
+    valid[1] = mi > 0.0;
+    thr[1] = __dmul_rn(tau_inf, mi);
+  }
+  __syncthreads();
+  const int start = suffix_k >= n ? 0 : n - suffix_k;
+  double margin = 1e300;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    uint32_t f = 0;
+    const double s = s_dev[j];
+    if (valid[0] && s >= thr[0]) f |= RK_SEL_DEVIATION;
+    if (valid[1] && (double)influence[j] >= thr[1]) f |= RK_SEL_INFLUENCE_SCORE;
+    if (suffix_k > 0 && j >= start) f |= RK_SEL_INFLUENCE_SUFFIX;
+    flags[j] = f;
+    if (valid[0]) margin = fmin(margin, fabs(s - thr[0]) / thr[0]);
+  }
+  __shared__ double mred[32];
+  for (int o = 16; o > 0; o >>= 1) margin = fmin(margin, __shfl_xor_sync(0xffffffffu, margin, o));
+  if ((threadIdx.x & 31) == 0) mred[threadIdx.x >> 5] = margin;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 1e300;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmin(m, mred[w]);
+    dinfo[0] = valid[0] ? thr[0] : 0.0;
+    dinfo[1] = valid[0] ? m : __longlong_as_double(0x7ff0000000000000LL);
+  }
+  __syncthreads();
+  block_compact(nullptr, n, flags, sel_idx, sel_tags, info);
+}
+
+// BLEND score (relay_engine.cpp:318-330): L2 norm of fresh-vs-stale V at layer 1.
+__global__ void blend_score_kernel(const void* ctx_v, const void* cache_v, size_t elem, int n,
+                                   int kv, double* score) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double acc = 0.0;
+  for (int e = 0; e < kv; ++e) {
+    const double diff = __dsub_rn((double)load_elem(ctx_v, (size_t)j * kv + e, elem),
+                                  (double)load_elem(cache_v, (size_t)j * kv + e, elem));
+    acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+  }
+  score[j] = __dsqrt_rn(acc);
+}
+
+// top_k_by_score (selector.cpp:90-105): rank by (score desc, index asc).
+__global__ void topk_flags_kernel(const double* score, int n, int count, uint32_t* flags) {
+  extern __shared__ double tile[];
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const double sj = j < n ? score[j] : 0.0;
+  int rank = 0;
+  for (int t0 = 0; t0 < n; t0 += blockDim.x) {
+    if (t0 + (int)threadIdx.x < n) tile[threadIdx.x] = score[t0 + threadIdx.x];
+    __syncthreads();
+    const int lim = min((int)blockDim.x, n - t0);
+    for (int i = 0; i < lim; ++i) {
+      const double si = tile[i];
+      const int ii = t0 + i;
+      rank += (si > sj) || (si == sj && ii < j);
+    }
+    __syncthreads();
+  }
+  if (j < n) flags[j] = rank < count ? RK_SEL_BLEND_TOPK : 0u;
+}
+
+__global__ void __launch_bounds__(1024) compact_kernel(int n, const uint32_t* flags, int* sel_idx,
+                                                       uint32_t* sel_tags, int* info) {
+  block_compact(nullptr, n, flags, sel_idx, sel_tags, info);
+}
+
+__global__ void seq_mean_kernel(const float* x, int n, double* out) {
+  double m = 0.0;
+  for (int j = 0; j < n; ++j) m = __dadd_rn(m, (double)x[j]);
+  *out = __ddiv_rn(m, (double)n);
+}
+
+}  // namespace
+
+namespace k {
+
+void init_uniform(cudaStream_t s, float* dst, size_t n, uint64_t state0, float scale) {
+  init_uniform_kernel<<<blocks_for(n) < 4096 ? blocks_for(n) : 4096, kThreads, 0, s>>>(dst, n, state0, scale);
+}
+void fill(cudaStream_t s, float* dst, size_t n, float v) {
+  fill_kernel<<<blocks_for(n) < 4096 ? blocks_for(n) : 4096, kThreads, 0, s>>>(dst, n, v);
+}
+void copy_cols_f32(cudaStream_t s, float* dst, size_t ldd, size_t c0, const float* src, size_t lds,
+                   size_t rows, size_t cols, size_t cstride) {
+  const size_t n = rows * cols;
+  copy_cols_kernel<<<blocks_for(n) < 8192 ? blocks_for(n) : 8192, kThreads, 0, s>>>(dst, ldd, c0, src, lds, rows, cols, cstride);
+}
+void transpose_to_bf16(cudaStream_t s, __nv_bfloat16* dst, size_t ldd, size_t c0, size_t cstride,
+                       const float* src, size_t rows, size_t cols) {
+  dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
+  transpose_bf16_kernel<<<grid, dim3(32, 8), 0, s>>>(dst, ldd, c0, cstride, src, rows, cols);
+}
+void f32_to_bf16(cudaStream_t s, __nv_bfloat16* dst, const float* src, size_t n) {
+  f32_to_bf16_kernel<<<blocks_for(n) < 8192 ? blocks_for(n) : 8192, kThreads, 0, s>>>(dst, src, n);
+}
+void bf16_to_f32(cudaStream_t s, float* dst, const __nv_bfloat16* src, size_t n) {
+  bf16_to_f32_kernel<<<blocks_for(n) < 8192 ? blocks_for(n) : 8192, kThreads, 0, s>>>(dst, src, n);
+}
+void copy2d_f32(cudaStream_t s, float* dst, size_t dld, size_t dcs, const float* src, size_t sld,
+                size_t scs, size_t rows, size_t cols) {
+  const size_t n = rows * cols;
+  copy2d_kernel<<<blocks_for(n) < 8192 ? blocks_for(n) : 8192, kThreads, 0, s>>>(dst, dld, dcs, src, sld, scs, rows, cols);
+}
+void untranspose_bf16(cudaStream_t s, float* dst, const __nv_bfloat16* src, size_t ld, size_t c0,
+                      size_t cstride, size_t rows, size_t cols) {
+  const size_t n = rows * cols;
+  untranspose_bf16_kernel<<<blocks_for(n) < 8192 ? blocks_for(n) : 8192, kThreads, 0, s>>>(dst, src, ld, c0, cstride, rows, cols);
+}
+void doubles_to_floats(cudaStream_t s, float* dst, const double* src, int n) {
+  d2f_kernel<<<blocks_for(n), kThreads, 0, s>>>(dst, src, n);
+}
+void embed(cudaStream_t s, float* hidden, const void* emb, size_t elem, const int32_t* tokens,
+           int n, int d, int, int*) {
+  const size_t total = (size_t)n * d;
+  embed_kernel<<<blocks_for(total) < 4096 ? blocks_for(total) : 4096, kThreads, 0, s>>>(hidden, emb, elem, tokens, n, d);
+}
+void gather_rows(cudaStream_t s, float* dst, const float* src, const int* idx, const int* count,
+                 int rows_max, int d) {
+  const size_t total = (size_t)rows_max * d;
+  gather_rows_kernel<<<blocks_for(total) < 4096 ? blocks_for(total) : 4096, kThreads, 0, s>>>(dst, src, idx, count, rows_max, d);
+}
+void scatter_rows(cudaStream_t s, float* dst, const float* src, const int* idx, const int* count,
+                  int rows_max, int d, uint64_t* depth, uint64_t depth_value) {
+  const size_t total = (size_t)rows_max * d;
+  scatter_rows_kernel<<<blocks_for(total) < 4096 ? blocks_for(total) : 4096, kThreads, 0, s>>>(
+      dst, src, idx, count, rows_max, d, depth, depth_value);
+}
+void positions_from_sel(cudaStream_t s, int* pos, const int* sel, const int* count, int rows_max,
+                        int base) {
+  positions_from_sel_kernel<<<blocks_for(rows_max), kThreads, 0, s>>>(pos, sel, count, rows_max, base);
+}
+void iota_positions(cudaStream_t s, int* pos, int n, int base) {
+  iota_kernel<<<blocks_for(n), kThreads, 0, s>>>(pos, n, base);
+}
+void mark_rows(cudaStream_t s, uint8_t* origin, int len, int lo, int hi, const int* sel,
+               const int* count, int rows_max) {
+  if (hi < lo) return;
+  mark_rows_kernel<<<blocks_for((size_t)rows_max * (hi - lo + 1)), kThreads, 0, s>>>(origin, len, lo, hi, sel, count, rows_max);
+}
+void mark_layers(cudaStream_t s, uint8_t* origin, int len, int lo, int hi) {
+  if (hi < lo) return;
+  mark_layers_kernel<<<blocks_for((size_t)(hi - lo + 1) * len), kThreads, 0, s>>>(origin, len, lo, hi);
+}
+void set_depth(cudaStream_t s, uint64_t* depth, int n, uint64_t v) {
+  set_depth_kernel<<<blocks_for(n), kThreads, 0, s>>>(depth, n, v);
+}
+void argmax(cudaStream_t s, const float* x, int n, int* out) {
+  argmax_kernel<<<1, 1024, 0, s>>>(x, n, out);
+}
+
+void realign_graft(cudaStream_t s, const void* k_pre, const void* v_src, size_t elem, int L, int n,
+                   int kv, int dh, const double2* rope, int base, void* ctx_k, void* ctx_v,
+                   size_t ctx_layer_stride, int skip_lo, int skip_hi) {
+  constexpr int kPos = 8;
+  const int grid = (n + kPos - 1) / kPos;
+  const size_t smem = kPos * (dh / 2) * sizeof(double2);
+  if (elem == 4)
+    realign_graft_kernel<float><<<grid, 256, smem, s>>>(
+        (const float*)k_pre, (const float*)v_src, L, n, kv, dh, rope, base, (float*)ctx_k,
+        (float*)ctx_v, ctx_layer_stride, skip_lo, skip_hi);
+  else
+    realign_graft_kernel<__nv_bfloat16><<<grid, 256, smem, s>>>(
+        (const __nv_bfloat16*)k_pre, (const __nv_bfloat16*)v_src, L, n, kv, dh, rope, base,
+        (__nv_bfloat16*)ctx_k, (__nv_bfloat16*)ctx_v, ctx_layer_stride, skip_lo, skip_hi);
+}
+
+void score_deviation(cudaStream_t s, const void* ctx_v, const void* cache_v, const void* ctx_k,
+                     const void* cache_kpre, size_t elem, int n, int kv, int heads, int dh,
+                     const double2* rope, int base, double* s_dev, double* s_key) {
+  int tok = 128 / (2 * heads);
+  if (tok < 1) tok = 1;
+  const int threads = tok * 2 * heads;
+  const int grid = (n + tok - 1) / tok;
+  score_kernel<<<grid, threads, (size_t)tok * 2 * heads * sizeof(double), s>>>(
+      ctx_v, cache_v, ctx_k, cache_kpre, elem, n, kv, heads, dh, rope, base, s_dev, s_key);
+}
+
+void select_relay(cudaStream_t s, const double* s_dev, const float* influence,
+                  const double* infl_mean, int n, double tau_dev, double tau_inf, int suffix_k,
+                  int* sel_idx, uint32_t* sel_tags, int* info, double* dinfo) {
+  // flags scratch lives after sel_tags (caller sizes sel_tags to 2n)
+  select_relay_kernel<<<1, 1024, 0, s>>>(s_dev, influence, infl_mean, n, tau_dev, tau_inf,
+                                         suffix_k, sel_tags + n, sel_idx, sel_tags, info, dinfo);
+}
+void blend_scores(cudaStream_t s, const void* ctx_v, const void* cache_v, size_t elem, int n,
+                  int kv, double* score) {
+  blend_score_kernel<<<blocks_for(n), kThreads, 0, s>>>(ctx_v, cache_v, elem, n, kv, score);
+}
+void select_topk(cudaStream_t s, const double* score, int n, int count, int* sel_idx,
+                 uint32_t* sel_tags, int* info) {
+  topk_flags_kernel<<<blocks_for(n), kThreads, kThreads * sizeof(double), s>>>(score, n, count, sel_tags + n);
+  compact_kernel<<<1, 1024, 0, s>>>(n, sel_tags + n, sel_idx, sel_tags, info);
+}
+void seq_mean(cudaStream_t s, const float* x, int n, double* out) {
+  seq_mean_kernel<<<1, 1, 0, s>>>(x, n, out);
+}
+
+}  // namespace k
+}  // namespace rk

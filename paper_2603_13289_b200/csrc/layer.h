@@ -1,0 +1,96 @@
+// layer.h -- per-call orchestration (Runner) shared by the C ABI entry points.
+#pragma once
+
+#include <vector>
+
+#include "internal.h"
+
+namespace rk {
+
+// Device-side state of one relay_extend, resolved on the host by finish().
+struct ExtendResult {
+  int mode = RK_MODE_RELAY;
+  uint64_t base = 0, n = 0, L = 0;
+  uint64_t band_layers = 0, sparse_layers = 0;  // recomputed = n*band + |I|*sparse
+  int slot = 0;                                 // scratch slot holding device buffers
+  size_t seg_index = 0;                         // SegmentMarks index in the context
+  int ev_begin = -1, ev_realign = -1, ev_band = -1, ev_select = -1, ev_end = -1;
+  int blend_count = 0;
+  uint64_t l_start = 0, l_det = 0, sparse_hi = 0;
+  bool resolved = false;
+  // host copies after finish()
+  int info[8] = {0};
+  double dinfo[2] = {0, 0};
+  rk_reuse_stats stats{};
+};
+
+// Grow-only device buffers of one extend slot.
+struct ExtendSlot {
+  DevBuf hidden, sub_hidden, depth, s_dev, s_key, sel_idx, sel_tags, info, dinfo, sub_pos, score;
+};
+
+class Runner {
+ public:
+  Runner(rk_engine* e, rk_weights* w);
+  ~Runner();
+
+  void prefill(rk_context* ctx, const int32_t* tokens, uint64_t n, uint64_t base, bool want_logits);
+  ExtendResult relay_extend(rk_context* ctx, rk_cache* cache, const rk_layer_profile* prof,
+                            const rk_relay_options& opts);
+  // relay_prefill's next-token logits at the segment end (relay_engine.cpp:381-393)
+  void segment_end_logits(rk_context* ctx, const ExtendResult& res);
+  void agent_prefill(rk_context* ctx, const int32_t* prefix, uint64_t n_prefix,
+                     rk_cache* const* ups, uint64_t n_up, const int32_t* suffix, uint64_t n_suffix,
+                     const rk_layer_profile* prof, const rk_relay_options& opts,
+                     std::vector<ExtendResult>& results);
+  rk_cache* capture_prefill(rk_context* ctx, const int32_t* tokens, uint64_t n, uint64_t snapshot,
+                            bool include_self);
+  rk_cache* capture_decode(rk_context* ctx, const float* first_logits, uint64_t n,
+                           uint64_t snapshot, bool include_self);
+
+  // Synchronize, raise on device-side errors, resolve pending ExtendResults.
+  void finish();
+  void resolve(ExtendResult& r);  // after finish(): counts, stats, timings
+  void fill_output(ExtendResult& res, rk_context* ctx, rk_relay_output* out);
+  void download_logits(float* dst);
+  int32_t first_token();
+
+  void begin_timer();
+  float lap_ms();  // ms since begin_timer (synchronizes)
+
+ private:
+  // one decoder layer over a row set (run_layer_rows, model.cpp:237-280)
+  void run_layer(rk_context* ctx, int layer, float* hidden, Rows rows, bool commit, int max_ctx,
+                 float* probs = nullptr, int key_lo = 0, int key_n = 0);
+  void last_row_logits(const float* hidden_row);  // output_logits (model.cpp:282-288)
+  void row_logits_from_layer(rk_context* ctx, const float* hidden_row, uint64_t first_layer,
+                             uint64_t position);
+  void ensure_rows(size_t rows);
+  int* upload_tokens(const int32_t* tokens, uint64_t n, int slot);
+  void check_tokens(const int32_t* tokens, uint64_t n);
+  int event();
+  ExtendSlot& slot(int i);
+
+  rk_engine* e_;
+  rk_weights* w_;
+  cudaStream_t st_;
+  std::vector<ExtendResult*> pending_;
+  int next_event_ = 0;
+  int next_slot_ = 0;
+  int timer_ev_ = -1;
+  bool have_logits_ = false;
+  int tok_cursor_ = 0;
+  float* cap_k_ = nullptr;  // capture destinations for pre-RoPE K / V rows
+  float* cap_v_ = nullptr;
+};
+
+// weights_export helper: unpack tensor idx of the engine layout to fp32 [rows x cols].
+void layer_unpack_tensor(rk_weights* w, size_t idx, float* dst, size_t rows, size_t cols);
+
+// bf16 layer path (layer_bf16.cu)
+void run_layer_bf16(rk_engine* e, rk_weights* w, rk_context* ctx, int layer, float* hidden,
+                    Rows rows, bool commit, int max_ctx, float* probs, int key_lo, int key_n,
+                    void* cap_k, void* cap_v);
+void last_row_logits_bf16(rk_engine* e, rk_weights* w, const float* hidden_row, float* logits);
+
+}  // namespace rk

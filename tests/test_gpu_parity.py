@@ -1,0 +1,168 @@
+"""GPU parity: the fp32-exact CUDA path through the C ABI against the oracle
+on identical seeded inputs. Bar: BIT-EXACT for everything (contexts, marks,
+selection + tags, s_dev/s_key_dev, hidden states, depths, logits, caches),
+which is stronger than the north_star's 1e-4 fp32 tolerance."""
+import numpy as np
+import pytest
+
+from paper_2603_13289_b200.abi import InvalidArgument, LayerProfile, RelayOptions, SchemaError
+from tests.compare import assert_bit_equal, assert_outputs_equal
+from tests.scenarios import c1_spec, parity_scenarios, pattern_tokens, spec_of, synthetic_tokens, triple
+
+pytestmark = pytest.mark.gpu
+SCEN = parity_scenarios()
+
+
+def test_weights_init_bit_exact(engine, oracle):
+    for spec in (spec_of(8, 32, 4), c1_spec()):
+        w = engine.weights(spec, 1234)
+        ow = oracle.weights(spec, 1234)
+        for i in range(w.num_tensors()):
+            want = oracle.weights_tensor(ow, i)
+            assert_bit_equal(w.tensor(i, want.size), want, f"tensor {i}")
+
+
+@pytest.mark.parametrize("scen", SCEN, ids=[s[0] for s in SCEN])
+def test_relay_prefill_bit_exact(engine, oracle, scen):
+    name, spec, seed, old, n, snap, new, prof, opts = scen
+    ow = oracle.weights(spec, seed)
+    cache = oracle.scenario(ow, old, n, snap)
+    want, octx = oracle.relay_prefill(ow, new, cache, prof, opts)
+    w = engine.weights(spec, seed)
+    ctx = w.context()
+    got = ctx.relay_prefill(new, w.upload_cache(cache), prof, opts)
+    assert_outputs_equal(got, want, name)
+    assert_bit_equal(got["logits"], want["logits"], f"{name}.logits")
+    K, V = ctx.all()
+    Ko, Vo = oracle.ctx_all(octx)
+    assert_bit_equal(K, Ko, f"{name}.ctx.K")
+    assert_bit_equal(V, Vo, f"{name}.ctx.V")
+    segs, osegs = ctx.segments(), oracle.ctx_segments(octx)
+    assert [(b, l) for b, l, _ in segs] == [(b, l) for b, l, _ in osegs]
+    for (_, _, a), (_, _, b) in zip(segs, osegs):
+        assert_bit_equal(a, b, f"{name}.marks")
+    # marks agree with the accounting identity (relay_engine.cpp:347-358)
+    assert int(segs[0][2].sum()) == got["stats"]["recomputed_entries"]
+
+
+def test_c1_bit_exact_and_capture(engine, oracle):
+    """BASELINE config 1 (2 layers, d=256, 4 heads, 512-token segment): GPU
+    decode-time capture == oracle capture, and the relay prefill is bit-exact."""
+    spec = c1_spec()
+    ow = oracle.weights(spec, 1234)
+    old = synthetic_tokens(1234, 1, 64, 256)
+    cache = oracle.scenario(ow, old, 512, 0)
+    w = engine.weights(spec, 1234)
+    dctx = w.context()
+    logits = dctx.prefill(old)
+    gcache = dctx.capture_decode(logits, 512, 0).to_host()
+    for f in ("segment_tokens", "k_pre", "v", "hidden_snapshot", "influence"):
+        assert_bit_equal(getattr(gcache, f), getattr(cache, f), f"c1.capture.{f}")
+    new = synthetic_tokens(1234, 2, 48, 256)
+    want, octx = oracle.relay_prefill(ow, new, cache, triple(0, 0, 1), RelayOptions.make())
+    ctx = w.context()
+    got = ctx.relay_prefill(new, w.upload_cache(cache), triple(0, 0, 1), RelayOptions.make())
+    assert_outputs_equal(got, want, "c1")
+    assert_bit_equal(got["logits"], want["logits"], "c1.logits")
+    K, V = ctx.all()
+    Ko, Vo = oracle.ctx_all(octx)
+    assert_bit_equal(K, Ko, "c1.K")
+    assert_bit_equal(V, Vo, "c1.V")
+
+
+@pytest.mark.parametrize("mode", ["relay", "full", "blend"])
+def test_agent_prefill_bit_exact(engine, oracle, mode):
+    spec = spec_of(8, 32, 4)
+    ow = oracle.weights(spec, 55)
+    c1 = oracle.scenario(ow, pattern_tokens(9, 64, 1), 12, 1)
+    c2 = oracle.scenario(ow, pattern_tokens(7, 64, 2), 9, 1)
+    opts = RelayOptions.make(mode=mode, suffix_k=3, blend_alpha=0.25)
+    prof = triple(1, 2, 5)
+    for suffix in (pattern_tokens(4, 64, 4), np.zeros(0, np.int32)):
+        logits, tok, octx = oracle.agent_prefill(ow, pattern_tokens(5, 64, 3), [c1, c2], suffix, prof, opts)
+        w = engine.weights(spec, 55)
+        ctx = w.context()
+        got = ctx.agent_prefill(pattern_tokens(5, 64, 3), [w.upload_cache(c1), w.upload_cache(c2)], suffix,
+                                prof, opts)
+        assert_bit_equal(got["logits"], logits, f"agent.{mode}.logits")
+        assert got["first_token"] == tok
+        K, V = ctx.all()
+        Ko, Vo = oracle.ctx_all(octx)
+        assert_bit_equal(K, Ko, f"agent.{mode}.K")
+        assert_bit_equal(V, Vo, f"agent.{mode}.V")
+
+
+def test_zero_mode_round_trip(engine, oracle):
+    """ZERO with the unchanged prefix reproduces decode-time KV (test_engine.cpp:124-137)."""
+    spec = spec_of(8, 32, 4)
+    ow = oracle.weights(spec, 102)
+    old = pattern_tokens(10, 64, 0)
+    cache, dctx = oracle.scenario(ow, old, 8, 2, return_decode_ctx=True)
+    w = engine.weights(spec, 102)
+    ctx = w.context()
+    got = ctx.relay_prefill(old, w.upload_cache(cache), LayerProfile(), RelayOptions.make(mode="zero"))
+    K, V = ctx.all()
+    Kd, Vd = oracle.ctx_all(dctx)
+    assert_bit_equal(K, Kd, "zero.K")
+    assert_bit_equal(V, Vd, "zero.V")
+    assert got["stats"]["recomputed_entries"] == 0 and got["stats"]["reuse_rate"] == 1.0
+
+
+def test_accounting_formula(engine, oracle):
+    """(1,3,18) on 32 layers, N=100, |I|=10 -> 450 entries, reuse 0.859375 (test_engine.cpp:139-178)."""
+    spec = spec_of(32, 16, 2)
+    ow = oracle.weights(spec, 103)
+    cache = oracle.scenario(ow, pattern_tokens(8, 64, 0), 100, 1)
+    w = engine.weights(spec, 103)
+    ctx = w.context()
+    opts = RelayOptions.make(tau_dev=1e9, tau_inf=1e9, suffix_k=10)
+    got = ctx.relay_prefill(pattern_tokens(12, 64, 3), w.upload_cache(cache), triple(1, 3, 18), opts)
+    st = got["stats"]
+    assert st["selected_count"] == 10 and st["total_entries"] == 3200
+    assert st["recomputed_entries"] == 450 and st["reuse_rate"] == 0.859375
+    marks = ctx.segments()[0][2]
+    assert marks[1:4].all() and not marks[0].any() and not marks[19:].any()
+    assert (marks[4:19, 90:] == 1).all() and not marks[4:19, :90].any()
+
+
+def test_suffix_never_touches_segment_cells(engine, oracle):
+    spec = spec_of(8, 32, 4)
+    ow = oracle.weights(spec, 106)
+    cache = oracle.scenario(ow, pattern_tokens(10, 64, 0), 8, 1)
+    w = engine.weights(spec, 106)
+    ctx = w.context()
+    ctx.relay_prefill(pattern_tokens(6, 64, 4), w.upload_cache(cache), triple(1, 2, 5), RelayOptions.make())
+    seg_end = ctx.size
+    a, b = ctx.clone(), ctx.clone()
+    a.prefill(pattern_tokens(5, 64, 11))
+    b.prefill(pattern_tokens(5, 64, 12))
+    Ka, _ = a.all()
+    Kb, _ = b.all()
+    assert_bit_equal(Ka[:, :seg_end], Kb[:, :seg_end], "suffix.K")
+
+
+def test_validation_errors(engine, oracle):
+    spec = spec_of(8, 32, 4)
+    ow = oracle.weights(spec, 107)
+    cache = oracle.scenario(ow, pattern_tokens(10, 64, 0), 8, 2)
+    w = engine.weights(spec, 107)
+    c = w.upload_cache(cache)
+    prefix = pattern_tokens(4, 64, 1)
+    with pytest.raises(SchemaError):
+        w.context().relay_prefill(prefix, c, triple(1, 2, 20), RelayOptions.make())
+    with pytest.raises(InvalidArgument):
+        w.context().relay_prefill(prefix, c, triple(1, 2, 5), RelayOptions.make())
+    with pytest.raises(InvalidArgument):
+        w.context().relay_prefill(prefix, c, LayerProfile(), RelayOptions.make(mode="blend", blend_alpha=0.0))
+    ctx = w.context()
+    with pytest.raises(InvalidArgument):
+        ctx.prefill(np.zeros(0, np.int32))
+    with pytest.raises(InvalidArgument):
+        ctx.prefill([64])  # outside vocab
+    tiny = spec_of(8, 32, 4, max_positions=10)
+    w2 = engine.weights(tiny, 107)
+    ow2 = oracle.weights(tiny, 107)
+    c2 = oracle.scenario(ow2, pattern_tokens(4, 64, 0), 4, 0)
+    with pytest.raises(InvalidArgument):
+        w2.context().relay_prefill(pattern_tokens(8, 64, 2), w2.upload_cache(c2), LayerProfile(),
+                                   RelayOptions.make(mode="zero"))
