@@ -287,11 +287,12 @@ void attn_exact(cudaStream_t s, const float* qkv, Rows rows, int H, int Hkv, int
                 int max_ctx, float* probs, int key_lo, int key_n) {
   if (rows.rows_max <= 0) return;
   const size_t smem = (size_t)(dh + max_ctx + 1) * sizeof(float);
+  constexpr size_t kMaxDyn = 220 * 1024;
   if (!g_attn_smem_set) {
-    RK_CUDA(cudaFuncSetAttribute(attn_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    RK_CUDA(cudaFuncSetAttribute(attn_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDyn));
     g_attn_smem_set = 1;
   }
-  if (smem > 227 * 1024) raise(RK_ERR_INVALID_ARGUMENT, "fp32-exact attention: context too long for shared memory");
+  if (smem > kMaxDyn) raise(RK_ERR_INVALID_ARGUMENT, "fp32-exact attention: context too long for shared memory");
   dim3 grid(rows.rows_max, H);
   attn_exact_kernel<<<grid, 128, smem, s>>>(qkv, rows, H, Hkv, dh, ctx_k, ctx_v, out, self_override,
                                             probs, key_lo, key_n);
