@@ -1,0 +1,26 @@
+/*
+ * relaykv_b200_debug.h -- kernel-level test hooks (not part of the drop-in
+ * boundary). Used by tests/test_gpu_kernels.py to check the bf16 tensor-core
+ * GEMM and attention kernels in isolation against fp32 numpy references.
+ */
+#ifndef RELAYKV_B200_DEBUG_H_
+#define RELAYKV_B200_DEBUG_H_
+#include "relaykv_b200.h"
+#ifdef __cplusplus
+extern "C" {
+#endif
+/* C[M x N] (+)= A[M x K] . B[N x K]^T with bf16-rounded operands; epi 1 adds
+ * into C (residual epilogue, deterministic split-K), 3 stores. live_rows <=
+ * rows_max is passed through device memory like a sparse pass. */
+int rk_debug_gemm_bf16(rk_engine* e, const float* A, const float* B, float* C, int rows_max, int live_rows,
+                       int N, int K, int epi);
+/* out[M x H*dh] = causal attention of q rows at positions pos (ascending)
+ * over ctx rows [T x Hkv*dh]; bf16 operands. */
+int rk_debug_attention_bf16(rk_engine* e, const float* q, const float* k, const float* v, const int32_t* pos,
+                            int M, int T, int H, int Hkv, int dh, float* out);
+/* y[i] = device glibc_expf(x[i]) */
+int rk_debug_expf(rk_engine* e, const float* x, float* y, uint64_t n);
+#ifdef __cplusplus
+}
+#endif
+#endif

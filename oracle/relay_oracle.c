@@ -1055,3 +1055,6 @@ int orc_agent_prefill(orc_weights* w, orc_ctx* ctx, const int32_t* prefix, uint6
 
 /* Host libm expf, for checking the device restatement of glibc expf. */
 float orc_host_expf(float x) { return expf(x); }
+void orc_host_expf_array(const float* x, float* y, uint64_t n) {
+  for (uint64_t i = 0; i < n; ++i) y[i] = expf(x[i]);
+}

@@ -1,0 +1,101 @@
+// debug_hooks.cu -- kernel-level test entry points (relaykv_b200_debug.h).
+#include <string>
+#include <vector>
+#include <cmath>
+
+#include "glibc_expf.h"
+#include "layer_bf16.h"
+#include "relaykv_b200_debug.h"
+
+using namespace rk;
+
+namespace {
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return RK_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return RK_ERR_RUNTIME;
+  }
+}
+__global__ void expf_kernel(const float* x, float* y, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    y[i] = glibc_expf(x[i]);
+}
+DevBuf to_bf16(cudaStream_t st, const float* h, size_t n) {
+  DevBuf f(n * 4), b(n * 2);
+  RK_CUDA(cudaMemcpyAsync(f.p, h, n * 4, cudaMemcpyHostToDevice, st));
+  k::f32_to_bf16(st, b.as<__nv_bfloat16>(), f.as<float>(), n);
+  RK_CUDA(cudaStreamSynchronize(st));
+  return b;
+}
+}  // namespace
+
+extern "C" {
+
+int rk_debug_gemm_bf16(rk_engine* e, const float* A, const float* B, float* C, int rows_max, int live_rows, int N,
+                       int K, int epi) {
+  return guard([&] {
+    cudaStream_t st = e->stream;
+    DevBuf a = to_bf16(st, A, (size_t)rows_max * K), b = to_bf16(st, B, (size_t)N * K);
+    DevBuf c((size_t)rows_max * N * 4), live(4), flags(1 << 18);
+    RK_CUDA(cudaMemcpy(c.p, C, (size_t)rows_max * N * 4, cudaMemcpyHostToDevice));
+    RK_CUDA(cudaMemcpy(live.p, &live_rows, 4, cudaMemcpyHostToDevice));
+    RK_CUDA(cudaMemset(flags.p, 0, 1 << 18));
+    GemmArgs g;
+    g.rows_max = rows_max;
+    g.rows_dev = live_rows == rows_max ? nullptr : live.as<int>();
+    g.N = N;
+    g.K = K;
+    g.epi = epi;
+    g.out_f32 = c.as<float>();
+    g.ld_out = N;
+    g.split_flags = flags.as<int>();
+    gemm_bf16(e, a.as<__nv_bfloat16>(), K, b.as<__nv_bfloat16>(), g, live_rows);
+    RK_CUDA(cudaStreamSynchronize(st));
+    RK_CUDA(cudaGetLastError());
+    RK_CUDA(cudaMemcpy(C, c.p, (size_t)rows_max * N * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+int rk_debug_attention_bf16(rk_engine* e, const float* q, const float* kk, const float* v, const int32_t* pos,
+                            int M, int T, int H, int Hkv, int dh, float* out) {
+  return guard([&] {
+    cudaStream_t st = e->stream;
+    DevBuf qb = to_bf16(st, q, (size_t)M * H * dh), kb = to_bf16(st, kk, (size_t)T * Hkv * dh),
+           vb = to_bf16(st, v, (size_t)T * Hkv * dh);
+    DevBuf p(M * 4), o((size_t)M * H * dh * 2), of((size_t)M * H * dh * 4);
+    RK_CUDA(cudaMemcpy(p.p, pos, M * 4, cudaMemcpyHostToDevice));
+    AttnArgs a;
+    a.q = qb.as<__nv_bfloat16>();
+    a.out = o.as<__nv_bfloat16>();
+    a.pos = p.as<int>();
+    a.rows_max = M;
+    a.H = H;
+    a.Hkv = Hkv;
+    a.dh = dh;
+    a.scale_log2 = 1.4426950408889634f / std::sqrt((float)dh);
+    attention_bf16(e, a, kb.as<__nv_bfloat16>(), vb.as<__nv_bfloat16>(), T);
+    k::bf16_to_f32(st, of.as<float>(), o.as<__nv_bfloat16>(), (size_t)M * H * dh);
+    RK_CUDA(cudaStreamSynchronize(st));
+    RK_CUDA(cudaGetLastError());
+    RK_CUDA(cudaMemcpy(out, of.p, (size_t)M * H * dh * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+int rk_debug_expf(rk_engine* e, const float* x, float* y, uint64_t n) {
+  return guard([&] {
+    DevBuf dx(n * 4), dy(n * 4);
+    RK_CUDA(cudaMemcpy(dx.p, x, n * 4, cudaMemcpyHostToDevice));
+    expf_kernel<<<1024, 256, 0, e->stream>>>(dx.as<float>(), dy.as<float>(), n);
+    RK_CUDA(cudaStreamSynchronize(e->stream));
+    RK_CUDA(cudaMemcpy(y, dy.p, n * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+}  // extern "C"

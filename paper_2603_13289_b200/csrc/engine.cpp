@@ -37,9 +37,12 @@ int guard(F&& f) {
 
 struct DeviceGuard {
   int prev = -1;
-  explicit DeviceGuard(int dev) {
+  explicit DeviceGuard(int dev, bool nothrow = false) {
     cudaGetDevice(&prev);
-    if (prev != dev) RK_CUDA(cudaSetDevice(dev));
+    if (prev != dev) {
+      const cudaError_t err = cudaSetDevice(dev);
+      if (!nothrow) RK_CUDA(err);
+    }
   }
   ~DeviceGuard() {
     int cur;
@@ -56,6 +59,8 @@ size_t num_tensors(const rk_model_spec& s) { return 1 + 9 * s.num_layers + 2; }
 }  // namespace
 
 namespace rk {
+
+void set_last_error(const std::string& msg) { g_err = msg; }
 
 void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
   if (e != cudaSuccess) {
@@ -105,6 +110,10 @@ RopeTable* rope_table(rk_engine* e, float theta, uint64_t d_head, uint64_t posit
   }
   t->cs.alloc(h.size() * sizeof(double2));
   RK_CUDA(cudaMemcpy(t->cs.p, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  std::vector<float2> hf(h.size());
+  for (size_t i = 0; i < h.size(); ++i) hf[i] = make_float2((float)h[i].x, (float)h[i].y);
+  t->csf.alloc(hf.size() * sizeof(float2));
+  RK_CUDA(cudaMemcpy(t->csf.p, hf.data(), hf.size() * sizeof(float2), cudaMemcpyHostToDevice));
   e->rope.push_back(std::move(t));
   return e->rope.back().get();
 }
@@ -126,6 +135,9 @@ void rk_context::reserve(uint64_t positions) {
   if (ncap > w->s.max_positions) ncap = std::max<uint64_t>(w->s.max_positions, positions);
   const size_t L = w->s.num_layers, row = w->kv() * elem;
   DevBuf nk(L * ncap * row), nv(L * ncap * row);
+  // zero-fill: masked keys beyond the live size must be finite (0 * NaN = NaN in P.V)
+  RK_CUDA(cudaMemsetAsync(nk.p, 0, nk.bytes, e->stream));
+  RK_CUDA(cudaMemsetAsync(nv.p, 0, nv.bytes, e->stream));
   if (size > 0) {
     RK_CUDA(cudaMemcpy2DAsync(nk.p, ncap * row, k.p, cap * row, size * row, L, cudaMemcpyDeviceToDevice, e->stream));
     RK_CUDA(cudaMemcpy2DAsync(nv.p, ncap * row, v.p, cap * row, size * row, L, cudaMemcpyDeviceToDevice, e->stream));
@@ -262,8 +274,9 @@ rk_weights* new_weights(rk_engine* e, const rk_model_spec* spec, int precision) 
   w->precision = precision;
   w->elem = precision == RK_BF16 ? 2 : 4;
   if (precision == RK_BF16) {
-    require(spec->d_model % 64 == 0 && (spec->num_heads * spec->d_head) % 64 == 0 && spec->d_ff % 64 == 0,
-            RK_ERR_INVALID_ARGUMENT, "bf16 mode requires d_model, q_dim and d_ff to be multiples of 64");
+    require(spec->d_model % 64 == 0 && (spec->num_heads * spec->d_head) % 64 == 0 && spec->d_ff % 64 == 0 &&
+                spec->vocab_size % 64 == 0,
+            RK_ERR_INVALID_ARGUMENT, "bf16 mode requires d_model, q_dim, d_ff and vocab to be multiples of 64");
     require(spec->d_head == 64 || spec->d_head == 128, RK_ERR_INVALID_ARGUMENT,
             "bf16 mode supports d_head 64 or 128");
   }
@@ -306,7 +319,7 @@ int rk_engine_create(int device, rk_engine** out) {
 
 void rk_engine_destroy(rk_engine* e) {
   if (!e) return;
-  DeviceGuard g(e->device);
+  DeviceGuard g(e->device, true);
   cudaStreamSynchronize(e->stream);
   delete e;
 }
@@ -420,7 +433,7 @@ int rk_weights_export(rk_weights* w, uint64_t idx, float* out, uint64_t count) {
 
 void rk_weights_destroy(rk_weights* w) {
   if (!w) return;
-  DeviceGuard g(w->e->device);
+  DeviceGuard g(w->e->device, true);
   cudaStreamSynchronize(w->e->stream);
   delete w;
 }
@@ -524,7 +537,7 @@ int rk_cache_export(rk_cache* c, int32_t* tokens, float* const* k_pre, float* co
 
 void rk_cache_destroy(rk_cache* c) {
   if (!c) return;
-  DeviceGuard g(c->e->device);
+  DeviceGuard g(c->e->device, true);
   cudaStreamSynchronize(c->e->stream);
   delete c;
 }
@@ -611,7 +624,7 @@ int rk_context_export(rk_context* c, uint64_t layer, uint64_t pos, uint64_t coun
 
 void rk_context_destroy(rk_context* c) {
   if (!c) return;
-  DeviceGuard g(c->e->device);
+  DeviceGuard g(c->e->device, true);
   cudaStreamSynchronize(c->e->stream);
   delete c;
 }

@@ -1,0 +1,363 @@
+// gemm_sm100.cu -- K3: the recompute GEMMs on 5th-gen tensor cores.
+//
+// D[M x N] = A[M x K] . B[N x K]^T, bf16 operands (both K-major), fp32
+// accumulation in TMEM. One persistent CTA per SM, warp-specialized:
+//   warp 0      TMA producer (one elected lane): A/B k-blocks into a
+//               STAGES-deep shared-memory ring (SWIZZLE_128B), mbarrier-tracked
+//   warp 1      TMEM allocator + MMA issuer (one elected lane):
+//               tcgen05.mma.cta_group::1.kind::f16, M=128, N=BN, K=16
+//   warps 2..5  epilogue: tcgen05.ld 32x32b rows -> fused epilogue -> global
+// TMEM holds two BN-column accumulators so the epilogue of tile i overlaps
+// the MMAs of tile i+1. Rows of A beyond the live row count (read from device
+// memory for sparse passes) are computed but never stored.
+//
+// Fused epilogues (the reference computes these as separate loops over the
+// matmul outputs, model.cpp:246-280 / 211-233):
+//   EPI_QKV   RoPE on Q and K (adjacent pairs, tensor.cpp:134-142), Q -> bf16
+//             buffer, K/V rows scattered into the context at each row's
+//             absolute position (model.cpp:266-269), optional capture of
+//             pre-RoPE K and V (decode-time capture, model.cpp:254-257)
+//   EPI_ADD   hidden += D (residual); split-K partials are added in split
+//             order (deterministic) via per-tile flags
+//   EPI_SILU  interleaved (gate, up) columns -> bf16 silu(g)*u (model.cpp:226)
+//   EPI_F32   plain fp32 store (logits)
+#include <cuda.h>
+
+#include "internal.h"
+#include "layer_bf16.h"
+#include "sm100.cuh"
+
+namespace rk {
+namespace {
+
+using namespace sm100;
+
+constexpr int kBM = 128;
+constexpr int kBK = 64;  // 64 bf16 = one 128-byte swizzle row
+constexpr int kThreads = 192;
+
+template <int BN>
+struct Cfg {
+  static constexpr int A_BYTES = kBM * kBK * 2;
+  static constexpr int B_BYTES = BN * kBK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (BN == 256) ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+struct Units {
+  int num_m, num_n, splits, kb_total, kb_per;
+  int total;
+};
+
+__device__ __forceinline__ Units units_of(const GemmArgs& p) {
+  Units u;
+  const int M = p.rows_dev ? *p.rows_dev : p.rows_max;
+  u.num_m = (M + kBM - 1) / kBM;
+  u.num_n = p.N / p.bn;
+  u.splits = p.splits;
+  u.kb_total = p.K / kBK;
+  u.kb_per = (u.kb_total + u.splits - 1) / u.splits;
+  u.total = u.num_m * u.num_n * u.splits;
+  return u;
+}
+
+// unit -> (m tile, n tile, split); split fastest so the splits of one tile run
+// concurrently on different CTAs, then m so CTAs share B tiles in L2.
+__device__ __forceinline__ void decode_unit(const Units& u, int unit, int& mt, int& nt, int& s) {
+  s = unit % u.splits;
+  const int tile = unit / u.splits;
+  mt = tile % u.num_m;
+  nt = tile / u.num_m;
+}
+
+template <int EPI>
+__device__ __forceinline__ void epilogue_chunk(const GemmArgs& p, int row, int col, const uint32_t (&r)[32]) {
+  float v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+  if constexpr (EPI == EPI_F32) {
+    float4* dst = reinterpret_cast<float4*>(p.out_f32 + (size_t)row * p.ld_out + col);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+  } else if constexpr (EPI == EPI_ADD) {
+    float4* dst = reinterpret_cast<float4*>(p.out_f32 + (size_t)row * p.ld_out + col);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float4 h = dst[j];
+      h.x += v[4 * j]; h.y += v[4 * j + 1]; h.z += v[4 * j + 2]; h.w += v[4 * j + 3];
+      dst[j] = h;
+    }
+  } else if constexpr (EPI == EPI_SILU) {
+    uint32_t packed[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float g0 = v[4 * j], u0 = v[4 * j + 1], g1 = v[4 * j + 2], u1 = v[4 * j + 3];
+      const float a0 = g0 / (1.0f + __expf(-g0)) * u0;
+      const float a1 = g1 / (1.0f + __expf(-g1)) * u1;
+      packed[j] = pack_bf16(a0, a1);
+    }
+    uint4* dst = reinterpret_cast<uint4*>(p.out_bf16 + (size_t)row * p.ld_bf16 + col / 2);
+    dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+    dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+  } else {  // EPI_QKV
+    const int q = p.q, kv = p.kv, dh = p.dh;
+    const int pos = p.pos[row];
+    const int region = col < q ? 0 : (col < q + kv ? 1 : 2);
+    if (region == 2) {
+      const int c = col - q - kv;
+      uint32_t pk[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) pk[j] = pack_bf16(v[2 * j], v[2 * j + 1]);
+      if (p.cap_v) {
+        uint4* d = reinterpret_cast<uint4*>(p.cap_v + (size_t)row * kv + c);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) d[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+      }
+      __nv_bfloat16* base = p.commit ? p.ctx_v + (size_t)pos * kv : p.self_v + (size_t)row * kv;
+      uint4* d = reinterpret_cast<uint4*>(base + c);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) d[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+      return;
+    }
+    const int c = region == 0 ? col : col - q;
+    if (region == 1 && p.cap_k) {
+      uint32_t pk[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) pk[j] = pack_bf16(v[2 * j], v[2 * j + 1]);
+      uint4* d = reinterpret_cast<uint4*>(p.cap_k + (size_t)row * kv + c);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) d[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+    }
+    const int half = dh / 2;
+    const float2* cs = p.rope + (size_t)pos * half + (c % dh) / 2;
+    uint32_t pk[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float2 t = cs[j];
+      const float x0 = v[2 * j], x1 = v[2 * j + 1];
+      pk[j] = pack_bf16(x0 * t.x - x1 * t.y, x0 * t.y + x1 * t.x);
+    }
+    __nv_bfloat16* base;
+    if (region == 0) base = p.out_bf16 + (size_t)row * p.ld_bf16;
+    else base = p.commit ? p.ctx_k + (size_t)pos * kv : p.self_k + (size_t)row * kv;
+    uint4* d = reinterpret_cast<uint4*>(base + c);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) d[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+  }
+}
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const GemmArgs p) {
+  using C = Cfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const Units U = units_of(p);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int i = 0; i < C::STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {  // ---------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int unit = blockIdx.x; unit < U.total; unit += gridDim.x) {
+        int mt, nt, s;
+        decode_unit(U, unit, mt, nt, s);
+        const int kb0 = s * U.kb_per, kb1 = min(U.kb_total, kb0 + U.kb_per);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * C::STAGE_BYTES;
+          mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+          tma_load_2d(sa, &tmA, &full[stage], kb * kBK, mt * kBM);
+          tma_load_2d(sa + C::A_BYTES, &tmB, &full[stage], kb * kBK, nt * BN);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (elect_one()) {  // ---------------- MMA issuer
+      constexpr uint32_t idesc = idesc_bf16(kBM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int unit = blockIdx.x; unit < U.total; unit += gridDim.x, ++local) {
+        int mt, nt, s;
+        decode_unit(U, unit, mt, nt, s);
+        const int kb0 = s * U.kb_per, kb1 = min(U.kb_total, kb0 + U.kb_per);
+        const int acc = local & 1;
+        mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(smem + stage * C::STAGE_BYTES);
+          const uint32_t b0 = a0 + C::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) {
+            mma_bf16_ss(d, sdesc_sw128(a0 + k * 32, 16, 1024), sdesc_sw128(b0 + k * 32, 16, 1024), idesc,
+                        (kb > kb0 || k > 0) ? 1u : 0u);
+          }
+          tc_commit(&empty[stage]);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(&tfull[acc]);
+      }
+    }
+  } else {  // ------------------------------- epilogue warps 2..5
+    const int quarter = warp & 3;
+    const int M = p.rows_dev ? *p.rows_dev : p.rows_max;
+    int local = 0;
+    for (int unit = blockIdx.x; unit < U.total; unit += gridDim.x, ++local) {
+      int mt, nt, s;
+      decode_unit(U, unit, mt, nt, s);
+      const int acc = local & 1;
+      mbar_wait(&tfull[acc], (local >> 1) & 1);
+      tc_fence_after();
+      const int row = mt * kBM + quarter * 32 + lane;
+      int* flag = nullptr;
+      if (EPI == EPI_ADD && U.splits > 1) {  // ordered split-K: wait for split s-1 on these rows
+        flag = p.split_flags + ((size_t)(nt * U.num_m + mt) * 4 + quarter);
+        if (lane == 0)
+          while (atomicAdd(flag, 0) != s) __nanosleep(64);
+        __syncwarp();
+        __threadfence();
+      }
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN + c, r);
+        tmem_ld_wait();
+        if (row < M) epilogue_chunk<EPI>(p, row, nt * BN + c, r);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (flag) {
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicExch(flag, s + 1 == U.splits ? 0 : s + 1);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, C::TMEM_COLS);
+}
+
+template <int BN, int EPI>
+void launch(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& p, int grid) {
+  static bool attr = false;
+  if (!attr) {
+    RK_CUDA(cudaFuncSetAttribute(gemm_bf16_kernel<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
+    attr = true;
+  }
+  gemm_bf16_kernel<BN, EPI><<<grid, kThreads, Cfg<BN>::SMEM, st>>>(a, b, p);
+}
+
+template <int EPI>
+void launch_bn(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& p, int grid) {
+  if (p.bn == 256) launch<256, EPI>(st, a, b, p, grid);
+  else if (p.bn == 128) launch<128, EPI>(st, a, b, p, grid);
+  else launch<64, EPI>(st, a, b, p, grid);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled encode_fn() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    RK_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !f) raise(RK_ERR_RUNTIME, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_encodeTiled>(f);
+  }
+  return fn;
+}
+
+// 2-D bf16 row-major [rows x cols] tensor map, box {64, box_rows}, 128B swizzle.
+void make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows,
+                    uint64_t row_stride_elems) {
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {row_stride_elems * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box,
+                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) raise(RK_ERR_RUNTIME, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+}
+
+// Pick the N tile and split count so the grid fills the SMs.
+static void choose_config(GemmArgs& p, int sm_count, int rows_hint) {
+  const int num_m = (rows_hint + kBM - 1) / kBM;
+  int bn = 64;
+  for (int cand : {256, 128}) {
+    if (p.N % cand == 0 && num_m * (p.N / cand) >= sm_count) { bn = cand; break; }
+  }
+  if (p.N % bn) raise(RK_ERR_INVALID_ARGUMENT, "bf16 GEMM needs N % 64 == 0");
+  p.bn = bn;
+  p.splits = 1;
+  if (p.epi == EPI_ADD && p.split_flags) {
+    const int tiles = num_m * (p.N / bn);
+    const int kb = p.K / kBK;
+    while (tiles * p.splits * 2 <= sm_count && kb / (p.splits * 2) >= 4) p.splits *= 2;
+  }
+}
+
+void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat16* B, GemmArgs p,
+               int rows_hint) {
+  if (p.rows_max <= 0) return;
+  if (p.K % kBK) raise(RK_ERR_INVALID_ARGUMENT, "bf16 GEMM needs K % 64 == 0");
+  choose_config(p, e->sm_count, rows_hint > 0 ? rows_hint : p.rows_max);
+  CUtensorMap ta, tb;
+  make_tmap_bf16(&ta, A, (uint64_t)p.rows_max, (uint64_t)p.K, kBM, (uint64_t)lda);
+  make_tmap_bf16(&tb, B, (uint64_t)p.N, (uint64_t)p.K, (uint32_t)p.bn, (uint64_t)p.K);
+  const int num_m = (p.rows_max + kBM - 1) / kBM;
+  const int total = num_m * (p.N / p.bn) * p.splits;
+  const int grid = total < e->sm_count ? total : e->sm_count;
+  switch (p.epi) {
+    case EPI_QKV: launch_bn<EPI_QKV>(e->stream, ta, tb, p, grid); break;
+    case EPI_ADD: launch_bn<EPI_ADD>(e->stream, ta, tb, p, grid); break;
+    case EPI_SILU: launch_bn<EPI_SILU>(e->stream, ta, tb, p, grid); break;
+    default: launch_bn<EPI_F32>(e->stream, ta, tb, p, grid); break;
+  }
+  e->launches += 1;
+}
+
+}  // namespace rk

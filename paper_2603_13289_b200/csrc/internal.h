@@ -24,6 +24,7 @@ struct Error : std::runtime_error {
 [[noreturn]] inline void raise(int code, const std::string& msg) { throw Error(code, msg); }
 
 void cuda_check(cudaError_t e, const char* what, const char* file, int line);
+void set_last_error(const std::string& msg);
 #define RK_CUDA(x) ::rk::cuda_check((x), #x, __FILE__, __LINE__)
 
 // Owning device allocation.
@@ -52,7 +53,8 @@ struct DevBuf {
 struct RopeTable {
   float theta = 0;
   uint64_t d_head = 0, positions = 0;
-  DevBuf cs;  // double2 [positions][d_head/2]
+  DevBuf cs;   // double2 [positions][d_head/2]
+  DevBuf csf;  // float2, same angles (bf16 path)
 };
 
 struct Scratch;

@@ -1,0 +1,60 @@
+// layer_bf16.h -- argument blocks of the bf16 tensor-core kernels.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "internal.h"
+
+namespace rk {
+
+enum GemmEpi { EPI_QKV = 0, EPI_ADD = 1, EPI_SILU = 2, EPI_F32 = 3 };
+
+struct GemmArgs {
+  int rows_max = 0;             // launch bound on M (tensor-map rows)
+  const int* rows_dev = nullptr;  // live M on the device (sparse passes)
+  int N = 0, K = 0;
+  int epi = EPI_F32;
+  int bn = 128, splits = 1;     // chosen by gemm_bf16
+  int* split_flags = nullptr;   // ordered split-K flags (EPI_ADD), zero-initialised
+  // outputs
+  float* out_f32 = nullptr;     // EPI_ADD / EPI_F32, row stride ld_out
+  int ld_out = 0;
+  __nv_bfloat16* out_bf16 = nullptr;  // EPI_SILU (act) / EPI_QKV (Q), row stride ld_bf16
+  int ld_bf16 = 0;
+  // EPI_QKV
+  const int* pos = nullptr;
+  const float2* rope = nullptr;  // [positions][dh/2] {cos, sin}
+  int dh = 0, q = 0, kv = 0;
+  __nv_bfloat16* ctx_k = nullptr;
+  __nv_bfloat16* ctx_v = nullptr;
+  int commit = 1;
+  __nv_bfloat16* self_k = nullptr;
+  __nv_bfloat16* self_v = nullptr;
+  __nv_bfloat16* cap_k = nullptr;  // pre-RoPE K capture rows [M x kv]
+  __nv_bfloat16* cap_v = nullptr;
+};
+
+// A: [rows_max x K] bf16 row-major with row stride lda; B: [N x K] bf16.
+// rows_hint: expected live rows (tile-shape choice) when rows_dev is set.
+void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat16* B, GemmArgs p,
+               int rows_hint = 0);
+void make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows,
+                    uint64_t row_stride_elems);
+
+struct AttnArgs {
+  const __nv_bfloat16* q = nullptr;  // [rows_max x H*dh]
+  __nv_bfloat16* out = nullptr;      // [rows_max x H*dh]
+  const int* pos = nullptr;          // ascending absolute positions
+  int rows_max = 0;
+  const int* rows_dev = nullptr;
+  int H = 0, Hkv = 0, dh = 0;
+  float scale_log2 = 0.f;            // log2(e) / sqrt(dh)
+  // probability capture for influence (key window [key_lo, key_lo+key_n))
+  float* probs = nullptr;
+  int key_lo = 0, key_n = 0;
+};
+// ctx_k / ctx_v: the layer's [ctx_rows x kv] bf16 context rows.
+void attention_bf16(rk_engine* e, const AttnArgs& a, const __nv_bfloat16* ctx_k, const __nv_bfloat16* ctx_v,
+                    int ctx_rows);
+
+}  // namespace rk

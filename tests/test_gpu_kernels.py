@@ -1,0 +1,128 @@
+"""Kernel-level checks of the bf16 tensor-core kernels (tcgen05 GEMM, flash
+attention) against fp64 numpy on bf16-rounded operands, and of the device
+glibc-expf restatement against the host libm."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from paper_2603_13289_b200.engine import P, _check, lib
+
+pytestmark = pytest.mark.gpu
+F32P = C.POINTER(C.c_float)
+
+
+def bf16_round(x):
+    x = np.ascontiguousarray(x, np.float32)
+    u = x.view(np.uint32).astype(np.uint64)
+    u = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
+    return u.astype(np.uint32).view(np.float32)
+
+
+def run_gemm(engine, A, B, C0, live, epi):
+    M, K = A.shape
+    N = B.shape[0]
+    out = np.ascontiguousarray(C0, np.float32).copy()
+    _check(lib().rk_debug_gemm_bf16(P(engine.ptr), np.ascontiguousarray(A, np.float32).ctypes.data_as(F32P),
+                                    np.ascontiguousarray(B, np.float32).ctypes.data_as(F32P),
+                                    out.ctypes.data_as(F32P), M, live, N, K, epi))
+    return out
+
+
+SHAPES = [(1, 64, 64), (7, 192, 128), (128, 256, 256), (200, 384, 512), (333, 1024, 2048),
+          (1000, 128, 1024), (64, 3072, 2048), (256, 2048, 8192), (513, 16384, 256)]
+
+
+@pytest.mark.parametrize("shape", SHAPES, ids=[f"{m}x{n}x{k}" for m, n, k in SHAPES])
+def test_gemm_store(engine, shape):
+    M, N, K = shape
+    rng = np.random.default_rng(M * 7 + N + K)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    B = (rng.standard_normal((N, K)) / np.sqrt(K)).astype(np.float32)
+    got = run_gemm(engine, A, B, np.zeros((M, N)), M, 3)
+    ref = bf16_round(A).astype(np.float64) @ bf16_round(B).astype(np.float64).T
+    err = np.abs(got - ref).max() / max(np.abs(ref).max(), 1e-30)
+    assert err < 2e-5, f"rel err {err}"
+
+
+@pytest.mark.parametrize("shape", [(128, 256, 8192), (256, 2048, 8192), (40, 512, 4096)])
+def test_gemm_residual_split_k_deterministic(engine, shape):
+    M, N, K = shape
+    rng = np.random.default_rng(3)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    B = (rng.standard_normal((N, K)) / np.sqrt(K)).astype(np.float32)
+    H = rng.standard_normal((M, N)).astype(np.float32)
+    got = run_gemm(engine, A, B, H, M, 1)
+    again = run_gemm(engine, A, B, H, M, 1)
+    assert np.array_equal(got.view(np.uint32), again.view(np.uint32)), "split-K residual not deterministic"
+    ref = H + bf16_round(A).astype(np.float64) @ bf16_round(B).astype(np.float64).T
+    assert np.abs(got - ref).max() / np.abs(ref).max() < 2e-5
+
+
+def test_gemm_live_rows(engine):
+    M, N, K, live = 300, 256, 512, 77
+    rng = np.random.default_rng(5)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    B = rng.standard_normal((N, K)).astype(np.float32) / 20
+    C0 = np.full((M, N), 7.0, np.float32)
+    got = run_gemm(engine, A, B, C0, live, 3)
+    ref = bf16_round(A[:live]).astype(np.float64) @ bf16_round(B).astype(np.float64).T
+    assert np.abs(got[:live] - ref).max() / np.abs(ref).max() < 2e-5
+    assert (got[live:] == 7.0).all(), "rows beyond the live count were written"
+
+
+def ref_attention(q, k, v, pos, H, Hkv, dh):
+    M, T = q.shape[0], k.shape[0]
+    out = np.zeros((M, H * dh))
+    g = H // Hkv
+    qd, kd, vd = (bf16_round(x).astype(np.float64) for x in (q, k, v))
+    for h in range(H):
+        kh = h // g
+        s = qd[:, h * dh:(h + 1) * dh] @ kd[:, kh * dh:(kh + 1) * dh].T / np.sqrt(dh)
+        mask = np.arange(T)[None, :] > pos[:, None]
+        s[mask] = -np.inf
+        s -= s.max(1, keepdims=True)
+        p = np.exp(s)
+        p /= p.sum(1, keepdims=True)
+        out[:, h * dh:(h + 1) * dh] = p @ vd[:, kh * dh:(kh + 1) * dh]
+    return out
+
+
+ATT = [(64, 200, 4, 2, 64, "band"), (300, 700, 8, 2, 64, "sparse"), (130, 1000, 4, 4, 128, "band"),
+       (1, 333, 4, 1, 128, "band"), (257, 1500, 32, 8, 64, "sparse")]
+
+
+@pytest.mark.parametrize("case", ATT, ids=[f"{c[5]}-M{c[0]}-T{c[1]}-dh{c[4]}" for c in ATT])
+def test_attention(engine, case):
+    M, T, H, Hkv, dh, kind = case
+    rng = np.random.default_rng(M + T)
+    if kind == "band":
+        pos = np.arange(T - M, T, dtype=np.int32)
+    else:
+        pos = np.sort(rng.choice(T, M, replace=False)).astype(np.int32)
+    q = rng.standard_normal((M, H * dh)).astype(np.float32)
+    k = rng.standard_normal((T, Hkv * dh)).astype(np.float32)
+    v = rng.standard_normal((T, Hkv * dh)).astype(np.float32)
+    out = np.zeros((M, H * dh), np.float32)
+    _check(lib().rk_debug_attention_bf16(P(engine.ptr), q.ctypes.data_as(F32P), k.ctypes.data_as(F32P),
+                                         v.ctypes.data_as(F32P), pos.ctypes.data_as(C.POINTER(C.c_int32)),
+                                         M, T, H, Hkv, dh, out.ctypes.data_as(F32P)))
+    ref = ref_attention(q, k, v, pos, H, Hkv, dh)
+    err = np.abs(out - ref).max()
+    assert err < 3e-2, f"max abs err {err}"
+
+
+def test_device_expf_matches_host_libm(engine):
+    """The device restatement of glibc expf vs this host's libm, every 256th float."""
+    from oracle.oracle import Oracle
+    orc = Oracle("restatement")
+    fn = orc.lib.orc_host_expf_array
+    fn.argtypes = [F32P, F32P, C.c_uint64]
+    x = (np.arange(0, 2 ** 32, 256, dtype=np.uint64).astype(np.uint32)).view(np.float32)
+    x = np.ascontiguousarray(x[~np.isnan(x)])
+    want = np.empty_like(x)
+    fn(x.ctypes.data_as(F32P), want.ctypes.data_as(F32P), x.size)
+    got = np.empty_like(x)
+    _check(lib().rk_debug_expf(P(engine.ptr), x.ctypes.data_as(F32P), got.ctypes.data_as(F32P), C.c_uint64(x.size)))
+    bad = np.flatnonzero(got.view(np.uint32) != want.view(np.uint32))
+    assert bad.size == 0, f"{bad.size} mismatches, first x={x[bad[0]]!r}"
