@@ -178,6 +178,19 @@ uint64_t rk_engine_launch_count(rk_engine* e);
 /* CUDA-graph replay of repeated identical rk_agent_prefill calls (0/1). */
 int rk_engine_set_graphs(rk_engine* e, int enable);
 
+/* Per-kernel instrumentation: when enabled, each hot-kernel launch is
+ * bracketed by CUDA events on the engine stream and tagged with its
+ * algorithmic FLOPs / bytes (for roofline reporting). Enabling clears. */
+typedef struct rk_kernel_stat {
+  char name[32];
+  uint64_t launches;
+  double total_ms;
+  double flops;
+  double bytes;
+} rk_kernel_stat;
+int rk_engine_profile(rk_engine* e, int enable);
+int rk_engine_profile_read(rk_engine* e, rk_kernel_stat* out, uint64_t cap, uint64_t* count);
+
 /* ---- weights (model.hpp:42-58) ----------------------------------------- */
 /* == init_weights(spec, seed) (model.cpp:81-114) computed on the device,
  * without spec.validate() (model.cpp:82) so 2-layer specs are accepted. */
@@ -217,6 +230,8 @@ void rk_cache_destroy(rk_cache* c);
 /* ---- merged KV context (model.hpp:68-87, relay_engine.hpp:37-40) ------- */
 int rk_context_create(rk_engine* e, rk_weights* w, rk_context** out);
 int rk_context_clone(rk_context* src, rk_context** out);
+/* Empty the context (size 0, no segments), keeping its device allocation. */
+int rk_context_reset(rk_context* c);
 uint64_t rk_context_size(const rk_context* c);
 uint64_t rk_context_num_segments(const rk_context* c);
 int rk_context_segment(rk_context* c, uint64_t index, uint64_t* base, uint64_t* len,

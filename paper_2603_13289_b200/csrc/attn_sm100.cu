@@ -18,6 +18,7 @@
 
 #include "internal.h"
 #include "layer_bf16.h"
+#include "prof.h"
 #include "sm100.cuh"
 
 namespace rk {
@@ -334,6 +335,13 @@ void attention_bf16(rk_engine* e, const AttnArgs& a, const __nv_bfloat16* ctx_k,
   make_tmap_bf16(&tq, a.q, (uint64_t)a.rows_max, (uint64_t)q, kQ, (uint64_t)q);
   make_tmap_bf16(&tk, ctx_k, (uint64_t)ctx_rows, (uint64_t)kv, kKeys, (uint64_t)kv);
   make_tmap_bf16(&tv, ctx_v, (uint64_t)ctx_rows, (uint64_t)kv, kKeys, (uint64_t)kv);
+  ProfScope ps(e, "attention_bf16_tcgen05", 0, 0);
+  ps.rec.kind = 2;
+  ps.rec.rows_dev = a.rows_dev;
+  ps.rec.rows_max = a.rows_max;
+  ps.rec.pos = a.pos;
+  ps.rec.H = a.H;
+  ps.rec.dh = a.dh;
   if (a.dh == 64) launch_attn<64>(e, tq, tk, tv, a);
   else if (a.dh == 128) launch_attn<128>(e, tq, tk, tv, a);
   else raise(RK_ERR_INVALID_ARGUMENT, "bf16 attention supports d_head 64 or 128");

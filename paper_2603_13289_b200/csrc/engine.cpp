@@ -12,6 +12,7 @@
 
 #include "internal.h"
 #include "layer.h"
+#include "prof.h"
 
 using namespace rk;
 
@@ -741,4 +742,92 @@ double rk_flops_segment_schedule(const rk_model_spec* s, uint64_t base, uint64_t
   return band + sparse;
 }
 
+}  // extern "C"
+
+// ============================================================================
+// profiling + context reset
+// ============================================================================
+namespace rk {
+Profiler& profiler(rk_engine* e) {
+  if (!e->prof) e->prof.reset(new Profiler());
+  return *e->prof;
+}
+ProfScope::ProfScope(rk_engine* eng, const char* name, double flops, double bytes) : e(eng) {
+  on = eng->prof && eng->prof->on;
+  rec.name = name;
+  rec.flops = flops;
+  rec.bytes = bytes;
+  if (on) rec.ev0 = eng->prof->ev(eng->stream);
+}
+ProfScope::~ProfScope() {
+  if (!on) return;
+  try {
+    rec.ev1 = e->prof->ev(e->stream);
+    e->prof->recs.push_back(rec);
+  } catch (...) {
+  }
+}
+}  // namespace rk
+
+extern "C" {
+int rk_engine_profile(rk_engine* e, int enable) {
+  return guard([&] {
+    DeviceGuard g(e->device);
+    RK_CUDA(cudaStreamSynchronize(e->stream));
+    Profiler& p = profiler(e);
+    p.on = enable != 0;
+    p.recs.clear();
+    p.next = 0;
+  });
+}
+
+int rk_engine_profile_read(rk_engine* e, rk_kernel_stat* out, uint64_t cap, uint64_t* count) {
+  return guard([&] {
+    DeviceGuard g(e->device);
+    RK_CUDA(cudaStreamSynchronize(e->stream));
+    Profiler& p = profiler(e);
+    std::vector<rk_kernel_stat> agg;
+    for (const ProfRec& r : p.recs) {
+      float ms = 0.f;
+      RK_CUDA(cudaEventElapsedTime(&ms, p.pool[r.ev0], p.pool[r.ev1]));
+      double flops = r.flops, bytes = r.bytes;
+      if (r.kind != 0) {
+        int M = r.rows_max;
+        if (r.rows_dev) RK_CUDA(cudaMemcpy(&M, r.rows_dev, 4, cudaMemcpyDeviceToHost));
+        if (r.kind == 1) {
+          flops = 2.0 * M * r.N * r.K;
+        } else {
+          std::vector<int> pos(M);
+          if (M) RK_CUDA(cudaMemcpy(pos.data(), r.pos, M * 4, cudaMemcpyDeviceToHost));
+          double ctx = 0;
+          for (int v : pos) ctx += v + 1;
+          flops = 4.0 * r.dh * r.H * ctx;
+        }
+      }
+      rk_kernel_stat* st = nullptr;
+      for (auto& a : agg)
+        if (std::strncmp(a.name, r.name, sizeof a.name) == 0) st = &a;
+      if (!st) {
+        agg.push_back(rk_kernel_stat{});
+        st = &agg.back();
+        std::strncpy(st->name, r.name, sizeof st->name - 1);
+      }
+      st->launches += 1;
+      st->total_ms += ms;
+      st->flops += flops;
+      st->bytes += bytes;
+    }
+    if (count) *count = agg.size();
+    for (size_t i = 0; i < agg.size() && i < cap; ++i) out[i] = agg[i];
+  });
+}
+
+int rk_context_reset(rk_context* c) {
+  return guard([&] {
+    DeviceGuard g(c->e->device);
+    RK_CUDA(cudaStreamSynchronize(c->e->stream));
+    c->size = 0;
+    c->segs.clear();
+  });
+}
 }  // extern "C"

@@ -25,6 +25,7 @@
 
 #include "internal.h"
 #include "layer_bf16.h"
+#include "prof.h"
 #include "sm100.cuh"
 
 namespace rk {
@@ -351,6 +352,12 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
   const int num_m = (p.rows_max + kBM - 1) / kBM;
   const int total = num_m * (p.N / p.bn) * p.splits;
   const int grid = total < e->sm_count ? total : e->sm_count;
+  ProfScope ps(e, "gemm_bf16_tcgen05", 0, 0);
+  ps.rec.kind = 1;
+  ps.rec.rows_dev = p.rows_dev;
+  ps.rec.rows_max = rows_hint > 0 && !p.rows_dev ? p.rows_max : p.rows_max;
+  ps.rec.N = p.N;
+  ps.rec.K = p.K;
   switch (p.epi) {
     case EPI_QKV: launch_bn<EPI_QKV>(e->stream, ta, tb, p, grid); break;
     case EPI_ADD: launch_bn<EPI_ADD>(e->stream, ta, tb, p, grid); break;

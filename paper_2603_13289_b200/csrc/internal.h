@@ -59,6 +59,7 @@ struct RopeTable {
 
 struct Scratch;
 struct ExtendSlot;
+struct Profiler;
 
 }  // namespace rk
 
@@ -76,6 +77,7 @@ struct rk_engine {
   rk::DevBuf status;  // int flags: [0] non-finite
   std::vector<cudaEvent_t> events;
   std::vector<std::unique_ptr<rk::ExtendSlot>> slots;
+  std::unique_ptr<rk::Profiler> prof;
   rk_engine();
   ~rk_engine();
 };

@@ -9,6 +9,7 @@
 #include <cstring>
 
 #include "layer.h"
+#include "prof.h"
 
 namespace rk {
 namespace {
@@ -297,6 +298,8 @@ ExtendResult Runner::relay_extend(rk_context* ctx, rk_cache* cache, const rk_lay
     int skip_lo = 1, skip_hi = 0;
     if (mode == RK_MODE_RELAY) { skip_lo = (int)l_start; skip_hi = (int)l_det; }
     if (mode == RK_MODE_BLEND) { skip_lo = 0; skip_hi = 1; }
+    const int grafted = (int)L - (skip_hi >= skip_lo ? skip_hi - skip_lo + 1 : 0);
+    ProfScope ps(e_, "realign_graft", 3.0 * kv * n * grafted, 4.0 * grafted * n * kv * w_->elem);
     k::realign_graft(st_, cache->k_pre.p, cache->v.p, w_->elem, (int)L, (int)n, (int)kv, (int)s.d_head,
                      rope, (int)base, ctx->k.p, ctx->v.p, layer_stride, skip_lo, skip_hi);
     e_->launches += 1;
@@ -344,12 +347,18 @@ ExtendResult Runner::relay_extend(rk_context* ctx, rk_cache* cache, const rk_lay
         // one-shot selection at the detection layer (relay_engine.cpp:266-282)
         const char* ctx_k_det = static_cast<const char*>(ctx->k_layer(l_det)) + base * kv * el;
         const char* cache_k_det = static_cast<const char*>(cache->k_pre.p) + l_det * n * kv * el;
-        k::score_deviation(st_, ctx_v_det, cache_v_det, ctx_k_det, cache_k_det, el, (int)n, (int)kv,
-                           (int)s.num_kv_heads, (int)s.d_head, rope, (int)base, X.s_dev.as<double>(),
-                           X.s_key.as<double>());
-        k::select_relay(st_, X.s_dev.as<double>(), cache->influence.as<float>(), cache->infl_mean.as<double>(),
-                        (int)n, opts.tau_dev, opts.tau_inf, (int)std::min<uint64_t>(opts.suffix_k, 0x7fffffff),
-                        X.sel_idx.as<int>(), X.sel_tags.as<uint32_t>(), X.info.as<int>(), X.dinfo.as<double>());
+        {
+          ProfScope ps(e_, "score_deviation", 0, 4.0 * n * kv * el);
+          k::score_deviation(st_, ctx_v_det, cache_v_det, ctx_k_det, cache_k_det, el, (int)n, (int)kv,
+                             (int)s.num_kv_heads, (int)s.d_head, rope, (int)base, X.s_dev.as<double>(),
+                             X.s_key.as<double>());
+        }
+        {
+          ProfScope ps(e_, "select_relay", 0, n * 20.0);
+          k::select_relay(st_, X.s_dev.as<double>(), cache->influence.as<float>(), cache->infl_mean.as<double>(),
+                          (int)n, opts.tau_dev, opts.tau_inf, (int)std::min<uint64_t>(opts.suffix_k, 0x7fffffff),
+                          X.sel_idx.as<int>(), X.sel_tags.as<uint32_t>(), X.info.as<int>(), X.dinfo.as<double>());
+        }
         e_->launches += 2;
       } else {
         // CacheBlend ranking at layer 1 (relay_engine.cpp:318-332)

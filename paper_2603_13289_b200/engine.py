@@ -82,6 +82,11 @@ class _Obj:
             pass
 
 
+class KernelStat(C.Structure):
+    _fields_ = [("name", C.c_char * 32), ("launches", C.c_uint64), ("total_ms", C.c_double),
+                ("flops", C.c_double), ("bytes", C.c_double)]
+
+
 class Engine(_Obj):
     """One engine per CUDA device (rk_engine_create)."""
     _dtor = "rk_engine_destroy"
@@ -105,6 +110,18 @@ class Engine(_Obj):
 
     def set_graphs(self, enable):
         _check(lib().rk_engine_set_graphs(P(self.ptr), int(enable)))
+
+    def profile(self, enable=True):
+        """Per-kernel CUDA-event instrumentation of the hot kernels (clears)."""
+        _check(lib().rk_engine_profile(P(self.ptr), int(enable)))
+
+    def profile_read(self):
+        stats = (KernelStat * 64)()
+        n = U64()
+        _check(lib().rk_engine_profile_read(P(self.ptr), stats, U64(64), C.byref(n)))
+        return [{"name": stats[i].name.decode(), "launches": int(stats[i].launches),
+                 "total_ms": stats[i].total_ms, "flops": stats[i].flops, "bytes": stats[i].bytes}
+                for i in range(min(n.value, 64))]
 
     # ---- factories ------------------------------------------------------------
     def weights(self, spec, seed, precision="fp32"):
@@ -197,6 +214,10 @@ class Context(_Obj):
         out = P()
         _check(lib().rk_context_clone(P(self.ptr), C.byref(out)))
         return Context(out.value, self.weights)
+
+    def reset(self):
+        """Empty the context, keeping its device allocation."""
+        _check(lib().rk_context_reset(P(self.ptr)))
 
     def export(self, layer, pos=0, count=None):
         kv = self.spec.kv_dim
