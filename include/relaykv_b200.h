@@ -175,6 +175,10 @@ int rk_engine_synchronize(rk_engine* e);
 void* rk_engine_stream(rk_engine* e);
 /* Number of engine kernel launches issued so far (instrumentation). */
 uint64_t rk_engine_launch_count(rk_engine* e);
+/* rk_agent_prefill schedule: 1 (default) = layer-major fused schedule (all
+ * phases of the prompt share one pass per layer; identical results), 0 = the
+ * reference's sequential prefill / relay_extend / prefill order. */
+int rk_engine_set_fused(rk_engine* e, int enable);
 /* CUDA-graph replay of repeated identical rk_agent_prefill calls (0/1). */
 int rk_engine_set_graphs(rk_engine* e, int enable);
 

@@ -76,8 +76,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (m0 >= M) return;
   const int h = blockIdx.y;
   const int kvh = h / (a.H / a.Hkv);
-  const int last_row = min(m0 + kQ, M) - 1;
-  const int kmax = a.pos[last_row];
+  // key range: up to the largest position among the tile's rows (rows need
+  // not be sorted: the fused schedule packs prefix, suffix and segment rows)
+  __shared__ int s_kmax;
+  if (threadIdx.x == 0) s_kmax = 0;
+  __syncthreads();
+  if (threadIdx.x < kQ && m0 + (int)threadIdx.x < M) atomicMax(&s_kmax, a.pos[m0 + threadIdx.x]);
+  __syncthreads();
+  const int kmax = s_kmax;
   const int nk = kmax / kKeys + 1;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
 

@@ -333,6 +333,10 @@ int rk_engine_synchronize(rk_engine* e) {
 }
 void* rk_engine_stream(rk_engine* e) { return e ? (void*)e->stream : nullptr; }
 uint64_t rk_engine_launch_count(rk_engine* e) { return e ? e->launches : 0; }
+int rk_engine_set_fused(rk_engine* e, int enable) {
+  return guard([&] { e->fused = enable; });
+}
+
 int rk_engine_set_graphs(rk_engine* e, int enable) {
   return guard([&] { e->use_graphs = enable; });
 }

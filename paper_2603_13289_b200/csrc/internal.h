@@ -69,6 +69,7 @@ struct rk_engine {
   cudaStream_t stream = nullptr;
   uint64_t launches = 0;
   int use_graphs = 0;
+  int fused = 1;  // layer-major fused agent schedule (runner.cpp agent_fused)
   std::vector<std::unique_ptr<rk::RopeTable>> rope;
   std::unique_ptr<rk::Scratch> scratch;
   // pinned host staging
@@ -208,6 +209,16 @@ void blend_scores(cudaStream_t s, const void* ctx_v, const void* cache_v, size_t
 void select_topk(cudaStream_t s, const double* score, int n, int count, int* sel_idx,
                  uint32_t* sel_tags, int* info);
 void seq_mean(cudaStream_t s, const float* x, int n, double* out);
+
+// fused agent schedule
+struct SegCounts {
+  const int* count[8];
+};
+void segment_offsets(cudaStream_t s, const SegCounts& c, int U, int start, int* offs);
+void gather_rows_to(cudaStream_t s, float* H, const int* off, const float* src, const int* idx, const int* count,
+                    int rows_max, int d, int* pos, int base);
+void scatter_rows_from(cudaStream_t s, float* dst, const float* H, const int* off, const int* idx, const int* count,
+                       int rows_max, int d, uint64_t* depth, uint64_t value);
 
 // fp32 exact path
 void rmsnorm_exact(cudaStream_t s, const float* x, const float* gain, float eps, float* out,

@@ -623,3 +623,58 @@ void seq_mean(cudaStream_t s, const float* x, int n, double* out) {
 
 }  // namespace k
 }  // namespace rk
+
+// ---------------------------------------------------------------------------
+// layer-major fused agent schedule helpers (runner.cpp agent_fused)
+// ---------------------------------------------------------------------------
+namespace rk {
+namespace {
+__global__ void segment_offsets_kernel(k::SegCounts c, int U, int start, int* offs) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int o = start;
+  for (int u = 0; u < U; ++u) {
+    offs[u] = o;
+    o += *c.count[u];
+  }
+  offs[U] = o;
+}
+// H[off + r] = src[idx[r]]; pos[off + r] = base + idx[r]
+__global__ void gather_rows_to_kernel(float* H, const int* off, const float* src, const int* idx, const int* count,
+                                      int d, int* pos, int base) {
+  const int rows = *count, o = *off;
+  const size_t total = (size_t)rows * d;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t r = i / d, c = i % d;
+    H[(size_t)(o + r) * d + c] = src[(size_t)idx[r] * d + c];
+    if (c == 0) pos[o + r] = base + idx[r];
+  }
+}
+// dst[idx[r]] = H[off + r]; depth[idx[r]] = value
+__global__ void scatter_rows_from_kernel(float* dst, const float* H, const int* off, const int* idx, const int* count,
+                                         int d, uint64_t* depth, uint64_t value) {
+  const int rows = *count, o = *off;
+  const size_t total = (size_t)rows * d;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t r = i / d, c = i % d;
+    dst[(size_t)idx[r] * d + c] = H[(size_t)(o + r) * d + c];
+    if (c == 0) depth[idx[r]] = value;
+  }
+}
+}  // namespace
+
+namespace k {
+void segment_offsets(cudaStream_t s, const SegCounts& c, int U, int start, int* offs) {
+  segment_offsets_kernel<<<1, 32, 0, s>>>(c, U, start, offs);
+}
+void gather_rows_to(cudaStream_t s, float* H, const int* off, const float* src, const int* idx, const int* count,
+                    int rows_max, int d, int* pos, int base) {
+  const size_t total = (size_t)rows_max * d;
+  gather_rows_to_kernel<<<blocks_for(total) < 4096 ? blocks_for(total) : 4096, kThreads, 0, s>>>(H, off, src, idx, count, d, pos, base);
+}
+void scatter_rows_from(cudaStream_t s, float* dst, const float* H, const int* off, const int* idx, const int* count,
+                       int rows_max, int d, uint64_t* depth, uint64_t value) {
+  const size_t total = (size_t)rows_max * d;
+  scatter_rows_from_kernel<<<blocks_for(total) < 4096 ? blocks_for(total) : 4096, kThreads, 0, s>>>(dst, H, off, idx, count, d, depth, value);
+}
+}  // namespace k
+}  // namespace rk

@@ -24,6 +24,10 @@ struct ExtendResult {
   rk_reuse_stats stats{};
 };
 
+struct ExtendPlan {
+  uint64_t l_start = 0, l_det = 0, sparse_hi = 0;
+};
+
 // Grow-only device buffers of one extend slot.
 struct ExtendSlot {
   DevBuf hidden, sub_hidden, depth, s_dev, s_key, sel_idx, sel_tags, info, dinfo, sub_pos, score;
@@ -65,6 +69,11 @@ class Runner {
   void last_row_logits(const float* hidden_row);  // output_logits (model.cpp:282-288)
   void row_logits_from_layer(rk_context* ctx, const float* hidden_row, uint64_t first_layer,
                              uint64_t position);
+  ExtendPlan plan_extend(uint64_t base, rk_cache* cache, const rk_layer_profile* prof,
+                         const rk_relay_options& opts);
+  void agent_fused(rk_context* ctx, const int32_t* prefix, uint64_t P, rk_cache* const* ups, uint64_t U,
+                   const int32_t* suffix, uint64_t S, const rk_layer_profile* prof, const rk_relay_options& opts,
+                   std::vector<ExtendResult>& results);
   void ensure_rows(size_t rows);
   int* upload_tokens(const int32_t* tokens, uint64_t n, int slot);
   void check_tokens(const int32_t* tokens, uint64_t n);

@@ -191,31 +191,22 @@ void Runner::prefill(rk_context* ctx, const int32_t* tokens, uint64_t n, uint64_
   if (want_logits) last_row_logits(S.hidden.as<float>() + (n - 1) * s.d_model);
 }
 
-// ---------------------------------------------------------------------------
-// relay_extend (relay_engine.cpp:183-361)
-// ---------------------------------------------------------------------------
-ExtendResult Runner::relay_extend(rk_context* ctx, rk_cache* cache, const rk_layer_profile* prof,
-                                  const rk_relay_options& opts) {
+// Validation of one relay_extend (relay_engine.cpp:186-192, 236-243, 296-298;
+// relay_cache.cpp:43-49, 157-161) and its layer window.
+ExtendPlan Runner::plan_extend(uint64_t base, rk_cache* cache, const rk_layer_profile* prof,
+                               const rk_relay_options& opts) {
   const rk_model_spec& s = w_->s;
-  require(ctx != nullptr && ctx->w == w_, RK_ERR_INVALID_ARGUMENT, "context belongs to other weights");
   require(cache != nullptr, RK_ERR_INVALID_ARGUMENT, "null relay cache");
-  // cache.validate_for(spec) (relay_cache.cpp:43-49)
   require(cache->L == s.num_layers && cache->Hkv == s.num_kv_heads && cache->dh == s.d_head &&
               cache->d == s.d_model && cache->theta == s.theta_base,
           RK_ERR_INVALID_ARGUMENT, "relay cache geometry does not match model spec");
   require(cache->elem == w_->elem, RK_ERR_INVALID_ARGUMENT,
           "relay cache was uploaded for weights of another precision");
-  const uint64_t n = cache->n, base = ctx->size, L = s.num_layers;
+  const uint64_t n = cache->n, L = s.num_layers;
   require(base + n <= s.max_positions, RK_ERR_INVALID_ARGUMENT, "relay_extend: segment overflows max_positions");
   const int mode = opts.mode;
   require(mode >= RK_MODE_FULL && mode <= RK_MODE_BLEND, RK_ERR_INVALID_ARGUMENT, "unknown relay mode");
-
-  ExtendResult r;
-  r.mode = mode;
-  r.base = base;
-  r.n = n;
-  r.L = L;
-  uint64_t l_start = 0, l_det = 0, sparse_hi = 0;
+  ExtendPlan p;
   if (mode == RK_MODE_RELAY) {
     require(prof != nullptr, RK_ERR_INVALID_ARGUMENT, "null layer profile");
     // LayerProfile::validate (profiler.cpp:28-35) -> SchemaError
@@ -228,26 +219,41 @@ ExtendResult Runner::relay_extend(rk_context* ctx, rk_cache* cache, const rk_lay
     require(cache->snapshot == prof->l_start, RK_ERR_INVALID_ARGUMENT,
             "relay_extend: cache snapshot layer " + std::to_string(cache->snapshot) +
                 " does not match profile l_start " + std::to_string(prof->l_start));
-    l_start = prof->l_start;
-    l_det = prof->l_det;
-    sparse_hi = opts.rectify_above_end ? L - 1 : prof->l_end;
+    p.l_start = prof->l_start;
+    p.l_det = prof->l_det;
+    p.sparse_hi = opts.rectify_above_end ? L - 1 : prof->l_end;
   }
   if (mode == RK_MODE_BLEND) {
     require(opts.blend_alpha > 0.0 && opts.blend_alpha <= 1.0, RK_ERR_INVALID_ARGUMENT,
             "relay_extend: blend alpha must be in (0, 1]");
     require(L >= 2, RK_ERR_INVALID_ARGUMENT, "blend needs at least 2 layers");
-    l_start = 0;
-    l_det = 1;
-    sparse_hi = L - 1;
+    p.l_start = 0;
+    p.l_det = 1;
+    p.sparse_hi = L - 1;
   }
-  if (mode == RK_MODE_FULL) {
-    check_tokens(cache->host_tokens.data(), n);
-  } else {
-    // realign() capacity check (relay_cache.cpp:157-161) uses the cache's max_positions
+  if (mode != RK_MODE_FULL)
     require(base + n <= cache->maxpos, RK_ERR_INVALID_ARGUMENT,
             "realign: base " + std::to_string(base) + " overflows max_positions " + std::to_string(cache->maxpos));
-  }
-  if (mode == RK_MODE_BLEND) check_tokens(cache->host_tokens.data(), n);
+  if (mode == RK_MODE_FULL || mode == RK_MODE_BLEND) check_tokens(cache->host_tokens.data(), n);
+  return p;
+}
+
+// ---------------------------------------------------------------------------
+// relay_extend (relay_engine.cpp:183-361)
+// ---------------------------------------------------------------------------
+ExtendResult Runner::relay_extend(rk_context* ctx, rk_cache* cache, const rk_layer_profile* prof,
+                                  const rk_relay_options& opts) {
+  const rk_model_spec& s = w_->s;
+  require(ctx != nullptr && ctx->w == w_, RK_ERR_INVALID_ARGUMENT, "context belongs to other weights");
+  const ExtendPlan plan = plan_extend(ctx->size, cache, prof, opts);
+  const uint64_t n = cache->n, base = ctx->size, L = s.num_layers;
+  const int mode = opts.mode;
+  const uint64_t l_start = plan.l_start, l_det = plan.l_det, sparse_hi = plan.sparse_hi;
+  ExtendResult r;
+  r.mode = mode;
+  r.base = base;
+  r.n = n;
+  r.L = L;
   r.l_start = l_start;
   r.l_det = l_det;
   r.sparse_hi = sparse_hi;
@@ -461,6 +467,8 @@ void Runner::agent_prefill(rk_context* ctx, const int32_t* prefix, uint64_t n_pr
     for (uint64_t u = 0; u < n_up; ++u) full.insert(full.end(), ups[u]->host_tokens.begin(), ups[u]->host_tokens.end());
     if (n_suffix) full.insert(full.end(), suffix, suffix + n_suffix);
     prefill(ctx, full.data(), full.size(), 0, true);
+  } else if (e_->fused && n_up <= 8) {
+    agent_fused(ctx, prefix, n_prefix, ups, n_up, suffix, n_suffix, prof, opts, results);
   } else {
     prefill(ctx, prefix, n_prefix, 0, false);
     for (uint64_t u = 0; u < n_up; ++u) results.push_back(relay_extend(ctx, ups[u], prof, opts));
@@ -473,6 +481,232 @@ void Runner::agent_prefill(rk_context* ctx, const int32_t* prefix, uint64_t n_pr
   }
   k::argmax(st_, e_->scratch->logits.as<float>(), (int)w_->s.vocab_size, e_->scratch->argmax.as<int>());
   e_->launches += 1;
+}
+
+// ---------------------------------------------------------------------------
+// Layer-major fused schedule of the downstream agent's prompt
+// (run_workflow relay branch, workflow.cpp:316-369).
+//
+// The reference runs prefill(prefix), relay_extend per segment, prefill(suffix)
+// one after another, each through all its layers. Each of those is a set of
+// rows passing through run_layer_rows, which commits all rows' K/V before any
+// attention and lets row r see exactly the cells at positions <= pos_r. So at
+// every layer the rows of all phases can run as ONE row set: a row's inputs
+// (its own hidden state, and the layer-l cells at earlier positions: fresh
+// prefix K/V, band K/V, rectified K/V of selected rows, grafted K/V of the
+// rest) are the same values the sequential order gives it -- later phases only
+// ever read earlier positions, earlier phases only earlier positions. Results
+// are identical (bit-identical in RK_FP32_EXACT; tests compare against the
+// oracle's sequential order), with 16 layer passes instead of ~50 and weights
+// streamed once per layer.
+//
+// Row layout of the pass buffer: [prefix | suffix | segment rows], where the
+// segment rows are all segment rows during the band [l_start, l_det] and the
+// compacted selected rows during (l_det, sparse_hi] (live count on the device).
+// ---------------------------------------------------------------------------
+void Runner::agent_fused(rk_context* ctx, const int32_t* prefix, uint64_t P, rk_cache* const* ups, uint64_t U,
+                         const int32_t* suffix, uint64_t S, const rk_layer_profile* prof,
+                         const rk_relay_options& opts, std::vector<ExtendResult>& results) {
+  const rk_model_spec& s = w_->s;
+  const int mode = opts.mode;
+  const uint64_t L = s.num_layers, d = s.d_model;
+  require(ctx != nullptr && ctx->w == w_, RK_ERR_INVALID_ARGUMENT, "context belongs to other weights");
+  require(ctx->size == 0, RK_ERR_INVALID_ARGUMENT, "agent prefill: context must be empty");
+  // prefill(prefix) checks (model.cpp:309-316)
+  require(P > 0 && prefix != nullptr, RK_ERR_INVALID_ARGUMENT, "prefill: empty token chunk");
+  require(P <= s.max_positions, RK_ERR_INVALID_ARGUMENT,
+          "prefill: position overflow beyond max_positions " + std::to_string(s.max_positions));
+  check_tokens(prefix, P);
+  std::vector<uint64_t> base(U), n(U);
+  std::vector<ExtendPlan> plan(U);
+  uint64_t off = P;
+  for (uint64_t u = 0; u < U; ++u) {
+    plan[u] = plan_extend(off, ups[u], prof, opts);
+    base[u] = off;
+    n[u] = ups[u]->n;
+    off += n[u];
+  }
+  if (S > 0) {
+    require(suffix != nullptr, RK_ERR_INVALID_ARGUMENT, "null suffix");
+    require(off + S <= s.max_positions, RK_ERR_INVALID_ARGUMENT,
+            "prefill: position overflow beyond max_positions " + std::to_string(s.max_positions));
+    check_tokens(suffix, S);
+  }
+  require(S > 0 || U > 0, RK_ERR_INVALID_ARGUMENT, "agent prefill: no suffix and no upstream segment");
+  const uint64_t sbase = off, total = off + S, head = P + S, segrows = sbase - P;
+  const bool segs = mode != RK_MODE_ZERO && U > 0;
+  const uint64_t l_start = U ? plan[0].l_start : 0, l_det = U ? plan[0].l_det : 0;
+  const uint64_t sparse_hi = U ? plan[0].sparse_hi : 0;
+
+  ensure_rows(head + segrows);
+  Scratch& Sc = *e_->scratch;
+  float* H = Sc.hidden.as<float>();
+  int* pos = Sc.positions.as<int>();
+  Sc.sel_info.ensure(64 * 4);
+  int* offs = Sc.sel_info.as<int>();  // [U+1]: row offset of each segment's selected rows, live count
+  int* dtok_p = upload_tokens(prefix, P, tok_cursor_);
+  tok_cursor_ += (int)P;
+  int* dtok_s = nullptr;
+  if (S) {
+    dtok_s = upload_tokens(suffix, S, tok_cursor_);
+    tok_cursor_ += (int)S;
+  }
+
+  results.clear();
+  std::vector<rk_segment_marks> marks(U);
+  for (uint64_t u = 0; u < U; ++u) {
+    ExtendResult r;
+    r.mode = mode;
+    r.base = base[u];
+    r.n = n[u];
+    r.L = L;
+    r.l_start = plan[u].l_start;
+    r.l_det = plan[u].l_det;
+    r.sparse_hi = plan[u].sparse_hi;
+    r.slot = next_slot_++;
+    ExtendSlot& X = slot(r.slot);
+    X.hidden.ensure(n[u] * d * 4);
+    X.depth.ensure(n[u] * 8);
+    X.s_dev.ensure(n[u] * 8);
+    X.s_key.ensure(n[u] * 8);
+    X.sel_idx.ensure(n[u] * 4);
+    X.sel_tags.ensure(2 * n[u] * 4);
+    X.info.ensure(64);
+    X.dinfo.ensure(64);
+    X.score.ensure(n[u] * 8);
+    RK_CUDA(cudaMemsetAsync(X.info.p, 0, 64, st_));
+    RK_CUDA(cudaMemsetAsync(X.dinfo.p, 0, 64, st_));
+    marks[u].base = base[u];
+    marks[u].len = n[u];
+    marks[u].origin.alloc(L * n[u]);
+    RK_CUDA(cudaMemsetAsync(marks[u].origin.p, 0, L * n[u], st_));
+    results.push_back(r);
+  }
+  const int ev_begin = event();
+  ctx->resize(total);
+  const size_t layer_stride = ctx->cap * w_->kv();
+  const double2* rope = w_->rope->cs.as<double2>();
+  for (uint64_t u = 0; u < U; ++u) {  // realign + graft (band layers skipped)
+    rk_cache* c = ups[u];
+    int skip_lo = 1, skip_hi = 0;
+    if (mode == RK_MODE_RELAY) { skip_lo = (int)l_start; skip_hi = (int)l_det; }
+    if (mode == RK_MODE_BLEND) { skip_lo = 0; skip_hi = 1; }
+    const int grafted = (int)L - (skip_hi >= skip_lo ? skip_hi - skip_lo + 1 : 0);
+    ProfScope ps(e_, "realign_graft", 3.0 * w_->kv() * n[u] * grafted, 4.0 * grafted * n[u] * w_->kv() * w_->elem);
+    k::realign_graft(st_, c->k_pre.p, c->v.p, w_->elem, (int)L, (int)n[u], (int)w_->kv(), (int)s.d_head, rope,
+                     (int)base[u], ctx->k.p, ctx->v.p, layer_stride, skip_lo, skip_hi);
+    e_->launches += 1;
+  }
+  const int ev_realign = event();
+  // pass inputs: prefix / suffix embeddings, segment snapshots (or embeddings for BLEND)
+  k::embed(st_, H, w_->emb, w_->elem, dtok_p, (int)P, (int)d, 0, nullptr);
+  k::iota_positions(st_, pos, (int)P, 0);
+  e_->launches += 2;
+  if (S) {
+    k::embed(st_, H + P * d, w_->emb, w_->elem, dtok_s, (int)S, (int)d, 0, nullptr);
+    k::iota_positions(st_, pos + P, (int)S, (int)sbase);
+    e_->launches += 2;
+  }
+  if (segs) {
+    for (uint64_t u = 0; u < U; ++u) {
+      float* dst = H + (head + base[u] - P) * d;
+      if (mode == RK_MODE_RELAY)
+        RK_CUDA(cudaMemcpyAsync(dst, ups[u]->hidden.p, n[u] * d * 4, cudaMemcpyDeviceToDevice, st_));
+      else
+        k::embed(st_, dst, w_->emb, w_->elem, ups[u]->tokens.as<int>(), (int)n[u], (int)d, 0, nullptr);
+      k::iota_positions(st_, pos + head + (base[u] - P), (int)n[u], (int)base[u]);
+      e_->launches += 2;
+    }
+  }
+  int ev_band = -1, ev_select = -1;
+  for (uint64_t l = 0; l < L; ++l) {
+    Rows rows{(int)head, nullptr, pos};
+    if (segs && l >= l_start && l <= l_det) rows = Rows{(int)(head + segrows), nullptr, pos};
+    else if (segs && l > l_det && l <= sparse_hi) rows = Rows{(int)(head + segrows), offs + U, pos};
+    run_layer(ctx, (int)l, H, rows, true, (int)total);
+    if (segs && l == l_det) {
+      ev_band = event();
+      for (uint64_t u = 0; u < U; ++u) {
+        ExtendSlot& X = slot(results[u].slot);
+        rk_cache* c = ups[u];
+        RK_CUDA(cudaMemcpyAsync(X.hidden.p, H + (head + base[u] - P) * d, n[u] * d * 4, cudaMemcpyDeviceToDevice, st_));
+        k::set_depth(st_, X.depth.as<uint64_t>(), (int)n[u], l_det + 1);
+        k::mark_layers(st_, marks[u].origin.as<uint8_t>(), (int)n[u], (int)l_start, (int)l_det);
+        const size_t el = w_->elem, kv = w_->kv();
+        const char* ctx_v_det = static_cast<const char*>(ctx->v_layer(l_det)) + base[u] * kv * el;
+        const char* cache_v_det = static_cast<const char*>(c->v.p) + l_det * n[u] * kv * el;
+        if (mode == RK_MODE_RELAY) {
+          const char* ctx_k_det = static_cast<const char*>(ctx->k_layer(l_det)) + base[u] * kv * el;
+          const char* cache_k_det = static_cast<const char*>(c->k_pre.p) + l_det * n[u] * kv * el;
+          {
+            ProfScope ps(e_, "score_deviation", 0, 4.0 * n[u] * kv * el);
+            k::score_deviation(st_, ctx_v_det, cache_v_det, ctx_k_det, cache_k_det, el, (int)n[u], (int)kv,
+                               (int)s.num_kv_heads, (int)s.d_head, rope, (int)base[u], X.s_dev.as<double>(),
+                               X.s_key.as<double>());
+          }
+          ProfScope ps(e_, "select_relay", 0, n[u] * 20.0);
+          k::select_relay(st_, X.s_dev.as<double>(), c->influence.as<float>(), c->infl_mean.as<double>(),
+                          (int)n[u], opts.tau_dev, opts.tau_inf, (int)std::min<uint64_t>(opts.suffix_k, 0x7fffffff),
+                          X.sel_idx.as<int>(), X.sel_tags.as<uint32_t>(), X.info.as<int>(), X.dinfo.as<double>());
+        } else {
+          k::blend_scores(st_, ctx_v_det, cache_v_det, el, (int)n[u], (int)kv, X.score.as<double>());
+          size_t count = static_cast<size_t>(opts.blend_alpha * static_cast<double>(n[u]));
+          if (count > n[u]) count = n[u];
+          results[u].blend_count = (int)count;
+          k::select_topk(st_, X.score.as<double>(), (int)n[u], (int)count, X.sel_idx.as<int>(),
+                         X.sel_tags.as<uint32_t>(), X.info.as<int>());
+          e_->launches += 1;
+        }
+        e_->launches += 5;
+        results[u].band_layers = l_det - l_start + 1;
+      }
+      ev_select = event();
+      if (sparse_hi > l_det) {  // compact the selected rows of every segment after [prefix | suffix]
+        k::SegCounts cnt{};
+        for (uint64_t u = 0; u < U; ++u) cnt.count[u] = slot(results[u].slot).info.as<int>();
+        k::segment_offsets(st_, cnt, (int)U, (int)head, offs);
+        e_->launches += 1;
+        for (uint64_t u = 0; u < U; ++u) {
+          ExtendSlot& X = slot(results[u].slot);
+          k::gather_rows_to(st_, H, offs + u, X.hidden.as<float>(), X.sel_idx.as<int>(), X.info.as<int>(), (int)n[u],
+                            (int)d, pos, (int)base[u]);
+          e_->launches += 1;
+        }
+      }
+    }
+    if (segs && l == sparse_hi && sparse_hi > l_det) {
+      for (uint64_t u = 0; u < U; ++u) {
+        ExtendSlot& X = slot(results[u].slot);
+        k::scatter_rows_from(st_, X.hidden.as<float>(), H, offs + u, X.sel_idx.as<int>(), X.info.as<int>(), (int)n[u],
+                             (int)d, X.depth.as<uint64_t>(), sparse_hi + 1);
+        k::mark_rows(st_, marks[u].origin.as<uint8_t>(), (int)n[u], (int)l_det + 1, (int)sparse_hi,
+                     X.sel_idx.as<int>(), X.info.as<int>(), (int)n[u]);
+        e_->launches += 2;
+        results[u].sparse_layers = sparse_hi - l_det;
+      }
+    }
+  }
+  if (!segs) {  // ZERO (relay_engine.cpp:224-234): the segment keeps its snapshot
+    for (uint64_t u = 0; u < U; ++u) {
+      ExtendSlot& X = slot(results[u].slot);
+      RK_CUDA(cudaMemcpyAsync(X.hidden.p, ups[u]->hidden.p, n[u] * d * 4, cudaMemcpyDeviceToDevice, st_));
+      k::set_depth(st_, X.depth.as<uint64_t>(), (int)n[u], ups[u]->snapshot);
+      e_->launches += 1;
+    }
+  }
+  const int ev_end = event();
+  for (uint64_t u = 0; u < U; ++u) {
+    ExtendResult& r = results[u];
+    r.ev_begin = ev_begin;
+    r.ev_realign = ev_realign;
+    r.ev_band = ev_band >= 0 ? ev_band : ev_end;
+    r.ev_select = ev_select >= 0 ? ev_select : r.ev_band;
+    r.ev_end = ev_end;
+    ctx->segs.push_back(std::move(marks[u]));
+    r.seg_index = ctx->segs.size() - 1;
+  }
+  if (S > 0) last_row_logits(H + (head - 1) * d);
+  else segment_end_logits(ctx, results.back());
 }
 
 // ---------------------------------------------------------------------------

@@ -111,6 +111,10 @@ class Engine(_Obj):
     def set_graphs(self, enable):
         _check(lib().rk_engine_set_graphs(P(self.ptr), int(enable)))
 
+    def set_fused(self, enable):
+        """Layer-major fused agent schedule (default) vs the sequential order."""
+        _check(lib().rk_engine_set_fused(P(self.ptr), int(enable)))
+
     def profile(self, enable=True):
         """Per-kernel CUDA-event instrumentation of the hot kernels (clears)."""
         _check(lib().rk_engine_profile(P(self.ptr), int(enable)))

@@ -70,14 +70,21 @@ def test_c1_bit_exact_and_capture(engine, oracle):
     assert_bit_equal(V, Vo, "c1.V")
 
 
-@pytest.mark.parametrize("mode", ["relay", "full", "blend"])
-def test_agent_prefill_bit_exact(engine, oracle, mode):
+@pytest.mark.parametrize("fused", [1, 0], ids=["fused", "sequential"])
+@pytest.mark.parametrize("mode", ["relay", "full", "blend", "zero"])
+def test_agent_prefill_bit_exact(engine, oracle, mode, fused):
+    """The downstream agent's prompt (prefix + 2 relayed segments + suffix, or
+    no suffix): the engine's layer-major fused schedule and its sequential
+    schedule are both bit-identical to the oracle's sequential order."""
+    engine.set_fused(fused)
     spec = spec_of(8, 32, 4)
     ow = oracle.weights(spec, 55)
     c1 = oracle.scenario(ow, pattern_tokens(9, 64, 1), 12, 1)
     c2 = oracle.scenario(ow, pattern_tokens(7, 64, 2), 9, 1)
     opts = RelayOptions.make(mode=mode, suffix_k=3, blend_alpha=0.25)
     prof = triple(1, 2, 5)
+    if mode == "zero":
+        c1 = oracle.scenario(ow, pattern_tokens(9, 64, 1), 12, 1)
     for suffix in (pattern_tokens(4, 64, 4), np.zeros(0, np.int32)):
         logits, tok, octx = oracle.agent_prefill(ow, pattern_tokens(5, 64, 3), [c1, c2], suffix, prof, opts)
         w = engine.weights(spec, 55)
@@ -90,6 +97,12 @@ def test_agent_prefill_bit_exact(engine, oracle, mode):
         Ko, Vo = oracle.ctx_all(octx)
         assert_bit_equal(K, Ko, f"agent.{mode}.K")
         assert_bit_equal(V, Vo, f"agent.{mode}.V")
+        segs, osegs = ctx.segments(), oracle.ctx_segments(octx)
+        assert len(segs) == len(osegs)
+        for (b, l, a), (ob, ol, oa) in zip(segs, osegs):
+            assert (b, l) == (ob, ol)
+            assert_bit_equal(a, oa, f"agent.{mode}.marks")
+    engine.set_fused(1)
 
 
 def test_zero_mode_round_trip(engine, oracle):
