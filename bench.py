@@ -204,6 +204,18 @@ def cpu_sample(gpu_caches=None, threads=None, steps=1, warmup=0, kind="reference
     return tps, meta
 
 
+def merge_kernel_stats(stats):
+    """Collapse per-shape labels (gemm_qkv_m320_..., attn_m...) into kernel families."""
+    fam = {}
+    for k in stats:
+        name = "gemm_bf16_tcgen05" if k["name"].startswith("gemm") else \
+            "attention_bf16_tcgen05" if k["name"].startswith("attn") else k["name"]
+        f = fam.setdefault(name, {"name": name, "launches": 0, "total_ms": 0.0, "flops": 0.0, "bytes": 0.0})
+        for key in ("launches", "total_ms", "flops", "bytes"):
+            f[key] += k[key]
+    return list(fam.values())
+
+
 # ---- our engine ------------------------------------------------------------------
 def build_workload(eng, rank):
     from paper_2603_13289_b200.engine import Engine  # noqa: F401
@@ -312,6 +324,8 @@ def run_ours(args, world, rank, local, dist):
         dist.all_gather(allt, t)
 
     hbm, tf_burst, tf_sus, src = peaks()
+    detail = sorted(kstats, key=lambda k: -k["total_ms"])
+    kstats = merge_kernel_stats(kstats)
     gemm = next((k for k in kstats if k["name"].startswith("gemm")), None)
     roofline = None
     if gemm and gemm["total_ms"] > 0:
@@ -362,6 +376,9 @@ def run_ours(args, world, rank, local, dist):
         "gpu_launches": int(launches),
         "roofline": roofline,
         "kernels": kernels,
+        "kernel_detail": [{"name": k["name"], "launches": k["launches"], "ms": round(k["total_ms"], 4),
+                           "tflops": round(k["flops"] / (k["total_ms"] / 1e3) / 1e12, 1) if k["flops"] and k["total_ms"] else None}
+                          for k in detail[:40]],
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
     }

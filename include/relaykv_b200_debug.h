@@ -18,6 +18,10 @@ int rk_debug_gemm_bf16(rk_engine* e, const float* A, const float* B, float* C, i
  * over ctx rows [T x Hkv*dh]; bf16 operands. */
 int rk_debug_attention_bf16(rk_engine* e, const float* q, const float* k, const float* v, const int32_t* pos,
                             int M, int T, int H, int Hkv, int dh, float* out);
+/* Device-resident timing (random operands, CUDA events): avg ms per call.
+ * attention: band rows at positions T-M..T-1 over T context rows. */
+int rk_debug_bench_attention(rk_engine* e, int M, int T, int H, int Hkv, int dh, int iters, float* ms);
+int rk_debug_bench_gemm(rk_engine* e, int M, int N, int K, int epi, int iters, float* ms);
 /* y[i] = device glibc_expf(x[i]) */
 int rk_debug_expf(rk_engine* e, const float* x, float* y, uint64_t n);
 #ifdef __cplusplus

@@ -88,6 +88,81 @@ int rk_debug_attention_bf16(rk_engine* e, const float* q, const float* kk, const
   });
 }
 
+// Device-resident timing of one kernel shape (random bf16 operands), avg ms per call.
+int rk_debug_bench_attention(rk_engine* e, int M, int T, int H, int Hkv, int dh, int iters, float* ms) {
+  return guard([&] {
+    cudaStream_t st = e->stream;
+    const size_t nq = (size_t)M * H * dh, nk = (size_t)T * Hkv * dh;
+    DevBuf f((nq > nk ? nq : nk) * 4), qb(nq * 2), kb(nk * 2), vb(nk * 2), o(nq * 2), p(M * 4);
+    k::init_uniform(st, f.as<float>(), nq, 11, 1.0f);
+    k::f32_to_bf16(st, qb.as<__nv_bfloat16>(), f.as<float>(), nq);
+    k::init_uniform(st, f.as<float>(), nk, 12, 1.0f);
+    k::f32_to_bf16(st, kb.as<__nv_bfloat16>(), f.as<float>(), nk);
+    k::init_uniform(st, f.as<float>(), nk, 13, 1.0f);
+    k::f32_to_bf16(st, vb.as<__nv_bfloat16>(), f.as<float>(), nk);
+    k::iota_positions(st, p.as<int>(), M, T - M);
+    AttnArgs a;
+    a.q = qb.as<__nv_bfloat16>();
+    a.out = o.as<__nv_bfloat16>();
+    a.pos = p.as<int>();
+    a.rows_max = M;
+    a.H = H;
+    a.Hkv = Hkv;
+    a.dh = dh;
+    a.scale_log2 = 1.4426950408889634f / std::sqrt((float)dh);
+    attention_bf16(e, a, kb.as<__nv_bfloat16>(), vb.as<__nv_bfloat16>(), T);
+    cudaEvent_t e0, e1;
+    RK_CUDA(cudaEventCreate(&e0));
+    RK_CUDA(cudaEventCreate(&e1));
+    RK_CUDA(cudaEventRecord(e0, st));
+    for (int i = 0; i < iters; ++i) attention_bf16(e, a, kb.as<__nv_bfloat16>(), vb.as<__nv_bfloat16>(), T);
+    RK_CUDA(cudaEventRecord(e1, st));
+    RK_CUDA(cudaEventSynchronize(e1));
+    RK_CUDA(cudaEventElapsedTime(ms, e0, e1));
+    *ms /= iters;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    RK_CUDA(cudaGetLastError());
+  });
+}
+
+int rk_debug_bench_gemm(rk_engine* e, int M, int N, int K, int epi, int iters, float* ms) {
+  return guard([&] {
+    cudaStream_t st = e->stream;
+    DevBuf f((size_t)(M > N ? M : N) * K * 4), a((size_t)M * K * 2), b((size_t)N * K * 2), c((size_t)M * N * 4),
+        flags(1 << 18);
+    k::init_uniform(st, f.as<float>(), (size_t)M * K, 21, 1.0f);
+    k::f32_to_bf16(st, a.as<__nv_bfloat16>(), f.as<float>(), (size_t)M * K);
+    k::init_uniform(st, f.as<float>(), (size_t)N * K, 22, 0.02f);
+    k::f32_to_bf16(st, b.as<__nv_bfloat16>(), f.as<float>(), (size_t)N * K);
+    RK_CUDA(cudaMemsetAsync(c.p, 0, c.bytes, st));
+    RK_CUDA(cudaMemsetAsync(flags.p, 0, flags.bytes, st));
+    GemmArgs g;
+    g.rows_max = M;
+    g.N = N;
+    g.K = K;
+    g.epi = epi;
+    g.out_f32 = c.as<float>();
+    g.ld_out = N;
+    g.out_bf16 = reinterpret_cast<__nv_bfloat16*>(c.p);
+    g.ld_bf16 = N / 2;
+    g.split_flags = flags.as<int>();
+    gemm_bf16(e, a.as<__nv_bfloat16>(), K, b.as<__nv_bfloat16>(), g, M);
+    cudaEvent_t e0, e1;
+    RK_CUDA(cudaEventCreate(&e0));
+    RK_CUDA(cudaEventCreate(&e1));
+    RK_CUDA(cudaEventRecord(e0, st));
+    for (int i = 0; i < iters; ++i) gemm_bf16(e, a.as<__nv_bfloat16>(), K, b.as<__nv_bfloat16>(), g, M);
+    RK_CUDA(cudaEventRecord(e1, st));
+    RK_CUDA(cudaEventSynchronize(e1));
+    RK_CUDA(cudaEventElapsedTime(ms, e0, e1));
+    *ms /= iters;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    RK_CUDA(cudaGetLastError());
+  });
+}
+
 int rk_debug_expf(rk_engine* e, const float* x, float* y, uint64_t n) {
   return guard([&] {
     DevBuf dx(n * 4), dy(n * 4);

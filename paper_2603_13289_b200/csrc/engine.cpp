@@ -752,6 +752,12 @@ double rk_flops_segment_schedule(const rk_model_spec* s, uint64_t base, uint64_t
 // profiling + context reset
 // ============================================================================
 namespace rk {
+const char* intern(const std::string& s) {
+  static std::set<std::string> pool;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  return pool.insert(s).first->c_str();
+}
 Profiler& profiler(rk_engine* e) {
   if (!e->prof) e->prof.reset(new Profiler());
   return *e->prof;

@@ -352,7 +352,13 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
   const int num_m = (p.rows_max + kBM - 1) / kBM;
   const int total = num_m * (p.N / p.bn) * p.splits;
   const int grid = total < e->sm_count ? total : e->sm_count;
-  ProfScope ps(e, "gemm_bf16_tcgen05", 0, 0);
+  static const char* kEpi[] = {"qkv", "add", "silu", "f32"};
+  ProfScope ps(e, (e->prof && e->prof->on)
+                      ? intern(std::string("gemm_") + kEpi[p.epi] + "_m" + std::to_string(p.rows_max) +
+                               (p.rows_dev ? "dyn" : "") + "_n" + std::to_string(p.N) + "_k" + std::to_string(p.K) +
+                               "_bn" + std::to_string(p.bn) + "_s" + std::to_string(p.splits))
+                      : "gemm",
+               0, 0);
   ps.rec.kind = 1;
   ps.rec.rows_dev = p.rows_dev;
   ps.rec.rows_max = rows_hint > 0 && !p.rows_dev ? p.rows_max : p.rows_max;

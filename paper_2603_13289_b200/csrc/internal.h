@@ -152,7 +152,7 @@ namespace rk {
 struct Scratch {
   DevBuf hidden, sub_hidden, normed, qkv, attn, act, logits, tokens, positions, sub_positions;
   DevBuf s_dev, s_key, sel_idx, sel_tags, sel_info, depth, argmax, seg_hidden_out;
-  DevBuf gemm_tmp;
+  DevBuf gemm_tmp, attn_ws;
 };
 
 RopeTable* rope_table(rk_engine* e, float theta, uint64_t d_head, uint64_t positions);

@@ -52,6 +52,10 @@ struct AttnArgs {
   // probability capture for influence (key window [key_lo, key_lo+key_n))
   float* probs = nullptr;
   int key_lo = 0, key_n = 0;
+  // split-KV (set by attention_bf16): partial O / (m, l) workspace
+  int splits = 1, tiles_per_split = 1 << 20;
+  float* ws_o = nullptr;
+  float* ws_ml = nullptr;
 };
 // ctx_k / ctx_v: the layer's [ctx_rows x kv] bf16 context rows.
 void attention_bf16(rk_engine* e, const AttnArgs& a, const __nv_bfloat16* ctx_k, const __nv_bfloat16* ctx_v,

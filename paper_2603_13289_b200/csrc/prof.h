@@ -1,6 +1,8 @@
 // prof.h -- optional per-launch timing of the hot kernels (CUDA events on the
 // engine stream) with their algorithmic work, for roofline reporting.
 #pragma once
+#include <set>
+#include <string>
 #include <vector>
 
 #include "internal.h"
@@ -36,6 +38,8 @@ struct Profiler {
 };
 
 Profiler& profiler(rk_engine* e);
+// Stable storage for generated kernel labels.
+const char* intern(const std::string& s);
 
 // RAII scope around one launch.
 struct ProfScope {

@@ -89,7 +89,8 @@ def ref_attention(q, k, v, pos, H, Hkv, dh):
 
 
 ATT = [(64, 200, 4, 2, 64, "band"), (300, 700, 8, 2, 64, "sparse"), (130, 1000, 4, 4, 128, "band"),
-       (1, 333, 4, 1, 128, "band"), (257, 1500, 32, 8, 64, "sparse")]
+       (1, 333, 4, 1, 128, "band"), (257, 1500, 32, 8, 64, "sparse"), (320, 4032, 32, 8, 64, "mixed"),
+       (700, 2000, 16, 4, 128, "mixed")]
 
 
 @pytest.mark.parametrize("case", ATT, ids=[f"{c[5]}-M{c[0]}-T{c[1]}-dh{c[4]}" for c in ATT])
@@ -98,6 +99,10 @@ def test_attention(engine, case):
     rng = np.random.default_rng(M + T)
     if kind == "band":
         pos = np.arange(T - M, T, dtype=np.int32)
+    elif kind == "mixed":  # fused-schedule layout: [prefix | suffix | segment rows], unsorted
+        n_pre, n_suf = M // 4, M // 8
+        seg = np.sort(rng.choice(np.arange(n_pre, T - n_suf), M - n_pre - n_suf, replace=False))
+        pos = np.concatenate([np.arange(n_pre), np.arange(T - n_suf, T), seg]).astype(np.int32)
     else:
         pos = np.sort(rng.choice(T, M, replace=False)).astype(np.int32)
     q = rng.standard_normal((M, H * dh)).astype(np.float32)
