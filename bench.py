@@ -217,11 +217,10 @@ def merge_kernel_stats(stats):
 
 
 # ---- our engine ------------------------------------------------------------------
-def build_workload(eng, rank):
-    from paper_2603_13289_b200.engine import Engine  # noqa: F401
-    spec = spec_obj()
-    w = eng.weights(spec, SEED + rank, "bf16")
-    pr = prompts(rank)
+def build_session(w, session):
+    """One collaboration session: the Architect's and Developer's decode-time
+    caches (captured on the device) and the Reviewer's prompt parts."""
+    pr = prompts(session)
     prof, opts = options()
     snap = PROFILE[0]
     # Architect: decode-time capture of its output after its prompt
@@ -233,25 +232,34 @@ def build_workload(eng, rank):
     ctx2.agent_prefill(pr["dev_prefix"], [cache1], pr["dev_suffix"], prof, opts, want_logits=False)
     cache2 = ctx2.capture_prefill(pr["dev_out"], snap)
     del ctx1, ctx2
-    return w, [cache1, cache2], pr
+    return {"caches": [cache1, cache2], "prompts": pr, "ctx": w.context(), "session": session}
 
 
 def run_ours(args, world, rank, local, dist):
     import torch
     from paper_2603_13289_b200.engine import Engine
+    from paper_2603_13289_b200.sessions import gather_records, shard
     torch.cuda.set_device(local)
     eng = Engine(local)
-    w, caches, pr = build_workload(eng, rank)
+    w = eng.weights(spec_obj(), SEED, "bf16")
+    n_sessions = args.sessions or world
+    mine = [build_session(w, sid) for sid in shard(n_sessions, world, rank)]
     prof, opts = options()
     _, full_opts = options("full")
-    ctx = w.context()
     stream = torch.cuda.ExternalStream(eng.stream)
     n_tokens = PREFIX + 2 * SEGMENT + SUFFIX
+    # first local session carries the single-session diagnostics
+    caches, pr, ctx = mine[0]["caches"], mine[0]["prompts"], mine[0]["ctx"]
 
-    def step(o=opts, want_outputs=False):
-        ctx.reset()
-        return ctx.agent_prefill(pr["rev_prefix"], caches, pr["rev_suffix"], prof, o, want_logits=False,
-                                 outputs=want_outputs)
+    def run_session(sess, o=opts, want_outputs=False):
+        sess["ctx"].reset()
+        p = sess["prompts"]
+        return sess["ctx"].agent_prefill(p["rev_prefix"], sess["caches"], p["rev_suffix"], prof, o,
+                                         want_logits=False, outputs=want_outputs)
+
+    def step(o=opts):
+        for sess in mine:
+            run_session(sess, o)
 
     def timed(fn, K, W):
         for _ in range(W):
@@ -273,8 +281,8 @@ def run_ours(args, world, rank, local, dist):
         barrier(dist)
         return t0.elapsed_time(t1), host_ms, eng.launches - launches0
 
-    # correctness / reuse diagnostics of one step
-    diag = step(want_outputs=True)
+    # correctness / reuse diagnostics of one session
+    diag = run_session(mine[0], want_outputs=True)
     segs = diag["segments"]
     reuse = [s["stats"]["reuse_rate"] for s in segs]
     selected = [int(s["selection_count"]) for s in segs]
@@ -283,9 +291,10 @@ def run_ours(args, world, rank, local, dist):
         dev_ms, host_ms, launches = timed(step, args.steps, args.warmup)
     dev_ms = reduce_max(dist, dev_ms, local)
     ms_step = dev_ms / args.steps
-    value = world * n_tokens * args.steps / (dev_ms / 1e3)
+    value = n_sessions * n_tokens * args.steps / (dev_ms / 1e3)
+    ttft = ms_step / len(mine)  # per session, sessions of a GPU run back to back
 
-    full_ms, _, _ = timed(lambda: step(full_opts), max(2, args.steps // 2), 1)
+    full_ms, _, _ = timed(lambda: run_session(mine[0], full_opts), max(2, args.steps // 2), 1)
     full_ms = reduce_max(dist, full_ms, local) / max(2, args.steps // 2)
 
     # end to end through the C ABI with HOST buffers: RelayCache fp32 arrays
@@ -305,23 +314,26 @@ def run_ours(args, world, rank, local, dist):
     h0 = time.perf_counter()
     for _ in range(e2e_K):
         e2e_step()
-    e2e_ms = reduce_max(dist, (time.perf_counter() - h0) * 1e3, local) / e2e_K
+    e2e_ms = reduce_max(dist, (time.perf_counter() - h0) * 1e3, local) / e2e_K  # one session per rank
     h2d = sum(h.k_pre.nbytes + h.v.nbytes + h.hidden_snapshot.nbytes + h.influence.nbytes + h.segment_tokens.nbytes
               for h in hosts) + 4 * (PREFIX + SUFFIX)
     d2h = 4 * SPEC["vocab_size"] + 4
 
     # per-kernel instrumentation pass (same step, CUDA events per launch)
     eng.profile(True)
-    step()
+    run_session(mine[0])
     kstats = eng.profile_read()
     eng.profile(False)
 
     # results gather over NCCL (after timing; no collective on the hot path)
-    tok = diag["first_token"]
-    if dist is not None:
-        t = torch.tensor([tok], dtype=torch.int64, device=f"cuda:{local}")
-        allt = [torch.zeros_like(t) for _ in range(world)]
-        dist.all_gather(allt, t)
+    recs = []
+    for sess in mine:
+        o = run_session(sess, want_outputs=True)
+        recs.append({"session": sess["session"], "first_token": o["first_token"], "segments": len(o["segments"]),
+                     "selected_total": sum(int(x["selection_count"]) for x in o["segments"]),
+                     "reuse": sum(x["stats"]["reuse_rate"] for x in o["segments"]) / len(o["segments"]),
+                     "ttft_ms": ttft})
+    gathered = gather_records(recs, n_sessions, dist, device=f"cuda:{local}")
 
     hbm, tf_burst, tf_sus, src = peaks()
     detail = sorted(kstats, key=lambda k: -k["total_ms"])
@@ -363,11 +375,13 @@ def run_ours(args, world, rank, local, dist):
                                "Architect->Developer->Reviewer chain, Reviewer TTFT at 4032-token prompt "
                                f"(prefix {PREFIX} + 2 relayed segments x {SEGMENT} + suffix {SUFFIX}), "
                                f"profile {PROFILE}, thresholds (1.5, 1.45, 10)",
-                   "sessions_per_gpu": 1, "l2": "inputs larger than L2 (2.8 GB of bf16 weights streamed per step)",
+                   "sessions_per_gpu": len(mine), "l2": "inputs larger than L2 (2.8 GB of bf16 weights streamed per step)",
                    "parallelism": f"sessions sharded, {world} GPU(s), no hot-path collective"},
-        "ttft_ms": round(ms_step, 4),
+        "ttft_ms": round(ttft, 4),
         "full_prefill_ttft_ms": round(full_ms, 4),
-        "speedup_vs_full_prefill": round(full_ms / ms_step, 3),
+        "speedup_vs_full_prefill": round(full_ms / ttft, 3),
+        "sessions": n_sessions, "sessions_gathered": len(gathered),
+        "first_tokens": [r["first_token"] for r in gathered][:16],
         "reuse_rate_per_segment": [round(r, 4) for r in reuse],
         "selected_per_segment": selected,
         "host_ms_per_step": round(host_ms / args.steps, 4),
@@ -442,6 +456,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--sessions", type=int, default=0,
+                    help="collaboration sessions in total, sharded contiguously over the GPUs (default: one per GPU)")
     args = ap.parse_args()
     world, rank, local, dist = dist_setup(args)
     if args.impl == "reference":

@@ -78,7 +78,37 @@ def build(jobs=8, force=False, verbose=False):
             raise RuntimeError(f"link failed\n{p.stdout}\n{p.stderr}")
         shutil.move(LIB + ".tmp", LIB)
         print(f"[build] linked {os.path.relpath(LIB, ROOT)}", flush=True)
+    build_dropin(force)
     return LIB
+
+
+DROPIN = os.path.join(HERE, "librelaykv_dropin.so")
+DROPIN_TEST = os.path.join(HERE, "_bin", "test_dropin")
+
+
+def build_dropin(force=False):
+    """The C++ drop-in (namespace relaykv, cpp/) over the C ABI, and its test binary."""
+    src = os.path.join(HERE, "cpp", "relaykv_dropin.cpp")
+    hdrs = glob.glob(os.path.join(HERE, "cpp", "include", "relaykv", "*.hpp")) + \
+        [os.path.join(ROOT, "include", "relaykv_b200.h")]
+    newest = max(os.path.getmtime(f) for f in [src, LIB] + hdrs)
+    inc = ["-I", os.path.join(HERE, "cpp", "include"), "-I", os.path.join(ROOT, "include")]
+    if force or not os.path.exists(DROPIN) or os.path.getmtime(DROPIN) < newest:
+        subprocess.run([_cxx(), "-std=c++20", "-O2", "-fPIC", "-shared", *inc, src, "-o", DROPIN,
+                        "-L", HERE, "-lrelaykv_b200", "-Wl,-rpath,$ORIGIN"], check=True)
+        print(f"[build] linked {os.path.relpath(DROPIN, ROOT)}", flush=True)
+    test_src = os.path.join(ROOT, "tests", "cpp", "test_dropin.cpp")
+    oracle_lib = os.path.join(ROOT, "oracle", "build", "liboracle.so")
+    if os.path.exists(test_src) and os.path.exists(oracle_lib) and \
+            (force or not os.path.exists(DROPIN_TEST) or
+             os.path.getmtime(DROPIN_TEST) < max(newest, os.path.getmtime(test_src), os.path.getmtime(DROPIN))):
+        os.makedirs(os.path.dirname(DROPIN_TEST), exist_ok=True)
+        subprocess.run([_cxx(), "-std=c++20", "-O2", *inc, "-I", os.path.join(ROOT, "oracle", "doctest_shim"),
+                        test_src, "-o", DROPIN_TEST, "-L", HERE, "-lrelaykv_dropin", "-lrelaykv_b200",
+                        "-L", os.path.dirname(oracle_lib), "-loracle",
+                        f"-Wl,-rpath,{HERE}", f"-Wl,-rpath,{os.path.dirname(oracle_lib)}",
+                        "-Wl,-rpath,$ORIGIN/..", "-Wl,-rpath,$ORIGIN/../../oracle/build"], check=True)
+        print(f"[build] linked {os.path.relpath(DROPIN_TEST, ROOT)}", flush=True)
 
 
 if __name__ == "__main__":

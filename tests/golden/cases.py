@@ -1,0 +1,33 @@
+"""Golden-vector scenarios (inputs only; outputs come from the reference via
+make_golden.py). Mirrors the reference's own test scenarios
+(test_engine.cpp:101-324) plus BASELINE config 1."""
+from paper_2603_13289_b200.abi import LayerProfile, RelayOptions
+from tests.scenarios import c1_spec, pattern_tokens, spec_of, synthetic_tokens, triple
+
+CASES = {
+    # test_engine.cpp:298-324 "selection diagnostics are exposed and consistent"
+    "relay_diag_L8_d32": dict(kind="relay_prefill", spec=lambda: spec_of(8, 32, 4), seed=108,
+                              upstream=[(pattern_tokens(14, 64, 0), 20, 1)], prefix=pattern_tokens(10, 64, 8),
+                              profile=triple(1, 3, 6), opts=RelayOptions.make(suffix_k=4), store_cache=True,
+                              checked=True),
+    # test_engine.cpp:139-178 accounting: (1,3,18) on 32 layers, N=100
+    "relay_accounting_L32": dict(kind="relay_prefill", spec=lambda: spec_of(32, 16, 2), seed=103,
+                                 upstream=[(pattern_tokens(8, 64, 0), 100, 1)], prefix=pattern_tokens(12, 64, 3),
+                                 profile=triple(1, 3, 18),
+                                 opts=RelayOptions.make(tau_dev=1e9, tau_inf=1e9, suffix_k=10), checked=True),
+    # test_engine.cpp:180-208 blend baseline
+    "blend_alpha02_L8": dict(kind="relay_prefill", spec=lambda: spec_of(8, 32, 4), seed=104,
+                             upstream=[(pattern_tokens(10, 64, 0), 12, 0)], prefix=pattern_tokens(7, 64, 9),
+                             profile=LayerProfile(), opts=RelayOptions.make(mode="blend", blend_alpha=0.25),
+                             checked=True),
+    # BASELINE config 1: 2 layers, d=256, 4 heads, 512-token segment (unchecked init mirror)
+    "c1_relay_L2_d256_N512": dict(kind="relay_prefill", spec=c1_spec, seed=1234,
+                                  upstream=[(synthetic_tokens(1234, 1, 64, 256), 512, 0)],
+                                  prefix=synthetic_tokens(1234, 2, 48, 256), profile=triple(0, 0, 1),
+                                  opts=RelayOptions.make()),
+    # workflow.cpp:316-369: prefix + 2 relayed segments + suffix, GQA
+    "agent_gqa_two_segments": dict(kind="agent", spec=lambda: spec_of(6, 64, 4, kv_heads=2), seed=77,
+                                   upstream=[(pattern_tokens(9, 64, 1), 16, 1), (pattern_tokens(7, 64, 2), 11, 1)],
+                                   prefix=pattern_tokens(5, 64, 3), suffix=pattern_tokens(4, 64, 4),
+                                   profile=triple(1, 2, 4), opts=RelayOptions.make(suffix_k=3), checked=True),
+}
