@@ -291,6 +291,10 @@ def run_ours(args, world, rank, local, dist):
         dev_ms, host_ms, launches = timed(step, args.steps, args.warmup)
     dev_ms = reduce_max(dist, dev_ms, local)
     ms_step = dev_ms / args.steps
+    if args.lean:
+        if rank == 0:
+            print(json.dumps({"lean": True, "ms_per_step": round(ms_step, 4), "gpu_launches": int(launches)}), flush=True)
+        return
     value = n_sessions * n_tokens * args.steps / (dev_ms / 1e3)
     ttft = ms_step / len(mine)  # per session, sessions of a GPU run back to back
 
@@ -456,6 +460,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--lean", action="store_true",
+                    help="timed relay steps only (for ncu launch lists): no full-prefill, e2e or profiling legs")
     ap.add_argument("--sessions", type=int, default=0,
                     help="collaboration sessions in total, sharded contiguously over the GPUs (default: one per GPU)")
     args = ap.parse_args()
