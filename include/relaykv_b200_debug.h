@@ -14,10 +14,12 @@ extern "C" {
  * rows_max is passed through device memory like a sparse pass. */
 int rk_debug_gemm_bf16(rk_engine* e, const float* A, const float* B, float* C, int rows_max, int live_rows,
                        int N, int K, int epi);
-/* out[M x H*dh] = causal attention of q rows at positions pos (ascending)
- * over ctx rows [T x Hkv*dh]; bf16 operands. */
+/* out[M x H*dh] = causal attention of q rows at positions pos over ctx rows
+ * [T x Hkv*dh]; bf16 operands. Rows [live, M) are not computed (live passed
+ * through device memory like a sparse pass); row groups [0,g1) [g1,g2)
+ * [g2,live) as in the fused schedule (0, 0 = one group). */
 int rk_debug_attention_bf16(rk_engine* e, const float* q, const float* k, const float* v, const int32_t* pos,
-                            int M, int T, int H, int Hkv, int dh, float* out);
+                            int M, int live, int g1, int g2, int T, int H, int Hkv, int dh, float* out);
 /* Device-resident timing (random operands, CUDA events): avg ms per call.
  * attention: band rows at positions T-M..T-1 over T context rows. */
 int rk_debug_bench_attention(rk_engine* e, int M, int T, int H, int Hkv, int dh, int iters, float* ms);

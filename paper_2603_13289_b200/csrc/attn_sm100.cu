@@ -7,13 +7,20 @@
 // any ascending subset of positions (dense band or gathered sparse rows), so
 // the causal limit is per row, by absolute position.
 //
-// One CTA = 128 query rows x one head, flash-style over 128-key tiles:
-//   warp 0      TMA: Q once; K_j and V_j into a 2-stage ring
-//   warp 1      TMEM alloc + MMA issue: S_j = Q K_j^T -> TMEM (double buffered);
-//               O_j = P_j V_j -> TMEM (P from smem, V as MN-major B operand)
-//   warps 2..5  one query row per thread: S_j from TMEM, scale + causal mask,
-//               online softmax (exp2), P_j (bf16) into swizzled smem, then
-//               acc = acc * corr_j + O_j in registers; finally O = acc / l.
+// One CTA = up to kQT query tiles (128 rows each) x one head, flash-style over
+// 128-key tiles:
+//   warp 0      TMA: Q tiles once; K_j and V_j into a 2-stage ring
+//   warp 1      TMEM alloc + MMA issue: S_t(j+1) = Q_t K_{j+1}^T -> TMEM as soon
+//               as softmax t has pulled S_t(j) into registers, then
+//               O_t += P_t(j) [V_j | 1] -> TMEM (accumulated across key tiles)
+//   warps 2..   one softmax warpgroup per query tile, one row per thread:
+//               S into registers (TMEM freed at once), scale + causal mask, row
+//               max, lazy rescale of O in TMEM only when the max grows by more
+//               than 2^8, P = exp2(.) (MUFU + a cubic on the FMA pipe for a
+//               quarter of the columns) as bf16 into swizzled smem.
+// The row sum l rides along as the ones column of [V | 1]. Query tiles never
+// straddle a row group (prefix / suffix / segment rows of the fused schedule),
+// and each tile stops at its own last key tile.
 #include <cuda.h>
 
 #include <algorithm>
@@ -33,12 +40,40 @@ __device__ __forceinline__ float fast_exp2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// 2^x on the FMA pipe: round-to-nearest split x = n + f (f in [-0.5, 0.5]),
+// minimax cubic for 2^f (max rel. err 7.5e-5, far below bf16's 2^-9), n added
+// straight into the exponent. Valid for x <= 64; clamps far below underflow.
+__device__ __forceinline__ float poly_exp2(float x) {
+  x = fmaxf(x, -127.0f);
+  const float t = x + 12582912.0f;  // 1.5 * 2^23: integer part lands in the low mantissa bits
+  const float f = x - (t - 12582912.0f);
+  const float p = fmaf(fmaf(fmaf(0.05517166f, f, 0.24261115f), f, 0.69326097f), f, 0.99992806f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st1(uint32_t taddr, uint32_t v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 constexpr int kQ = 128;     // query rows per tile (one softmax warpgroup each)
 constexpr int kKeys = 128;  // keys per tile
+constexpr float kRescaleLog2 = 8.0f;  // lazy O rescale threshold (P <= 2^8)
 // query tiles per CTA (ping-pong softmax warpgroups over shared K/V tiles)
 template <int DH> constexpr int qtiles() { return DH == 64 ? 2 : 1; }
-template <int DH> constexpr int threads() { return 64 + qtiles<DH>() * 128; }  // TMA, MMA, softmax WGs
+// softmax warpgroups first (warp w reads TMEM lanes 32*(w%4)..), then one control
+// warpgroup: TMA warp, MMA warp, two idle warps (setmaxnreg works per warpgroup)
+template <int DH> constexpr int threads() { return (qtiles<DH>() + 1) * 128; }
 
 template <int DH>
 struct ACfg {
@@ -59,6 +94,23 @@ struct ACfg {
   static constexpr uint32_t S_COL = 0, O_COL = 256;
 };
 
+// Query tile `tile` of the launch -> rows [r0, r1) within one row group.
+__device__ __forceinline__ void tile_rows(const AttnArgs& a, int M, int tile, int& r0, int& r1) {
+  const int g1 = min(a.g1, M), g2 = min(max(a.g2, g1), M);
+  const int b[4] = {0, g1, g2, M};
+#pragma unroll
+  for (int g = 0; g < 3; ++g) {
+    const int nt = (b[g + 1] - b[g] + kQ - 1) / kQ;
+    if (tile < nt) {
+      r0 = b[g] + tile * kQ;
+      r1 = min(r0 + kQ, b[g + 1]);
+      return;
+    }
+    tile -= nt;
+  }
+  r0 = r1 = 0;
+}
+
 template <int DH>
 __global__ void __launch_bounds__(threads<DH>(), 1)
     attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -74,39 +126,45 @@ __global__ void __launch_bounds__(threads<DH>(), 1)
   uint64_t* s_full = bar + 5;    // [kQT]
   uint64_t* s_free = bar + 7;    // [kQT]
   uint64_t* p_full = bar + 9;    // [kQT]
-  uint64_t* o_full = bar + 11;   // [kQT]
-  uint64_t* o_free = bar + 13;   // [kQT]
+  uint64_t* o_done = bar + 11;   // [kQT]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+  __shared__ int s_kmax[kQT];
 
   const int M = a.rows_dev ? *a.rows_dev : a.rows_max;
-  const int m0 = blockIdx.x * (kQ * kQT);
-  if (m0 >= M) return;
+  int r0[kQT], r1[kQT];
+#pragma unroll
+  for (int t = 0; t < kQT; ++t) tile_rows(a, M, blockIdx.x * kQT + t, r0[t], r1[t]);
+  if (r1[0] <= r0[0]) return;  // no rows (tiles past the live count)
   const int h = blockIdx.y;
   const int kvh = h / (a.H / a.Hkv);
-  // key range: up to the largest position among the CTA's rows (rows need not
-  // be sorted: the fused schedule packs prefix, suffix and segment rows)
-  __shared__ int s_kmax;
-  if (threadIdx.x == 0) s_kmax = 0;
+  if (threadIdx.x < kQT) s_kmax[threadIdx.x] = -1;
   __syncthreads();
-  for (int i = threadIdx.x; i < kQ * kQT; i += blockDim.x)
-    if (m0 + i < M) atomicMax(&s_kmax, a.pos[m0 + i]);
+#pragma unroll
+  for (int t = 0; t < kQT; ++t)
+    for (int i = r0[t] + threadIdx.x; i < r1[t]; i += blockDim.x) atomicMax(&s_kmax[t], a.pos[i]);
   __syncthreads();
-  const int kmax = s_kmax;
-  // split-KV: this CTA covers key tiles [j0, j0 + nk)
+  // split-KV: this CTA covers key tiles [j0, j0 + tiles_per_split); tile t needs nk[t] of them
   const int j0 = blockIdx.z * a.tiles_per_split;
-  const int nk = min(kmax / kKeys + 1 - j0, a.tiles_per_split);
+  int nk[kQT], nk_all = 0;
+#pragma unroll
+  for (int t = 0; t < kQT; ++t) {
+    nk[t] = r1[t] > r0[t] ? min(s_kmax[t] / kKeys + 1 - j0, a.tiles_per_split) : 0;
+    nk_all = max(nk_all, nk[t]);
+  }
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  if (nk <= 0) {  // no keys for this split: an empty partial (m = -inf, l = 0)
-    for (int i = threadIdx.x; i < kQ * kQT; i += blockDim.x)
-      if (m0 + i < M) {
-        float* ml = a.ws_ml + (((size_t)blockIdx.z * a.rows_max + m0 + i) * a.H + h) * 2;
+  if (nk_all <= 0) {  // no keys for this split: empty partials (m = -inf, l = 0)
+#pragma unroll
+    for (int t = 0; t < kQT; ++t)
+      for (int i = r0[t] + threadIdx.x; i < r1[t]; i += blockDim.x) {
+        float* ml = a.ws_ml + (((size_t)blockIdx.z * a.rows_max + i) * a.H + h) * 2;
         ml[0] = -INFINITY;
         ml[1] = 0.f;
       }
     return;
   }
 
-  if (warp == 0 && lane == 0) {
+  const int ctl = 4 * kQT;  // first warp of the control warpgroup
+  if (warp == ctl && lane == 0) {
     tma_prefetch(&tmQ);
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
@@ -119,12 +177,11 @@ __global__ void __launch_bounds__(threads<DH>(), 1)
       mbar_init(&s_full[t], 1);
       mbar_init(&s_free[t], 4);
       mbar_init(&p_full[t], 4);
-      mbar_init(&o_full[t], 1);
-      mbar_init(&o_free[t], 4);
+      mbar_init(&o_done[t], 1);
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  if (warp == ctl + 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
   for (int st = 0; st < 2; ++st) {  // the constant ones block of each K/V stage
     uint4* ones = reinterpret_cast<uint4*>(smem + C::OFF_KV + st * C::STAGE_BYTES + 2 * C::KV_BYTES);
     for (int i = threadIdx.x; i < C::ONES_BYTES / 16; i += blockDim.x) ones[i] = make_uint4(0x3f803f80u, 0x3f803f80u, 0x3f803f80u, 0x3f803f80u);
@@ -136,14 +193,20 @@ __global__ void __launch_bounds__(threads<DH>(), 1)
   const uint32_t tmem = *tmem_slot;
   constexpr int DB = DH / 64;  // 64-wide swizzle blocks along d
 
-  if (warp == 0) {
+  if (warp >= ctl) {
+    // control warpgroup: hand registers to the softmax warpgroups
+    if constexpr (kQT == 2) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+  if (warp == ctl) {
     if (elect_one()) {  // ------------------------------------------------ TMA
       uint8_t* sq = smem + C::OFF_Q;
-      mbar_arrive_expect_tx(q_full, kQT * C::Q_TILE);
+      int nq = 0;
+      for (int t = 0; t < kQT; ++t) nq += nk[t] > 0;
+      mbar_arrive_expect_tx(q_full, nq * C::Q_TILE);
       for (int t = 0; t < kQT; ++t)
-        for (int b = 0; b < DB; ++b)
-          tma_load_2d(sq + t * C::Q_TILE + b * kQ * 128, &tmQ, q_full, h * DH + b * 64, m0 + t * kQ);
-      for (int j = 0; j < nk; ++j) {
+        if (nk[t] > 0)
+          for (int b = 0; b < DB; ++b)
+            tma_load_2d(sq + t * C::Q_TILE + b * kQ * 128, &tmQ, q_full, h * DH + b * 64, r0[t]);
+      for (int j = 0; j < nk_all; ++j) {
         const int st = j & 1;
         mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
         uint8_t* sk = smem + C::OFF_KV + st * C::STAGE_BYTES;
@@ -155,7 +218,7 @@ __global__ void __launch_bounds__(threads<DH>(), 1)
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == ctl + 1) {
     if (elect_one()) {  // ------------------------------------------------ MMA
       constexpr uint32_t idesc_s = idesc_bf16(kQ, kKeys);
       constexpr uint32_t idesc_o = idesc_bf16(kQ, C::ON, /*b_mn_major=*/true);
@@ -178,7 +241,6 @@ __global__ void __launch_bounds__(threads<DH>(), 1)
       auto issue_pv = [&](int j, int t) {
         const int st = j & 1;
         mbar_wait(&p_full[t], j & 1);
-        mbar_wait(&o_free[t], (j & 1) ^ 1);
         tc_fence_after();
         const uint32_t sp = smem_u32(smem + C::OFF_P + t * C::P_BYTES);
         const uint32_t sv = smem_u32(smem + C::OFF_KV + st * C::STAGE_BYTES + C::KV_BYTES);
@@ -186,164 +248,174 @@ __global__ void __launch_bounds__(threads<DH>(), 1)
         for (int k = 0; k < kKeys / 16; ++k) {
           const uint64_t ad = sdesc_sw128(sp + (k >> 2) * (kQ * 128) + (k & 3) * 32, 16, 1024);
           const uint64_t bd = sdesc_sw128(sv + k * 2048, kKeys * 128, 1024);
-          mma_bf16_ss(tmem + C::O_COL + t * 128, ad, bd, idesc_o, k > 0 ? 1u : 0u);
+          mma_bf16_ss(tmem + C::O_COL + t * 128, ad, bd, idesc_o, (j > 0 || k > 0) ? 1u : 0u);
         }
-        tc_commit(&o_full[t]);
+        tc_commit(&o_done[t]);
       };
-      // ping-pong order: as soon as warpgroup t has turned S_t(j) into P_t(j),
-      // issue its P.V and its next S, so one group's softmax overlaps the
-      // other group's MMAs.
+      // S_t(j+1) goes in as soon as softmax t has S_t(j) in registers, ahead of
+      // P_t(j) V_j, so the tensor pipe computes the next scores while the
+      // softmax warpgroups exponentiate the current ones.
       mbar_wait(&kv_full[0], 0);
-      for (int t = 0; t < kQT; ++t) issue_s(0, t);
-      for (int j = 0; j < nk; ++j) {
-        if (j + 1 < nk) mbar_wait(&kv_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
-        for (int t = 0; t < kQT; ++t) {
-          if (j + 1 < nk) issue_s(j + 1, t);  // its softmax needs S first; O only later
-          issue_pv(j, t);
-        }
+      for (int t = 0; t < kQT; ++t)
+        if (nk[t] > 0) issue_s(0, t);
+      for (int j = 0; j < nk_all; ++j) {
+        if (j + 1 < nk_all) mbar_wait(&kv_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+        for (int t = 0; t < kQT; ++t)
+          if (j + 1 < nk[t]) issue_s(j + 1, t);
+        for (int t = 0; t < kQT; ++t)
+          if (j < nk[t]) issue_pv(j, t);
         tc_commit(&kv_empty[j & 1]);
       }
     }
-  } else {  // ----------------------------------------- softmax warpgroups
-    const int t = (warp - 2) / 4;        // query tile of this warpgroup
+  }
+  } else {  // ------------------------------------------------ softmax warpgroups
+    if constexpr (kQT == 2) asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+    const int t = warp / 4;              // query tile of this warpgroup
     const int quarter = warp & 3;        // TMEM lane quarter this warp may access
     const int rl = quarter * 32 + lane;  // row within the tile == TMEM lane
-    const int row = m0 + t * kQ + rl;
-    const bool valid = row < M;
-    const int pos = valid ? a.pos[row] : kmax;
-    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
-    const uint32_t s_col = tmem + lane_base + C::S_COL + t * 128;
-    const uint32_t o_col = tmem + lane_base + C::O_COL + t * 128;
-    uint8_t* sp = smem + C::OFF_P + t * C::P_BYTES;
-    const float scale = a.scale_log2;
-    float acc[DH];
-#pragma unroll
-    for (int d = 0; d < DH; ++d) acc[d] = 0.f;
-    float m_run = -INFINITY, l_run = 0.f, corr_pending = 0.f;
-    for (int j = 0; j < nk; ++j) {
-      mbar_wait(&s_full[t], j & 1);
-      tc_fence_after();
-      const int kbase = (j0 + j) * kKeys;
-      // warp-uniform: no causal mask anywhere in this tile for this warp's rows
-      const bool full = __all_sync(0xffffffffu, kbase + kKeys - 1 <= pos);
-      // pass 1: row max of the raw scores (scale > 0 commutes with max); two
-      // 32-column TMEM loads per wait, four independent max chains
-      float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
-#pragma unroll
-      for (int c = 0; c < kKeys; c += 64) {
-        uint32_t r[32], q2[32];
-        tmem_ld32(s_col + c, r);
-        tmem_ld32(s_col + c + 32, q2);
-        tmem_ld_wait();
-        if (full) {
-#pragma unroll
-          for (int u = 0; u < 32; u += 4) {
-            mx0 = fmaxf(mx0, fmaxf(__uint_as_float(r[u]), __uint_as_float(r[u + 1])));
-            mx1 = fmaxf(mx1, fmaxf(__uint_as_float(r[u + 2]), __uint_as_float(r[u + 3])));
-            mx2 = fmaxf(mx2, fmaxf(__uint_as_float(q2[u]), __uint_as_float(q2[u + 1])));
-            mx3 = fmaxf(mx3, fmaxf(__uint_as_float(q2[u + 2]), __uint_as_float(q2[u + 3])));
-          }
-        } else {
-#pragma unroll
-          for (int u = 0; u < 32; ++u) {
-            if (kbase + c + u <= pos) mx0 = fmaxf(mx0, __uint_as_float(r[u]));
-            if (kbase + c + 32 + u <= pos) mx1 = fmaxf(mx1, __uint_as_float(q2[u]));
-          }
-        }
+    const int row = r0[t] + rl;
+    const bool valid = row < r1[t];
+    const int my_nk = nk[t];
+    if (my_nk <= 0) {  // this tile has no keys in this split
+      if (valid && a.splits > 1) {
+        float* ml = a.ws_ml + (((size_t)blockIdx.z * a.rows_max + row) * a.H + h) * 2;
+        ml[0] = -INFINITY;
+        ml[1] = 0.f;
       }
-      const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
-      const float m_new = fmaxf(m_run, mx * scale);
-      const float corr = fast_exp2(m_run - m_new);  // 0 on the first tile
-      // PV_{j-1} done: P buffer free, O_{j-1} (and its row sum) ready
-      if (j > 0) {
-        mbar_wait(&o_full[t], (j - 1) & 1);
+    } else {
+      const int pos = valid ? a.pos[row] : s_kmax[t];
+      const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+      const uint32_t s_col = tmem + lane_base + C::S_COL + t * 128;
+      const uint32_t o_col = tmem + lane_base + C::O_COL + t * 128;
+      uint8_t* sp = smem + C::OFF_P + t * C::P_BYTES;
+      const float scale = a.scale_log2;
+      float m_run = -INFINITY;
+      for (int j = 0; j < my_nk; ++j) {
+        mbar_wait(&s_full[t], j & 1);
         tc_fence_after();
-#pragma unroll
-        for (int c = 0; c < DH; c += 32) {
-          uint32_t r[32];
-          tmem_ld32(o_col + c, r);
-          tmem_ld_wait();
-#pragma unroll
-          for (int u = 0; u < 32; ++u) acc[c + u] = fmaf(acc[c + u], corr_pending, __uint_as_float(r[u]));
-        }
-        const uint32_t rs = tmem_ld1(o_col + DH);
+        uint32_t r[128];
+        tmem_ld32(s_col + 0, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+        tmem_ld32(s_col + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+        tmem_ld32(s_col + 64, *reinterpret_cast<uint32_t(*)[32]>(&r[64]));
+        tmem_ld32(s_col + 96, *reinterpret_cast<uint32_t(*)[32]>(&r[96]));
         tmem_ld_wait();
-        l_run = fmaf(l_run, corr_pending, __uint_as_float(rs));
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&o_free[t]);
-      }
-      // pass 2: P = exp2(s*scale - m_new) -> bf16, K-major SW128 (2 blocks of 64 keys)
-      const float neg_m = -m_new;
+        if (lane == 0) mbar_arrive(&s_free[t]);  // S_t(j+1) may overwrite TMEM now
+        const int kbase = (j0 + j) * kKeys;
+        // warp-uniform: no causal mask anywhere in this tile for this warp's rows
+        if (!__all_sync(0xffffffffu, kbase + kKeys - 1 <= pos)) {
 #pragma unroll
-      for (int b = 0; b < 2; ++b) {
-        uint32_t r[64];
-        tmem_ld32(s_col + b * 64, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
-        tmem_ld32(s_col + b * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
-        tmem_ld_wait();
-        if (!full) {
-#pragma unroll
-          for (int u = 0; u < 64; ++u)
-            if (kbase + b * 64 + u > pos) r[u] = __float_as_uint(-INFINITY);
+          for (int u = 0; u < kKeys; ++u)
+            if (kbase + u > pos) r[u] = __float_as_uint(-INFINITY);
         }
+        float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
 #pragma unroll
-        for (int ch = 0; ch < 8; ++ch) {
-          uint32_t pk[4];
+        for (int u = 0; u < kKeys; u += 8) {
+          mx0 = fmaxf(mx0, fmaxf(__uint_as_float(r[u]), __uint_as_float(r[u + 1])));
+          mx1 = fmaxf(mx1, fmaxf(__uint_as_float(r[u + 2]), __uint_as_float(r[u + 3])));
+          mx2 = fmaxf(mx2, fmaxf(__uint_as_float(r[u + 4]), __uint_as_float(r[u + 5])));
+          mx3 = fmaxf(mx3, fmaxf(__uint_as_float(r[u + 6]), __uint_as_float(r[u + 7])));
+        }
+        const float m_new = fmaxf(m_run, fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * scale);
+        if (j == 0) {
+          m_run = m_new;  // O is written (not accumulated) by the first P.V
+        } else {
+          // P_t(j-1) V_{j-1} done: the P buffer is free and O is stable
+          mbar_wait(&o_done[t], (j - 1) & 1);
+          tc_fence_after();
+          const bool need = m_new > m_run + kRescaleLog2;
+          if (__any_sync(0xffffffffu, need)) {
+            const float corr = need ? fast_exp2(m_run - m_new) : 1.0f;
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int i0 = ch * 8 + 2 * u;
-            const float p0 = fast_exp2(fmaf(__uint_as_float(r[i0]), scale, neg_m));
-            const float p1 = fast_exp2(fmaf(__uint_as_float(r[i0 + 1]), scale, neg_m));
-            pk[u] = pack_bf16(p0, p1);
+            for (int c = 0; c < DH; c += 32) {
+              uint32_t o[32];
+              tmem_ld32(o_col + c, o);
+              tmem_ld_wait();
+#pragma unroll
+              for (int u = 0; u < 32; ++u) o[u] = __float_as_uint(__uint_as_float(o[u]) * corr);
+              tmem_st32(o_col + c, o);
+            }
+            const uint32_t l = tmem_ld1(o_col + DH);
+            tmem_ld_wait();
+            tmem_st1(o_col + DH, __float_as_uint(__uint_as_float(l) * corr));
+            tmem_st_wait();
+            if (need) m_run = m_new;
           }
-          uint4* dst = reinterpret_cast<uint4*>(sp + b * (kQ * 128) + rl * 128 + ((ch ^ (rl & 7)) * 16));
-          *dst = make_uint4(pk[0], pk[1], pk[2], pk[3]);
         }
+        // P = exp2(s * scale - m_run) -> bf16, K-major SW128 (2 blocks of 64 keys);
+        // chunks 3 and 7 of each block via the FMA-pipe cubic, the rest on MUFU
+        const float neg_m = m_run == -INFINITY ? 0.f : -m_run;
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+#pragma unroll
+          for (int ch = 0; ch < 8; ++ch) {
+            uint32_t pk[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int i0 = b * 64 + ch * 8 + 2 * u;
+              const float x0 = fmaf(__uint_as_float(r[i0]), scale, neg_m);
+              const float x1 = fmaf(__uint_as_float(r[i0 + 1]), scale, neg_m);
+              if ((ch & 3) == 3) pk[u] = pack_bf16(poly_exp2(x0), poly_exp2(x1));
+              else pk[u] = pack_bf16(fast_exp2(x0), fast_exp2(x1));
+            }
+            uint4* dst = reinterpret_cast<uint4*>(sp + b * (kQ * 128) + rl * 128 + ((ch ^ (rl & 7)) * 16));
+            *dst = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          }
+        }
+        tc_fence_before();
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[t]);
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_free[t]);
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[t]);
-      m_run = m_new;
-      corr_pending = corr;
-    }
-    mbar_wait(&o_full[t], (nk - 1) & 1);
-    tc_fence_after();
-#pragma unroll
-    for (int c = 0; c < DH; c += 32) {
-      uint32_t r[32];
-      tmem_ld32(o_col + c, r);
+      mbar_wait(&o_done[t], (my_nk - 1) & 1);
+      tc_fence_after();
+      uint32_t lb = tmem_ld1(o_col + DH);
       tmem_ld_wait();
+      const float l_run = __uint_as_float(lb);
+      if (a.splits > 1) {
+        const size_t pr = ((size_t)blockIdx.z * a.rows_max + row) * a.H + h;
 #pragma unroll
-      for (int u = 0; u < 32; ++u) acc[c + u] = fmaf(acc[c + u], corr_pending, __uint_as_float(r[u]));
-    }
-    {
-      const uint32_t rs = tmem_ld1(o_col + DH);
-      tmem_ld_wait();
-      l_run = fmaf(l_run, corr_pending, __uint_as_float(rs));
-    }
-    if (valid && a.splits > 1) {
-      const size_t pr = ((size_t)blockIdx.z * a.rows_max + row) * a.H + h;
-      float4* dst = reinterpret_cast<float4*>(a.ws_o + pr * DH);
+        for (int c = 0; c < DH; c += 32) {
+          uint32_t o[32];
+          tmem_ld32(o_col + c, o);
+          tmem_ld_wait();
+          if (valid) {
+            float4* dst = reinterpret_cast<float4*>(a.ws_o + pr * DH + c);
 #pragma unroll
-      for (int c = 0; c < DH; c += 4) dst[c / 4] = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
-      a.ws_ml[pr * 2] = m_run;
-      a.ws_ml[pr * 2 + 1] = l_run;
-    } else if (valid) {
-      const float inv = 1.f / l_run;
-      uint4* dst = reinterpret_cast<uint4*>(a.out + (size_t)row * (a.H * DH) + h * DH);
+            for (int u = 0; u < 32; u += 4)
+              dst[u / 4] = make_float4(__uint_as_float(o[u]), __uint_as_float(o[u + 1]), __uint_as_float(o[u + 2]),
+                                       __uint_as_float(o[u + 3]));
+          }
+        }
+        if (valid) {
+          a.ws_ml[pr * 2] = m_run;
+          a.ws_ml[pr * 2 + 1] = l_run;
+        }
+      } else {
+        const float inv = 1.f / l_run;
+        uint4* dst = reinterpret_cast<uint4*>(a.out + (size_t)row * (a.H * DH) + h * DH);
 #pragma unroll
-      for (int c = 0; c < DH; c += 8) {
-        dst[c / 8] = make_uint4(pack_bf16(acc[c] * inv, acc[c + 1] * inv), pack_bf16(acc[c + 2] * inv, acc[c + 3] * inv),
-                                pack_bf16(acc[c + 4] * inv, acc[c + 5] * inv), pack_bf16(acc[c + 6] * inv, acc[c + 7] * inv));
+        for (int c = 0; c < DH; c += 32) {
+          uint32_t o[32];
+          tmem_ld32(o_col + c, o);
+          tmem_ld_wait();
+          if (valid) {
+#pragma unroll
+            for (int u = 0; u < 32; u += 8)
+              dst[(c + u) / 8] = make_uint4(
+                  pack_bf16(__uint_as_float(o[u]) * inv, __uint_as_float(o[u + 1]) * inv),
+                  pack_bf16(__uint_as_float(o[u + 2]) * inv, __uint_as_float(o[u + 3]) * inv),
+                  pack_bf16(__uint_as_float(o[u + 4]) * inv, __uint_as_float(o[u + 5]) * inv),
+                  pack_bf16(__uint_as_float(o[u + 6]) * inv, __uint_as_float(o[u + 7]) * inv));
+          }
+        }
       }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, C::TMEM_COLS);
+  if (warp == ctl + 1) tmem_dealloc(tmem, C::TMEM_COLS);
 }
 
 // Normalised attention probabilities over a window of segment keys for the
@@ -422,6 +494,12 @@ __global__ void attn_combine_kernel(const AttnArgs a) {
   for (int i = 0; i < PER; i += 2) *reinterpret_cast<uint32_t*>(dst + i) = pack_bf16(o[i] * inv, o[i + 1] * inv);
 }
 
+// Upper bound on query tiles of a launch (row groups split at their bounds).
+int max_tiles(const AttnArgs& a) {
+  const int M = a.rows_max, g1 = std::min(a.g1, M), g2 = std::min(std::max(a.g2, g1), M);
+  return (g1 + kQ - 1) / kQ + (g2 - g1 + kQ - 1) / kQ + (M - g2 + kQ - 1) / kQ;
+}
+
 template <int DH>
 void launch_attn(rk_engine* e, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                  const AttnArgs& a) {
@@ -430,7 +508,7 @@ void launch_attn(rk_engine* e, const CUtensorMap& tq, const CUtensorMap& tk, con
     RK_CUDA(cudaFuncSetAttribute(attn_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, ACfg<DH>::SMEM));
     attr = true;
   }
-  dim3 grid((a.rows_max + kQ * qtiles<DH>() - 1) / (kQ * qtiles<DH>()), a.H, a.splits);
+  dim3 grid((max_tiles(a) + qtiles<DH>() - 1) / qtiles<DH>(), a.H, a.splits);
   attn_kernel<DH><<<grid, threads<DH>(), ACfg<DH>::SMEM, e->stream>>>(tq, tk, tv, a);
   if (a.splits > 1) {
     const int warps = a.rows_max * a.H;
@@ -447,7 +525,7 @@ void attention_bf16(rk_engine* e, const AttnArgs& a_in, const __nv_bfloat16* ctx
   AttnArgs a = a_in;
   // split-KV when the query tiles alone cannot fill the SMs
   const int qt = a.dh == 64 ? qtiles<64>() : qtiles<128>();
-  const int q_tiles = (a.rows_max + kQ * qt - 1) / (kQ * qt);
+  const int q_tiles = (max_tiles(a) + qt - 1) / qt;
   const int base = q_tiles * a.H;
   const int nk_max = (ctx_rows + kKeys - 1) / kKeys;
   a.splits = 1;

@@ -64,18 +64,23 @@ int rk_debug_gemm_bf16(rk_engine* e, const float* A, const float* B, float* C, i
 }
 
 int rk_debug_attention_bf16(rk_engine* e, const float* q, const float* kk, const float* v, const int32_t* pos,
-                            int M, int T, int H, int Hkv, int dh, float* out) {
+                            int M, int live, int g1, int g2, int T, int H, int Hkv, int dh, float* out) {
   return guard([&] {
     cudaStream_t st = e->stream;
     DevBuf qb = to_bf16(st, q, (size_t)M * H * dh), kb = to_bf16(st, kk, (size_t)T * Hkv * dh),
            vb = to_bf16(st, v, (size_t)T * Hkv * dh);
-    DevBuf p(M * 4), o((size_t)M * H * dh * 2), of((size_t)M * H * dh * 4);
+    DevBuf p(M * 4 + 16), o((size_t)M * H * dh * 2), of((size_t)M * H * dh * 4);
     RK_CUDA(cudaMemcpy(p.p, pos, M * 4, cudaMemcpyHostToDevice));
+    RK_CUDA(cudaMemcpy(p.as<int>() + M, &live, 4, cudaMemcpyHostToDevice));
+    RK_CUDA(cudaMemsetAsync(o.p, 0, (size_t)M * H * dh * 2, st));
     AttnArgs a;
     a.q = qb.as<__nv_bfloat16>();
     a.out = o.as<__nv_bfloat16>();
     a.pos = p.as<int>();
     a.rows_max = M;
+    a.rows_dev = live < M ? p.as<int>() + M : nullptr;
+    a.g1 = g1;
+    a.g2 = g2;
     a.H = H;
     a.Hkv = Hkv;
     a.dh = dh;

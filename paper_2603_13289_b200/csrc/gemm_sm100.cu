@@ -52,12 +52,26 @@ struct Units {
   int total;
 };
 
+// Split-K count for the residual epilogue: the s minimising the number of
+// waves per unit of K work, ceil(tiles*s / sms) / s, with a small charge per
+// extra split (each split re-reads and re-writes the output tile in order).
+__host__ __device__ __forceinline__ int best_splits(int tiles, int kb, int sms) {
+  int best = 1;
+  float best_cost = 1e30f;
+  for (int s = 1; s <= 16 && kb / s >= 4; ++s) {
+    const float cost = (float)((tiles * s + sms - 1) / sms) / (float)s * (1.0f + 0.04f * (float)(s - 1));
+    if (cost < best_cost - 1e-6f) { best_cost = cost; best = s; }
+  }
+  return best;
+}
+
 __device__ __forceinline__ Units units_of(const GemmArgs& p) {
   Units u;
   const int M = p.rows_dev ? *p.rows_dev : p.rows_max;
   u.num_m = (M + kBM - 1) / kBM;
   u.num_n = p.N / p.bn;
-  u.splits = p.splits;
+  // live row count known only on the device: pick split-K here (grid = all SMs)
+  u.splits = (p.rows_dev && p.split_flags) ? best_splits(u.num_m * u.num_n, p.K / kBK, p.sms) : p.splits;
   u.kb_total = p.K / kBK;
   u.kb_per = (u.kb_total + u.splits - 1) / u.splits;
   u.total = u.num_m * u.num_n * u.splits;
@@ -324,21 +338,20 @@ void make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t c
   if (r != CUDA_SUCCESS) raise(RK_ERR_RUNTIME, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
 }
 
-// Pick the N tile and split count so the grid fills the SMs.
+// Pick the N tile and split count so the grid fills the SMs. The residual
+// epilogue (split-K capable) always takes the widest tile (BN=256 keeps the
+// SS-MMA under the shared-memory bandwidth) and fills the SMs with K splits.
 static void choose_config(GemmArgs& p, int sm_count, int rows_hint) {
   const int num_m = (rows_hint + kBM - 1) / kBM;
+  p.sms = sm_count;
   int bn = 64;
+  const bool splitk = p.epi == EPI_ADD && p.split_flags;
   for (int cand : {256, 128}) {
-    if (p.N % cand == 0 && num_m * (p.N / cand) >= sm_count) { bn = cand; break; }
+    if (p.N % cand == 0 && (splitk || num_m * (p.N / cand) >= sm_count)) { bn = cand; break; }
   }
   if (p.N % bn) raise(RK_ERR_INVALID_ARGUMENT, "bf16 GEMM needs N % 64 == 0");
   p.bn = bn;
-  p.splits = 1;
-  if (p.epi == EPI_ADD && p.split_flags) {
-    const int tiles = num_m * (p.N / bn);
-    const int kb = p.K / kBK;
-    while (tiles * p.splits * 2 <= sm_count && kb / (p.splits * 2) >= 4) p.splits *= 2;
-  }
+  p.splits = splitk ? best_splits(num_m * (p.N / bn), p.K / kBK, sm_count) : 1;
 }
 
 void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat16* B, GemmArgs p,
@@ -350,7 +363,7 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
   make_tmap_bf16(&ta, A, (uint64_t)p.rows_max, (uint64_t)p.K, kBM, (uint64_t)lda);
   make_tmap_bf16(&tb, B, (uint64_t)p.N, (uint64_t)p.K, (uint32_t)p.bn, (uint64_t)p.K);
   const int num_m = (p.rows_max + kBM - 1) / kBM;
-  const int total = num_m * (p.N / p.bn) * p.splits;
+  const int total = num_m * (p.N / p.bn) * (p.rows_dev && p.split_flags ? 16 : p.splits);
   const int grid = total < e->sm_count ? total : e->sm_count;
   static const char* kEpi[] = {"qkv", "add", "silu", "f32"};
   ProfScope ps(e, (e->prof && e->prof->on)

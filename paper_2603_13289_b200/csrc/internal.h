@@ -163,6 +163,10 @@ struct Rows {
   int rows_max = 0;
   const int* rows_dev = nullptr;
   const int* pos = nullptr;  // int32 [rows_max] absolute positions
+  // Row groups of the fused schedule ([prefix | suffix | segment rows]):
+  // rows [0, g1), [g1, g2), [g2, live). Attention tiles never straddle a
+  // group boundary, so a tile's key range follows its own rows' positions.
+  int g1 = 0, g2 = 0;
 };
 
 // ---- kernel launchers (kernels_*.cu) -------------------------------------
@@ -192,7 +196,8 @@ void mark_rows(cudaStream_t s, uint8_t* origin, int len, int layer_lo, int layer
                const int* count, int rows_max);
 void mark_layers(cudaStream_t s, uint8_t* origin, int len, int layer_lo, int layer_hi);
 void set_depth(cudaStream_t s, uint64_t* depth, int n, uint64_t v);
-void argmax(cudaStream_t s, const float* x, int n, int* out);
+// ws: >= 148 float2 of scratch
+void argmax(cudaStream_t s, const float* x, int n, int* out, void* ws);
 
 // relay (both precisions)
 void realign_graft(cudaStream_t s, const void* k_pre, const void* v_src, size_t elem, int L,

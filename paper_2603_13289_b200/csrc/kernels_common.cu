@@ -8,6 +8,8 @@
 // (-ffp-contract=off, proj/src/CMakeLists.txt:16-18).
 #include <cuda_bf16.h>
 
+#include <algorithm>
+
 #include "internal.h"
 
 namespace rk {
@@ -177,98 +179,113 @@ __global__ void set_depth_kernel(uint64_t* depth, int n, uint64_t v) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) depth[i] = v;
 }
 
-// argmax (model.cpp:364-370): first index of the maximum.
-__global__ void argmax_kernel(const float* x, int n, int* out) {
+// argmax (model.cpp:364-370): first index of the maximum. Two passes: kArgBlocks
+// CTAs reduce strided chunks with 16-byte loads, one CTA merges the partials.
+constexpr int kArgBlocks = 148;
+__device__ __forceinline__ void arg_better(float v, int i, float& bv, int& bi) {
+  if (v > bv || (v == bv && i < bi)) { bv = v; bi = i; }
+}
+__device__ void block_argmax(float& best, int& bi) {
+  __shared__ float sv[32];
+  __shared__ int si[32];
+  for (int o = 16; o; o >>= 1) {
+    const float v = __shfl_xor_sync(0xffffffffu, best, o);
+    const int i = __shfl_xor_sync(0xffffffffu, bi, o);
+    arg_better(v, i, best, bi);
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) { sv[w] = best; si[w] = bi; }
+  __syncthreads();
+  if (w == 0) {
+    best = lane < (int)(blockDim.x >> 5) ? sv[lane] : -__int_as_float(0x7f800000);
+    bi = lane < (int)(blockDim.x >> 5) ? si[lane] : 0x7fffffff;
+    for (int o = 16; o; o >>= 1) {
+      const float v = __shfl_xor_sync(0xffffffffu, best, o);
+      const int i = __shfl_xor_sync(0xffffffffu, bi, o);
+      arg_better(v, i, best, bi);
+    }
+  }
+}
+__global__ void __launch_bounds__(256) argmax_partial_kernel(const float* __restrict__ x, int n,
+                                                             float2* __restrict__ part) {
   float best = -__int_as_float(0x7f800000);
   int bi = 0x7fffffff;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const float v = x[i];
-    if (v > best || (v == best && i < bi)) { best = v; bi = i; }
+  const int n4 = (reinterpret_cast<uintptr_t>(x) & 15) ? 0 : n / 4;
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x) {
+    const float4 v = x4[i];
+    arg_better(v.x, 4 * i, best, bi);
+    arg_better(v.y, 4 * i + 1, best, bi);
+    arg_better(v.z, 4 * i + 2, best, bi);
+    arg_better(v.w, 4 * i + 3, best, bi);
   }
-  __shared__ float sv[1024];
-  __shared__ int si[1024];
-  sv[threadIdx.x] = best;
-  si[threadIdx.x] = bi;
-  __syncthreads();
-  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) {
-      const float v = sv[threadIdx.x + s];
-      const int i = si[threadIdx.x + s];
-      if (v > sv[threadIdx.x] || (v == sv[threadIdx.x] && i < si[threadIdx.x])) {
-        sv[threadIdx.x] = v;
-        si[threadIdx.x] = i;
-      }
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) *out = si[0] == 0x7fffffff ? 0 : si[0];
+  for (int i = 4 * n4 + blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    arg_better(x[i], i, best, bi);
+  block_argmax(best, bi);
+  if (threadIdx.x == 0) part[blockIdx.x] = make_float2(best, __int_as_float(bi));
+}
+__global__ void argmax_final_kernel(const float2* __restrict__ part, int parts, int* out) {
+  float best = -__int_as_float(0x7f800000);
+  int bi = 0x7fffffff;
+  for (int i = threadIdx.x; i < parts; i += blockDim.x)
+    arg_better(part[i].x, __float_as_int(part[i].y), best, bi);
+  block_argmax(best, bi);
+  if (threadIdx.x == 0) *out = bi == 0x7fffffff ? 0 : bi;
 }
 
 // ---------------------------------------------------------------------------
 // K1 realign + graft (relay_cache.cpp:154-174 + relay_engine.cpp:136-148).
-// One CTA owns kPos consecutive segment positions: their double cos/sin rows
-// (host-built with glibc, exactly rope_rotate's) are staged in shared memory
-// once and reused across all L layers and all KV heads. Each thread moves
-// 16-byte vectors: K pairs are rotated in double without FMA then rounded
-// (tensor.cpp:140-141); V is a bit copy. Layers [skip_lo, skip_hi] are
-// skipped (the band recompute overwrites them; relay_engine.cpp:261-264).
+// HBM-bound stream: grid (vector blocks of the segment, grafted layers), one
+// 16-byte vector of K_pre and one of V per thread, both loads issued before
+// any use so every thread keeps 32 B in flight. K pairs are rotated in double
+// without FMA from the host-built glibc cos/sin table (L1/L2-resident), then
+// rounded (tensor.cpp:140-141); V is a bit copy. Layers [skip_lo, skip_hi]
+// are skipped (the band recompute overwrites them; relay_engine.cpp:261-264).
 // ---------------------------------------------------------------------------
 template <typename T>
 __global__ void __launch_bounds__(256) realign_graft_kernel(
-    const T* __restrict__ k_pre, const T* __restrict__ v_src, int L, int n, int kv, int dh,
+    const T* __restrict__ k_pre, const T* __restrict__ v_src, int n, int kv, int dh,
     const double2* __restrict__ rope, int base, T* __restrict__ ctx_k, T* __restrict__ ctx_v,
     size_t ctx_layer_stride, int skip_lo, int skip_hi) {
-  constexpr int kPos = 8;
   constexpr int VEC = 16 / sizeof(T);  // elements per 16-byte vector
-  extern __shared__ double2 cs[];      // [kPos][dh/2]
-  const int p0 = blockIdx.x * kPos;
-  const int npos = min(kPos, n - p0);
-  const int half = dh / 2;
-  for (int i = threadIdx.x; i < npos * half; i += blockDim.x)
-    cs[i] = rope[(size_t)(base + p0 + i / half) * half + (i % half)];
-  __syncthreads();
-  const int vecs_per_row = kv / VEC;
-  const int total = npos * vecs_per_row;
-  for (int l = 0; l < L; ++l) {
-    if (l >= skip_lo && l <= skip_hi) continue;
-    const T* ks = k_pre + (size_t)l * n * kv + (size_t)p0 * kv;
-    const T* vs = v_src + (size_t)l * n * kv + (size_t)p0 * kv;
-    T* kd = ctx_k + (size_t)l * ctx_layer_stride + (size_t)(base + p0) * kv;
-    T* vd = ctx_v + (size_t)l * ctx_layer_stride + (size_t)(base + p0) * kv;
-    for (int t = threadIdx.x; t < total; t += blockDim.x) {
-      const int p = t / vecs_per_row;
-      const int off = (t % vecs_per_row) * VEC;
-      const uint4 kraw = *reinterpret_cast<const uint4*>(ks + (size_t)p * kv + off);
-      const uint4 vraw = *reinterpret_cast<const uint4*>(vs + (size_t)p * kv + off);
-      const T* kin = reinterpret_cast<const T*>(&kraw);
-      uint4 kout_raw;
-      T* kout = reinterpret_cast<T*>(&kout_raw);
+  int l = blockIdx.y;
+  if (skip_hi >= skip_lo && l >= skip_lo) l += skip_hi - skip_lo + 1;
+  const int vpr = kv / VEC;  // vectors per row
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (size_t)n * vpr) return;
+  const int p = (int)(t / vpr);
+  const int off = (int)(t % vpr) * VEC;
+  const size_t src = (size_t)l * n * kv + (size_t)p * kv + off;
+  const uint4 kraw = __ldcs(reinterpret_cast<const uint4*>(k_pre + src));
+  const uint4 vraw = __ldcs(reinterpret_cast<const uint4*>(v_src + src));
+  const size_t dst = (size_t)l * ctx_layer_stride + (size_t)(base + p) * kv + off;
+  *reinterpret_cast<uint4*>(ctx_v + dst) = vraw;
+  const double2* cs = rope + (size_t)(base + p) * (dh / 2);
+  const T* kin = reinterpret_cast<const T*>(&kraw);
+  uint4 kout_raw;
+  T* kout = reinterpret_cast<T*>(&kout_raw);
 #pragma unroll
-      for (int e = 0; e < VEC; e += 2) {
-        const int pair = ((off + e) % dh) / 2;
-        const double2 c_s = cs[p * half + pair];
-        double x0, x1;
-        if constexpr (sizeof(T) == 4) {
-          x0 = (double)kin[e];
-          x1 = (double)kin[e + 1];
-        } else {
-          x0 = (double)__bfloat162float(kin[e]);
-          x1 = (double)__bfloat162float(kin[e + 1]);
-        }
-        const double r0 = __dsub_rn(__dmul_rn(c_s.x, x0), __dmul_rn(c_s.y, x1));
-        const double r1 = __dadd_rn(__dmul_rn(c_s.y, x0), __dmul_rn(c_s.x, x1));
-        if constexpr (sizeof(T) == 4) {
-          kout[e] = __double2float_rn(r0);
-          kout[e + 1] = __double2float_rn(r1);
-        } else {
-          kout[e] = __float2bfloat16_rn(__double2float_rn(r0));
-          kout[e + 1] = __float2bfloat16_rn(__double2float_rn(r1));
-        }
-      }
-      *reinterpret_cast<uint4*>(kd + (size_t)p * kv + off) = kout_raw;
-      *reinterpret_cast<uint4*>(vd + (size_t)p * kv + off) = vraw;
+  for (int e = 0; e < VEC; e += 2) {
+    const double2 c_s = cs[((off + e) % dh) / 2];
+    double x0, x1;
+    if constexpr (sizeof(T) == 4) {
+      x0 = (double)kin[e];
+      x1 = (double)kin[e + 1];
+    } else {
+      x0 = (double)__bfloat162float(kin[e]);
+      x1 = (double)__bfloat162float(kin[e + 1]);
+    }
+    const double r0 = __dsub_rn(__dmul_rn(c_s.x, x0), __dmul_rn(c_s.y, x1));
+    const double r1 = __dadd_rn(__dmul_rn(c_s.y, x0), __dmul_rn(c_s.x, x1));
+    if constexpr (sizeof(T) == 4) {
+      kout[e] = __double2float_rn(r0);
+      kout[e + 1] = __double2float_rn(r1);
+    } else {
+      kout[e] = __float2bfloat16_rn(__double2float_rn(r0));
+      kout[e + 1] = __float2bfloat16_rn(__double2float_rn(r1));
     }
   }
+  *reinterpret_cast<uint4*>(ctx_k + dst) = kout_raw;
 }
 
 // ---------------------------------------------------------------------------
@@ -314,36 +331,58 @@ __device__ double cosine_slice(const void* a, size_t ai, const void* b, size_t b
   return c < -1.0 ? -1.0 : (c > 1.0 ? 1.0 : c);
 }
 
-__global__ void score_kernel(const void* ctx_v, const void* cache_v, const void* ctx_k,
-                             const void* cache_kpre, size_t elem, int n, int kv, int heads, int dh,
-                             const double2* rope, int base, double* s_dev, double* s_key) {
-  extern __shared__ double cosv[];  // [tok][2][heads]
-  const int tok_per_cta = blockDim.x / (2 * heads);
-  const int t = threadIdx.x / (2 * heads);
-  const int which = (threadIdx.x / heads) % 2;  // 0 = V, 1 = K
-  const int h = threadIdx.x % heads;
-  const int j = blockIdx.x * tok_per_cta + t;
-  if (t < tok_per_cta && j < n) {
-    const size_t ai = (size_t)j * kv + h * dh;
+// Copy `bytes` from global to shared with 16-byte vectors when both sides allow.
+__device__ __forceinline__ void stage_bytes(void* dst, const void* src, size_t bytes) {
+  if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst) | bytes) & 15) == 0) {
+    const uint4* s4 = static_cast<const uint4*>(src);
+    uint4* d4 = static_cast<uint4*>(dst);
+    for (size_t i = threadIdx.x; i < bytes / 16; i += blockDim.x) d4[i] = __ldcs(s4 + i);
+  } else {
+    const unsigned short* s2 = static_cast<const unsigned short*>(src);
+    unsigned short* d2 = static_cast<unsigned short*>(dst);
+    for (size_t i = threadIdx.x; i < bytes / 2; i += blockDim.x) d2[i] = s2[i];
+  }
+}
+
+// One CTA scores `tok` consecutive tokens: their four rows (ctx V, cache V,
+// ctx K, cache K_pre) are staged in shared memory with coalesced 16-byte loads
+// (the HBM-bound part), then one thread per (token, head, {V,K}) runs the
+// reference's sequential double loops out of shared memory.
+__global__ void __launch_bounds__(256) score_kernel(const void* ctx_v, const void* cache_v, const void* ctx_k,
+                                                    const void* cache_kpre, size_t elem, int n, int kv, int heads,
+                                                    int dh, const double2* rope, int base, double* s_dev,
+                                                    double* s_key, int tok) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int j0 = blockIdx.x * tok;
+  const int nt = min(tok, n - j0);
+  const size_t row = (size_t)kv * elem, blk = (size_t)tok * row;
+  uint8_t* s_cv = sm;             // ctx V rows
+  uint8_t* s_rv = sm + blk;       // cache V rows
+  uint8_t* s_ck = sm + 2 * blk;   // ctx K rows
+  uint8_t* s_rk = sm + 3 * blk;   // cache K_pre rows
+  double* cosv = reinterpret_cast<double*>(sm + 4 * blk);  // [tok][2][heads]
+  const size_t off = (size_t)j0 * row;
+  stage_bytes(s_cv, static_cast<const uint8_t*>(ctx_v) + off, nt * row);
+  stage_bytes(s_rv, static_cast<const uint8_t*>(cache_v) + off, nt * row);
+  stage_bytes(s_ck, static_cast<const uint8_t*>(ctx_k) + off, nt * row);
+  stage_bytes(s_rk, static_cast<const uint8_t*>(cache_kpre) + off, nt * row);
+  __syncthreads();
+  for (int w = threadIdx.x; w < nt * 2 * heads; w += blockDim.x) {
+    const int t = w / (2 * heads), which = (w / heads) % 2, h = w % heads;
+    const size_t ai = (size_t)t * kv + h * dh;
     double c;
-    if (which == 0) {
-      c = cosine_slice(ctx_v, ai, cache_v, ai, elem, dh, nullptr, false);
-    } else {
-      c = cosine_slice(ctx_k, ai, cache_kpre, ai, elem, dh,
-                       rope + (size_t)(base + j) * (dh / 2), true);
-    }
+    if (which == 0)
+      c = cosine_slice(s_cv, ai, s_rv, ai, elem, dh, nullptr, false);
+    else
+      c = cosine_slice(s_ck, ai, s_rk, ai, elem, dh, rope + (size_t)(base + j0 + t) * (dh / 2), true);
     cosv[(t * 2 + which) * heads + h] = c;
   }
   __syncthreads();
-  if (threadIdx.x < tok_per_cta * 2) {
-    const int tt = threadIdx.x / 2, w = threadIdx.x % 2;
-    const int jj = blockIdx.x * tok_per_cta + tt;
-    if (jj < n) {
-      double acc = 0.0;
-      for (int hh = 0; hh < heads; ++hh) acc = __dadd_rn(acc, cosv[(tt * 2 + w) * heads + hh]);
-      const double dev = __dsub_rn(1.0, __ddiv_rn(acc, (double)heads));
-      (w == 0 ? s_dev : s_key)[jj] = dev;
-    }
+  for (int w = threadIdx.x; w < nt * 2; w += blockDim.x) {
+    const int t = w / 2, which = w % 2;
+    double acc = 0.0;
+    for (int hh = 0; hh < heads; ++hh) acc = __dadd_rn(acc, cosv[(t * 2 + which) * heads + hh]);
+    (which == 0 ? s_dev : s_key)[j0 + t] = __dsub_rn(1.0, __ddiv_rn(acc, (double)heads));
   }
 }
 
@@ -414,16 +453,38 @@ __global__ void __launch_bounds__(1024) select_relay_kernel(
     double* dinfo) {
   __shared__ double thr[2];
   __shared__ int valid[2];
-  if (threadIdx.x == 0) {
-    // mean_relative (selector.cpp:37-39): sequential sum, then divide.
+  if (threadIdx.x < 32) {
+    // mean_relative (selector.cpp:37-39): sequential sum, then divide. Warp 0
+    // loads 4 x 32 values per round (coalesced, all in flight together); the
+    // dependent DADD chain then walks them in index order via shuffles, every
+    // lane computing the identical chain.
+    const int lane = threadIdx.x;
     double mean = 0.0;
-    for (int j = 0; j < n; ++j) mean = __dadd_rn(mean, s_dev[j]);
+    for (int b = 0; b < n; b += 128) {
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = b + u * 32 + lane;
+        v[u] = j < n ? s_dev[j] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int lim = min(32, n - (b + u * 32));
+#pragma unroll 8
+        for (int i = 0; i < 32; ++i) {
+          const double x = __shfl_sync(0xffffffffu, v[u], i);
+          if (i < lim) mean = __dadd_rn(mean, x);
+        }
+      }
+    }
     mean = __ddiv_rn(mean, (double)n);
-    valid[0] = mean > 0.0;
-    thr[0] = __dmul_rn(tau_dev, mean);
-    const double mi = *infl_mean;
-    valid[1] = mi > 0.0;
-    thr[1] = __dmul_rn(tau_inf, mi);
+    if (lane == 0) {
+      valid[0] = mean > 0.0;
+      thr[0] = __dmul_rn(tau_dev, mean);
+      const double mi = *infl_mean;
+      valid[1] = mi > 0.0;
+      thr[1] = __dmul_rn(tau_inf, mi);
+    }
   }
   __syncthreads();
   const int start = suffix_k >= n ? 0 : n - suffix_k;
@@ -570,35 +631,46 @@ void mark_layers(cudaStream_t s, uint8_t* origin, int len, int lo, int hi) {
 void set_depth(cudaStream_t s, uint64_t* depth, int n, uint64_t v) {
   set_depth_kernel<<<blocks_for(n), kThreads, 0, s>>>(depth, n, v);
 }
-void argmax(cudaStream_t s, const float* x, int n, int* out) {
-  argmax_kernel<<<1, 1024, 0, s>>>(x, n, out);
+void argmax(cudaStream_t s, const float* x, int n, int* out, void* ws) {
+  const int g = std::min(kArgBlocks, blocks_for((size_t)(n + 3) / 4));
+  argmax_partial_kernel<<<g, kThreads, 0, s>>>(x, n, static_cast<float2*>(ws));
+  argmax_final_kernel<<<1, kThreads, 0, s>>>(static_cast<const float2*>(ws), g, out);
 }
 
 void realign_graft(cudaStream_t s, const void* k_pre, const void* v_src, size_t elem, int L, int n,
                    int kv, int dh, const double2* rope, int base, void* ctx_k, void* ctx_v,
                    size_t ctx_layer_stride, int skip_lo, int skip_hi) {
-  constexpr int kPos = 8;
-  const int grid = (n + kPos - 1) / kPos;
-  const size_t smem = kPos * (dh / 2) * sizeof(double2);
+  const int skipped = skip_hi >= skip_lo ? skip_hi - skip_lo + 1 : 0;
+  const int layers = L - skipped;
+  if (layers <= 0 || n <= 0) return;
+  const size_t vecs = (size_t)n * (kv * elem / 16);
+  dim3 grid((unsigned)((vecs + 255) / 256), (unsigned)layers);
   if (elem == 4)
-    realign_graft_kernel<float><<<grid, 256, smem, s>>>(
-        (const float*)k_pre, (const float*)v_src, L, n, kv, dh, rope, base, (float*)ctx_k,
+    realign_graft_kernel<float><<<grid, 256, 0, s>>>(
+        (const float*)k_pre, (const float*)v_src, n, kv, dh, rope, base, (float*)ctx_k,
         (float*)ctx_v, ctx_layer_stride, skip_lo, skip_hi);
   else
-    realign_graft_kernel<__nv_bfloat16><<<grid, 256, smem, s>>>(
-        (const __nv_bfloat16*)k_pre, (const __nv_bfloat16*)v_src, L, n, kv, dh, rope, base,
+    realign_graft_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(
+        (const __nv_bfloat16*)k_pre, (const __nv_bfloat16*)v_src, n, kv, dh, rope, base,
         (__nv_bfloat16*)ctx_k, (__nv_bfloat16*)ctx_v, ctx_layer_stride, skip_lo, skip_hi);
 }
 
 void score_deviation(cudaStream_t s, const void* ctx_v, const void* cache_v, const void* ctx_k,
                      const void* cache_kpre, size_t elem, int n, int kv, int heads, int dh,
                      const double2* rope, int base, double* s_dev, double* s_key) {
-  int tok = 128 / (2 * heads);
-  if (tok < 1) tok = 1;
-  const int threads = tok * 2 * heads;
-  const int grid = (n + tok - 1) / tok;
-  score_kernel<<<grid, threads, (size_t)tok * 2 * heads * sizeof(double), s>>>(
-      ctx_v, cache_v, ctx_k, cache_kpre, elem, n, kv, heads, dh, rope, base, s_dev, s_key);
+  if (n <= 0) return;
+  const size_t row = (size_t)kv * elem;
+  int tok = (int)std::min<size_t>(16, std::max<size_t>(1, 40960 / (4 * row)));
+  const size_t smem = 4 * row * tok + (size_t)tok * 2 * heads * sizeof(double);
+  if (smem > 48 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      RK_CUDA(cudaFuncSetAttribute(score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr = true;
+    }
+  }
+  score_kernel<<<(n + tok - 1) / tok, 256, smem, s>>>(ctx_v, cache_v, ctx_k, cache_kpre, elem, n, kv, heads, dh,
+                                                      rope, base, s_dev, s_key, tok);
 }
 
 void select_relay(cudaStream_t s, const double* s_dev, const float* influence,

@@ -124,6 +124,8 @@ void run_layer_bf16(rk_engine* e, rk_weights* w, rk_context* ctx, int l, float* 
   a.pos = rows.pos;
   a.rows_max = rows.rows_max;
   a.rows_dev = rows.rows_dev;
+  a.g1 = rows.g1;
+  a.g2 = rows.g2;
   a.H = s.num_heads;
   a.Hkv = s.num_kv_heads;
   a.dh = s.d_head;

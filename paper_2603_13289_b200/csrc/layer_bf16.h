@@ -14,7 +14,8 @@ struct GemmArgs {
   const int* rows_dev = nullptr;  // live M on the device (sparse passes)
   int N = 0, K = 0;
   int epi = EPI_F32;
-  int bn = 128, splits = 1;     // chosen by gemm_bf16
+  int bn = 128, splits = 1;     // chosen by gemm_bf16 (splits re-chosen on the device for live rows)
+  int sms = 148;
   int* split_flags = nullptr;   // ordered split-K flags (EPI_ADD), zero-initialised
   // outputs
   float* out_f32 = nullptr;     // EPI_ADD / EPI_F32, row stride ld_out
@@ -47,6 +48,7 @@ struct AttnArgs {
   const int* pos = nullptr;          // ascending absolute positions
   int rows_max = 0;
   const int* rows_dev = nullptr;
+  int g1 = 0, g2 = 0;                // row groups [0,g1) [g1,g2) [g2,live) (Rows::g1/g2)
   int H = 0, Hkv = 0, dh = 0;
   float scale_log2 = 0.f;            // log2(e) / sqrt(dh)
   // probability capture for influence (key window [key_lo, key_lo+key_n))

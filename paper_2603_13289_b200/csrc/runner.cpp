@@ -63,7 +63,7 @@ void Runner::ensure_rows(size_t R) {
   S.positions.ensure(std::max<size_t>(R, s.max_positions) * 4);
   S.sub_positions.ensure(64);
   S.logits.ensure(s.vocab_size * 4);
-  S.argmax.ensure(64);
+  S.argmax.ensure(64 + 148 * 8);  // [0] result, +64: argmax partials
   S.seg_hidden_out.ensure(d * 4);
   S.tokens.ensure((s.max_positions + 64) * 4);
 }
@@ -479,8 +479,9 @@ void Runner::agent_prefill(rk_context* ctx, const int32_t* prefix, uint64_t n_pr
       segment_end_logits(ctx, results.back());
     }
   }
-  k::argmax(st_, e_->scratch->logits.as<float>(), (int)w_->s.vocab_size, e_->scratch->argmax.as<int>());
-  e_->launches += 1;
+  k::argmax(st_, e_->scratch->logits.as<float>(), (int)w_->s.vocab_size, e_->scratch->argmax.as<int>(),
+            e_->scratch->argmax.as<char>() + 64);
+  e_->launches += 2;
 }
 
 // ---------------------------------------------------------------------------
@@ -623,6 +624,8 @@ void Runner::agent_fused(rk_context* ctx, const int32_t* prefix, uint64_t P, rk_
     Rows rows{(int)head, nullptr, pos};
     if (segs && l >= l_start && l <= l_det) rows = Rows{(int)(head + segrows), nullptr, pos};
     else if (segs && l > l_det && l <= sparse_hi) rows = Rows{(int)(head + segrows), offs + U, pos};
+    rows.g1 = (int)P;
+    rows.g2 = (int)head;
     run_layer(ctx, (int)l, H, rows, true, (int)total);
     if (segs && l == l_det) {
       ev_band = event();
@@ -799,8 +802,8 @@ rk_cache* Runner::capture_decode(rk_context* ctx, const float* first_logits, uin
   RK_CUDA(cudaMemsetAsync(acc.p, 0, n * 8, st_));
   int* tok = c->tokens.as<int>();
   // greedy_generate (model.cpp:372-389): next = argmax(prompt-end logits)
-  k::argmax(st_, S.logits.as<float>(), (int)V, tok);
-  e_->launches += 1;
+  k::argmax(st_, S.logits.as<float>(), (int)V, tok, S.argmax.as<char>() + 64);
+  e_->launches += 2;
   for (uint64_t t = 0; t < n; ++t) {
     const uint64_t pos = src + t;
     ctx->resize(pos + 1);
@@ -820,8 +823,8 @@ rk_cache* Runner::capture_decode(rk_context* ctx, const float* first_logits, uin
     }
     if (t + 1 < n) {
       last_row_logits(S.hidden.as<float>());
-      k::argmax(st_, S.logits.as<float>(), (int)V, tok + t + 1);
-      e_->launches += 1;
+      k::argmax(st_, S.logits.as<float>(), (int)V, tok + t + 1, S.argmax.as<char>() + 64);
+      e_->launches += 2;
     }
   }
   k::doubles_to_floats(st_, c->influence.as<float>(), acc.as<double>(), (int)n);

@@ -90,19 +90,24 @@ def ref_attention(q, k, v, pos, H, Hkv, dh):
 
 ATT = [(64, 200, 4, 2, 64, "band"), (300, 700, 8, 2, 64, "sparse"), (130, 1000, 4, 4, 128, "band"),
        (1, 333, 4, 1, 128, "band"), (257, 1500, 32, 8, 64, "sparse"), (320, 4032, 32, 8, 64, "mixed"),
-       (700, 2000, 16, 4, 128, "mixed")]
+       (700, 2000, 16, 4, 128, "mixed"), (1356, 4032, 32, 8, 64, "mixed"), (900, 3000, 8, 2, 64, "live"),
+       (600, 2500, 8, 4, 128, "live"), (4032, 4032, 32, 8, 64, "band"), (2048, 4096, 8, 2, 128, "band")]
 
 
 @pytest.mark.parametrize("case", ATT, ids=[f"{c[5]}-M{c[0]}-T{c[1]}-dh{c[4]}" for c in ATT])
 def test_attention(engine, case):
     M, T, H, Hkv, dh, kind = case
     rng = np.random.default_rng(M + T)
+    live, g1, g2 = M, 0, 0
     if kind == "band":
         pos = np.arange(T - M, T, dtype=np.int32)
-    elif kind == "mixed":  # fused-schedule layout: [prefix | suffix | segment rows], unsorted
+    elif kind in ("mixed", "live"):  # fused-schedule layout: [prefix | suffix | segment rows], unsorted
         n_pre, n_suf = M // 4, M // 8
         seg = np.sort(rng.choice(np.arange(n_pre, T - n_suf), M - n_pre - n_suf, replace=False))
         pos = np.concatenate([np.arange(n_pre), np.arange(T - n_suf, T), seg]).astype(np.int32)
+        g1, g2 = n_pre, n_pre + n_suf
+        if kind == "live":  # sparse pass: only the first `live` rows exist
+            live = g2 + (M - g2) // 3
     else:
         pos = np.sort(rng.choice(T, M, replace=False)).astype(np.int32)
     q = rng.standard_normal((M, H * dh)).astype(np.float32)
@@ -111,10 +116,11 @@ def test_attention(engine, case):
     out = np.zeros((M, H * dh), np.float32)
     _check(lib().rk_debug_attention_bf16(P(engine.ptr), q.ctypes.data_as(F32P), k.ctypes.data_as(F32P),
                                          v.ctypes.data_as(F32P), pos.ctypes.data_as(C.POINTER(C.c_int32)),
-                                         M, T, H, Hkv, dh, out.ctypes.data_as(F32P)))
-    ref = ref_attention(q, k, v, pos, H, Hkv, dh)
-    err = np.abs(out - ref).max()
+                                         M, live, g1, g2, T, H, Hkv, dh, out.ctypes.data_as(F32P)))
+    ref = ref_attention(q[:live], k, v, pos[:live], H, Hkv, dh)
+    err = np.abs(out[:live] - ref).max()
     assert err < 3e-2, f"max abs err {err}"
+    assert (out[live:] == 0).all(), "rows beyond the live count were written"
 
 
 def test_device_expf_matches_host_libm(engine):
