@@ -9,7 +9,7 @@
 //
 // One CTA = up to kQT query tiles (128 rows each) x one head, flash-style over
 // 128-key tiles:
-//   warp 0      TMA: Q tiles once; K_j and V_j into a 2-stage ring
+//   TMA warps   Q tiles once; K_j into a 3-stage ring, V_j into a 2-stage ring
 //   warp 1      TMEM alloc + MMA issue: S_t(j+1) = Q_t K_{j+1}^T -> TMEM as soon
 //               as softmax t has pulled S_t(j) into registers, then
 //               O_t += P_t(j) [V_j | 1] -> TMEM (accumulated across key tiles)
@@ -40,15 +40,24 @@ __device__ __forceinline__ float fast_exp2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// 2^x on the FMA pipe: round-to-nearest split x = n + f (f in [-0.5, 0.5]),
-// minimax cubic for 2^f (max rel. err 7.5e-5, far below bf16's 2^-9), n added
-// straight into the exponent. Valid for x <= 64; clamps far below underflow.
-__device__ __forceinline__ float poly_exp2(float x) {
-  x = fmaxf(x, -127.0f);
-  const float t = x + 12582912.0f;  // 1.5 * 2^23: integer part lands in the low mantissa bits
-  const float f = x - (t - 12582912.0f);
-  const float p = fmaf(fmaf(fmaf(0.05517166f, f, 0.24261115f), f, 0.69326097f), f, 0.99992806f);
-  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+// 2^x for a pair on the FMA pipe (FADD2/FFMA2): round-to-nearest split
+// x = n + f (f in [-0.5, 0.5]), minimax cubic for 2^f (max rel. err 7.5e-5,
+// far below bf16's 2^-9), n added straight into the exponent bits. Valid for
+// x <= 64; x is clamped at -125 so p * 2^n stays a normal float.
+__device__ __forceinline__ uint32_t poly_exp2_bf16x2(float x0, float x1) {
+  constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: integer part lands in the low mantissa bits
+  x0 = fmaxf(x0, -125.0f);
+  x1 = fmaxf(x1, -125.0f);
+  float t0, t1, r0, r1, f0, f1, p0, p1;
+  add2(t0, t1, x0, x1, kMagic, kMagic);
+  sub2(r0, r1, t0, t1, kMagic, kMagic);
+  sub2(f0, f1, x0, x1, r0, r1);
+  fma2(p0, p1, f0, f1, 0.05517166f, 0.05517166f, 0.24261115f, 0.24261115f);
+  fma2(p0, p1, p0, p1, f0, f1, 0.69326097f, 0.69326097f);
+  fma2(p0, p1, p0, p1, f0, f1, 0.99992806f, 0.99992806f);
+  const float e0 = __int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23));
+  const float e1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
+  return pack_bf16(e0, e1);
 }
 
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
@@ -81,14 +90,20 @@ struct ACfg {
   static constexpr int Q_TILE = kQ * DH * 2;
   static constexpr int KV_BYTES = kKeys * DH * 2;  // one of K or V
   static constexpr int ONES_BYTES = kKeys * 128;   // 64-wide block of ones after V: P.[V|1] gives row sums
-  static constexpr int STAGE_BYTES = 2 * KV_BYTES + ONES_BYTES;
+  // K and V stream through separate rings: K_j is free once S(j) is done, V_j
+  // only after P(j).V_j, so K runs further ahead (TMA latency off the path)
+  static constexpr int KST = DH == 64 ? 3 : 2;
+  static constexpr int VST = 2;
+  static constexpr int V_STAGE = KV_BYTES + ONES_BYTES;
   static constexpr int ON = DH + 16;               // PV MMA N: DH value columns + 16 ones columns
   static constexpr int P_BYTES = kQ * kKeys * 2;
   static constexpr int OFF_Q = 0;
-  static constexpr int OFF_KV = kQT * Q_TILE;
-  static constexpr int OFF_P = OFF_KV + 2 * STAGE_BYTES;
+  static constexpr int OFF_K = kQT * Q_TILE;
+  static constexpr int OFF_V = OFF_K + KST * KV_BYTES;
+  static constexpr int OFF_P = OFF_V + VST * V_STAGE;
   static constexpr int OFF_BAR = OFF_P + kQT * P_BYTES;
   static constexpr int SMEM = OFF_BAR + 512 + 1024;
+  static_assert(SMEM + 64 <= 232448, "shared memory per CTA");
   static constexpr uint32_t TMEM_COLS = 512;
   // TMEM columns: S_t at t*128, O_t (DH values + row-sum column) at 256 + t*128
   static constexpr uint32_t S_COL = 0, O_COL = 256;
@@ -121,13 +136,15 @@ __global__ void __launch_bounds__(threads<DH>(), 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* q_full = bar + 0;
-  uint64_t* kv_full = bar + 1;   // [2]
-  uint64_t* kv_empty = bar + 3;  // [2]
-  uint64_t* s_full = bar + 5;    // [kQT]
-  uint64_t* s_free = bar + 7;    // [kQT]
-  uint64_t* p_full = bar + 9;    // [kQT]
-  uint64_t* o_done = bar + 11;   // [kQT]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+  uint64_t* k_full = bar + 1;    // [KST <= 3]
+  uint64_t* k_empty = bar + 4;   // [KST]
+  uint64_t* v_full = bar + 7;    // [VST = 2]
+  uint64_t* v_empty = bar + 9;   // [VST]
+  uint64_t* s_full = bar + 11;   // [kQT]
+  uint64_t* s_free = bar + 13;   // [kQT]
+  uint64_t* p_full = bar + 15;   // [kQT]
+  uint64_t* o_done = bar + 17;   // [kQT]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 24);
   __shared__ int s_kmax[kQT];
 
   const int M = a.rows_dev ? *a.rows_dev : a.rows_max;
@@ -169,9 +186,13 @@ __global__ void __launch_bounds__(threads<DH>(), 1)
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
     mbar_init(q_full, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&kv_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
+    for (int i = 0; i < C::KST; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+    }
+    for (int i = 0; i < C::VST; ++i) {
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
     }
     for (int t = 0; t < kQT; ++t) {
       mbar_init(&s_full[t], 1);
@@ -182,8 +203,8 @@ __global__ void __launch_bounds__(threads<DH>(), 1)
     fence_barrier_init();
   }
   if (warp == ctl + 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
-  for (int st = 0; st < 2; ++st) {  // the constant ones block of each K/V stage
-    uint4* ones = reinterpret_cast<uint4*>(smem + C::OFF_KV + st * C::STAGE_BYTES + 2 * C::KV_BYTES);
+  for (int st = 0; st < C::VST; ++st) {  // the constant ones block of each V stage
+    uint4* ones = reinterpret_cast<uint4*>(smem + C::OFF_V + st * C::V_STAGE + C::KV_BYTES);
     for (int i = threadIdx.x; i < C::ONES_BYTES / 16; i += blockDim.x) ones[i] = make_uint4(0x3f803f80u, 0x3f803f80u, 0x3f803f80u, 0x3f803f80u);
   }
   fence_proxy_async();
@@ -206,16 +227,24 @@ __global__ void __launch_bounds__(threads<DH>(), 1)
         if (nk[t] > 0)
           for (int b = 0; b < DB; ++b)
             tma_load_2d(sq + t * C::Q_TILE + b * kQ * 128, &tmQ, q_full, h * DH + b * 64, r0[t]);
+      for (int j = 0; j < nk_all; ++j) {  // K ring
+        const int st = j % C::KST;
+        mbar_wait(&k_empty[st], ((j / C::KST) & 1) ^ 1);
+        uint8_t* sk = smem + C::OFF_K + st * C::KV_BYTES;
+        mbar_arrive_expect_tx(&k_full[st], C::KV_BYTES);
+        for (int b = 0; b < DB; ++b)
+          tma_load_2d(sk + b * kKeys * 128, &tmK, &k_full[st], kvh * DH + b * 64, (j0 + j) * kKeys);
+      }
+    }
+  } else if (warp == ctl + 2) {
+    if (elect_one()) {  // --------------------------------------------- TMA V
       for (int j = 0; j < nk_all; ++j) {
-        const int st = j & 1;
-        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
-        uint8_t* sk = smem + C::OFF_KV + st * C::STAGE_BYTES;
-        uint8_t* sv = sk + C::KV_BYTES;
-        mbar_arrive_expect_tx(&kv_full[st], 2 * C::KV_BYTES);
-        for (int b = 0; b < DB; ++b) {
-          tma_load_2d(sk + b * kKeys * 128, &tmK, &kv_full[st], kvh * DH + b * 64, (j0 + j) * kKeys);
-          tma_load_2d(sv + b * kKeys * 128, &tmV, &kv_full[st], kvh * DH + b * 64, (j0 + j) * kKeys);
-        }
+        const int st = j % C::VST;
+        mbar_wait(&v_empty[st], ((j / C::VST) & 1) ^ 1);
+        uint8_t* sv = smem + C::OFF_V + st * C::V_STAGE;
+        mbar_arrive_expect_tx(&v_full[st], C::KV_BYTES);
+        for (int b = 0; b < DB; ++b)
+          tma_load_2d(sv + b * kKeys * 128, &tmV, &v_full[st], kvh * DH + b * 64, (j0 + j) * kKeys);
       }
     }
   } else if (warp == ctl + 1) {
@@ -224,11 +253,11 @@ __global__ void __launch_bounds__(threads<DH>(), 1)
       constexpr uint32_t idesc_o = idesc_bf16(kQ, C::ON, /*b_mn_major=*/true);
       mbar_wait(q_full, 0);
       auto issue_s = [&](int j, int t) {
-        const int st = j & 1;
+        const int st = j % C::KST;
         mbar_wait(&s_free[t], (j & 1) ^ 1);
         tc_fence_after();
         const uint32_t sq = smem_u32(smem + C::OFF_Q + t * C::Q_TILE);
-        const uint32_t sk = smem_u32(smem + C::OFF_KV + st * C::STAGE_BYTES);
+        const uint32_t sk = smem_u32(smem + C::OFF_K + st * C::KV_BYTES);
 #pragma unroll
         for (int k = 0; k < DH / 16; ++k) {
           const uint32_t off = (k >> 2) * (kQ * 128) + (k & 3) * 32;
@@ -239,11 +268,11 @@ __global__ void __launch_bounds__(threads<DH>(), 1)
         tc_commit(&s_full[t]);
       };
       auto issue_pv = [&](int j, int t) {
-        const int st = j & 1;
+        const int st = j % C::VST;
         mbar_wait(&p_full[t], j & 1);
         tc_fence_after();
         const uint32_t sp = smem_u32(smem + C::OFF_P + t * C::P_BYTES);
-        const uint32_t sv = smem_u32(smem + C::OFF_KV + st * C::STAGE_BYTES + C::KV_BYTES);
+        const uint32_t sv = smem_u32(smem + C::OFF_V + st * C::V_STAGE);
 #pragma unroll
         for (int k = 0; k < kKeys / 16; ++k) {
           const uint64_t ad = sdesc_sw128(sp + (k >> 2) * (kQ * 128) + (k & 3) * 32, 16, 1024);
@@ -255,16 +284,25 @@ __global__ void __launch_bounds__(threads<DH>(), 1)
       // S_t(j+1) goes in as soon as softmax t has S_t(j) in registers, ahead of
       // P_t(j) V_j, so the tensor pipe computes the next scores while the
       // softmax warpgroups exponentiate the current ones.
-      mbar_wait(&kv_full[0], 0);
+      mbar_wait(&k_full[0], 0);
+      tc_fence_after();
       for (int t = 0; t < kQT; ++t)
         if (nk[t] > 0) issue_s(0, t);
+      tc_commit(&k_empty[0]);
       for (int j = 0; j < nk_all; ++j) {
-        if (j + 1 < nk_all) mbar_wait(&kv_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
-        for (int t = 0; t < kQT; ++t)
-          if (j + 1 < nk[t]) issue_s(j + 1, t);
+        if (j + 1 < nk_all) {
+          const int jk = j + 1;
+          mbar_wait(&k_full[jk % C::KST], (jk / C::KST) & 1);
+          tc_fence_after();
+          for (int t = 0; t < kQT; ++t)
+            if (jk < nk[t]) issue_s(jk, t);
+          tc_commit(&k_empty[jk % C::KST]);
+        }
+        mbar_wait(&v_full[j % C::VST], (j / C::VST) & 1);
+        tc_fence_after();
         for (int t = 0; t < kQT; ++t)
           if (j < nk[t]) issue_pv(j, t);
-        tc_commit(&kv_empty[j & 1]);
+        tc_commit(&v_empty[j % C::VST]);
       }
     }
   }
@@ -276,6 +314,12 @@ __global__ void __launch_bounds__(threads<DH>(), 1)
     const int row = r0[t] + rl;
     const bool valid = row < r1[t];
     const int my_nk = nk[t];
+    // Ping-pong (kQT == 2): the exponentiation phases of the two warpgroups
+    // alternate through named barriers 8/9, so one group's exp2 burst runs
+    // while the other waits on its P.V and loads its next scores. Every group
+    // takes nk_all turns (idle turns just pass the token); group 0 goes first.
+    constexpr uint32_t kTurn = 8;
+    if (kQT == 2 && t == 1) named_bar_arrive(kTurn, 256);
     if (my_nk <= 0) {  // this tile has no keys in this split
       if (valid && a.splits > 1) {
         float* ml = a.ws_ml + (((size_t)blockIdx.z * a.rows_max + row) * a.H + h) * 2;
@@ -346,6 +390,7 @@ __global__ void __launch_bounds__(threads<DH>(), 1)
         // P = exp2(s * scale - m_run) -> bf16, K-major SW128 (2 blocks of 64 keys);
         // chunks 3 and 7 of each block via the FMA-pipe cubic, the rest on MUFU
         const float neg_m = m_run == -INFINITY ? 0.f : -m_run;
+        if (kQT == 2) named_bar_sync(kTurn + t, 256);
 #pragma unroll
         for (int b = 0; b < 2; ++b) {
 #pragma unroll
@@ -354,9 +399,9 @@ __global__ void __launch_bounds__(threads<DH>(), 1)
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
               const int i0 = b * 64 + ch * 8 + 2 * u;
-              const float x0 = fmaf(__uint_as_float(r[i0]), scale, neg_m);
-              const float x1 = fmaf(__uint_as_float(r[i0 + 1]), scale, neg_m);
-              if ((ch & 3) == 3) pk[u] = pack_bf16(poly_exp2(x0), poly_exp2(x1));
+              float x0, x1;
+              fma2(x0, x1, __uint_as_float(r[i0]), __uint_as_float(r[i0 + 1]), scale, scale, neg_m, neg_m);
+              if ((ch & 3) == 3) pk[u] = poly_exp2_bf16x2(x0, x1);
               else pk[u] = pack_bf16(fast_exp2(x0), fast_exp2(x1));
             }
             uint4* dst = reinterpret_cast<uint4*>(sp + b * (kQ * 128) + rl * 128 + ((ch ^ (rl & 7)) * 16));
@@ -367,6 +412,7 @@ __global__ void __launch_bounds__(threads<DH>(), 1)
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[t]);
+        if (kQT == 2) named_bar_arrive(kTurn + (t ^ 1), 256);
       }
       mbar_wait(&o_done[t], (my_nk - 1) & 1);
       tc_fence_after();
@@ -411,6 +457,13 @@ __global__ void __launch_bounds__(threads<DH>(), 1)
           }
         }
       }
+    }
+    if (kQT == 2) {
+      for (int j = my_nk > 0 ? my_nk : 0; j < nk_all; ++j) {  // idle turns
+        named_bar_sync(kTurn + t, 256);
+        named_bar_arrive(kTurn + (t ^ 1), 256);
+      }
+      if (t == 0) named_bar_sync(kTurn, 256);  // group 1's last pass
     }
   }
   tc_fence_before();

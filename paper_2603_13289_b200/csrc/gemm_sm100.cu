@@ -52,17 +52,14 @@ struct Units {
   int total;
 };
 
-// Split-K count for the residual epilogue: the s minimising the number of
-// waves per unit of K work, ceil(tiles*s / sms) / s, with a small charge per
-// extra split (each split re-reads and re-writes the output tile in order).
+// Split-K count for the residual epilogue: splits double while the grid is
+// still under half the SMs (every split re-reads and re-writes the fp32
+// output tile in split order, so splitting a grid that already fills the SMs
+// only adds traffic).
 __host__ __device__ __forceinline__ int best_splits(int tiles, int kb, int sms) {
-  int best = 1;
-  float best_cost = 1e30f;
-  for (int s = 1; s <= 16 && kb / s >= 4; ++s) {
-    const float cost = (float)((tiles * s + sms - 1) / sms) / (float)s * (1.0f + 0.04f * (float)(s - 1));
-    if (cost < best_cost - 1e-6f) { best_cost = cost; best = s; }
-  }
-  return best;
+  int s = 1;
+  while (tiles * s * 2 <= sms && kb / (s * 2) >= 4) s *= 2;
+  return s;
 }
 
 __device__ __forceinline__ Units units_of(const GemmArgs& p) {
@@ -71,7 +68,7 @@ __device__ __forceinline__ Units units_of(const GemmArgs& p) {
   u.num_m = (M + kBM - 1) / kBM;
   u.num_n = p.N / p.bn;
   // live row count known only on the device: pick split-K here (grid = all SMs)
-  u.splits = (p.rows_dev && p.split_flags) ? best_splits(u.num_m * u.num_n, p.K / kBK, p.sms) : p.splits;
+  u.splits = (p.rows_dev && p.split_flags && p.epi == EPI_ADD) ? best_splits(u.num_m * u.num_n, p.K / kBK, p.sms) : p.splits;
   u.kb_total = p.K / kBK;
   u.kb_per = (u.kb_total + u.splits - 1) / u.splits;
   u.total = u.num_m * u.num_n * u.splits;
@@ -254,8 +251,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       int mt, nt, s;
       decode_unit(U, unit, mt, nt, s);
       const int acc = local & 1;
-      mbar_wait(&tfull[acc], (local >> 1) & 1);
-      tc_fence_after();
       const int row = mt * kBM + quarter * 32 + lane;
       int* flag = nullptr;
       if (EPI == EPI_ADD && U.splits > 1) {  // ordered split-K: wait for split s-1 on these rows
@@ -265,12 +260,53 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         __threadfence();
       }
+      if constexpr (EPI == EPI_ADD) {
+        // residual rows are read through a 4-chunk register ring issued before
+        // the accumulator is even ready, so the load latency overlaps the MMAs
+        constexpr int NCH = BN / 32, D = NCH < 4 ? NCH : 4;
+        const bool live = row < M;
+        float4* hrow = reinterpret_cast<float4*>(p.out_f32 + (size_t)(live ? row : 0) * p.ld_out + nt * BN);
+        float4 hb[D][8];
+#pragma unroll
+        for (int c = 0; c < D; ++c)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) hb[c][j] = live ? __ldcg(hrow + c * 8 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+        mbar_wait(&tfull[acc], (local >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+          uint32_t r[32];
+          tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN + c * 32, r);
+          tmem_ld_wait();
+          float4 cur[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) cur[j] = hb[c % D][j];
+          if (c + D < NCH && live) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) hb[c % D][j] = __ldcg(hrow + (c + D) * 8 + j);
+          }
+          if (live) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              float4 h = cur[j];
+              h.x += __uint_as_float(r[4 * j]);
+              h.y += __uint_as_float(r[4 * j + 1]);
+              h.z += __uint_as_float(r[4 * j + 2]);
+              h.w += __uint_as_float(r[4 * j + 3]);
+              hrow[c * 8 + j] = h;
+            }
+          }
+        }
+      } else {
+        mbar_wait(&tfull[acc], (local >> 1) & 1);
+        tc_fence_after();
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        uint32_t r[32];
-        tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN + c, r);
-        tmem_ld_wait();
-        if (row < M) epilogue_chunk<EPI>(p, row, nt * BN + c, r);
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t r[32];
+          tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN + c, r);
+          tmem_ld_wait();
+          if (row < M) epilogue_chunk<EPI>(p, row, nt * BN + c, r);
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -338,19 +374,19 @@ void make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t c
   if (r != CUDA_SUCCESS) raise(RK_ERR_RUNTIME, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
 }
 
-// Pick the N tile and split count so the grid fills the SMs. The residual
-// epilogue (split-K capable) always takes the widest tile (BN=256 keeps the
-// SS-MMA under the shared-memory bandwidth) and fills the SMs with K splits.
+// Pick the N tile and split count so the grid fills the SMs: the widest tile
+// that still gives a full wave, else BN=64; split-K only while the grid is
+// under half the SMs (split_flags present, residual epilogue).
 static void choose_config(GemmArgs& p, int sm_count, int rows_hint) {
   const int num_m = (rows_hint + kBM - 1) / kBM;
   p.sms = sm_count;
   int bn = 64;
-  const bool splitk = p.epi == EPI_ADD && p.split_flags;
   for (int cand : {256, 128}) {
-    if (p.N % cand == 0 && (splitk || num_m * (p.N / cand) >= sm_count)) { bn = cand; break; }
+    if (p.N % cand == 0 && num_m * (p.N / cand) >= sm_count) { bn = cand; break; }
   }
   if (p.N % bn) raise(RK_ERR_INVALID_ARGUMENT, "bf16 GEMM needs N % 64 == 0");
   p.bn = bn;
+  const bool splitk = p.epi == EPI_ADD && p.split_flags;
   p.splits = splitk ? best_splits(num_m * (p.N / bn), p.K / kBK, sm_count) : 1;
 }
 
@@ -363,7 +399,7 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
   make_tmap_bf16(&ta, A, (uint64_t)p.rows_max, (uint64_t)p.K, kBM, (uint64_t)lda);
   make_tmap_bf16(&tb, B, (uint64_t)p.N, (uint64_t)p.K, (uint32_t)p.bn, (uint64_t)p.K);
   const int num_m = (p.rows_max + kBM - 1) / kBM;
-  const int total = num_m * (p.N / p.bn) * (p.rows_dev && p.split_flags ? 16 : p.splits);
+  const int total = num_m * (p.N / p.bn) * (p.rows_dev && p.split_flags && p.epi == EPI_ADD ? 16 : p.splits);
   const int grid = total < e->sm_count ? total : e->sm_count;
   static const char* kEpi[] = {"qkv", "add", "silu", "f32"};
   ProfScope ps(e, (e->prof && e->prof->on)

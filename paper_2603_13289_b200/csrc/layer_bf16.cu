@@ -87,7 +87,8 @@ void run_layer_bf16(rk_engine* e, rk_weights* w, rk_context* ctx, int l, float* 
   auto* act = S.act.as<__nv_bfloat16>();
   auto* ck = static_cast<__nv_bfloat16*>(ctx->k_layer(l));
   auto* cv = static_cast<__nv_bfloat16*>(ctx->v_layer(l));
-  const int hint = rows.rows_dev ? std::max(1, rows.rows_max / 4) : rows.rows_max;
+  // live rows of a sparse pass are known only on the device: plan tiles for ~1/3
+  const int hint = rows.rows_dev ? std::max(1, rows.rows_max / 3) : rows.rows_max;
   int* flags = split_flags(e);
   __nv_bfloat16* save = reinterpret_cast<__nv_bfloat16*>(S.seg_hidden_out.as<char>() + 0);
   if (!commit) {

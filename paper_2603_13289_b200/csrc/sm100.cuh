@@ -30,25 +30,27 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// try_wait with a suspend hint: the warp sleeps in hardware (NANOSLEEP.SYNCS)
+// until the barrier changes instead of spinning on issue slots.
 __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
       "selp.u32 %0, 1, 0, p;\n"
       "}\n"
       : "=r"(ok)
-      : "r"(addr), "r"(parity)
+      : "r"(addr), "r"(parity), "r"(0x989680)
       : "memory");
   return ok != 0;
 }
-// Blocking wait; a pipeline bug traps (~seconds) instead of hanging the GPU.
+// Blocking wait; a pipeline bug traps (after ~seconds) instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   uint32_t spins = 0;
   while (!mbar_try_wait(addr, parity)) {
-    if (++spins > (1u << 24)) __trap();
+    if (++spins > (1u << 20)) __trap();
   }
 }
 
@@ -155,6 +157,30 @@ __device__ __forceinline__ bool elect_one() {
 
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(uint32_t id, uint32_t threads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+// Packed fp32x2 arithmetic (FFMA2 / FADD2 on sm_100): two lanes per issue slot.
+__device__ __forceinline__ void fma2(float& y0, float& y1, float x0, float x1, float a0, float a1, float b0,
+                                     float b1) {
+  asm("{\n.reg .b64 xa, aa, ba, da;\nmov.b64 xa, {%2, %3};\nmov.b64 aa, {%4, %5};\nmov.b64 ba, {%6, %7};\n"
+      "fma.rn.f32x2 da, xa, aa, ba;\nmov.b64 {%0, %1}, da;\n}"
+      : "=f"(y0), "=f"(y1)
+      : "f"(x0), "f"(x1), "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+__device__ __forceinline__ void add2(float& y0, float& y1, float x0, float x1, float a0, float a1) {
+  asm("{\n.reg .b64 xa, aa, da;\nmov.b64 xa, {%2, %3};\nmov.b64 aa, {%4, %5};\nadd.rn.f32x2 da, xa, aa;\n"
+      "mov.b64 {%0, %1}, da;\n}"
+      : "=f"(y0), "=f"(y1)
+      : "f"(x0), "f"(x1), "f"(a0), "f"(a1));
+}
+__device__ __forceinline__ void sub2(float& y0, float& y1, float x0, float x1, float a0, float a1) {
+  asm("{\n.reg .b64 xa, aa, da;\nmov.b64 xa, {%2, %3};\nmov.b64 aa, {%4, %5};\nsub.rn.f32x2 da, xa, aa;\n"
+      "mov.b64 {%0, %1}, da;\n}"
+      : "=f"(y0), "=f"(y1)
+      : "f"(x0), "f"(x1), "f"(a0), "f"(a1));
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
