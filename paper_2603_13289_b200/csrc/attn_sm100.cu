@@ -7,23 +7,25 @@
 // any ascending subset of positions (dense band or gathered sparse rows), so
 // the causal limit is per row, by absolute position.
 //
-// One CTA = up to kQT query tiles (128 rows each) x one head, flash-style over
-// 128-key tiles:
-//   TMA warps   Q tiles once; K_j into a 3-stage ring, V_j into a 2-stage ring
-//   warp 1      TMEM alloc + MMA issue: S_t(j+1) = Q_t K_{j+1}^T -> TMEM as soon
-//               as softmax t has pulled S_t(j) into registers, then
-//               O_t += P_t(j) [V_j | 1] -> TMEM (accumulated across key tiles)
-//   warps 2..   one softmax warpgroup per query tile, one row per thread:
-//               S into registers (TMEM freed at once), scale + causal mask, row
-//               max, lazy rescale of O in TMEM only when the max grows by more
-//               than 2^8, P = exp2(.) (MUFU + a cubic on the FMA pipe for a
-//               quarter of the columns) as bf16 into swizzled smem.
-// The row sum l rides along as the ones column of [V | 1]. Query tiles never
-// straddle a row group (prefix / suffix / segment rows of the fused schedule),
-// and each tile stops at its own last key tile.
+// One CTA = one query tile (128 rows) x one head, flash-style over 128-key
+// tiles; d_head 64 fits two CTAs per SM (112 KB smem, 256 TMEM columns each),
+// so one CTA's exponentials overlap the other's MMAs, loads and epilogue.
+//   warp 4      TMA: K_j into a 2-stage ring
+//   warp 6      TMA: Q once, V_j into a 2-stage ring
+//   warp 5      TMEM alloc + MMA issue: S(j+1) = Q K_{j+1}^T -> TMEM as soon
+//               as the softmax has pulled S(j) into registers, then
+//               O += P(j) V_j -> TMEM (accumulated across key tiles)
+//   warps 0-3   softmax, one row per thread: S into registers (TMEM freed at
+//               once), scale + causal mask, row max, lazy rescale of O in TMEM
+//               only when the max grows by more than 2^8, P = exp2(.) (MUFU +
+//               a cubic on the FMA pipe for a quarter of the columns) as bf16
+//               into swizzled smem, row sum l in registers.
+// Query tiles never straddle a row group (prefix / suffix / segment rows of
+// the fused schedule), and each tile stops at its own last key tile.
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "internal.h"
 #include "layer_bf16.h"
@@ -44,7 +46,7 @@ __device__ __forceinline__ float fast_exp2(float x) {
 // x = n + f (f in [-0.5, 0.5]), minimax cubic for 2^f (max rel. err 7.5e-5,
 // far below bf16's 2^-9), n added straight into the exponent bits. Valid for
 // x <= 64; x is clamped at -125 so p * 2^n stays a normal float.
-__device__ __forceinline__ uint32_t poly_exp2_bf16x2(float x0, float x1) {
+__device__ __forceinline__ void poly_exp2_pair(float x0, float x1, float& e0, float& e1) {
   constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: integer part lands in the low mantissa bits
   x0 = fmaxf(x0, -125.0f);
   x1 = fmaxf(x1, -125.0f);
@@ -55,9 +57,8 @@ __device__ __forceinline__ uint32_t poly_exp2_bf16x2(float x0, float x1) {
   fma2(p0, p1, f0, f1, 0.05517166f, 0.05517166f, 0.24261115f, 0.24261115f);
   fma2(p0, p1, p0, p1, f0, f1, 0.69326097f, 0.69326097f);
   fma2(p0, p1, p0, p1, f0, f1, 0.99992806f, 0.99992806f);
-  const float e0 = __int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23));
-  const float e1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
-  return pack_bf16(e0, e1);
+  e0 = __int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23));
+  e1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
 }
 
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
@@ -75,38 +76,33 @@ __device__ __forceinline__ void tmem_st1(uint32_t taddr, uint32_t v) {
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-constexpr int kQ = 128;     // query rows per tile (one softmax warpgroup each)
+// Debug timeline (AttnArgs::trace): one CTA records clock64 at pipeline events.
+#define RK_TRACE(role, step, ev)                                                                           \
+  do {                                                                                                   \
+    if (TRACE && tracing && (step) < 64) a.trace[((role) * 64 + (step)) * 8 + (ev)] = clock64();         \
+  } while (0)
+
+constexpr int kQ = 128;     // query rows per tile (TMEM lanes)
 constexpr int kKeys = 128;  // keys per tile
 constexpr float kRescaleLog2 = 8.0f;  // lazy O rescale threshold (P <= 2^8)
-// query tiles per CTA (ping-pong softmax warpgroups over shared K/V tiles)
-template <int DH> constexpr int qtiles() { return DH == 64 ? 2 : 1; }
-// softmax warpgroups first (warp w reads TMEM lanes 32*(w%4)..), then one control
-// warpgroup: TMA warp, MMA warp, two idle warps (setmaxnreg works per warpgroup)
-template <int DH> constexpr int threads() { return (qtiles<DH>() + 1) * 128; }
+constexpr int kThreadsA = 256;        // softmax warpgroup + control warpgroup
 
 template <int DH>
 struct ACfg {
-  static constexpr int kQT = qtiles<DH>();
   static constexpr int Q_TILE = kQ * DH * 2;
-  static constexpr int KV_BYTES = kKeys * DH * 2;  // one of K or V
-  static constexpr int ONES_BYTES = kKeys * 128;   // 64-wide block of ones after V: P.[V|1] gives row sums
-  // K and V stream through separate rings: K_j is free once S(j) is done, V_j
-  // only after P(j).V_j, so K runs further ahead (TMA latency off the path)
-  static constexpr int KST = DH == 64 ? 3 : 2;
-  static constexpr int VST = 2;
-  static constexpr int V_STAGE = KV_BYTES + ONES_BYTES;
-  static constexpr int ON = DH + 16;               // PV MMA N: DH value columns + 16 ones columns
+  static constexpr int KV_BYTES = kKeys * DH * 2;  // one stage of K or V
+  static constexpr int KST = 2, VST = 2;
   static constexpr int P_BYTES = kQ * kKeys * 2;
   static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = kQT * Q_TILE;
+  static constexpr int OFF_K = Q_TILE;
   static constexpr int OFF_V = OFF_K + KST * KV_BYTES;
-  static constexpr int OFF_P = OFF_V + VST * V_STAGE;
-  static constexpr int OFF_BAR = OFF_P + kQT * P_BYTES;
-  static constexpr int SMEM = OFF_BAR + 512 + 1024;
-  static_assert(SMEM + 64 <= 232448, "shared memory per CTA");
-  static constexpr uint32_t TMEM_COLS = 512;
-  // TMEM columns: S_t at t*128, O_t (DH values + row-sum column) at 256 + t*128
-  static constexpr uint32_t S_COL = 0, O_COL = 256;
+  static constexpr int OFF_P = OFF_V + VST * KV_BYTES;
+  static constexpr int OFF_BAR = OFF_P + P_BYTES;
+  static constexpr int SMEM = OFF_BAR + 128;
+  static constexpr int CTAS = DH == 64 ? 2 : 1;  // CTAs per SM
+  static_assert(CTAS * (SMEM + 1024) <= 233472, "shared memory per SM");
+  static constexpr uint32_t TMEM_COLS = 256;
+  static constexpr uint32_t S_COL = 0, O_COL = 128;  // S [0,128), O [128, 128+DH)
 };
 
 // Query tile `tile` of the launch -> rows [r0, r1) within one row group.
@@ -126,349 +122,313 @@ __device__ __forceinline__ void tile_rows(const AttnArgs& a, int M, int tile, in
   r0 = r1 = 0;
 }
 
-template <int DH>
-__global__ void __launch_bounds__(threads<DH>(), 1)
+__device__ __forceinline__ void exp2_pair(float x0, float x1, bool poly, float& e0, float& e1) {
+  if (poly) {
+    poly_exp2_pair(x0, x1, e0, e1);
+  } else {
+    e0 = fast_exp2(x0);
+    e1 = fast_exp2(x1);
+  }
+}
+
+template <int DH, bool TRACE>
+__global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
     attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                 const __grid_constant__ CUtensorMap tmV, const AttnArgs a) {
   using C = ACfg<DH>;
-  constexpr int kQT = C::kQT;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* q_full = bar + 0;
-  uint64_t* k_full = bar + 1;    // [KST <= 3]
-  uint64_t* k_empty = bar + 4;   // [KST]
-  uint64_t* v_full = bar + 7;    // [VST = 2]
-  uint64_t* v_empty = bar + 9;   // [VST]
-  uint64_t* s_full = bar + 11;   // [kQT]
-  uint64_t* s_free = bar + 13;   // [kQT]
-  uint64_t* p_full = bar + 15;   // [kQT]
-  uint64_t* o_done = bar + 17;   // [kQT]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 24);
-  __shared__ int s_kmax[kQT];
+  uint64_t* k_full = bar + 1;   // [2]
+  uint64_t* k_empty = bar + 3;  // [2]
+  uint64_t* v_full = bar + 5;   // [2]
+  uint64_t* v_empty = bar + 7;  // [2]
+  uint64_t* s_full = bar + 9;
+  uint64_t* s_free = bar + 10;
+  uint64_t* p_full = bar + 11;
+  uint64_t* o_done = bar + 12;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 13);
+  int* s_kmax = reinterpret_cast<int*>(bar + 14);
 
   const int M = a.rows_dev ? *a.rows_dev : a.rows_max;
-  int r0[kQT], r1[kQT];
-#pragma unroll
-  for (int t = 0; t < kQT; ++t) tile_rows(a, M, blockIdx.x * kQT + t, r0[t], r1[t]);
-  if (r1[0] <= r0[0]) return;  // no rows (tiles past the live count)
-  const int h = blockIdx.y;
-  const int kvh = h / (a.H / a.Hkv);
-  if (threadIdx.x < kQT) s_kmax[threadIdx.x] = -1;
-  __syncthreads();
-#pragma unroll
-  for (int t = 0; t < kQT; ++t)
-    for (int i = r0[t] + threadIdx.x; i < r1[t]; i += blockDim.x) atomicMax(&s_kmax[t], a.pos[i]);
-  __syncthreads();
-  // split-KV: this CTA covers key tiles [j0, j0 + tiles_per_split); tile t needs nk[t] of them
-  const int j0 = blockIdx.z * a.tiles_per_split;
-  int nk[kQT], nk_all = 0;
-#pragma unroll
-  for (int t = 0; t < kQT; ++t) {
-    nk[t] = r1[t] > r0[t] ? min(s_kmax[t] / kKeys + 1 - j0, a.tiles_per_split) : 0;
-    nk_all = max(nk_all, nk[t]);
+  // grid (head, tile, split) with heads fastest and tiles in reverse order:
+  // the CTAs of the latest (longest) query tiles of every head dispatch first
+  int r0, r1;
+  tile_rows(a, M, (int)gridDim.y - 1 - (int)blockIdx.y, r0, r1);
+  if (r1 <= r0) return;  // no rows (tiles past the live count)
+  if (threadIdx.x == 0) {
+    if (smem_u32(smem) & 1023) __trap();  // SW128 tiles need a 1 KB aligned base
+    *s_kmax = -1;
   }
+  __syncthreads();
+  for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) atomicMax(s_kmax, a.pos[i]);
+  __syncthreads();
+  const int h = blockIdx.x;
+  const int kvh = h / (a.H / a.Hkv);
+  // split-KV: this CTA covers key tiles [j0, j0 + nk)
+  const int j0 = blockIdx.z * a.tiles_per_split;
+  const int nk = min(*s_kmax / kKeys + 1 - j0, a.tiles_per_split);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  if (nk_all <= 0) {  // no keys for this split: empty partials (m = -inf, l = 0)
-#pragma unroll
-    for (int t = 0; t < kQT; ++t)
-      for (int i = r0[t] + threadIdx.x; i < r1[t]; i += blockDim.x) {
-        float* ml = a.ws_ml + (((size_t)blockIdx.z * a.rows_max + i) * a.H + h) * 2;
-        ml[0] = -INFINITY;
-        ml[1] = 0.f;
-      }
+  const bool trace_cta = TRACE && a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
+  if (nk <= 0) {  // no keys for this split: empty partials (m = -inf, l = 0)
+    for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+      float* ml = a.ws_ml + (((size_t)blockIdx.z * a.rows_max + i) * a.H + h) * 2;
+      ml[0] = -INFINITY;
+      ml[1] = 0.f;
+    }
     return;
   }
 
-  const int ctl = 4 * kQT;  // first warp of the control warpgroup
-  if (warp == ctl && lane == 0) {
+  if (warp == 4 && lane == 0) {
     tma_prefetch(&tmQ);
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
     mbar_init(q_full, 1);
-    for (int i = 0; i < C::KST; ++i) {
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&k_empty[i], 1);
-    }
-    for (int i = 0; i < C::VST; ++i) {
       mbar_init(&v_full[i], 1);
       mbar_init(&v_empty[i], 1);
     }
-    for (int t = 0; t < kQT; ++t) {
-      mbar_init(&s_full[t], 1);
-      mbar_init(&s_free[t], 4);
-      mbar_init(&p_full[t], 4);
-      mbar_init(&o_done[t], 1);
-    }
+    mbar_init(s_full, 1);
+    mbar_init(s_free, 4);
+    mbar_init(p_full, 4);
+    mbar_init(o_done, 1);
     fence_barrier_init();
   }
-  if (warp == ctl + 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
-  for (int st = 0; st < C::VST; ++st) {  // the constant ones block of each V stage
-    uint4* ones = reinterpret_cast<uint4*>(smem + C::OFF_V + st * C::V_STAGE + C::KV_BYTES);
-    for (int i = threadIdx.x; i < C::ONES_BYTES / 16; i += blockDim.x) ones[i] = make_uint4(0x3f803f80u, 0x3f803f80u, 0x3f803f80u, 0x3f803f80u);
-  }
-  fence_proxy_async();
+  if (warp == 5) tmem_alloc(tmem_slot, C::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   constexpr int DB = DH / 64;  // 64-wide swizzle blocks along d
 
-  if (warp >= ctl) {
-    // control warpgroup: hand registers to the softmax warpgroups
-    if constexpr (kQT == 2) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
-  if (warp == ctl) {
-    if (elect_one()) {  // ------------------------------------------------ TMA
-      uint8_t* sq = smem + C::OFF_Q;
-      int nq = 0;
-      for (int t = 0; t < kQT; ++t) nq += nk[t] > 0;
-      mbar_arrive_expect_tx(q_full, nq * C::Q_TILE);
-      for (int t = 0; t < kQT; ++t)
-        if (nk[t] > 0)
+  if (warp >= 4) {  // ------------------------------------------ control warpgroup
+    if constexpr (C::CTAS == 2) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
+    if (warp == 4) {
+      if (elect_one()) {  // ---------------------------------------- TMA K
+        for (int j = 0; j < nk; ++j) {
+          const int st = j & 1;
+          mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
+          uint8_t* sk = smem + C::OFF_K + st * C::KV_BYTES;
+          mbar_arrive_expect_tx(&k_full[st], C::KV_BYTES);
           for (int b = 0; b < DB; ++b)
-            tma_load_2d(sq + t * C::Q_TILE + b * kQ * 128, &tmQ, q_full, h * DH + b * 64, r0[t]);
-      for (int j = 0; j < nk_all; ++j) {  // K ring
-        const int st = j % C::KST;
-        mbar_wait(&k_empty[st], ((j / C::KST) & 1) ^ 1);
-        uint8_t* sk = smem + C::OFF_K + st * C::KV_BYTES;
-        mbar_arrive_expect_tx(&k_full[st], C::KV_BYTES);
-        for (int b = 0; b < DB; ++b)
-          tma_load_2d(sk + b * kKeys * 128, &tmK, &k_full[st], kvh * DH + b * 64, (j0 + j) * kKeys);
-      }
-    }
-  } else if (warp == ctl + 2) {
-    if (elect_one()) {  // --------------------------------------------- TMA V
-      for (int j = 0; j < nk_all; ++j) {
-        const int st = j % C::VST;
-        mbar_wait(&v_empty[st], ((j / C::VST) & 1) ^ 1);
-        uint8_t* sv = smem + C::OFF_V + st * C::V_STAGE;
-        mbar_arrive_expect_tx(&v_full[st], C::KV_BYTES);
-        for (int b = 0; b < DB; ++b)
-          tma_load_2d(sv + b * kKeys * 128, &tmV, &v_full[st], kvh * DH + b * 64, (j0 + j) * kKeys);
-      }
-    }
-  } else if (warp == ctl + 1) {
-    if (elect_one()) {  // ------------------------------------------------ MMA
-      constexpr uint32_t idesc_s = idesc_bf16(kQ, kKeys);
-      constexpr uint32_t idesc_o = idesc_bf16(kQ, C::ON, /*b_mn_major=*/true);
-      mbar_wait(q_full, 0);
-      auto issue_s = [&](int j, int t) {
-        const int st = j % C::KST;
-        mbar_wait(&s_free[t], (j & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t sq = smem_u32(smem + C::OFF_Q + t * C::Q_TILE);
-        const uint32_t sk = smem_u32(smem + C::OFF_K + st * C::KV_BYTES);
-#pragma unroll
-        for (int k = 0; k < DH / 16; ++k) {
-          const uint32_t off = (k >> 2) * (kQ * 128) + (k & 3) * 32;
-          const uint32_t offk = (k >> 2) * (kKeys * 128) + (k & 3) * 32;
-          mma_bf16_ss(tmem + C::S_COL + t * 128, sdesc_sw128(sq + off, 16, 1024), sdesc_sw128(sk + offk, 16, 1024),
-                      idesc_s, k > 0 ? 1u : 0u);
+            tma_load_2d(sk + b * kKeys * 128, &tmK, &k_full[st], kvh * DH + b * 64, (j0 + j) * kKeys);
         }
-        tc_commit(&s_full[t]);
-      };
-      auto issue_pv = [&](int j, int t) {
-        const int st = j % C::VST;
-        mbar_wait(&p_full[t], j & 1);
-        tc_fence_after();
-        const uint32_t sp = smem_u32(smem + C::OFF_P + t * C::P_BYTES);
-        const uint32_t sv = smem_u32(smem + C::OFF_V + st * C::V_STAGE);
-#pragma unroll
-        for (int k = 0; k < kKeys / 16; ++k) {
-          const uint64_t ad = sdesc_sw128(sp + (k >> 2) * (kQ * 128) + (k & 3) * 32, 16, 1024);
-          const uint64_t bd = sdesc_sw128(sv + k * 2048, kKeys * 128, 1024);
-          mma_bf16_ss(tmem + C::O_COL + t * 128, ad, bd, idesc_o, (j > 0 || k > 0) ? 1u : 0u);
+      }
+    } else if (warp == 6) {
+      if (elect_one()) {  // ------------------------------------- TMA Q, V
+        mbar_arrive_expect_tx(q_full, C::Q_TILE);
+        for (int b = 0; b < DB; ++b)
+          tma_load_2d(smem + C::OFF_Q + b * kQ * 128, &tmQ, q_full, h * DH + b * 64, r0);
+        for (int j = 0; j < nk; ++j) {
+          const int st = j & 1;
+          mbar_wait(&v_empty[st], ((j >> 1) & 1) ^ 1);
+          uint8_t* sv = smem + C::OFF_V + st * C::KV_BYTES;
+          mbar_arrive_expect_tx(&v_full[st], C::KV_BYTES);
+          for (int b = 0; b < DB; ++b)
+            tma_load_2d(sv + b * kKeys * 128, &tmV, &v_full[st], kvh * DH + b * 64, (j0 + j) * kKeys);
         }
-        tc_commit(&o_done[t]);
-      };
-      // S_t(j+1) goes in as soon as softmax t has S_t(j) in registers, ahead of
-      // P_t(j) V_j, so the tensor pipe computes the next scores while the
-      // softmax warpgroups exponentiate the current ones.
-      mbar_wait(&k_full[0], 0);
-      tc_fence_after();
-      for (int t = 0; t < kQT; ++t)
-        if (nk[t] > 0) issue_s(0, t);
-      tc_commit(&k_empty[0]);
-      for (int j = 0; j < nk_all; ++j) {
-        if (j + 1 < nk_all) {
-          const int jk = j + 1;
-          mbar_wait(&k_full[jk % C::KST], (jk / C::KST) & 1);
+      }
+    } else if (warp == 5) {
+      if (elect_one()) {  // ------------------------------------------ MMA
+        const bool tracing = trace_cta;
+        constexpr uint32_t idesc_s = idesc_bf16(kQ, kKeys);
+        constexpr uint32_t idesc_o = idesc_bf16(kQ, DH, /*b_mn_major=*/true);
+        const uint32_t sq = smem_u32(smem + C::OFF_Q);
+        mbar_wait(q_full, 0);
+        auto issue_s = [&](int j) {
+          const int st = j & 1;
+          mbar_wait(&k_full[st], (j >> 1) & 1);
+          mbar_wait(s_free, (j & 1) ^ 1);
+          RK_TRACE(2, j, 1);
           tc_fence_after();
-          for (int t = 0; t < kQT; ++t)
-            if (jk < nk[t]) issue_s(jk, t);
-          tc_commit(&k_empty[jk % C::KST]);
+          const uint32_t sk = smem_u32(smem + C::OFF_K + st * C::KV_BYTES);
+#pragma unroll
+          for (int k = 0; k < DH / 16; ++k) {
+            const uint32_t off = (k >> 2) * (kQ * 128) + (k & 3) * 32;
+            const uint32_t offk = (k >> 2) * (kKeys * 128) + (k & 3) * 32;
+            mma_bf16_ss(tmem + C::S_COL, sdesc_sw128(sq + off, 16, 1024), sdesc_sw128(sk + offk, 16, 1024), idesc_s,
+                        k > 0 ? 1u : 0u);
+          }
+          tc_commit(s_full);
+          tc_commit(&k_empty[st]);
+        };
+        auto issue_pv = [&](int j) {
+          const int st = j & 1;
+          mbar_wait(&v_full[st], (j >> 1) & 1);
+          mbar_wait(p_full, j & 1);
+          RK_TRACE(2, j, 4);
+          tc_fence_after();
+          const uint32_t sp = smem_u32(smem + C::OFF_P);
+          const uint32_t sv = smem_u32(smem + C::OFF_V + st * C::KV_BYTES);
+#pragma unroll
+          for (int k = 0; k < kKeys / 16; ++k) {
+            const uint64_t ad = sdesc_sw128(sp + (k >> 2) * (kQ * 128) + (k & 3) * 32, 16, 1024);
+            const uint64_t bd = sdesc_sw128(sv + k * 2048, kKeys * 128, 1024);
+            mma_bf16_ss(tmem + C::O_COL, ad, bd, idesc_o, (j > 0 || k > 0) ? 1u : 0u);
+          }
+          tc_commit(o_done);
+          tc_commit(&v_empty[st]);
+        };
+        // S(j+1) goes in as soon as the softmax holds S(j) in registers, ahead
+        // of P(j) V_j, so the next scores compute while exponentials run
+        issue_s(0);
+        for (int j = 0; j < nk; ++j) {
+          if (j + 1 < nk) issue_s(j + 1);
+          issue_pv(j);
         }
-        mbar_wait(&v_full[j % C::VST], (j / C::VST) & 1);
-        tc_fence_after();
-        for (int t = 0; t < kQT; ++t)
-          if (j < nk[t]) issue_pv(j, t);
-        tc_commit(&v_empty[j % C::VST]);
       }
     }
-  }
-  } else {  // ------------------------------------------------ softmax warpgroups
-    if constexpr (kQT == 2) asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
-    const int t = warp / 4;              // query tile of this warpgroup
-    const int quarter = warp & 3;        // TMEM lane quarter this warp may access
-    const int rl = quarter * 32 + lane;  // row within the tile == TMEM lane
-    const int row = r0[t] + rl;
-    const bool valid = row < r1[t];
-    const int my_nk = nk[t];
-    // Ping-pong (kQT == 2): the exponentiation phases of the two warpgroups
-    // alternate through named barriers 8/9, so one group's exp2 burst runs
-    // while the other waits on its P.V and loads its next scores. Every group
-    // takes nk_all turns (idle turns just pass the token); group 0 goes first.
-    constexpr uint32_t kTurn = 8;
-    if (kQT == 2 && t == 1) named_bar_arrive(kTurn, 256);
-    if (my_nk <= 0) {  // this tile has no keys in this split
-      if (valid && a.splits > 1) {
-        float* ml = a.ws_ml + (((size_t)blockIdx.z * a.rows_max + row) * a.H + h) * 2;
-        ml[0] = -INFINITY;
-        ml[1] = 0.f;
+  } else {  // ------------------------------------------------ softmax warpgroup
+    if constexpr (C::CTAS == 2) asm volatile("setmaxnreg.inc.sync.aligned.u32 200;\n" ::: "memory");
+    const bool tracing = trace_cta && warp == 0 && lane == 0;
+    const int rl = warp * 32 + lane;  // row within the tile == TMEM lane
+    const int row = r0 + rl;
+    const bool valid = row < r1;
+    const int pos = valid ? a.pos[row] : *s_kmax;
+    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    const uint32_t s_col = tmem + lane_base + C::S_COL;
+    const uint32_t o_col = tmem + lane_base + C::O_COL;
+    uint8_t* sp = smem + C::OFF_P;
+    const float scale = a.scale_log2;
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int j = 0; j < nk; ++j) {
+      RK_TRACE(0, j, 0);
+      mbar_wait(s_full, j & 1);
+      RK_TRACE(0, j, 1);
+      tc_fence_after();
+      uint32_t r[128];
+      tmem_ld32(s_col + 0, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+      tmem_ld32(s_col + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+      tmem_ld32(s_col + 64, *reinterpret_cast<uint32_t(*)[32]>(&r[64]));
+      tmem_ld32(s_col + 96, *reinterpret_cast<uint32_t(*)[32]>(&r[96]));
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(s_free);  // S(j+1) may overwrite TMEM now
+      RK_TRACE(0, j, 2);
+      const int kbase = (j0 + j) * kKeys;
+      // warp-uniform: no causal mask anywhere in this tile for this warp's rows
+      if (!__all_sync(0xffffffffu, kbase + kKeys - 1 <= pos)) {
+#pragma unroll
+        for (int u = 0; u < kKeys; ++u)
+          if (kbase + u > pos) r[u] = __float_as_uint(-INFINITY);
+      }
+      float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+#pragma unroll
+      for (int u = 0; u < kKeys; u += 8) {
+        mx0 = fmaxf(mx0, fmaxf(__uint_as_float(r[u]), __uint_as_float(r[u + 1])));
+        mx1 = fmaxf(mx1, fmaxf(__uint_as_float(r[u + 2]), __uint_as_float(r[u + 3])));
+        mx2 = fmaxf(mx2, fmaxf(__uint_as_float(r[u + 4]), __uint_as_float(r[u + 5])));
+        mx3 = fmaxf(mx3, fmaxf(__uint_as_float(r[u + 6]), __uint_as_float(r[u + 7])));
+      }
+      const float m_new = fmaxf(m_run, fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * scale);
+      bool waited = false;  // P(j-1) V_{j-1} known complete (P buffer free, O stable)
+      if (j == 0) {
+        m_run = m_new;  // O is written (not accumulated) by the first P.V
+      } else {
+        const bool need = m_new > m_run + kRescaleLog2;
+        if (__any_sync(0xffffffffu, need)) {  // rare: rescale O in TMEM once P.V_{j-1} landed
+          mbar_wait(o_done, (j - 1) & 1);
+          tc_fence_after();
+          waited = true;
+          const float corr = need ? fast_exp2(m_run - m_new) : 1.0f;
+#pragma unroll
+          for (int c = 0; c < DH; c += 32) {
+            uint32_t o[32];
+            tmem_ld32(o_col + c, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int u = 0; u < 32; ++u) o[u] = __float_as_uint(__uint_as_float(o[u]) * corr);
+            tmem_st32(o_col + c, o);
+          }
+          tmem_st_wait();
+          l_run *= corr;
+          if (need) m_run = m_new;
+        }
+      }
+      RK_TRACE(0, j, 3);
+      // P = exp2(s * scale - m_run) -> bf16, K-major SW128 (2 blocks of 64
+      // keys, 16-byte chunks swizzled by row); chunks 3 and 7 of each block via
+      // the FMA-pipe cubic, the rest on MUFU. The first block is computed
+      // before waiting for the previous P.V, so that wait overlaps the exps.
+      const float neg_m = m_run == -INFINITY ? 0.f : -m_run;
+      float ls0 = 0.f, ls1 = 0.f, ls2 = 0.f, ls3 = 0.f;
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        uint32_t pk[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int u = b * 64 + 2 * i;
+          float x0, x1, e0, e1;
+          fma2(x0, x1, __uint_as_float(r[u]), __uint_as_float(r[u + 1]), scale, scale, neg_m, neg_m);
+          exp2_pair(x0, x1, ((i >> 2) & 3) == 3, e0, e1);
+          if (i & 1) add2(ls2, ls3, ls2, ls3, e0, e1);
+          else add2(ls0, ls1, ls0, ls1, e0, e1);
+          pk[i] = pack_bf16(e0, e1);
+        }
+        if (b == 0 && j > 0 && !waited) {
+          mbar_wait(o_done, (j - 1) & 1);
+          tc_fence_after();
+        }
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {
+          uint4* dst = reinterpret_cast<uint4*>(sp + b * (kQ * 128) + rl * 128 + ((ch ^ (rl & 7)) * 16));
+          *dst = make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
+        }
+      }
+      l_run += (ls0 + ls1) + (ls2 + ls3);
+      RK_TRACE(0, j, 4);
+      tc_fence_before();
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+      RK_TRACE(0, j, 5);
+    }
+    mbar_wait(o_done, (nk - 1) & 1);
+    tc_fence_after();
+    if (a.splits > 1) {
+      const size_t pr = ((size_t)blockIdx.z * a.rows_max + row) * a.H + h;
+#pragma unroll
+      for (int c = 0; c < DH; c += 32) {
+        uint32_t o[32];
+        tmem_ld32(o_col + c, o);
+        tmem_ld_wait();
+        if (valid) {
+          float4* dst = reinterpret_cast<float4*>(a.ws_o + pr * DH + c);
+#pragma unroll
+          for (int u = 0; u < 32; u += 4)
+            dst[u / 4] = make_float4(__uint_as_float(o[u]), __uint_as_float(o[u + 1]), __uint_as_float(o[u + 2]),
+                                     __uint_as_float(o[u + 3]));
+        }
+      }
+      if (valid) {
+        a.ws_ml[pr * 2] = m_run;
+        a.ws_ml[pr * 2 + 1] = l_run;
       }
     } else {
-      const int pos = valid ? a.pos[row] : s_kmax[t];
-      const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
-      const uint32_t s_col = tmem + lane_base + C::S_COL + t * 128;
-      const uint32_t o_col = tmem + lane_base + C::O_COL + t * 128;
-      uint8_t* sp = smem + C::OFF_P + t * C::P_BYTES;
-      const float scale = a.scale_log2;
-      float m_run = -INFINITY;
-      for (int j = 0; j < my_nk; ++j) {
-        mbar_wait(&s_full[t], j & 1);
-        tc_fence_after();
-        uint32_t r[128];
-        tmem_ld32(s_col + 0, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
-        tmem_ld32(s_col + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
-        tmem_ld32(s_col + 64, *reinterpret_cast<uint32_t(*)[32]>(&r[64]));
-        tmem_ld32(s_col + 96, *reinterpret_cast<uint32_t(*)[32]>(&r[96]));
+      const float inv = 1.f / l_run;
+      uint4* dst = reinterpret_cast<uint4*>(a.out + (size_t)row * (a.H * DH) + h * DH);
+#pragma unroll
+      for (int c = 0; c < DH; c += 32) {
+        uint32_t o[32];
+        tmem_ld32(o_col + c, o);
         tmem_ld_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&s_free[t]);  // S_t(j+1) may overwrite TMEM now
-        const int kbase = (j0 + j) * kKeys;
-        // warp-uniform: no causal mask anywhere in this tile for this warp's rows
-        if (!__all_sync(0xffffffffu, kbase + kKeys - 1 <= pos)) {
-#pragma unroll
-          for (int u = 0; u < kKeys; ++u)
-            if (kbase + u > pos) r[u] = __float_as_uint(-INFINITY);
-        }
-        float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
-#pragma unroll
-        for (int u = 0; u < kKeys; u += 8) {
-          mx0 = fmaxf(mx0, fmaxf(__uint_as_float(r[u]), __uint_as_float(r[u + 1])));
-          mx1 = fmaxf(mx1, fmaxf(__uint_as_float(r[u + 2]), __uint_as_float(r[u + 3])));
-          mx2 = fmaxf(mx2, fmaxf(__uint_as_float(r[u + 4]), __uint_as_float(r[u + 5])));
-          mx3 = fmaxf(mx3, fmaxf(__uint_as_float(r[u + 6]), __uint_as_float(r[u + 7])));
-        }
-        const float m_new = fmaxf(m_run, fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * scale);
-        if (j == 0) {
-          m_run = m_new;  // O is written (not accumulated) by the first P.V
-        } else {
-          // P_t(j-1) V_{j-1} done: the P buffer is free and O is stable
-          mbar_wait(&o_done[t], (j - 1) & 1);
-          tc_fence_after();
-          const bool need = m_new > m_run + kRescaleLog2;
-          if (__any_sync(0xffffffffu, need)) {
-            const float corr = need ? fast_exp2(m_run - m_new) : 1.0f;
-#pragma unroll
-            for (int c = 0; c < DH; c += 32) {
-              uint32_t o[32];
-              tmem_ld32(o_col + c, o);
-              tmem_ld_wait();
-#pragma unroll
-              for (int u = 0; u < 32; ++u) o[u] = __float_as_uint(__uint_as_float(o[u]) * corr);
-              tmem_st32(o_col + c, o);
-            }
-            const uint32_t l = tmem_ld1(o_col + DH);
-            tmem_ld_wait();
-            tmem_st1(o_col + DH, __float_as_uint(__uint_as_float(l) * corr));
-            tmem_st_wait();
-            if (need) m_run = m_new;
-          }
-        }
-        // P = exp2(s * scale - m_run) -> bf16, K-major SW128 (2 blocks of 64 keys);
-        // chunks 3 and 7 of each block via the FMA-pipe cubic, the rest on MUFU
-        const float neg_m = m_run == -INFINITY ? 0.f : -m_run;
-        if (kQT == 2) named_bar_sync(kTurn + t, 256);
-#pragma unroll
-        for (int b = 0; b < 2; ++b) {
-#pragma unroll
-          for (int ch = 0; ch < 8; ++ch) {
-            uint32_t pk[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int i0 = b * 64 + ch * 8 + 2 * u;
-              float x0, x1;
-              fma2(x0, x1, __uint_as_float(r[i0]), __uint_as_float(r[i0 + 1]), scale, scale, neg_m, neg_m);
-              if ((ch & 3) == 3) pk[u] = poly_exp2_bf16x2(x0, x1);
-              else pk[u] = pack_bf16(fast_exp2(x0), fast_exp2(x1));
-            }
-            uint4* dst = reinterpret_cast<uint4*>(sp + b * (kQ * 128) + rl * 128 + ((ch ^ (rl & 7)) * 16));
-            *dst = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-          }
-        }
-        tc_fence_before();
-        fence_proxy_async();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[t]);
-        if (kQT == 2) named_bar_arrive(kTurn + (t ^ 1), 256);
-      }
-      mbar_wait(&o_done[t], (my_nk - 1) & 1);
-      tc_fence_after();
-      uint32_t lb = tmem_ld1(o_col + DH);
-      tmem_ld_wait();
-      const float l_run = __uint_as_float(lb);
-      if (a.splits > 1) {
-        const size_t pr = ((size_t)blockIdx.z * a.rows_max + row) * a.H + h;
-#pragma unroll
-        for (int c = 0; c < DH; c += 32) {
-          uint32_t o[32];
-          tmem_ld32(o_col + c, o);
-          tmem_ld_wait();
-          if (valid) {
-            float4* dst = reinterpret_cast<float4*>(a.ws_o + pr * DH + c);
-#pragma unroll
-            for (int u = 0; u < 32; u += 4)
-              dst[u / 4] = make_float4(__uint_as_float(o[u]), __uint_as_float(o[u + 1]), __uint_as_float(o[u + 2]),
-                                       __uint_as_float(o[u + 3]));
-          }
-        }
         if (valid) {
-          a.ws_ml[pr * 2] = m_run;
-          a.ws_ml[pr * 2 + 1] = l_run;
-        }
-      } else {
-        const float inv = 1.f / l_run;
-        uint4* dst = reinterpret_cast<uint4*>(a.out + (size_t)row * (a.H * DH) + h * DH);
 #pragma unroll
-        for (int c = 0; c < DH; c += 32) {
-          uint32_t o[32];
-          tmem_ld32(o_col + c, o);
-          tmem_ld_wait();
-          if (valid) {
-#pragma unroll
-            for (int u = 0; u < 32; u += 8)
-              dst[(c + u) / 8] = make_uint4(
-                  pack_bf16(__uint_as_float(o[u]) * inv, __uint_as_float(o[u + 1]) * inv),
-                  pack_bf16(__uint_as_float(o[u + 2]) * inv, __uint_as_float(o[u + 3]) * inv),
-                  pack_bf16(__uint_as_float(o[u + 4]) * inv, __uint_as_float(o[u + 5]) * inv),
-                  pack_bf16(__uint_as_float(o[u + 6]) * inv, __uint_as_float(o[u + 7]) * inv));
-          }
+          for (int u = 0; u < 32; u += 8)
+            dst[(c + u) / 8] = make_uint4(pack_bf16(__uint_as_float(o[u]) * inv, __uint_as_float(o[u + 1]) * inv),
+                                          pack_bf16(__uint_as_float(o[u + 2]) * inv, __uint_as_float(o[u + 3]) * inv),
+                                          pack_bf16(__uint_as_float(o[u + 4]) * inv, __uint_as_float(o[u + 5]) * inv),
+                                          pack_bf16(__uint_as_float(o[u + 6]) * inv, __uint_as_float(o[u + 7]) * inv));
         }
       }
-    }
-    if (kQT == 2) {
-      for (int j = my_nk > 0 ? my_nk : 0; j < nk_all; ++j) {  // idle turns
-        named_bar_sync(kTurn + t, 256);
-        named_bar_arrive(kTurn + (t ^ 1), 256);
-      }
-      if (t == 0) named_bar_sync(kTurn, 256);  // group 1's last pass
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == ctl + 1) tmem_dealloc(tmem, C::TMEM_COLS);
+  if (warp == 5) tmem_dealloc(tmem, C::TMEM_COLS);
 }
 
 // Normalised attention probabilities over a window of segment keys for the
@@ -558,11 +518,13 @@ void launch_attn(rk_engine* e, const CUtensorMap& tq, const CUtensorMap& tk, con
                  const AttnArgs& a) {
   static bool attr = false;
   if (!attr) {
-    RK_CUDA(cudaFuncSetAttribute(attn_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, ACfg<DH>::SMEM));
+    RK_CUDA(cudaFuncSetAttribute(attn_kernel<DH, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ACfg<DH>::SMEM));
+    RK_CUDA(cudaFuncSetAttribute(attn_kernel<DH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ACfg<DH>::SMEM));
     attr = true;
   }
-  dim3 grid((max_tiles(a) + qtiles<DH>() - 1) / qtiles<DH>(), a.H, a.splits);
-  attn_kernel<DH><<<grid, threads<DH>(), ACfg<DH>::SMEM, e->stream>>>(tq, tk, tv, a);
+  dim3 grid(a.H, max_tiles(a), a.splits);
+  if (a.trace) attn_kernel<DH, true><<<grid, kThreadsA, ACfg<DH>::SMEM, e->stream>>>(tq, tk, tv, a);
+  else attn_kernel<DH, false><<<grid, kThreadsA, ACfg<DH>::SMEM, e->stream>>>(tq, tk, tv, a);
   if (a.splits > 1) {
     const int warps = a.rows_max * a.H;
     attn_combine_kernel<DH><<<(warps + 7) / 8, 256, 0, e->stream>>>(a);
@@ -576,15 +538,23 @@ void attention_bf16(rk_engine* e, const AttnArgs& a_in, const __nv_bfloat16* ctx
                     int ctx_rows) {
   if (a_in.rows_max <= 0) return;
   AttnArgs a = a_in;
-  // split-KV when the query tiles alone cannot fill the SMs
-  const int qt = a.dh == 64 ? qtiles<64>() : qtiles<128>();
-  const int q_tiles = (max_tiles(a) + qt - 1) / qt;
-  const int base = q_tiles * a.H;
+  // split-KV when the query tiles alone cannot fill the SMs (sparse passes:
+  // plan for ~1/3 of rows_max live). A split covers >= 2 key tiles; CTAs
+  // whose rows end before their split exit at once, so long tiles (suffix,
+  // late segment rows) spread over many CTAs while short ones stay whole.
+  AttnArgs hint = a;
+  if (a.rows_dev) hint.rows_max = std::max(a.g2 + 1, a.rows_max / 3);
+  const int ctas_per_sm = a.dh == 64 ? ACfg<64>::CTAS : ACfg<128>::CTAS;
+  const int base = max_tiles(hint) * a.H;          // CTAs without splitting
+  const int slots = ctas_per_sm * e->sm_count;     // CTAs resident at once
   const int nk_max = (ctx_rows + kKeys - 1) / kKeys;
   a.splits = 1;
   a.tiles_per_split = nk_max > 0 ? nk_max : 1;
-  if (base < 2 * e->sm_count && nk_max > 2) {
-    int splits = std::min((2 * e->sm_count + base - 1) / base, (nk_max + 1) / 2);
+  // split the key range only while the grid is well under 1.5 waves; each
+  // split keeps >= 4 key tiles (a CTA's fixed cost is a few microseconds)
+  const int want = (3 * slots / 2) / std::max(1, base);
+  if (want >= 2 && nk_max >= 8) {
+    const int splits = std::min(want, nk_max / 4);
     a.tiles_per_split = (nk_max + splits - 1) / splits;
     a.splits = (nk_max + a.tiles_per_split - 1) / a.tiles_per_split;
   }

@@ -131,6 +131,37 @@ int rk_debug_bench_attention(rk_engine* e, int M, int T, int H, int Hkv, int dh,
   });
 }
 
+int rk_debug_trace_attention(rk_engine* e, int M, int T, int H, int Hkv, int dh, unsigned long long* out) {
+  return guard([&] {
+    cudaStream_t st = e->stream;
+    const size_t nq = (size_t)M * H * dh, nk = (size_t)T * Hkv * dh;
+    DevBuf f((nq > nk ? nq : nk) * 4), qb(nq * 2), kb(nk * 2), vb(nk * 2), o(nq * 2), p(M * 4), tr(3 * 64 * 8 * 8);
+    k::init_uniform(st, f.as<float>(), nq, 11, 1.0f);
+    k::f32_to_bf16(st, qb.as<__nv_bfloat16>(), f.as<float>(), nq);
+    k::init_uniform(st, f.as<float>(), nk, 12, 1.0f);
+    k::f32_to_bf16(st, kb.as<__nv_bfloat16>(), f.as<float>(), nk);
+    k::init_uniform(st, f.as<float>(), nk, 13, 1.0f);
+    k::f32_to_bf16(st, vb.as<__nv_bfloat16>(), f.as<float>(), nk);
+    k::iota_positions(st, p.as<int>(), M, T - M);
+    RK_CUDA(cudaMemsetAsync(tr.p, 0, tr.bytes, st));
+    AttnArgs a;
+    a.q = qb.as<__nv_bfloat16>();
+    a.out = o.as<__nv_bfloat16>();
+    a.pos = p.as<int>();
+    a.rows_max = M;
+    a.H = H;
+    a.Hkv = Hkv;
+    a.dh = dh;
+    a.scale_log2 = 1.4426950408889634f / std::sqrt((float)dh);
+    attention_bf16(e, a, kb.as<__nv_bfloat16>(), vb.as<__nv_bfloat16>(), T);  // warm
+    a.trace = tr.as<unsigned long long>();
+    attention_bf16(e, a, kb.as<__nv_bfloat16>(), vb.as<__nv_bfloat16>(), T);
+    RK_CUDA(cudaStreamSynchronize(st));
+    RK_CUDA(cudaGetLastError());
+    RK_CUDA(cudaMemcpy(out, tr.p, tr.bytes, cudaMemcpyDeviceToHost));
+  });
+}
+
 int rk_debug_bench_gemm(rk_engine* e, int M, int N, int K, int epi, int iters, float* ms) {
   return guard([&] {
     cudaStream_t st = e->stream;

@@ -58,6 +58,10 @@ struct AttnArgs {
   int splits = 1, tiles_per_split = 1 << 20;
   float* ws_o = nullptr;
   float* ws_ml = nullptr;
+  // debug: clock64 timeline of the last CTA of head 0 ([role 0..2][step < 64][event < 8];
+  // roles: softmax group 0, group 1, MMA issuer)
+  unsigned long long* trace = nullptr;
+  int pingpong = 1;  // set by attention_bf16
 };
 // ctx_k / ctx_v: the layer's [ctx_rows x kv] bf16 context rows.
 void attention_bf16(rk_engine* e, const AttnArgs& a, const __nv_bfloat16* ctx_k, const __nv_bfloat16* ctx_v,
