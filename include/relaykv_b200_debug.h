@@ -27,6 +27,11 @@ int rk_debug_bench_attention(rk_engine* e, int M, int T, int H, int Hkv, int dh,
  * the band case: out[3 roles][64 steps][8 events] (see attn_sm100.cu). */
 int rk_debug_trace_attention(rk_engine* e, int M, int T, int H, int Hkv, int dh, unsigned long long* out);
 int rk_debug_bench_gemm(rk_engine* e, int M, int N, int K, int epi, int iters, float* ms);
+/* K2b selection (select_relay) on host-given scores: sorted indices + tags,
+ * count, dinfo = {exact threshold, min relative margin}. */
+int rk_debug_select_relay(rk_engine* e, const double* s_dev, const float* influence, double infl_mean, int n,
+                          double tau_dev, double tau_inf, int suffix_k, int32_t* sel_idx, uint32_t* sel_tags,
+                          int32_t* count, double* dinfo);
 /* y[i] = device glibc_expf(x[i]) */
 int rk_debug_expf(rk_engine* e, const float* x, float* y, uint64_t n);
 #ifdef __cplusplus

@@ -199,6 +199,29 @@ int rk_debug_bench_gemm(rk_engine* e, int M, int N, int K, int epi, int iters, f
   });
 }
 
+int rk_debug_select_relay(rk_engine* e, const double* s_dev, const float* influence, double infl_mean, int n,
+                          double tau_dev, double tau_inf, int suffix_k, int32_t* sel_idx, uint32_t* sel_tags,
+                          int32_t* count, double* dinfo) {
+  return guard([&] {
+    cudaStream_t st = e->stream;
+    DevBuf sd(n * 8), inf(n * 4), im(8), idx(n * 4), tags(2 * n * 4), info(64), di(64);
+    RK_CUDA(cudaMemcpy(sd.p, s_dev, n * 8, cudaMemcpyHostToDevice));
+    RK_CUDA(cudaMemcpy(inf.p, influence, n * 4, cudaMemcpyHostToDevice));
+    RK_CUDA(cudaMemcpy(im.p, &infl_mean, 8, cudaMemcpyHostToDevice));
+    RK_CUDA(cudaMemset(info.p, 0, 64));
+    k::select_relay(st, sd.as<double>(), inf.as<float>(), im.as<double>(), n, tau_dev, tau_inf, suffix_k,
+                    idx.as<int>(), tags.as<uint32_t>(), info.as<int>(), di.as<double>(), e->side, e->side_fork,
+                    e->side_join);
+    RK_CUDA(cudaStreamSynchronize(st));
+    RK_CUDA(cudaStreamSynchronize(e->side));
+    RK_CUDA(cudaGetLastError());
+    RK_CUDA(cudaMemcpy(count, info.p, 4, cudaMemcpyDeviceToHost));
+    RK_CUDA(cudaMemcpy(sel_idx, idx.p, (size_t)*count * 4, cudaMemcpyDeviceToHost));
+    RK_CUDA(cudaMemcpy(sel_tags, tags.p, (size_t)*count * 4, cudaMemcpyDeviceToHost));
+    RK_CUDA(cudaMemcpy(dinfo, di.p, 16, cudaMemcpyDeviceToHost));
+  });
+}
+
 int rk_debug_expf(rk_engine* e, const float* x, float* y, uint64_t n) {
   return guard([&] {
     DevBuf dx(n * 4), dy(n * 4);

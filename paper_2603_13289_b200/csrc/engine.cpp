@@ -126,6 +126,12 @@ rk_engine::~rk_engine() {
   scratch.reset();
   rope.clear();
   if (pinned) cudaFreeHost(pinned);
+  if (side) {
+    cudaStreamSynchronize(side);
+    cudaStreamDestroy(side);
+  }
+  if (side_fork) cudaEventDestroy(side_fork);
+  if (side_join) cudaEventDestroy(side_join);
   if (stream) cudaStreamDestroy(stream);
 }
 
@@ -310,6 +316,9 @@ int rk_engine_create(int device, rk_engine** out) {
     RK_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
     require(major == 10, RK_ERR_RUNTIME, "relaykv-b200 kernels are built for sm_100a (B200)");
     RK_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+    RK_CUDA(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
+    RK_CUDA(cudaEventCreateWithFlags(&e->side_fork, cudaEventDisableTiming));
+    RK_CUDA(cudaEventCreateWithFlags(&e->side_join, cudaEventDisableTiming));
     e->status.alloc(64);
     RK_CUDA(cudaMemset(e->status.p, 0, 64));
     e->pinned_bytes = 1 << 20;
@@ -329,6 +338,7 @@ int rk_engine_synchronize(rk_engine* e) {
   return guard([&] {
     DeviceGuard g(e->device);
     RK_CUDA(cudaStreamSynchronize(e->stream));
+    if (e->side) RK_CUDA(cudaStreamSynchronize(e->side));
   });
 }
 void* rk_engine_stream(rk_engine* e) { return e ? (void*)e->stream : nullptr; }

@@ -67,6 +67,9 @@ struct rk_engine {
   int device = 0;
   int sm_count = 0;
   cudaStream_t stream = nullptr;
+  // side stream for off-critical-path reporting kernels (joined at the next call)
+  cudaStream_t side = nullptr;
+  cudaEvent_t side_fork = nullptr, side_join = nullptr;
   uint64_t launches = 0;
   int use_graphs = 0;
   int fused = 1;  // layer-major fused agent schedule (runner.cpp agent_fused)
@@ -206,9 +209,12 @@ void realign_graft(cudaStream_t s, const void* k_pre, const void* v_src, size_t 
 void score_deviation(cudaStream_t s, const void* ctx_v, const void* cache_v, const void* ctx_k,
                      const void* cache_kpre, size_t elem, int n, int kv, int heads, int dh,
                      const double2* rope, int base, double* s_dev, double* s_key);
+// Selection (certified parallel threshold) on s; the exact reported threshold
+// and margin (dinfo) on `side` (forked from s via `fork`, recorded on `join`).
 void select_relay(cudaStream_t s, const double* s_dev, const float* influence,
                   const double* infl_mean, int n, double tau_dev, double tau_inf, int suffix_k,
-                  int* sel_idx, uint32_t* sel_tags, int* info, double* dinfo);
+                  int* sel_idx, uint32_t* sel_tags, int* info, double* dinfo, cudaStream_t side = nullptr,
+                  cudaEvent_t fork = nullptr, cudaEvent_t join = nullptr);
 void blend_scores(cudaStream_t s, const void* ctx_v, const void* cache_v, size_t elem, int n,
                   int kv, double* score);
 void select_topk(cudaStream_t s, const double* score, int n, int count, int* sel_idx,

@@ -242,6 +242,57 @@ __global__ void argmax_final_kernel(const float2* __restrict__ part, int parts, 
 // rounded (tensor.cpp:140-141); V is a bit copy. Layers [skip_lo, skip_hi]
 // are skipped (the band recompute overwrites them; relay_engine.cpp:261-264).
 // ---------------------------------------------------------------------------
+// Fast path for d_head 64/128: every index is a shift or mask except one
+// division per thread (the segment position, for the cos/sin row).
+template <typename T, int DH>
+__global__ void __launch_bounds__(256) realign_graft_dh_kernel(
+    const T* __restrict__ k_pre, const T* __restrict__ v_src, int n, int kv,
+    const double2* __restrict__ rope, int base, T* __restrict__ ctx_k, T* __restrict__ ctx_v,
+    size_t ctx_layer_stride, int skip_lo, int skip_hi) {
+  constexpr int VEC = 16 / sizeof(T);
+  int l = blockIdx.y;
+  if (skip_hi >= skip_lo && l >= skip_lo) l += skip_hi - skip_lo + 1;
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t e0 = t * VEC;  // element offset within the layer's [n x kv] block
+  if (e0 >= (size_t)n * kv) return;
+  const int p = (int)(e0 / (unsigned)kv);
+  const int pair0 = (int)(e0 & (DH - 1)) / 2;
+  const size_t src = (size_t)l * n * kv + e0;
+  const uint4 kraw = __ldcs(reinterpret_cast<const uint4*>(k_pre + src));
+  const uint4 vraw = __ldcs(reinterpret_cast<const uint4*>(v_src + src));
+  const size_t dst = (size_t)l * ctx_layer_stride + (size_t)base * kv + e0;
+  *reinterpret_cast<uint4*>(ctx_v + dst) = vraw;
+  const double2* cs = rope + (size_t)(base + p) * (DH / 2) + pair0;
+  double2 c_s[VEC / 2];
+#pragma unroll
+  for (int i = 0; i < VEC / 2; ++i) c_s[i] = cs[i];
+  const T* kin = reinterpret_cast<const T*>(&kraw);
+  uint4 kout_raw;
+  T* kout = reinterpret_cast<T*>(&kout_raw);
+#pragma unroll
+  for (int e = 0; e < VEC; e += 2) {
+    double x0, x1;
+    if constexpr (sizeof(T) == 4) {
+      x0 = (double)kin[e];
+      x1 = (double)kin[e + 1];
+    } else {
+      x0 = (double)__bfloat162float(kin[e]);
+      x1 = (double)__bfloat162float(kin[e + 1]);
+    }
+    const double2 c = c_s[e / 2];
+    const double r0 = __dsub_rn(__dmul_rn(c.x, x0), __dmul_rn(c.y, x1));
+    const double r1 = __dadd_rn(__dmul_rn(c.y, x0), __dmul_rn(c.x, x1));
+    if constexpr (sizeof(T) == 4) {
+      kout[e] = __double2float_rn(r0);
+      kout[e + 1] = __double2float_rn(r1);
+    } else {
+      kout[e] = __float2bfloat16_rn(__double2float_rn(r0));
+      kout[e + 1] = __float2bfloat16_rn(__double2float_rn(r1));
+    }
+  }
+  *reinterpret_cast<uint4*>(ctx_k + dst) = kout_raw;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) realign_graft_kernel(
     const T* __restrict__ k_pre, const T* __restrict__ v_src, int n, int kv, int dh,
@@ -386,6 +437,90 @@ __global__ void __launch_bounds__(256) score_kernel(const void* ctx_v, const voi
   }
 }
 
+// Fast path for d_head 64/128: one thread per (token, {V,K}, head) holds its
+// two head slices in registers (16-byte loads, all in flight at once) and runs
+// the reference's sequential double loops (cosine_d) on them; heads are then
+// summed in order through shared memory. Same operation order as
+// cosine_slice, so the scores are bit-identical.
+template <typename T, int DH>
+__device__ __forceinline__ float elem_f(const uint4 (&v)[DH * sizeof(T) / 16], int i) {
+  const T* p = reinterpret_cast<const T*>(&v[0]);
+  if constexpr (sizeof(T) == 4) return p[i];
+  else return __bfloat162float(p[i]);
+}
+
+template <typename T, int DH>
+__global__ void __launch_bounds__(256) score_dh_kernel(const T* __restrict__ ctx_v, const T* __restrict__ cache_v,
+                                                       const T* __restrict__ ctx_k, const T* __restrict__ cache_kpre,
+                                                       int n, int heads, const double2* __restrict__ rope,
+                                                       int base, double* __restrict__ s_dev,
+                                                       double* __restrict__ s_key) {
+  constexpr int NV = DH * sizeof(T) / 16;  // 16-byte vectors per head slice
+  extern __shared__ double cosv[];          // [tokens of this CTA][2][heads]
+  const int per_tok = 2 * heads;
+  const int tok = blockDim.x / per_tok;
+  const int t = threadIdx.x / per_tok, which = (threadIdx.x / heads) % 2, h = threadIdx.x % heads;
+  const int j = blockIdx.x * tok + t;
+  const int kv = heads * DH;
+  if (t < tok && j < n) {
+    const size_t off = (size_t)j * kv + (size_t)h * DH;
+    const T* a = which == 0 ? ctx_v : ctx_k;
+    const T* b = which == 0 ? cache_v : cache_kpre;
+    uint4 x[NV], y[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      x[i] = __ldcs(reinterpret_cast<const uint4*>(a + off) + i);
+      y[i] = __ldcs(reinterpret_cast<const uint4*>(b + off) + i);
+    }
+    const double2* cs = rope + (size_t)(base + j) * (DH / 2);
+    double dot = 0.0, na = 0.0, nb = 0.0;
+    bool same = true;
+#pragma unroll  // fully: the slices stay in registers (compile-time indices)
+    for (int i = 0; i < DH; i += 2) {
+      const float x0 = elem_f<T, DH>(x, i), x1 = elem_f<T, DH>(x, i + 1);
+      float y0 = elem_f<T, DH>(y, i), y1 = elem_f<T, DH>(y, i + 1);
+      if (which == 1) {  // realigned key, bit-identical to realign()
+        const double2 c = cs[i / 2];
+        const double r0 = __dsub_rn(__dmul_rn(c.x, (double)y0), __dmul_rn(c.y, (double)y1));
+        const double r1 = __dadd_rn(__dmul_rn(c.y, (double)y0), __dmul_rn(c.x, (double)y1));
+        y0 = __double2float_rn(r0);
+        y1 = __double2float_rn(r1);
+        if constexpr (sizeof(T) == 2) {
+          y0 = __bfloat162float(__float2bfloat16_rn(y0));
+          y1 = __bfloat162float(__float2bfloat16_rn(y1));
+        }
+      }
+      same = same && __float_as_uint(x0) == __float_as_uint(y0) && __float_as_uint(x1) == __float_as_uint(y1);
+      const double a0 = x0, a1 = x1, b0 = y0, b1 = y1;
+      dot = __dadd_rn(dot, __dmul_rn(a0, b0));
+      na = __dadd_rn(na, __dmul_rn(a0, a0));
+      nb = __dadd_rn(nb, __dmul_rn(b0, b0));
+      dot = __dadd_rn(dot, __dmul_rn(a1, b1));
+      na = __dadd_rn(na, __dmul_rn(a1, a1));
+      nb = __dadd_rn(nb, __dmul_rn(b1, b1));
+    }
+    const double sa = __dsqrt_rn(na), sb = __dsqrt_rn(nb);
+    double c;
+    if (sa < 1e-12 || sb < 1e-12) c = 0.0;
+    else if (same) c = 1.0;
+    else {
+      c = __ddiv_rn(dot, __dmul_rn(sa, sb));
+      c = c < -1.0 ? -1.0 : (c > 1.0 ? 1.0 : c);
+    }
+    cosv[(t * 2 + which) * heads + h] = c;
+  }
+  __syncthreads();
+  if (threadIdx.x < tok * 2) {
+    const int tt = threadIdx.x / 2, w = threadIdx.x % 2;
+    const int jj = blockIdx.x * tok + tt;
+    if (jj < n) {
+      double acc = 0.0;
+      for (int hh = 0; hh < heads; ++hh) acc = __dadd_rn(acc, cosv[(tt * 2 + w) * heads + hh]);
+      (w == 0 ? s_dev : s_key)[jj] = __dsub_rn(1.0, __ddiv_rn(acc, (double)heads));
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K2b selection (selector.cpp:32-88): mean-relative thresholds with the
 // reference's sequential double mean, suffix window, sorted union with tag
@@ -447,69 +582,146 @@ __device__ void block_compact(const uint32_t* flags_smem_unused, int n, const ui
   }
 }
 
-__global__ void __launch_bounds__(1024) select_relay_kernel(
-    const double* s_dev, const float* influence, const double* infl_mean, int n, double tau_dev,
-    double tau_inf, int suffix_k, uint32_t* flags, int* sel_idx, uint32_t* sel_tags, int* info,
-    double* dinfo) {
-  __shared__ double thr[2];
-  __shared__ int valid[2];
-  if (threadIdx.x < 32) {
-    // mean_relative (selector.cpp:37-39): sequential sum, then divide. Warp 0
-    // loads 4 x 32 values per round (coalesced, all in flight together); the
-    // dependent DADD chain then walks them in index order via shuffles, every
-    // lane computing the identical chain.
-    const int lane = threadIdx.x;
-    double mean = 0.0;
-    for (int b = 0; b < n; b += 128) {
-      double v[4];
+// mean_relative's threshold (selector.cpp:37-39): sequential double sum, then
+// divide, then tau * mean. Warp 0 loads 4 x 32 values per round (coalesced,
+// all in flight); the dependent DADD chain walks them in index order via
+// shuffles, every lane computing the identical chain.
+__device__ double seq_threshold_warp(const double* s_dev, int n, double tau, bool& valid) {
+  const int lane = threadIdx.x & 31;
+  double mean = 0.0;
+  for (int b = 0; b < n; b += 128) {
+    double v[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int j = b + u * 32 + lane;
-        v[u] = j < n ? s_dev[j] : 0.0;
-      }
+    for (int u = 0; u < 4; ++u) {
+      const int j = b + u * 32 + lane;
+      v[u] = j < n ? s_dev[j] : 0.0;
+    }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int lim = min(32, n - (b + u * 32));
+    for (int u = 0; u < 4; ++u) {
+      const int lim = min(32, n - (b + u * 32));
 #pragma unroll 8
-        for (int i = 0; i < 32; ++i) {
-          const double x = __shfl_sync(0xffffffffu, v[u], i);
-          if (i < lim) mean = __dadd_rn(mean, x);
-        }
+      for (int i = 0; i < 32; ++i) {
+        const double x = __shfl_sync(0xffffffffu, v[u], i);
+        if (i < lim) mean = __dadd_rn(mean, x);
       }
     }
-    mean = __ddiv_rn(mean, (double)n);
-    if (lane == 0) {
-      valid[0] = mean > 0.0;
-      thr[0] = __dmul_rn(tau_dev, mean);
-      const double mi = *infl_mean;
-      valid[1] = mi > 0.0;
-      thr[1] = __dmul_rn(tau_inf, mi);
+  }
+  mean = __ddiv_rn(mean, (double)n);
+  valid = mean > 0.0;
+  return __dmul_rn(tau, mean);
+}
+
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+  s = __dadd_rn(a, b);
+  const double bp = __dsub_rn(s, a);
+  e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bp)), __dsub_rn(b, bp));
+}
+
+// Selection with a certified parallel threshold: the sequential sum differs
+// from the exact sum by at most (n-1) u sum|s_j| (u = 2^-53), and the divide
+// and tau-multiply add two roundings. The exact sum comes from a compensated
+// (TwoSum) block reduction; any token within that bound of the threshold
+// sends the block to the reference's sequential order (rare), otherwise every
+// decision s_j >= thr equals the reference's. The exact reported threshold
+// and margin are computed off the critical path (seq_threshold_report_kernel
+// on the engine's side stream).
+__global__ void __launch_bounds__(1024) select_relay_kernel(
+    const double* s_dev, const float* influence, const double* infl_mean, int n, double tau_dev,
+    double tau_inf, int suffix_k, uint32_t* flags, int* sel_idx, uint32_t* sel_tags, int* info) {
+  __shared__ double thr[2], margin_abs;
+  __shared__ int valid[2], uncertain;
+  __shared__ double red_hi[32], red_lo[32];
+  double hi = 0.0, lo = 0.0;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    double e;
+    two_sum(hi, s_dev[j], hi, e);
+    lo = __dadd_rn(lo, e);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double h2 = __shfl_xor_sync(0xffffffffu, hi, o), l2 = __shfl_xor_sync(0xffffffffu, lo, o);
+    double e;
+    two_sum(hi, h2, hi, e);
+    lo = __dadd_rn(__dadd_rn(lo, l2), e);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red_hi[threadIdx.x >> 5] = hi;
+    red_lo[threadIdx.x >> 5] = lo;
+  }
+  if (threadIdx.x == 0) uncertain = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double H = 0.0, Lo = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      double e;
+      two_sum(H, red_hi[w], H, e);
+      Lo = __dadd_rn(__dadd_rn(Lo, red_lo[w]), e);
+    }
+    const double S = __dadd_rn(H, Lo);  // s_dev >= 0: S > 0 iff some s_j > 0 iff the sequential mean > 0
+    valid[0] = S > 0.0;
+    thr[0] = __dmul_rn(tau_dev, __ddiv_rn(S, (double)n));
+    margin_abs = __dmul_rn(thr[0], ((double)n + 16.0) * 2.3e-16);
+    const double mi = *infl_mean;
+    valid[1] = mi > 0.0;
+    thr[1] = __dmul_rn(tau_inf, mi);
+  }
+  __syncthreads();
+  if (valid[0]) {
+    bool near = false;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) near |= fabs(__dsub_rn(s_dev[j], thr[0])) <= margin_abs;
+    if (__any_sync(0xffffffffu, near) && (threadIdx.x & 31) == 0) atomicOr(&uncertain, 1);
+  }
+  __syncthreads();
+  if (uncertain && threadIdx.x < 32) {  // fall back to the reference's sequential order
+    bool v;
+    const double t = seq_threshold_warp(s_dev, n, tau_dev, v);
+    if (threadIdx.x == 0) {
+      thr[0] = t;
+      valid[0] = v;
     }
   }
   __syncthreads();
   const int start = suffix_k >= n ? 0 : n - suffix_k;
-  double margin = 1e300;
   for (int j = threadIdx.x; j < n; j += blockDim.x) {
     uint32_t f = 0;
-    const double s = s_dev[j];
-    if (valid[0] && s >= thr[0]) f |= RK_SEL_DEVIATION;
+    if (valid[0] && s_dev[j] >= thr[0]) f |= RK_SEL_DEVIATION;
     if (valid[1] && (double)influence[j] >= thr[1]) f |= RK_SEL_INFLUENCE_SCORE;
     if (suffix_k > 0 && j >= start) f |= RK_SEL_INFLUENCE_SUFFIX;
     flags[j] = f;
-    if (valid[0]) margin = fmin(margin, fabs(s - thr[0]) / thr[0]);
   }
+  __syncthreads();
+  block_compact(nullptr, n, flags, sel_idx, sel_tags, info);
+}
+
+// Reported values (rk_relay_output::dev_threshold / min_dev_margin): the
+// reference's exact sequential threshold and the smallest relative distance of
+// any score to it. Runs on the side stream, concurrent with the next layers.
+// dinfo: [0] threshold (0 if none) [1] min relative margin
+__global__ void __launch_bounds__(1024) seq_threshold_report_kernel(const double* s_dev, int n, double tau_dev,
+                                                                    double* dinfo) {
+  __shared__ double thr;
+  __shared__ int valid;
   __shared__ double mred[32];
+  if (threadIdx.x < 32) {
+    bool v;
+    const double t = seq_threshold_warp(s_dev, n, tau_dev, v);
+    if (threadIdx.x == 0) {
+      thr = t;
+      valid = v;
+    }
+  }
+  __syncthreads();
+  double margin = 1e300;
+  if (valid)
+    for (int j = threadIdx.x; j < n; j += blockDim.x) margin = fmin(margin, fabs(s_dev[j] - thr) / thr);
   for (int o = 16; o > 0; o >>= 1) margin = fmin(margin, __shfl_xor_sync(0xffffffffu, margin, o));
   if ((threadIdx.x & 31) == 0) mred[threadIdx.x >> 5] = margin;
   __syncthreads();
   if (threadIdx.x == 0) {
     double m = 1e300;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmin(m, mred[w]);
-    dinfo[0] = valid[0] ? thr[0] : 0.0;
-    dinfo[1] = valid[0] ? m : __longlong_as_double(0x7ff0000000000000LL);
+    dinfo[0] = valid ? thr : 0.0;
+    dinfo[1] = valid ? m : __longlong_as_double(0x7ff0000000000000LL);
   }
-  __syncthreads();
-  block_compact(nullptr, n, flags, sel_idx, sel_tags, info);
 }
 
 // BLEND score (relay_engine.cpp:318-330): L2 norm of fresh-vs-stale V at layer 1.
@@ -645,7 +857,14 @@ void realign_graft(cudaStream_t s, const void* k_pre, const void* v_src, size_t 
   if (layers <= 0 || n <= 0) return;
   const size_t vecs = (size_t)n * (kv * elem / 16);
   dim3 grid((unsigned)((vecs + 255) / 256), (unsigned)layers);
-  if (elem == 4)
+#define RK_REALIGN_DH(T, D)                                                                                  \
+  realign_graft_dh_kernel<T, D><<<grid, 256, 0, s>>>((const T*)k_pre, (const T*)v_src, n, kv, rope, base,     \
+                                                     (T*)ctx_k, (T*)ctx_v, ctx_layer_stride, skip_lo, skip_hi)
+  if (elem == 4 && dh == 64) RK_REALIGN_DH(float, 64);
+  else if (elem == 4 && dh == 128) RK_REALIGN_DH(float, 128);
+  else if (elem == 2 && dh == 64) RK_REALIGN_DH(__nv_bfloat16, 64);
+  else if (elem == 2 && dh == 128) RK_REALIGN_DH(__nv_bfloat16, 128);
+  else if (elem == 4)
     realign_graft_kernel<float><<<grid, 256, 0, s>>>(
         (const float*)k_pre, (const float*)v_src, n, kv, dh, rope, base, (float*)ctx_k,
         (float*)ctx_v, ctx_layer_stride, skip_lo, skip_hi);
@@ -653,6 +872,7 @@ void realign_graft(cudaStream_t s, const void* k_pre, const void* v_src, size_t 
     realign_graft_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(
         (const __nv_bfloat16*)k_pre, (const __nv_bfloat16*)v_src, n, kv, dh, rope, base,
         (__nv_bfloat16*)ctx_k, (__nv_bfloat16*)ctx_v, ctx_layer_stride, skip_lo, skip_hi);
+#undef RK_REALIGN_DH
 }
 
 void score_deviation(cudaStream_t s, const void* ctx_v, const void* cache_v, const void* ctx_k,
@@ -660,6 +880,22 @@ void score_deviation(cudaStream_t s, const void* ctx_v, const void* cache_v, con
                      const double2* rope, int base, double* s_dev, double* s_key) {
   if (n <= 0) return;
   const size_t row = (size_t)kv * elem;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(ctx_v) | reinterpret_cast<uintptr_t>(cache_v) |
+                         reinterpret_cast<uintptr_t>(ctx_k) | reinterpret_cast<uintptr_t>(cache_kpre)) & 15) == 0;
+  if (aligned && (dh == 64 || dh == 128) && 2 * heads <= 256) {
+    const int tok = 256 / (2 * heads);
+    const size_t smem = (size_t)tok * 2 * heads * sizeof(double);
+    const int grid = (n + tok - 1) / tok;
+#define RK_SCORE_DH(T, D)                                                                                      \
+  score_dh_kernel<T, D><<<grid, 256, smem, s>>>((const T*)ctx_v, (const T*)cache_v, (const T*)ctx_k,          \
+                                                (const T*)cache_kpre, n, heads, rope, base, s_dev, s_key)
+    if (elem == 4 && dh == 64) RK_SCORE_DH(float, 64);
+    else if (elem == 4) RK_SCORE_DH(float, 128);
+    else if (dh == 64) RK_SCORE_DH(__nv_bfloat16, 64);
+    else RK_SCORE_DH(__nv_bfloat16, 128);
+#undef RK_SCORE_DH
+    return;
+  }
   int tok = (int)std::min<size_t>(16, std::max<size_t>(1, 40960 / (4 * row)));
   const size_t smem = 4 * row * tok + (size_t)tok * 2 * heads * sizeof(double);
   if (smem > 48 * 1024) {
@@ -675,10 +911,19 @@ void score_deviation(cudaStream_t s, const void* ctx_v, const void* cache_v, con
 
 void select_relay(cudaStream_t s, const double* s_dev, const float* influence,
                   const double* infl_mean, int n, double tau_dev, double tau_inf, int suffix_k,
-                  int* sel_idx, uint32_t* sel_tags, int* info, double* dinfo) {
+                  int* sel_idx, uint32_t* sel_tags, int* info, double* dinfo, cudaStream_t side,
+                  cudaEvent_t fork, cudaEvent_t join) {
   // flags scratch lives after sel_tags (caller sizes sel_tags to 2n)
-  select_relay_kernel<<<1, 1024, 0, s>>>(s_dev, influence, infl_mean, n, tau_dev, tau_inf,
-                                         suffix_k, sel_tags + n, sel_idx, sel_tags, info, dinfo);
+  if (side) {
+    RK_CUDA(cudaEventRecord(fork, s));
+    RK_CUDA(cudaStreamWaitEvent(side, fork, 0));
+    seq_threshold_report_kernel<<<1, 1024, 0, side>>>(s_dev, n, tau_dev, dinfo);
+    RK_CUDA(cudaEventRecord(join, side));
+  } else {
+    seq_threshold_report_kernel<<<1, 1024, 0, s>>>(s_dev, n, tau_dev, dinfo);
+  }
+  select_relay_kernel<<<1, 1024, 0, s>>>(s_dev, influence, infl_mean, n, tau_dev, tau_inf, suffix_k, sel_tags + n,
+                                         sel_idx, sel_tags, info);
 }
 void blend_scores(cudaStream_t s, const void* ctx_v, const void* cache_v, size_t elem, int n,
                   int kv, double* score) {

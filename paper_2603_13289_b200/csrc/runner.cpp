@@ -23,6 +23,9 @@ Runner::Runner(rk_engine* e, rk_weights* w) : e_(e), w_(w), st_(e->stream) {
   require(e != nullptr && w != nullptr, RK_ERR_INVALID_ARGUMENT, "null engine / weights");
   require(w->e == e, RK_ERR_INVALID_ARGUMENT, "weights belong to another engine");
   RK_CUDA(cudaMemsetAsync(e->status.p, 0, 64, st_));
+  // side-stream reporting work of the previous call must finish before its
+  // buffers (selection slots) are reused
+  if (e->side_join) RK_CUDA(cudaStreamWaitEvent(st_, e->side_join, 0));
 }
 Runner::~Runner() = default;
 
@@ -363,7 +366,9 @@ ExtendResult Runner::relay_extend(rk_context* ctx, rk_cache* cache, const rk_lay
           ProfScope ps(e_, "select_relay", 0, n * 20.0);
           k::select_relay(st_, X.s_dev.as<double>(), cache->influence.as<float>(), cache->infl_mean.as<double>(),
                           (int)n, opts.tau_dev, opts.tau_inf, (int)std::min<uint64_t>(opts.suffix_k, 0x7fffffff),
-                          X.sel_idx.as<int>(), X.sel_tags.as<uint32_t>(), X.info.as<int>(), X.dinfo.as<double>());
+                          X.sel_idx.as<int>(), X.sel_tags.as<uint32_t>(), X.info.as<int>(), X.dinfo.as<double>(),
+                          e_->side, e_->side_fork, e_->side_join);
+          e_->launches += 1;  // the side-stream report kernel
         }
         e_->launches += 2;
       } else {
@@ -650,7 +655,9 @@ void Runner::agent_fused(rk_context* ctx, const int32_t* prefix, uint64_t P, rk_
           ProfScope ps(e_, "select_relay", 0, n[u] * 20.0);
           k::select_relay(st_, X.s_dev.as<double>(), c->influence.as<float>(), c->infl_mean.as<double>(),
                           (int)n[u], opts.tau_dev, opts.tau_inf, (int)std::min<uint64_t>(opts.suffix_k, 0x7fffffff),
-                          X.sel_idx.as<int>(), X.sel_tags.as<uint32_t>(), X.info.as<int>(), X.dinfo.as<double>());
+                          X.sel_idx.as<int>(), X.sel_tags.as<uint32_t>(), X.info.as<int>(), X.dinfo.as<double>(),
+                          e_->side, e_->side_fork, e_->side_join);
+          e_->launches += 1;  // the side-stream report kernel
         } else {
           k::blend_scores(st_, ctx_v_det, cache_v_det, el, (int)n[u], (int)kv, X.score.as<double>());
           size_t count = static_cast<size_t>(opts.blend_alpha * static_cast<double>(n[u]));
@@ -838,6 +845,7 @@ rk_cache* Runner::capture_decode(rk_context* ctx, const float* first_logits, uin
 // ---------------------------------------------------------------------------
 void Runner::finish() {
   RK_CUDA(cudaStreamSynchronize(st_));
+  if (e_->side) RK_CUDA(cudaStreamSynchronize(e_->side));
   RK_CUDA(cudaGetLastError());
   int flags[2] = {0, 0};
   RK_CUDA(cudaMemcpy(flags, e_->status.p, sizeof flags, cudaMemcpyDeviceToHost));

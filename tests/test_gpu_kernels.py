@@ -137,3 +137,62 @@ def test_device_expf_matches_host_libm(engine):
     _check(lib().rk_debug_expf(P(engine.ptr), x.ctypes.data_as(F32P), got.ctypes.data_as(F32P), C.c_uint64(x.size)))
     bad = np.flatnonzero(got.view(np.uint32) != want.view(np.uint32))
     assert bad.size == 0, f"{bad.size} mismatches, first x={x[bad[0]]!r}"
+
+
+def ref_select(s_dev, infl, infl_mean, tau_dev, tau_inf, suffix_k):
+    """selector.cpp:32-88 in plain Python (sequential double mean)."""
+    n = len(s_dev)
+    mean = 0.0
+    for x in s_dev:
+        mean += float(x)
+    mean /= n
+    thr = tau_dev * mean
+    tags = {}
+    if mean > 0:
+        for j, x in enumerate(s_dev):
+            if float(x) >= thr:
+                tags[j] = tags.get(j, 0) | 1
+    if infl_mean > 0:
+        ti = tau_inf * infl_mean
+        for j, x in enumerate(infl):
+            if float(x) >= ti:
+                tags[j] = tags.get(j, 0) | 2
+    for j in range(max(0, n - suffix_k), n):
+        tags[j] = tags.get(j, 0) | 4
+    idx = sorted(tags)
+    return np.array(idx, np.int32), np.array([tags[j] for j in idx], np.uint32), thr
+
+
+@pytest.mark.parametrize("case", ["random", "ties", "zeros", "big"])
+def test_select_certified_threshold(engine, case):
+    """The certified parallel threshold must reproduce the sequential-mean
+    selection bit for bit, including scores placed exactly on (and one ulp
+    below) the reference's sequential threshold, which forces the fallback."""
+    rng = np.random.default_rng(7)
+    n = {"random": 1856, "ties": 1000, "zeros": 300, "big": 40000}[case]
+    s = rng.random(n) * 0.02
+    if case == "zeros":
+        s[:] = 0.0
+    infl = rng.random(n).astype(np.float32)
+    infl_mean = float(np.mean(infl.astype(np.float64)))
+    if case == "ties":
+        _, _, thr = ref_select(s, infl, infl_mean, 1.5, 1.45, 10)
+        for _ in range(8):  # the mean moves when scores change: iterate to a fixed point
+            s[5] = thr
+            s[6] = np.nextafter(thr, 0.0)
+            s[7] = np.nextafter(thr, 1.0)
+            _, _, thr = ref_select(s, infl, infl_mean, 1.5, 1.45, 10)
+    want_idx, want_tags, thr = ref_select(s, infl, infl_mean, 1.5, 1.45, 10)
+    idx = np.zeros(n, np.int32)
+    tags = np.zeros(n, np.uint32)
+    cnt = C.c_int32(0)
+    dinfo = np.zeros(2, np.float64)
+    _check(lib().rk_debug_select_relay(P(engine.ptr), s.ctypes.data_as(C.POINTER(C.c_double)),
+                                       infl.ctypes.data_as(F32P), C.c_double(infl_mean), n, C.c_double(1.5),
+                                       C.c_double(1.45), 10, idx.ctypes.data_as(C.POINTER(C.c_int32)),
+                                       tags.ctypes.data_as(C.POINTER(C.c_uint32)), C.byref(cnt),
+                                       dinfo.ctypes.data_as(C.POINTER(C.c_double))))
+    assert np.array_equal(idx[:cnt.value], want_idx)
+    assert np.array_equal(tags[:cnt.value], want_tags)
+    if case != "zeros":
+        assert dinfo[0] == thr, (dinfo[0], thr)
