@@ -233,8 +233,10 @@ void pack_tensor(rk_weights* w, size_t idx, const float* src) {
     else RK_CUDA(cudaMemcpyAsync(dst, src, n * 4, cudaMemcpyDeviceToDevice, st));
   };
   // exact: dst[r][c0 + c*cs] (row length ldd); bf16: transposed dst[c0 + c*cs][r] (row length ld_t)
-  auto place = [&](void* dst, size_t ldd, size_t c0, size_t cs, size_t ld_t) {
-    if (bf) k::transpose_to_bf16(st, static_cast<__nv_bfloat16*>(dst), ld_t, c0, cs, src, td.rows, td.cols);
+  // bf16: the RMSNorm gain feeding W_q/W_k/W_v (attn_norm) or W_gate/W_up
+  // (mlp_norm) is folded into the weight rows; the GEMM epilogue applies 1/rms
+  auto place = [&](void* dst, size_t ldd, size_t c0, size_t cs, size_t ld_t, const float* gain = nullptr) {
+    if (bf) k::transpose_to_bf16(st, static_cast<__nv_bfloat16*>(dst), ld_t, c0, cs, src, td.rows, td.cols, gain);
     else k::copy_cols_f32(st, static_cast<float*>(dst), ldd, c0, src, td.cols, td.rows, td.cols, cs);
   };
   if (idx == 0) { copy_plain(w->emb, V * d); return; }
@@ -243,13 +245,13 @@ void pack_tensor(rk_weights* w, size_t idx, const float* src) {
     rk_layer_dev& ly = w->layers[i / 9];
     switch (i % 9) {
       case 0: RK_CUDA(cudaMemcpyAsync(ly.attn_norm, src, d * 4, cudaMemcpyDeviceToDevice, st)); break;
-      case 1: place(ly.w_qkv, q + 2 * kv, 0, 1, d); break;
-      case 2: place(ly.w_qkv, q + 2 * kv, q, 1, d); break;
-      case 3: place(ly.w_qkv, q + 2 * kv, q + kv, 1, d); break;
+      case 1: place(ly.w_qkv, q + 2 * kv, 0, 1, d, ly.attn_norm); break;
+      case 2: place(ly.w_qkv, q + 2 * kv, q, 1, d, ly.attn_norm); break;
+      case 3: place(ly.w_qkv, q + 2 * kv, q + kv, 1, d, ly.attn_norm); break;
       case 4: place(ly.w_o, d, 0, 1, q); break;
       case 5: RK_CUDA(cudaMemcpyAsync(ly.mlp_norm, src, d * 4, cudaMemcpyDeviceToDevice, st)); break;
-      case 6: place(ly.w_gu, 2 * ff, 0, 2, d); break;
-      case 7: place(ly.w_gu, 2 * ff, 1, 2, d); break;
+      case 6: place(ly.w_gu, 2 * ff, 0, 2, d, ly.mlp_norm); break;
+      case 7: place(ly.w_gu, 2 * ff, 1, 2, d, ly.mlp_norm); break;
       default: place(ly.w_down, d, 0, 1, ff); break;
     }
     return;

@@ -85,10 +85,11 @@ __device__ __forceinline__ void decode_unit(const Units& u, int unit, int& mt, i
 }
 
 template <int EPI>
-__device__ __forceinline__ void epilogue_chunk(const GemmArgs& p, int row, int col, const uint32_t (&r)[32]) {
+__device__ __forceinline__ void epilogue_chunk(const GemmArgs& p, int row, int col, const uint32_t (&r)[32],
+                                               float rs) {
   float v[32];
 #pragma unroll
-  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * rs;
   if constexpr (EPI == EPI_F32) {
     float4* dst = reinterpret_cast<float4*>(p.out_f32 + (size_t)row * p.ld_out + col);
 #pragma unroll
@@ -265,6 +266,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // the accumulator is even ready, so the load latency overlaps the MMAs
         constexpr int NCH = BN / 32, D = NCH < 4 ? NCH : 4;
         const bool live = row < M;
+        const bool norm = p.norm_part != nullptr && s + 1 == U.splits;  // final values: fused RMSNorm stats
+        float ss = 0.f;
         float4* hrow = reinterpret_cast<float4*>(p.out_f32 + (size_t)(live ? row : 0) * p.ld_out + nt * BN);
         float4 hb[D][8];
 #pragma unroll
@@ -286,6 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < 8; ++j) hb[c % D][j] = __ldcg(hrow + (c + D) * 8 + j);
           }
           if (live) {
+            uint32_t hb16[16];
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
               float4 h = cur[j];
@@ -294,18 +298,45 @@ __global__ void __launch_bounds__(kThreads, 1)
               h.z += __uint_as_float(r[4 * j + 2]);
               h.w += __uint_as_float(r[4 * j + 3]);
               hrow[c * 8 + j] = h;
+              ss = fmaf(h.x, h.x, fmaf(h.y, h.y, fmaf(h.z, h.z, fmaf(h.w, h.w, ss))));
+              hb16[2 * j] = pack_bf16(h.x, h.y);
+              hb16[2 * j + 1] = pack_bf16(h.z, h.w);
             }
+            if (norm) {
+              uint4* d16 = reinterpret_cast<uint4*>(p.norm_bf16 + (size_t)row * p.N + nt * BN + c * 32);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) d16[j] = make_uint4(hb16[4 * j], hb16[4 * j + 1], hb16[4 * j + 2], hb16[4 * j + 3]);
+            }
+          }
+        }
+        if (norm) {
+          if (live) p.norm_part[(size_t)row * kNormSlots + nt] = ss;
+          // the last of the num_n tiles of these 32 rows turns partials into 1/rms
+          __threadfence();
+          __syncwarp();
+          int done = 0;
+          if (lane == 0) done = atomicAdd(p.norm_cnt + (size_t)mt * 4 + quarter, 1) + 1;
+          done = __shfl_sync(0xffffffffu, done, 0);
+          if (done == U.num_n) {
+            __threadfence();
+            if (live) {
+              float tot = 0.f;
+              for (int t = 0; t < U.num_n; ++t) tot += __ldcg(p.norm_part + (size_t)row * kNormSlots + t);
+              p.norm_inv[row] = rsqrtf(tot / (float)p.N + p.norm_eps);
+            }
+            if (lane == 0) p.norm_cnt[(size_t)mt * 4 + quarter] = 0;
           }
         }
       } else {
         mbar_wait(&tfull[acc], (local >> 1) & 1);
         tc_fence_after();
+        const float rs = (p.row_scale && row < M) ? p.row_scale[row] : 1.0f;
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
           uint32_t r[32];
           tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN + c, r);
           tmem_ld_wait();
-          if (row < M) epilogue_chunk<EPI>(p, row, nt * BN + c, r);
+          if (row < M) epilogue_chunk<EPI>(p, row, nt * BN + c, r, rs);
         }
       }
       tc_fence_before();
@@ -395,6 +426,7 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
   if (p.rows_max <= 0) return;
   if (p.K % kBK) raise(RK_ERR_INVALID_ARGUMENT, "bf16 GEMM needs K % 64 == 0");
   choose_config(p, e->sm_count, rows_hint > 0 ? rows_hint : p.rows_max);
+  if (p.norm_part && p.N / p.bn > kNormSlots) raise(RK_ERR_INVALID_ARGUMENT, "fused RMSNorm: too many N tiles");
   CUtensorMap ta, tb;
   make_tmap_bf16(&ta, A, (uint64_t)p.rows_max, (uint64_t)p.K, kBM, (uint64_t)lda);
   make_tmap_bf16(&tb, B, (uint64_t)p.N, (uint64_t)p.K, (uint32_t)p.bn, (uint64_t)p.K);

@@ -156,6 +156,7 @@ struct Scratch {
   DevBuf hidden, sub_hidden, normed, qkv, attn, act, logits, tokens, positions, sub_positions;
   DevBuf s_dev, s_key, sel_idx, sel_tags, sel_info, depth, argmax, seg_hidden_out;
   DevBuf gemm_tmp, attn_ws;
+  DevBuf norm_inv, norm_part, norm_cnt;  // fused RMSNorm (layer_bf16.cu)
 };
 
 RopeTable* rope_table(rk_engine* e, float theta, uint64_t d_head, uint64_t positions);
@@ -182,7 +183,7 @@ void copy_cols_f32(cudaStream_t s, float* dst, size_t ldd, size_t c0, const floa
                    size_t rows, size_t cols, size_t dst_col_stride);
 // dst[(c0 + c*cstride) * ldd + r] = bf16(src[r * lds + c])  (transpose to K-major bf16)
 void transpose_to_bf16(cudaStream_t s, __nv_bfloat16* dst, size_t ldd, size_t c0, size_t cstride,
-                       const float* src, size_t rows, size_t cols);
+                       const float* src, size_t rows, size_t cols, const float* row_gain = nullptr);
 void f32_to_bf16(cudaStream_t s, __nv_bfloat16* dst, const float* src, size_t n);
 void bf16_to_f32(cudaStream_t s, float* dst, const __nv_bfloat16* src, size_t n);
 
@@ -248,7 +249,7 @@ void influence_accum(cudaStream_t s, double* acc, const float* probs, Rows rows,
 void copy2d_f32(cudaStream_t s, float* dst, size_t dld, size_t dcs, const float* src, size_t sld,
                 size_t scs, size_t rows, size_t cols);
 void untranspose_bf16(cudaStream_t s, float* dst, const __nv_bfloat16* src, size_t ld, size_t c0,
-                      size_t cstride, size_t rows, size_t cols);
+                      size_t cstride, size_t rows, size_t cols, const float* row_gain = nullptr);
 void doubles_to_floats(cudaStream_t s, float* dst, const double* src, int n);
 
 // bf16 tensor-core path

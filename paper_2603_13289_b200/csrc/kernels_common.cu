@@ -66,13 +66,17 @@ __global__ void copy_cols_kernel(float* dst, size_t ldd, size_t c0, const float*
 }
 
 // src [rows x cols] row-major fp32 -> dst row (c0 + c*cstride), column r, bf16.
+// row_gain (optional, [rows]): src row r is multiplied by row_gain[r] (a
+// RMSNorm gain folded into the weight that consumes the normalised rows).
 __global__ void transpose_bf16_kernel(__nv_bfloat16* dst, size_t ldd, size_t c0, size_t cstride,
-                                      const float* src, size_t rows, size_t cols) {
+                                      const float* src, size_t rows, size_t cols, const float* row_gain) {
   __shared__ float tile[32][33];
   const size_t bc = blockIdx.x * 32, br = blockIdx.y * 32;
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
     const size_t r = br + i, c = bc + threadIdx.x;
-    tile[i][threadIdx.x] = (r < rows && c < cols) ? src[r * cols + c] : 0.f;
+    float v = (r < rows && c < cols) ? src[r * cols + c] : 0.f;
+    if (row_gain && r < rows) v = __fmul_rn(v, row_gain[r]);
+    tile[i][threadIdx.x] = v;
   }
   __syncthreads();
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
@@ -92,12 +96,14 @@ __global__ void copy2d_kernel(float* dst, size_t dld, size_t dcs, const float* s
 }
 // dst[r][c] = float(src[(c0 + c*cstride) * ld + r])
 __global__ void untranspose_bf16_kernel(float* dst, const __nv_bfloat16* src, size_t ld, size_t c0,
-                                        size_t cstride, size_t rows, size_t cols) {
+                                        size_t cstride, size_t rows, size_t cols, const float* row_gain) {
   const size_t total = rows * cols;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
        i += (size_t)gridDim.x * blockDim.x) {
     const size_t r = i / cols, c = i % cols;
-    dst[i] = __bfloat162float(src[(c0 + c * cstride) * ld + r]);
+    float v = __bfloat162float(src[(c0 + c * cstride) * ld + r]);
+    if (row_gain && row_gain[r] != 0.f) v = __fdiv_rn(v, row_gain[r]);
+    dst[i] = v;
   }
 }
 __global__ void d2f_kernel(float* dst, const double* src, int n) {
@@ -785,9 +791,9 @@ void copy_cols_f32(cudaStream_t s, float* dst, size_t ldd, size_t c0, const floa
   copy_cols_kernel<<<blocks_for(n) < 8192 ? blocks_for(n) : 8192, kThreads, 0, s>>>(dst, ldd, c0, src, lds, rows, cols, cstride);
 }
 void transpose_to_bf16(cudaStream_t s, __nv_bfloat16* dst, size_t ldd, size_t c0, size_t cstride,
-                       const float* src, size_t rows, size_t cols) {
+                       const float* src, size_t rows, size_t cols, const float* row_gain) {
   dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
-  transpose_bf16_kernel<<<grid, dim3(32, 8), 0, s>>>(dst, ldd, c0, cstride, src, rows, cols);
+  transpose_bf16_kernel<<<grid, dim3(32, 8), 0, s>>>(dst, ldd, c0, cstride, src, rows, cols, row_gain);
 }
 void f32_to_bf16(cudaStream_t s, __nv_bfloat16* dst, const float* src, size_t n) {
   f32_to_bf16_kernel<<<blocks_for(n) < 8192 ? blocks_for(n) : 8192, kThreads, 0, s>>>(dst, src, n);
@@ -801,9 +807,9 @@ void copy2d_f32(cudaStream_t s, float* dst, size_t dld, size_t dcs, const float*
   copy2d_kernel<<<blocks_for(n) < 8192 ? blocks_for(n) : 8192, kThreads, 0, s>>>(dst, dld, dcs, src, sld, scs, rows, cols);
 }
 void untranspose_bf16(cudaStream_t s, float* dst, const __nv_bfloat16* src, size_t ld, size_t c0,
-                      size_t cstride, size_t rows, size_t cols) {
+                      size_t cstride, size_t rows, size_t cols, const float* row_gain) {
   const size_t n = rows * cols;
-  untranspose_bf16_kernel<<<blocks_for(n) < 8192 ? blocks_for(n) : 8192, kThreads, 0, s>>>(dst, src, ld, c0, cstride, rows, cols);
+  untranspose_bf16_kernel<<<blocks_for(n) < 8192 ? blocks_for(n) : 8192, kThreads, 0, s>>>(dst, src, ld, c0, cstride, rows, cols, row_gain);
 }
 void doubles_to_floats(cudaStream_t s, float* dst, const double* src, int n) {
   d2f_kernel<<<blocks_for(n), kThreads, 0, s>>>(dst, src, n);

@@ -91,15 +91,20 @@ class Runner {
   int tok_cursor_ = 0;
   float* cap_k_ = nullptr;  // capture destinations for pre-RoPE K / V rows
   float* cap_v_ = nullptr;
+  // bf16 path: the last layer left its rows' fused-RMSNorm inputs (bf16 rows,
+  // 1/rms) for the same row set; cleared whenever the rows or hidden change.
+  bool prepared_ = false;
 };
 
 // weights_export helper: unpack tensor idx of the engine layout to fp32 [rows x cols].
 void layer_unpack_tensor(rk_weights* w, size_t idx, float* dst, size_t rows, size_t cols);
 
 // bf16 layer path (layer_bf16.cu)
+// prepared: the rows' bf16 copy and 1/rms were left by the previous layer's
+// residual GEMM (same row set); otherwise they are computed first.
 void run_layer_bf16(rk_engine* e, rk_weights* w, rk_context* ctx, int layer, float* hidden,
                     Rows rows, bool commit, int max_ctx, float* probs, int key_lo, int key_n,
-                    void* cap_k, void* cap_v);
+                    void* cap_k, void* cap_v, bool prepared);
 void last_row_logits_bf16(rk_engine* e, rk_weights* w, const float* hidden_row, float* logits);
 
 }  // namespace rk

@@ -38,6 +38,28 @@ __global__ void rmsnorm_bf16_kernel(const float* __restrict__ x, const float* __
   }
 }
 
+// First layer of a row set (rows not produced by the previous residual GEMM):
+// bf16 copy of the residual rows (the GEMM operand; the norm gain is folded
+// into the weights) and 1/rms per row, applied in the consumer's epilogue.
+__global__ void norm_prep_kernel(const float* __restrict__ x, float eps, __nv_bfloat16* __restrict__ out,
+                                 float* __restrict__ inv, Rows rows, int d) {
+  const int M = live(rows);
+  const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (row >= M) return;
+  const float4* xr = reinterpret_cast<const float4*>(x + (size_t)row * d);
+  uint2* o = reinterpret_cast<uint2*>(out + (size_t)row * d);
+  float ss = 0.f;
+  for (int i = lane; i < d / 4; i += 32) {
+    const float4 v = xr[i];
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+    __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    o[i] = make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
+  }
+  for (int m = 16; m; m >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, m);
+  if (lane == 0) inv[row] = rsqrtf(ss / (float)d + eps);
+}
+
 // Pure-query pass (row_logits_from_layer, model.cpp:339-362): the row's own
 // context cell is temporarily replaced by its fresh K/V and restored after
 // the attention, so nothing is committed.
@@ -73,8 +95,26 @@ void rmsnorm_bf16(cudaStream_t st, const float* x, const float* gain, float eps,
   rmsnorm_bf16_kernel<<<(rows.rows_max + 7) / 8, 256, 0, st>>>(x, gain, eps, out, rows, d);
 }
 
+// Fused-RMSNorm buffers (scratch): per-row 1/rms, partial sums, m-tile counters.
+struct NormBufs {
+  float* inv;
+  float* part;
+  int* cnt;
+};
+static NormBufs norm_bufs(rk_engine* e, size_t rows) {
+  Scratch& S = *e->scratch;
+  S.norm_inv.ensure(rows * 4 + 256);
+  S.norm_part.ensure(rows * kNormSlots * 4 + 256);
+  const size_t cnt_bytes = ((rows + 127) / 128 * 4 + 64) * 4;
+  if (S.norm_cnt.bytes < cnt_bytes) {
+    S.norm_cnt.ensure(cnt_bytes);
+    RK_CUDA(cudaMemsetAsync(S.norm_cnt.p, 0, S.norm_cnt.bytes, e->stream));
+  }
+  return {S.norm_inv.as<float>(), S.norm_part.as<float>(), S.norm_cnt.as<int>()};
+}
+
 void run_layer_bf16(rk_engine* e, rk_weights* w, rk_context* ctx, int l, float* hidden, Rows rows, bool commit,
-                    int max_ctx, float* probs, int key_lo, int key_n, void* cap_k, void* cap_v) {
+                    int max_ctx, float* probs, int key_lo, int key_n, void* cap_k, void* cap_v, bool prepared) {
   (void)max_ctx;
   Scratch& S = *e->scratch;
   const rk_model_spec& s = w->s;
@@ -98,8 +138,13 @@ void run_layer_bf16(rk_engine* e, rk_weights* w, rk_context* ctx, int l, float* 
     e->launches += 1;
   }
 
-  rmsnorm_bf16(st, hidden, ly.attn_norm, s.norm_eps, normed, rows, d);
+  const NormBufs nb = norm_bufs(e, (size_t)rows.rows_max);
+  if (!prepared) {  // else the previous layer's down GEMM left bf16 rows + 1/rms
+    norm_prep_kernel<<<(rows.rows_max + 7) / 8, 256, 0, st>>>(hidden, s.norm_eps, normed, nb.inv, rows, d);
+    e->launches += 1;
+  }
   GemmArgs g;
+  g.row_scale = nb.inv;
   g.rows_max = rows.rows_max;
   g.rows_dev = rows.rows_dev;
   g.N = q + 2 * kv;
@@ -145,10 +190,15 @@ void run_layer_bf16(rk_engine* e, rk_weights* w, rk_context* ctx, int l, float* 
   o.out_f32 = hidden;
   o.ld_out = d;
   o.split_flags = flags;
+  o.norm_bf16 = normed;  // mlp RMSNorm fused: bf16 rows + 1/rms for the gate/up GEMM
+  o.norm_part = nb.part;
+  o.norm_inv = nb.inv;
+  o.norm_cnt = nb.cnt;
+  o.norm_eps = s.norm_eps;
   gemm_bf16(e, attn, q, static_cast<const __nv_bfloat16*>(ly.w_o), o, hint);
 
-  rmsnorm_bf16(st, hidden, ly.mlp_norm, s.norm_eps, normed, rows, d);
   GemmArgs gu;
+  gu.row_scale = nb.inv;
   gu.rows_max = rows.rows_max;
   gu.rows_dev = rows.rows_dev;
   gu.N = 2 * ff;
@@ -167,8 +217,12 @@ void run_layer_bf16(rk_engine* e, rk_weights* w, rk_context* ctx, int l, float* 
   dn.out_f32 = hidden;
   dn.ld_out = d;
   dn.split_flags = flags;
+  dn.norm_bf16 = normed;  // next layer's attention RMSNorm fused likewise
+  dn.norm_part = nb.part;
+  dn.norm_inv = nb.inv;
+  dn.norm_cnt = nb.cnt;
+  dn.norm_eps = s.norm_eps;
   gemm_bf16(e, act, ff, static_cast<const __nv_bfloat16*>(ly.w_down), dn, hint);
-  e->launches += 2;  // the two RMSNorms
 
   if (!commit) {
     swap_row_kernel<<<1, 256, 0, st>>>(ck, cv, rows.pos, kv, save, 1);

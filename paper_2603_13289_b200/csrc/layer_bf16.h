@@ -33,7 +33,21 @@ struct GemmArgs {
   __nv_bfloat16* self_v = nullptr;
   __nv_bfloat16* cap_k = nullptr;  // pre-RoPE K capture rows [M x kv]
   __nv_bfloat16* cap_v = nullptr;
+  // Fused RMSNorm (rms_norm, tensor.cpp:109-119). Consumer side (QKV, SILU):
+  // the accumulator row is scaled by row_scale[row] = 1/sqrt(mean(h^2)+eps)
+  // before the epilogue (the norm gain is folded into the weights). Producer
+  // side (ADD, final split): the new residual row is also written as bf16
+  // (norm_bf16, row stride N) and its sum of squares per N tile goes to
+  // norm_part[row][nt]; the last tile of each 32-row group to finish sums the
+  // partials in tile order and writes norm_inv[row] (deterministic).
+  const float* row_scale = nullptr;
+  __nv_bfloat16* norm_bf16 = nullptr;
+  float* norm_part = nullptr;   // [rows_max][64]
+  float* norm_inv = nullptr;    // [rows_max]
+  int* norm_cnt = nullptr;      // [m tiles * 4], zero-initialised, self-resetting
+  float norm_eps = 1e-5f;
 };
+constexpr int kNormSlots = 64;  // max N tiles of a residual GEMM (d_model / BN)
 
 // A: [rows_max x K] bf16 row-major with row stride lda; B: [N x K] bf16.
 // rows_hint: expected live rows (tile-shape choice) when rows_dev is set.

@@ -103,7 +103,8 @@ int* Runner::upload_tokens(const int32_t* tokens, uint64_t n, int off) {
 void Runner::run_layer(rk_context* ctx, int l, float* hidden, Rows rows, bool commit, int max_ctx,
                        float* probs, int key_lo, int key_n) {
   if (w_->precision == RK_BF16) {
-    run_layer_bf16(e_, w_, ctx, l, hidden, rows, commit, max_ctx, probs, key_lo, key_n, cap_k_, cap_v_);
+    run_layer_bf16(e_, w_, ctx, l, hidden, rows, commit, max_ctx, probs, key_lo, key_n, cap_k_, cap_v_, prepared_);
+    prepared_ = true;
     return;
   }
   Scratch& S = *e_->scratch;
@@ -163,6 +164,7 @@ void Runner::row_logits_from_layer(rk_context* ctx, const float* hidden_row, uin
   k::iota_positions(st_, S.sub_positions.as<int>(), 1, (int)position);
   e_->launches += 1;
   Rows one{1, nullptr, S.sub_positions.as<int>()};
+  prepared_ = false;
   for (uint64_t l = first_layer; l < s.num_layers; ++l)
     run_layer(ctx, (int)l, row, one, /*commit=*/false, (int)position + 1);
   last_row_logits(row);
@@ -190,6 +192,7 @@ void Runner::prefill(rk_context* ctx, const int32_t* tokens, uint64_t n, uint64_
   k::iota_positions(st_, S.positions.as<int>(), (int)n, (int)base);
   e_->launches += 2;
   Rows rows{(int)n, nullptr, S.positions.as<int>()};
+  prepared_ = false;
   for (uint64_t l = 0; l < s.num_layers; ++l) run_layer(ctx, (int)l, S.hidden.as<float>(), rows, true, (int)(base + n));
   if (want_logits) last_row_logits(S.hidden.as<float>() + (n - 1) * s.d_model);
 }
@@ -320,6 +323,7 @@ ExtendResult Runner::relay_extend(rk_context* ctx, rk_cache* cache, const rk_lay
       int* dev_tok = cache->tokens.as<int>();
       k::embed(st_, hidden, w_->emb, w_->elem, dev_tok, (int)n, (int)d, 0, nullptr);
       e_->launches += 1;
+      prepared_ = false;
       for (uint64_t l = 0; l < L; ++l) run_layer(ctx, (int)l, hidden, band_rows, true, max_ctx);
       k::mark_layers(st_, origin, (int)n, 0, (int)L - 1);
       k::set_depth(st_, depth, (int)n, L);
@@ -343,6 +347,7 @@ ExtendResult Runner::relay_extend(rk_context* ctx, rk_cache* cache, const rk_lay
         e_->launches += 1;
       }
       // full-recompute band: every segment row, layers [l_start, l_det]
+      prepared_ = false;
       for (uint64_t l = l_start; l <= l_det; ++l) run_layer(ctx, (int)l, hidden, band_rows, true, max_ctx);
       k::mark_layers(st_, origin, (int)n, (int)l_start, (int)l_det);
       k::set_depth(st_, depth, (int)n, l_det + 1);
@@ -390,6 +395,7 @@ ExtendResult Runner::relay_extend(rk_context* ctx, rk_cache* cache, const rk_lay
         k::positions_from_sel(st_, X.sub_pos.as<int>(), X.sel_idx.as<int>(), count, (int)n, (int)base);
         e_->launches += 2;
         Rows sparse_rows{(int)n, count, X.sub_pos.as<int>()};
+        prepared_ = false;
         for (uint64_t l = l_det + 1; l <= sparse_hi; ++l)
           run_layer(ctx, (int)l, X.sub_hidden.as<float>(), sparse_rows, true, max_ctx);
         k::mark_rows(st_, origin, (int)n, (int)l_det + 1, (int)sparse_hi, X.sel_idx.as<int>(), count, (int)n);
@@ -631,6 +637,9 @@ void Runner::agent_fused(rk_context* ctx, const int32_t* prefix, uint64_t P, rk_
     else if (segs && l > l_det && l <= sparse_hi) rows = Rows{(int)(head + segrows), offs + U, pos};
     rows.g1 = (int)P;
     rows.g2 = (int)head;
+    // the row set grows at l = 0, at the band start and after the selected
+    // rows are gathered (it only shrinks, to the head rows, after sparse_hi)
+    if (l == 0 || (segs && (l == l_start || l == l_det + 1))) prepared_ = false;
     run_layer(ctx, (int)l, H, rows, true, (int)total);
     if (segs && l == l_det) {
       ev_band = event();
@@ -775,6 +784,7 @@ rk_cache* Runner::capture_prefill(rk_context* ctx, const int32_t* tokens, uint64
     k::iota_positions(st_, S.positions.as<int>(), (int)m, (int)(src + c0));
     e_->launches += 2;
     Rows rows{(int)m, nullptr, S.positions.as<int>()};
+    prepared_ = false;
     for (uint64_t l = 0; l < s.num_layers; ++l) {
       if (l == snapshot)
         RK_CUDA(cudaMemcpyAsync(c->hidden.as<float>() + c0 * d, S.hidden.p, m * d * 4, cudaMemcpyDeviceToDevice, st_));
@@ -818,6 +828,7 @@ rk_cache* Runner::capture_decode(rk_context* ctx, const float* first_logits, uin
     k::iota_positions(st_, S.positions.as<int>(), 1, (int)pos);
     e_->launches += 2;
     Rows rows{1, nullptr, S.positions.as<int>()};
+    prepared_ = false;
     for (uint64_t l = 0; l < s.num_layers; ++l) {
       if (l == snapshot)
         RK_CUDA(cudaMemcpyAsync(c->hidden.as<float>() + t * d, S.hidden.p, d * 4, cudaMemcpyDeviceToDevice, st_));
@@ -905,8 +916,9 @@ void layer_unpack_tensor(rk_weights* w, size_t idx, float* dst, size_t rows, siz
     if (bf) k::bf16_to_f32(st, dst, static_cast<const __nv_bfloat16*>(src), rows * cols);
     else RK_CUDA(cudaMemcpyAsync(dst, src, rows * cols * 4, cudaMemcpyDeviceToDevice, st));
   };
-  auto strided = [&](const void* src, size_t ld_exact, size_t c0, size_t cs, size_t ld_t) {
-    if (bf) k::untranspose_bf16(st, dst, static_cast<const __nv_bfloat16*>(src), ld_t, c0, cs, rows, cols);
+  auto strided = [&](const void* src, size_t ld_exact, size_t c0, size_t cs, size_t ld_t,
+                     const float* gain = nullptr) {
+    if (bf) k::untranspose_bf16(st, dst, static_cast<const __nv_bfloat16*>(src), ld_t, c0, cs, rows, cols, gain);
     else k::copy2d_f32(st, dst, cols, 1, static_cast<const float*>(src) + c0, ld_exact, cs, rows, cols);
   };
   auto f32 = [&](const float* src) { RK_CUDA(cudaMemcpyAsync(dst, src, rows * cols * 4, cudaMemcpyDeviceToDevice, st)); };
@@ -916,13 +928,13 @@ void layer_unpack_tensor(rk_weights* w, size_t idx, float* dst, size_t rows, siz
     const rk_layer_dev& ly = w->layers[i / 9];
     switch (i % 9) {
       case 0: f32(ly.attn_norm); break;
-      case 1: strided(ly.w_qkv, q + 2 * kv, 0, 1, d); break;
-      case 2: strided(ly.w_qkv, q + 2 * kv, q, 1, d); break;
-      case 3: strided(ly.w_qkv, q + 2 * kv, q + kv, 1, d); break;
+      case 1: strided(ly.w_qkv, q + 2 * kv, 0, 1, d, ly.attn_norm); break;
+      case 2: strided(ly.w_qkv, q + 2 * kv, q, 1, d, ly.attn_norm); break;
+      case 3: strided(ly.w_qkv, q + 2 * kv, q + kv, 1, d, ly.attn_norm); break;
       case 4: strided(ly.w_o, d, 0, 1, q); break;
       case 5: f32(ly.mlp_norm); break;
-      case 6: strided(ly.w_gu, 2 * ff, 0, 2, d); break;
-      case 7: strided(ly.w_gu, 2 * ff, 1, 2, d); break;
+      case 6: strided(ly.w_gu, 2 * ff, 0, 2, d, ly.mlp_norm); break;
+      case 7: strided(ly.w_gu, 2 * ff, 1, 2, d, ly.mlp_norm); break;
       default: strided(ly.w_down, d, 0, 1, ff); break;
     }
     return;

@@ -80,3 +80,34 @@ def test_bf16_capture_prefill_matches_exact(engine):
     a, b = hosts["fp32"], hosts["bf16"]
     for f in ("k_pre", "v", "hidden_snapshot", "influence"):
         assert rel(getattr(b, f), getattr(a, f)) < 5e-2, f
+
+
+def test_bf16_nonunit_norm_gains(engine, oracle):
+    """Uploaded weights with non-unit RMSNorm gains: the bf16 path folds the
+    attention/MLP gains into W_qkv / W_gate,up and applies 1/rms in the GEMM
+    epilogue (fused RMSNorm); it must still track the exact path."""
+    spec = SPECS[0][1]
+    d, q, kv, ff, V, L = (spec.d_model, spec.num_heads * spec.d_head, spec.num_kv_heads * spec.d_head, spec.d_ff,
+                          spec.vocab_size, spec.num_layers)
+    layer = [d, d * q, d * kv, d * kv, q * d, d, d * ff, d * ff, ff * d]  # weights_io.cpp:21-38 order
+    sizes = [V * d] + layer * L + [d, d * V]
+    gains = {1 + 9 * l for l in range(L)} | {6 + 9 * l for l in range(L)} | {1 + 9 * L}
+    w0 = engine.weights(spec, 21, "fp32")
+    rng = np.random.default_rng(3)
+    tensors = []
+    for i, n in enumerate(sizes):
+        t = w0.tensor(i, n)
+        if i in gains:
+            t = (0.5 + rng.random(n)).astype(np.float32)
+        tensors.append(t)
+    cache = oracle.scenario(oracle.weights(spec, 21), pattern_tokens(30, 256, 1), 160, 1)
+    prefix = pattern_tokens(40, 256, 2)
+    res = {}
+    for prec in ("fp32", "bf16"):
+        w = engine.weights_from_tensors(spec, tensors, prec)
+        back = w.tensor(1 + 9 + 1, sizes[1 + 9 + 1])  # layer 1 W_q comes back without the folded gain
+        assert rel(back, tensors[1 + 9 + 1]) < 1e-2
+        out = w.context().agent_prefill(prefix, [w.upload_cache(cache)], pattern_tokens(8, 256, 4), triple(1, 1, 2),
+                                        RelayOptions.make(suffix_k=4))
+        res[prec] = out["logits"]
+    assert rel(res["bf16"], res["fp32"]) < 5e-2
