@@ -1,15 +1,18 @@
 #!/usr/bin/env python
 """Benchmark: downstream-agent TTFT and relay-prefill tokens/s (BASELINE.json
-metric) on BASELINE config 2 -- a Llama-3.2-1B-shaped random-init model, the
-3-agent Architect/Developer/Reviewer chain with ~4K accumulated context, 1 B200
-per session group (one process per GPU, weak scaling, no data-path collective).
+metric). Default workload: BASELINE config 2 -- a Llama-3.2-1B-shaped
+random-init model, the 3-agent Architect/Developer/Reviewer chain with ~4K
+accumulated context. --config c3 (Llama-3-8B shape, 8-turn chain, 16K context)
+and c4 (Qwen2.5-7B shape, 64 sessions sharded over the GPUs) run the larger
+BASELINE configs. One process per GPU, sessions sharded, weak scaling, no
+data-path collective.
 
-One step = the Reviewer's TTFT sequence through the engine (run_workflow's
-relay branch, workflow.cpp:316-369): prefix prefill -> relay_extend of the
-Architect's and the Developer's decode-time caches -> suffix prefill ->
-last-row logits -> argmax, first token read back on the host.
+One step = the last agent's TTFT sequence through the engine (run_workflow's
+relay branch, workflow.cpp:316-369): prefix prefill -> relay_extend of every
+upstream agent's decode-time cache -> suffix prefill -> last-row logits ->
+argmax, first token read back on the host.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2|c3|c4]
 
 Prints ONE JSON line on rank 0.
 """
@@ -29,20 +32,44 @@ sys.path.insert(0, ROOT)
 
 from paper_2603_13289_b200.abi import LayerProfile, ModelSpec, RelayOptions  # noqa: E402
 
-# ---- workload (BASELINE config 2) -------------------------
-SPEC = dict(num_layers=16, d_model=2048, num_heads=32, num_kv_heads=8, d_head=64, d_ff=8192,
-            vocab_size=128256, theta_base=500000.0, max_positions=8192)
-PREFIX, SEGMENT, SUFFIX = 256, 1856, 64          # per agent; Reviewer prompt = 4032 tokens
-PROFILE = (1, 2, 9)                               # (1,3,18)/32 scaled to 16 layers
+# ---- workloads (BASELINE.json configs) --------------------------
+# The default (c2) is the config the metric is quoted on; c3/c4 are the larger
+# single-GPU shapes, run with --config (the driver runs the default).
+WORKLOADS = {
+    "c2": dict(title="c2: Llama-3.2-1B-shaped random init (L16 d2048 H32/8 dh64 ff8192 V128256), "
+                     "Architect->Developer->Reviewer chain",
+               spec=dict(num_layers=16, d_model=2048, num_heads=32, num_kv_heads=8, d_head=64, d_ff=8192,
+                         vocab_size=128256, theta_base=500000.0, max_positions=8192),
+               agents=3, prefix=256, segment=1856, suffix=64, profile=(1, 2, 9), cpu=(4, 4, 2)),
+    "c3": dict(title="c3: Llama-3-8B-shaped bf16 GQA random init (L32 d4096 H32/8 dh128 ff14336 V128256), "
+                     "8-turn chain",
+               spec=dict(num_layers=32, d_model=4096, num_heads=32, num_kv_heads=8, d_head=128, d_ff=14336,
+                         vocab_size=128256, theta_base=500000.0, max_positions=16384),
+               agents=8, prefix=256, segment=2240, suffix=64, profile=(1, 3, 18), cpu=(2, 1, 1)),
+    "c4": dict(title="c4: Qwen2.5-7B-shaped random init (L28 d3584 H28/4 dh128 ff18944 V152064), "
+                     "3-agent chain per session",
+               spec=dict(num_layers=28, d_model=3584, num_heads=28, num_kv_heads=4, d_head=128, d_ff=18944,
+                         vocab_size=152064, theta_base=1000000.0, max_positions=8192),
+               agents=3, prefix=256, segment=1856, suffix=64, profile=(3, 4, 22), cpu=(2, 1, 1), sessions=64),
+}
+WL = WORKLOADS["c2"]
 SEED = 1234
-# CPU sample (reference arm / cpu_baseline): same model, shortened chain
-CPU_PREFIX, CPU_SEGMENT, CPU_SUFFIX = 4, 4, 2
+
+
+def set_workload(name):
+    global WL
+    WL = WORKLOADS[name]
 
 
 def spec_obj():
-    return ModelSpec.make(SPEC["num_layers"], SPEC["d_model"], SPEC["num_heads"], SPEC["num_kv_heads"],
-                          SPEC["d_head"], SPEC["d_ff"], SPEC["vocab_size"], SPEC["theta_base"],
-                          SPEC["max_positions"])
+    S = WL["spec"]
+    return ModelSpec.make(S["num_layers"], S["d_model"], S["num_heads"], S["num_kv_heads"], S["d_head"], S["d_ff"],
+                          S["vocab_size"], S["theta_base"], S["max_positions"])
+
+
+def prompt_tokens():
+    """Tokens in the downstream agent's prompt: prefix + upstream segments + suffix."""
+    return WL["prefix"] + (WL["agents"] - 1) * WL["segment"] + WL["suffix"]
 
 
 def synthetic_tokens(seed, salt, count, vocab):
@@ -56,18 +83,20 @@ def synthetic_tokens(seed, salt, count, vocab):
     return (z % np.uint64(vocab)).astype(np.int32)
 
 
-def prompts(rank=0):
-    V = SPEC["vocab_size"]
-    base = SEED + 7919 * rank
-    return {f"{name}_{part}": synthetic_tokens(base, salt, n, V)
-            for salt, (name, part, n) in enumerate(
-                [("arch", "prefix", PREFIX), ("arch", "out", SEGMENT), ("dev", "prefix", PREFIX),
-                 ("dev", "suffix", SUFFIX), ("dev", "out", SEGMENT), ("rev", "prefix", PREFIX),
-                 ("rev", "suffix", SUFFIX)])}
+def prompts(session=0):
+    """Per agent a: prefix, suffix and its output segment (captured as its cache)."""
+    V = WL["spec"]["vocab_size"]
+    base = SEED + 7919 * session
+    out = {}
+    for a in range(WL["agents"]):
+        out[f"a{a}_prefix"] = synthetic_tokens(base, 3 * a, WL["prefix"], V)
+        out[f"a{a}_suffix"] = synthetic_tokens(base, 3 * a + 1, WL["suffix"], V)
+        out[f"a{a}_out"] = synthetic_tokens(base, 3 * a + 2, WL["segment"], V)
+    return out
 
 
 def options(mode="relay"):
-    return LayerProfile(*PROFILE), RelayOptions.make(mode=mode, tau_dev=1.5, tau_inf=1.45, suffix_k=10)
+    return LayerProfile(*WL["profile"]), RelayOptions.make(mode=mode, tau_dev=1.5, tau_inf=1.45, suffix_k=10)
 
 
 # ---- clocks -------------------------------------------------------------------
@@ -158,8 +187,8 @@ def barrier(dist):
 def cpu_sample(gpu_caches=None, threads=None, steps=1, warmup=0, kind="reference"):
     """Time the reference's own relay path (oracle/_ref: the reference library
     built from its sources) -- or the restatement if _ref is absent -- on a
-    bounded sample of the c2 workload: same model, prefix/segments/suffix cut
-    to CPU_PREFIX/CPU_SEGMENT/CPU_SUFFIX tokens. Returns (tokens/s, meta)."""
+    bounded sample of the workload: same model, prefix/segments/suffix cut to
+    WL["cpu"] tokens, one independent session per host core. Returns (tokens/s, meta)."""
     from oracle.oracle import Oracle, available
     if kind == "reference" and not available("reference"):
         kind = "restatement"
@@ -167,19 +196,20 @@ def cpu_sample(gpu_caches=None, threads=None, steps=1, warmup=0, kind="reference
     spec = spec_obj()
     w = orc.weights(spec, SEED, checked=(kind == "reference"))
     pr = prompts(0)
+    cp, cs, cx = WL["cpu"]
     caches = []
     for host in gpu_caches:
         c = host.copy()
-        n = CPU_SEGMENT
-        c.segment_tokens = c.segment_tokens[:n].copy()
-        c.k_pre = np.ascontiguousarray(c.k_pre[:, :n])
-        c.v = np.ascontiguousarray(c.v[:, :n])
-        c.hidden_snapshot = np.ascontiguousarray(c.hidden_snapshot[:n])
-        c.influence = np.ascontiguousarray(c.influence[:n])
-        c.decode_steps_observed = n
+        c.segment_tokens = c.segment_tokens[:cs].copy()
+        c.k_pre = np.ascontiguousarray(c.k_pre[:, :cs])
+        c.v = np.ascontiguousarray(c.v[:, :cs])
+        c.hidden_snapshot = np.ascontiguousarray(c.hidden_snapshot[:cs])
+        c.influence = np.ascontiguousarray(c.influence[:cs])
+        c.decode_steps_observed = cs
         caches.append(c)
     prof, opts = options()
-    prefix, suffix = pr["rev_prefix"][:CPU_PREFIX], pr["rev_suffix"][:CPU_SUFFIX]
+    last = WL["agents"] - 1
+    prefix, suffix = pr[f"a{last}_prefix"][:cp], pr[f"a{last}_suffix"][:cx]
     tokens = len(prefix) + sum(c.segment_len for c in caches) + len(suffix)
     threads = threads or (os.cpu_count() or 1)
     times = []
@@ -197,9 +227,9 @@ def cpu_sample(gpu_caches=None, threads=None, steps=1, warmup=0, kind="reference
     ms = sum(times) / len(times)
     tps = used * tokens / (ms / 1e3)
     meta = {"kind": "reference" if kind == "reference" else "port", "cores": used,
-            "sample": f"c2 model (L16 d2048 V128256), prefix {CPU_PREFIX} + 2 relayed segments x "
-                      f"{CPU_SEGMENT} + suffix {CPU_SUFFIX} = {tokens} tokens per session, "
-                      f"{used} concurrent sessions, profile {PROFILE}",
+            "sample": f"{WL['title'].split(':')[0]} model, prefix {cp} + {len(caches)} relayed segments x "
+                      f"{cs} + suffix {cx} = {tokens} tokens per session, {used} concurrent sessions, "
+                      f"profile {WL['profile']}",
             "ms_per_session_step": ms}
     return tps, meta
 
@@ -218,21 +248,24 @@ def merge_kernel_stats(stats):
 
 # ---- our engine ------------------------------------------------------------------
 def build_session(w, session):
-    """One collaboration session: the Architect's and Developer's decode-time
-    caches (captured on the device) and the Reviewer's prompt parts."""
+    """One collaboration session: the decode-time caches of agents 0..A-2
+    (captured on the device; each agent relays all upstream segments,
+    workflow.cpp:285-288) and the last agent's prompt parts."""
     pr = prompts(session)
     prof, opts = options()
-    snap = PROFILE[0]
-    # Architect: decode-time capture of its output after its prompt
-    ctx1 = w.context()
-    ctx1.prefill(pr["arch_prefix"], logits=False)
-    cache1 = ctx1.capture_prefill(pr["arch_out"], snap)
-    # Developer: relays the Architect's output, then its own output is captured
-    ctx2 = w.context()
-    ctx2.agent_prefill(pr["dev_prefix"], [cache1], pr["dev_suffix"], prof, opts, want_logits=False)
-    cache2 = ctx2.capture_prefill(pr["dev_out"], snap)
-    del ctx1, ctx2
-    return {"caches": [cache1, cache2], "prompts": pr, "ctx": w.context(), "session": session}
+    snap = WL["profile"][0]
+    caches = []
+    for a in range(WL["agents"] - 1):
+        ctx = w.context()
+        if caches:
+            ctx.agent_prefill(pr[f"a{a}_prefix"], caches, pr[f"a{a}_suffix"], prof, opts, want_logits=False)
+        else:
+            ctx.prefill(pr[f"a{a}_prefix"], logits=False)
+        caches.append(ctx.capture_prefill(pr[f"a{a}_out"], snap))
+        del ctx
+    last = WL["agents"] - 1
+    return {"caches": caches, "prefix": pr[f"a{last}_prefix"], "suffix": pr[f"a{last}_suffix"],
+            "ctx": w.context(), "session": session}
 
 
 def run_ours(args, world, rank, local, dist):
@@ -242,19 +275,18 @@ def run_ours(args, world, rank, local, dist):
     torch.cuda.set_device(local)
     eng = Engine(local)
     w = eng.weights(spec_obj(), SEED, "bf16")
-    n_sessions = args.sessions or world
+    n_sessions = args.sessions or WL.get("sessions", world)
     mine = [build_session(w, sid) for sid in shard(n_sessions, world, rank)]
     prof, opts = options()
     _, full_opts = options("full")
     stream = torch.cuda.ExternalStream(eng.stream)
-    n_tokens = PREFIX + 2 * SEGMENT + SUFFIX
+    n_tokens = prompt_tokens()
     # first local session carries the single-session diagnostics
-    caches, pr, ctx = mine[0]["caches"], mine[0]["prompts"], mine[0]["ctx"]
+    caches, ctx = mine[0]["caches"], mine[0]["ctx"]
 
     def run_session(sess, o=opts, want_outputs=False):
         sess["ctx"].reset()
-        p = sess["prompts"]
-        return sess["ctx"].agent_prefill(p["rev_prefix"], sess["caches"], p["rev_suffix"], prof, o,
+        return sess["ctx"].agent_prefill(sess["prefix"], sess["caches"], sess["suffix"], prof, o,
                                          want_logits=False, outputs=want_outputs)
 
     def step(o=opts):
@@ -308,7 +340,7 @@ def run_ours(args, world, rank, local, dist):
     def e2e_step():
         ups = [w.upload_cache(h) for h in hosts]
         ctx.reset()
-        out = ctx.agent_prefill(pr["rev_prefix"], ups, pr["rev_suffix"], prof, opts, want_logits=True)
+        out = ctx.agent_prefill(mine[0]["prefix"], ups, mine[0]["suffix"], prof, opts, want_logits=True)
         return out["first_token"]
 
     e2e_K = max(2, args.steps // 2)
@@ -320,8 +352,8 @@ def run_ours(args, world, rank, local, dist):
         e2e_step()
     e2e_ms = reduce_max(dist, (time.perf_counter() - h0) * 1e3, local) / e2e_K  # one session per rank
     h2d = sum(h.k_pre.nbytes + h.v.nbytes + h.hidden_snapshot.nbytes + h.influence.nbytes + h.segment_tokens.nbytes
-              for h in hosts) + 4 * (PREFIX + SUFFIX)
-    d2h = 4 * SPEC["vocab_size"] + 4
+              for h in hosts) + 4 * (WL["prefix"] + WL["suffix"])
+    d2h = 4 * WL["spec"]["vocab_size"] + 4
 
     # per-kernel instrumentation pass (same step, CUDA events per launch)
     eng.profile(True)
@@ -375,11 +407,11 @@ def run_ours(args, world, rank, local, dist):
         "value": round(value, 1), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": "c2: Llama-3.2-1B-shaped random init (L16 d2048 H32/8 dh64 ff8192 V128256), "
-                               "Architect->Developer->Reviewer chain, Reviewer TTFT at 4032-token prompt "
-                               f"(prefix {PREFIX} + 2 relayed segments x {SEGMENT} + suffix {SUFFIX}), "
-                               f"profile {PROFILE}, thresholds (1.5, 1.45, 10)",
-                   "sessions_per_gpu": len(mine), "l2": "inputs larger than L2 (2.8 GB of bf16 weights streamed per step)",
+        "config": {"workload": f"{WL['title']}, last agent's TTFT at a {n_tokens}-token prompt "
+                               f"(prefix {WL['prefix']} + {WL['agents'] - 1} relayed segments x {WL['segment']} + "
+                               f"suffix {WL['suffix']}), profile {WL['profile']}, thresholds (1.5, 1.45, 10)",
+                   "config_id": args.config,
+                   "sessions_per_gpu": len(mine), "l2": "inputs larger than L2 (bf16 weights streamed per step)",
                    "parallelism": f"sessions sharded, {world} GPU(s), no hot-path collective"},
         "ttft_ms": round(ttft, 4),
         "full_prefill_ttft_ms": round(full_ms, 4),
@@ -416,35 +448,36 @@ def run_reference(args, world, rank, local, dist):
             print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference "
                                                                   "at build time)"}))
             return
-        # inputs: caches of the c2 chain are data; build them with the reference
-        # itself (decode-time capture of CPU_SEGMENT tokens) to stay CPU-only.
+        # inputs: the chain's caches are data; build them with the reference
+        # itself (decode-time capture of the cut segments) to stay CPU-only.
         from oracle.oracle import Oracle
         orc = Oracle("reference")
         spec = spec_obj()
         w = orc.weights(spec, SEED, checked=True)
         pr = prompts(0)
-        c1 = orc.scenario(w, pr["arch_prefix"][:CPU_PREFIX], CPU_SEGMENT, PROFILE[0])
-        c2 = orc.scenario(w, pr["dev_prefix"][:CPU_PREFIX], CPU_SEGMENT, PROFILE[0])
+        cp, cs, cx = WL["cpu"]
+        last = WL["agents"] - 1
+        caches = [orc.scenario(w, pr[f"a{a}_prefix"][:cp], cs, WL["profile"][0]) for a in range(last)]
         prof, opts = options()
-        prefix, suffix = pr["rev_prefix"][:CPU_PREFIX], pr["rev_suffix"][:CPU_SUFFIX]
-        tokens = len(prefix) + 2 * CPU_SEGMENT + len(suffix)
+        prefix, suffix = pr[f"a{last}_prefix"][:cp], pr[f"a{last}_suffix"][:cx]
+        tokens = len(prefix) + last * cs + len(suffix)
         threads = os.cpu_count() or 1
         for _ in range(args.warmup):
-            orc.agent_prefill_parallel(w, threads, prefix, [c1, c2], suffix, prof, opts)
+            orc.agent_prefill_parallel(w, threads, prefix, caches, suffix, prof, opts)
         times = []
         for _ in range(args.steps):
-            ms, _ = orc.agent_prefill_parallel(w, threads, prefix, [c1, c2], suffix, prof, opts)
+            ms, _ = orc.agent_prefill_parallel(w, threads, prefix, caches, suffix, prof, opts)
             times.append(ms)
         ms = sum(times) / len(times)
         value = threads * tokens / (ms / 1e3)
-        sample = (f"c2 model (L16 d2048 V128256, fp32 reference), prefix {CPU_PREFIX} + 2 relayed segments x "
-                  f"{CPU_SEGMENT} + suffix {CPU_SUFFIX} = {tokens} tokens/session, {threads} concurrent sessions")
+        sample = (f"{WL['title'].split(':')[0]} model (fp32 reference), prefix {cp} + {last} relayed segments x "
+                  f"{cs} + suffix {cx} = {tokens} tokens/session, {threads} concurrent sessions")
         print(json.dumps({
             "impl": "reference", "metric": "relay-prefill tokens/s (downstream-agent TTFT at ~80% KV reuse)",
             "value": round(value, 4), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
-            "config": {"workload": "c2 chain, bounded CPU sample", "sample": sample},
+            "config": {"workload": f"{WL['title']}, bounded CPU sample", "config_id": args.config, "sample": sample},
             "cpu_baseline": {"value": round(value, 4), "unit": "tokens/s", "kind": "reference", "cores": threads,
                              "sample": sample},
             "e2e": {"value": round(value, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -459,12 +492,15 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(WORKLOADS), default="c2",
+                    help="workload (default c2: the config BASELINE.json's metric is quoted on)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--lean", action="store_true",
                     help="timed relay steps only (for ncu launch lists): no full-prefill, e2e or profiling legs")
     ap.add_argument("--sessions", type=int, default=0,
                     help="collaboration sessions in total, sharded contiguously over the GPUs (default: one per GPU)")
     args = ap.parse_args()
+    set_workload(args.config)
     world, rank, local, dist = dist_setup(args)
     if args.impl == "reference":
         run_reference(args, world, rank, local, dist)
