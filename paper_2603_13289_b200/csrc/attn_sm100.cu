@@ -8,7 +8,7 @@
 // the causal limit is per row, by absolute position.
 //
 // One CTA = one query tile (128 rows) x one head, flash-style over 128-key
-// tiles; d_head 64 fits two CTAs per SM (112 KB smem, 256 TMEM columns each),
+// tiles (64-key tiles at d_head 128); two CTAs per SM (112 KB smem, 256 TMEM columns each),
 // so one CTA's exponentials overlap the other's MMAs, loads and epilogue.
 //   warp 4      TMA: K_j into a 2-stage ring
 //   warp 6      TMA: Q once, V_j into a 2-stage ring
@@ -83,23 +83,26 @@ __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.
   } while (0)
 
 constexpr int kQ = 128;     // query rows per tile (TMEM lanes)
-constexpr int kKeys = 128;  // keys per tile
 constexpr float kRescaleLog2 = 8.0f;  // lazy O rescale threshold (P <= 2^8)
 constexpr int kThreadsA = 256;        // softmax warpgroup + control warpgroup
 
 template <int DH>
 struct ACfg {
+  // keys per tile: 128 at d_head 64; 64 at d_head 128 so that two CTAs fit
+  // per SM there too (112 KB smem each)
+  static constexpr int KEYS = DH == 64 ? 128 : 64;
+  static constexpr int KB = KEYS / 64;             // 64-key swizzle blocks of S / P
   static constexpr int Q_TILE = kQ * DH * 2;
-  static constexpr int KV_BYTES = kKeys * DH * 2;  // one stage of K or V
+  static constexpr int KV_BYTES = KEYS * DH * 2;   // one stage of K or V
   static constexpr int KST = 2, VST = 2;
-  static constexpr int P_BYTES = kQ * kKeys * 2;
+  static constexpr int P_BYTES = kQ * KEYS * 2;
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = Q_TILE;
   static constexpr int OFF_V = OFF_K + KST * KV_BYTES;
   static constexpr int OFF_P = OFF_V + VST * KV_BYTES;
   static constexpr int OFF_BAR = OFF_P + P_BYTES;
   static constexpr int SMEM = OFF_BAR + 128;
-  static constexpr int CTAS = DH == 64 ? 2 : 1;  // CTAs per SM
+  static constexpr int CTAS = 2;  // CTAs per SM
   static_assert(CTAS * (SMEM + 1024) <= 233472, "shared memory per SM");
   static constexpr uint32_t TMEM_COLS = 256;
   static constexpr uint32_t S_COL = 0, O_COL = 128;  // S [0,128), O [128, 128+DH)
@@ -167,7 +170,8 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
   const int kvh = h / (a.H / a.Hkv);
   // split-KV: this CTA covers key tiles [j0, j0 + nk)
   const int j0 = blockIdx.z * a.tiles_per_split;
-  const int nk = min(*s_kmax / kKeys + 1 - j0, a.tiles_per_split);
+  constexpr int KEYS = C::KEYS;
+  const int nk = min(*s_kmax / KEYS + 1 - j0, a.tiles_per_split);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const bool trace_cta = TRACE && a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
   if (nk <= 0) {  // no keys for this split: empty partials (m = -inf, l = 0)
@@ -213,7 +217,7 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
           uint8_t* sk = smem + C::OFF_K + st * C::KV_BYTES;
           mbar_arrive_expect_tx(&k_full[st], C::KV_BYTES);
           for (int b = 0; b < DB; ++b)
-            tma_load_2d(sk + b * kKeys * 128, &tmK, &k_full[st], kvh * DH + b * 64, (j0 + j) * kKeys);
+            tma_load_2d(sk + b * KEYS * 128, &tmK, &k_full[st], kvh * DH + b * 64, (j0 + j) * KEYS);
         }
       }
     } else if (warp == 6) {
@@ -227,13 +231,13 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
           uint8_t* sv = smem + C::OFF_V + st * C::KV_BYTES;
           mbar_arrive_expect_tx(&v_full[st], C::KV_BYTES);
           for (int b = 0; b < DB; ++b)
-            tma_load_2d(sv + b * kKeys * 128, &tmV, &v_full[st], kvh * DH + b * 64, (j0 + j) * kKeys);
+            tma_load_2d(sv + b * KEYS * 128, &tmV, &v_full[st], kvh * DH + b * 64, (j0 + j) * KEYS);
         }
       }
     } else if (warp == 5) {
       if (elect_one()) {  // ------------------------------------------ MMA
         const bool tracing = trace_cta;
-        constexpr uint32_t idesc_s = idesc_bf16(kQ, kKeys);
+        constexpr uint32_t idesc_s = idesc_bf16(kQ, KEYS);
         constexpr uint32_t idesc_o = idesc_bf16(kQ, DH, /*b_mn_major=*/true);
         const uint32_t sq = smem_u32(smem + C::OFF_Q);
         mbar_wait(q_full, 0);
@@ -247,7 +251,7 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
 #pragma unroll
           for (int k = 0; k < DH / 16; ++k) {
             const uint32_t off = (k >> 2) * (kQ * 128) + (k & 3) * 32;
-            const uint32_t offk = (k >> 2) * (kKeys * 128) + (k & 3) * 32;
+            const uint32_t offk = (k >> 2) * (KEYS * 128) + (k & 3) * 32;
             mma_bf16_ss(tmem + C::S_COL, sdesc_sw128(sq + off, 16, 1024), sdesc_sw128(sk + offk, 16, 1024), idesc_s,
                         k > 0 ? 1u : 0u);
           }
@@ -263,9 +267,9 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
           const uint32_t sp = smem_u32(smem + C::OFF_P);
           const uint32_t sv = smem_u32(smem + C::OFF_V + st * C::KV_BYTES);
 #pragma unroll
-          for (int k = 0; k < kKeys / 16; ++k) {
+          for (int k = 0; k < KEYS / 16; ++k) {
             const uint64_t ad = sdesc_sw128(sp + (k >> 2) * (kQ * 128) + (k & 3) * 32, 16, 1024);
-            const uint64_t bd = sdesc_sw128(sv + k * 2048, kKeys * 128, 1024);
+            const uint64_t bd = sdesc_sw128(sv + k * 2048, KEYS * 128, 1024);
             mma_bf16_ss(tmem + C::O_COL, ad, bd, idesc_o, (j > 0 || k > 0) ? 1u : 0u);
           }
           tc_commit(o_done);
@@ -298,26 +302,24 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
       mbar_wait(s_full, j & 1);
       RK_TRACE(0, j, 1);
       tc_fence_after();
-      uint32_t r[128];
-      tmem_ld32(s_col + 0, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
-      tmem_ld32(s_col + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
-      tmem_ld32(s_col + 64, *reinterpret_cast<uint32_t(*)[32]>(&r[64]));
-      tmem_ld32(s_col + 96, *reinterpret_cast<uint32_t(*)[32]>(&r[96]));
+      uint32_t r[KEYS];
+#pragma unroll
+      for (int c = 0; c < KEYS; c += 32) tmem_ld32(s_col + c, *reinterpret_cast<uint32_t(*)[32]>(&r[c]));
       tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(s_free);  // S(j+1) may overwrite TMEM now
       RK_TRACE(0, j, 2);
-      const int kbase = (j0 + j) * kKeys;
+      const int kbase = (j0 + j) * KEYS;
       // warp-uniform: no causal mask anywhere in this tile for this warp's rows
-      if (!__all_sync(0xffffffffu, kbase + kKeys - 1 <= pos)) {
+      if (!__all_sync(0xffffffffu, kbase + KEYS - 1 <= pos)) {
 #pragma unroll
-        for (int u = 0; u < kKeys; ++u)
+        for (int u = 0; u < KEYS; ++u)
           if (kbase + u > pos) r[u] = __float_as_uint(-INFINITY);
       }
       float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
 #pragma unroll
-      for (int u = 0; u < kKeys; u += 8) {
+      for (int u = 0; u < KEYS; u += 8) {
         mx0 = fmaxf(mx0, fmaxf(__uint_as_float(r[u]), __uint_as_float(r[u + 1])));
         mx1 = fmaxf(mx1, fmaxf(__uint_as_float(r[u + 2]), __uint_as_float(r[u + 3])));
         mx2 = fmaxf(mx2, fmaxf(__uint_as_float(r[u + 4]), __uint_as_float(r[u + 5])));
@@ -356,7 +358,7 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
       const float neg_m = m_run == -INFINITY ? 0.f : -m_run;
       float ls0 = 0.f, ls1 = 0.f, ls2 = 0.f, ls3 = 0.f;
 #pragma unroll
-      for (int b = 0; b < 2; ++b) {
+      for (int b = 0; b < C::KB; ++b) {
         uint32_t pk[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
@@ -547,7 +549,8 @@ void attention_bf16(rk_engine* e, const AttnArgs& a_in, const __nv_bfloat16* ctx
   const int ctas_per_sm = a.dh == 64 ? ACfg<64>::CTAS : ACfg<128>::CTAS;
   const int base = max_tiles(hint) * a.H;          // CTAs without splitting
   const int slots = ctas_per_sm * e->sm_count;     // CTAs resident at once
-  const int nk_max = (ctx_rows + kKeys - 1) / kKeys;
+  const int keys = a.dh == 64 ? ACfg<64>::KEYS : ACfg<128>::KEYS;
+  const int nk_max = (ctx_rows + keys - 1) / keys;
   a.splits = 1;
   a.tiles_per_split = nk_max > 0 ? nk_max : 1;
   // split the key range only while the grid is well under 1.5 waves; each
@@ -568,8 +571,8 @@ void attention_bf16(rk_engine* e, const AttnArgs& a_in, const __nv_bfloat16* ctx
   const int q = a.H * a.dh, kv = a.Hkv * a.dh;
   CUtensorMap tq, tk, tv;
   make_tmap_bf16(&tq, a.q, (uint64_t)a.rows_max, (uint64_t)q, kQ, (uint64_t)q);
-  make_tmap_bf16(&tk, ctx_k, (uint64_t)ctx_rows, (uint64_t)kv, kKeys, (uint64_t)kv);
-  make_tmap_bf16(&tv, ctx_v, (uint64_t)ctx_rows, (uint64_t)kv, kKeys, (uint64_t)kv);
+  make_tmap_bf16(&tk, ctx_k, (uint64_t)ctx_rows, (uint64_t)kv, keys, (uint64_t)kv);
+  make_tmap_bf16(&tv, ctx_v, (uint64_t)ctx_rows, (uint64_t)kv, keys, (uint64_t)kv);
   ProfScope ps(e, (e->prof && e->prof->on)
                       ? intern("attn_m" + std::to_string(a.rows_max) + (a.rows_dev ? "dyn" : "") + "_ctx" +
                                std::to_string(ctx_rows) + "_s" + std::to_string(a.splits))

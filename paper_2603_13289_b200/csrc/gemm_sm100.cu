@@ -52,23 +52,13 @@ struct Units {
   int total;
 };
 
-// Split-K count for the residual epilogue: splits double while the grid is
-// still under half the SMs (every split re-reads and re-writes the fp32
-// output tile in split order, so splitting a grid that already fills the SMs
-// only adds traffic).
-__host__ __device__ __forceinline__ int best_splits(int tiles, int kb, int sms) {
-  int s = 1;
-  while (tiles * s * 2 <= sms && kb / (s * 2) >= 4) s *= 2;
-  return s;
-}
-
 __device__ __forceinline__ Units units_of(const GemmArgs& p) {
   Units u;
   const int M = p.rows_dev ? *p.rows_dev : p.rows_max;
   u.num_m = (M + kBM - 1) / kBM;
   u.num_n = p.N / p.bn;
   // live row count known only on the device: pick split-K here (grid = all SMs)
-  u.splits = (p.rows_dev && p.split_flags && p.epi == EPI_ADD) ? best_splits(u.num_m * u.num_n, p.K / kBK, p.sms) : p.splits;
+  u.splits = p.splits;
   u.kb_total = p.K / kBK;
   u.kb_per = (u.kb_total + u.splits - 1) / u.splits;
   u.total = u.num_m * u.num_n * u.splits;
@@ -86,12 +76,14 @@ __device__ __forceinline__ void decode_unit(const Units& u, int unit, int& mt, i
 
 template <int EPI>
 __device__ __forceinline__ void epilogue_chunk(const GemmArgs& p, int row, int col, const uint32_t (&r)[32],
-                                               float rs) {
+                                               float rs, int split = 0) {
   float v[32];
 #pragma unroll
   for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * rs;
-  if constexpr (EPI == EPI_F32) {
-    float4* dst = reinterpret_cast<float4*>(p.out_f32 + (size_t)row * p.ld_out + col);
+  if constexpr (EPI == EPI_F32 || EPI == EPI_PART) {
+    float* base = EPI == EPI_PART ? p.ws_part + ((size_t)split * p.rows_max + row) * p.N + col
+                                  : p.out_f32 + (size_t)row * p.ld_out + col;
+    float4* dst = reinterpret_cast<float4*>(base);
 #pragma unroll
     for (int j = 0; j < 8; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
   } else if constexpr (EPI == EPI_ADD) {
@@ -336,7 +328,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint32_t r[32];
           tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN + c, r);
           tmem_ld_wait();
-          if (row < M) epilogue_chunk<EPI>(p, row, nt * BN + c, r, rs);
+          if (row < M) epilogue_chunk<EPI>(p, row, nt * BN + c, r, rs, s);
         }
       }
       tc_fence_before();
@@ -352,6 +344,43 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tmem, C::TMEM_COLS);
+}
+
+// Split-K reduction + residual epilogue (EPI_PART partials): one CTA per row,
+// h[row] += sum_s part[s][row] in split order (deterministic); with the fused
+// RMSNorm the bf16 row copy and 1/rms come out of the same pass.
+__global__ void __launch_bounds__(256) splitk_reduce_add_kernel(const GemmArgs p, int splits) {
+  const int M = p.rows_dev ? *p.rows_dev : p.rows_max;
+  const int row = blockIdx.x;
+  if (row >= M) return;
+  const int n4 = p.N / 4;
+  float ss = 0.f;
+  float4* h = reinterpret_cast<float4*>(p.out_f32 + (size_t)row * p.ld_out);
+  for (int c = threadIdx.x; c < n4; c += blockDim.x) {
+    float4 acc = __ldcg(reinterpret_cast<const float4*>(p.ws_part + (size_t)row * p.N) + c);
+    for (int s = 1; s < splits; ++s) {
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(p.ws_part + ((size_t)s * p.rows_max + row) * p.N) + c);
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    float4 x = h[c];
+    x.x += acc.x; x.y += acc.y; x.z += acc.z; x.w += acc.w;
+    h[c] = x;
+    if (p.norm_bf16) {
+      ss += x.x * x.x + x.y * x.y + x.z * x.z + x.w * x.w;
+      reinterpret_cast<uint2*>(p.norm_bf16 + (size_t)row * p.N)[c] = make_uint2(pack_bf16(x.x, x.y), pack_bf16(x.z, x.w));
+    }
+  }
+  if (p.norm_inv) {
+    __shared__ float red[8];
+    for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float t = 0.f;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+      p.norm_inv[row] = rsqrtf(t / (float)p.N + p.norm_eps);
+    }
+  }
 }
 
 template <int BN, int EPI>
@@ -417,8 +446,35 @@ static void choose_config(GemmArgs& p, int sm_count, int rows_hint) {
   }
   if (p.N % bn) raise(RK_ERR_INVALID_ARGUMENT, "bf16 GEMM needs N % 64 == 0");
   p.bn = bn;
-  const bool splitk = p.epi == EPI_ADD && p.split_flags;
-  p.splits = splitk ? best_splits(num_m * (p.N / bn), p.K / kBK, sm_count) : 1;
+  p.splits = 1;
+  if (p.epi == EPI_ADD && p.split_flags) {
+    // residual GEMMs that cannot fill the SMs: widest tile, K split s ways with
+    // the s partials reduced (in order) by splitk_reduce_add_kernel; s picks
+    // the best wave efficiency of tiles*s units over the SMs
+    // Cost model (calibrated on B200): a 128x256 k-block ~0.45 us per CTA;
+    // partials cost s * M * N * 4 B written + read at ~8 TB/s plus ~3 us for
+    // the reduce launch.
+    const int wide = p.N % 256 == 0 ? 256 : (p.N % 128 == 0 ? 128 : 64);
+    const int tiles = num_m * (p.N / wide), kb = p.K / kBK;
+    if (4 * tiles < 3 * sm_count) {
+      const double t_kb = 0.45 * wide / 256.0;
+      auto cost = [&](int s) {
+        const int units = tiles * s, waves = (units + sm_count - 1) / sm_count;
+        const double mma = waves * ((kb + s - 1) / s) * t_kb;
+        const double part = s > 1 ? 3.0 + 2.0 * s * (double)rows_hint * p.N * 4 / 8e6 : 0.0;
+        return mma + part;
+      };
+      int best = 1;
+      double best_cost = cost(1);
+      for (int s = 2; s <= 8 && kb / s >= 4; ++s)
+        if (cost(s) < best_cost) { best = s; best_cost = cost(s); }
+      if (best > 1) {
+        p.bn = wide;
+        p.splits = best;
+        p.epi = EPI_PART;
+      }
+    }
+  }
 }
 
 void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat16* B, GemmArgs p,
@@ -431,9 +487,13 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
   make_tmap_bf16(&ta, A, (uint64_t)p.rows_max, (uint64_t)p.K, kBM, (uint64_t)lda);
   make_tmap_bf16(&tb, B, (uint64_t)p.N, (uint64_t)p.K, (uint32_t)p.bn, (uint64_t)p.K);
   const int num_m = (p.rows_max + kBM - 1) / kBM;
-  const int total = num_m * (p.N / p.bn) * (p.rows_dev && p.split_flags && p.epi == EPI_ADD ? 16 : p.splits);
+  const int total = num_m * (p.N / p.bn) * p.splits;
   const int grid = total < e->sm_count ? total : e->sm_count;
-  static const char* kEpi[] = {"qkv", "add", "silu", "f32"};
+  if (p.epi == EPI_PART) {
+    e->scratch->gemm_ws.ensure((size_t)p.splits * p.rows_max * p.N * 4);
+    p.ws_part = e->scratch->gemm_ws.as<float>();
+  }
+  static const char* kEpi[] = {"qkv", "add", "silu", "f32", "addsplit"};
   ProfScope ps(e, (e->prof && e->prof->on)
                       ? intern(std::string("gemm_") + kEpi[p.epi] + "_m" + std::to_string(p.rows_max) +
                                (p.rows_dev ? "dyn" : "") + "_n" + std::to_string(p.N) + "_k" + std::to_string(p.K) +
@@ -449,6 +509,11 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
     case EPI_QKV: launch_bn<EPI_QKV>(e->stream, ta, tb, p, grid); break;
     case EPI_ADD: launch_bn<EPI_ADD>(e->stream, ta, tb, p, grid); break;
     case EPI_SILU: launch_bn<EPI_SILU>(e->stream, ta, tb, p, grid); break;
+    case EPI_PART:
+      launch_bn<EPI_PART>(e->stream, ta, tb, p, grid);
+      splitk_reduce_add_kernel<<<p.rows_max, 256, 0, e->stream>>>(p, p.splits);
+      e->launches += 1;
+      break;
     default: launch_bn<EPI_F32>(e->stream, ta, tb, p, grid); break;
   }
   e->launches += 1;

@@ -7,7 +7,9 @@
 
 namespace rk {
 
-enum GemmEpi { EPI_QKV = 0, EPI_ADD = 1, EPI_SILU = 2, EPI_F32 = 3 };
+// EPI_PART: raw fp32 split-K partials to ws_part[split][row][N] (the residual
+// add and fused RMSNorm then run in splitk_reduce_add_kernel)
+enum GemmEpi { EPI_QKV = 0, EPI_ADD = 1, EPI_SILU = 2, EPI_F32 = 3, EPI_PART = 4 };
 
 struct GemmArgs {
   int rows_max = 0;             // launch bound on M (tensor-map rows)
@@ -46,6 +48,7 @@ struct GemmArgs {
   float* norm_inv = nullptr;    // [rows_max]
   int* norm_cnt = nullptr;      // [m tiles * 4], zero-initialised, self-resetting
   float norm_eps = 1e-5f;
+  float* ws_part = nullptr;  // EPI_PART workspace [splits][rows_max][N]
 };
 constexpr int kNormSlots = 64;  // max N tiles of a residual GEMM (d_model / BN)
 
