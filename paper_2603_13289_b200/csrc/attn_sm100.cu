@@ -88,8 +88,11 @@ constexpr int kThreadsA = 256;        // softmax warpgroup + control warpgroup
 
 template <int DH>
 struct ACfg {
-  // keys per tile: 128 at d_head 64; 64 at d_head 128 so that two CTAs fit
-  // per SM there too (112 KB smem each)
+  // keys per tile: 128 at d_head 64, 64 at d_head 128, so that two CTAs
+  // (112 KB smem, 256 TMEM columns each) share every SM and one CTA's softmax
+  // overlaps the other's MMAs, loads and epilogue. (Measured: 64-key tiles
+  // with three CTAs per SM at d_head 64 are slower -- the per-tile fixed
+  // softmax latency dominates.)
   static constexpr int KEYS = DH == 64 ? 128 : 64;
   static constexpr int KB = KEYS / 64;             // 64-key swizzle blocks of S / P
   static constexpr int Q_TILE = kQ * DH * 2;
@@ -104,8 +107,13 @@ struct ACfg {
   static constexpr int SMEM = OFF_BAR + 128;
   static constexpr int CTAS = 2;  // CTAs per SM
   static_assert(CTAS * (SMEM + 1024) <= 233472, "shared memory per SM");
-  static constexpr uint32_t TMEM_COLS = 256;
-  static constexpr uint32_t S_COL = 0, O_COL = 128;  // S [0,128), O [128, 128+DH)
+  static constexpr uint32_t TMEM_COLS = KEYS + DH <= 128 ? 128 : 256;
+  static_assert(CTAS * TMEM_COLS <= 512, "tensor memory per SM");
+  static constexpr uint32_t S_COL = 0, O_COL = KEYS;  // S [0,KEYS), O [KEYS, KEYS+DH)
+  // setmaxnreg: control warpgroup down to REG_CTL, softmax up to REG_SM
+  static constexpr int REG_LAUNCH = (65536 / (CTAS * 256)) / 8 * 8;
+  static constexpr int REG_CTL = CTAS == 3 ? 24 : 56;
+  static constexpr int REG_SM = (REG_LAUNCH * 2 - REG_CTL) / 8 * 8;
 };
 
 // Query tile `tile` of the launch -> rows [r0, r1) within one row group.
@@ -208,7 +216,7 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
   constexpr int DB = DH / 64;  // 64-wide swizzle blocks along d
 
   if (warp >= 4) {  // ------------------------------------------ control warpgroup
-    if constexpr (C::CTAS == 2) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(C::REG_CTL) : "memory");
     if (warp == 4) {
       if (elect_one()) {  // ---------------------------------------- TMA K
         for (int j = 0; j < nk; ++j) {
@@ -285,7 +293,7 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
       }
     }
   } else {  // ------------------------------------------------ softmax warpgroup
-    if constexpr (C::CTAS == 2) asm volatile("setmaxnreg.inc.sync.aligned.u32 200;\n" ::: "memory");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(C::REG_SM) : "memory");
     const bool tracing = trace_cta && warp == 0 && lane == 0;
     const int rl = warp * 32 + lane;  // row within the tile == TMEM lane
     const int row = r0 + rl;

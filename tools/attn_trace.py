@@ -17,6 +17,7 @@ if __name__ == "__main__":
     _check(lib().rk_debug_trace_attention(P(e.ptr), M, T, H, Hkv, dh, out.ctypes.data_as(C.POINTER(C.c_uint64))))
     tr = out.reshape(3, 64, 8).astype(np.int64)
     t0 = tr[tr > 0].min()
+    print("grid-wide: CTA (head 0, last tile, split 0); timestamps in SM clocks from its first event")
     for role in range(3):
         names = EV_MMA if role == 2 else EV_SM
         print(f"role {role} ({'MMA' if role == 2 else 'softmax ' + str(role)})")
