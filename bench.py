@@ -234,6 +234,21 @@ def cpu_sample(gpu_caches=None, threads=None, steps=1, warmup=0, kind="reference
     return tps, meta
 
 
+def pin_host(host):
+    """Move a HostRelayCache's arrays into page-locked memory (torch pinned
+    tensors; the tensors are kept alive on the object)."""
+    import torch
+    keep = []
+    for f in ("segment_tokens", "k_pre", "v", "hidden_snapshot", "influence"):
+        a = getattr(host, f)
+        t = torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype, pin_memory=True)
+        t.numpy()[...] = a
+        keep.append(t)
+        setattr(host, f, t.numpy())
+    host._pinned = keep
+    return host
+
+
 def merge_kernel_stats(stats):
     """Collapse per-shape labels (gemm_qkv_m320_..., attn_m...) into kernel families."""
     fam = {}
@@ -334,8 +349,9 @@ def run_ours(args, world, rank, local, dist):
     full_ms = reduce_max(dist, full_ms, local) / max(2, args.steps // 2)
 
     # end to end through the C ABI with HOST buffers: RelayCache fp32 arrays
-    # uploaded every step (rk_cache_upload), tokens staged, logits read back.
-    hosts = [c.to_host() for c in caches]
+    # (the reference's struct, in pinned host memory) uploaded every step
+    # (rk_cache_upload), tokens staged, logits read back.
+    hosts = [pin_host(c.to_host()) for c in caches]
 
     def e2e_step():
         ups = [w.upload_cache(h) for h in hosts]

@@ -85,10 +85,28 @@ void DevBuf::alloc(size_t n) {
                                     cudaGetErrorString(e));
   }
 }
+void DevBuf::alloc_pooled(BlockPool* pl, size_t n) {
+  release();
+  pool = pl;
+  auto it = pl->find(n);
+  if (it != pl->end()) {
+    p = it->second;
+    bytes = n;
+    pl->erase(it);
+    return;
+  }
+  alloc(n);
+  pool = pl;
+}
+
 void DevBuf::release() {
-  if (p) cudaFree(p);
+  if (p) {
+    if (pool) pool->emplace(bytes, p);
+    else cudaFree(p);
+  }
   p = nullptr;
   bytes = 0;
+  pool = nullptr;
 }
 
 RopeTable* rope_table(rk_engine* e, float theta, uint64_t d_head, uint64_t positions) {
@@ -123,6 +141,8 @@ RopeTable* rope_table(rk_engine* e, float theta, uint64_t d_head, uint64_t posit
 
 rk_engine::rk_engine() : scratch(new Scratch()) {}
 rk_engine::~rk_engine() {
+  for (auto& kv : cache_pool) cudaFree(kv.second);
+  cache_pool.clear();
   scratch.reset();
   rope.clear();
   if (pinned) cudaFreeHost(pinned);
@@ -484,19 +504,24 @@ int rk_cache_upload(rk_engine* e, rk_weights* w, const rk_relay_cache_view* v, r
     c->snapshot = v->snapshot_layer;
     c->steps = v->decode_steps_observed;
     const size_t kv = c->kv();
-    c->tokens.alloc(n * 4);
+    BlockPool* pl = &e->cache_pool;
+    c->tokens.alloc_pooled(pl, n * 4);
     c->host_tokens.assign(v->segment_tokens, v->segment_tokens + n);
-    c->k_pre.alloc(c->L * n * kv * c->elem);
-    c->v.alloc(c->L * n * kv * c->elem);
-    c->hidden.alloc(n * c->d * 4);
-    c->influence.alloc(n * 4);
-    c->infl_mean.alloc(8);
+    c->k_pre.alloc_pooled(pl, c->L * n * kv * c->elem);
+    c->v.alloc_pooled(pl, c->L * n * kv * c->elem);
+    c->hidden.alloc_pooled(pl, n * c->d * 4);
+    c->influence.alloc_pooled(pl, n * 4);
+    c->infl_mean.alloc_pooled(pl, 8);
     cudaStream_t st = e->stream;
     RK_CUDA(cudaMemcpyAsync(c->tokens.p, v->segment_tokens, n * 4, cudaMemcpyHostToDevice, st));
     RK_CUDA(cudaMemcpyAsync(c->hidden.p, v->hidden_snapshot, n * c->d * 4, cudaMemcpyHostToDevice, st));
     RK_CUDA(cudaMemcpyAsync(c->influence.p, v->influence, n * 4, cudaMemcpyHostToDevice, st));
+    // bf16: each fp32 layer lands in a staging buffer and is converted on the
+    // device; two staging buffers alternate (stream order keeps them safe, no
+    // host round trip), so pinned sources stream at copy-engine speed
     DevBuf tmp;
-    if (c->elem == 2) tmp.alloc(n * kv * 4);
+    if (c->elem == 2) tmp.alloc_pooled(pl, 2 * n * kv * 4);
+    int flip = 0;
     for (uint64_t l = 0; l < c->L; ++l) {
       for (int which = 0; which < 2; ++which) {
         const float* src = which == 0 ? v->k_pre[l] : v->v[l];
@@ -504,11 +529,12 @@ int rk_cache_upload(rk_engine* e, rk_weights* w, const rk_relay_cache_view* v, r
         if (c->elem == 4) {
           RK_CUDA(cudaMemcpyAsync(dst, src, n * kv * 4, cudaMemcpyHostToDevice, st));
         } else {
-          RK_CUDA(cudaMemcpyAsync(tmp.p, src, n * kv * 4, cudaMemcpyHostToDevice, st));
-          k::f32_to_bf16(st, reinterpret_cast<__nv_bfloat16*>(dst), tmp.as<float>(), n * kv);
+          float* stage = tmp.as<float>() + (size_t)flip * n * kv;
+          flip ^= 1;
+          RK_CUDA(cudaMemcpyAsync(stage, src, n * kv * 4, cudaMemcpyHostToDevice, st));
+          k::f32_to_bf16(st, reinterpret_cast<__nv_bfloat16*>(dst), stage, n * kv);
         }
       }
-      if (c->elem == 2) RK_CUDA(cudaStreamSynchronize(st));  // tmp reuse
     }
     // influence mean, sequential in double (selector.cpp:37-39) -- cache-static
     double mean = 0.0;

@@ -27,21 +27,34 @@ void cuda_check(cudaError_t e, const char* what, const char* file, int line);
 void set_last_error(const std::string& msg);
 #define RK_CUDA(x) ::rk::cuda_check((x), #x, __FILE__, __LINE__)
 
-// Owning device allocation.
+// Free device blocks kept for reuse (exact-size match), so per-call objects
+// (relay caches uploaded every agent hop) do not pay cudaMalloc/cudaFree --
+// cudaFree synchronizes the whole device.
+using BlockPool = std::multimap<size_t, void*>;
+
+// Owning device allocation (optionally drawn from / returned to a BlockPool).
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  BlockPool* pool = nullptr;
   DevBuf() = default;
   explicit DevBuf(size_t n) { alloc(n); }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes), pool(o.pool) { o.p = nullptr; o.bytes = 0; o.pool = nullptr; }
   DevBuf& operator=(DevBuf&& o) noexcept {
-    if (this != &o) { release(); p = o.p; bytes = o.bytes; o.p = nullptr; o.bytes = 0; }
+    if (this != &o) {
+      release();
+      p = o.p; bytes = o.bytes; pool = o.pool;
+      o.p = nullptr; o.bytes = 0; o.pool = nullptr;
+    }
     return *this;
   }
   ~DevBuf() { release(); }
   void alloc(size_t n);
+  // take an exact-size block from `pl` if one is free (callers must have
+  // synchronized the stream that last used blocks returned to it)
+  void alloc_pooled(BlockPool* pl, size_t n);
   void release();
   // grow (contents discarded) to at least n bytes
   void ensure(size_t n) { if (n > bytes) { release(); alloc(n); } }
@@ -81,6 +94,7 @@ struct rk_engine {
   rk::DevBuf status;  // int flags: [0] non-finite
   std::vector<cudaEvent_t> events;
   std::vector<std::unique_ptr<rk::ExtendSlot>> slots;
+  rk::BlockPool cache_pool;  // device blocks of destroyed relay caches
   std::unique_ptr<rk::Profiler> prof;
   rk_engine();
   ~rk_engine();

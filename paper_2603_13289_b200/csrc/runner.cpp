@@ -748,12 +748,13 @@ static rk_cache* new_cache(rk_engine* e, rk_weights* w, uint64_t n, uint64_t src
   c->snapshot = snapshot;
   c->steps = n;
   const size_t kv = c->kv();
-  c->tokens.alloc(n * 4);
-  c->k_pre.alloc(c->L * n * kv * c->elem);
-  c->v.alloc(c->L * n * kv * c->elem);
-  c->hidden.alloc(n * c->d * 4);
-  c->influence.alloc(n * 4);
-  c->infl_mean.alloc(8);
+  BlockPool* pl = &e->cache_pool;
+  c->tokens.alloc_pooled(pl, n * 4);
+  c->k_pre.alloc_pooled(pl, c->L * n * kv * c->elem);
+  c->v.alloc_pooled(pl, c->L * n * kv * c->elem);
+  c->hidden.alloc_pooled(pl, n * c->d * 4);
+  c->influence.alloc_pooled(pl, n * 4);
+  c->infl_mean.alloc_pooled(pl, 8);
   c->host_tokens.resize(n);
   return c.release();
 }
