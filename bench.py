@@ -354,7 +354,9 @@ def run_ours(args, world, rank, local, dist):
     hosts = [pin_host(c.to_host()) for c in caches]
 
     def e2e_step():
-        ups = [w.upload_cache(h) for h in hosts]
+        # layer-streamed uploads: the relay prefill starts while later layers
+        # of the caches are still crossing PCIe (rk_cache_upload_async)
+        ups = [w.upload_cache(h, asynchronous=True) for h in hosts]
         ctx.reset()
         out = ctx.agent_prefill(mine[0]["prefix"], ups, mine[0]["suffix"], prof, opts, want_logits=True)
         return out["first_token"]
@@ -367,6 +369,14 @@ def run_ours(args, world, rank, local, dist):
     for _ in range(e2e_K):
         e2e_step()
     e2e_ms = reduce_max(dist, (time.perf_counter() - h0) * 1e3, local) / e2e_K  # one session per rank
+    # the upload alone (diagnostic: how much of e2e is PCIe)
+    h0 = time.perf_counter()
+    for _ in range(e2e_K):
+        ups = [w.upload_cache(h, asynchronous=True) for h in hosts]
+        for c in ups:
+            c.wait()
+        del ups
+    upload_ms = (time.perf_counter() - h0) * 1e3 / e2e_K
     h2d = sum(h.k_pre.nbytes + h.v.nbytes + h.hidden_snapshot.nbytes + h.influence.nbytes + h.segment_tokens.nbytes
               for h in hosts) + 4 * (WL["prefix"] + WL["suffix"])
     d2h = 4 * WL["spec"]["vocab_size"] + 4
@@ -438,7 +448,8 @@ def run_ours(args, world, rank, local, dist):
         "selected_per_segment": selected,
         "host_ms_per_step": round(host_ms / args.steps, 4),
         "e2e": {"value": round(world * n_tokens / (e2e_ms / 1e3), 1), "unit": "tokens/s",
-                "ttft_ms": round(e2e_ms, 3), "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+                "ttft_ms": round(e2e_ms, 3), "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "upload_only_ms": round(upload_ms, 3), "h2d_gbs": round(h2d / (upload_ms / 1e3) / 1e9, 1)},
         "gpu_launches": int(launches),
         "roofline": roofline,
         "kernels": kernels,

@@ -224,6 +224,16 @@ int rk_cache_capture_decode(rk_engine* e, rk_weights* w, rk_context* ctx,
 int rk_cache_capture_prefill(rk_engine* e, rk_weights* w, rk_context* ctx,
                              const int32_t* segment_tokens, uint64_t n, uint64_t snapshot_layer,
                              int include_self, rk_cache** out);
+/* Asynchronous upload: validates and returns at once; the layers stream to
+ * the device in layer order on the engine's copy stream, and every later call
+ * that reads layer l of this cache waits (on the device) for that layer only,
+ * so a relay prefill starts while the cache is still arriving. The view's host
+ * arrays must stay valid until rk_cache_wait or rk_cache_destroy; pinned host
+ * memory makes the copies truly asynchronous. */
+int rk_cache_upload_async(rk_engine* e, rk_weights* w, const rk_relay_cache_view* view,
+                          rk_cache** out);
+/* Block until an asynchronous upload has landed (the host arrays may be freed). */
+int rk_cache_wait(rk_cache* c);
 uint64_t rk_cache_segment_len(const rk_cache* c);
 /* Copy a cache back to host (fp32). Any pointer may be NULL. k_pre/v: [L] arrays of [n x kv]. */
 int rk_cache_export(rk_cache* c, int32_t* tokens, float* const* k_pre, float* const* v,

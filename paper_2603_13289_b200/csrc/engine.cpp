@@ -150,6 +150,11 @@ rk_engine::~rk_engine() {
     cudaStreamSynchronize(side);
     cudaStreamDestroy(side);
   }
+  for (auto& x : xfer)
+    if (x) {
+      cudaStreamSynchronize(x);
+      cudaStreamDestroy(x);
+    }
   if (side_fork) cudaEventDestroy(side_fork);
   if (side_join) cudaEventDestroy(side_join);
   if (stream) cudaStreamDestroy(stream);
@@ -175,13 +180,17 @@ void rk_context::reserve(uint64_t positions) {
   cap = ncap;
 }
 
-void rk_context::resize(uint64_t positions) {  // KVContext::resize (model.cpp:124-131)
+void rk_context::resize(uint64_t positions, bool zero_fill) {  // KVContext::resize (model.cpp:124-131)
   if (positions < size) raise(RK_ERR_INVALID_ARGUMENT, "KVContext::resize: cannot shrink");
   if (positions == size) return;
   reserve(positions);
   const size_t L = w->s.num_layers, row = w->kv() * elem;
-  RK_CUDA(cudaMemset2DAsync(static_cast<char*>(k.p) + size * row, cap * row, 0, (positions - size) * row, L, e->stream));
-  RK_CUDA(cudaMemset2DAsync(static_cast<char*>(v.p) + size * row, cap * row, 0, (positions - size) * row, L, e->stream));
+  if (!zero_fill) {
+    size = positions;
+    return;
+  }
+  rk::k::zero_rows(e->stream, static_cast<char*>(k.p) + size * row, cap * row, (positions - size) * row, L);
+  rk::k::zero_rows(e->stream, static_cast<char*>(v.p) + size * row, cap * row, (positions - size) * row, L);
   size = positions;
 }
 
@@ -339,6 +348,11 @@ int rk_engine_create(int device, rk_engine** out) {
     require(major == 10, RK_ERR_RUNTIME, "relaykv-b200 kernels are built for sm_100a (B200)");
     RK_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
     RK_CUDA(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
+    // copy streams at the highest priority: their small fp32->bf16 convert
+    // kernels take the next free SM slot instead of queueing behind the pass
+    int prio_lo = 0, prio_hi = 0;
+    RK_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    for (auto& x : e->xfer) RK_CUDA(cudaStreamCreateWithPriority(&x, cudaStreamNonBlocking, prio_hi));
     RK_CUDA(cudaEventCreateWithFlags(&e->side_fork, cudaEventDisableTiming));
     RK_CUDA(cudaEventCreateWithFlags(&e->side_join, cudaEventDisableTiming));
     e->status.alloc(64);
@@ -476,73 +490,113 @@ void rk_weights_destroy(rk_weights* w) {
 }
 
 // ---- relay caches ---------------------------------------------------------
+namespace {
+// RelayCache::validate + upload (relay_cache.cpp:18-41). async: everything on
+// the copy stream with per-layer events, no host synchronization.
+rk_cache* upload_cache(rk_engine* e, rk_weights* w, const rk_relay_cache_view* v, bool async) {
+  require(v != nullptr && w != nullptr, RK_ERR_INVALID_ARGUMENT, "null cache view / weights");
+  const uint64_t n = v->segment_len;
+  require(n > 0, RK_ERR_INVALID_ARGUMENT, "relay cache: empty segment");
+  require(v->num_layers > 0 && v->k_pre && v->v, RK_ERR_INVALID_ARGUMENT,
+          "relay cache: per-layer K/V tables disagree");
+  require(v->snapshot_layer < v->num_layers, RK_ERR_INVALID_ARGUMENT,
+          "relay cache: snapshot layer out of range");
+  for (uint64_t j = 0; j < n; ++j)
+    require(v->influence[j] >= 0.0f, RK_ERR_INVALID_ARGUMENT, "relay cache: negative influence score");
+  auto c = std::make_unique<rk_cache>();
+  c->e = e;
+  c->precision = w->precision;
+  c->elem = w->elem;
+  c->L = v->num_layers;
+  c->Hkv = v->num_kv_heads;
+  c->dh = v->d_head;
+  c->d = v->d_model;
+  c->n = n;
+  c->maxpos = v->max_positions;
+  c->theta = v->theta_base;
+  c->src_base = v->source_base_position;
+  c->snapshot = v->snapshot_layer;
+  c->steps = v->decode_steps_observed;
+  const size_t kv = c->kv();
+  BlockPool* pl = &e->cache_pool;
+  c->tokens.alloc_pooled(pl, n * 4);
+  c->host_tokens.assign(v->segment_tokens, v->segment_tokens + n);
+  c->k_pre.alloc_pooled(pl, c->L * n * kv * c->elem);
+  c->v.alloc_pooled(pl, c->L * n * kv * c->elem);
+  c->hidden.alloc_pooled(pl, n * c->d * 4);
+  c->influence.alloc_pooled(pl, n * 4);
+  c->infl_mean.alloc_pooled(pl, 8);
+  // (pooled blocks are idle: rk_cache_destroy synchronized their last reader)
+  cudaStream_t st = e->stream;
+  if (async) {
+    st = e->xfer[e->next_xfer];
+    e->next_xfer = (e->next_xfer + 1) % rk_engine::kXfer;
+    c->xfer = st;
+  }
+  // influence mean, sequential in double (selector.cpp:37-39) -- cache-static
+  double mean = 0.0;
+  for (uint64_t j = 0; j < n; ++j) mean += static_cast<double>(v->influence[j]);
+  mean /= static_cast<double>(n);
+  RK_CUDA(cudaMemcpyAsync(c->tokens.p, v->segment_tokens, n * 4, cudaMemcpyHostToDevice, st));
+  RK_CUDA(cudaMemcpyAsync(c->hidden.p, v->hidden_snapshot, n * c->d * 4, cudaMemcpyHostToDevice, st));
+  RK_CUDA(cudaMemcpyAsync(c->influence.p, v->influence, n * 4, cudaMemcpyHostToDevice, st));
+  k::fill_doubles(st, c->infl_mean.as<double>(), 1, mean);
+  if (async) {
+    c->async = true;
+    RK_CUDA(cudaEventCreateWithFlags(&c->ev_meta, cudaEventDisableTiming));
+    RK_CUDA(cudaEventRecord(c->ev_meta, st));
+    c->ev_layer.resize(c->L);
+  }
+  // bf16: each fp32 layer lands in a staging buffer and is converted on the
+  // device; two staging buffers alternate (stream order keeps them safe, no
+  // host round trip), so pinned sources stream at copy-engine speed
+  if (c->elem == 2) c->staging.alloc_pooled(pl, 2 * n * kv * 4);
+  int flip = 0;
+  for (uint64_t l = 0; l < c->L; ++l) {
+    for (int which = 0; which < 2; ++which) {
+      const float* src = which == 0 ? v->k_pre[l] : v->v[l];
+      char* dst = static_cast<char*>(which == 0 ? c->k_pre.p : c->v.p) + l * n * kv * c->elem;
+      if (c->elem == 4) {
+        RK_CUDA(cudaMemcpyAsync(dst, src, n * kv * 4, cudaMemcpyHostToDevice, st));
+      } else {
+        float* stage = c->staging.as<float>() + (size_t)flip * n * kv;
+        flip ^= 1;
+        RK_CUDA(cudaMemcpyAsync(stage, src, n * kv * 4, cudaMemcpyHostToDevice, st));
+        k::f32_to_bf16(st, reinterpret_cast<__nv_bfloat16*>(dst), stage, n * kv);
+      }
+    }
+    if (async) {
+      RK_CUDA(cudaEventCreateWithFlags(&c->ev_layer[l], cudaEventDisableTiming));
+      RK_CUDA(cudaEventRecord(c->ev_layer[l], st));
+    }
+  }
+  if (!async) {
+    RK_CUDA(cudaStreamSynchronize(st));
+    c->staging.release();
+  }
+  return c.release();
+}
+}  // namespace
+
 int rk_cache_upload(rk_engine* e, rk_weights* w, const rk_relay_cache_view* v, rk_cache** out) {
   return guard([&] {
     DeviceGuard g(e->device);
-    require(v != nullptr && w != nullptr, RK_ERR_INVALID_ARGUMENT, "null cache view / weights");
-    // RelayCache::validate (relay_cache.cpp:18-41)
-    const uint64_t n = v->segment_len;
-    require(n > 0, RK_ERR_INVALID_ARGUMENT, "relay cache: empty segment");
-    require(v->num_layers > 0 && v->k_pre && v->v, RK_ERR_INVALID_ARGUMENT,
-            "relay cache: per-layer K/V tables disagree");
-    require(v->snapshot_layer < v->num_layers, RK_ERR_INVALID_ARGUMENT,
-            "relay cache: snapshot layer out of range");
-    for (uint64_t j = 0; j < n; ++j)
-      require(v->influence[j] >= 0.0f, RK_ERR_INVALID_ARGUMENT, "relay cache: negative influence score");
-    auto c = std::make_unique<rk_cache>();
-    c->e = e;
-    c->precision = w->precision;
-    c->elem = w->elem;
-    c->L = v->num_layers;
-    c->Hkv = v->num_kv_heads;
-    c->dh = v->d_head;
-    c->d = v->d_model;
-    c->n = n;
-    c->maxpos = v->max_positions;
-    c->theta = v->theta_base;
-    c->src_base = v->source_base_position;
-    c->snapshot = v->snapshot_layer;
-    c->steps = v->decode_steps_observed;
-    const size_t kv = c->kv();
-    BlockPool* pl = &e->cache_pool;
-    c->tokens.alloc_pooled(pl, n * 4);
-    c->host_tokens.assign(v->segment_tokens, v->segment_tokens + n);
-    c->k_pre.alloc_pooled(pl, c->L * n * kv * c->elem);
-    c->v.alloc_pooled(pl, c->L * n * kv * c->elem);
-    c->hidden.alloc_pooled(pl, n * c->d * 4);
-    c->influence.alloc_pooled(pl, n * 4);
-    c->infl_mean.alloc_pooled(pl, 8);
-    cudaStream_t st = e->stream;
-    RK_CUDA(cudaMemcpyAsync(c->tokens.p, v->segment_tokens, n * 4, cudaMemcpyHostToDevice, st));
-    RK_CUDA(cudaMemcpyAsync(c->hidden.p, v->hidden_snapshot, n * c->d * 4, cudaMemcpyHostToDevice, st));
-    RK_CUDA(cudaMemcpyAsync(c->influence.p, v->influence, n * 4, cudaMemcpyHostToDevice, st));
-    // bf16: each fp32 layer lands in a staging buffer and is converted on the
-    // device; two staging buffers alternate (stream order keeps them safe, no
-    // host round trip), so pinned sources stream at copy-engine speed
-    DevBuf tmp;
-    if (c->elem == 2) tmp.alloc_pooled(pl, 2 * n * kv * 4);
-    int flip = 0;
-    for (uint64_t l = 0; l < c->L; ++l) {
-      for (int which = 0; which < 2; ++which) {
-        const float* src = which == 0 ? v->k_pre[l] : v->v[l];
-        char* dst = static_cast<char*>(which == 0 ? c->k_pre.p : c->v.p) + l * n * kv * c->elem;
-        if (c->elem == 4) {
-          RK_CUDA(cudaMemcpyAsync(dst, src, n * kv * 4, cudaMemcpyHostToDevice, st));
-        } else {
-          float* stage = tmp.as<float>() + (size_t)flip * n * kv;
-          flip ^= 1;
-          RK_CUDA(cudaMemcpyAsync(stage, src, n * kv * 4, cudaMemcpyHostToDevice, st));
-          k::f32_to_bf16(st, reinterpret_cast<__nv_bfloat16*>(dst), stage, n * kv);
-        }
-      }
-    }
-    // influence mean, sequential in double (selector.cpp:37-39) -- cache-static
-    double mean = 0.0;
-    for (uint64_t j = 0; j < n; ++j) mean += static_cast<double>(v->influence[j]);
-    mean /= static_cast<double>(n);
-    RK_CUDA(cudaMemcpyAsync(c->infl_mean.p, &mean, 8, cudaMemcpyHostToDevice, st));
-    RK_CUDA(cudaStreamSynchronize(st));
-    *out = c.release();
+    *out = upload_cache(e, w, v, false);
+  });
+}
+
+int rk_cache_upload_async(rk_engine* e, rk_weights* w, const rk_relay_cache_view* v, rk_cache** out) {
+  return guard([&] {
+    DeviceGuard g(e->device);
+    *out = upload_cache(e, w, v, true);
+  });
+}
+
+int rk_cache_wait(rk_cache* c) {
+  return guard([&] {
+    require(c != nullptr, RK_ERR_INVALID_ARGUMENT, "null cache");
+    DeviceGuard g(c->e->device);
+    if (c->async) RK_CUDA(cudaStreamSynchronize(c->xfer));
   });
 }
 
@@ -552,6 +606,7 @@ int rk_cache_export(rk_cache* c, int32_t* tokens, float* const* k_pre, float* co
                     float* hidden, float* influence, uint64_t* src_base, uint64_t* snapshot) {
   return guard([&] {
     DeviceGuard g(c->e->device);
+    if (c->async) RK_CUDA(cudaStreamSynchronize(c->xfer));
     cudaStream_t st = c->e->stream;
     const size_t kv = c->kv(), n = c->n;
     if (tokens) RK_CUDA(cudaMemcpyAsync(tokens, c->tokens.p, n * 4, cudaMemcpyDeviceToHost, st));
@@ -578,10 +633,17 @@ int rk_cache_export(rk_cache* c, int32_t* tokens, float* const* k_pre, float* co
   });
 }
 
+rk_cache::~rk_cache() {
+  if (ev_meta) cudaEventDestroy(ev_meta);
+  for (cudaEvent_t ev : ev_layer)
+    if (ev) cudaEventDestroy(ev);
+}
+
 void rk_cache_destroy(rk_cache* c) {
   if (!c) return;
   DeviceGuard g(c->e->device, true);
   cudaStreamSynchronize(c->e->stream);
+  if (c->async) cudaStreamSynchronize(c->xfer);
   delete c;
 }
 

@@ -83,6 +83,11 @@ struct rk_engine {
   // side stream for off-critical-path reporting kernels (joined at the next call)
   cudaStream_t side = nullptr;
   cudaEvent_t side_fork = nullptr, side_join = nullptr;
+  // copy streams of asynchronous relay-cache uploads (round-robin per cache, so
+  // the layers of several upstream caches arrive interleaved)
+  static constexpr int kXfer = 4;
+  cudaStream_t xfer[kXfer] = {};
+  int next_xfer = 0;
   uint64_t launches = 0;
   int use_graphs = 0;
   int fused = 1;  // layer-major fused agent schedule (runner.cpp agent_fused)
@@ -142,7 +147,15 @@ struct rk_cache {
   rk::DevBuf influence;  // fp32 [n]
   rk::DevBuf infl_mean;  // double [1], sequential mean (selector.cpp:37-39)
   std::vector<int32_t> host_tokens;
+  // asynchronous upload (rk_cache_upload_async): per-layer readiness on the
+  // engine's copy stream; ev_meta covers tokens / hidden / influence
+  bool async = false;
+  cudaStream_t xfer = nullptr;
+  cudaEvent_t ev_meta = nullptr;
+  std::vector<cudaEvent_t> ev_layer;
+  rk::DevBuf staging;  // fp32 layer staging of the bf16 conversion
   size_t kv() const { return Hkv * dh; }
+  ~rk_cache();
 };
 
 struct rk_segment_marks {
@@ -160,7 +173,9 @@ struct rk_context {
   void* k_layer(size_t l) const { return static_cast<char*>(k.p) + l * cap * w->kv() * elem; }
   void* v_layer(size_t l) const { return static_cast<char*>(v.p) + l * cap * w->kv() * elem; }
   void reserve(uint64_t positions);
-  void resize(uint64_t positions);
+  // zero_fill=false: the caller writes every new cell of every layer before
+  // anything reads it (the fused agent schedule), so the fill is skipped
+  void resize(uint64_t positions, bool zero_fill = true);
 };
 
 namespace rk {
@@ -213,6 +228,12 @@ void iota_positions(cudaStream_t s, int* pos, int n, int base);
 void mark_rows(cudaStream_t s, uint8_t* origin, int len, int layer_lo, int layer_hi, const int* sel,
                const int* count, int rows_max);
 void mark_layers(cudaStream_t s, uint8_t* origin, int len, int layer_lo, int layer_hi);
+// device memset / memcpy / 2-D row zero as kernels (see kernels_common.cu)
+void zero_dev(cudaStream_t s, void* dst, size_t bytes);
+void copy_dev(cudaStream_t s, void* dst, const void* src, size_t bytes);
+void zero_rows(cudaStream_t s, void* dst, size_t pitch, size_t width, size_t rows);
+void copy_i32(cudaStream_t s, int* dst, const int* src, int n);  // src may be mapped host memory
+void fill_doubles(cudaStream_t s, double* dst, int n, double v);
 void set_depth(cudaStream_t s, uint64_t* depth, int n, uint64_t v);
 // ws: >= 148 float2 of scratch
 void argmax(cudaStream_t s, const float* x, int n, int* out, void* ws);

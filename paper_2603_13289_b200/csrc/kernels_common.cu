@@ -181,6 +181,48 @@ __global__ void mark_layers_kernel(uint8_t* origin, int len, int lo, int hi) {
        i += (size_t)gridDim.x * blockDim.x)
     origin[(size_t)lo * len + i] = 1;
 }
+// Device-side zero fill / copy as kernels (not copy-engine operations, which
+// would queue behind relay-cache uploads streaming on the copy engines).
+__global__ void zero_bytes_kernel(uint8_t* dst, size_t n) {
+  const size_t i0 = (blockIdx.x * (size_t)blockDim.x + threadIdx.x), stride = (size_t)gridDim.x * blockDim.x;
+  if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+    for (size_t i = i0; i < n / 16; i += stride) d4[i] = make_uint4(0, 0, 0, 0);
+    for (size_t i = n / 16 * 16 + i0; i < n; i += stride) dst[i] = 0;
+  } else {
+    for (size_t i = i0; i < n; i += stride) dst[i] = 0;
+  }
+}
+__global__ void copy_bytes_kernel(uint8_t* dst, const uint8_t* src, size_t n) {
+  const size_t i0 = (blockIdx.x * (size_t)blockDim.x + threadIdx.x), stride = (size_t)gridDim.x * blockDim.x;
+  if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+    const uint4* s4 = reinterpret_cast<const uint4*>(src);
+    for (size_t i = i0; i < n / 16; i += stride) d4[i] = s4[i];
+    for (size_t i = n / 16 * 16 + i0; i < n; i += stride) dst[i] = src[i];
+  } else {
+    for (size_t i = i0; i < n; i += stride) dst[i] = src[i];
+  }
+}
+// rows x width bytes at pitch
+__global__ void zero_rows_kernel(uint8_t* dst, size_t pitch, size_t width, size_t rows) {
+  for (size_t r = blockIdx.y; r < rows; r += gridDim.y) {
+    uint8_t* d = dst + r * pitch;
+    if (((reinterpret_cast<uintptr_t>(d) | width) & 15) == 0) {
+      for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < width / 16; i += (size_t)gridDim.x * blockDim.x)
+        reinterpret_cast<uint4*>(d)[i] = make_uint4(0, 0, 0, 0);
+    } else {
+      for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < width; i += (size_t)gridDim.x * blockDim.x)
+        d[i] = 0;
+    }
+  }
+}
+__global__ void copy_i32_kernel(int* dst, const int* src, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = src[i];
+}
+__global__ void fill_doubles_kernel(double* dst, int n, double v) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = v;
+}
 __global__ void set_depth_kernel(uint64_t* depth, int n, uint64_t v) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) depth[i] = v;
 }
@@ -845,6 +887,29 @@ void mark_rows(cudaStream_t s, uint8_t* origin, int len, int lo, int hi, const i
 void mark_layers(cudaStream_t s, uint8_t* origin, int len, int lo, int hi) {
   if (hi < lo) return;
   mark_layers_kernel<<<blocks_for((size_t)(hi - lo + 1) * len), kThreads, 0, s>>>(origin, len, lo, hi);
+}
+void zero_dev(cudaStream_t s, void* dst, size_t bytes) {
+  if (!bytes) return;
+  const size_t blocks = std::min<size_t>(1184, (bytes / 16 + kThreads - 1) / kThreads + 1);
+  zero_bytes_kernel<<<(unsigned)blocks, kThreads, 0, s>>>(static_cast<uint8_t*>(dst), bytes);
+}
+void copy_dev(cudaStream_t s, void* dst, const void* src, size_t bytes) {
+  if (!bytes) return;
+  const size_t blocks = std::min<size_t>(1184, (bytes / 16 + kThreads - 1) / kThreads + 1);
+  copy_bytes_kernel<<<(unsigned)blocks, kThreads, 0, s>>>(static_cast<uint8_t*>(dst),
+                                                          static_cast<const uint8_t*>(src), bytes);
+}
+void zero_rows(cudaStream_t s, void* dst, size_t pitch, size_t width, size_t rows) {
+  if (!width || !rows) return;
+  dim3 grid((unsigned)std::min<size_t>(64, (width / 16 + kThreads - 1) / kThreads + 1),
+            (unsigned)std::min<size_t>(rows, 1024));
+  zero_rows_kernel<<<grid, kThreads, 0, s>>>(static_cast<uint8_t*>(dst), pitch, width, rows);
+}
+void copy_i32(cudaStream_t s, int* dst, const int* src, int n) {
+  if (n > 0) copy_i32_kernel<<<std::min(64, blocks_for(n)), kThreads, 0, s>>>(dst, src, n);
+}
+void fill_doubles(cudaStream_t s, double* dst, int n, double v) {
+  fill_doubles_kernel<<<blocks_for(n), kThreads, 0, s>>>(dst, n, v);
 }
 void set_depth(cudaStream_t s, uint64_t* depth, int n, uint64_t v) {
   set_depth_kernel<<<blocks_for(n), kThreads, 0, s>>>(depth, n, v);

@@ -22,7 +22,7 @@ float* fptr(void* p, size_t off_elems = 0) { return static_cast<float*>(p) + off
 Runner::Runner(rk_engine* e, rk_weights* w) : e_(e), w_(w), st_(e->stream) {
   require(e != nullptr && w != nullptr, RK_ERR_INVALID_ARGUMENT, "null engine / weights");
   require(w->e == e, RK_ERR_INVALID_ARGUMENT, "weights belong to another engine");
-  RK_CUDA(cudaMemsetAsync(e->status.p, 0, 64, st_));
+  k::zero_dev(st_, e->status.p, 64);
   // side-stream reporting work of the previous call must finish before its
   // buffers (selection slots) are reused
   if (e->side_join) RK_CUDA(cudaStreamWaitEvent(st_, e->side_join, 0));
@@ -37,6 +37,21 @@ int Runner::event() {
   }
   RK_CUDA(cudaEventRecord(e_->events[next_event_], st_));
   return next_event_++;
+}
+
+// Asynchronously uploaded caches: the compute stream waits (on the device)
+// for the pieces it is about to read.
+void Runner::wait_cache_meta(rk_cache* c) {
+  if (c->async) RK_CUDA(cudaStreamWaitEvent(st_, c->ev_meta, 0));
+}
+void Runner::wait_cache_layer(rk_cache* c, uint64_t l) {
+  if (c->async) RK_CUDA(cudaStreamWaitEvent(st_, c->ev_layer[l], 0));
+}
+void Runner::wait_cache_all(rk_cache* c) {
+  if (c->async) {
+    RK_CUDA(cudaStreamWaitEvent(st_, c->ev_meta, 0));
+    RK_CUDA(cudaStreamWaitEvent(st_, c->ev_layer.back(), 0));
+  }
 }
 
 ExtendSlot& Runner::slot(int i) {
@@ -93,7 +108,13 @@ int* Runner::upload_tokens(const int32_t* tokens, uint64_t n, int off) {
   int32_t* pin = static_cast<int32_t*>(e_->pinned) + off;
   std::memcpy(pin, tokens, n * 4);
   int* dev = S.tokens.as<int>() + off;
-  RK_CUDA(cudaMemcpyAsync(dev, pin, n * 4, cudaMemcpyHostToDevice, st_));
+  // a kernel reads the (mapped) pinned tokens over PCIe instead of a copy:
+  // the copy engine may be busy streaming relay caches (rk_cache_upload_async)
+  // and a memcpy would queue behind them
+  int32_t* mapped = nullptr;
+  RK_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&mapped), pin, 0));
+  k::copy_i32(st_, dev, mapped, (int)n);
+  e_->launches += 1;
   return dev;
 }
 
@@ -160,7 +181,7 @@ void Runner::row_logits_from_layer(rk_context* ctx, const float* hidden_row, uin
   Scratch& S = *e_->scratch;
   const rk_model_spec& s = w_->s;
   float* row = S.seg_hidden_out.as<float>();
-  RK_CUDA(cudaMemcpyAsync(row, hidden_row, s.d_model * 4, cudaMemcpyDeviceToDevice, st_));
+  k::copy_dev(st_, row, hidden_row, s.d_model * 4);
   k::iota_positions(st_, S.sub_positions.as<int>(), 1, (int)position);
   e_->launches += 1;
   Rows one{1, nullptr, S.sub_positions.as<int>()};
@@ -252,6 +273,7 @@ ExtendResult Runner::relay_extend(rk_context* ctx, rk_cache* cache, const rk_lay
   const rk_model_spec& s = w_->s;
   require(ctx != nullptr && ctx->w == w_, RK_ERR_INVALID_ARGUMENT, "context belongs to other weights");
   const ExtendPlan plan = plan_extend(ctx->size, cache, prof, opts);
+  wait_cache_all(cache);
   const uint64_t n = cache->n, base = ctx->size, L = s.num_layers;
   const int mode = opts.mode;
   const uint64_t l_start = plan.l_start, l_det = plan.l_det, sparse_hi = plan.sparse_hi;
@@ -278,16 +300,16 @@ ExtendResult Runner::relay_extend(rk_context* ctx, rk_cache* cache, const rk_lay
   X.dinfo.ensure(64);
   X.sub_pos.ensure(n * 4);
   X.score.ensure(n * 8);
-  RK_CUDA(cudaMemsetAsync(X.info.p, 0, 64, st_));
-  RK_CUDA(cudaMemsetAsync(X.dinfo.p, 0, 64, st_));
+  k::zero_dev(st_, X.info.p, 64);
+  k::zero_dev(st_, X.dinfo.p, 64);
   ensure_rows(n);
   Scratch& S = *e_->scratch;
 
   rk_segment_marks marks;
   marks.base = base;
   marks.len = n;
-  marks.origin.alloc(L * n);
-  RK_CUDA(cudaMemsetAsync(marks.origin.p, 0, L * n, st_));
+  marks.origin.alloc_pooled(&e_->cache_pool, L * n);  // pooled: freeing would sync the device
+  k::zero_dev(st_, marks.origin.p, L * n);
   uint8_t* origin = marks.origin.as<uint8_t>();
   float* hidden = X.hidden.as<float>();
   uint64_t* depth = X.depth.as<uint64_t>();
@@ -333,7 +355,7 @@ ExtendResult Runner::relay_extend(rk_context* ctx, rk_cache* cache, const rk_lay
       break;
     }
     case RK_MODE_ZERO: {  // relay_engine.cpp:224-234
-      RK_CUDA(cudaMemcpyAsync(hidden, cache->hidden.p, n * d * 4, cudaMemcpyDeviceToDevice, st_));
+      k::copy_dev(st_, hidden, cache->hidden.p, n * d * 4);
       k::set_depth(st_, depth, (int)n, cache->snapshot);
       e_->launches += 1;
       r.ev_band = r.ev_select = r.ev_end = event();
@@ -341,7 +363,7 @@ ExtendResult Runner::relay_extend(rk_context* ctx, rk_cache* cache, const rk_lay
     }
     default: {  // RELAY (236-293) and BLEND (295-344)
       if (mode == RK_MODE_RELAY) {
-        RK_CUDA(cudaMemcpyAsync(hidden, cache->hidden.p, n * d * 4, cudaMemcpyDeviceToDevice, st_));
+        k::copy_dev(st_, hidden, cache->hidden.p, n * d * 4);
       } else {
         k::embed(st_, hidden, w_->emb, w_->elem, cache->tokens.as<int>(), (int)n, (int)d, 0, nullptr);
         e_->launches += 1;
@@ -586,28 +608,52 @@ void Runner::agent_fused(rk_context* ctx, const int32_t* prefix, uint64_t P, rk_
     X.info.ensure(64);
     X.dinfo.ensure(64);
     X.score.ensure(n[u] * 8);
-    RK_CUDA(cudaMemsetAsync(X.info.p, 0, 64, st_));
-    RK_CUDA(cudaMemsetAsync(X.dinfo.p, 0, 64, st_));
+    k::zero_dev(st_, X.info.p, 64);
+    k::zero_dev(st_, X.dinfo.p, 64);
     marks[u].base = base[u];
     marks[u].len = n[u];
-    marks[u].origin.alloc(L * n[u]);
-    RK_CUDA(cudaMemsetAsync(marks[u].origin.p, 0, L * n[u], st_));
+    marks[u].origin.alloc_pooled(&e_->cache_pool, L * n[u]);  // pooled: freeing would sync the device
+    k::zero_dev(st_, marks[u].origin.p, L * n[u]);
     results.push_back(r);
   }
   const int ev_begin = event();
-  ctx->resize(total);
+  // every cell is written before it is read: prefix / suffix rows by each
+  // layer's QKV pass, segment rows by the graft (reused layers) or the band
+  // recompute -- no zero fill needed
+  ctx->resize(total, /*zero_fill=*/false);
   const size_t layer_stride = ctx->cap * w_->kv();
   const double2* rope = w_->rope->cs.as<double2>();
-  for (uint64_t u = 0; u < U; ++u) {  // realign + graft (band layers skipped)
-    rk_cache* c = ups[u];
-    int skip_lo = 1, skip_hi = 0;
-    if (mode == RK_MODE_RELAY) { skip_lo = (int)l_start; skip_hi = (int)l_det; }
-    if (mode == RK_MODE_BLEND) { skip_lo = 0; skip_hi = 1; }
-    const int grafted = (int)L - (skip_hi >= skip_lo ? skip_hi - skip_lo + 1 : 0);
-    ProfScope ps(e_, "realign_graft", 3.0 * w_->kv() * n[u] * grafted, 4.0 * grafted * n[u] * w_->kv() * w_->elem);
-    k::realign_graft(st_, c->k_pre.p, c->v.p, w_->elem, (int)L, (int)n[u], (int)w_->kv(), (int)s.d_head, rope,
-                     (int)base[u], ctx->k.p, ctx->v.p, layer_stride, skip_lo, skip_hi);
-    e_->launches += 1;
+  int skip_lo = 1, skip_hi = 0;  // band layers are recomputed, never grafted
+  if (mode == RK_MODE_RELAY) { skip_lo = (int)l_start; skip_hi = (int)l_det; }
+  if (mode == RK_MODE_BLEND) { skip_lo = 0; skip_hi = 1; }
+  bool streamed = false;  // some cache still arriving: graft layer by layer as the pass reaches it
+  for (uint64_t u = 0; u < U; ++u) {
+    streamed |= ups[u]->async;
+    wait_cache_meta(ups[u]);
+  }
+  const size_t el = w_->elem, kvd = w_->kv();
+  auto graft_layer = [&](uint64_t l) {  // realign + graft of layer l of every segment
+    if ((int)l >= skip_lo && (int)l <= skip_hi) return;
+    for (uint64_t u = 0; u < U; ++u) {
+      rk_cache* c = ups[u];
+      wait_cache_layer(c, l);
+      ProfScope ps(e_, "realign_graft", 3.0 * kvd * n[u], 4.0 * n[u] * kvd * el);
+      k::realign_graft(st_, static_cast<char*>(c->k_pre.p) + l * n[u] * kvd * el,
+                       static_cast<char*>(c->v.p) + l * n[u] * kvd * el, el, 1, (int)n[u], (int)kvd, (int)s.d_head,
+                       rope, (int)base[u], static_cast<char*>(ctx->k.p) + l * layer_stride * el,
+                       static_cast<char*>(ctx->v.p) + l * layer_stride * el, layer_stride, 1, 0);
+      e_->launches += 1;
+    }
+  };
+  if (!streamed) {
+    for (uint64_t u = 0; u < U; ++u) {  // one launch per segment over all grafted layers
+      rk_cache* c = ups[u];
+      const int grafted = (int)L - (skip_hi >= skip_lo ? skip_hi - skip_lo + 1 : 0);
+      ProfScope ps(e_, "realign_graft", 3.0 * kvd * n[u] * grafted, 4.0 * grafted * n[u] * kvd * el);
+      k::realign_graft(st_, c->k_pre.p, c->v.p, el, (int)L, (int)n[u], (int)kvd, (int)s.d_head, rope,
+                       (int)base[u], ctx->k.p, ctx->v.p, layer_stride, skip_lo, skip_hi);
+      e_->launches += 1;
+    }
   }
   const int ev_realign = event();
   // pass inputs: prefix / suffix embeddings, segment snapshots (or embeddings for BLEND)
@@ -623,7 +669,7 @@ void Runner::agent_fused(rk_context* ctx, const int32_t* prefix, uint64_t P, rk_
     for (uint64_t u = 0; u < U; ++u) {
       float* dst = H + (head + base[u] - P) * d;
       if (mode == RK_MODE_RELAY)
-        RK_CUDA(cudaMemcpyAsync(dst, ups[u]->hidden.p, n[u] * d * 4, cudaMemcpyDeviceToDevice, st_));
+        k::copy_dev(st_, dst, ups[u]->hidden.p, n[u] * d * 4);
       else
         k::embed(st_, dst, w_->emb, w_->elem, ups[u]->tokens.as<int>(), (int)n[u], (int)d, 0, nullptr);
       k::iota_positions(st_, pos + head + (base[u] - P), (int)n[u], (int)base[u]);
@@ -640,16 +686,18 @@ void Runner::agent_fused(rk_context* ctx, const int32_t* prefix, uint64_t P, rk_
     // the row set grows at l = 0, at the band start and after the selected
     // rows are gathered (it only shrinks, to the head rows, after sparse_hi)
     if (l == 0 || (segs && (l == l_start || l == l_det + 1))) prepared_ = false;
+    if (streamed) graft_layer(l);
     run_layer(ctx, (int)l, H, rows, true, (int)total);
     if (segs && l == l_det) {
       ev_band = event();
       for (uint64_t u = 0; u < U; ++u) {
         ExtendSlot& X = slot(results[u].slot);
         rk_cache* c = ups[u];
-        RK_CUDA(cudaMemcpyAsync(X.hidden.p, H + (head + base[u] - P) * d, n[u] * d * 4, cudaMemcpyDeviceToDevice, st_));
+        k::copy_dev(st_, X.hidden.p, H + (head + base[u] - P) * d, n[u] * d * 4);
         k::set_depth(st_, X.depth.as<uint64_t>(), (int)n[u], l_det + 1);
         k::mark_layers(st_, marks[u].origin.as<uint8_t>(), (int)n[u], (int)l_start, (int)l_det);
-        const size_t el = w_->elem, kv = w_->kv();
+        const size_t kv = w_->kv();
+        wait_cache_layer(c, l_det);
         const char* ctx_v_det = static_cast<const char*>(ctx->v_layer(l_det)) + base[u] * kv * el;
         const char* cache_v_det = static_cast<const char*>(c->v.p) + l_det * n[u] * kv * el;
         if (mode == RK_MODE_RELAY) {
@@ -708,7 +756,7 @@ void Runner::agent_fused(rk_context* ctx, const int32_t* prefix, uint64_t P, rk_
   if (!segs) {  // ZERO (relay_engine.cpp:224-234): the segment keeps its snapshot
     for (uint64_t u = 0; u < U; ++u) {
       ExtendSlot& X = slot(results[u].slot);
-      RK_CUDA(cudaMemcpyAsync(X.hidden.p, ups[u]->hidden.p, n[u] * d * 4, cudaMemcpyDeviceToDevice, st_));
+      k::copy_dev(st_, X.hidden.p, ups[u]->hidden.p, n[u] * d * 4);
       k::set_depth(st_, X.depth.as<uint64_t>(), (int)n[u], ups[u]->snapshot);
       e_->launches += 1;
     }
@@ -777,7 +825,7 @@ rk_cache* Runner::capture_prefill(rk_context* ctx, const int32_t* tokens, uint64
   ensure_rows(chunk);
   Scratch& S = *e_->scratch;
   DevBuf acc(n * 8), probs(chunk * H * n * 4);
-  RK_CUDA(cudaMemsetAsync(acc.p, 0, n * 8, st_));
+  k::zero_dev(st_, acc.p, n * 8);
   ctx->resize(src + n);
   for (uint64_t c0 = 0; c0 < n; c0 += chunk) {
     const uint64_t m = std::min(chunk, n - c0);
@@ -788,7 +836,7 @@ rk_cache* Runner::capture_prefill(rk_context* ctx, const int32_t* tokens, uint64
     prepared_ = false;
     for (uint64_t l = 0; l < s.num_layers; ++l) {
       if (l == snapshot)
-        RK_CUDA(cudaMemcpyAsync(c->hidden.as<float>() + c0 * d, S.hidden.p, m * d * 4, cudaMemcpyDeviceToDevice, st_));
+        k::copy_dev(st_, c->hidden.as<float>() + c0 * d, S.hidden.p, m * d * 4);
       cap_k_ = static_cast<float*>(static_cast<void*>(static_cast<char*>(c->k_pre.p) + (l * n + c0) * kv * c->elem));
       cap_v_ = static_cast<float*>(static_cast<void*>(static_cast<char*>(c->v.p) + (l * n + c0) * kv * c->elem));
       run_layer(ctx, (int)l, S.hidden.as<float>(), rows, true, (int)(src + c0 + m), probs.as<float>(), (int)src, (int)n);
@@ -817,7 +865,7 @@ rk_cache* Runner::capture_decode(rk_context* ctx, const float* first_logits, uin
   const size_t d = s.d_model, kv = w_->kv(), H = s.num_heads, V = s.vocab_size;
   if (first_logits) RK_CUDA(cudaMemcpyAsync(S.logits.p, first_logits, V * 4, cudaMemcpyHostToDevice, st_));
   DevBuf acc(n * 8), probs(H * n * 4);
-  RK_CUDA(cudaMemsetAsync(acc.p, 0, n * 8, st_));
+  k::zero_dev(st_, acc.p, n * 8);
   int* tok = c->tokens.as<int>();
   // greedy_generate (model.cpp:372-389): next = argmax(prompt-end logits)
   k::argmax(st_, S.logits.as<float>(), (int)V, tok, S.argmax.as<char>() + 64);
@@ -832,7 +880,7 @@ rk_cache* Runner::capture_decode(rk_context* ctx, const float* first_logits, uin
     prepared_ = false;
     for (uint64_t l = 0; l < s.num_layers; ++l) {
       if (l == snapshot)
-        RK_CUDA(cudaMemcpyAsync(c->hidden.as<float>() + t * d, S.hidden.p, d * 4, cudaMemcpyDeviceToDevice, st_));
+        k::copy_dev(st_, c->hidden.as<float>() + t * d, S.hidden.p, d * 4);
       cap_k_ = static_cast<float*>(static_cast<void*>(static_cast<char*>(c->k_pre.p) + (l * n + t) * kv * c->elem));
       cap_v_ = static_cast<float*>(static_cast<void*>(static_cast<char*>(c->v.p) + (l * n + t) * kv * c->elem));
       run_layer(ctx, (int)l, S.hidden.as<float>(), rows, true, (int)(pos + 1), probs.as<float>(), (int)src, (int)n);

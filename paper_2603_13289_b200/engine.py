@@ -164,11 +164,17 @@ class Weights(_Obj):
         _check(lib().rk_context_create(P(self.engine.ptr), P(self.ptr), C.byref(out)))
         return Context(out.value, self)
 
-    def upload_cache(self, host):
-        """RelayCache host arrays -> device (rk_cache_upload)."""
+    def upload_cache(self, host, asynchronous=False):
+        """RelayCache host arrays -> device (rk_cache_upload). asynchronous:
+        rk_cache_upload_async -- layers stream in on the copy stream while
+        later calls run; the host arrays stay referenced by the Cache."""
         out = P()
-        _check(lib().rk_cache_upload(P(self.engine.ptr), P(self.ptr), C.byref(host.view()), C.byref(out)))
-        return Cache(out.value, self)
+        fn = lib().rk_cache_upload_async if asynchronous else lib().rk_cache_upload
+        _check(fn(P(self.engine.ptr), P(self.ptr), C.byref(host.view()), C.byref(out)))
+        c = Cache(out.value, self)
+        if asynchronous:
+            c._host = host
+        return c
 
 
 class Cache(_Obj):
@@ -181,6 +187,10 @@ class Cache(_Obj):
     @property
     def segment_len(self):
         return int(lib().rk_cache_segment_len(P(self.ptr)))
+
+    def wait(self):
+        """Block until an asynchronous upload has landed (rk_cache_wait)."""
+        _check(lib().rk_cache_wait(P(self.ptr)))
 
     def to_host(self):
         s = self.weights.spec

@@ -179,3 +179,22 @@ def test_validation_errors(engine, oracle):
     with pytest.raises(InvalidArgument):
         w2.context().relay_prefill(pattern_tokens(8, 64, 2), w2.upload_cache(c2), LayerProfile(),
                                    RelayOptions.make(mode="zero"))
+
+
+@pytest.mark.parametrize("mode", ["relay", "zero", "blend"])
+def test_async_upload_bit_exact(engine, oracle, mode):
+    """rk_cache_upload_async (layers streamed on the copy stream, grafted layer
+    by layer) gives the same bits as the synchronous upload."""
+    spec = spec_of(6, 64, 4, kv_heads=2)
+    ow = oracle.weights(spec, 31)
+    c1 = oracle.scenario(ow, pattern_tokens(9, 64, 1), 16, 1)
+    c2 = oracle.scenario(ow, pattern_tokens(7, 64, 2), 11, 1)
+    prof = triple(1, 2, 4) if mode == "relay" else LayerProfile()
+    opts = RelayOptions.make(mode=mode, suffix_k=3, blend_alpha=0.5)
+    res = []
+    for asynchronous in (False, True):
+        w = engine.weights(spec, 31)
+        ups = [w.upload_cache(c, asynchronous=asynchronous) for c in (c1, c2)]
+        out = w.context().agent_prefill(pattern_tokens(5, 64, 3), ups, pattern_tokens(4, 64, 4), prof, opts)
+        res.append(out["logits"])
+    assert_bit_equal(res[1], res[0], f"async.{mode}.logits")
