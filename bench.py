@@ -305,8 +305,11 @@ def run_ours(args, world, rank, local, dist):
                                          want_logits=False, outputs=want_outputs)
 
     def step(o=opts):
+        import torch
+        torch.cuda.nvtx.range_push("relay_step")  # ncu --nvtx --nvtx-include relay_step/
         for sess in mine:
             run_session(sess, o)
+        torch.cuda.nvtx.range_pop()
 
     def timed(fn, K, W):
         for _ in range(W):

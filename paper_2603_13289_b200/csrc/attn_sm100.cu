@@ -562,7 +562,11 @@ void attention_bf16(rk_engine* e, const AttnArgs& a_in, const __nv_bfloat16* ctx
   a.splits = 1;
   a.tiles_per_split = nk_max > 0 ? nk_max : 1;
   // split the key range only while the grid is well under 1.5 waves; each
-  // split keeps >= 4 key tiles (a CTA's fixed cost is a few microseconds)
+  // split keeps >= 4 key tiles (a CTA's fixed cost is a few microseconds).
+  // (Measured: splitting the c2 sparse layers 2-way to shorten the longest
+  // CTA is slower -- the partial writes and the combine cost more. Also
+  // measured and dropped: a column-split softmax with two warpgroups per tile
+  // and 50% polynomial exp2 -- both slower than this layout.)
   const int want = (3 * slots / 2) / std::max(1, base);
   if (want >= 2 && nk_max >= 8) {
     const int splits = std::min(want, nk_max / 4);

@@ -7,7 +7,7 @@ import numpy as np
 sys.path.insert(0, ".")
 from paper_2603_13289_b200.engine import Engine, P, _check, lib  # noqa: E402
 
-EV_SM = ["start", "s_full", "s_free", "max", "P", "p_full", "-", "-"]
+EV_SM = ["start", "s_full", "s_free", "max", "P stored", "p_full", "exp done", "o_done"]
 EV_MMA = ["-", "S issue", "-", "-", "PV issue", "-", "-", "-"]
 
 if __name__ == "__main__":
