@@ -23,6 +23,8 @@
 //   EPI_F32   plain fp32 store (logits)
 #include <cuda.h>
 
+#include <algorithm>
+
 #include "internal.h"
 #include "layer_bf16.h"
 #include "prof.h"
@@ -349,10 +351,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 // Split-K reduction + residual epilogue (EPI_PART partials): one CTA per row,
 // h[row] += sum_s part[s][row] in split order (deterministic); with the fused
 // RMSNorm the bf16 row copy and 1/rms come out of the same pass.
-__global__ void __launch_bounds__(256) splitk_reduce_add_kernel(const GemmArgs p, int splits) {
-  const int M = p.rows_dev ? *p.rows_dev : p.rows_max;
-  const int row = blockIdx.x;
-  if (row >= M) return;
+// one row of splitk_reduce_add_kernel
+__device__ __forceinline__ void splitk_reduce_row(const GemmArgs& p, int splits, int row) {
   const int n4 = p.N / 4;
   float ss = 0.f;
   float4* h = reinterpret_cast<float4*>(p.out_f32 + (size_t)row * p.ld_out);
@@ -380,7 +380,14 @@ __global__ void __launch_bounds__(256) splitk_reduce_add_kernel(const GemmArgs p
       for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
       p.norm_inv[row] = rsqrtf(t / (float)p.N + p.norm_eps);
     }
+    __syncthreads();  // red[] is reused by the CTA's next row
   }
+}
+
+__global__ void __launch_bounds__(256) splitk_reduce_add_kernel(const GemmArgs p, int splits) {
+  const int M = p.rows_dev ? *p.rows_dev : p.rows_max;
+  for (int row = blockIdx.x; row < M; row += gridDim.x)
+    splitk_reduce_row(p, splits, row);
 }
 
 template <int BN, int EPI>
@@ -511,7 +518,7 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
     case EPI_SILU: launch_bn<EPI_SILU>(e->stream, ta, tb, p, grid); break;
     case EPI_PART:
       launch_bn<EPI_PART>(e->stream, ta, tb, p, grid);
-      splitk_reduce_add_kernel<<<p.rows_max, 256, 0, e->stream>>>(p, p.splits);
+      splitk_reduce_add_kernel<<<std::min(p.rows_max, 8 * e->sm_count), 256, 0, e->stream>>>(p, p.splits);
       e->launches += 1;
       break;
     default: launch_bn<EPI_F32>(e->stream, ta, tb, p, grid); break;
