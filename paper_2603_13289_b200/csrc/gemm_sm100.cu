@@ -46,7 +46,9 @@ struct Cfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (BN == 256) ? 4 : (BN == 128 ? 6 : 8);
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  // per epilogue warp: a 32x32 fp32 staging tile for the coalesced residual epilogue
+  static constexpr int EPI_STAGE = 4 * 32 * 32 * 4;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + EPI_STAGE;
 };
 
 struct Units {
@@ -167,6 +169,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint8_t* epi_stage = smem + C::STAGES * C::STAGE_BYTES + 256;  // [4 warps][32 rows][128 B]
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const Units U = units_of(p);
@@ -256,55 +259,75 @@ __global__ void __launch_bounds__(kThreads, 1)
         __threadfence();
       }
       if constexpr (EPI == EPI_ADD) {
-        // residual rows are read through a 4-chunk register ring issued before
-        // the accumulator is even ready, so the load latency overlaps the MMAs
-        constexpr int NCH = BN / 32, D = NCH < 4 ? NCH : 4;
-        const bool live = row < M;
+        // Coalesced residual epilogue: each 32x32 accumulator chunk (thread =
+        // row) goes through a swizzled smem tile so that 8 lanes cover one
+        // row's 128 contiguous bytes -- every load/store instruction touches 4
+        // full lines instead of 32 partial ones. The residual of the next chunk
+        // is prefetched while the current one is written.
         const bool norm = p.norm_part != nullptr && s + 1 == U.splits;  // final values: fused RMSNorm stats
-        float ss = 0.f;
-        float4* hrow = reinterpret_cast<float4*>(p.out_f32 + (size_t)(live ? row : 0) * p.ld_out + nt * BN);
-        float4 hb[D][8];
+        uint8_t* T = epi_stage + quarter * 4096;
+        const int sub = lane >> 3, ch = lane & 7;  // row-within-4 and 16-byte chunk of the read-back layout
+        const int row0 = mt * kBM + quarter * 32;
+        auto hptr = [&](int i, int c) {  // residual of local row 4i+sub, columns c + 4*ch ..
+          const int rr = row0 + 4 * i + sub;
+          return reinterpret_cast<float4*>(p.out_f32 + (size_t)(rr < M ? rr : 0) * p.ld_out + nt * BN + c) + ch;
+        };
+        float4 hb[8];
 #pragma unroll
-        for (int c = 0; c < D; ++c)
-#pragma unroll
-          for (int j = 0; j < 8; ++j) hb[c][j] = live ? __ldcg(hrow + c * 8 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int i = 0; i < 8; ++i) hb[i] = (row0 + 4 * i + sub < M) ? __ldcg(hptr(i, 0)) : make_float4(0.f, 0.f, 0.f, 0.f);
         mbar_wait(&tfull[acc], (local >> 1) & 1);
         tc_fence_after();
+        float ss[8];
 #pragma unroll
-        for (int c = 0; c < NCH; ++c) {
+        for (int i = 0; i < 8; ++i) ss[i] = 0.f;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
           uint32_t r[32];
-          tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN + c * 32, r);
+          tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN + c, r);
           tmem_ld_wait();
+          __syncwarp();  // previous chunk's read-back of T is done
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<uint4*>(T + lane * 128 + ((j ^ (lane & 7)) * 16)) =
+                make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
+          __syncwarp();
           float4 cur[8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) cur[j] = hb[c % D][j];
-          if (c + D < NCH && live) {
+          for (int i = 0; i < 8; ++i) cur[i] = hb[i];
+          if (c + 32 < BN) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) hb[c % D][j] = __ldcg(hrow + (c + D) * 8 + j);
+            for (int i = 0; i < 8; ++i)
+              hb[i] = (row0 + 4 * i + sub < M) ? __ldcg(hptr(i, c + 32)) : make_float4(0.f, 0.f, 0.f, 0.f);
           }
-          if (live) {
-            uint32_t hb16[16];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              float4 h = cur[j];
-              h.x += __uint_as_float(r[4 * j]);
-              h.y += __uint_as_float(r[4 * j + 1]);
-              h.z += __uint_as_float(r[4 * j + 2]);
-              h.w += __uint_as_float(r[4 * j + 3]);
-              hrow[c * 8 + j] = h;
-              ss = fmaf(h.x, h.x, fmaf(h.y, h.y, fmaf(h.z, h.z, fmaf(h.w, h.w, ss))));
-              hb16[2 * j] = pack_bf16(h.x, h.y);
-              hb16[2 * j + 1] = pack_bf16(h.z, h.w);
-            }
-            if (norm) {
-              uint4* d16 = reinterpret_cast<uint4*>(p.norm_bf16 + (size_t)row * p.N + nt * BN + c * 32);
-#pragma unroll
-              for (int j = 0; j < 4; ++j) d16[j] = make_uint4(hb16[4 * j], hb16[4 * j + 1], hb16[4 * j + 2], hb16[4 * j + 3]);
+          for (int i = 0; i < 8; ++i) {
+            const int rl = 4 * i + sub, rr = row0 + rl;
+            const uint4 a4 = *reinterpret_cast<const uint4*>(T + rl * 128 + ((ch ^ (rl & 7)) * 16));
+            float4 h = cur[i];
+            h.x += __uint_as_float(a4.x);
+            h.y += __uint_as_float(a4.y);
+            h.z += __uint_as_float(a4.z);
+            h.w += __uint_as_float(a4.w);
+            if (rr < M) {
+              *hptr(i, c) = h;
+              if (norm) {
+                ss[i] = fmaf(h.x, h.x, fmaf(h.y, h.y, fmaf(h.z, h.z, fmaf(h.w, h.w, ss[i]))));
+                *reinterpret_cast<uint2*>(p.norm_bf16 + (size_t)rr * p.N + nt * BN + c + 4 * ch) =
+                    make_uint2(pack_bf16(h.x, h.y), pack_bf16(h.z, h.w));
+              }
             }
           }
         }
         if (norm) {
-          if (live) p.norm_part[(size_t)row * kNormSlots + nt] = ss;
+          // row sums over the 8 lanes of each row group; lane ch==0 owns rows 4i+sub
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            ss[i] += __shfl_xor_sync(0xffffffffu, ss[i], 1);
+            ss[i] += __shfl_xor_sync(0xffffffffu, ss[i], 2);
+            ss[i] += __shfl_xor_sync(0xffffffffu, ss[i], 4);
+            const int rr = row0 + 4 * i + sub;
+            if (ch == 0 && rr < M) p.norm_part[(size_t)rr * kNormSlots + nt] = ss[i];
+          }
           // the last of the num_n tiles of these 32 rows turns partials into 1/rms
           __threadfence();
           __syncwarp();
@@ -313,7 +336,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           done = __shfl_sync(0xffffffffu, done, 0);
           if (done == U.num_n) {
             __threadfence();
-            if (live) {
+            if (row < M) {
               float tot = 0.f;
               for (int t = 0; t < U.num_n; ++t) tot += __ldcg(p.norm_part + (size_t)row * kNormSlots + t);
               p.norm_inv[row] = rsqrtf(tot / (float)p.N + p.norm_eps);
