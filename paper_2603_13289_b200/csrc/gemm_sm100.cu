@@ -24,6 +24,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "internal.h"
 #include "layer_bf16.h"
@@ -78,6 +79,42 @@ __device__ __forceinline__ void decode_unit(const Units& u, int unit, int& mt, i
   nt = tile / u.num_m;
 }
 
+// One accumulator's worth of work: tile (mt, nt), k-blocks [kb0, kb1); s is
+// the split index (split-K) or the CTA-local slot (stream-K).
+struct Work {
+  int mt, nt, s, kb0, kb1;
+};
+
+// Stream-K: the tile-major k-block space (tile t = mt + nt*num_m) is cut into
+// gridDim.x equal contiguous ranges; CTA g takes range g, touching at most
+// kSkSlots tiles (the host uses it only with at most 2 tiles per CTA, counting
+// the largest live row count).
+constexpr int kSkSlots = 4;
+__device__ __forceinline__ long long sk_lo(const Units& u, int g, int G) {
+  return (long long)u.num_m * u.num_n * u.kb_total * g / G;
+}
+
+// k-th work item of this CTA; false when the CTA is done.
+__device__ __forceinline__ bool get_work(const Units& U, bool streamk, int k, Work& w) {
+  if (!streamk) {
+    const int unit = blockIdx.x + k * gridDim.x;
+    if (unit >= U.total) return false;
+    decode_unit(U, unit, w.mt, w.nt, w.s);
+    w.kb0 = w.s * U.kb_per;
+    w.kb1 = min(U.kb_total, w.kb0 + U.kb_per);
+    return true;
+  }
+  const long long lo = sk_lo(U, blockIdx.x, gridDim.x), hi = sk_lo(U, blockIdx.x + 1, gridDim.x);
+  const long long t = lo / U.kb_total + k, tlo = t * U.kb_total;
+  if (tlo >= hi || lo >= hi) return false;
+  w.kb0 = (int)((lo > tlo ? lo : tlo) - tlo);
+  w.kb1 = (int)((hi < tlo + U.kb_total ? hi : tlo + U.kb_total) - tlo);
+  w.mt = (int)(t % U.num_m);
+  w.nt = (int)(t / U.num_m);
+  w.s = k;
+  return true;
+}
+
 template <int EPI>
 __device__ __forceinline__ void epilogue_chunk(const GemmArgs& p, int row, int col, const uint32_t (&r)[32],
                                                float rs, int split = 0) {
@@ -85,8 +122,9 @@ __device__ __forceinline__ void epilogue_chunk(const GemmArgs& p, int row, int c
 #pragma unroll
   for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * rs;
   if constexpr (EPI == EPI_F32 || EPI == EPI_PART) {
-    float* base = EPI == EPI_PART ? p.ws_part + ((size_t)split * p.rows_max + row) * p.N + col
-                                  : p.out_f32 + (size_t)row * p.ld_out + col;
+    float* base = EPI != EPI_PART ? p.out_f32 + (size_t)row * p.ld_out + col
+                  : p.streamk ? p.ws_part + (((size_t)blockIdx.x * kSkSlots + split) * kBM + row % kBM) * p.bn + col % p.bn
+                              : p.ws_part + ((size_t)split * p.rows_max + row) * p.N + col;
     float4* dst = reinterpret_cast<float4*>(base);
 #pragma unroll
     for (int j = 0; j < 8; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
@@ -197,10 +235,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (elect_one()) {  // ---------------- TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      for (int unit = blockIdx.x; unit < U.total; unit += gridDim.x) {
-        int mt, nt, s;
-        decode_unit(U, unit, mt, nt, s);
-        const int kb0 = s * U.kb_per, kb1 = min(U.kb_total, kb0 + U.kb_per);
+      Work w;
+      for (int it = 0; get_work(U, p.streamk, it, w); ++it) {
+        const int mt = w.mt, nt = w.nt, kb0 = w.kb0, kb1 = w.kb1;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
@@ -217,10 +254,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      for (int unit = blockIdx.x; unit < U.total; unit += gridDim.x, ++local) {
-        int mt, nt, s;
-        decode_unit(U, unit, mt, nt, s);
-        const int kb0 = s * U.kb_per, kb1 = min(U.kb_total, kb0 + U.kb_per);
+      Work w;
+      for (int it = 0; get_work(U, p.streamk, it, w); ++it, ++local) {
+        const int kb0 = w.kb0, kb1 = w.kb1;
         const int acc = local & 1;
         mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -245,9 +281,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int quarter = warp & 3;
     const int M = p.rows_dev ? *p.rows_dev : p.rows_max;
     int local = 0;
-    for (int unit = blockIdx.x; unit < U.total; unit += gridDim.x, ++local) {
-      int mt, nt, s;
-      decode_unit(U, unit, mt, nt, s);
+    Work w;
+    for (int it = 0; get_work(U, p.streamk, it, w); ++it, ++local) {
+      const int mt = w.mt, nt = w.nt, s = w.s;
       const int acc = local & 1;
       const int row = mt * kBM + quarter * 32 + lane;
       int* flag = nullptr;
@@ -375,15 +411,36 @@ __global__ void __launch_bounds__(kThreads, 1)
 // h[row] += sum_s part[s][row] in split order (deterministic); with the fused
 // RMSNorm the bf16 row copy and 1/rms come out of the same pass.
 // one row of splitk_reduce_add_kernel
-__device__ __forceinline__ void splitk_reduce_row(const GemmArgs& p, int splits, int row) {
+__device__ __forceinline__ void splitk_reduce_row(const GemmArgs& p, int splits, int row, const Units& U,
+                                                  int G, const int* sk_tab) {
   const int n4 = p.N / 4;
   float ss = 0.f;
   float4* h = reinterpret_cast<float4*>(p.out_f32 + (size_t)row * p.ld_out);
   for (int c = threadIdx.x; c < n4; c += blockDim.x) {
-    float4 acc = __ldcg(reinterpret_cast<const float4*>(p.ws_part + (size_t)row * p.N) + c);
-    for (int s = 1; s < splits; ++s) {
-      const float4 v = __ldcg(reinterpret_cast<const float4*>(p.ws_part + ((size_t)s * p.rows_max + row) * p.N) + c);
-      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    float4 acc;
+    if (p.streamk) {  // partials of the CTAs whose k-block ranges cover this tile, in CTA order
+      const int mt = row / kBM, nt = (4 * c) / p.bn;
+      const int t = mt + nt * U.num_m, tlo = t * U.kb_total, thi = tlo + U.kb_total;
+      int lo = 0, hi = G - 1;  // last CTA whose range starts at or before tlo (binary search)
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) / 2;
+        if (sk_tab[mid] <= tlo) lo = mid;
+        else hi = mid - 1;
+      }
+      acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int g = lo; g < G && sk_tab[g] < thi; ++g) {
+        if (sk_tab[g + 1] == sk_tab[g]) continue;  // empty range: no partial
+        const int slot = t - sk_tab[g] / U.kb_total;
+        const float4 v = __ldcg(reinterpret_cast<const float4*>(
+            p.ws_part + (((size_t)g * kSkSlots + slot) * kBM + row % kBM) * p.bn + (4 * c) % p.bn));
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      }
+    } else {
+      acc = __ldcg(reinterpret_cast<const float4*>(p.ws_part + (size_t)row * p.N) + c);
+      for (int s = 1; s < splits; ++s) {
+        const float4 v = __ldcg(reinterpret_cast<const float4*>(p.ws_part + ((size_t)s * p.rows_max + row) * p.N) + c);
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      }
     }
     float4 x = h[c];
     x.x += acc.x; x.y += acc.y; x.z += acc.z; x.w += acc.w;
@@ -407,10 +464,16 @@ __device__ __forceinline__ void splitk_reduce_row(const GemmArgs& p, int splits,
   }
 }
 
-__global__ void __launch_bounds__(256) splitk_reduce_add_kernel(const GemmArgs p, int splits) {
+__global__ void __launch_bounds__(256) splitk_reduce_add_kernel(const GemmArgs p, int splits, int G) {
   const int M = p.rows_dev ? *p.rows_dev : p.rows_max;
+  const Units U = units_of(p);
+  __shared__ int sk_tab[1025];  // stream-K range starts of the G CTAs (+ end)
+  if (p.streamk) {
+    for (int g = threadIdx.x; g <= G; g += blockDim.x) sk_tab[g] = (int)sk_lo(U, g, G);
+    __syncthreads();
+  }
   for (int row = blockIdx.x; row < M; row += gridDim.x)
-    splitk_reduce_row(p, splits, row);
+    splitk_reduce_row(p, splits, row, U, G, sk_tab);
 }
 
 template <int BN, int EPI>
@@ -488,6 +551,19 @@ static void choose_config(GemmArgs& p, int sm_count, int rows_hint) {
     const int tiles = num_m * (p.N / wide), kb = p.K / kBK;
     if (4 * tiles < 3 * sm_count) {
       const double t_kb = 0.45 * wide / 256.0;
+      // stream-K: every SM gets the same k-block count; partials of the
+      // ~tiles + SMs segments go through L2 to the reduce kernel
+      // (measured on c2: slower than split-K at these shapes -- opt-in with
+      // RK_GEMM_STREAMK=1 for experiments)
+      static const bool sk_enabled = [] {
+        const char* v = std::getenv("RK_GEMM_STREAMK");
+        return v && std::atoi(v) != 0;
+      }();
+      const int tiles_max = ((p.rows_max + kBM - 1) / kBM) * (p.N / wide);
+      const bool sk_ok = sk_enabled && kb >= 2 && tiles_max <= 2 * sm_count;
+      const double sk_cost = sk_ok ? ((double)tiles * kb + sm_count - 1) / sm_count * t_kb + 1.0 +
+                                         2.0 * (tiles + sm_count) * (double)kBM * wide * 4 / 8e6
+                                   : 1e30;
       auto cost = [&](int s) {
         const int units = tiles * s, waves = (units + sm_count - 1) / sm_count;
         const double mma = waves * ((kb + s - 1) / s) * t_kb;
@@ -498,7 +574,12 @@ static void choose_config(GemmArgs& p, int sm_count, int rows_hint) {
       double best_cost = cost(1);
       for (int s = 2; s <= 8 && kb / s >= 4; ++s)
         if (cost(s) < best_cost) { best = s; best_cost = cost(s); }
-      if (best > 1) {
+      if (sk_cost < best_cost) {
+        p.bn = wide;
+        p.splits = 1;
+        p.streamk = 1;
+        p.epi = EPI_PART;
+      } else if (best > 1) {
         p.bn = wide;
         p.splits = best;
         p.epi = EPI_PART;
@@ -518,16 +599,17 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
   make_tmap_bf16(&tb, B, (uint64_t)p.N, (uint64_t)p.K, (uint32_t)p.bn, (uint64_t)p.K);
   const int num_m = (p.rows_max + kBM - 1) / kBM;
   const int total = num_m * (p.N / p.bn) * p.splits;
-  const int grid = total < e->sm_count ? total : e->sm_count;
+  const int grid = p.streamk ? e->sm_count : (total < e->sm_count ? total : e->sm_count);
   if (p.epi == EPI_PART) {
-    e->scratch->gemm_ws.ensure((size_t)p.splits * p.rows_max * p.N * 4);
+    e->scratch->gemm_ws.ensure(p.streamk ? (size_t)grid * kSkSlots * kBM * p.bn * 4
+                                         : (size_t)p.splits * p.rows_max * p.N * 4);
     p.ws_part = e->scratch->gemm_ws.as<float>();
   }
   static const char* kEpi[] = {"qkv", "add", "silu", "f32", "addsplit"};
   ProfScope ps(e, (e->prof && e->prof->on)
                       ? intern(std::string("gemm_") + kEpi[p.epi] + "_m" + std::to_string(p.rows_max) +
                                (p.rows_dev ? "dyn" : "") + "_n" + std::to_string(p.N) + "_k" + std::to_string(p.K) +
-                               "_bn" + std::to_string(p.bn) + "_s" + std::to_string(p.splits))
+                               "_bn" + std::to_string(p.bn) + (p.streamk ? std::string("_sk") : "_s" + std::to_string(p.splits)))
                       : "gemm",
                0, 0);
   ps.rec.kind = 1;
@@ -541,7 +623,7 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
     case EPI_SILU: launch_bn<EPI_SILU>(e->stream, ta, tb, p, grid); break;
     case EPI_PART:
       launch_bn<EPI_PART>(e->stream, ta, tb, p, grid);
-      splitk_reduce_add_kernel<<<std::min(p.rows_max, 8 * e->sm_count), 256, 0, e->stream>>>(p, p.splits);
+      splitk_reduce_add_kernel<<<std::min(p.rows_max, 8 * e->sm_count), 256, 0, e->stream>>>(p, p.splits, grid);
       e->launches += 1;
       break;
     default: launch_bn<EPI_F32>(e->stream, ta, tb, p, grid); break;

@@ -48,7 +48,8 @@ struct GemmArgs {
   float* norm_inv = nullptr;    // [rows_max]
   int* norm_cnt = nullptr;      // [m tiles * 4], zero-initialised, self-resetting
   float norm_eps = 1e-5f;
-  float* ws_part = nullptr;  // EPI_PART workspace [splits][rows_max][N]
+  float* ws_part = nullptr;  // EPI_PART workspace [splits][rows_max][N], or stream-K [grid*2][128][bn]
+  int streamk = 0;           // EPI_PART: stream-K work split (set by gemm_bf16)
 };
 constexpr int kNormSlots = 64;  // max N tiles of a residual GEMM (d_model / BN)
 

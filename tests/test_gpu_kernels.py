@@ -196,3 +196,34 @@ def test_select_certified_threshold(engine, case):
     assert np.array_equal(tags[:cnt.value], want_tags)
     if case != "zeros":
         assert dinfo[0] == thr, (dinfo[0], thr)
+
+
+@pytest.mark.parametrize("shape", [(40, 512, 4096), (320, 2048, 8192), (1356, 2048, 2048)])
+def test_gemm_residual_streamk(engine, shape):
+    """The opt-in stream-K residual path (RK_GEMM_STREAMK=1) in a subprocess:
+    deterministic and equal to the reference within bf16-operand tolerance."""
+    import os
+    import subprocess
+    import sys
+    code = f"""
+import numpy as np, sys
+sys.path.insert(0, {os.getcwd()!r})
+from paper_2603_13289_b200.engine import Engine
+from tests.test_gpu_kernels import run_gemm, bf16_round
+e = Engine(0)
+M, N, K = {shape}
+rng = np.random.default_rng(4)
+A = rng.standard_normal((M, K)).astype(np.float32)
+B = (rng.standard_normal((N, K)) / np.sqrt(K)).astype(np.float32)
+H = rng.standard_normal((M, N)).astype(np.float32)
+got = run_gemm(e, A, B, H, M, 1)
+again = run_gemm(e, A, B, H, M, 1)
+assert np.array_equal(got.view(np.uint32), again.view(np.uint32))
+ref = H + bf16_round(A).astype(np.float64) @ bf16_round(B).astype(np.float64).T
+err = np.abs(got - ref).max() / np.abs(ref).max()
+assert err < 2e-5, err
+print("ok")
+"""
+    env = dict(os.environ, RK_GEMM_STREAMK="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
