@@ -162,10 +162,11 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
   int* s_kmax = reinterpret_cast<int*>(bar + 14);
 
   const int M = a.rows_dev ? *a.rows_dev : a.rows_max;
-  // grid (head, tile, split) with heads fastest and tiles in reverse order:
-  // the CTAs of the latest (longest) query tiles of every head dispatch first
+  // grid (split part, head, tile) with tiles in reverse order: the CTAs of the
+  // latest (longest) query tiles of every head dispatch first, all parts of a
+  // tile together
   int r0, r1;
-  tile_rows(a, M, (int)gridDim.y - 1 - (int)blockIdx.y, r0, r1);
+  tile_rows(a, M, (int)gridDim.z - 1 - (int)blockIdx.z, r0, r1);
   if (r1 <= r0) return;  // no rows (tiles past the live count)
   if (threadIdx.x == 0) {
     if (smem_u32(smem) & 1023) __trap();  // SW128 tiles need a 1 KB aligned base
@@ -174,22 +175,25 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
   __syncthreads();
   for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) atomicMax(s_kmax, a.pos[i]);
   __syncthreads();
-  const int h = blockIdx.x;
+  const int h = blockIdx.y;
+  const int part = blockIdx.x;  // split-KV part (fastest grid dim: a tile's parts dispatch together)
   const int kvh = h / (a.H / a.Hkv);
-  // split-KV: this CTA covers key tiles [j0, j0 + nk)
-  const int j0 = blockIdx.z * a.tiles_per_split;
+  // Adaptive split-KV: a tile whose key range exceeds tiles_per_split key
+  // tiles is cut into ts = ceil(nk_tile / tiles_per_split) (<= gridDim.x)
+  // equal parts; CTA z covers part z. Tiles that fit in one part write their
+  // output directly (no partials, no combine); row_splits tells the combine.
   constexpr int KEYS = C::KEYS;
-  const int nk = min(*s_kmax / KEYS + 1 - j0, a.tiles_per_split);
+  const int nk_tile = *s_kmax / KEYS + 1;
+  const int ts = min((int)gridDim.x, (nk_tile + a.tiles_per_split - 1) / a.tiles_per_split);
+  const int tps = (nk_tile + ts - 1) / ts;
+  const int j0 = part * tps;
+  const int nk = min(nk_tile - j0, tps);
+  const bool partial = ts > 1;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const bool trace_cta = TRACE && a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
-  if (nk <= 0) {  // no keys for this split: empty partials (m = -inf, l = 0)
-    for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
-      float* ml = a.ws_ml + (((size_t)blockIdx.z * a.rows_max + i) * a.H + h) * 2;
-      ml[0] = -INFINITY;
-      ml[1] = 0.f;
-    }
-    return;
-  }
+  if (a.row_splits && part == 0 && h == 0)
+    for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) a.row_splits[i] = ts;
+  if (part >= ts || nk <= 0) return;  // this tile has no such part
 
   if (warp == 4 && lane == 0) {
     tma_prefetch(&tmQ);
@@ -398,8 +402,8 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
     }
     mbar_wait(o_done, (nk - 1) & 1);
     tc_fence_after();
-    if (a.splits > 1) {
-      const size_t pr = ((size_t)blockIdx.z * a.rows_max + row) * a.H + h;
+    if (partial) {
+      const size_t pr = ((size_t)part * a.rows_max + row) * a.H + h;
 #pragma unroll
       for (int c = 0; c < DH; c += 32) {
         uint32_t o[32];
@@ -489,20 +493,18 @@ __global__ void attn_probs_kernel(const __nv_bfloat16* __restrict__ q, const __n
 // Merge split-KV partials: out = sum_z 2^(m_z - m) acc_z / sum_z 2^(m_z - m) l_z.
 // One warp per (row, head).
 template <int DH>
-__global__ void attn_combine_kernel(const AttnArgs a) {
-  const int M = a.rows_dev ? *a.rows_dev : a.rows_max;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
-  const int row = gw / a.H, h = gw % a.H;
-  if (row >= M) return;
+__device__ __forceinline__ void attn_combine_one(const AttnArgs& a, int row, int h, int lane) {
+  const int ts = a.row_splits[row];  // parts of this row's tile (1: written directly)
+  if (ts <= 1) return;
   float m = -INFINITY;
-  for (int z = 0; z < a.splits; ++z)
+  for (int z = 0; z < ts; ++z)
     m = fmaxf(m, a.ws_ml[(((size_t)z * a.rows_max + row) * a.H + h) * 2]);
   constexpr int PER = DH / 32;
   float o[PER];
 #pragma unroll
   for (int i = 0; i < PER; ++i) o[i] = 0.f;
   float lsum = 0.f;
-  for (int z = 0; z < a.splits; ++z) {
+  for (int z = 0; z < ts; ++z) {
     const size_t pr = ((size_t)z * a.rows_max + row) * a.H + h;
     const float mz = a.ws_ml[pr * 2];
     if (mz == -INFINITY) continue;
@@ -515,6 +517,18 @@ __global__ void attn_combine_kernel(const AttnArgs a) {
   __nv_bfloat16* dst = a.out + (size_t)row * (a.H * DH) + h * DH + lane * PER;
 #pragma unroll
   for (int i = 0; i < PER; i += 2) *reinterpret_cast<uint32_t*>(dst + i) = pack_bf16(o[i] * inv, o[i + 1] * inv);
+}
+
+// grid-strided over the live (row, head) pairs (the live row count may be
+// far below rows_max in sparse passes)
+template <int DH>
+__global__ void attn_combine_kernel(const AttnArgs a) {
+  const int M = a.rows_dev ? *a.rows_dev : a.rows_max;
+  const int lane = threadIdx.x % 32;
+  const long long n = (long long)M * a.H;
+  for (long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / 32; gw < n;
+       gw += (long long)gridDim.x * blockDim.x / 32)
+    attn_combine_one<DH>(a, (int)(gw / a.H), (int)(gw % a.H), lane);
 }
 
 // Upper bound on query tiles of a launch (row groups split at their bounds).
@@ -532,12 +546,12 @@ void launch_attn(rk_engine* e, const CUtensorMap& tq, const CUtensorMap& tk, con
     RK_CUDA(cudaFuncSetAttribute(attn_kernel<DH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ACfg<DH>::SMEM));
     attr = true;
   }
-  dim3 grid(a.H, max_tiles(a), a.splits);
+  dim3 grid(a.splits, a.H, max_tiles(a));
   if (a.trace) attn_kernel<DH, true><<<grid, kThreadsA, ACfg<DH>::SMEM, e->stream>>>(tq, tk, tv, a);
   else attn_kernel<DH, false><<<grid, kThreadsA, ACfg<DH>::SMEM, e->stream>>>(tq, tk, tv, a);
   if (a.splits > 1) {
     const int warps = a.rows_max * a.H;
-    attn_combine_kernel<DH><<<(warps + 7) / 8, 256, 0, e->stream>>>(a);
+    attn_combine_kernel<DH><<<std::min((warps + 7) / 8, 4 * e->sm_count), 256, 0, e->stream>>>(a);
     e->launches += 1;
   }
 }
@@ -561,24 +575,27 @@ void attention_bf16(rk_engine* e, const AttnArgs& a_in, const __nv_bfloat16* ctx
   const int nk_max = (ctx_rows + keys - 1) / keys;
   a.splits = 1;
   a.tiles_per_split = nk_max > 0 ? nk_max : 1;
-  // split the key range only while the grid is well under 1.5 waves; each
-  // split keeps >= 4 key tiles (a CTA's fixed cost is a few microseconds).
-  // (Measured: splitting the c2 sparse layers 2-way to shorten the longest
-  // CTA is slower -- the partial writes and the combine cost more. Also
-  // measured and dropped: a column-split softmax with two warpgroups per tile
-  // and 50% polynomial exp2 -- both slower than this layout.)
-  const int want = (3 * slots / 2) / std::max(1, base);
-  if (want >= 2 && nk_max >= 8) {
-    const int splits = std::min(want, nk_max / 4);
-    a.tiles_per_split = (nk_max + splits - 1) / splits;
-    a.splits = (nk_max + a.tiles_per_split - 1) / a.tiles_per_split;
+  // Adaptive split-KV when the grid cannot fill ~1.5 waves: the longest
+  // tile should not walk more key tiles than the average load of a resident
+  // slot (~ base * nk_max / (2 * slots), causal), and no part below 4 key
+  // tiles (a CTA's fixed cost is a few microseconds). Only tiles longer than
+  // that are cut (per tile, on the device); the rest write their output
+  // directly. (Measured: a uniform 2-way split of the c2 sparse layers and a
+  // column-split softmax with two warpgroups per tile were both slower.)
+  if (base < slots && nk_max >= 8) {  // (at 1-1.5 waves, c2's sparse layers, splitting measured slower)
+    const int target = std::max(4, (int)((double)nk_max * base / (2.0 * slots) + 0.999));
+    if (target < nk_max) {
+      a.tiles_per_split = target;
+      a.splits = std::min(16, (nk_max + target - 1) / target);
+    }
   }
   if (a.splits > 1) {
     Scratch& S = *e->scratch;
     const size_t per = (size_t)a.splits * a.rows_max * a.H;
-    S.attn_ws.ensure(per * (a.dh + 2) * 4);
+    S.attn_ws.ensure(per * (a.dh + 2) * 4 + (size_t)a.rows_max * 4 + 256);
     a.ws_o = S.attn_ws.as<float>();
     a.ws_ml = a.ws_o + per * a.dh;
+    a.row_splits = reinterpret_cast<int*>(a.ws_ml + per * 2);
   }
   const int q = a.H * a.dh, kv = a.Hkv * a.dh;
   CUtensorMap tq, tk, tv;
