@@ -401,6 +401,12 @@ def run_ours(args, world, rank, local, dist):
     gathered = gather_records(recs, n_sessions, dist, device=f"cuda:{local}")
 
     hbm, tf_burst, tf_sus, src = peaks()
+    traffic = {}  # ncu DRAM bytes per launch, from the committed capture of this workload
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+            traffic = json.load(f)["kernels"] if args.config == "c2" else {}
+    except Exception:
+        traffic = {}
     detail = sorted(kstats, key=lambda k: -k["total_ms"])
     kstats = merge_kernel_stats(kstats)
     gemm = next((k for k in kstats if k["name"].startswith("gemm")), None)
@@ -409,7 +415,9 @@ def run_ours(args, world, rank, local, dist):
         achieved = gemm["flops"] / (gemm["total_ms"] / 1e3) / 1e12
         roofline = {"kernel": "gemm_bf16_tcgen05", "bound": "tensor", "achieved": round(achieved, 1),
                     "peak": tf_sus, "peak_source": f"{src} bf16_tflops_sustained", "unit": "TFLOP/s",
-                    "frac": round(achieved / tf_sus, 4), "traffic": None,
+                    "frac": round(achieved / tf_sus, 4),
+                    "traffic": traffic.get("gemm_bf16_tcgen05", {}).get("traffic_bytes"),
+                    "traffic_launch": traffic.get("gemm_bf16_tcgen05", {}).get("launch"),
                     "launches_per_step": gemm["launches"],
                     "gemm_ms_per_step": round(gemm["total_ms"], 4),
                     "gemm_tflop_per_step": round(gemm["flops"] / 1e12, 4)}
@@ -421,6 +429,9 @@ def run_ours(args, world, rank, local, dist):
         if k["bytes"] and not k["name"].startswith(("gemm", "attention")):
             e["gbs"] = round(k["bytes"] / (k["total_ms"] / 1e3) / 1e9, 1) if k["total_ms"] else None
             e["hbm_frac"] = round(e["gbs"] / hbm, 4) if e.get("gbs") else None
+            e["bytes_per_launch"] = round(k["bytes"] / max(1, k["launches"]))
+        if k["name"] in traffic:
+            e["ncu_traffic_bytes"] = traffic[k["name"]]["traffic_bytes"]
         kernels[k["name"]] = e
 
     cpu = None
