@@ -39,7 +39,8 @@ typedef enum rk_status {
   RK_ERR_SCHEMA = 2,           /* relaykv::SchemaError (profile window, profiler.cpp:28-35) */
   RK_ERR_LOGIC = 3,            /* std::logic_error (accounting, relay_engine.cpp:57-66) */
   RK_ERR_NONFINITE = 4,        /* std::runtime_error "<what>: non-finite value" (tensor.cpp:58-64) */
-  RK_ERR_RUNTIME = 5           /* other std::runtime_error: CUDA failure, out of memory */
+  RK_ERR_RUNTIME = 5,          /* other std::runtime_error: CUDA failure, out of memory */
+  RK_ERR_IO = 6                /* relaykv::IoError (errors.hpp:12): cannot open / read / write a file */
 } rk_status;
 
 /* Numerics of a weights object (and of everything computed with it).
@@ -240,6 +241,29 @@ int rk_cache_export(rk_cache* c, int32_t* tokens, float* const* k_pre, float* co
                     float* hidden_snapshot, float* influence, uint64_t* source_base,
                     uint64_t* snapshot_layer);
 void rk_cache_destroy(rk_cache* c);
+
+/* ---- RKRC relay-cache files (relay_cache.cpp:176-253, serialize.cpp:45-117)
+ * "RKRC" | u32 1 | u64 manifest length | JSON manifest | fp32 blob, FNV-1a-64
+ * blob checksum. Files are byte-identical to the reference's
+ * save_relay_cache; corrupt files fail with RK_ERR_SCHEMA, unreadable paths
+ * with RK_ERR_IO, exactly where load_relay_cache throws. */
+/* save_relay_cache (relay_cache.cpp:238-245). A bf16 cache saves its bf16
+ * values widened to fp32. */
+int rk_cache_save(rk_cache* c, const char* path);
+/* load_relay_cache (relay_cache.cpp:247-253) straight onto the device.
+ * asynchronous != 0: the blob is read into pinned memory owned by the cache
+ * and streamed layer by layer as in rk_cache_upload_async. */
+int rk_cache_load(rk_engine* e, rk_weights* w, const char* path, int asynchronous, rk_cache** out);
+/* Host-only codec (no device work): a host view to a file, a file to a view
+ * whose arrays live until rk_cache_file_free. */
+typedef struct rk_cache_file rk_cache_file;
+int rk_cache_file_write(const rk_relay_cache_view* view, const char* path);
+int rk_cache_file_read(const char* path, rk_cache_file** out, rk_relay_cache_view* view);
+/* export_relay_cache / import_relay_cache (relay_cache.cpp:176-236) on byte
+ * buffers. encode: out == NULL queries *size; capacity < *size fails. */
+int rk_cache_file_encode(const rk_relay_cache_view* view, uint8_t* out, uint64_t capacity, uint64_t* size);
+int rk_cache_file_decode(const uint8_t* bytes, uint64_t size, rk_cache_file** out, rk_relay_cache_view* view);
+void rk_cache_file_free(rk_cache_file* f);
 
 /* ---- merged KV context (model.hpp:68-87, relay_engine.hpp:37-40) ------- */
 int rk_context_create(rk_engine* e, rk_weights* w, rk_context** out);

@@ -220,6 +220,20 @@ class Oracle:
         self._check(getattr(self.lib, self.pre + "cache_from_view")(C.byref(host.view()), C.byref(out)))
         return _Handle(self.lib, out.value, getattr(self.lib, self.pre + "cache_destroy"))
 
+    def save_cache(self, host, path):
+        """save_relay_cache (relay_cache.cpp:238-245) -- the reference library only."""
+        assert self.kind == "reference", "RKRC files exist only in the reference build"
+        c = self.upload_cache(host)
+        self._check(self.lib.ref_cache_save(P(c.ptr), os.fsencode(path)))
+
+    def load_cache(self, path):
+        """load_relay_cache (relay_cache.cpp:247-253) -> HostRelayCache."""
+        assert self.kind == "reference", "RKRC files exist only in the reference build"
+        out = P()
+        self._check(self.lib.ref_cache_load(os.fsencode(path), C.byref(out)))
+        h = _Handle(self.lib, out.value, self.lib.ref_cache_destroy)
+        return self._cache_to_host(h.ptr)
+
     def realign(self, host, base):
         c = self.upload_cache(host)
         L, n, kv = host.k_pre.shape

@@ -44,6 +44,9 @@ int guard(F&& f) {
   } catch (const SchemaError& e) {
     g_err = e.what();
     return RK_ERR_SCHEMA;
+  } catch (const IoError& e) {
+    g_err = e.what();
+    return RK_ERR_IO;
   } catch (const std::invalid_argument& e) {
     g_err = e.what();
     return RK_ERR_INVALID_ARGUMENT;
@@ -332,6 +335,13 @@ int ref_cache_view(void* c, rk_relay_cache_view* v, const float** k_ptrs, const 
   v->hidden_snapshot = C.hidden_snapshot.data.data();
   v->influence = C.influence.data();
   return RK_OK;
+}
+// save_relay_cache / load_relay_cache (relay_cache.cpp:238-253).
+int ref_cache_save(void* c, const char* path) {
+  return guard([&] { save_relay_cache(*static_cast<RelayCache*>(c), path); });
+}
+int ref_cache_load(const char* path, void** out) {
+  return guard([&] { *out = new RelayCache(load_relay_cache(path)); });
 }
 // realign (relay_cache.cpp:154-174) of every layer into out[L][n x kv].
 int ref_realign(void* c, uint64_t base, float* const* out) {

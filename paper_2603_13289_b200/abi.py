@@ -11,6 +11,7 @@ RK_ERR_SCHEMA = 2
 RK_ERR_LOGIC = 3
 RK_ERR_NONFINITE = 4
 RK_ERR_RUNTIME = 5
+RK_ERR_IO = 6
 
 RK_FP32_EXACT = 0
 RK_BF16 = 1
@@ -169,9 +170,10 @@ class StatusError(RuntimeError):
 def exception_for(code, msg):
     """Map an rk_status to the exception type the reference throws (errors.hpp,
     SURVEY.md 8(b)): invalid_argument -> ValueError, SchemaError -> SchemaError,
-    logic_error -> LogicError, non-finite/runtime -> RuntimeError subclasses."""
+    logic_error -> LogicError, IoError -> IoError (an OSError),
+    non-finite/runtime -> RuntimeError subclasses."""
     cls = {RK_ERR_INVALID_ARGUMENT: InvalidArgument, RK_ERR_SCHEMA: SchemaError,
-           RK_ERR_LOGIC: LogicError, RK_ERR_NONFINITE: NonFiniteError}.get(code, StatusError)
+           RK_ERR_LOGIC: LogicError, RK_ERR_NONFINITE: NonFiniteError, RK_ERR_IO: IoError}.get(code, StatusError)
     return cls(code, msg)
 
 
@@ -189,3 +191,7 @@ class LogicError(StatusError):
 
 class NonFiniteError(StatusError):
     pass
+
+
+class IoError(StatusError, OSError):
+    """relaykv::IoError (errors.hpp:12): a file could not be opened/read/written."""

@@ -35,6 +35,7 @@ void check(int st) {
     case RK_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
     case RK_ERR_SCHEMA: throw SchemaError(msg);
     case RK_ERR_LOGIC: throw std::logic_error(msg);
+    case RK_ERR_IO: throw IoError(msg);
     default: throw std::runtime_error(msg);
   }
 }
@@ -86,11 +87,10 @@ rk_weights* device_weights(const Weights& w) {
   return dw;
 }
 
-struct CacheUpload {
+struct CacheView {
   std::vector<const float*> kp, vp;
   rk_relay_cache_view view{};
-  rk_cache* dev = nullptr;
-  CacheUpload(const RelayCache& c, rk_weights* w) {
+  explicit CacheView(const RelayCache& c) {
     for (std::size_t l = 0; l < c.num_layers(); ++l) {
       kp.push_back(c.k_pre[l].data.data());
       vp.push_back(c.v[l].data.data());
@@ -99,8 +99,12 @@ struct CacheUpload {
                                c.segment_len(), c.segment_tokens.data(), c.source_base_position, c.snapshot_layer,
                                c.decode_steps_observed, kp.data(), vp.data(), c.hidden_snapshot.data.data(),
                                c.influence.data()};
-    check(rk_cache_upload(engine(), w, &view, &dev));
   }
+};
+
+struct CacheUpload : CacheView {
+  rk_cache* dev = nullptr;
+  CacheUpload(const RelayCache& c, rk_weights* w) : CacheView(c) { check(rk_cache_upload(engine(), w, &view, &dev)); }
   ~CacheUpload() { rk_cache_destroy(dev); }
 };
 
@@ -306,6 +310,63 @@ PrefillResult prefill(const Weights& w, std::span<const TokenId> tokens, KVConte
   check(rk_prefill(engine(), device_weights(w), ctx.handle(w), tokens.data(), tokens.size(), base,
                    r.logits.data.data()));
   return r;
+}
+
+namespace {
+// A decoded RKRC file (rk_cache_file) -> RelayCache, freeing the file.
+RelayCache take_file(rk_cache_file* f, const rk_relay_cache_view& v) {
+  RelayCache c;
+  const std::size_t n = v.segment_len, kv = v.num_kv_heads * v.d_head;
+  c.num_kv_heads = v.num_kv_heads;
+  c.d_head = v.d_head;
+  c.d_model = v.d_model;
+  c.theta_base = v.theta_base;
+  c.max_positions = v.max_positions;
+  c.segment_tokens.assign(v.segment_tokens, v.segment_tokens + n);
+  c.source_base_position = v.source_base_position;
+  c.snapshot_layer = v.snapshot_layer;
+  c.decode_steps_observed = v.decode_steps_observed;
+  for (std::size_t l = 0; l < v.num_layers; ++l) {
+    Tensor k({n, kv}), vv({n, kv});
+    std::copy(v.k_pre[l], v.k_pre[l] + n * kv, k.data.begin());
+    std::copy(v.v[l], v.v[l] + n * kv, vv.data.begin());
+    c.k_pre.push_back(std::move(k));
+    c.v.push_back(std::move(vv));
+  }
+  c.hidden_snapshot = Tensor({n, v.d_model});
+  std::copy(v.hidden_snapshot, v.hidden_snapshot + n * v.d_model, c.hidden_snapshot.data.begin());
+  c.influence.assign(v.influence, v.influence + n);
+  rk_cache_file_free(f);
+  return c;
+}
+}  // namespace
+
+std::vector<std::uint8_t> export_relay_cache(const RelayCache& cache) {
+  const CacheView v(cache);
+  uint64_t size = 0;
+  check(rk_cache_file_encode(&v.view, nullptr, 0, &size));
+  std::vector<std::uint8_t> out(size);
+  check(rk_cache_file_encode(&v.view, out.data(), out.size(), &size));
+  return out;
+}
+
+RelayCache import_relay_cache(std::vector<std::uint8_t> bytes) {
+  rk_cache_file* f = nullptr;
+  rk_relay_cache_view v{};
+  check(rk_cache_file_decode(bytes.data(), bytes.size(), &f, &v));
+  return take_file(f, v);
+}
+
+void save_relay_cache(const RelayCache& cache, const std::filesystem::path& path) {
+  const CacheView v(cache);
+  check(rk_cache_file_write(&v.view, path.c_str()));
+}
+
+RelayCache load_relay_cache(const std::filesystem::path& path) {
+  rk_cache_file* f = nullptr;
+  rk_relay_cache_view v{};
+  check(rk_cache_file_read(path.c_str(), &f, &v));
+  return take_file(f, v);
 }
 
 RelayCache capture_relay_cache(const Weights& w, std::span<const TokenId> prompt, std::size_t n,

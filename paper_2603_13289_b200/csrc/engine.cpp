@@ -13,6 +13,7 @@
 #include "internal.h"
 #include "layer.h"
 #include "prof.h"
+#include "rkrc.h"
 
 using namespace rk;
 
@@ -602,36 +603,136 @@ int rk_cache_wait(rk_cache* c) {
 
 uint64_t rk_cache_segment_len(const rk_cache* c) { return c ? c->n : 0; }
 
+namespace {
+void export_cache(rk_cache* c, int32_t* tokens, float* const* k_pre, float* const* v, float* hidden,
+                  float* influence) {
+  DeviceGuard g(c->e->device);
+  if (c->async) RK_CUDA(cudaStreamSynchronize(c->xfer));
+  cudaStream_t st = c->e->stream;
+  const size_t kv = c->kv(), n = c->n;
+  if (tokens) RK_CUDA(cudaMemcpyAsync(tokens, c->tokens.p, n * 4, cudaMemcpyDeviceToHost, st));
+  if (hidden) RK_CUDA(cudaMemcpyAsync(hidden, c->hidden.p, n * c->d * 4, cudaMemcpyDeviceToHost, st));
+  if (influence) RK_CUDA(cudaMemcpyAsync(influence, c->influence.p, n * 4, cudaMemcpyDeviceToHost, st));
+  DevBuf tmp;
+  if (c->elem == 2) tmp.alloc(n * kv * 4);
+  for (uint64_t l = 0; l < c->L; ++l)
+    for (int which = 0; which < 2; ++which) {
+      float* dst = which == 0 ? (k_pre ? k_pre[l] : nullptr) : (v ? v[l] : nullptr);
+      if (!dst) continue;
+      const char* src = static_cast<const char*>(which == 0 ? c->k_pre.p : c->v.p) + l * n * kv * c->elem;
+      if (c->elem == 4) {
+        RK_CUDA(cudaMemcpyAsync(dst, src, n * kv * 4, cudaMemcpyDeviceToHost, st));
+      } else {
+        k::bf16_to_f32(st, tmp.as<float>(), reinterpret_cast<const __nv_bfloat16*>(src), n * kv);
+        RK_CUDA(cudaMemcpyAsync(dst, tmp.p, n * kv * 4, cudaMemcpyDeviceToHost, st));
+        RK_CUDA(cudaStreamSynchronize(st));
+      }
+    }
+  RK_CUDA(cudaStreamSynchronize(st));
+}
+}  // namespace
+
 int rk_cache_export(rk_cache* c, int32_t* tokens, float* const* k_pre, float* const* v,
                     float* hidden, float* influence, uint64_t* src_base, uint64_t* snapshot) {
   return guard([&] {
-    DeviceGuard g(c->e->device);
-    if (c->async) RK_CUDA(cudaStreamSynchronize(c->xfer));
-    cudaStream_t st = c->e->stream;
-    const size_t kv = c->kv(), n = c->n;
-    if (tokens) RK_CUDA(cudaMemcpyAsync(tokens, c->tokens.p, n * 4, cudaMemcpyDeviceToHost, st));
-    if (hidden) RK_CUDA(cudaMemcpyAsync(hidden, c->hidden.p, n * c->d * 4, cudaMemcpyDeviceToHost, st));
-    if (influence) RK_CUDA(cudaMemcpyAsync(influence, c->influence.p, n * 4, cudaMemcpyDeviceToHost, st));
-    DevBuf tmp;
-    if (c->elem == 2) tmp.alloc(n * kv * 4);
-    for (uint64_t l = 0; l < c->L; ++l)
-      for (int which = 0; which < 2; ++which) {
-        float* dst = which == 0 ? (k_pre ? k_pre[l] : nullptr) : (v ? v[l] : nullptr);
-        if (!dst) continue;
-        const char* src = static_cast<const char*>(which == 0 ? c->k_pre.p : c->v.p) + l * n * kv * c->elem;
-        if (c->elem == 4) {
-          RK_CUDA(cudaMemcpyAsync(dst, src, n * kv * 4, cudaMemcpyDeviceToHost, st));
-        } else {
-          k::bf16_to_f32(st, tmp.as<float>(), reinterpret_cast<const __nv_bfloat16*>(src), n * kv);
-          RK_CUDA(cudaMemcpyAsync(dst, tmp.p, n * kv * 4, cudaMemcpyDeviceToHost, st));
-          RK_CUDA(cudaStreamSynchronize(st));
-        }
-      }
+    require(c != nullptr, RK_ERR_INVALID_ARGUMENT, "null cache");
+    export_cache(c, tokens, k_pre, v, hidden, influence);
     if (src_base) *src_base = c->src_base;
     if (snapshot) *snapshot = c->snapshot;
-    RK_CUDA(cudaStreamSynchronize(st));
   });
 }
+
+// ---- RKRC files (relay_cache.cpp:176-253) ---------------------------------
+int rk_cache_save(rk_cache* c, const char* path) {
+  return guard([&] {
+    require(c != nullptr && path != nullptr, RK_ERR_INVALID_ARGUMENT, "null cache / path");
+    const size_t n = c->n, kv = c->kv();
+    std::vector<int32_t> tokens(n);
+    std::vector<std::vector<float>> kb(c->L, std::vector<float>(n * kv)), vb(c->L, std::vector<float>(n * kv));
+    std::vector<float*> kp(c->L), vp(c->L);
+    for (uint64_t l = 0; l < c->L; ++l) {
+      kp[l] = kb[l].data();
+      vp[l] = vb[l].data();
+    }
+    std::vector<float> hidden(n * c->d), infl(n);
+    export_cache(c, tokens.data(), kp.data(), vp.data(), hidden.data(), infl.data());
+    std::vector<const float*> kc(kp.begin(), kp.end()), vc(vp.begin(), vp.end());
+    rk_relay_cache_view view{c->L, c->Hkv, c->dh, c->d, c->theta, c->maxpos, n, tokens.data(),
+                             c->src_base, c->snapshot, c->steps, kc.data(), vc.data(), hidden.data(), infl.data()};
+    rkrc_write(path, rkrc_encode(view));
+  });
+}
+
+int rk_cache_load(rk_engine* e, rk_weights* w, const char* path, int asynchronous, rk_cache** out) {
+  return guard([&] {
+    require(e != nullptr && path != nullptr && out != nullptr, RK_ERR_INVALID_ARGUMENT, "null engine / path");
+    DeviceGuard g(e->device);
+    auto file = std::make_shared<HostCacheFile>(rkrc_read(path, asynchronous != 0));
+    rk_cache* c = upload_cache(e, w, &file->view, asynchronous != 0);
+    if (asynchronous) c->host_keep = file;  // the pinned blob outlives the copies
+    *out = c;
+  });
+}
+
+struct rk_cache_file {
+  HostCacheFile f;
+};
+
+namespace {
+// export_relay_cache validates first (relay_cache.cpp:177)
+std::vector<uint8_t> encode_checked(const rk_relay_cache_view* view) {
+  require(view != nullptr, RK_ERR_INVALID_ARGUMENT, "null view");
+  const rk_relay_cache_view& v = *view;
+  require(v.segment_len > 0, RK_ERR_INVALID_ARGUMENT, "relay cache: empty segment");
+  require(v.num_layers > 0 && v.k_pre && v.v, RK_ERR_INVALID_ARGUMENT, "relay cache: per-layer K/V tables disagree");
+  require(v.snapshot_layer < v.num_layers, RK_ERR_INVALID_ARGUMENT, "relay cache: snapshot layer out of range");
+  for (uint64_t j = 0; j < v.segment_len; ++j)
+    require(v.influence[j] >= 0.0f, RK_ERR_INVALID_ARGUMENT, "relay cache: negative influence score");
+  return rkrc_encode(v);
+}
+}  // namespace
+
+int rk_cache_file_write(const rk_relay_cache_view* view, const char* path) {
+  return guard([&] {
+    require(path != nullptr, RK_ERR_INVALID_ARGUMENT, "null path");
+    rkrc_write(path, encode_checked(view));
+  });
+}
+
+int rk_cache_file_encode(const rk_relay_cache_view* view, uint8_t* out, uint64_t capacity, uint64_t* size) {
+  return guard([&] {
+    require(size != nullptr, RK_ERR_INVALID_ARGUMENT, "null size");
+    const std::vector<uint8_t> b = encode_checked(view);
+    *size = b.size();
+    if (out) {
+      require(capacity >= b.size(), RK_ERR_INVALID_ARGUMENT, "rk_cache_file_encode: buffer too small");
+      std::memcpy(out, b.data(), b.size());
+    }
+  });
+}
+
+int rk_cache_file_decode(const uint8_t* bytes, uint64_t size, rk_cache_file** out, rk_relay_cache_view* view) {
+  return guard([&] {
+    require((bytes != nullptr || size == 0) && out != nullptr && view != nullptr, RK_ERR_INVALID_ARGUMENT,
+            "null argument");
+    auto f = std::make_unique<rk_cache_file>();
+    f->f = rkrc_decode(bytes, size);
+    *view = f->f.view;
+    *out = f.release();
+  });
+}
+
+int rk_cache_file_read(const char* path, rk_cache_file** out, rk_relay_cache_view* view) {
+  return guard([&] {
+    require(path != nullptr && out != nullptr && view != nullptr, RK_ERR_INVALID_ARGUMENT, "null argument");
+    auto f = std::make_unique<rk_cache_file>();
+    f->f = rkrc_read(path, false);
+    *view = f->f.view;
+    *out = f.release();
+  });
+}
+
+void rk_cache_file_free(rk_cache_file* f) { delete f; }
 
 rk_cache::~rk_cache() {
   if (ev_meta) cudaEventDestroy(ev_meta);

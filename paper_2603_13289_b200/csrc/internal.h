@@ -154,6 +154,7 @@ struct rk_cache {
   cudaEvent_t ev_meta = nullptr;
   std::vector<cudaEvent_t> ev_layer;
   rk::DevBuf staging;  // fp32 layer staging of the bf16 conversion
+  std::shared_ptr<void> host_keep;  // host source of an async upload owned by the cache (rk_cache_load)
   size_t kv() const { return Hkv * dh; }
   ~rk_cache();
 };

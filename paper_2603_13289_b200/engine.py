@@ -42,7 +42,8 @@ def lib():
             getattr(L, f).argtypes = [P]
         L.rk_weights_num_tensors.restype = U64
         L.rk_weights_num_tensors.argtypes = [C.POINTER(ModelSpec)]
-        for f in ("rk_engine_destroy", "rk_weights_destroy", "rk_cache_destroy", "rk_context_destroy"):
+        for f in ("rk_engine_destroy", "rk_weights_destroy", "rk_cache_destroy", "rk_context_destroy",
+                  "rk_cache_file_free"):
             getattr(L, f).restype = None
             getattr(L, f).argtypes = [P]
         L.rk_flops_span_full.restype = C.c_double
@@ -176,6 +177,15 @@ class Weights(_Obj):
             c._host = host
         return c
 
+    def load_cache(self, path, asynchronous=False):
+        """load_relay_cache (relay_cache.cpp:247-253) of an RKRC file straight
+        onto the device (rk_cache_load). asynchronous: the blob is read into
+        pinned memory and streams in layer by layer like upload_cache."""
+        out = P()
+        _check(lib().rk_cache_load(P(self.engine.ptr), P(self.ptr), os.fsencode(path), int(asynchronous),
+                                   C.byref(out)))
+        return Cache(out.value, self)
+
 
 class Cache(_Obj):
     _dtor = "rk_cache_destroy"
@@ -191,6 +201,10 @@ class Cache(_Obj):
     def wait(self):
         """Block until an asynchronous upload has landed (rk_cache_wait)."""
         _check(lib().rk_cache_wait(P(self.ptr)))
+
+    def save(self, path):
+        """save_relay_cache (relay_cache.cpp:238-245): the RKRC file (rk_cache_save)."""
+        _check(lib().rk_cache_save(P(self.ptr), os.fsencode(path)))
 
     def to_host(self):
         s = self.weights.spec

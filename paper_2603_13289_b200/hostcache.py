@@ -4,6 +4,7 @@ Produces the rk_relay_cache_view the C ABI consumes (rk_cache_upload) and can
 be built from any view (e.g. one exported by another library).
 """
 import ctypes as C
+import os
 
 import numpy as np
 
@@ -86,3 +87,43 @@ class HostRelayCache:
             snapshot_layer=self.snapshot_layer, k_pre=self.k_pre.copy(), v=self.v.copy(),
             hidden_snapshot=self.hidden_snapshot.copy(), influence=self.influence.copy(),
             decode_steps_observed=self.decode_steps_observed)
+
+    def save(self, path):
+        """save_relay_cache (relay_cache.cpp:238-245) on the host: the RKRC
+        file, byte-identical to the reference's (rk_cache_file_write)."""
+        from .engine import _check, lib
+        _check(lib().rk_cache_file_write(C.byref(self.view()), os.fsencode(path)))
+
+    @classmethod
+    def load(cls, path):
+        """load_relay_cache (relay_cache.cpp:247-253) on the host: validates the
+        container and the cache like the reference (rk_cache_file_read)."""
+        from .engine import _check, lib
+        h, v = C.c_void_p(), RelayCacheView()
+        _check(lib().rk_cache_file_read(os.fsencode(path), C.byref(h), C.byref(v)))
+        try:
+            return cls.from_view(v)
+        finally:
+            lib().rk_cache_file_free(h)
+
+    def to_bytes(self):
+        """export_relay_cache (relay_cache.cpp:176-201): the RKRC bytes."""
+        from .engine import _check, lib
+        size = C.c_uint64()
+        v = self.view()
+        _check(lib().rk_cache_file_encode(C.byref(v), None, C.c_uint64(0), C.byref(size)))
+        buf = (C.c_uint8 * size.value)()
+        _check(lib().rk_cache_file_encode(C.byref(v), buf, size, C.byref(size)))
+        return bytes(buf)
+
+    @classmethod
+    def from_bytes(cls, data):
+        """import_relay_cache (relay_cache.cpp:203-236)."""
+        from .engine import _check, lib
+        data = bytes(data)
+        h, v = C.c_void_p(), RelayCacheView()
+        _check(lib().rk_cache_file_decode(C.c_char_p(data), C.c_uint64(len(data)), C.byref(h), C.byref(v)))
+        try:
+            return cls.from_view(v)
+        finally:
+            lib().rk_cache_file_free(h)

@@ -241,3 +241,35 @@ TEST_CASE("drop-in relay_prefill is bit-identical to the oracle restatement") {
   orc_cache_destroy(oc);
   orc_weights_destroy(ow);
 }
+
+// test_relay_cache.cpp:251-276 "cache export/import is the identity", plus the
+// file round trip (relay_cache.cpp:238-253).
+TEST_CASE("cache export/import is the identity") {
+  const Weights w = init_weights(spec_of(4, 32, 4), 31);
+  const RelayCache cache = capture_relay_cache(w, pattern_tokens(7, 64, 0), 5, 1);
+  const auto bytes = export_relay_cache(cache);
+  const RelayCache back = import_relay_cache(bytes);
+  CHECK(back.segment_tokens == cache.segment_tokens);
+  CHECK(back.source_base_position == cache.source_base_position);
+  CHECK(back.snapshot_layer == cache.snapshot_layer);
+  CHECK(back.decode_steps_observed == cache.decode_steps_observed);
+  CHECK(back.influence == cache.influence);
+  CHECK(std::memcmp(back.hidden_snapshot.data.data(), cache.hidden_snapshot.data.data(),
+                    cache.hidden_snapshot.data.size() * 4) == 0);
+  for (std::size_t l = 0; l < cache.num_layers(); ++l) {
+    CHECK(std::memcmp(back.k_pre[l].data.data(), cache.k_pre[l].data.data(), cache.k_pre[l].data.size() * 4) == 0);
+    CHECK(std::memcmp(back.v[l].data.data(), cache.v[l].data.data(), cache.v[l].data.size() * 4) == 0);
+  }
+  auto truncated = bytes;
+  truncated.resize(truncated.size() - 3);
+  CHECK_THROWS_AS(import_relay_cache(truncated), SchemaError);
+  RelayCache empty;
+  CHECK_THROWS_AS(export_relay_cache(empty), std::invalid_argument);
+
+  const std::filesystem::path p = std::filesystem::temp_directory_path() / "relaykv_dropin_cache.rkrc";
+  save_relay_cache(cache, p);
+  const RelayCache again = load_relay_cache(p);
+  CHECK(export_relay_cache(again) == bytes);
+  std::filesystem::remove(p);
+  CHECK_THROWS_AS(load_relay_cache(p), IoError);
+}

@@ -2,10 +2,15 @@
 on identical seeded inputs. Bar: BIT-EXACT for everything (contexts, marks,
 selection + tags, s_dev/s_key_dev, hidden states, depths, logits, caches),
 which is stronger than the north_star's 1e-4 fp32 tolerance."""
+import glob
+import json
+import os
+
 import numpy as np
 import pytest
 
 from paper_2603_13289_b200.abi import InvalidArgument, LayerProfile, RelayOptions, SchemaError
+from tests.golden.cases import CASES
 from tests.compare import assert_bit_equal, assert_outputs_equal
 from tests.scenarios import c1_spec, parity_scenarios, pattern_tokens, spec_of, synthetic_tokens, triple
 
@@ -198,3 +203,56 @@ def test_async_upload_bit_exact(engine, oracle, mode):
         out = w.context().agent_prefill(pattern_tokens(5, 64, 3), ups, pattern_tokens(4, 64, 4), prof, opts)
         res.append(out["logits"])
     assert_bit_equal(res[1], res[0], f"async.{mode}.logits")
+
+
+RKRC = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "*.rkrc")))
+
+
+@pytest.mark.parametrize("path", RKRC, ids=os.path.basename)
+@pytest.mark.parametrize("asynchronous", [False, True])
+def test_rkrc_load_onto_device(engine, path, asynchronous):
+    """load_relay_cache of a reference-written file straight onto the device
+    (rk_cache_load; async = pinned blob streamed by layer) holds the file's bits."""
+    from paper_2603_13289_b200.hostcache import HostRelayCache
+    meta = json.load(open(path + ".json"))
+    want = HostRelayCache.load(path)
+    spec = CASES[meta["case"]]["spec"]()
+    w = engine.weights(spec, meta["seed"])
+    c = w.load_cache(path, asynchronous=asynchronous)
+    got = c.to_host()
+    for f in ("segment_tokens", "k_pre", "v", "hidden_snapshot", "influence"):
+        assert_bit_equal(getattr(got, f), getattr(want, f), f"rkrc.{f}")
+    assert (got.source_base_position, got.snapshot_layer) == (want.source_base_position, want.snapshot_layer)
+
+
+@pytest.mark.parametrize("path", RKRC, ids=os.path.basename)
+def test_rkrc_device_capture_saves_reference_bytes(engine, path, tmp_path):
+    """Engine decode-time capture of the golden scenario, saved with
+    rk_cache_save, is byte-identical to the file the reference saved."""
+    meta = json.load(open(path + ".json"))
+    spec = CASES[meta["case"]]["spec"]()
+    w = engine.weights(spec, meta["seed"])
+    dctx = w.context()
+    logits = dctx.prefill(np.array(meta["old_prefix"], np.int32))
+    cache = dctx.capture_decode(logits, meta["segment_len"], meta["snapshot_layer"])
+    out = tmp_path / "engine.rkrc"
+    cache.save(out)
+    assert out.read_bytes() == open(path, "rb").read()
+
+
+def test_rkrc_loaded_cache_relays_like_uploaded(engine, oracle):
+    """A relay prefill through a loaded cache equals the reference's relay
+    prefill through the same cache (bit-exact)."""
+    path = [p for p in RKRC if "diag" in p][0]
+    meta = json.load(open(path + ".json"))
+    case = CASES[meta["case"]]
+    spec = case["spec"]()
+    from paper_2603_13289_b200.hostcache import HostRelayCache
+    host = HostRelayCache.load(path)
+    ow = oracle.weights(spec, meta["seed"])
+    want, _ = oracle.relay_prefill(ow, case["prefix"], host, case["profile"], case["opts"])
+    w = engine.weights(spec, meta["seed"])
+    got = w.context().relay_prefill(case["prefix"], w.load_cache(path, asynchronous=True), case["profile"],
+                                    case["opts"])
+    assert_outputs_equal(got, want, "rkrc.relay")
+    assert_bit_equal(got["logits"], want["logits"], "rkrc.relay.logits")
