@@ -245,7 +245,7 @@ TEST_CASE("drop-in relay_prefill is bit-identical to the oracle restatement") {
 // test_relay_cache.cpp:251-276 "cache export/import is the identity", plus the
 // file round trip (relay_cache.cpp:238-253).
 TEST_CASE("cache export/import is the identity") {
-  const Weights w = init_weights(spec_of(4, 32, 4), 31);
+  const Weights w = init_weights(spec_of(6, 32, 4), 31);
   const RelayCache cache = capture_relay_cache(w, pattern_tokens(7, 64, 0), 5, 1);
   const auto bytes = export_relay_cache(cache);
   const RelayCache back = import_relay_cache(bytes);
