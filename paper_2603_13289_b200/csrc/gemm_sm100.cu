@@ -40,12 +40,16 @@ constexpr int kBM = 128;
 constexpr int kBK = 64;  // 64 bf16 = one 128-byte swizzle row
 constexpr int kThreads = 192;
 
-template <int BN>
+// PAIR = 2: a CTA pair (cluster of 2, tcgen05 cta_group::2) computes a
+// 256 x BN tile; each CTA stages its own 128 rows of A and HALF of the BN rows
+// of B, so a CTA's shared-memory fill per k-block drops from 48 KB to 32 KB
+// (BN=256) -- the L2->SM feed, not the tensor pipe, bounds the 1-CTA kernel.
+template <int BN, int PAIR = 1>
 struct Cfg {
   static constexpr int A_BYTES = kBM * kBK * 2;
-  static constexpr int B_BYTES = BN * kBK * 2;
+  static constexpr int B_BYTES = BN / PAIR * kBK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (BN == 256) ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int STAGES = PAIR == 1 ? ((BN == 256) ? 4 : (BN == 128 ? 6 : 8)) : (BN == 256 ? 6 : 8);
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
   // per epilogue warp: a 32x32 fp32 staging tile for the coalesced residual epilogue
   static constexpr int EPI_STAGE = 4 * 32 * 32 * 4;
@@ -57,10 +61,11 @@ struct Units {
   int total;
 };
 
+template <int PAIR = 1>
 __device__ __forceinline__ Units units_of(const GemmArgs& p) {
   Units u;
   const int M = p.rows_dev ? *p.rows_dev : p.rows_max;
-  u.num_m = (M + kBM - 1) / kBM;
+  u.num_m = (M + kBM * PAIR - 1) / (kBM * PAIR);  // m tiles of 128 (or 256-row pair tiles)
   u.num_n = p.N / p.bn;
   // live row count known only on the device: pick split-K here (grid = all SMs)
   u.splits = p.splits;
@@ -94,10 +99,12 @@ __device__ __forceinline__ long long sk_lo(const Units& u, int g, int G) {
   return (long long)u.num_m * u.num_n * u.kb_total * g / G;
 }
 
-// k-th work item of this CTA; false when the CTA is done.
+// k-th work item of this CTA (both CTAs of a pair walk the same units);
+// false when the CTA is done.
+template <int PAIR = 1>
 __device__ __forceinline__ bool get_work(const Units& U, bool streamk, int k, Work& w) {
-  if (!streamk) {
-    const int unit = blockIdx.x + k * gridDim.x;
+  if (PAIR == 2 || !streamk) {
+    const int unit = blockIdx.x / PAIR + k * (gridDim.x / PAIR);
     if (unit >= U.total) return false;
     decode_unit(U, unit, w.mt, w.nt, w.s);
     w.kb0 = w.s * U.kb_per;
@@ -195,11 +202,11 @@ __device__ __forceinline__ void epilogue_chunk(const GemmArgs& p, int row, int c
   }
 }
 
-template <int BN, int EPI>
+template <int BN, int EPI, int PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const GemmArgs p) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, PAIR>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
@@ -210,7 +217,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* epi_stage = smem + C::STAGES * C::STAGE_BYTES + 256;  // [4 warps][32 rows][128 B]
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const Units U = units_of(p);
+  const Units U = units_of<PAIR>(p);
+  const uint32_t rank = PAIR == 2 ? cluster_ctarank() : 0;  // 0 = leader (issues the MMAs)
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
@@ -221,13 +229,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 4);
+      mbar_init(&tempty[i], 4 * PAIR);  // the epilogue warps of both CTAs drain the leader's accumulator
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  if (warp == 1) {
+    if constexpr (PAIR == 2) tmem_alloc_pair(tmem_slot, C::TMEM_COLS);
+    else tmem_alloc(tmem_slot, C::TMEM_COLS);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR == 2) cluster_sync();  // barriers of both CTAs initialised before any remote use
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -236,26 +248,35 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       Work w;
-      for (int it = 0; get_work(U, p.streamk, it, w); ++it) {
+      for (int it = 0; get_work<PAIR>(U, p.streamk, it, w); ++it) {
         const int mt = w.mt, nt = w.nt, kb0 = w.kb0, kb1 = w.kb1;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
-          mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-          tma_load_2d(sa, &tmA, &full[stage], kb * kBK, mt * kBM);
-          tma_load_2d(sa + C::A_BYTES, &tmB, &full[stage], kb * kBK, nt * BN);
+          const bool same = p.dbg & 1;
+          const int kx = same ? 0 : kb * kBK, am = same ? 0 : mt, bn_ = same ? 0 : nt;
+          if constexpr (PAIR == 2) {
+            // the leader's barrier counts both CTAs' bytes
+            if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+            tma_load_2d_pair(sa, &tmA, &full[stage], kx, (am * 2 + rank) * kBM);
+            tma_load_2d_pair(sa + C::A_BYTES, &tmB, &full[stage], kx, bn_ * BN + rank * (BN / 2));
+          } else {
+            mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+            tma_load_2d(sa, &tmA, &full[stage], kx, am * kBM);
+            tma_load_2d(sa + C::A_BYTES, &tmB, &full[stage], kx, bn_ * BN);
+          }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    if (elect_one()) {  // ---------------- MMA issuer
-      constexpr uint32_t idesc = idesc_bf16(kBM, BN);
+    if (rank == 0 && elect_one()) {  // ---------------- MMA issuer (the pair's leader)
+      constexpr uint32_t idesc = idesc_bf16(kBM * PAIR, BN);
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
       Work w;
-      for (int it = 0; get_work(U, p.streamk, it, w); ++it, ++local) {
+      for (int it = 0; get_work<PAIR>(U, p.streamk, it, w); ++it, ++local) {
         const int kb0 = w.kb0, kb1 = w.kb1;
         const int acc = local & 1;
         mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);
@@ -268,13 +289,20 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t b0 = a0 + C::A_BYTES;
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k) {
-            mma_bf16_ss(d, sdesc_sw128(a0 + k * 32, 16, 1024), sdesc_sw128(b0 + k * 32, 16, 1024), idesc,
-                        (kb > kb0 || k > 0) ? 1u : 0u);
+            if (p.dbg & 2) break;
+            if constexpr (PAIR == 2)
+              mma_bf16_ss_pair(d, sdesc_sw128(a0 + k * 32, 16, 1024), sdesc_sw128(b0 + k * 32, 16, 1024), idesc,
+                               (kb > kb0 || k > 0) ? 1u : 0u);
+            else
+              mma_bf16_ss(d, sdesc_sw128(a0 + k * 32, 16, 1024), sdesc_sw128(b0 + k * 32, 16, 1024), idesc,
+                          (kb > kb0 || k > 0) ? 1u : 0u);
           }
-          tc_commit(&empty[stage]);
+          if constexpr (PAIR == 2) tc_commit_pair(&empty[stage]);
+          else tc_commit(&empty[stage]);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
-        tc_commit(&tfull[acc]);
+        if constexpr (PAIR == 2) tc_commit_pair(&tfull[acc]);
+        else tc_commit(&tfull[acc]);
       }
     }
   } else {  // ------------------------------- epilogue warps 2..5
@@ -282,8 +310,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int M = p.rows_dev ? *p.rows_dev : p.rows_max;
     int local = 0;
     Work w;
-    for (int it = 0; get_work(U, p.streamk, it, w); ++it, ++local) {
-      const int mt = w.mt, nt = w.nt, s = w.s;
+    for (int it = 0; get_work<PAIR>(U, p.streamk, it, w); ++it, ++local) {
+      const int mt = w.mt * PAIR + rank, nt = w.nt, s = w.s;  // this CTA's 128-row tile
       const int acc = local & 1;
       const int row = mt * kBM + quarter * 32 + lane;
       int* flag = nullptr;
@@ -394,7 +422,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if constexpr (PAIR == 2) mbar_arrive_cluster(&tempty[acc], 0);
+        else mbar_arrive(&tempty[acc]);
+      }
       if (flag) {
         __threadfence();
         __syncwarp();
@@ -403,8 +434,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   tc_fence_before();
-  __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, C::TMEM_COLS);
+  if constexpr (PAIR == 2) {
+    cluster_sync();  // neither CTA leaves while its peer may still signal its barriers
+    if (warp == 1) tmem_dealloc_pair(tmem, C::TMEM_COLS);
+  } else {
+    __syncthreads();
+    if (warp == 1) tmem_dealloc(tmem, C::TMEM_COLS);
+  }
 }
 
 // Split-K reduction + residual epilogue (EPI_PART partials): one CTA per row,
@@ -466,7 +502,7 @@ __device__ __forceinline__ void splitk_reduce_row(const GemmArgs& p, int splits,
 
 __global__ void __launch_bounds__(256) splitk_reduce_add_kernel(const GemmArgs p, int splits, int G) {
   const int M = p.rows_dev ? *p.rows_dev : p.rows_max;
-  const Units U = units_of(p);
+  const Units U = units_of<1>(p);
   __shared__ int sk_tab[1025];  // stream-K range starts of the G CTAs (+ end)
   if (p.streamk) {
     for (int g = threadIdx.x; g <= G; g += blockDim.x) sk_tab[g] = (int)sk_lo(U, g, G);
@@ -476,21 +512,71 @@ __global__ void __launch_bounds__(256) splitk_reduce_add_kernel(const GemmArgs p
     splitk_reduce_row(p, splits, row, U, G, sk_tab);
 }
 
-template <int BN, int EPI>
+template <int BN, int EPI, int PAIR>
 void launch(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& p, int grid) {
+  using C = Cfg<BN, PAIR>;
   static bool attr = false;
   if (!attr) {
-    RK_CUDA(cudaFuncSetAttribute(gemm_bf16_kernel<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
+    RK_CUDA(cudaFuncSetAttribute(gemm_bf16_kernel<BN, EPI, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr = true;
   }
-  gemm_bf16_kernel<BN, EPI><<<grid, kThreads, Cfg<BN>::SMEM, st>>>(a, b, p);
+  if constexpr (PAIR == 1) {
+    gemm_bf16_kernel<BN, EPI, 1><<<grid, kThreads, C::SMEM, st>>>(a, b, p);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    RK_CUDA(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<BN, EPI, 2>, a, b, p));
+  }
 }
 
 template <int EPI>
 void launch_bn(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& p, int grid) {
-  if (p.bn == 256) launch<256, EPI>(st, a, b, p, grid);
-  else if (p.bn == 128) launch<128, EPI>(st, a, b, p, grid);
-  else launch<64, EPI>(st, a, b, p, grid);
+  if (p.pair == 2) {
+    if (p.bn == 256) launch<256, EPI, 2>(st, a, b, p, grid);
+    else if (p.bn == 128) launch<128, EPI, 2>(st, a, b, p, grid);
+    else launch<64, EPI, 2>(st, a, b, p, grid);
+  } else {
+    if (p.bn == 256) launch<256, EPI, 1>(st, a, b, p, grid);
+    else if (p.bn == 128) launch<128, EPI, 1>(st, a, b, p, grid);
+    else launch<64, EPI, 1>(st, a, b, p, grid);
+  }
+}
+
+// CTA pairs the GPU can hold at once (a GPC's odd SM cannot host a pair).
+int pair_slots(int sm_count) {
+  static int slots = -1;
+  if (slots < 0) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * sm_count);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = Cfg<256, 2>::SMEM;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    RK_CUDA(cudaFuncSetAttribute(gemm_bf16_kernel<256, EPI_F32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 Cfg<256, 2>::SMEM));
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, gemm_bf16_kernel<256, EPI_F32, 2>, &cfg) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = 0;
+    }
+    slots = n;
+  }
+  return slots;
 }
 
 }  // namespace
@@ -527,45 +613,74 @@ void make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t c
   if (r != CUDA_SUCCESS) raise(RK_ERR_RUNTIME, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
 }
 
-// Pick the N tile and split count so the grid fills the SMs: the widest tile
-// that still gives a full wave, else BN=64; split-K only while the grid is
-// under half the SMs (split_flags present, residual epilogue).
+// Pick the CTA shape (single CTA with 128-row tiles, or a CTA pair with
+// 256-row tiles), the N tile and the split count so the grid fills the GPU:
+// the widest tile that still gives a full wave of units, else BN=64; split-K
+// only for residual GEMMs that cannot fill the GPU.
 static void choose_config(GemmArgs& p, int sm_count, int rows_hint) {
-  const int num_m = (rows_hint + kBM - 1) / kBM;
+  static const int pair_env = [] {
+    const char* v = std::getenv("RK_GEMM_PAIR");
+    return v ? std::atoi(v) : 1;
+  }();
+  static const int dbg_env = [] {
+    const char* v = std::getenv("RK_GEMM_DBG");
+    return v ? std::atoi(v) : 0;
+  }();
+  p.dbg = dbg_env;
+  const int pslots = pair_env ? pair_slots(sm_count) : 0;
+  // Pairs tile M by 256 and cut each CTA's k-block fill from 48 to 32 KB
+  // (B200: ~0.425 vs ~0.46 us per k-block of a 128x256 per-CTA tile) but run
+  // half as many units at once: take them when the rounds of units allow, and
+  // never for short M, where the last pair tile is mostly padding.
+  p.pair = 1;
+  if (pslots > 0 && rows_hint > kBM) {
+    auto rounds = [&](int tm, int slots_) {
+      int best = 1 << 30;
+      for (int cand : {256, 128})
+        if (p.N % cand == 0) best = std::min(best, ((rows_hint + tm - 1) / tm * (p.N / cand) + slots_ - 1) / slots_ *
+                                                       (cand / 128));
+      return best;
+    };
+    const double single = rounds(kBM, sm_count) * 0.46, pair = rounds(2 * kBM, pslots) * 0.425;
+    if (pair_env == 2 || (rows_hint >= 640 && pair <= single)) p.pair = 2;
+  }
+  const int slots = p.pair == 2 ? pslots : sm_count;  // concurrent units
+  const int tile_m = kBM * p.pair;
+  const int num_m = (rows_hint + tile_m - 1) / tile_m;
   p.sms = sm_count;
   int bn = 64;
   for (int cand : {256, 128}) {
-    if (p.N % cand == 0 && num_m * (p.N / cand) >= sm_count) { bn = cand; break; }
+    if (p.N % cand == 0 && num_m * (p.N / cand) >= slots) { bn = cand; break; }
   }
   if (p.N % bn) raise(RK_ERR_INVALID_ARGUMENT, "bf16 GEMM needs N % 64 == 0");
   p.bn = bn;
   p.splits = 1;
   if (p.epi == EPI_ADD && p.split_flags) {
-    // residual GEMMs that cannot fill the SMs: widest tile, K split s ways with
+    // residual GEMMs that cannot fill the GPU: widest tile, K split s ways with
     // the s partials reduced (in order) by splitk_reduce_add_kernel; s picks
-    // the best wave efficiency of tiles*s units over the SMs
-    // Cost model (calibrated on B200): a 128x256 k-block ~0.45 us per CTA;
-    // partials cost s * M * N * 4 B written + read at ~8 TB/s plus ~3 us for
-    // the reduce launch.
+    // the best wave efficiency of tiles*s units over the slots.
+    // Cost model (calibrated on B200): a k-block of a 128x256 per-CTA tile
+    // ~0.45 us (1 CTA, L2-feed bound) / ~0.30 us (pair); partials cost
+    // s * M * N * 4 B written + read at ~8 TB/s plus ~3 us for the reduce launch.
     const int wide = p.N % 256 == 0 ? 256 : (p.N % 128 == 0 ? 128 : 64);
     const int tiles = num_m * (p.N / wide), kb = p.K / kBK;
-    if (4 * tiles < 3 * sm_count) {
-      const double t_kb = 0.45 * wide / 256.0;
-      // stream-K: every SM gets the same k-block count; partials of the
-      // ~tiles + SMs segments go through L2 to the reduce kernel
-      // (measured on c2: slower than split-K at these shapes -- opt-in with
-      // RK_GEMM_STREAMK=1 for experiments)
+    if (4 * tiles < 3 * slots) {
+      const double t_kb = (p.pair == 2 ? 0.30 : 0.45) * wide / 256.0;
+      // stream-K (1-CTA kernel only): every SM gets the same k-block count;
+      // partials of the ~tiles + SMs segments go through L2 to the reduce
+      // kernel (measured on c2: slower than split-K at these shapes -- opt-in
+      // with RK_GEMM_STREAMK=1 for experiments)
       static const bool sk_enabled = [] {
         const char* v = std::getenv("RK_GEMM_STREAMK");
         return v && std::atoi(v) != 0;
       }();
       const int tiles_max = ((p.rows_max + kBM - 1) / kBM) * (p.N / wide);
-      const bool sk_ok = sk_enabled && kb >= 2 && tiles_max <= 2 * sm_count;
+      const bool sk_ok = sk_enabled && p.pair == 1 && kb >= 2 && tiles_max <= 2 * sm_count;
       const double sk_cost = sk_ok ? ((double)tiles * kb + sm_count - 1) / sm_count * t_kb + 1.0 +
                                          2.0 * (tiles + sm_count) * (double)kBM * wide * 4 / 8e6
                                    : 1e30;
       auto cost = [&](int s) {
-        const int units = tiles * s, waves = (units + sm_count - 1) / sm_count;
+        const int units = tiles * s, waves = (units + slots - 1) / slots;
         const double mma = waves * ((kb + s - 1) / s) * t_kb;
         const double part = s > 1 ? 3.0 + 2.0 * s * (double)rows_hint * p.N * 4 / 8e6 : 0.0;
         return mma + part;
@@ -596,10 +711,11 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
   if (p.norm_part && p.N / p.bn > kNormSlots) raise(RK_ERR_INVALID_ARGUMENT, "fused RMSNorm: too many N tiles");
   CUtensorMap ta, tb;
   make_tmap_bf16(&ta, A, (uint64_t)p.rows_max, (uint64_t)p.K, kBM, (uint64_t)lda);
-  make_tmap_bf16(&tb, B, (uint64_t)p.N, (uint64_t)p.K, (uint32_t)p.bn, (uint64_t)p.K);
-  const int num_m = (p.rows_max + kBM - 1) / kBM;
-  const int total = num_m * (p.N / p.bn) * p.splits;
-  const int grid = p.streamk ? e->sm_count : (total < e->sm_count ? total : e->sm_count);
+  make_tmap_bf16(&tb, B, (uint64_t)p.N, (uint64_t)p.K, (uint32_t)(p.bn / p.pair), (uint64_t)p.K);
+  const int num_m = (p.rows_max + kBM * p.pair - 1) / (kBM * p.pair);
+  const int total = num_m * (p.N / p.bn) * p.splits;  // units (pair units for the pair kernel)
+  const int slots = p.pair == 2 ? pair_slots(e->sm_count) : e->sm_count;
+  const int grid = p.streamk ? e->sm_count : p.pair * (total < slots ? total : slots);
   if (p.epi == EPI_PART) {
     e->scratch->gemm_ws.ensure(p.streamk ? (size_t)grid * kSkSlots * kBM * p.bn * 4
                                          : (size_t)p.splits * p.rows_max * p.N * 4);
@@ -609,7 +725,8 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
   ProfScope ps(e, (e->prof && e->prof->on)
                       ? intern(std::string("gemm_") + kEpi[p.epi] + "_m" + std::to_string(p.rows_max) +
                                (p.rows_dev ? "dyn" : "") + "_n" + std::to_string(p.N) + "_k" + std::to_string(p.K) +
-                               "_bn" + std::to_string(p.bn) + (p.streamk ? std::string("_sk") : "_s" + std::to_string(p.splits)))
+                               "_bn" + std::to_string(p.bn) + (p.streamk ? std::string("_sk") : "_s" + std::to_string(p.splits)) +
+                               (p.pair == 2 ? "_pair" : ""))
                       : "gemm",
                0, 0);
   ps.rec.kind = 1;

@@ -18,6 +18,8 @@ struct GemmArgs {
   int epi = EPI_F32;
   int bn = 128, splits = 1;     // chosen by gemm_bf16 (splits re-chosen on the device for live rows)
   int sms = 148;
+  int dbg = 0;                  // experiments (RK_GEMM_DBG): 1 = every k-block loads tile (0,0), 2 = no MMAs
+  int pair = 1;                 // 2: CTA-pair kernel (256-row tiles, cta_group::2), chosen by gemm_bf16
   int* split_flags = nullptr;   // ordered split-K flags (EPI_ADD), zero-initialised
   // outputs
   float* out_f32 = nullptr;     // EPI_ADD / EPI_F32, row stride ld_out

@@ -30,7 +30,8 @@ def run_gemm(engine, A, B, C0, live, epi):
 
 
 SHAPES = [(1, 64, 64), (7, 192, 128), (128, 256, 256), (200, 384, 512), (333, 1024, 2048),
-          (1000, 128, 1024), (64, 3072, 2048), (256, 2048, 8192), (513, 16384, 256)]
+          (1000, 128, 1024), (64, 3072, 2048), (256, 2048, 8192), (513, 16384, 256), (129, 64, 64),
+          (4032, 3072, 2048), (320, 16384, 2048)]
 
 
 @pytest.mark.parametrize("shape", SHAPES, ids=[f"{m}x{n}x{k}" for m, n, k in SHAPES])
@@ -224,6 +225,35 @@ err = np.abs(got - ref).max() / np.abs(ref).max()
 assert err < 2e-5, err
 print("ok")
 """
-    env = dict(os.environ, RK_GEMM_STREAMK="1")
+    env = dict(os.environ, RK_GEMM_STREAMK="1", RK_GEMM_PAIR="0")  # stream-K is a 1-CTA-kernel mode
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_gemm_single_cta_kernel():
+    """The 1-CTA GEMM kernel (RK_GEMM_PAIR=0; the default uses CTA pairs for
+    M > 128) on the store / residual / live-row shapes, in a subprocess."""
+    import os
+    import subprocess
+    import sys
+    code = f"""
+import numpy as np, sys
+sys.path.insert(0, {os.getcwd()!r})
+from paper_2603_13289_b200.engine import Engine
+from tests.test_gpu_kernels import run_gemm, bf16_round, SHAPES
+e = Engine(0)
+for (M, N, K) in SHAPES + [(1356, 2048, 2048), (320, 16384, 2048)]:
+    rng = np.random.default_rng(M + N + K)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    B = (rng.standard_normal((N, K)) / np.sqrt(K)).astype(np.float32)
+    H = rng.standard_normal((M, N)).astype(np.float32)
+    for epi, C0 in ((3, np.zeros((M, N))), (1, H)):
+        got = run_gemm(e, A, B, C0, M, epi)
+        ref = C0 + bf16_round(A).astype(np.float64) @ bf16_round(B).astype(np.float64).T
+        err = np.abs(got - ref).max() / np.abs(ref).max()
+        assert err < 2e-5, (M, N, K, epi, err)
+print("ok")
+"""
+    env = dict(os.environ, RK_GEMM_PAIR="0")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
