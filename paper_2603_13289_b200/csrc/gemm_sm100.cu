@@ -24,6 +24,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "internal.h"
@@ -202,7 +203,116 @@ __device__ __forceinline__ void epilogue_chunk(const GemmArgs& p, int row, int c
   }
 }
 
-template <int BN, int EPI, int PAIR>
+// Cluster split-K epilogue (CSK): the p.splits CTAs of a cluster computed the
+// K slices of one 128 x BN tile; row group o (g = ceil(128/s) rows) is owned
+// by CTA o. Each CTA stores its slice of group o into CTA o's (now idle)
+// pipeline shared memory over DSMEM, then every owner adds the s slices in
+// split order -- the same order as splitk_reduce_add_kernel, so the result is
+// bit-identical to the EPI_PART path without the global partial round trip
+// and the second launch -- to the residual, with the fused RMSNorm statistics.
+template <int BN>
+__device__ __forceinline__ void csk_epilogue(const GemmArgs& p, const Units& U, uint8_t* smem, uint32_t tmem,
+                                             int warp, int lane) {
+  const int s = p.splits, g = (kBM + s - 1) / s;
+  const uint32_t me = cluster_ctarank();
+  Work w;
+  if (!get_work<1>(U, false, 0, w)) return;  // the whole cluster is past the live rows
+  const int mt = w.mt, nt = w.nt;
+  const int M = p.rows_dev ? *p.rows_dev : p.rows_max;
+  float* red = reinterpret_cast<float*>(smem);  // [src split][g rows][BN], 16-B units XOR-swizzled by row
+  cluster_sync();  // every CTA's MMAs are done: all pipeline memory in the cluster is free
+  if (warp >= 2) {
+    const int quarter = warp & 3, row = quarter * 32 + lane;
+    const int o = row / g, lr = row - o * g;
+    const float rs = (p.row_scale && mt * kBM + row < M) ? p.row_scale[mt * kBM + row] : 1.0f;
+    const uint32_t dst = mapa_u32(smem_u32(red + ((size_t)me * g + lr) * BN), (p.dbg & 4) ? me : (uint32_t)o);
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t r[32];
+      tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + c, r);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int u = c / 4 + (j ^ (lr & 7));
+        st_cluster_v4(dst + u * 16, __float_as_uint(__uint_as_float(r[4 * j]) * rs),
+                      __float_as_uint(__uint_as_float(r[4 * j + 1]) * rs),
+                      __float_as_uint(__uint_as_float(r[4 * j + 2]) * rs),
+                      __float_as_uint(__uint_as_float(r[4 * j + 3]) * rs));
+      }
+    }
+  }
+  cluster_sync();  // all slices landed
+  if (warp < 2 || (p.dbg & 8)) return;
+  const bool norm = p.norm_part != nullptr;
+  const int r0 = (int)me * g, r1 = min(kBM, r0 + g), nrows = r1 - r0;
+  // warp w takes rows w, w+4, ...; RB rows at a time with their residuals
+  // loaded up front (the global-load latency is paid once per batch)
+  constexpr int NP = BN >= 128 ? BN / 128 : 1, RB = 8;
+  for (int base = warp - 2; base < nrows; base += 4 * RB) {
+    float4 hv[RB][NP];
+#pragma unroll
+    for (int i = 0; i < RB; ++i) {
+      const int lr = base + 4 * i, grow = mt * kBM + r0 + lr;
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        const int cc = lane * 4 + 128 * k;
+        hv[i][k] = (lr < nrows && grow < M && cc < BN)
+                       ? __ldcg(reinterpret_cast<const float4*>(p.out_f32 + (size_t)grow * p.ld_out + nt * BN + cc))
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < RB; ++i) {
+      const int lr = base + 4 * i, grow = mt * kBM + r0 + lr;
+      if (lr >= nrows || grow >= M) break;
+      float ss = 0.f;
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        const int cc = lane * 4 + 128 * k;
+        if (cc >= BN) break;
+        const int unit = cc / 4, phys = (unit & ~7) | ((unit & 7) ^ (lr & 7));
+        float4 acc = *reinterpret_cast<const float4*>(red + (size_t)lr * BN + phys * 4);
+        for (int src = 1; src < s; ++src) {
+          const float4 v = *reinterpret_cast<const float4*>(red + ((size_t)src * g + lr) * BN + phys * 4);
+          acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+        float4 h = hv[i][k];
+        h.x += acc.x; h.y += acc.y; h.z += acc.z; h.w += acc.w;
+        *reinterpret_cast<float4*>(p.out_f32 + (size_t)grow * p.ld_out + nt * BN + cc) = h;
+        if (norm) {
+          ss = fmaf(h.x, h.x, fmaf(h.y, h.y, fmaf(h.z, h.z, fmaf(h.w, h.w, ss))));
+          *reinterpret_cast<uint2*>(p.norm_bf16 + (size_t)grow * p.N + nt * BN + cc) =
+              make_uint2(pack_bf16(h.x, h.y), pack_bf16(h.z, h.w));
+        }
+      }
+      if (norm) {
+        for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        if (lane == 0) p.norm_part[(size_t)grow * kNormSlots + nt] = ss;
+      }
+    }
+  }
+  if (norm) {
+    // the last of the num_n tiles of this row group turns the partials into 1/rms
+    __shared__ int done_sh;
+    __threadfence();
+    named_bar_sync(1, 128);
+    if (threadIdx.x == 64) done_sh = atomicAdd(p.norm_cnt + (size_t)mt * 8 + me, 1) + 1;
+    named_bar_sync(1, 128);
+    if (done_sh == U.num_n) {
+      __threadfence();
+      for (int lr = threadIdx.x - 64; lr < r1 - r0; lr += 128) {
+        const int grow = mt * kBM + r0 + lr;
+        if (grow >= M) break;
+        float tot = 0.f;
+        for (int t = 0; t < U.num_n; ++t) tot += __ldcg(p.norm_part + (size_t)grow * kNormSlots + t);
+        p.norm_inv[grow] = rsqrtf(tot / (float)p.N + p.norm_eps);
+      }
+      if (threadIdx.x == 64) p.norm_cnt[(size_t)mt * 8 + me] = 0;
+    }
+  }
+}
+
+template <int BN, int EPI, int PAIR, bool CSK = false>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const GemmArgs p) {
@@ -304,6 +414,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (PAIR == 2) tc_commit_pair(&tfull[acc]);
         else tc_commit(&tfull[acc]);
       }
+    }
+  } else if constexpr (CSK) {  // epilogue warps: wait for this CTA's K slice, then the cluster epilogue
+    Work w0;
+    if (get_work<1>(U, false, 0, w0)) {  // (a cluster past the live rows has no tile)
+      mbar_wait(&tfull[0], 0);
+      tc_fence_after();
     }
   } else {  // ------------------------------- epilogue warps 2..5
     const int quarter = warp & 3;
@@ -433,6 +549,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
+  if constexpr (CSK) {
+    __syncwarp();
+    csk_epilogue<BN>(p, U, smem, tmem, warp, lane);
+  }
   tc_fence_before();
   if constexpr (PAIR == 2) {
     cluster_sync();  // neither CTA leaves while its peer may still signal its barriers
@@ -512,15 +632,30 @@ __global__ void __launch_bounds__(256) splitk_reduce_add_kernel(const GemmArgs p
     splitk_reduce_row(p, splits, row, U, G, sk_tab);
 }
 
-template <int BN, int EPI, int PAIR>
+template <int BN, int EPI, int PAIR, bool CSK = false>
 void launch(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& p, int grid) {
   using C = Cfg<BN, PAIR>;
   static bool attr = false;
   if (!attr) {
-    RK_CUDA(cudaFuncSetAttribute(gemm_bf16_kernel<BN, EPI, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    RK_CUDA(cudaFuncSetAttribute(gemm_bf16_kernel<BN, EPI, PAIR, CSK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 C::SMEM));
     attr = true;
   }
-  if constexpr (PAIR == 1) {
+  if constexpr (CSK) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = p.splits;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    RK_CUDA(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<BN, EPI, 1, true>, a, b, p));
+  } else if constexpr (PAIR == 1) {
     gemm_bf16_kernel<BN, EPI, 1><<<grid, kThreads, C::SMEM, st>>>(a, b, p);
   } else {
     cudaLaunchConfig_t cfg = {};
@@ -541,6 +676,14 @@ void launch(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const G
 
 template <int EPI>
 void launch_bn(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& p, int grid) {
+  if constexpr (EPI == EPI_ADD) {
+    if (p.csk) {
+      if (p.bn == 256) launch<256, EPI_ADD, 1, true>(st, a, b, p, grid);
+      else if (p.bn == 128) launch<128, EPI_ADD, 1, true>(st, a, b, p, grid);
+      else launch<64, EPI_ADD, 1, true>(st, a, b, p, grid);
+      return;
+    }
+  }
   if (p.pair == 2) {
     if (p.bn == 256) launch<256, EPI, 2>(st, a, b, p, grid);
     else if (p.bn == 128) launch<128, EPI, 2>(st, a, b, p, grid);
@@ -550,6 +693,34 @@ void launch_bn(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, cons
     else if (p.bn == 128) launch<128, EPI, 1>(st, a, b, p, grid);
     else launch<64, EPI, 1>(st, a, b, p, grid);
   }
+}
+
+// Clusters of s CSK CTAs the GPU can hold at once.
+int csk_slots(int s) {
+  static int slots[9] = {-1, -1, -1, -1, -1, -1, -1, -1, -1};
+  if (s < 2 || s > 8) return 0;
+  if (slots[s] < 0) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(s * 64);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = Cfg<256, 1>::SMEM;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = s;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    RK_CUDA(cudaFuncSetAttribute(gemm_bf16_kernel<256, EPI_ADD, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 Cfg<256, 1>::SMEM));
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, gemm_bf16_kernel<256, EPI_ADD, 1, true>, &cfg) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = 0;
+    }
+    slots[s] = n;
+  }
+  return slots[s];
 }
 
 // CTA pairs the GPU can hold at once (a GPC's odd SM cannot host a pair).
@@ -656,16 +827,26 @@ static void choose_config(GemmArgs& p, int sm_count, int rows_hint) {
   p.bn = bn;
   p.splits = 1;
   if (p.epi == EPI_ADD && p.split_flags) {
-    // residual GEMMs that cannot fill the GPU: widest tile, K split s ways with
-    // the s partials reduced (in order) by splitk_reduce_add_kernel; s picks
-    // the best wave efficiency of tiles*s units over the slots.
+    // Residual GEMMs that cannot fill the GPU split K s ways over 1-CTA tiles
+    // (widest tile), either
+    //  CSK:      the s CTAs of one tile form a cluster and reduce over DSMEM
+    //            (one launch, no global partials), or
+    //  EPI_PART: s partials in global memory, reduced in split order by
+    //            splitk_reduce_add_kernel (any s, any cluster occupancy).
     // Cost model (calibrated on B200): a k-block of a 128x256 per-CTA tile
-    // ~0.45 us (1 CTA, L2-feed bound) / ~0.30 us (pair); partials cost
-    // s * M * N * 4 B written + read at ~8 TB/s plus ~3 us for the reduce launch.
+    // ~0.46 us (1 CTA, L2-feed bound) / ~0.42 us (pair); EPI_PART partials
+    // cost s * M * N * 4 B written + read at ~8 TB/s plus ~3 us for the reduce
+    // launch; the CSK exchange ~1 us.
+    static const int csk_env = [] {
+      const char* v = std::getenv("RK_GEMM_CSK");
+      return v ? std::atoi(v) : 0;  // opt-in: measured slower than EPI_PART + reduce on c2 shapes
+    }();
     const int wide = p.N % 256 == 0 ? 256 : (p.N % 128 == 0 ? 128 : 64);
     const int tiles = num_m * (p.N / wide), kb = p.K / kBK;
+    const int tiles1 = (rows_hint + kBM - 1) / kBM * (p.N / wide);
     if (4 * tiles < 3 * slots) {
-      const double t_kb = (p.pair == 2 ? 0.30 : 0.45) * wide / 256.0;
+      const double t_kb1 = 0.46 * wide / 256.0;
+      const double t_now = (p.pair == 2 ? 0.42 : 0.46) * wide / 256.0;
       // stream-K (1-CTA kernel only): every SM gets the same k-block count;
       // partials of the ~tiles + SMs segments go through L2 to the reduce
       // kernel (measured on c2: slower than split-K at these shapes -- opt-in
@@ -675,29 +856,35 @@ static void choose_config(GemmArgs& p, int sm_count, int rows_hint) {
         return v && std::atoi(v) != 0;
       }();
       const int tiles_max = ((p.rows_max + kBM - 1) / kBM) * (p.N / wide);
-      const bool sk_ok = sk_enabled && p.pair == 1 && kb >= 2 && tiles_max <= 2 * sm_count;
-      const double sk_cost = sk_ok ? ((double)tiles * kb + sm_count - 1) / sm_count * t_kb + 1.0 +
-                                         2.0 * (tiles + sm_count) * (double)kBM * wide * 4 / 8e6
+      const bool sk_ok = sk_enabled && kb >= 2 && tiles_max <= 2 * sm_count;
+      const double sk_cost = sk_ok ? ((double)tiles1 * kb + sm_count - 1) / sm_count * t_kb1 + 1.0 +
+                                         2.0 * (tiles1 + sm_count) * (double)kBM * wide * 4 / 8e6
                                    : 1e30;
-      auto cost = [&](int s) {
-        const int units = tiles * s, waves = (units + slots - 1) / slots;
-        const double mma = waves * ((kb + s - 1) / s) * t_kb;
-        const double part = s > 1 ? 3.0 + 2.0 * s * (double)rows_hint * p.N * 4 / 8e6 : 0.0;
-        return mma + part;
-      };
-      int best = 1;
-      double best_cost = cost(1);
-      for (int s = 2; s <= 8 && kb / s >= 4; ++s)
-        if (cost(s) < best_cost) { best = s; best_cost = cost(s); }
+      double best_cost = (double)((tiles + slots - 1) / slots) * kb * t_now;
+      int best = 1, best_csk = 0;
+      for (int s = 2; s <= 8 && kb / s >= 4; ++s) {
+        if ((s - 1) * ((kb + s - 1) / s) >= kb) continue;  // the last split would get no k-blocks
+        const int waves = (tiles1 * s + sm_count - 1) / sm_count;
+        const double part = waves * ((kb + s - 1) / s) * t_kb1 + 3.0 + 2.0 * s * (double)rows_hint * p.N * 4 / 8e6;
+        if (part < best_cost) { best = s; best_cost = part; best_csk = 0; }
+        const int cs = csk_env ? csk_slots(s) : 0;
+        if (cs > 0) {
+          const double csk = (double)((tiles1 + cs - 1) / cs) * ((kb + s - 1) / s) * t_kb1 + 1.0;
+          if (csk < best_cost) { best = s; best_cost = csk; best_csk = 1; }
+        }
+      }
       if (sk_cost < best_cost) {
+        p.pair = 1;
         p.bn = wide;
         p.splits = 1;
         p.streamk = 1;
         p.epi = EPI_PART;
       } else if (best > 1) {
+        p.pair = 1;
         p.bn = wide;
         p.splits = best;
-        p.epi = EPI_PART;
+        p.csk = best_csk;
+        if (!best_csk) p.epi = EPI_PART;
       }
     }
   }
@@ -708,6 +895,10 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
   if (p.rows_max <= 0) return;
   if (p.K % kBK) raise(RK_ERR_INVALID_ARGUMENT, "bf16 GEMM needs K % 64 == 0");
   choose_config(p, e->sm_count, rows_hint > 0 ? rows_hint : p.rows_max);
+  static const bool log = std::getenv("RK_GEMM_LOG") != nullptr;
+  if (log)
+    std::fprintf(stderr, "[gemm] M=%d%s N=%d K=%d epi=%d -> bn=%d pair=%d splits=%d csk=%d streamk=%d\n", p.rows_max,
+                 p.rows_dev ? "(dyn)" : "", p.N, p.K, p.epi, p.bn, p.pair, p.splits, p.csk, p.streamk);
   if (p.norm_part && p.N / p.bn > kNormSlots) raise(RK_ERR_INVALID_ARGUMENT, "fused RMSNorm: too many N tiles");
   CUtensorMap ta, tb;
   make_tmap_bf16(&ta, A, (uint64_t)p.rows_max, (uint64_t)p.K, kBM, (uint64_t)lda);
@@ -715,7 +906,8 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
   const int num_m = (p.rows_max + kBM * p.pair - 1) / (kBM * p.pair);
   const int total = num_m * (p.N / p.bn) * p.splits;  // units (pair units for the pair kernel)
   const int slots = p.pair == 2 ? pair_slots(e->sm_count) : e->sm_count;
-  const int grid = p.streamk ? e->sm_count : p.pair * (total < slots ? total : slots);
+  const int grid = p.csk ? total  // one tile per cluster of p.splits CTAs
+                   : p.streamk ? e->sm_count : p.pair * (total < slots ? total : slots);
   if (p.epi == EPI_PART) {
     e->scratch->gemm_ws.ensure(p.streamk ? (size_t)grid * kSkSlots * kBM * p.bn * 4
                                          : (size_t)p.splits * p.rows_max * p.N * 4);
@@ -726,7 +918,7 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
                       ? intern(std::string("gemm_") + kEpi[p.epi] + "_m" + std::to_string(p.rows_max) +
                                (p.rows_dev ? "dyn" : "") + "_n" + std::to_string(p.N) + "_k" + std::to_string(p.K) +
                                "_bn" + std::to_string(p.bn) + (p.streamk ? std::string("_sk") : "_s" + std::to_string(p.splits)) +
-                               (p.pair == 2 ? "_pair" : ""))
+                               (p.pair == 2 ? "_pair" : "") + (p.csk ? "_csk" : ""))
                       : "gemm",
                0, 0);
   ps.rec.kind = 1;

@@ -105,7 +105,7 @@ static NormBufs norm_bufs(rk_engine* e, size_t rows) {
   Scratch& S = *e->scratch;
   S.norm_inv.ensure(rows * 4 + 256);
   S.norm_part.ensure(rows * kNormSlots * 4 + 256);
-  const size_t cnt_bytes = ((rows + 127) / 128 * 4 + 64) * 4;
+  const size_t cnt_bytes = ((rows + 127) / 128 * 8 + 64) * 4;  // [m tile][quarter or cluster owner]
   if (S.norm_cnt.bytes < cnt_bytes) {
     S.norm_cnt.ensure(cnt_bytes);
     RK_CUDA(cudaMemsetAsync(S.norm_cnt.p, 0, S.norm_cnt.bytes, e->stream));

@@ -19,6 +19,7 @@ struct GemmArgs {
   int bn = 128, splits = 1;     // chosen by gemm_bf16 (splits re-chosen on the device for live rows)
   int sms = 148;
   int dbg = 0;                  // experiments (RK_GEMM_DBG): 1 = every k-block loads tile (0,0), 2 = no MMAs
+  int csk = 0;                  // 1: split-K inside a cluster of `splits` CTAs, reduced over DSMEM
   int pair = 1;                 // 2: CTA-pair kernel (256-row tiles, cta_group::2), chosen by gemm_bf16
   int* split_flags = nullptr;   // ordered split-K flags (EPI_ADD), zero-initialised
   // outputs

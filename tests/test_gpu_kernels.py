@@ -257,3 +257,39 @@ print("ok")
     env = dict(os.environ, RK_GEMM_PAIR="0")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("shape", [(320, 2048, 8192), (1356, 2048, 2048), (40, 512, 4096), (320, 4096, 14336)])
+def test_gemm_cluster_split_k_matches_global_split_k(engine, shape, tmp_path):
+    """Split-K reduced inside a cluster over DSMEM (opt-in RK_GEMM_CSK=1,
+    subprocess) and the global-partials split-K path (default) both match the
+    fp64 reference; each is deterministic. (Their split counts may differ, so
+    their bits may too; with equal splits the summation order is the same.)"""
+    import os
+    import subprocess
+    import sys
+    M, N, K = shape
+    rng = np.random.default_rng(11)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    B = (rng.standard_normal((N, K)) / np.sqrt(K)).astype(np.float32)
+    H = rng.standard_normal((M, N)).astype(np.float32)
+    np.savez(tmp_path / "in.npz", A=A, B=B, H=H)
+    got = run_gemm(engine, A, B, H, M, 1)
+    code = f"""
+import numpy as np, sys
+sys.path.insert(0, {os.getcwd()!r})
+from paper_2603_13289_b200.engine import Engine
+from tests.test_gpu_kernels import run_gemm
+e = Engine(0)
+d = np.load({str(tmp_path / "in.npz")!r})
+np.save({str(tmp_path / "out.npy")!r}, run_gemm(e, d["A"], d["B"], d["H"], {M}, 1))
+"""
+    env = dict(os.environ, RK_GEMM_CSK="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    want = np.load(tmp_path / "out.npy")
+    again = run_gemm(engine, A, B, H, M, 1)
+    assert np.array_equal(got.view(np.uint32), again.view(np.uint32)), "split-K not deterministic"
+    ref = H + bf16_round(A).astype(np.float64) @ bf16_round(B).astype(np.float64).T
+    assert np.abs(got - ref).max() / np.abs(ref).max() < 2e-5
+    assert np.abs(want - ref).max() / np.abs(ref).max() < 2e-5
