@@ -265,6 +265,62 @@ int rk_cache_file_encode(const rk_relay_cache_view* view, uint8_t* out, uint64_t
 int rk_cache_file_decode(const uint8_t* bytes, uint64_t size, rk_cache_file** out, rk_relay_cache_view* view);
 void rk_cache_file_free(rk_cache_file* f);
 
+/* ---- offline layer profiler (profiler.cpp:155-175, metrics.cpp:118-238) --
+ * Calibrates a LayerProfile: per calibration instance, a decode-time capture
+ * of a segment under one prefix (reuse side) against a full prefill of the
+ * same segment under another (full side), token_deviation over all layers,
+ * layer curves (similarity s, adjacent-layer Spearman rho), averaged, then the
+ * start / end / detection scans. In RK_FP32_EXACT every number is
+ * bit-identical to the reference. */
+/* ProfilerParams (profiler.hpp:19-28). */
+typedef struct rk_profiler_params {
+  double tau_start;           /* 0.99 */
+  uint64_t tail_layers;       /* 5 */
+  double stability_lambda;    /* 2.0 */
+  uint64_t consecutive;       /* 2 */
+  uint64_t min_rise;          /* 3 */
+  int32_t first_negative_alpha; /* 0 */
+} rk_profiler_params;
+/* TwoStageConfig (metrics.hpp:93-107). */
+typedef struct rk_two_stage_config {
+  uint64_t seed;              /* 1 */
+  uint64_t instances;         /* 8 */
+  uint64_t stage1_prefix_min, stage1_prefix_max; /* 32, 64 */
+  uint64_t stage2_prefix_min, stage2_prefix_max; /* 24, 72 */
+  uint64_t segment_len;       /* 48 */
+  uint64_t stage2_suffix_len; /* 16 */
+  uint64_t sweep_instances;   /* 2 */
+  int32_t identical_prefix;   /* 0 */
+  uint64_t snapshot_layer;    /* 0 */
+} rk_two_stage_config;
+/* The scans' result (LayerProfile window + the two fallback warnings). */
+typedef struct rk_profile_result {
+  uint64_t l_start, l_det, l_end;
+  int32_t end_fallback;       /* "end-layer scan found no stable window; using last layer" */
+  int32_t det_fallback;       /* "no correlation-trend transition; detection at l_start + 1" */
+} rk_profile_result;
+/* token_deviation (metrics.cpp:118-159) of two caches of one segment (reuse
+ * side, full side) on the device; outputs [n x L] row-major (position, layer),
+ * any may be NULL. */
+int rk_token_deviation(rk_cache* reuse, rk_cache* full, double* value_cos, double* key_cos,
+                       double* value_norm, double* key_norm);
+/* Host-only: make_layer_curve (metrics.cpp:191-213) of a value-cosine
+ * deviation matrix [n x L]: s[L], rho[L] (rho[0] = NaN), rho_degenerate[L]. */
+int rk_layer_curve(const double* value_cos, uint64_t n, uint64_t L, double* s, double* rho,
+                   uint8_t* rho_degenerate);
+/* Host-only: average_curves (metrics.cpp:215-238) of k curves laid out [k][L]. */
+int rk_average_curves(const double* s, const double* rho, const uint8_t* rho_degenerate, uint64_t k,
+                      uint64_t L, double* s_out, double* rho_out, uint8_t* rho_degenerate_out);
+/* Host-only: profile_from_curve (profiler.cpp:123-155); curve_rho_out [L-1]
+ * (curve_rho[i] correlates layers i and i+1) may be NULL. */
+int rk_profile_from_curve(const double* s, const double* rho, const uint8_t* rho_degenerate, uint64_t L,
+                          const rk_profiler_params* params, rk_profile_result* out, double* curve_rho_out);
+/* profile_model (profiler.cpp:157-175) with every instance's captures,
+ * prefills and deviations on the device. curve_s [L], curve_rho [L-1] may be NULL. */
+int rk_profile_model(rk_engine* e, rk_weights* w, const rk_two_stage_config* calib,
+                     const rk_profiler_params* params, rk_profile_result* out, double* curve_s,
+                     double* curve_rho);
+
 /* ---- merged KV context (model.hpp:68-87, relay_engine.hpp:37-40) ------- */
 int rk_context_create(rk_engine* e, rk_weights* w, rk_context** out);
 int rk_context_clone(rk_context* src, rk_context** out);

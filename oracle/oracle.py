@@ -234,6 +234,66 @@ class Oracle:
         h = _Handle(self.lib, out.value, self.lib.ref_cache_destroy)
         return self._cache_to_host(h.ptr)
 
+    # ---- offline profiler (reference library only) ---------------------------
+    def profile_model(self, w, calib, params):
+        from paper_2603_13289_b200.abi import ProfileResult
+        assert self.kind == "reference"
+        L = w.spec.num_layers
+        out, s, rho = ProfileResult(), np.empty(L), np.empty(max(L - 1, 1))
+        dp = C.POINTER(C.c_double)
+        self._check(self.lib.ref_profile_model(P(w.ptr), C.byref(calib), C.byref(params), C.byref(out),
+                                               s.ctypes.data_as(dp), rho.ctypes.data_as(dp)))
+        d = out.as_dict()
+        d["curve_s"], d["curve_rho"] = s, rho[:L - 1]
+        return d
+
+    def token_deviation(self, reuse_host, full_host):
+        assert self.kind == "reference"
+        a, b = self.upload_cache(reuse_host), self.upload_cache(full_host)
+        L, n = reuse_host.num_layers, reuse_host.segment_len
+        out = {k: np.empty((n, L), np.float64) for k in ("value_cos", "key_cos", "value_norm", "key_norm")}
+        dp = C.POINTER(C.c_double)
+        self._check(self.lib.ref_token_deviation(P(a.ptr), P(b.ptr), *[out[k].ctypes.data_as(dp) for k in
+                                                                        ("value_cos", "key_cos", "value_norm",
+                                                                         "key_norm")]))
+        return out
+
+    def layer_curve(self, value_cos):
+        m = np.ascontiguousarray(value_cos, np.float64)
+        n, L = m.shape
+        s, rho, deg = np.empty(L), np.empty(L), np.empty(L, np.uint8)
+        dp = C.POINTER(C.c_double)
+        self._check(self.lib.ref_layer_curve(m.ctypes.data_as(dp), U64(n), U64(L), s.ctypes.data_as(dp),
+                                             rho.ctypes.data_as(dp), deg.ctypes.data_as(C.POINTER(C.c_uint8))))
+        return {"s": s, "rho": rho, "rho_degenerate": deg.astype(bool)}
+
+    def average_curves(self, curves):
+        s = np.ascontiguousarray([c["s"] for c in curves], np.float64)
+        rho = np.ascontiguousarray([c["rho"] for c in curves], np.float64)
+        deg = np.ascontiguousarray([c["rho_degenerate"] for c in curves], np.uint8)
+        k, L = s.shape
+        so, ro, do = np.empty(L), np.empty(L), np.empty(L, np.uint8)
+        dp, up = C.POINTER(C.c_double), C.POINTER(C.c_uint8)
+        self._check(self.lib.ref_average_curves(s.ctypes.data_as(dp), rho.ctypes.data_as(dp), deg.ctypes.data_as(up),
+                                                U64(k), U64(L), so.ctypes.data_as(dp), ro.ctypes.data_as(dp),
+                                                do.ctypes.data_as(up)))
+        return {"s": so, "rho": ro, "rho_degenerate": do.astype(bool)}
+
+    def profile_from_curve(self, curve, params):
+        from paper_2603_13289_b200.abi import ProfileResult
+        s = np.ascontiguousarray(curve["s"], np.float64)
+        rho = np.ascontiguousarray(curve["rho"], np.float64)
+        deg = np.ascontiguousarray(curve["rho_degenerate"], np.uint8)
+        L = s.shape[0]
+        out, crho = ProfileResult(), np.empty(max(L - 1, 1))
+        dp = C.POINTER(C.c_double)
+        self._check(self.lib.ref_profile_from_curve(s.ctypes.data_as(dp), rho.ctypes.data_as(dp),
+                                                    deg.ctypes.data_as(C.POINTER(C.c_uint8)), U64(L),
+                                                    C.byref(params), C.byref(out), crho.ctypes.data_as(dp)))
+        d = out.as_dict()
+        d["curve_s"], d["curve_rho"] = s, crho[:L - 1]
+        return d
+
     def realign(self, host, base):
         c = self.upload_cache(host)
         L, n, kv = host.k_pre.shape

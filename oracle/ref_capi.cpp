@@ -23,6 +23,7 @@
 #include <vector>
 
 #include "relaykv/errors.hpp"
+#include "relaykv/metrics.hpp"
 #include "relaykv/model.hpp"
 #include "relaykv/profiler.hpp"
 #include "relaykv/relay_cache.hpp"
@@ -543,5 +544,104 @@ double ref_flops_segment_schedule(const rk_model_spec* s, uint64_t base, uint64_
 
 // libm expf of this host, for checking the device restatement of it.
 float ref_host_expf(float x) { return std::exp(x); }
+
+// ---- offline profiler (profiler.cpp:155-175, metrics.cpp:118-238) ----------
+namespace {
+ProfilerParams to_params(const rk_profiler_params& p) {
+  ProfilerParams q;
+  q.tau_start = p.tau_start;
+  q.tail_layers = p.tail_layers;
+  q.stability_lambda = p.stability_lambda;
+  q.consecutive = p.consecutive;
+  q.min_rise = p.min_rise;
+  q.first_negative_alpha = p.first_negative_alpha != 0;
+  return q;
+}
+void put_profile(const LayerProfile& lp, rk_profile_result* out, double* curve_s, double* curve_rho) {
+  out->l_start = lp.l_start;
+  out->l_det = lp.l_det;
+  out->l_end = lp.l_end;
+  out->end_fallback = 0;
+  out->det_fallback = 0;
+  for (const auto& w : lp.warnings) {
+    if (w.find("end-layer") != std::string::npos) out->end_fallback = 1;
+    if (w.find("detection") != std::string::npos) out->det_fallback = 1;
+  }
+  if (curve_s) std::copy(lp.curve_s.begin(), lp.curve_s.end(), curve_s);
+  if (curve_rho) std::copy(lp.curve_rho.begin(), lp.curve_rho.end(), curve_rho);
+}
+LayerCurve to_curve(const double* s, const double* rho, const uint8_t* deg, uint64_t L) {
+  LayerCurve c;
+  c.s.assign(s, s + L);
+  c.rho.assign(rho, rho + L);
+  for (uint64_t l = 0; l < L; ++l) c.rho_degenerate.push_back(deg[l] != 0);
+  return c;
+}
+}  // namespace
+
+int ref_profile_model(void* w, const rk_two_stage_config* c, const rk_profiler_params* p, rk_profile_result* out,
+                      double* curve_s, double* curve_rho) {
+  return guard([&] {
+    TwoStageConfig cfg;
+    cfg.seed = c->seed;
+    cfg.instances = c->instances;
+    cfg.stage1_prefix_min = c->stage1_prefix_min;
+    cfg.stage1_prefix_max = c->stage1_prefix_max;
+    cfg.stage2_prefix_min = c->stage2_prefix_min;
+    cfg.stage2_prefix_max = c->stage2_prefix_max;
+    cfg.segment_len = c->segment_len;
+    cfg.stage2_suffix_len = c->stage2_suffix_len;
+    cfg.sweep_instances = c->sweep_instances;
+    cfg.identical_prefix = c->identical_prefix != 0;
+    cfg.snapshot_layer = c->snapshot_layer;
+    put_profile(profile_model(*static_cast<Weights*>(w), cfg, to_params(*p)), out, curve_s, curve_rho);
+  });
+}
+// token_deviation of two caches' (k_pre, v); outputs [n x L].
+int ref_token_deviation(void* reuse, void* full, double* vc, double* kc, double* vn, double* kn) {
+  return guard([&] {
+    const RelayCache& a = *static_cast<RelayCache*>(reuse);
+    const RelayCache& b = *static_cast<RelayCache*>(full);
+    SegmentKV ra{a.k_pre, a.v}, fb{b.k_pre, b.v};
+    const DeviationMatrix m = token_deviation(ra, fb, a.num_kv_heads);
+    std::copy(m.value_cos.begin(), m.value_cos.end(), vc);
+    std::copy(m.key_cos.begin(), m.key_cos.end(), kc);
+    std::copy(m.value_norm.begin(), m.value_norm.end(), vn);
+    std::copy(m.key_norm.begin(), m.key_norm.end(), kn);
+  });
+}
+int ref_layer_curve(const double* value_cos, uint64_t n, uint64_t L, double* s, double* rho, uint8_t* deg) {
+  return guard([&] {
+    DeviationMatrix m;
+    m.segment_len = n;
+    m.num_layers = L;
+    m.value_cos.assign(value_cos, value_cos + n * L);
+    m.key_cos = m.value_norm = m.key_norm = m.value_cos;
+    const LayerCurve c = make_layer_curve(m);
+    for (uint64_t l = 0; l < L; ++l) {
+      s[l] = c.s[l];
+      rho[l] = c.rho[l];
+      deg[l] = c.rho_degenerate[l];
+    }
+  });
+}
+int ref_profile_from_curve(const double* s, const double* rho, const uint8_t* deg, uint64_t L,
+                           const rk_profiler_params* p, rk_profile_result* out, double* curve_rho) {
+  return guard([&] { put_profile(profile_from_curve(to_curve(s, rho, deg, L), to_params(*p), "m"), out, nullptr,
+                                 curve_rho); });
+}
+int ref_average_curves(const double* s, const double* rho, const uint8_t* deg, uint64_t k, uint64_t L, double* so,
+                       double* ro, uint8_t* dout) {
+  return guard([&] {
+    std::vector<LayerCurve> cs;
+    for (uint64_t i = 0; i < k; ++i) cs.push_back(to_curve(s + i * L, rho + i * L, deg + i * L, L));
+    const LayerCurve a = average_curves(cs);
+    for (uint64_t l = 0; l < L; ++l) {
+      so[l] = a.s[l];
+      ro[l] = a.rho[l];
+      dout[l] = a.rho_degenerate[l];
+    }
+  });
+}
 
 }  // extern "C"

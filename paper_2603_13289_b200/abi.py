@@ -153,6 +153,55 @@ class RelayOutput(C.Structure):
     ]
 
 
+class ProfilerParams(C.Structure):
+    """rk_profiler_params == ProfilerParams (profiler.hpp:19-28)."""
+    _fields_ = [
+        ("tau_start", C.c_double),
+        ("tail_layers", C.c_uint64),
+        ("stability_lambda", C.c_double),
+        ("consecutive", C.c_uint64),
+        ("min_rise", C.c_uint64),
+        ("first_negative_alpha", C.c_int32),
+    ]
+
+    @classmethod
+    def make(cls, tau_start=0.99, tail_layers=5, stability_lambda=2.0, consecutive=2, min_rise=3,
+             first_negative_alpha=False):
+        return cls(tau_start, tail_layers, stability_lambda, consecutive, min_rise, int(first_negative_alpha))
+
+
+class TwoStageConfig(C.Structure):
+    """rk_two_stage_config == TwoStageConfig (metrics.hpp:93-107)."""
+    _fields_ = [
+        ("seed", C.c_uint64),
+        ("instances", C.c_uint64),
+        ("stage1_prefix_min", C.c_uint64),
+        ("stage1_prefix_max", C.c_uint64),
+        ("stage2_prefix_min", C.c_uint64),
+        ("stage2_prefix_max", C.c_uint64),
+        ("segment_len", C.c_uint64),
+        ("stage2_suffix_len", C.c_uint64),
+        ("sweep_instances", C.c_uint64),
+        ("identical_prefix", C.c_int32),
+        ("snapshot_layer", C.c_uint64),
+    ]
+
+    @classmethod
+    def make(cls, seed=1, instances=8, stage1_prefix=(32, 64), stage2_prefix=(24, 72), segment_len=48,
+             stage2_suffix_len=16, sweep_instances=2, identical_prefix=False, snapshot_layer=0):
+        return cls(seed, instances, stage1_prefix[0], stage1_prefix[1], stage2_prefix[0], stage2_prefix[1],
+                   segment_len, stage2_suffix_len, sweep_instances, int(identical_prefix), snapshot_layer)
+
+
+class ProfileResult(C.Structure):
+    """rk_profile_result: the LayerProfile window + fallback warnings (profiler.cpp:123-155)."""
+    _fields_ = [("l_start", C.c_uint64), ("l_det", C.c_uint64), ("l_end", C.c_uint64),
+                ("end_fallback", C.c_int32), ("det_fallback", C.c_int32)]
+
+    def as_dict(self):
+        return {f: int(getattr(self, f)) for f, _ in self._fields_}
+
+
 def stats_dict(st):
     d = {f: getattr(st, f) for f, _ in ReuseStats._fields_ if f != "wall"}
     d["wall"] = {f: getattr(st.wall, f) for f, _ in PhaseTimings._fields_}

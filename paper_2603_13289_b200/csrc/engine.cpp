@@ -13,6 +13,7 @@
 #include "internal.h"
 #include "layer.h"
 #include "prof.h"
+#include "profiler.h"
 #include "rkrc.h"
 
 using namespace rk;
@@ -1042,3 +1043,149 @@ int rk_context_reset(rk_context* c) {
   });
 }
 }  // extern "C"
+
+// ---- offline layer profiler (profiler.cpp:155-175, metrics.cpp:118-238) -----
+int rk_token_deviation(rk_cache* reuse, rk_cache* full, double* value_cos, double* key_cos, double* value_norm,
+                       double* key_norm) {
+  return guard([&] {
+    require(reuse != nullptr && full != nullptr, RK_ERR_INVALID_ARGUMENT, "null cache");
+    // token_deviation's shape checks (metrics.cpp:120-147)
+    require(reuse->L == full->L && reuse->L > 0, RK_ERR_INVALID_ARGUMENT, "token_deviation: layer count mismatch");
+    require(reuse->n == full->n && reuse->kv() == full->kv() && reuse->elem == full->elem, RK_ERR_INVALID_ARGUMENT,
+            "token_deviation: shape mismatch at layer 0");
+    require(reuse->Hkv > 0 && reuse->kv() % reuse->Hkv == 0, RK_ERR_INVALID_ARGUMENT,
+            "token_deviation: kv width not divisible by head count");
+    DeviceGuard g(reuse->e->device);
+    rk_engine* e = reuse->e;
+    if (reuse->async) RK_CUDA(cudaStreamSynchronize(reuse->xfer));
+    if (full->async) RK_CUDA(cudaStreamSynchronize(full->xfer));
+    const size_t n = reuse->n, L = reuse->L;
+    DevBuf out(4 * n * L * sizeof(double));
+    k::token_deviation(e->stream, reuse->k_pre.p, reuse->v.p, full->k_pre.p, full->v.p, reuse->elem, (int)L, (int)n,
+                       (int)reuse->kv(), (int)reuse->Hkv, out.as<double>());
+    e->launches += 1;
+    double* dst[4] = {value_cos, key_cos, value_norm, key_norm};
+    for (int m = 0; m < 4; ++m)
+      if (dst[m])
+        RK_CUDA(cudaMemcpyAsync(dst[m], out.as<double>() + m * n * L, n * L * sizeof(double), cudaMemcpyDeviceToHost,
+                                e->stream));
+    RK_CUDA(cudaStreamSynchronize(e->stream));
+  });
+}
+
+namespace {
+void put_curve(const prof::Curve& c, double* s, double* rho, uint8_t* deg) {
+  for (size_t l = 0; l < c.s.size(); ++l) {
+    if (s) s[l] = c.s[l];
+    if (rho) rho[l] = c.rho[l];
+    if (deg) deg[l] = c.deg[l];
+  }
+}
+}  // namespace
+
+int rk_layer_curve(const double* value_cos, uint64_t n, uint64_t L, double* s, double* rho, uint8_t* deg) {
+  return guard([&] {
+    require(value_cos != nullptr || n * L == 0, RK_ERR_INVALID_ARGUMENT, "null deviation matrix");
+    put_curve(prof::layer_curve(value_cos, n, L), s, rho, deg);
+  });
+}
+
+int rk_average_curves(const double* s, const double* rho, const uint8_t* deg, uint64_t k, uint64_t L, double* s_out,
+                      double* rho_out, uint8_t* deg_out) {
+  return guard([&] {
+    std::vector<prof::Curve> cs(k);
+    for (uint64_t i = 0; i < k; ++i) {
+      cs[i].s.assign(s + i * L, s + (i + 1) * L);
+      cs[i].rho.assign(rho + i * L, rho + (i + 1) * L);
+      cs[i].deg.assign(deg + i * L, deg + (i + 1) * L);
+    }
+    put_curve(prof::average(cs), s_out, rho_out, deg_out);
+  });
+}
+
+int rk_profile_from_curve(const double* s, const double* rho, const uint8_t* deg, uint64_t L,
+                          const rk_profiler_params* params, rk_profile_result* out, double* curve_rho_out) {
+  return guard([&] {
+    require(s && rho && deg && params && out, RK_ERR_INVALID_ARGUMENT, "null argument");
+    prof::Curve c;
+    c.s.assign(s, s + L);
+    c.rho.assign(rho, rho + L);
+    c.deg.assign(deg, deg + L);
+    std::vector<double> crho;
+    *out = prof::from_curve(c, *params, &crho);
+    if (curve_rho_out) std::copy(crho.begin(), crho.end(), curve_rho_out);
+  });
+}
+
+int rk_profile_model(rk_engine* e, rk_weights* w, const rk_two_stage_config* calib, const rk_profiler_params* params,
+                     rk_profile_result* out, double* curve_s, double* curve_rho) {
+  return guard([&] {
+    require(e && w && calib && params && out, RK_ERR_INVALID_ARGUMENT, "null argument");
+    prof::validate_params(*params);
+    prof::validate_calib(*calib);
+    DeviceGuard g(e->device);
+    const rk_model_spec& spec = w->s;
+    const size_t L = spec.num_layers, V = spec.vocab_size;
+    struct CacheDel {
+      void operator()(rk_cache* c) const { rk_cache_destroy(c); }
+    };
+    std::vector<prof::Curve> curves;
+    std::vector<float> logits(V);
+    for (uint64_t i = 0; i < calib->instances; ++i) {
+      try {
+        // make_two_stage_instance (metrics.cpp:280-322)
+        const uint64_t seed = calib->seed + 0x9e37u * (i + 1);
+        const size_t p1 = prof::pick_length(seed, 11, calib->stage1_prefix_min, calib->stage1_prefix_max);
+        const std::vector<int32_t> pre1 = prof::synthetic_tokens(seed, 21, p1, V);
+        const std::vector<int32_t> pre2 =
+            calib->identical_prefix
+                ? pre1
+                : prof::synthetic_tokens(seed, 22,
+                                         prof::pick_length(seed, 12, calib->stage2_prefix_min, calib->stage2_prefix_max),
+                                         V);
+        auto make_ctx = [&] {
+          auto c = std::make_unique<rk_context>();
+          c->e = e;
+          c->w = w;
+          c->elem = w->elem;
+          return c;
+        };
+        // stage 1: prompt prefill, then greedy decode of the segment with capture
+        auto ctx1 = make_ctx();
+        std::unique_ptr<rk_cache, CacheDel> reuse, full;
+        {
+          Runner r(e, w);
+          r.prefill(ctx1.get(), pre1.data(), pre1.size(), 0, true);
+          r.finish();
+          r.download_logits(logits.data());
+        }
+        {
+          Runner r(e, w);
+          reuse.reset(r.capture_decode(ctx1.get(), logits.data(), calib->segment_len, calib->snapshot_layer, false));
+          r.finish();
+        }
+        // full side: prefill of (stage-2 prefix + segment), pre-RoPE keys of
+        // the segment rows (build_comparison_setting kDecoding, metrics.cpp:336-352)
+        auto ctx2 = make_ctx();
+        {
+          Runner r(e, w);
+          r.prefill(ctx2.get(), pre2.data(), pre2.size(), 0, false);
+          full.reset(r.capture_prefill(ctx2.get(), reuse->host_tokens.data(), reuse->n, calib->snapshot_layer, false));
+          r.finish();
+        }
+        const size_t n = reuse->n;
+        std::vector<double> vc(n * L);
+        const int st = rk_token_deviation(reuse.get(), full.get(), vc.data(), nullptr, nullptr, nullptr);
+        if (st != RK_OK) raise(st, rk_last_error());
+        curves.push_back(prof::layer_curve(vc.data(), n, L));
+      } catch (const Error& ex) {
+        raise(RK_ERR_RUNTIME, "calibration instance " + std::to_string(i) + ": " + ex.what());
+      }
+    }
+    const prof::Curve avg = prof::average(curves);
+    std::vector<double> crho;
+    *out = prof::from_curve(avg, *params, &crho);
+    if (curve_s) std::copy(avg.s.begin(), avg.s.end(), curve_s);
+    if (curve_rho) std::copy(crho.begin(), crho.end(), curve_rho);
+  });
+}

@@ -252,6 +252,9 @@ void select_relay(cudaStream_t s, const double* s_dev, const float* influence,
                   const double* infl_mean, int n, double tau_dev, double tau_inf, int suffix_k,
                   int* sel_idx, uint32_t* sel_tags, int* info, double* dinfo, cudaStream_t side = nullptr,
                   cudaEvent_t fork = nullptr, cudaEvent_t join = nullptr);
+// offline profiler: token_deviation (metrics.cpp:118-159); out [4][n][L]
+void token_deviation(cudaStream_t s, const void* reuse_k, const void* reuse_v, const void* full_k,
+                     const void* full_v, size_t elem, int L, int n, int kv, int heads, double* out);
 void blend_scores(cudaStream_t s, const void* ctx_v, const void* cache_v, size_t elem, int n,
                   int kv, double* score);
 void select_topk(cudaStream_t s, const double* score, int n, int count, int* sel_idx,

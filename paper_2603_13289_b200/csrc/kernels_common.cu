@@ -946,6 +946,68 @@ void realign_graft(cudaStream_t s, const void* k_pre, const void* v_src, size_t 
 #undef RK_REALIGN_DH
 }
 
+// ---------------------------------------------------------------------------
+// Offline profiler: token_deviation (metrics.cpp:118-159) on the device. For
+// every (position j, layer l) and both V and K_pre rows of the reuse-side and
+// the full-prefill cache: mean-over-heads cosine deviation (cosine_d,
+// metrics.cpp:21-32) and norm-ratio deviation (norm_ratio_d, 40-46), in the
+// reference's sequential double order. One CTA per (j, l), one thread per
+// (row kind, head); heads are summed in order. out: [4][n][L] doubles
+// (value_cos, key_cos, value_norm, key_norm), row-major [position][layer].
+// ---------------------------------------------------------------------------
+__global__ void token_deviation_kernel(const void* rk, const void* rv, const void* fk, const void* fv, size_t elem,
+                                       int L, int n, int kv, int heads, double* out) {
+  extern __shared__ double dsh[];  // [2 kinds][heads][cos, ratio]
+  const int j = blockIdx.x / L, l = blockIdx.x % L;
+  const int dh = kv / heads;
+  const size_t rowi = ((size_t)l * n + j) * kv;
+  for (int t = threadIdx.x; t < 2 * heads; t += blockDim.x) {
+    const int which = t / heads, h = t % heads;  // 0 = V, 1 = K_pre
+    const void* a = which == 0 ? rv : rk;  // reuse side (metrics.cpp:151-154: a = reuse, b = full)
+    const void* b = which == 0 ? fv : fk;
+    const size_t ai = rowi + (size_t)h * dh;
+    double dot = 0.0, na = 0.0, nb = 0.0;
+    bool same = true;
+    for (int i = 0; i < dh; ++i) {
+      const float x = load_elem(a, ai + i, elem), y = load_elem(b, ai + i, elem);
+      same = same && __float_as_uint(x) == __float_as_uint(y);
+      const double xd = x, yd = y;
+      dot = __dadd_rn(dot, __dmul_rn(xd, yd));
+      na = __dadd_rn(na, __dmul_rn(xd, xd));
+      nb = __dadd_rn(nb, __dmul_rn(yd, yd));
+    }
+    const double sa = __dsqrt_rn(na), sb = __dsqrt_rn(nb);
+    double c;
+    if (sa < 1e-12 || sb < 1e-12) c = 0.0;
+    else if (same) c = 1.0;
+    else {
+      c = __ddiv_rn(dot, __dmul_rn(sa, sb));
+      c = c < -1.0 ? -1.0 : (c > 1.0 ? 1.0 : c);
+    }
+    const double hi = sa > sb ? sa : sb, lo = sa > sb ? sb : sa;
+    const double ratio = hi < 1e-12 ? 1.0 : __ddiv_rn(lo, hi);
+    dsh[(which * heads + h) * 2] = c;
+    dsh[(which * heads + h) * 2 + 1] = ratio;
+  }
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    const int which = threadIdx.x & 1, metric = threadIdx.x >> 1;  // metric 0 cos, 1 ratio
+    double acc = 0.0;
+    for (int h = 0; h < heads; ++h) acc = __dadd_rn(acc, dsh[(which * heads + h) * 2 + metric]);
+    // out planes: 0 value_cos, 1 key_cos, 2 value_norm, 3 key_norm
+    out[((size_t)(metric * 2 + which) * n + j) * L + l] = __dsub_rn(1.0, __ddiv_rn(acc, (double)heads));
+  }
+}
+
+void token_deviation(cudaStream_t s, const void* reuse_k, const void* reuse_v, const void* full_k,
+                     const void* full_v, size_t elem, int L, int n, int kv, int heads, double* out) {
+  if (n <= 0 || L <= 0) return;
+  const int threads = std::max(32, ((2 * heads + 31) / 32) * 32);
+  token_deviation_kernel<<<n * L, threads, (size_t)4 * heads * sizeof(double), s>>>(reuse_k, reuse_v, full_k, full_v,
+                                                                                   elem, L, n, kv, heads, out);
+  RK_CUDA(cudaGetLastError());
+}
+
 void score_deviation(cudaStream_t s, const void* ctx_v, const void* cache_v, const void* ctx_k,
                      const void* cache_kpre, size_t elem, int n, int kv, int heads, int dh,
                      const double2* rope, int base, double* s_dev, double* s_key) {

@@ -256,3 +256,55 @@ def test_rkrc_loaded_cache_relays_like_uploaded(engine, oracle):
                                     case["opts"])
     assert_outputs_equal(got, want, "rkrc.relay")
     assert_bit_equal(got["logits"], want["logits"], "rkrc.relay.logits")
+
+
+def test_token_deviation_bit_exact(engine, oracle):
+    """token_deviation (metrics.cpp:118-159) on the device == the reference's,
+    all four planes, bit for bit; identical caches give exact zeros."""
+    from oracle.oracle import Oracle, available
+    if not available("reference"):
+        pytest.skip("oracle/_ref not built")
+    ref = Oracle("reference")
+    from paper_2603_13289_b200.profiler import token_deviation
+    spec = spec_of(6, 64, 4, kv_heads=2)
+    ow = oracle.weights(spec, 5)
+    a = oracle.scenario(ow, pattern_tokens(9, 64, 1), 16, 1)
+    b = oracle.scenario(ow, pattern_tokens(13, 64, 2), 16, 1)
+    w = engine.weights(spec, 5)
+    got = token_deviation(w.upload_cache(a), w.upload_cache(b))
+    want = ref.token_deviation(a, b)
+    for k in want:
+        assert_bit_equal(got[k], want[k], f"token_deviation.{k}")
+    zero = token_deviation(w.upload_cache(a), w.upload_cache(a))
+    for k in zero:
+        assert (zero[k] == 0.0).all(), k
+
+
+@pytest.mark.parametrize("identical", [False, True])
+def test_profile_model_bit_exact(engine, identical):
+    """profile_model (profiler.cpp:157-175) with the captures, prefills and
+    deviations on the device: same window, same fallbacks, bit-identical
+    averaged curves as the reference run on the CPU."""
+    from oracle.oracle import Oracle, available
+    if not available("reference"):
+        pytest.skip("oracle/_ref not built")
+    ref = Oracle("reference")
+    from paper_2603_13289_b200.profiler import ProfilerParams, TwoStageConfig, profile_model
+    spec = spec_of(8, 32, 4)
+    calib = TwoStageConfig.make(seed=3, instances=3, stage1_prefix=(8, 16), stage2_prefix=(6, 18), segment_len=12,
+                                identical_prefix=identical, snapshot_layer=1)
+    params = ProfilerParams.make(tau_start=0.95)
+    got = profile_model(engine.weights(spec, 77), calib, params)
+    want = ref.profile_model(ref.weights(spec, 77), calib, params)
+    for k in ("l_start", "l_det", "l_end", "end_fallback", "det_fallback"):
+        assert got[k] == want[k], (k, got, want)
+    assert_bit_equal(got["curve_s"], want["curve_s"], "curve_s")
+    assert_bit_equal(got["curve_rho"], want["curve_rho"], "curve_rho")
+
+
+def test_profile_model_bf16_runs(engine):
+    from paper_2603_13289_b200.profiler import TwoStageConfig, profile_model
+    spec = spec_of(8, 256, 4)
+    got = profile_model(engine.weights(spec, 9, "bf16"), TwoStageConfig.make(instances=2, segment_len=16))
+    assert got["l_start"] <= got["l_det"] <= got["l_end"] < 8
+    assert np.isfinite(got["curve_s"]).all()
