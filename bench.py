@@ -380,8 +380,11 @@ def run_ours(args, world, rank, local, dist):
             c.wait()
         del ups
     upload_ms = (time.perf_counter() - h0) * 1e3 / e2e_K
-    h2d = sum(h.k_pre.nbytes + h.v.nbytes + h.hidden_snapshot.nbytes + h.influence.nbytes + h.segment_tokens.nbytes
-              for h in hosts) + 4 * (WL["prefix"] + WL["suffix"])
+    # bytes that cross PCIe: fp32 K/V, unless RK_HOST_CONVERT=1 converts them
+    # to bf16 on the host first (rk_cache_upload_async), then half of that
+    kv_div = 2 if os.environ.get("RK_HOST_CONVERT", "0") != "0" else 1
+    h2d = sum((h.k_pre.nbytes + h.v.nbytes) // kv_div + h.hidden_snapshot.nbytes + h.influence.nbytes +
+              h.segment_tokens.nbytes for h in hosts) + 4 * (WL["prefix"] + WL["suffix"])
     d2h = 4 * WL["spec"]["vocab_size"] + 4
 
     # per-kernel instrumentation pass (same step, CUDA events per launch)

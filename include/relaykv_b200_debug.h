@@ -34,6 +34,8 @@ int rk_debug_select_relay(rk_engine* e, const double* s_dev, const float* influe
                           int32_t* count, double* dinfo);
 /* y[i] = device glibc_expf(x[i]) */
 int rk_debug_expf(rk_engine* e, const float* x, float* y, uint64_t n);
+/* Host only: the upload path's fp32 -> bf16 conversion on a `threads`-worker pool. */
+int rk_debug_f32_to_bf16_host(const float* x, uint16_t* y, uint64_t n, int threads);
 #ifdef __cplusplus
 }
 #endif

@@ -232,4 +232,11 @@ int rk_debug_expf(rk_engine* e, const float* x, float* y, uint64_t n) {
   });
 }
 
+int rk_debug_f32_to_bf16_host(const float* x, uint16_t* y, uint64_t n, int threads) {
+  return guard([&] {
+    HostPool pool(threads);
+    pool.parallel_for(n, 4096, [&](size_t b, size_t e) { f32_to_bf16_host(x + b, y + b, e - b); });
+  });
+}
+
 }  // extern "C"

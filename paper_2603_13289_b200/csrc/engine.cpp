@@ -5,10 +5,15 @@
 // arithmetic runs in the CUDA kernels of kernels_*.cu / gemm_sm100.cu /
 // attn_sm100.cu. Compiled with -ffp-contract=off: the few float expressions
 // evaluated here (init scales, thresholds) must round as the reference's.
+#include <cuda.h>
+
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
+#include <future>
 #include <mutex>
+#include <thread>
 
 #include "internal.h"
 #include "layer.h"
@@ -157,6 +162,7 @@ rk_engine::~rk_engine() {
       cudaStreamSynchronize(x);
       cudaStreamDestroy(x);
     }
+  uploader.reset();  // drains queued conversion jobs
   if (side_fork) cudaEventDestroy(side_fork);
   if (side_join) cudaEventDestroy(side_join);
   if (stream) cudaStreamDestroy(stream);
@@ -355,6 +361,11 @@ int rk_engine_create(int device, rk_engine** out) {
     int prio_lo = 0, prio_hi = 0;
     RK_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     for (auto& x : e->xfer) RK_CUDA(cudaStreamCreateWithPriority(&x, cudaStreamNonBlocking, prio_hi));
+    {
+      const char* env = std::getenv("RK_HOST_THREADS");
+      int t = env ? std::atoi(env) : (int)std::min(16u, std::max(1u, std::thread::hardware_concurrency()));
+      e->host_pool = std::make_unique<HostPool>(std::max(1, t));
+    }
     RK_CUDA(cudaEventCreateWithFlags(&e->side_fork, cudaEventDisableTiming));
     RK_CUDA(cudaEventCreateWithFlags(&e->side_join, cudaEventDisableTiming));
     e->status.alloc(64);
@@ -493,6 +504,24 @@ void rk_weights_destroy(rk_weights* w) {
 
 // ---- relay caches ---------------------------------------------------------
 namespace {
+typedef CUresult (*PFN_waitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+// cuStreamWaitValue32 through the runtime's driver entry point (no libcuda link)
+PFN_waitValue32 wait_value_fn() {
+  static PFN_waitValue32 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return (PFN_waitValue32) nullptr;
+    }
+    return reinterpret_cast<PFN_waitValue32>(f);
+  }();
+  return fn;
+}
+inline uint32_t* c_flags_of(char* stage, uint64_t R, size_t slot) {
+  return reinterpret_cast<uint32_t*>(stage + R * slot);
+}
 // RelayCache::validate + upload (relay_cache.cpp:18-41). async: everything on
 // the copy stream with per-layer events, no host synchronization.
 rk_cache* upload_cache(rk_engine* e, rk_weights* w, const rk_relay_cache_view* v, bool async) {
@@ -548,6 +577,71 @@ rk_cache* upload_cache(rk_engine* e, rk_weights* w, const rk_relay_cache_view* v
     RK_CUDA(cudaEventCreateWithFlags(&c->ev_meta, cudaEventDisableTiming));
     RK_CUDA(cudaEventRecord(c->ev_meta, st));
     c->ev_layer.resize(c->L);
+  }
+  // bf16, asynchronous: the engine's uploader thread converts each layer to
+  // bf16 on the host worker pool into a ring of pinned slots and raises a
+  // per-layer flag; the copy stream waits on that flag (cuStreamWaitValue32)
+  // and moves half the fp32 bytes across PCIe. The conversion of layer l+R
+  // waits for the copy that frees its slot. The call returns at once.
+  // Opt-in (RK_HOST_CONVERT=1): on the 16-vCPU B200 hosts measured so far the
+  // conversion (72 GB/s alone, less next to the running step) is slower than
+  // letting PCIe carry fp32 (~50 GB/s) and converting on the device.
+  static const bool host_conv_env = [] {
+    const char* v = std::getenv("RK_HOST_CONVERT");
+    return v ? std::atoi(v) != 0 : false;
+  }();
+  if (async && c->elem == 2 && host_conv_env && wait_value_fn()) {
+    const uint64_t L = c->L, R = std::min<uint64_t>(L, 4);
+    const size_t cnt = n * kv, slot = 2 * cnt * 2;
+    c->stage_host = e->pinned_pool.acquire(R * slot + L * 4 + 64, &c->stage_host_bytes);
+    char* stage = static_cast<char*>(c->stage_host);
+    c->flags = reinterpret_cast<volatile uint32_t*>(stage + R * slot);
+    for (uint64_t l = 0; l < L; ++l) c->flags[l] = 0;
+    void* dflags = nullptr;
+    RK_CUDA(cudaHostGetDevicePointer(&dflags, const_cast<uint32_t*>(c->flags), 0));
+    auto release_all = [flags = c->flags, L] {
+      for (uint64_t l = 0; l < L; ++l) __atomic_store_n(const_cast<uint32_t*>(flags + l), 1u, __ATOMIC_SEQ_CST);
+    };
+    for (uint64_t l = 0; l < L; ++l) {
+      const uint16_t* sk = reinterpret_cast<const uint16_t*>(stage + (l % R) * slot);
+      const CUresult r = wait_value_fn()(st, reinterpret_cast<CUdeviceptr>(dflags) + 4 * l, 1u, CU_STREAM_WAIT_VALUE_GEQ);
+      if (r != CUDA_SUCCESS) {
+        release_all();  // nothing may stay blocked on a flag
+        raise(RK_ERR_RUNTIME, "cuStreamWaitValue32 failed: " + std::to_string((int)r));
+      }
+      RK_CUDA(cudaMemcpyAsync(static_cast<char*>(c->k_pre.p) + l * cnt * 2, sk, cnt * 2, cudaMemcpyHostToDevice, st));
+      RK_CUDA(cudaMemcpyAsync(static_cast<char*>(c->v.p) + l * cnt * 2, sk + cnt, cnt * 2, cudaMemcpyHostToDevice, st));
+      RK_CUDA(cudaEventCreateWithFlags(&c->ev_layer[l], cudaEventDisableTiming));
+      RK_CUDA(cudaEventRecord(c->ev_layer[l], st));
+    }
+    std::vector<const float*> ks(v->k_pre, v->k_pre + L), vs(v->v, v->v + L);
+    std::vector<cudaEvent_t> evs = c->ev_layer;
+    HostPool* pool = e->host_pool.get();
+    auto task = std::make_shared<std::packaged_task<void()>>([=] {
+      try {
+        for (uint64_t l = 0; l < L; ++l) {
+          if (l >= R && cudaEventSynchronize(evs[l - R]) != cudaSuccess) break;  // slot l % R is free
+          uint16_t* dk = reinterpret_cast<uint16_t*>(stage + (l % R) * slot);
+          const float* srck = ks[l];
+          const float* srcv = vs[l];
+          pool->parallel_for(2 * cnt, size_t{1} << 16, [&](size_t b, size_t end) {
+            if (b < cnt) f32_to_bf16_host(srck + b, dk + b, std::min(end, cnt) - b);
+            if (end > cnt) {
+              const size_t b2 = b > cnt ? b - cnt : 0;
+              f32_to_bf16_host(srcv + b2, dk + cnt + b2, end - cnt - b2);
+            }
+          });
+          std::atomic_thread_fence(std::memory_order_seq_cst);
+          __atomic_store_n(const_cast<uint32_t*>(c_flags_of(stage, R, slot) + l), 1u, __ATOMIC_SEQ_CST);
+        }
+      } catch (...) {
+      }
+      release_all();  // (no-op when every layer went through)
+    });
+    c->conv_done = task->get_future().share();
+    if (!e->uploader) e->uploader = std::make_unique<Uploader>(e->device);
+    e->uploader->submit([task] { (*task)(); });
+    return c.release();
   }
   // bf16: each fp32 layer lands in a staging buffer and is converted on the
   // device; two staging buffers alternate (stream order keeps them safe, no
@@ -736,6 +830,8 @@ int rk_cache_file_read(const char* path, rk_cache_file** out, rk_relay_cache_vie
 void rk_cache_file_free(rk_cache_file* f) { delete f; }
 
 rk_cache::~rk_cache() {
+  if (conv_done.valid()) conv_done.wait();  // the uploader job is done with the staging ring and events
+  if (stage_host) e->pinned_pool.release(stage_host, stage_host_bytes);
   if (ev_meta) cudaEventDestroy(ev_meta);
   for (cudaEvent_t ev : ev_layer)
     if (ev) cudaEventDestroy(ev);

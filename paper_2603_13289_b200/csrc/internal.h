@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <future>
 #include <map>
 #include <memory>
 #include <stdexcept>
@@ -12,6 +13,7 @@
 #include <utility>
 #include <vector>
 
+#include "hostconv.h"
 #include "relaykv_b200.h"
 
 namespace rk {
@@ -88,6 +90,9 @@ struct rk_engine {
   static constexpr int kXfer = 4;
   cudaStream_t xfer[kXfer] = {};
   int next_xfer = 0;
+  std::unique_ptr<rk::HostPool> host_pool;
+  std::unique_ptr<rk::Uploader> uploader;
+  rk::PinnedPool pinned_pool;
   uint64_t launches = 0;
   int use_graphs = 0;
   int fused = 1;  // layer-major fused agent schedule (runner.cpp agent_fused)
@@ -154,6 +159,13 @@ struct rk_cache {
   cudaEvent_t ev_meta = nullptr;
   std::vector<cudaEvent_t> ev_layer;
   rk::DevBuf staging;  // fp32 layer staging of the bf16 conversion
+  // host-converted upload (bf16 weights, async): the engine's uploader thread
+  // converts layer l into a ring of pinned bf16 slots and sets flags[l]; the
+  // copy stream waits on the flag (cuStreamWaitValue32) before copying it
+  void* stage_host = nullptr;
+  size_t stage_host_bytes = 0;
+  volatile uint32_t* flags = nullptr;  // in stage_host, [L]
+  std::shared_future<void> conv_done;
   std::shared_ptr<void> host_keep;  // host source of an async upload owned by the cache (rk_cache_load)
   size_t kv() const { return Hkv * dh; }
   ~rk_cache();

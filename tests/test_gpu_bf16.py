@@ -111,3 +111,47 @@ def test_bf16_nonunit_norm_gains(engine, oracle):
                                         RelayOptions.make(suffix_k=4))
         res[prec] = out["logits"]
     assert rel(res["bf16"], res["fp32"]) < 5e-2
+
+
+def test_async_upload_bf16_bit_exact(engine, oracle):
+    """bf16 weights: asynchronous (layer-streamed) and synchronous uploads give
+    the same caches and logits."""
+    from tests.scenarios import pattern_tokens, spec_of, triple
+    from paper_2603_13289_b200.abi import RelayOptions
+    spec = spec_of(6, 256, 4, kv_heads=2)
+    ow = oracle.weights(spec, 31)
+    c1 = oracle.scenario(ow, pattern_tokens(9, 64, 1), 40, 1)
+    c2 = oracle.scenario(ow, pattern_tokens(7, 64, 2), 33, 1)
+    res, caches = [], []
+    for asynchronous in (False, True):
+        w = engine.weights(spec, 31, "bf16")
+        ups = [w.upload_cache(c, asynchronous=asynchronous) for c in (c1, c2)]
+        out = w.context().agent_prefill(pattern_tokens(5, 64, 3), ups, pattern_tokens(4, 64, 4), triple(1, 2, 4),
+                                        RelayOptions.make(suffix_k=3))
+        res.append(out["logits"])
+        caches.append([u.to_host() for u in ups])
+    for a, b in zip(caches[0], caches[1]):
+        assert np.array_equal(a.k_pre.view(np.uint32), b.k_pre.view(np.uint32))
+        assert np.array_equal(a.v.view(np.uint32), b.v.view(np.uint32))
+    assert np.array_equal(res[0].view(np.uint32), res[1].view(np.uint32))
+
+
+def test_async_upload_host_conversion_subprocess():
+    """The opt-in host-side conversion (RK_HOST_CONVERT=1: uploader thread,
+    worker pool, pinned bf16 ring, cuStreamWaitValue32 per layer) gives the
+    same bits as the device conversion."""
+    import os
+    import subprocess
+    import sys
+    code = f"""
+import sys
+sys.path.insert(0, {os.getcwd()!r})
+from paper_2603_13289_b200.engine import Engine
+from oracle.oracle import Oracle
+from tests.test_gpu_bf16 import test_async_upload_bf16_bit_exact
+test_async_upload_bf16_bit_exact(Engine(0), Oracle("restatement"))
+print("ok")
+"""
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, RK_HOST_CONVERT="1"), capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
