@@ -45,13 +45,21 @@ constexpr int kThreads = 192;
 // 256 x BN tile; each CTA stages its own 128 rows of A and HALF of the BN rows
 // of B, so a CTA's shared-memory fill per k-block drops from 48 KB to 32 KB
 // (BN=256) -- the L2->SM feed, not the tensor pipe, bounds the 1-CTA kernel.
-template <int BN, int PAIR = 1>
+//
+// MT > 1 (short M, <= MT*128 rows): one CTA computes all MT m-tiles of its N
+// tile, so each weight (B) tile is staged by exactly one SM instead of MT --
+// for the prefix/suffix-only layers the weight stream, not the tiny A, is the
+// traffic. MT accumulators of BN columns each (single-buffered when 2 do not fit).
+constexpr int pow2_cols(int c) { return c <= 32 ? 32 : (c <= 64 ? 64 : (c <= 128 ? 128 : (c <= 256 ? 256 : 512))); }
+template <int BN, int PAIR = 1, int MT = 1>
 struct Cfg {
-  static constexpr int A_BYTES = kBM * kBK * 2;
+  static constexpr int A_BYTES = MT * kBM * kBK * 2;
   static constexpr int B_BYTES = BN / PAIR * kBK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = PAIR == 1 ? ((BN == 256) ? 4 : (BN == 128 ? 6 : 8)) : (BN == 256 ? 6 : 8);
-  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+  static constexpr int STAGES = MT > 1 ? (192 * 1024) / STAGE_BYTES
+                                       : PAIR == 1 ? ((BN == 256) ? 4 : (BN == 128 ? 6 : 8)) : (BN == 256 ? 6 : 8);
+  static constexpr int NACC = 2 * MT * BN <= 512 ? 2 : 1;  // TMEM accumulator buffers
+  static constexpr int TMEM_COLS = pow2_cols(NACC * MT * BN);
   // per epilogue warp: a 32x32 fp32 staging tile for the coalesced residual epilogue
   static constexpr int EPI_STAGE = 4 * 32 * 32 * 4;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + EPI_STAGE;
@@ -62,11 +70,12 @@ struct Units {
   int total;
 };
 
-template <int PAIR = 1>
+template <int PAIR = 1, int MT = 1>
 __device__ __forceinline__ Units units_of(const GemmArgs& p) {
   Units u;
   const int M = p.rows_dev ? *p.rows_dev : p.rows_max;
-  u.num_m = (M + kBM * PAIR - 1) / (kBM * PAIR);  // m tiles of 128 (or 256-row pair tiles)
+  // m tiles of 128 (or 256-row pair tiles); one group of MT tiles when MT > 1
+  u.num_m = MT > 1 ? (M > 0 ? 1 : 0) : (M + kBM * PAIR - 1) / (kBM * PAIR);
   u.num_n = p.N / p.bn;
   // live row count known only on the device: pick split-K here (grid = all SMs)
   u.splits = p.splits;
@@ -312,11 +321,11 @@ __device__ __forceinline__ void csk_epilogue(const GemmArgs& p, const Units& U, 
   }
 }
 
-template <int BN, int EPI, int PAIR, bool CSK = false>
+template <int BN, int EPI, int PAIR, bool CSK = false, int MT = 1>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const GemmArgs p) {
-  using C = Cfg<BN, PAIR>;
+  using C = Cfg<BN, PAIR, MT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
@@ -327,7 +336,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* epi_stage = smem + C::STAGES * C::STAGE_BYTES + 256;  // [4 warps][32 rows][128 B]
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const Units U = units_of<PAIR>(p);
+  const Units U = units_of<PAIR, MT>(p);
   const uint32_t rank = PAIR == 2 ? cluster_ctarank() : 0;  // 0 = leader (issues the MMAs)
 
   if (warp == 0 && lane == 0) {
@@ -358,9 +367,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       Work w;
+      const int pf = p.prefetch;
       for (int it = 0; get_work<PAIR>(U, p.streamk, it, w); ++it) {
         const int mt = w.mt, nt = w.nt, kb0 = w.kb0, kb1 = w.kb1;
+        const int bcol = nt * BN + rank * (BN / PAIR);
+        for (int kb = kb0; kb < kb0 + pf && kb < kb1; ++kb) tma_prefetch_2d(&tmB, kb * kBK, bcol);
         for (int kb = kb0; kb < kb1; ++kb) {
+          if (pf && kb + pf < kb1) tma_prefetch_2d(&tmB, (kb + pf) * kBK, bcol);  // weights: L2 ahead of the ring
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
           const bool same = p.dbg & 1;
@@ -372,7 +385,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_2d_pair(sa + C::A_BYTES, &tmB, &full[stage], kx, bn_ * BN + rank * (BN / 2));
           } else {
             mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-            tma_load_2d(sa, &tmA, &full[stage], kx, am * kBM);
+#pragma unroll
+            for (int mi = 0; mi < MT; ++mi)
+              tma_load_2d(sa + mi * kBM * kBK * 2, &tmA, &full[stage], kx, (am * MT + mi) * kBM);
             tma_load_2d(sa + C::A_BYTES, &tmB, &full[stage], kx, bn_ * BN);
           }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
@@ -388,24 +403,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       Work w;
       for (int it = 0; get_work<PAIR>(U, p.streamk, it, w); ++it, ++local) {
         const int kb0 = w.kb0, kb1 = w.kb1;
-        const int acc = local & 1;
-        mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);
+        const int acc = local % C::NACC;
+        mbar_wait(&tempty[acc], ((local / C::NACC) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d = tmem + acc * BN;
+        const uint32_t d = tmem + acc * MT * BN;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a0 = smem_u32(smem + stage * C::STAGE_BYTES);
           const uint32_t b0 = a0 + C::A_BYTES;
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k) {
-            if (p.dbg & 2) break;
-            if constexpr (PAIR == 2)
-              mma_bf16_ss_pair(d, sdesc_sw128(a0 + k * 32, 16, 1024), sdesc_sw128(b0 + k * 32, 16, 1024), idesc,
-                               (kb > kb0 || k > 0) ? 1u : 0u);
-            else
-              mma_bf16_ss(d, sdesc_sw128(a0 + k * 32, 16, 1024), sdesc_sw128(b0 + k * 32, 16, 1024), idesc,
-                          (kb > kb0 || k > 0) ? 1u : 0u);
+          for (int mi = 0; mi < MT; ++mi) {
+#pragma unroll
+            for (int k = 0; k < kBK / 16; ++k) {
+              if (p.dbg & 2) break;
+              const uint32_t am = a0 + mi * kBM * kBK * 2 + k * 32;
+              if constexpr (PAIR == 2)
+                mma_bf16_ss_pair(d, sdesc_sw128(am, 16, 1024), sdesc_sw128(b0 + k * 32, 16, 1024), idesc,
+                                 (kb > kb0 || k > 0) ? 1u : 0u);
+              else
+                mma_bf16_ss(d + mi * BN, sdesc_sw128(am, 16, 1024), sdesc_sw128(b0 + k * 32, 16, 1024), idesc,
+                            (kb > kb0 || k > 0) ? 1u : 0u);
+            }
           }
           if constexpr (PAIR == 2) tc_commit_pair(&empty[stage]);
           else tc_commit(&empty[stage]);
@@ -427,8 +446,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     int local = 0;
     Work w;
     for (int it = 0; get_work<PAIR>(U, p.streamk, it, w); ++it, ++local) {
-      const int mt = w.mt * PAIR + rank, nt = w.nt, s = w.s;  // this CTA's 128-row tile
-      const int acc = local & 1;
+      const int acc = local % C::NACC, use = local / C::NACC;
+#pragma unroll 1
+      for (int mi = 0; mi < MT; ++mi) {
+      const int mt = (w.mt * PAIR + rank) * MT + mi, nt = w.nt, s = w.s;  // this CTA's 128-row tile
+      const uint32_t acol = (uint32_t)((acc * MT + mi) * BN);  // its accumulator's first TMEM column
       const int row = mt * kBM + quarter * 32 + lane;
       int* flag = nullptr;
       if (EPI == EPI_ADD && U.splits > 1) {  // ordered split-K: wait for split s-1 on these rows
@@ -455,7 +477,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         float4 hb[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) hb[i] = (row0 + 4 * i + sub < M) ? __ldcg(hptr(i, 0)) : make_float4(0.f, 0.f, 0.f, 0.f);
-        mbar_wait(&tfull[acc], (local >> 1) & 1);
+        mbar_wait(&tfull[acc], use & 1);
         tc_fence_after();
         float ss[8];
 #pragma unroll
@@ -463,7 +485,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
           uint32_t r[32];
-          tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN + c, r);
+          tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + acol + c, r);
           tmem_ld_wait();
           __syncwarp();  // previous chunk's read-back of T is done
 #pragma unroll
@@ -525,27 +547,28 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       } else {
-        mbar_wait(&tfull[acc], (local >> 1) & 1);
+        mbar_wait(&tfull[acc], use & 1);
         tc_fence_after();
         const float rs = (p.row_scale && row < M) ? p.row_scale[row] : 1.0f;
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
           uint32_t r[32];
-          tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + acc * BN + c, r);
+          tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + acol + c, r);
           tmem_ld_wait();
           if (row < M) epilogue_chunk<EPI>(p, row, nt * BN + c, r, rs, s);
         }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if constexpr (PAIR == 2) mbar_arrive_cluster(&tempty[acc], 0);
-        else mbar_arrive(&tempty[acc]);
       }
       if (flag) {
         __threadfence();
         __syncwarp();
         if (lane == 0) atomicExch(flag, s + 1 == U.splits ? 0 : s + 1);
+      }
+      }  // m tiles of the group
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (PAIR == 2) mbar_arrive_cluster(&tempty[acc], 0);
+        else mbar_arrive(&tempty[acc]);
       }
     }
   }
@@ -592,11 +615,18 @@ __device__ __forceinline__ void splitk_reduce_row(const GemmArgs& p, int splits,
         acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
       }
     } else {
-      acc = __ldcg(reinterpret_cast<const float4*>(p.ws_part + (size_t)row * p.N) + c);
-      for (int s = 1; s < splits; ++s) {
-        const float4 v = __ldcg(reinterpret_cast<const float4*>(p.ws_part + ((size_t)s * p.rows_max + row) * p.N) + c);
-        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-      }
+      // all partials in flight at once, then summed in split order
+      float4 v[8];
+#pragma unroll
+      for (int s = 0; s < 8; ++s)
+        if (s < splits)
+          v[s] = __ldcg(reinterpret_cast<const float4*>(p.ws_part + ((size_t)s * p.rows_max + row) * p.N) + c);
+      acc = v[0];
+#pragma unroll
+      for (int s = 1; s < 8; ++s)
+        if (s < splits) {
+          acc.x += v[s].x; acc.y += v[s].y; acc.z += v[s].z; acc.w += v[s].w;
+        }
     }
     float4 x = h[c];
     x.x += acc.x; x.y += acc.y; x.z += acc.z; x.w += acc.w;
@@ -607,7 +637,7 @@ __device__ __forceinline__ void splitk_reduce_row(const GemmArgs& p, int splits,
     }
   }
   if (p.norm_inv) {
-    __shared__ float red[8];
+    __shared__ float red[32];
     for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
     __syncthreads();
@@ -632,12 +662,12 @@ __global__ void __launch_bounds__(256) splitk_reduce_add_kernel(const GemmArgs p
     splitk_reduce_row(p, splits, row, U, G, sk_tab);
 }
 
-template <int BN, int EPI, int PAIR, bool CSK = false>
+template <int BN, int EPI, int PAIR, bool CSK = false, int MT = 1>
 void launch(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& p, int grid) {
-  using C = Cfg<BN, PAIR>;
+  using C = Cfg<BN, PAIR, MT>;
   static bool attr = false;
   if (!attr) {
-    RK_CUDA(cudaFuncSetAttribute(gemm_bf16_kernel<BN, EPI, PAIR, CSK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    RK_CUDA(cudaFuncSetAttribute(gemm_bf16_kernel<BN, EPI, PAIR, CSK, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  C::SMEM));
     attr = true;
   }
@@ -656,7 +686,7 @@ void launch(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const G
     cfg.numAttrs = 1;
     RK_CUDA(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<BN, EPI, 1, true>, a, b, p));
   } else if constexpr (PAIR == 1) {
-    gemm_bf16_kernel<BN, EPI, 1><<<grid, kThreads, C::SMEM, st>>>(a, b, p);
+    gemm_bf16_kernel<BN, EPI, 1, false, MT><<<grid, kThreads, C::SMEM, st>>>(a, b, p);
   } else {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
@@ -683,6 +713,14 @@ void launch_bn(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, cons
       else launch<64, EPI_ADD, 1, true>(st, a, b, p, grid);
       return;
     }
+  }
+  if (p.mt_group == 3) {
+    launch<128, EPI, 1, false, 3>(st, a, b, p, grid);
+    return;
+  }
+  if (p.mt_group == 2) {
+    launch<128, EPI, 1, false, 2>(st, a, b, p, grid);
+    return;
   }
   if (p.pair == 2) {
     if (p.bn == 256) launch<256, EPI, 2>(st, a, b, p, grid);
@@ -784,109 +822,109 @@ void make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t c
   if (r != CUDA_SUCCESS) raise(RK_ERR_RUNTIME, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
 }
 
-// Pick the CTA shape (single CTA with 128-row tiles, or a CTA pair with
-// 256-row tiles), the N tile and the split count so the grid fills the GPU:
-// the widest tile that still gives a full wave of units, else BN=64; split-K
-// only for residual GEMMs that cannot fill the GPU.
+// Pick the kernel shape for one GEMM with a small cost model calibrated on
+// B200 (time per k-block of one unit, by the bytes a CTA stages per k-block:
+// ~0.0096 us per KB, the L2->SM feed; 1-CTA 128x256 tile = 48 KB = 0.46 us,
+// pair = 0.42 us) times the rounds of units over the concurrent slots:
+//  - 1-CTA 128xBN tiles (the widest BN that still fills the SMs), or
+//  - CTA pairs (256-row tiles), when M >= 640 and the rounds allow, or
+//  - m-grouped tiles (MT = 2/3 m tiles per CTA, BN 128) for short M, or
+//  - for residual GEMMs that cannot fill the GPU, split-K over any of the
+//    1-CTA shapes: EPI_PART partials reduced in split order by
+//    splitk_reduce_add_kernel (+ ~3 us and 2*s*M*N*4 B at ~8 TB/s), or the
+//    opt-in cluster (DSMEM) reduction / stream-K.
 static void choose_config(GemmArgs& p, int sm_count, int rows_hint) {
-  static const int pair_env = [] {
-    const char* v = std::getenv("RK_GEMM_PAIR");
-    return v ? std::atoi(v) : 1;
-  }();
-  static const int dbg_env = [] {
-    const char* v = std::getenv("RK_GEMM_DBG");
-    return v ? std::atoi(v) : 0;
-  }();
+  auto env = [](const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v ? std::atoi(v) : dflt;
+  };
+  static const int pf_env = env("RK_GEMM_PREFETCH", 0);  // opt-in: slower on c2 (measured)
+  p.prefetch = pf_env;
+  static const int pair_env = env("RK_GEMM_PAIR", 1), dbg_env = env("RK_GEMM_DBG", 0),
+                   csk_env = env("RK_GEMM_CSK", 0), mm_env = env("RK_GEMM_MM", 0),
+                   sk_env = env("RK_GEMM_STREAMK", 0);
   p.dbg = dbg_env;
-  const int pslots = pair_env ? pair_slots(sm_count) : 0;
-  // Pairs tile M by 256 and cut each CTA's k-block fill from 48 to 32 KB
-  // (B200: ~0.425 vs ~0.46 us per k-block of a 128x256 per-CTA tile) but run
-  // half as many units at once: take them when the rounds of units allow, and
-  // never for short M, where the last pair tile is mostly padding.
+  p.sms = sm_count;
+  p.splits = 1;
   p.pair = 1;
+  p.mt_group = 1;
+  p.csk = 0;
+  p.streamk = 0;
+  const int kb = p.K / kBK;
+  auto ceil_div = [](long long a, long long b) { return (int)((a + b - 1) / b); };
+  auto t_kb = [](int a_kb, int b_kb) { return 0.0096 * (a_kb + b_kb); };  // us per k-block of one unit
+
+  // 1-CTA (or pair) tiles, BN by the fill rule
+  const int pslots = pair_env ? pair_slots(sm_count) : 0;
   if (pslots > 0 && rows_hint > kBM) {
     auto rounds = [&](int tm, int slots_) {
       int best = 1 << 30;
       for (int cand : {256, 128})
-        if (p.N % cand == 0) best = std::min(best, ((rows_hint + tm - 1) / tm * (p.N / cand) + slots_ - 1) / slots_ *
-                                                       (cand / 128));
+        if (p.N % cand == 0)
+          best = std::min(best, ceil_div((long long)ceil_div(rows_hint, tm) * (p.N / cand), slots_) * (cand / 128));
       return best;
     };
     const double single = rounds(kBM, sm_count) * 0.46, pair = rounds(2 * kBM, pslots) * 0.425;
     if (pair_env == 2 || (rows_hint >= 640 && pair <= single)) p.pair = 2;
   }
-  const int slots = p.pair == 2 ? pslots : sm_count;  // concurrent units
-  const int tile_m = kBM * p.pair;
-  const int num_m = (rows_hint + tile_m - 1) / tile_m;
-  p.sms = sm_count;
+  const int slots = p.pair == 2 ? pslots : sm_count;
+  const int num_m = ceil_div(rows_hint, kBM * p.pair);
   int bn = 64;
   for (int cand : {256, 128}) {
     if (p.N % cand == 0 && num_m * (p.N / cand) >= slots) { bn = cand; break; }
   }
   if (p.N % bn) raise(RK_ERR_INVALID_ARGUMENT, "bf16 GEMM needs N % 64 == 0");
   p.bn = bn;
-  p.splits = 1;
-  if (p.epi == EPI_ADD && p.split_flags) {
-    // Residual GEMMs that cannot fill the GPU split K s ways over 1-CTA tiles
-    // (widest tile), either
-    //  CSK:      the s CTAs of one tile form a cluster and reduce over DSMEM
-    //            (one launch, no global partials), or
-    //  EPI_PART: s partials in global memory, reduced in split order by
-    //            splitk_reduce_add_kernel (any s, any cluster occupancy).
-    // Cost model (calibrated on B200): a k-block of a 128x256 per-CTA tile
-    // ~0.46 us (1 CTA, L2-feed bound) / ~0.42 us (pair); EPI_PART partials
-    // cost s * M * N * 4 B written + read at ~8 TB/s plus ~3 us for the reduce
-    // launch; the CSK exchange ~1 us.
-    static const int csk_env = [] {
-      const char* v = std::getenv("RK_GEMM_CSK");
-      return v ? std::atoi(v) : 0;  // opt-in: measured slower than EPI_PART + reduce on c2 shapes
-    }();
+  double best = (double)ceil_div((long long)num_m * (p.N / bn), slots) * kb *
+                (p.pair == 2 ? 0.42 * bn / 256.0 : t_kb(16, bn / 8));
+
+  const bool residual_split = p.epi == EPI_ADD && p.split_flags;
+  auto part_cost = [&](int s) { return s > 1 ? 3.0 + 2.0 * s * (double)rows_hint * p.N * 4 / 8e6 : 0.0; };
+  auto split_ok = [&](int s) { return kb / s >= 4 && (s - 1) * ((kb + s - 1) / s) < kb; };
+  struct Choice {
+    int bn, splits, mt, csk, streamk;
+  } pick{-1, 1, 1, 0, 0};
+
+  // m-grouped tiles (short M): all ceil(M/128) m tiles in one CTA, BN = 128
+  const int mtc = ceil_div(p.rows_max, kBM);
+  if (mm_env && (mtc == 2 || mtc == 3) && p.N % 128 == 0 && p.epi != EPI_PART) {
+    const double t = t_kb(16 * mtc, 16);
+    for (int sp = 1; sp <= (residual_split ? 8 : 1); ++sp) {
+      if (sp > 1 && !split_ok(sp)) continue;
+      const double c = (double)ceil_div((long long)(p.N / 128) * sp, sm_count) * ((kb + sp - 1) / sp) * t + part_cost(sp);
+      if (c < best) { best = c; pick = {128, sp, mtc, 0, 0}; }
+    }
+  }
+  // split-K over 1-CTA 128 x wide tiles
+  if (residual_split) {
     const int wide = p.N % 256 == 0 ? 256 : (p.N % 128 == 0 ? 128 : 64);
-    const int tiles = num_m * (p.N / wide), kb = p.K / kBK;
-    const int tiles1 = (rows_hint + kBM - 1) / kBM * (p.N / wide);
-    if (4 * tiles < 3 * slots) {
-      const double t_kb1 = 0.46 * wide / 256.0;
-      const double t_now = (p.pair == 2 ? 0.42 : 0.46) * wide / 256.0;
-      // stream-K (1-CTA kernel only): every SM gets the same k-block count;
-      // partials of the ~tiles + SMs segments go through L2 to the reduce
-      // kernel (measured on c2: slower than split-K at these shapes -- opt-in
-      // with RK_GEMM_STREAMK=1 for experiments)
-      static const bool sk_enabled = [] {
-        const char* v = std::getenv("RK_GEMM_STREAMK");
-        return v && std::atoi(v) != 0;
-      }();
-      const int tiles_max = ((p.rows_max + kBM - 1) / kBM) * (p.N / wide);
-      const bool sk_ok = sk_enabled && kb >= 2 && tiles_max <= 2 * sm_count;
-      const double sk_cost = sk_ok ? ((double)tiles1 * kb + sm_count - 1) / sm_count * t_kb1 + 1.0 +
-                                         2.0 * (tiles1 + sm_count) * (double)kBM * wide * 4 / 8e6
-                                   : 1e30;
-      double best_cost = (double)((tiles + slots - 1) / slots) * kb * t_now;
-      int best = 1, best_csk = 0;
-      for (int s = 2; s <= 8 && kb / s >= 4; ++s) {
-        if ((s - 1) * ((kb + s - 1) / s) >= kb) continue;  // the last split would get no k-blocks
-        const int waves = (tiles1 * s + sm_count - 1) / sm_count;
-        const double part = waves * ((kb + s - 1) / s) * t_kb1 + 3.0 + 2.0 * s * (double)rows_hint * p.N * 4 / 8e6;
-        if (part < best_cost) { best = s; best_cost = part; best_csk = 0; }
-        const int cs = csk_env ? csk_slots(s) : 0;
-        if (cs > 0) {
-          const double csk = (double)((tiles1 + cs - 1) / cs) * ((kb + s - 1) / s) * t_kb1 + 1.0;
-          if (csk < best_cost) { best = s; best_cost = csk; best_csk = 1; }
-        }
-      }
-      if (sk_cost < best_cost) {
-        p.pair = 1;
-        p.bn = wide;
-        p.splits = 1;
-        p.streamk = 1;
-        p.epi = EPI_PART;
-      } else if (best > 1) {
-        p.pair = 1;
-        p.bn = wide;
-        p.splits = best;
-        p.csk = best_csk;
-        if (!best_csk) p.epi = EPI_PART;
+    const int tiles1 = ceil_div(rows_hint, kBM) * (p.N / wide);
+    const double t1 = t_kb(16, wide / 8);
+    for (int sp = 2; sp <= 8; ++sp) {
+      if (!split_ok(sp)) continue;
+      const double c = (double)ceil_div((long long)tiles1 * sp, sm_count) * ((kb + sp - 1) / sp) * t1 + part_cost(sp);
+      if (c < best) { best = c; pick = {wide, sp, 1, 0, 0}; }
+      const int cs = csk_env ? csk_slots(sp) : 0;
+      if (cs > 0) {
+        const double cc = (double)ceil_div(tiles1, cs) * ((kb + sp - 1) / sp) * t1 + 1.0;
+        if (cc < best) { best = cc; pick = {wide, sp, 1, 1, 0}; }
       }
     }
+    const int tiles_max = ceil_div(p.rows_max, kBM) * (p.N / wide);
+    if (sk_env && kb >= 2 && tiles_max <= 2 * sm_count) {  // stream-K (opt-in; slower at c2 shapes)
+      const double c = ((double)tiles1 * kb + sm_count - 1) / sm_count * t1 + 1.0 +
+                       2.0 * (tiles1 + sm_count) * (double)kBM * wide * 4 / 8e6;
+      if (c < best) { best = c; pick = {wide, 1, 1, 0, 1}; }
+    }
+  }
+  if (pick.bn > 0) {
+    p.pair = 1;
+    p.bn = pick.bn;
+    p.splits = pick.splits;
+    p.mt_group = pick.mt;
+    p.csk = pick.csk;
+    p.streamk = pick.streamk;
+    if (pick.streamk || (pick.splits > 1 && !pick.csk)) p.epi = EPI_PART;
   }
 }
 
@@ -897,13 +935,14 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
   choose_config(p, e->sm_count, rows_hint > 0 ? rows_hint : p.rows_max);
   static const bool log = std::getenv("RK_GEMM_LOG") != nullptr;
   if (log)
-    std::fprintf(stderr, "[gemm] M=%d%s N=%d K=%d epi=%d -> bn=%d pair=%d splits=%d csk=%d streamk=%d\n", p.rows_max,
-                 p.rows_dev ? "(dyn)" : "", p.N, p.K, p.epi, p.bn, p.pair, p.splits, p.csk, p.streamk);
+    std::fprintf(stderr, "[gemm] M=%d%s N=%d K=%d epi=%d -> bn=%d pair=%d mt=%d splits=%d csk=%d streamk=%d\n",
+                 p.rows_max, p.rows_dev ? "(dyn)" : "", p.N, p.K, p.epi, p.bn, p.pair, p.mt_group, p.splits, p.csk,
+                 p.streamk);
   if (p.norm_part && p.N / p.bn > kNormSlots) raise(RK_ERR_INVALID_ARGUMENT, "fused RMSNorm: too many N tiles");
   CUtensorMap ta, tb;
   make_tmap_bf16(&ta, A, (uint64_t)p.rows_max, (uint64_t)p.K, kBM, (uint64_t)lda);
   make_tmap_bf16(&tb, B, (uint64_t)p.N, (uint64_t)p.K, (uint32_t)(p.bn / p.pair), (uint64_t)p.K);
-  const int num_m = (p.rows_max + kBM * p.pair - 1) / (kBM * p.pair);
+  const int num_m = p.mt_group > 1 ? 1 : (p.rows_max + kBM * p.pair - 1) / (kBM * p.pair);
   const int total = num_m * (p.N / p.bn) * p.splits;  // units (pair units for the pair kernel)
   const int slots = p.pair == 2 ? pair_slots(e->sm_count) : e->sm_count;
   const int grid = p.csk ? total  // one tile per cluster of p.splits CTAs
@@ -918,7 +957,8 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
                       ? intern(std::string("gemm_") + kEpi[p.epi] + "_m" + std::to_string(p.rows_max) +
                                (p.rows_dev ? "dyn" : "") + "_n" + std::to_string(p.N) + "_k" + std::to_string(p.K) +
                                "_bn" + std::to_string(p.bn) + (p.streamk ? std::string("_sk") : "_s" + std::to_string(p.splits)) +
-                               (p.pair == 2 ? "_pair" : "") + (p.csk ? "_csk" : ""))
+                               (p.pair == 2 ? "_pair" : "") + (p.csk ? "_csk" : "") +
+                               (p.mt_group > 1 ? "_mt" + std::to_string(p.mt_group) : ""))
                       : "gemm",
                0, 0);
   ps.rec.kind = 1;

@@ -20,6 +20,8 @@ struct GemmArgs {
   int sms = 148;
   int dbg = 0;                  // experiments (RK_GEMM_DBG): 1 = every k-block loads tile (0,0), 2 = no MMAs
   int csk = 0;                  // 1: split-K inside a cluster of `splits` CTAs, reduced over DSMEM
+  int prefetch = 0;             // k-blocks of B (weights) prefetched into L2 ahead of the smem ring
+  int mt_group = 1;             // 2/3: one CTA computes all m tiles of an N tile (M <= 128*mt_group)
   int pair = 1;                 // 2: CTA-pair kernel (256-row tiles, cta_group::2), chosen by gemm_bf16
   int* split_flags = nullptr;   // ordered split-K flags (EPI_ADD), zero-initialised
   // outputs

@@ -1,14 +1,12 @@
 #!/bin/bash
-# GEMM bring-up: kernel tests, bf16 layer tests, then c2 bench with CSK off / on.
-OUT=gpurun_out/csk; mkdir -p $OUT
+# GEMM: L2 prefetch of B x MM: microbench + c2 bench
+OUT=gpurun_out/pf; mkdir -p $OUT
 timeout 400 python -m pytest tests/test_gpu_kernels.py -q -x -k gemm > $OUT/pytest_gemm.log 2>&1; echo "exit $?" >> $OUT/pytest_gemm.log
 tail -2 $OUT/pytest_gemm.log
-timeout 400 python -m pytest tests/test_gpu_bf16.py -q -x > $OUT/pytest_bf16.log 2>&1; echo "exit $?" >> $OUT/pytest_bf16.log
-tail -2 $OUT/pytest_bf16.log
-RK_GEMM_CSK=0 timeout 200 python tools/microbench.py gemm > $OUT/mb_part.log 2>&1
-timeout 200 python tools/microbench.py gemm > $OUT/mb_csk.log 2>&1
-paste -d'\n' $OUT/mb_part.log $OUT/mb_csk.log
-for csk in 0 1; do
-  RK_GEMM_CSK=$csk timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu > $OUT/bench_csk$csk.json 2> $OUT/bench_csk$csk.err
-  python -c "import json; d=json.load(open('$OUT/bench_csk$csk.json')); print('csk=$csk', d['ms_per_step'], d['value'], d['e2e']['value'])"
+for cfg in "0 0" "8 0" "8 1" "16 1" "4 1"; do
+  set -- $cfg
+  echo "== prefetch=$1 mm=$2"
+  RK_GEMM_PREFETCH=$1 RK_GEMM_MM=$2 timeout 200 python tools/microbench.py gemm 2>&1 | grep -v "^\[gemm"
+  RK_GEMM_PREFETCH=$1 RK_GEMM_MM=$2 timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu > $OUT/b.json 2> $OUT/b.err
+  python -c "import json; d=json.load(open('$OUT/b.json')); print('bench', d['ms_per_step'], d['roofline']['frac'], d['kernels']['gemm_bf16_tcgen05']['ms'])"
 done
