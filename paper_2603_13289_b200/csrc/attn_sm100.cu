@@ -133,6 +133,13 @@ __device__ __forceinline__ void tile_rows(const AttnArgs& a, int M, int tile, in
   r0 = r1 = 0;
 }
 
+// 3-input max (FMNMX3 on sm_100): two new values per instruction
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
 __device__ __forceinline__ void exp2_pair(float x0, float x1, bool poly, float& e0, float& e1) {
   if (poly) {
     poly_exp2_pair(x0, x1, e0, e1);
@@ -142,7 +149,9 @@ __device__ __forceinline__ void exp2_pair(float x0, float x1, bool poly, float& 
   }
 }
 
-template <int DH, bool TRACE>
+// POLY: bit c set -> the 4 pairs of 16-byte chunk c (of 8 per 64-key block)
+// take the FMA-pipe cubic instead of MUFU.EX2 (0x88: a quarter of the exps).
+template <int DH, bool TRACE, int POLY = 0x88>
 __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
     attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                 const __grid_constant__ CUtensorMap tmV, const AttnArgs a) {
@@ -332,10 +341,10 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
       float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
 #pragma unroll
       for (int u = 0; u < KEYS; u += 8) {
-        mx0 = fmaxf(mx0, fmaxf(__uint_as_float(r[u]), __uint_as_float(r[u + 1])));
-        mx1 = fmaxf(mx1, fmaxf(__uint_as_float(r[u + 2]), __uint_as_float(r[u + 3])));
-        mx2 = fmaxf(mx2, fmaxf(__uint_as_float(r[u + 4]), __uint_as_float(r[u + 5])));
-        mx3 = fmaxf(mx3, fmaxf(__uint_as_float(r[u + 6]), __uint_as_float(r[u + 7])));
+        mx0 = fmax3(mx0, __uint_as_float(r[u]), __uint_as_float(r[u + 1]));
+        mx1 = fmax3(mx1, __uint_as_float(r[u + 2]), __uint_as_float(r[u + 3]));
+        mx2 = fmax3(mx2, __uint_as_float(r[u + 4]), __uint_as_float(r[u + 5]));
+        mx3 = fmax3(mx3, __uint_as_float(r[u + 6]), __uint_as_float(r[u + 7]));
       }
       const float m_new = fmaxf(m_run, fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * scale);
       bool waited = false;  // P(j-1) V_{j-1} known complete (P buffer free, O stable)
@@ -377,7 +386,7 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
           const int u = b * 64 + 2 * i;
           float x0, x1, e0, e1;
           fma2(x0, x1, __uint_as_float(r[u]), __uint_as_float(r[u + 1]), scale, scale, neg_m, neg_m);
-          exp2_pair(x0, x1, ((i >> 2) & 3) == 3, e0, e1);
+          exp2_pair(x0, x1, (POLY >> (i >> 2)) & 1, e0, e1);
           if (i & 1) add2(ls2, ls3, ls2, ls3, e0, e1);
           else add2(ls0, ls1, ls0, ls1, e0, e1);
           pk[i] = pack_bf16(e0, e1);
@@ -541,13 +550,28 @@ template <int DH>
 void launch_attn(rk_engine* e, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                  const AttnArgs& a) {
   static bool attr = false;
+  // measured: a quarter of the exps on the FMA pipe pays at d_head 64 (MUFU
+  // bound, 128-key tiles); at d_head 128 (64-key tiles) MUFU alone is faster
+  static const int poly = [] {
+    const char* v = std::getenv("RK_ATTN_POLY");
+    return v ? (int)std::strtol(v, nullptr, 0) : (DH == 64 ? 0x88 : 0x00);
+  }();
   if (!attr) {
     RK_CUDA(cudaFuncSetAttribute(attn_kernel<DH, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ACfg<DH>::SMEM));
     RK_CUDA(cudaFuncSetAttribute(attn_kernel<DH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ACfg<DH>::SMEM));
+    RK_CUDA(cudaFuncSetAttribute(attn_kernel<DH, false, 0xAA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 ACfg<DH>::SMEM));
+    RK_CUDA(cudaFuncSetAttribute(attn_kernel<DH, false, 0x92>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 ACfg<DH>::SMEM));
+    RK_CUDA(cudaFuncSetAttribute(attn_kernel<DH, false, 0x00>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 ACfg<DH>::SMEM));
     attr = true;
   }
   dim3 grid(a.splits, a.H, max_tiles(a));
   if (a.trace) attn_kernel<DH, true><<<grid, kThreadsA, ACfg<DH>::SMEM, e->stream>>>(tq, tk, tv, a);
+  else if (poly == 0xAA) attn_kernel<DH, false, 0xAA><<<grid, kThreadsA, ACfg<DH>::SMEM, e->stream>>>(tq, tk, tv, a);
+  else if (poly == 0x92) attn_kernel<DH, false, 0x92><<<grid, kThreadsA, ACfg<DH>::SMEM, e->stream>>>(tq, tk, tv, a);
+  else if (poly == 0) attn_kernel<DH, false, 0x00><<<grid, kThreadsA, ACfg<DH>::SMEM, e->stream>>>(tq, tk, tv, a);
   else attn_kernel<DH, false><<<grid, kThreadsA, ACfg<DH>::SMEM, e->stream>>>(tq, tk, tv, a);
   if (a.splits > 1) {
     const int warps = a.rows_max * a.H;
