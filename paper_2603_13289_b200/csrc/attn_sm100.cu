@@ -391,10 +391,12 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
           else add2(ls0, ls1, ls0, ls1, e0, e1);
           pk[i] = pack_bf16(e0, e1);
         }
+        if (b == 0) RK_TRACE(0, j, 6);  // first block's exps done
         if (b == 0 && j > 0 && !waited) {
           mbar_wait(o_done, (j - 1) & 1);
           tc_fence_after();
         }
+        if (b == 0) RK_TRACE(0, j, 7);  // P(j-1) V done (P buffer free)
 #pragma unroll
         for (int ch = 0; ch < 8; ++ch) {
           uint4* dst = reinterpret_cast<uint4*>(sp + b * (kQ * 128) + rl * 128 + ((ch ^ (rl & 7)) * 16));

@@ -367,13 +367,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       Work w;
-      const int pf = p.prefetch;
       for (int it = 0; get_work<PAIR>(U, p.streamk, it, w); ++it) {
         const int mt = w.mt, nt = w.nt, kb0 = w.kb0, kb1 = w.kb1;
         const int bcol = nt * BN + rank * (BN / PAIR);
+        // one CTA per weight tile (m tile 0) prefetches it into L2 ahead of the ring
+        const int pf = mt == 0 ? p.prefetch : 0;
         for (int kb = kb0; kb < kb0 + pf && kb < kb1; ++kb) tma_prefetch_2d(&tmB, kb * kBK, bcol);
         for (int kb = kb0; kb < kb1; ++kb) {
-          if (pf && kb + pf < kb1) tma_prefetch_2d(&tmB, (kb + pf) * kBK, bcol);  // weights: L2 ahead of the ring
+          if (pf && kb + pf < kb1) tma_prefetch_2d(&tmB, (kb + pf) * kBK, bcol);
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
           const bool same = p.dbg & 1;
@@ -838,8 +839,8 @@ static void choose_config(GemmArgs& p, int sm_count, int rows_hint) {
     const char* v = std::getenv(name);
     return v ? std::atoi(v) : dflt;
   };
-  static const int pf_env = env("RK_GEMM_PREFETCH", 0);  // opt-in: slower on c2 (measured)
-  p.prefetch = pf_env;
+  static const int pf_env = env("RK_GEMM_PREFETCH", 0);  // opt-in
+  p.prefetch = 0;
   static const int pair_env = env("RK_GEMM_PAIR", 1), dbg_env = env("RK_GEMM_DBG", 0),
                    csk_env = env("RK_GEMM_CSK", 0), mm_env = env("RK_GEMM_MM", 0),
                    sk_env = env("RK_GEMM_STREAMK", 0);
@@ -917,6 +918,9 @@ static void choose_config(GemmArgs& p, int sm_count, int rows_hint) {
       if (c < best) { best = c; pick = {wide, 1, 1, 0, 1}; }
     }
   }
+  // short M: each weight tile is read by few CTAs, straight from HBM, and the
+  // smem ring alone cannot cover the DRAM latency -> prefetch ahead into L2
+  if (pf_env > 0 && rows_hint <= 512) p.prefetch = pf_env;
   if (pick.bn > 0) {
     p.pair = 1;
     p.bn = pick.bn;
