@@ -230,8 +230,21 @@ def cpu_sample(gpu_caches=None, threads=None, steps=1, warmup=0, kind="reference
             "sample": f"{WL['title'].split(':')[0]} model, prefix {cp} + {len(caches)} relayed segments x "
                       f"{cs} + suffix {cx} = {tokens} tokens per session, {used} concurrent sessions, "
                       f"profile {WL['profile']}",
-            "ms_per_session_step": ms}
+            "ms_per_session_step": ms, "host": host_info()}
     return tps, meta
+
+
+def host_info():
+    """The host the CPU arm ran on (the oracle's glibc expf/cos/sin are part of
+    the reference's numerics)."""
+    import platform
+    cpu = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            cpu = next((l.split(":", 1)[1].strip() for l in f if l.startswith("model name")), "")
+    except OSError:
+        pass
+    return {"cpu": cpu, "logical_cpus": os.cpu_count(), "libc": "-".join(platform.libc_ver())}
 
 
 def pin_host(host):
@@ -523,7 +536,7 @@ def run_reference(args, world, rank, local, dist):
             "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
             "config": {"workload": f"{WL['title']}, bounded CPU sample", "config_id": args.config, "sample": sample},
             "cpu_baseline": {"value": round(value, 4), "unit": "tokens/s", "kind": "reference", "cores": threads,
-                             "sample": sample},
+                             "sample": sample, "host": host_info()},
             "e2e": {"value": round(value, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         }), flush=True)
     except Exception as ex:
