@@ -663,6 +663,103 @@ __global__ void __launch_bounds__(256) splitk_reduce_add_kernel(const GemmArgs p
     splitk_reduce_row(p, splits, row, U, G, sk_tab);
 }
 
+// ---------------------------------------------------------------------------
+// M = 1 (the top layer's last row, the logits head): the GEMM is a weight
+// stream, so it runs on the CUDA cores as a GEMV at HBM speed instead of as
+// one mostly-empty 128-row tensor-core tile per N tile. The activation row is
+// staged in shared memory; each warp streams kGvRows weight rows with 16-byte
+// loads (kGvUnroll k-chunks of every row in flight), fp32 accumulation, and the
+// same epilogues: residual add, SiLU(gate)*up pairs, fp32 store.
+// ---------------------------------------------------------------------------
+constexpr int kGvRows = 4, kGvUnroll = 2, kGvWarps = 8;
+
+__device__ __forceinline__ float dot8(uint4 w, uint4 a) {
+  const __nv_bfloat162* w2 = reinterpret_cast<const __nv_bfloat162*>(&w);
+  const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 wf = __bfloat1622float2(w2[i]), af = __bfloat1622float2(a2[i]);
+    s = fmaf(wf.x, af.x, s);
+    s = fmaf(wf.y, af.y, s);
+  }
+  return s;
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(kGvWarps * 32) gemv_bf16_kernel(const __nv_bfloat16* __restrict__ a,
+                                                                  const __nv_bfloat16* __restrict__ B, GemmArgs p) {
+  extern __shared__ uint4 a_sm[];  // the activation row, K bf16
+  const int K = p.K, k8 = K / 8;
+  for (int i = threadIdx.x; i < k8; i += blockDim.x) a_sm[i] = reinterpret_cast<const uint4*>(a)[i];
+  __syncthreads();
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const float rs = p.row_scale ? p.row_scale[0] : 1.0f;
+  for (int n0 = (blockIdx.x * kGvWarps + warp) * kGvRows; n0 < p.N; n0 += gridDim.x * kGvWarps * kGvRows) {
+    float acc[kGvRows];
+#pragma unroll
+    for (int r = 0; r < kGvRows; ++r) acc[r] = 0.f;
+    const uint4* w4 = reinterpret_cast<const uint4*>(B + (size_t)n0 * K);
+    for (int c = lane; c < k8; c += 32 * kGvUnroll) {
+      uint4 wv[kGvUnroll][kGvRows], av[kGvUnroll];
+#pragma unroll
+      for (int u = 0; u < kGvUnroll; ++u) {
+        const int cc = c + 32 * u;
+        if (cc < k8) {
+          av[u] = a_sm[cc];
+#pragma unroll
+          for (int r = 0; r < kGvRows; ++r) wv[u][r] = __ldcs(w4 + (size_t)r * k8 + cc);  // streamed once
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kGvUnroll; ++u)
+        if (c + 32 * u < k8) {
+#pragma unroll
+          for (int r = 0; r < kGvRows; ++r) acc[r] += dot8(wv[u][r], av[u]);
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < kGvRows; ++r)
+#pragma unroll
+      for (int o = 16; o; o >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o);
+    if (lane == 0) {
+      if constexpr (EPI == EPI_SILU) {  // rows (2j, 2j+1) = (gate j, up j)
+#pragma unroll
+        for (int r = 0; r < kGvRows; r += 2) {
+          const float g = acc[r] * rs, u = acc[r + 1] * rs;
+          p.out_bf16[(n0 + r) / 2] = __float2bfloat16_rn(g / (1.0f + __expf(-g)) * u);
+        }
+      } else if constexpr (EPI == EPI_ADD) {
+#pragma unroll
+        for (int r = 0; r < kGvRows; ++r) p.out_f32[n0 + r] += acc[r] * rs;
+      } else {
+#pragma unroll
+        for (int r = 0; r < kGvRows; ++r) p.out_f32[n0 + r] = acc[r] * rs;
+      }
+    }
+  }
+}
+
+// The fused RMSNorm of a residual GEMM for one row: bf16 copy + 1/rms.
+__global__ void __launch_bounds__(256) row_norm_kernel(const float* __restrict__ h, int d, float eps,
+                                                       __nv_bfloat16* __restrict__ out, float* __restrict__ inv) {
+  __shared__ float red[8];
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    const float x = h[i];
+    ss = fmaf(x, x, ss);
+    out[i] = __float2bfloat16_rn(x);
+  }
+  for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    inv[0] = rsqrtf(t / (float)d + eps);
+  }
+}
+
 template <int BN, int EPI, int PAIR, bool CSK = false, int MT = 1>
 void launch(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& p, int grid) {
   using C = Cfg<BN, PAIR, MT>;
@@ -936,6 +1033,36 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
                int rows_hint) {
   if (p.rows_max <= 0) return;
   if (p.K % kBK) raise(RK_ERR_INVALID_ARGUMENT, "bf16 GEMM needs K % 64 == 0");
+  static const bool gemv_env = [] {
+    const char* v = std::getenv("RK_GEMV");
+    return v ? std::atoi(v) != 0 : true;
+  }();
+  if (gemv_env && p.rows_max == 1 && !p.rows_dev && (p.epi == EPI_ADD || p.epi == EPI_SILU || p.epi == EPI_F32) &&
+      p.N % kGvRows == 0) {
+    const size_t smem = (size_t)p.K * 2;
+    const int blocks = std::min((p.N + kGvWarps * kGvRows - 1) / (kGvWarps * kGvRows), 16 * e->sm_count);
+    ProfScope ps(e, (e->prof && e->prof->on)
+                        ? intern(std::string("gemv_n") + std::to_string(p.N) + "_k" + std::to_string(p.K))
+                        : "gemm",
+                 0, 0);
+    ps.rec.kind = 1;
+    ps.rec.rows_max = 1;
+    ps.rec.N = p.N;
+    ps.rec.K = p.K;
+    auto go = [&](auto kern) {
+      if (smem > 48 * 1024) RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kern<<<blocks, kGvWarps * 32, smem, e->stream>>>(A, B, p);
+    };
+    if (p.epi == EPI_ADD) go(gemv_bf16_kernel<EPI_ADD>);
+    else if (p.epi == EPI_SILU) go(gemv_bf16_kernel<EPI_SILU>);
+    else go(gemv_bf16_kernel<EPI_F32>);
+    e->launches += 1;
+    if (p.epi == EPI_ADD && p.norm_bf16 && p.norm_inv) {
+      row_norm_kernel<<<1, 256, 0, e->stream>>>(p.out_f32, p.N, p.norm_eps, p.norm_bf16, p.norm_inv);
+      e->launches += 1;
+    }
+    return;
+  }
   choose_config(p, e->sm_count, rows_hint > 0 ? rows_hint : p.rows_max);
   static const bool log = std::getenv("RK_GEMM_LOG") != nullptr;
   if (log)

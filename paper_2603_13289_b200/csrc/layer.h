@@ -65,7 +65,7 @@ class Runner {
  private:
   // one decoder layer over a row set (run_layer_rows, model.cpp:237-280)
   void run_layer(rk_context* ctx, int layer, float* hidden, Rows rows, bool commit, int max_ctx,
-                 float* probs = nullptr, int key_lo = 0, int key_n = 0);
+                 float* probs = nullptr, int key_lo = 0, int key_n = 0, int tail = -1);
   void last_row_logits(const float* hidden_row);  // output_logits (model.cpp:282-288)
   void row_logits_from_layer(rk_context* ctx, const float* hidden_row, uint64_t first_layer,
                              uint64_t position);
@@ -105,9 +105,11 @@ void layer_unpack_tensor(rk_weights* w, size_t idx, float* dst, size_t rows, siz
 // bf16 layer path (layer_bf16.cu)
 // prepared: the rows' bf16 copy and 1/rms were left by the previous layer's
 // residual GEMM (same row set); otherwise they are computed first.
+// tail >= 0: only the last `tail` rows go past the QKV GEMM (all rows' K/V are
+// still committed) -- the top layer when only the last row's output is used.
 void run_layer_bf16(rk_engine* e, rk_weights* w, rk_context* ctx, int layer, float* hidden,
                     Rows rows, bool commit, int max_ctx, float* probs, int key_lo, int key_n,
-                    void* cap_k, void* cap_v, bool prepared);
+                    void* cap_k, void* cap_v, bool prepared, int tail = -1);
 void last_row_logits_bf16(rk_engine* e, rk_weights* w, const float* hidden_row, float* logits);
 
 }  // namespace rk

@@ -114,7 +114,8 @@ static NormBufs norm_bufs(rk_engine* e, size_t rows) {
 }
 
 void run_layer_bf16(rk_engine* e, rk_weights* w, rk_context* ctx, int l, float* hidden, Rows rows, bool commit,
-                    int max_ctx, float* probs, int key_lo, int key_n, void* cap_k, void* cap_v, bool prepared) {
+                    int max_ctx, float* probs, int key_lo, int key_n, void* cap_k, void* cap_v, bool prepared,
+                    int tail) {
   (void)max_ctx;
   Scratch& S = *e->scratch;
   const rk_model_spec& s = w->s;
@@ -128,7 +129,7 @@ void run_layer_bf16(rk_engine* e, rk_weights* w, rk_context* ctx, int l, float* 
   auto* ck = static_cast<__nv_bfloat16*>(ctx->k_layer(l));
   auto* cv = static_cast<__nv_bfloat16*>(ctx->v_layer(l));
   // live rows of a sparse pass are known only on the device: plan tiles for ~1/3
-  const int hint = rows.rows_dev ? std::max(1, rows.rows_max / 3) : rows.rows_max;
+  int hint = rows.rows_dev ? std::max(1, rows.rows_max / 3) : rows.rows_max;
   int* flags = split_flags(e);
   __nv_bfloat16* save = reinterpret_cast<__nv_bfloat16*>(S.seg_hidden_out.as<char>() + 0);
   if (!commit) {
@@ -164,6 +165,20 @@ void run_layer_bf16(rk_engine* e, rk_weights* w, rk_context* ctx, int l, float* 
   g.cap_v = static_cast<__nv_bfloat16*>(cap_v);
   gemm_bf16(e, normed, d, static_cast<const __nv_bfloat16*>(ly.w_qkv), g, hint);
 
+  NormBufs tb = nb;
+  if (tail >= 0 && commit && !rows.rows_dev && tail < rows.rows_max) {
+    // only the last `tail` rows continue (their outputs are the only ones used)
+    if (tail == 0) return;
+    const int off = rows.rows_max - tail;
+    hidden += (size_t)off * d;
+    qbuf += (size_t)off * q;
+    normed += (size_t)off * d;
+    tb.inv += off;
+    rows = Rows{tail, nullptr, rows.pos + off};
+    rows.g1 = rows.g2 = 0;
+    hint = tail;
+  }
+
   AttnArgs a;
   a.q = qbuf;
   a.out = attn;
@@ -191,14 +206,14 @@ void run_layer_bf16(rk_engine* e, rk_weights* w, rk_context* ctx, int l, float* 
   o.ld_out = d;
   o.split_flags = flags;
   o.norm_bf16 = normed;  // mlp RMSNorm fused: bf16 rows + 1/rms for the gate/up GEMM
-  o.norm_part = nb.part;
-  o.norm_inv = nb.inv;
-  o.norm_cnt = nb.cnt;
+  o.norm_part = tb.part;
+  o.norm_inv = tb.inv;
+  o.norm_cnt = tb.cnt;
   o.norm_eps = s.norm_eps;
   gemm_bf16(e, attn, q, static_cast<const __nv_bfloat16*>(ly.w_o), o, hint);
 
   GemmArgs gu;
-  gu.row_scale = nb.inv;
+  gu.row_scale = tb.inv;
   gu.rows_max = rows.rows_max;
   gu.rows_dev = rows.rows_dev;
   gu.N = 2 * ff;
@@ -218,9 +233,9 @@ void run_layer_bf16(rk_engine* e, rk_weights* w, rk_context* ctx, int l, float* 
   dn.ld_out = d;
   dn.split_flags = flags;
   dn.norm_bf16 = normed;  // next layer's attention RMSNorm fused likewise
-  dn.norm_part = nb.part;
-  dn.norm_inv = nb.inv;
-  dn.norm_cnt = nb.cnt;
+  dn.norm_part = tb.part;
+  dn.norm_inv = tb.inv;
+  dn.norm_cnt = tb.cnt;
   dn.norm_eps = s.norm_eps;
   gemm_bf16(e, act, ff, static_cast<const __nv_bfloat16*>(ly.w_down), dn, hint);
 

@@ -122,9 +122,10 @@ int* Runner::upload_tokens(const int32_t* tokens, uint64_t n, int off) {
 // one decoder layer (run_layer_rows, model.cpp:237-280)
 // ---------------------------------------------------------------------------
 void Runner::run_layer(rk_context* ctx, int l, float* hidden, Rows rows, bool commit, int max_ctx,
-                       float* probs, int key_lo, int key_n) {
+                       float* probs, int key_lo, int key_n, int tail) {
   if (w_->precision == RK_BF16) {
-    run_layer_bf16(e_, w_, ctx, l, hidden, rows, commit, max_ctx, probs, key_lo, key_n, cap_k_, cap_v_, prepared_);
+    run_layer_bf16(e_, w_, ctx, l, hidden, rows, commit, max_ctx, probs, key_lo, key_n, cap_k_, cap_v_, prepared_,
+                   tail);
     prepared_ = true;
     return;
   }
@@ -146,7 +147,19 @@ void Runner::run_layer(rk_context* ctx, int l, float* hidden, Rows rows, bool co
     e_->launches += 2;
   }
   k::rope_commit_exact(st_, S.qkv.as<float>(), rows, H, Hkv, dh, rope, ck, cv, commit ? 1 : 0);
-  k::attn_exact(st_, S.qkv.as<float>(), rows, H, Hkv, dh, ck, cv, S.attn.as<float>(), commit ? 0 : 1,
+  const float* qkv = S.qkv.as<float>();
+  if (tail >= 0 && commit && !rows.rows_dev && tail < rows.rows_max) {
+    // only the last `tail` rows continue (see run_layer_bf16)
+    if (tail == 0) {
+      e_->launches += 3;
+      return;
+    }
+    const int off = rows.rows_max - tail;
+    hidden += (size_t)off * d;
+    qkv += (size_t)off * (q + 2 * kv);
+    rows = Rows{tail, nullptr, rows.pos + off};
+  }
+  k::attn_exact(st_, qkv, rows, H, Hkv, dh, ck, cv, S.attn.as<float>(), commit ? 0 : 1,
                 max_ctx, probs, key_lo, key_n);
   k::gemm_exact(st_, S.attn.as<float>(), static_cast<const float*>(ly.w_o), hidden, rows, d, q,
                 k::EPI_ADD, status);
@@ -214,7 +227,9 @@ void Runner::prefill(rk_context* ctx, const int32_t* tokens, uint64_t n, uint64_
   e_->launches += 2;
   Rows rows{(int)n, nullptr, S.positions.as<int>()};
   prepared_ = false;
-  for (uint64_t l = 0; l < s.num_layers; ++l) run_layer(ctx, (int)l, S.hidden.as<float>(), rows, true, (int)(base + n));
+  for (uint64_t l = 0; l < s.num_layers; ++l)  // top layer: only the last row's output is ever read
+    run_layer(ctx, (int)l, S.hidden.as<float>(), rows, true, (int)(base + n), nullptr, 0, 0,
+              l + 1 == s.num_layers ? (want_logits ? 1 : 0) : -1);
   if (want_logits) last_row_logits(S.hidden.as<float>() + (n - 1) * s.d_model);
 }
 
@@ -687,7 +702,10 @@ void Runner::agent_fused(rk_context* ctx, const int32_t* prefix, uint64_t P, rk_
     // rows are gathered (it only shrinks, to the head rows, after sparse_hi)
     if (l == 0 || (segs && (l == l_start || l == l_det + 1))) prepared_ = false;
     if (streamed) graft_layer(l);
-    run_layer(ctx, (int)l, H, rows, true, (int)total);
+    // top layer over the head rows only: just the suffix's last row feeds the
+    // logits (no rows at all when the logits come from the segment end)
+    const bool top_head = l + 1 == L && rows.rows_dev == nullptr && rows.rows_max == (int)head;
+    run_layer(ctx, (int)l, H, rows, true, (int)total, nullptr, 0, 0, top_head ? (S > 0 ? 1 : 0) : -1);
     if (segs && l == l_det) {
       ev_band = event();
       for (uint64_t u = 0; u < U; ++u) {

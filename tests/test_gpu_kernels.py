@@ -31,7 +31,7 @@ def run_gemm(engine, A, B, C0, live, epi):
 
 SHAPES = [(1, 64, 64), (7, 192, 128), (128, 256, 256), (200, 384, 512), (333, 1024, 2048),
           (1000, 128, 1024), (64, 3072, 2048), (256, 2048, 8192), (513, 16384, 256), (129, 64, 64),
-          (4032, 3072, 2048), (320, 16384, 2048)]
+          (4032, 3072, 2048), (320, 16384, 2048), (1, 16384, 2048), (1, 4096, 14336), (1, 128256, 2048)]
 
 
 @pytest.mark.parametrize("shape", SHAPES, ids=[f"{m}x{n}x{k}" for m, n, k in SHAPES])
@@ -293,3 +293,16 @@ np.save({str(tmp_path / "out.npy")!r}, run_gemm(e, d["A"], d["B"], d["H"], {M}, 
     ref = H + bf16_round(A).astype(np.float64) @ bf16_round(B).astype(np.float64).T
     assert np.abs(got - ref).max() / np.abs(ref).max() < 2e-5
     assert np.abs(want - ref).max() / np.abs(ref).max() < 2e-5
+
+
+@pytest.mark.parametrize("shape", [(1, 2048, 8192), (1, 4096, 14336), (1, 64, 64)])
+def test_gemv_residual(engine, shape):
+    """M = 1 residual GEMMs run as the CUDA-core GEMV; same result as fp64."""
+    M, N, K = shape
+    rng = np.random.default_rng(N + K)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    B = (rng.standard_normal((N, K)) / np.sqrt(K)).astype(np.float32)
+    H = rng.standard_normal((M, N)).astype(np.float32)
+    got = run_gemm(engine, A, B, H, M, 1)
+    ref = H + bf16_round(A).astype(np.float64) @ bf16_round(B).astype(np.float64).T
+    assert np.abs(got - ref).max() / np.abs(ref).max() < 2e-5
