@@ -671,7 +671,7 @@ __global__ void __launch_bounds__(256) splitk_reduce_add_kernel(const GemmArgs p
 // loads (kGvUnroll k-chunks of every row in flight), fp32 accumulation, and the
 // same epilogues: residual add, SiLU(gate)*up pairs, fp32 store.
 // ---------------------------------------------------------------------------
-constexpr int kGvRows = 4, kGvUnroll = 2, kGvWarps = 8;
+constexpr int kGvWarps = 8;
 
 __device__ __forceinline__ float dot8(uint4 w, uint4 a) {
   const __nv_bfloat162* w2 = reinterpret_cast<const __nv_bfloat162*>(&w);
@@ -686,7 +686,9 @@ __device__ __forceinline__ float dot8(uint4 w, uint4 a) {
   return s;
 }
 
-template <int EPI>
+// kGvRows weight rows per warp, kGvUnroll k-chunks of each in flight: 4 x 2 for
+// wide N, 2 x 4 when N/32 warps would leave SMs idle (kGvRows even: SiLU pairs)
+template <int EPI, int kGvRows, int kGvUnroll>
 __global__ void __launch_bounds__(kGvWarps * 32) gemv_bf16_kernel(const __nv_bfloat16* __restrict__ a,
                                                                   const __nv_bfloat16* __restrict__ B, GemmArgs p) {
   extern __shared__ uint4 a_sm[];  // the activation row, K bf16
@@ -1038,9 +1040,11 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
     return v ? std::atoi(v) != 0 : true;
   }();
   if (gemv_env && p.rows_max == 1 && !p.rows_dev && (p.epi == EPI_ADD || p.epi == EPI_SILU || p.epi == EPI_F32) &&
-      p.N % kGvRows == 0) {
+      p.N % 4 == 0) {
     const size_t smem = (size_t)p.K * 2;
-    const int blocks = std::min((p.N + kGvWarps * kGvRows - 1) / (kGvWarps * kGvRows), 16 * e->sm_count);
+    const bool narrow = p.N / (kGvWarps * 4) < 2 * e->sm_count;
+    const int per_block = kGvWarps * (narrow ? 2 : 4);
+    const int blocks = std::min((p.N + per_block - 1) / per_block, 16 * e->sm_count);
     ProfScope ps(e, (e->prof && e->prof->on)
                         ? intern(std::string("gemv_n") + std::to_string(p.N) + "_k" + std::to_string(p.K))
                         : "gemm",
@@ -1053,9 +1057,15 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
       if (smem > 48 * 1024) RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       kern<<<blocks, kGvWarps * 32, smem, e->stream>>>(A, B, p);
     };
-    if (p.epi == EPI_ADD) go(gemv_bf16_kernel<EPI_ADD>);
-    else if (p.epi == EPI_SILU) go(gemv_bf16_kernel<EPI_SILU>);
-    else go(gemv_bf16_kernel<EPI_F32>);
+    if (narrow) {
+      if (p.epi == EPI_ADD) go(gemv_bf16_kernel<EPI_ADD, 2, 4>);
+      else if (p.epi == EPI_SILU) go(gemv_bf16_kernel<EPI_SILU, 2, 4>);
+      else go(gemv_bf16_kernel<EPI_F32, 2, 4>);
+    } else {
+      if (p.epi == EPI_ADD) go(gemv_bf16_kernel<EPI_ADD, 4, 2>);
+      else if (p.epi == EPI_SILU) go(gemv_bf16_kernel<EPI_SILU, 4, 2>);
+      else go(gemv_bf16_kernel<EPI_F32, 4, 2>);
+    }
     e->launches += 1;
     if (p.epi == EPI_ADD && p.norm_bf16 && p.norm_inv) {
       row_norm_kernel<<<1, 256, 0, e->stream>>>(p.out_f32, p.N, p.norm_eps, p.norm_bf16, p.norm_inv);
