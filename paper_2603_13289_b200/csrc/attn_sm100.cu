@@ -608,8 +608,16 @@ void attention_bf16(rk_engine* e, const AttnArgs& a_in, const __nv_bfloat16* ctx
   // that are cut (per tile, on the device); the rest write their output
   // directly. (Measured: a uniform 2-way split of the c2 sparse layers and a
   // column-split softmax with two warpgroups per tile were both slower.)
-  if (base < slots && nk_max >= 8) {  // (at 1-1.5 waves, c2's sparse layers, splitting measured slower)
-    const int target = std::max(4, (int)((double)nk_max * base / (2.0 * slots) + 0.999));
+  static const int min_part = [] {
+    const char* v = std::getenv("RK_ATTN_MINPART");
+    return v ? std::max(1, std::atoi(v)) : 4;
+  }();
+  static const double split_div = [] {
+    const char* v = std::getenv("RK_ATTN_SPLITDIV");
+    return v ? std::atof(v) : 2.0;
+  }();
+  if (base < slots && nk_max >= 2 * min_part) {  // (at 1-1.5 waves, c2's sparse layers, splitting measured slower)
+    const int target = std::max(min_part, (int)((double)nk_max * base / (split_div * slots) + 0.999));
     if (target < nk_max) {
       a.tiles_per_split = target;
       a.splits = std::min(16, (nk_max + target - 1) / target);
