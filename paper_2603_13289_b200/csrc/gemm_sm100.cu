@@ -742,6 +742,76 @@ __global__ void __launch_bounds__(kGvWarps * 32) gemv_bf16_kernel(const __nv_bfl
   }
 }
 
+// Narrow N (few weight rows, long K): a whole block shares R rows, its 8 warps
+// splitting K, so the weight stream still spreads over every SM.
+template <int EPI, int R>
+__global__ void __launch_bounds__(kGvWarps * 32) gemv_bf16_ksplit_kernel(const __nv_bfloat16* __restrict__ a,
+                                                                         const __nv_bfloat16* __restrict__ B,
+                                                                         GemmArgs p) {
+  extern __shared__ uint4 a_sm[];
+  __shared__ float red[kGvWarps][R];
+  const int K = p.K, k8 = K / 8;
+  for (int i = threadIdx.x; i < k8; i += blockDim.x) a_sm[i] = reinterpret_cast<const uint4*>(a)[i];
+  __syncthreads();
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const float rs = p.row_scale ? p.row_scale[0] : 1.0f;
+  constexpr int U = 4;
+  for (int n0 = blockIdx.x * R; n0 < p.N; n0 += gridDim.x * R) {
+    float acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0.f;
+    const uint4* w4 = reinterpret_cast<const uint4*>(B + (size_t)n0 * K);
+    for (int c = threadIdx.x; c < k8; c += blockDim.x * U) {
+      uint4 wv[U][R], av[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int cc = c + blockDim.x * u;
+        if (cc < k8) {
+          av[u] = a_sm[cc];
+#pragma unroll
+          for (int r = 0; r < R; ++r) wv[u][r] = __ldcs(w4 + (size_t)r * k8 + cc);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (c + blockDim.x * u < k8) {
+#pragma unroll
+          for (int r = 0; r < R; ++r) acc[r] += dot8(wv[u][r], av[u]);
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+#pragma unroll
+      for (int o = 16; o; o >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o);
+      if (lane == 0) red[warp][r] = acc[r];
+    }
+    __syncthreads();
+    if (threadIdx.x < R) {
+      float t = 0.f;
+#pragma unroll
+      for (int w = 0; w < kGvWarps; ++w) t += red[w][threadIdx.x];
+      red[0][threadIdx.x] = t;  // (each thread reads its own column before writing row 0 of it)
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if constexpr (EPI == EPI_SILU) {
+#pragma unroll
+        for (int r = 0; r < R; r += 2) {
+          const float g = red[0][r] * rs, u2 = red[0][r + 1] * rs;
+          p.out_bf16[(n0 + r) / 2] = __float2bfloat16_rn(g / (1.0f + __expf(-g)) * u2);
+        }
+      } else if constexpr (EPI == EPI_ADD) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) p.out_f32[n0 + r] += red[0][r] * rs;
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) p.out_f32[n0 + r] = red[0][r] * rs;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // The fused RMSNorm of a residual GEMM for one row: bf16 copy + 1/rms.
 __global__ void __launch_bounds__(256) row_norm_kernel(const float* __restrict__ h, int d, float eps,
                                                        __nv_bfloat16* __restrict__ out, float* __restrict__ inv) {
@@ -1057,10 +1127,15 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
       if (smem > 48 * 1024) RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       kern<<<blocks, kGvWarps * 32, smem, e->stream>>>(A, B, p);
     };
-    if (narrow) {
-      if (p.epi == EPI_ADD) go(gemv_bf16_kernel<EPI_ADD, 2, 4>);
-      else if (p.epi == EPI_SILU) go(gemv_bf16_kernel<EPI_SILU, 2, 4>);
-      else go(gemv_bf16_kernel<EPI_F32, 2, 4>);
+    if (narrow) {  // a block per 2 rows, K split over its warps
+      const int nb = std::min(p.N / 2, 16 * e->sm_count);
+      auto go2 = [&](auto kern) {
+        if (smem > 48 * 1024) RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<nb, kGvWarps * 32, smem, e->stream>>>(A, B, p);
+      };
+      if (p.epi == EPI_ADD) go2(gemv_bf16_ksplit_kernel<EPI_ADD, 2>);
+      else if (p.epi == EPI_SILU) go2(gemv_bf16_ksplit_kernel<EPI_SILU, 2>);
+      else go2(gemv_bf16_ksplit_kernel<EPI_F32, 2>);
     } else {
       if (p.epi == EPI_ADD) go(gemv_bf16_kernel<EPI_ADD, 4, 2>);
       else if (p.epi == EPI_SILU) go(gemv_bf16_kernel<EPI_SILU, 4, 2>);
