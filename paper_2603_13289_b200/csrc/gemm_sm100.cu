@@ -686,6 +686,81 @@ __device__ __forceinline__ float dot8(uint4 w, uint4 a) {
   return s;
 }
 
+// Store R consecutive outputs n0.. of the single row (R even: SiLU pairs and
+// RoPE pairs stay together) with the GEMM's epilogue semantics.
+template <int EPI, int R>
+__device__ __forceinline__ void gemv_store(const GemmArgs& p, int n0, const float (&v)[R], float rs) {
+  if constexpr (EPI == EPI_SILU) {  // rows (2j, 2j+1) = (gate j, up j)
+#pragma unroll
+    for (int r = 0; r < R; r += 2) {
+      const float g = v[r] * rs, u = v[r + 1] * rs;
+      p.out_bf16[(n0 + r) / 2] = __float2bfloat16_rn(g / (1.0f + __expf(-g)) * u);
+    }
+  } else if constexpr (EPI == EPI_ADD) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) p.out_f32[n0 + r] += v[r] * rs;
+  } else if constexpr (EPI == EPI_QKV) {  // RoPE on Q/K, K/V rows into the context at the row's position
+    const int pos = p.pos[0], q = p.q, kv = p.kv, dh = p.dh;
+#pragma unroll
+    for (int r = 0; r < R; r += 2) {
+      const int col = n0 + r;
+      const float x0 = v[r] * rs, x1 = v[r + 1] * rs;
+      const __nv_bfloat162 raw = __floats2bfloat162_rn(x0, x1);
+      if (col >= q + kv) {
+        const int c = col - q - kv;
+        if (p.cap_v) *reinterpret_cast<__nv_bfloat162*>(p.cap_v + c) = raw;
+        __nv_bfloat16* base = p.commit ? p.ctx_v + (size_t)pos * kv : p.self_v;
+        *reinterpret_cast<__nv_bfloat162*>(base + c) = raw;
+        continue;
+      }
+      const bool is_k = col >= q;
+      const int c = is_k ? col - q : col;
+      if (is_k && p.cap_k) *reinterpret_cast<__nv_bfloat162*>(p.cap_k + c) = raw;
+      const float2 t = p.rope[(size_t)pos * (dh / 2) + (c % dh) / 2];
+      const __nv_bfloat162 rot = __floats2bfloat162_rn(x0 * t.x - x1 * t.y, x0 * t.y + x1 * t.x);
+      __nv_bfloat16* base = !is_k ? p.out_bf16 : (p.commit ? p.ctx_k + (size_t)pos * kv : p.self_k);
+      *reinterpret_cast<__nv_bfloat162*>(base + c) = rot;
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < R; ++r) p.out_f32[n0 + r] = v[r] * rs;
+  }
+}
+
+// EPI_ADD with the fused RMSNorm: the last block to finish turns the new
+// residual row into its bf16 copy and 1/rms (norm_cnt[0] is the ticket).
+template <int EPI>
+__device__ __forceinline__ void gemv_norm_finish(const GemmArgs& p) {
+  if constexpr (EPI == EPI_ADD) {
+    if (!p.norm_bf16 || !p.norm_inv || !p.norm_cnt) return;
+    __shared__ int last;
+    __shared__ float red[kGvWarps];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      last = atomicAdd(p.norm_cnt, 1) == (int)gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    float ss = 0.f;
+    for (int i = threadIdx.x; i < p.N; i += blockDim.x) {
+      const float x = __ldcg(p.out_f32 + i);
+      ss = fmaf(x, x, ss);
+      p.norm_bf16[i] = __float2bfloat16_rn(x);
+    }
+    for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float t = 0.f;
+      for (int w = 0; w < kGvWarps; ++w) t += red[w];
+      p.norm_inv[0] = rsqrtf(t / (float)p.N + p.norm_eps);
+      p.norm_cnt[0] = 0;
+    }
+  }
+}
+
 // kGvRows weight rows per warp, kGvUnroll k-chunks of each in flight: 4 x 2 for
 // wide N, 2 x 4 when N/32 warps would leave SMs idle (kGvRows even: SiLU pairs)
 template <int EPI, int kGvRows, int kGvUnroll>
@@ -724,22 +799,9 @@ __global__ void __launch_bounds__(kGvWarps * 32) gemv_bf16_kernel(const __nv_bfl
     for (int r = 0; r < kGvRows; ++r)
 #pragma unroll
       for (int o = 16; o; o >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o);
-    if (lane == 0) {
-      if constexpr (EPI == EPI_SILU) {  // rows (2j, 2j+1) = (gate j, up j)
-#pragma unroll
-        for (int r = 0; r < kGvRows; r += 2) {
-          const float g = acc[r] * rs, u = acc[r + 1] * rs;
-          p.out_bf16[(n0 + r) / 2] = __float2bfloat16_rn(g / (1.0f + __expf(-g)) * u);
-        }
-      } else if constexpr (EPI == EPI_ADD) {
-#pragma unroll
-        for (int r = 0; r < kGvRows; ++r) p.out_f32[n0 + r] += acc[r] * rs;
-      } else {
-#pragma unroll
-        for (int r = 0; r < kGvRows; ++r) p.out_f32[n0 + r] = acc[r] * rs;
-      }
-    }
+    if (lane == 0) gemv_store<EPI, kGvRows>(p, n0, acc, rs);
   }
+  gemv_norm_finish<EPI>(p);
 }
 
 // Narrow N (few weight rows, long K): a whole block shares R rows, its 8 warps
@@ -794,22 +856,14 @@ __global__ void __launch_bounds__(kGvWarps * 32) gemv_bf16_ksplit_kernel(const _
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      if constexpr (EPI == EPI_SILU) {
+      float v[R];
 #pragma unroll
-        for (int r = 0; r < R; r += 2) {
-          const float g = red[0][r] * rs, u2 = red[0][r + 1] * rs;
-          p.out_bf16[(n0 + r) / 2] = __float2bfloat16_rn(g / (1.0f + __expf(-g)) * u2);
-        }
-      } else if constexpr (EPI == EPI_ADD) {
-#pragma unroll
-        for (int r = 0; r < R; ++r) p.out_f32[n0 + r] += red[0][r] * rs;
-      } else {
-#pragma unroll
-        for (int r = 0; r < R; ++r) p.out_f32[n0 + r] = red[0][r] * rs;
-      }
+      for (int r = 0; r < R; ++r) v[r] = red[0][r];
+      gemv_store<EPI, R>(p, n0, v, rs);
     }
     __syncthreads();
   }
+  gemv_norm_finish<EPI>(p);
 }
 
 // The fused RMSNorm of a residual GEMM for one row: bf16 copy + 1/rms.
@@ -1109,8 +1163,8 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
     const char* v = std::getenv("RK_GEMV");
     return v ? std::atoi(v) != 0 : true;
   }();
-  if (gemv_env && p.rows_max == 1 && !p.rows_dev && (p.epi == EPI_ADD || p.epi == EPI_SILU || p.epi == EPI_F32) &&
-      p.N % 4 == 0) {
+  if (gemv_env && p.rows_max == 1 && !p.rows_dev &&
+      (p.epi == EPI_ADD || p.epi == EPI_SILU || p.epi == EPI_F32 || p.epi == EPI_QKV) && p.N % 4 == 0) {
     const size_t smem = (size_t)p.K * 2;
     const bool narrow = p.N / (kGvWarps * 4) < 2 * e->sm_count;
     const int per_block = kGvWarps * (narrow ? 2 : 4);
@@ -1135,14 +1189,16 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
       };
       if (p.epi == EPI_ADD) go2(gemv_bf16_ksplit_kernel<EPI_ADD, 2>);
       else if (p.epi == EPI_SILU) go2(gemv_bf16_ksplit_kernel<EPI_SILU, 2>);
+      else if (p.epi == EPI_QKV) go2(gemv_bf16_ksplit_kernel<EPI_QKV, 2>);
       else go2(gemv_bf16_ksplit_kernel<EPI_F32, 2>);
     } else {
       if (p.epi == EPI_ADD) go(gemv_bf16_kernel<EPI_ADD, 4, 2>);
       else if (p.epi == EPI_SILU) go(gemv_bf16_kernel<EPI_SILU, 4, 2>);
+      else if (p.epi == EPI_QKV) go(gemv_bf16_kernel<EPI_QKV, 4, 2>);
       else go(gemv_bf16_kernel<EPI_F32, 4, 2>);
     }
     e->launches += 1;
-    if (p.epi == EPI_ADD && p.norm_bf16 && p.norm_inv) {
+    if (p.epi == EPI_ADD && p.norm_bf16 && p.norm_inv && !p.norm_cnt) {  // (no ticket: separate pass)
       row_norm_kernel<<<1, 256, 0, e->stream>>>(p.out_f32, p.N, p.norm_eps, p.norm_bf16, p.norm_inv);
       e->launches += 1;
     }

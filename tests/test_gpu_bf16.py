@@ -82,6 +82,25 @@ def test_bf16_capture_prefill_matches_exact(engine):
         assert rel(getattr(b, f), getattr(a, f)) < 5e-2, f
 
 
+def test_bf16_capture_decode_matches_exact(engine):
+    """Decode-time capture in bf16 (one-row steps: the GEMV path incl. the
+    QKV epilogue and the fused RMSNorm ticket) against the exact capture: the
+    same greedy tokens while the logits margins allow, K/V/hidden/influence close."""
+    spec = SPECS[0][1]
+    hosts = {}
+    for prec in ("fp32", "bf16"):
+        w = engine.weights(spec, 11, prec)
+        ctx = w.context()
+        logits = ctx.prefill(pattern_tokens(25, 256, 1))
+        hosts[prec] = ctx.capture_decode(logits, 24, 1).to_host()
+    a, b = hosts["fp32"], hosts["bf16"]
+    agree = int(np.argmin(np.append(a.segment_tokens == b.segment_tokens, False)))
+    assert agree >= 4, (a.segment_tokens, b.segment_tokens)  # greedy paths diverge only at near-ties
+    for f in ("k_pre", "v"):
+        assert rel(getattr(b, f)[:, :agree], getattr(a, f)[:, :agree]) < 5e-2, f
+    assert rel(b.hidden_snapshot[:agree], a.hidden_snapshot[:agree]) < 5e-2
+
+
 def test_bf16_nonunit_norm_gains(engine, oracle):
     """Uploaded weights with non-unit RMSNorm gains: the bf16 path folds the
     attention/MLP gains into W_qkv / W_gate,up and applies 1/rms in the GEMM
