@@ -117,15 +117,20 @@ struct ACfg {
 };
 
 // Query tile `tile` of the launch -> rows [r0, r1) within one row group.
+// Tiles are numbered prefix, segment rows, suffix -- ascending key length
+// (the suffix sits after every segment) -- so the reversed dispatch order is
+// longest-first: the suffix tiles, whose rows see the whole context, start
+// at once instead of forming the launch's tail.
 __device__ __forceinline__ void tile_rows(const AttnArgs& a, int M, int tile, int& r0, int& r1) {
   const int g1 = min(a.g1, M), g2 = min(max(a.g2, g1), M);
-  const int b[4] = {0, g1, g2, M};
+  const int lo[3] = {0, g2, g1}, hi[3] = {g1, M, g2};  // prefix | segment rows | suffix
 #pragma unroll
   for (int g = 0; g < 3; ++g) {
-    const int nt = (b[g + 1] - b[g] + kQ - 1) / kQ;
+    const int b0 = lo[g], b1 = hi[g];
+    const int nt = (b1 - b0 + kQ - 1) / kQ;
     if (tile < nt) {
-      r0 = b[g] + tile * kQ;
-      r1 = min(r0 + kQ, b[g + 1]);
+      r0 = b0 + tile * kQ;
+      r1 = min(r0 + kQ, b1);
       return;
     }
     tile -= nt;
