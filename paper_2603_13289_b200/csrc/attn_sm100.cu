@@ -621,7 +621,11 @@ void attention_bf16(rk_engine* e, const AttnArgs& a_in, const __nv_bfloat16* ctx
     const char* v = std::getenv("RK_ATTN_SPLITDIV");
     return v ? std::atof(v) : 2.0;
   }();
-  if (base < slots && nk_max >= 2 * min_part) {  // (at 1-1.5 waves, c2's sparse layers, splitting measured slower)
+  static const double split_waves = [] {
+    const char* v = std::getenv("RK_ATTN_SPLITWAVES");
+    return v ? std::atof(v) : 1.0;
+  }();
+  if (base < split_waves * slots && nk_max >= 2 * min_part) {
     const int target = std::max(min_part, (int)((double)nk_max * base / (split_div * slots) + 0.999));
     if (target < nk_max) {
       a.tiles_per_split = target;
