@@ -635,25 +635,23 @@ __device__ void block_compact(const uint32_t* flags_smem_unused, int n, const ui
 // all in flight); the dependent DADD chain walks them in index order via
 // shuffles, every lane computing the identical chain.
 __device__ double seq_threshold_warp(const double* s_dev, int n, double tau, bool& valid) {
+  // The reference's sequential double sum (selector.cpp:37-39): the warp
+  // stages 1024 scores at a time in shared memory and lane 0 runs the add
+  // chain from there (the loads are off the chain; the chain is DADD-latency bound).
+  __shared__ double buf[1024];
   const int lane = threadIdx.x & 31;
   double mean = 0.0;
-  for (int b = 0; b < n; b += 128) {
-    double v[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int j = b + u * 32 + lane;
-      v[u] = j < n ? s_dev[j] : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int lim = min(32, n - (b + u * 32));
+  for (int b = 0; b < n; b += 1024) {
+    const int m = min(1024, n - b);
+    __syncwarp();
+    for (int i = lane; i < m; i += 32) buf[i] = s_dev[b + i];
+    __syncwarp();
+    if (lane == 0) {
 #pragma unroll 8
-      for (int i = 0; i < 32; ++i) {
-        const double x = __shfl_sync(0xffffffffu, v[u], i);
-        if (i < lim) mean = __dadd_rn(mean, x);
-      }
+      for (int i = 0; i < m; ++i) mean = __dadd_rn(mean, buf[i]);
     }
   }
+  mean = __shfl_sync(0xffffffffu, mean, 0);
   mean = __ddiv_rn(mean, (double)n);
   valid = mean > 0.0;
   return __dmul_rn(tau, mean);
