@@ -11,6 +11,16 @@
 // the MMAs of tile i+1. Rows of A beyond the live row count (read from device
 // memory for sparse passes) are computed but never stored.
 //
+// Shapes (choose_config picks one per GEMM from a calibrated cost model):
+//   1-CTA      128 x BN tiles, persistent, one CTA per SM
+//   CTA pair   cluster of 2, tcgen05 cta_group::2, 256 x BN tiles; each CTA
+//              stages half of B, halving the L2->SM feed per MMA
+//   split-K    residual GEMMs that cannot fill the GPU: fp32 partials reduced
+//              in split order (splitk_reduce_add_kernel) or, opt-in, over DSMEM
+//   m-grouped  (opt-in) all m tiles of a short M in one CTA
+//   GEMV       M = 1 (top-layer last row, logits head, decode steps): CUDA
+//              cores at HBM speed with the same epilogues
+//
 // Fused epilogues (the reference computes these as separate loops over the
 // matmul outputs, model.cpp:246-280 / 211-233):
 //   EPI_QKV   RoPE on Q and K (adjacent pairs, tensor.cpp:134-142), Q -> bf16
