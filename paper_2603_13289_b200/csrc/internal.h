@@ -243,6 +243,7 @@ void mark_rows(cudaStream_t s, uint8_t* origin, int len, int layer_lo, int layer
 void mark_layers(cudaStream_t s, uint8_t* origin, int len, int layer_lo, int layer_hi);
 // device memset / memcpy / 2-D row zero as kernels (see kernels_common.cu)
 void zero_dev(cudaStream_t s, void* dst, size_t bytes);
+void zero_many(cudaStream_t s, const std::vector<std::pair<void*, size_t>>& bufs);  // one launch
 void copy_dev(cudaStream_t s, void* dst, const void* src, size_t bytes);
 void zero_rows(cudaStream_t s, void* dst, size_t pitch, size_t width, size_t rows);
 void copy_i32(cudaStream_t s, int* dst, const int* src, int n);  // src may be mapped host memory

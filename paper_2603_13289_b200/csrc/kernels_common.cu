@@ -886,6 +886,37 @@ void mark_layers(cudaStream_t s, uint8_t* origin, int len, int lo, int hi) {
   if (hi < lo) return;
   mark_layers_kernel<<<blocks_for((size_t)(hi - lo + 1) * len), kThreads, 0, s>>>(origin, len, lo, hi);
 }
+struct ZeroList {
+  uint8_t* p[16];
+  size_t n[16];
+};
+__global__ void zero_many_kernel(ZeroList z) {  // blockIdx.y = buffer
+  uint8_t* dst = z.p[blockIdx.y];
+  const size_t n = z.n[blockIdx.y];
+  const size_t i0 = blockIdx.x * (size_t)blockDim.x + threadIdx.x, stride = (size_t)gridDim.x * blockDim.x;
+  if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+    for (size_t i = i0; i < n / 16; i += stride) d4[i] = make_uint4(0, 0, 0, 0);
+    for (size_t i = n / 16 * 16 + i0; i < n; i += stride) dst[i] = 0;
+  } else {
+    for (size_t i = i0; i < n; i += stride) dst[i] = 0;
+  }
+}
+void zero_many(cudaStream_t s, const std::vector<std::pair<void*, size_t>>& bufs) {
+  for (size_t b = 0; b < bufs.size(); b += 16) {
+    ZeroList z{};
+    size_t mx = 0;
+    const int m = (int)std::min<size_t>(16, bufs.size() - b);
+    for (int i = 0; i < m; ++i) {
+      z.p[i] = static_cast<uint8_t*>(bufs[b + i].first);
+      z.n[i] = bufs[b + i].second;
+      mx = std::max(mx, z.n[i]);
+    }
+    if (!mx) continue;
+    const unsigned blocks = (unsigned)std::min<size_t>(256, (mx / 16 + kThreads - 1) / kThreads + 1);
+    zero_many_kernel<<<dim3(blocks, m), kThreads, 0, s>>>(z);
+  }
+}
 void zero_dev(cudaStream_t s, void* dst, size_t bytes) {
   if (!bytes) return;
   const size_t blocks = std::min<size_t>(1184, (bytes / 16 + kThreads - 1) / kThreads + 1);

@@ -8,6 +8,8 @@
 #include <cmath>
 #include <cstring>
 
+#include <cstdlib>
+
 #include "layer.h"
 #include "prof.h"
 
@@ -23,6 +25,7 @@ Runner::Runner(rk_engine* e, rk_weights* w) : e_(e), w_(w), st_(e->stream) {
   require(e != nullptr && w != nullptr, RK_ERR_INVALID_ARGUMENT, "null engine / weights");
   require(w->e == e, RK_ERR_INVALID_ARGUMENT, "weights belong to another engine");
   k::zero_dev(st_, e->status.p, 64);
+  e->launches += 1;
   // side-stream reporting work of the previous call must finish before its
   // buffers (selection slots) are reused
   if (e->side_join) RK_CUDA(cudaStreamWaitEvent(st_, e->side_join, 0));
@@ -603,6 +606,7 @@ void Runner::agent_fused(rk_context* ctx, const int32_t* prefix, uint64_t P, rk_
 
   results.clear();
   std::vector<rk_segment_marks> marks(U);
+  std::vector<std::pair<void*, size_t>> zeros;
   for (uint64_t u = 0; u < U; ++u) {
     ExtendResult r;
     r.mode = mode;
@@ -623,13 +627,24 @@ void Runner::agent_fused(rk_context* ctx, const int32_t* prefix, uint64_t P, rk_
     X.info.ensure(64);
     X.dinfo.ensure(64);
     X.score.ensure(n[u] * 8);
-    k::zero_dev(st_, X.info.p, 64);
-    k::zero_dev(st_, X.dinfo.p, 64);
+    zeros.emplace_back(X.info.p, 64);
+    zeros.emplace_back(X.dinfo.p, 64);
     marks[u].base = base[u];
     marks[u].len = n[u];
     marks[u].origin.alloc_pooled(&e_->cache_pool, L * n[u]);  // pooled: freeing would sync the device
-    k::zero_dev(st_, marks[u].origin.p, L * n[u]);
+    zeros.emplace_back(marks[u].origin.p, L * n[u]);
     results.push_back(r);
+  }
+  static const bool zm = [] {
+    const char* v = std::getenv("RK_ZERO_MANY");
+    return v ? std::atoi(v) != 0 : true;
+  }();
+  if (zm) {
+    k::zero_many(st_, zeros);  // selection counters, diagnostics and marks of every segment in one launch
+    e_->launches += 1;
+  } else {
+    for (auto& z : zeros) k::zero_dev(st_, z.first, z.second);
+    e_->launches += zeros.size();
   }
   const int ev_begin = event();
   // every cell is written before it is read: prefix / suffix rows by each
