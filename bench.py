@@ -267,6 +267,7 @@ def merge_kernel_stats(stats):
     fam = {}
     for k in stats:
         name = "gemm_bf16_tcgen05" if k["name"].startswith("gemm") else \
+            "gemv_bf16" if k["name"].startswith("gemv") else \
             "attention_bf16_tcgen05" if k["name"].startswith("attn") else k["name"]
         f = fam.setdefault(name, {"name": name, "launches": 0, "total_ms": 0.0, "flops": 0.0, "bytes": 0.0})
         for key in ("launches", "total_ms", "flops", "bytes"):

@@ -1181,8 +1181,8 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
     const int blocks = std::min((p.N + per_block - 1) / per_block, 16 * e->sm_count);
     ProfScope ps(e, (e->prof && e->prof->on)
                         ? intern(std::string("gemv_n") + std::to_string(p.N) + "_k" + std::to_string(p.K))
-                        : "gemm",
-                 0, 0);
+                        : "gemv",
+                 0, 2.0 * p.N * p.K);  // the weight stream
     ps.rec.kind = 1;
     ps.rec.rows_max = 1;
     ps.rec.N = p.N;

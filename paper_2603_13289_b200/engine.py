@@ -121,12 +121,17 @@ class Engine(_Obj):
         _check(lib().rk_engine_profile(P(self.ptr), int(enable)))
 
     def profile_read(self):
-        stats = (KernelStat * 64)()
-        n = U64()
-        _check(lib().rk_engine_profile_read(P(self.ptr), stats, U64(64), C.byref(n)))
+        cap = 64
+        while True:  # every aggregated record (a c3 step has a few hundred distinct labels)
+            stats = (KernelStat * cap)()
+            n = U64()
+            _check(lib().rk_engine_profile_read(P(self.ptr), stats, U64(cap), C.byref(n)))
+            if n.value <= cap:
+                break
+            cap = int(n.value)
         return [{"name": stats[i].name.decode(), "launches": int(stats[i].launches),
                  "total_ms": stats[i].total_ms, "flops": stats[i].flops, "bytes": stats[i].bytes}
-                for i in range(min(n.value, 64))]
+                for i in range(n.value)]
 
     # ---- factories ------------------------------------------------------------
     def weights(self, spec, seed, precision="fp32"):
