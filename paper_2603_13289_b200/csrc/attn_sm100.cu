@@ -175,6 +175,8 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 13);
   int* s_kmax = reinterpret_cast<int*>(bar + 14);
 
+  pdl_trigger();
+  pdl_wait();  // rows_dev / positions / Q of the previous kernel
   const int M = a.rows_dev ? *a.rows_dev : a.rows_max;
   // grid (split part, head, tile) with tiles in reverse order: the CTAs of the
   // latest (longest) query tiles of every head dispatch first, all parts of a
@@ -575,11 +577,24 @@ void launch_attn(rk_engine* e, const CUtensorMap& tq, const CUtensorMap& tk, con
     attr = true;
   }
   dim3 grid(a.splits, a.H, max_tiles(a));
-  if (a.trace) attn_kernel<DH, true><<<grid, kThreadsA, ACfg<DH>::SMEM, e->stream>>>(tq, tk, tv, a);
-  else if (poly == 0xAA) attn_kernel<DH, false, 0xAA><<<grid, kThreadsA, ACfg<DH>::SMEM, e->stream>>>(tq, tk, tv, a);
-  else if (poly == 0x92) attn_kernel<DH, false, 0x92><<<grid, kThreadsA, ACfg<DH>::SMEM, e->stream>>>(tq, tk, tv, a);
-  else if (poly == 0) attn_kernel<DH, false, 0x00><<<grid, kThreadsA, ACfg<DH>::SMEM, e->stream>>>(tq, tk, tv, a);
-  else attn_kernel<DH, false><<<grid, kThreadsA, ACfg<DH>::SMEM, e->stream>>>(tq, tk, tv, a);
+  auto go = [&](auto kern) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kThreadsA);
+    cfg.dynamicSmemBytes = ACfg<DH>::SMEM;
+    cfg.stream = e->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    RK_CUDA(cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, a));
+  };
+  if (a.trace) go(attn_kernel<DH, true>);
+  else if (poly == 0xAA) go(attn_kernel<DH, false, 0xAA>);
+  else if (poly == 0x92) go(attn_kernel<DH, false, 0x92>);
+  else if (poly == 0) go(attn_kernel<DH, false, 0x00>);
+  else go(attn_kernel<DH, false>);
   if (a.splits > 1) {
     const int warps = a.rows_max * a.H;
     attn_combine_kernel<DH><<<std::min((warps + 7) / 8, 4 * e->sm_count), 256, 0, e->stream>>>(a);

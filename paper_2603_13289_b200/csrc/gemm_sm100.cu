@@ -346,8 +346,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* epi_stage = smem + C::STAGES * C::STAGE_BYTES + 256;  // [4 warps][32 rows][128 B]
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const Units U = units_of<PAIR, MT>(p);
   const uint32_t rank = PAIR == 2 ? cluster_ctarank() : 0;  // 0 = leader (issues the MMAs)
+  pdl_trigger();
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
@@ -371,6 +371,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // the prologue above overlapped the previous kernel; its outputs are visible from here
+  const Units U = units_of<PAIR, MT>(p);
 
   if (warp == 0) {
     if (elect_one()) {  // ---------------- TMA producer
@@ -662,6 +664,8 @@ __device__ __forceinline__ void splitk_reduce_row(const GemmArgs& p, int splits,
 }
 
 __global__ void __launch_bounds__(256) splitk_reduce_add_kernel(const GemmArgs p, int splits, int G) {
+  pdl_trigger();
+  pdl_wait();
   const int M = p.rows_dev ? *p.rows_dev : p.rows_max;
   const Units U = units_of<1>(p);
   __shared__ int sk_tab[1025];  // stream-K range starts of the G CTAs (+ end)
@@ -777,6 +781,8 @@ template <int EPI, int kGvRows, int kGvUnroll>
 __global__ void __launch_bounds__(kGvWarps * 32) gemv_bf16_kernel(const __nv_bfloat16* __restrict__ a,
                                                                   const __nv_bfloat16* __restrict__ B, GemmArgs p) {
   extern __shared__ uint4 a_sm[];  // the activation row, K bf16
+  pdl_trigger();
+  pdl_wait();
   const int K = p.K, k8 = K / 8;
   for (int i = threadIdx.x; i < k8; i += blockDim.x) a_sm[i] = reinterpret_cast<const uint4*>(a)[i];
   __syncthreads();
@@ -822,6 +828,8 @@ __global__ void __launch_bounds__(kGvWarps * 32) gemv_bf16_ksplit_kernel(const _
                                                                          GemmArgs p) {
   extern __shared__ uint4 a_sm[];
   __shared__ float red[kGvWarps][R];
+  pdl_trigger();
+  pdl_wait();
   const int K = p.K, k8 = K / 8;
   for (int i = threadIdx.x; i < k8; i += blockDim.x) a_sm[i] = reinterpret_cast<const uint4*>(a)[i];
   __syncthreads();
@@ -896,6 +904,34 @@ __global__ void __launch_bounds__(256) row_norm_kernel(const float* __restrict__
   }
 }
 
+}  // namespace
+
+// Programmatic dependent launch on for the hot kernels (RK_PDL=0 turns it off).
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("RK_PDL");
+    return v ? std::atoi(v) != 0 : true;
+  }();
+  return on;
+}
+
+namespace {
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  RK_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
+}
+
 template <int BN, int EPI, int PAIR, bool CSK = false, int MT = 1>
 void launch(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& p, int grid) {
   using C = Cfg<BN, PAIR, MT>;
@@ -920,20 +956,22 @@ void launch(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const G
     cfg.numAttrs = 1;
     RK_CUDA(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<BN, EPI, 1, true>, a, b, p));
   } else if constexpr (PAIR == 1) {
-    gemm_bf16_kernel<BN, EPI, 1, false, MT><<<grid, kThreads, C::SMEM, st>>>(a, b, p);
+    launch_pdl(gemm_bf16_kernel<BN, EPI, 1, false, MT>, dim3(grid), dim3(kThreads), C::SMEM, st, a, b, p);
   } else {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = C::SMEM;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = 2;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     RK_CUDA(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<BN, EPI, 2>, a, b, p));
   }
 }
@@ -1189,13 +1227,13 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
     ps.rec.K = p.K;
     auto go = [&](auto kern) {
       if (smem > 48 * 1024) RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      kern<<<blocks, kGvWarps * 32, smem, e->stream>>>(A, B, p);
+      launch_pdl(kern, dim3(blocks), dim3(kGvWarps * 32), smem, e->stream, A, B, p);
     };
     if (narrow) {  // a block per 2 rows, K split over its warps
       const int nb = std::min(p.N / 2, 16 * e->sm_count);
       auto go2 = [&](auto kern) {
         if (smem > 48 * 1024) RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        kern<<<nb, kGvWarps * 32, smem, e->stream>>>(A, B, p);
+        launch_pdl(kern, dim3(nb), dim3(kGvWarps * 32), smem, e->stream, A, B, p);
       };
       if (p.epi == EPI_ADD) go2(gemv_bf16_ksplit_kernel<EPI_ADD, 2>);
       else if (p.epi == EPI_SILU) go2(gemv_bf16_ksplit_kernel<EPI_SILU, 2>);
@@ -1254,7 +1292,8 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
     case EPI_SILU: launch_bn<EPI_SILU>(e->stream, ta, tb, p, grid); break;
     case EPI_PART:
       launch_bn<EPI_PART>(e->stream, ta, tb, p, grid);
-      splitk_reduce_add_kernel<<<std::min(p.rows_max, 8 * e->sm_count), 256, 0, e->stream>>>(p, p.splits, grid);
+      launch_pdl(splitk_reduce_add_kernel, dim3(std::min(p.rows_max, 8 * e->sm_count)), dim3(256), 0, e->stream, p,
+                 (int)p.splits, grid);
       e->launches += 1;
       break;
     default: launch_bn<EPI_F32>(e->stream, ta, tb, p, grid); break;

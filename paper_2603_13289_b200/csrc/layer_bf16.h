@@ -60,6 +60,8 @@ constexpr int kNormSlots = 64;  // max N tiles of a residual GEMM (d_model / BN)
 
 // A: [rows_max x K] bf16 row-major with row stride lda; B: [N x K] bf16.
 // rows_hint: expected live rows (tile-shape choice) when rows_dev is set.
+bool pdl_enabled();  // programmatic dependent launch of the hot kernels (RK_PDL, default on)
+
 void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat16* B, GemmArgs p,
                int rows_hint = 0);
 void make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows,

@@ -151,6 +151,15 @@ __device__ __forceinline__ uint32_t tmem_ld1(uint32_t taddr) {
 }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// ---- programmatic dependent launch ------------------------------------------
+// A kernel launched with programmatic stream serialization may start while its
+// predecessor is finishing: it lets its own dependents launch right away
+// (pdl_trigger) and, after a prologue that reads nothing the predecessor
+// writes, waits for the predecessor grid to complete (pdl_wait). Both are
+// no-ops for kernels launched without the attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ---- CTA pairs (cluster of 2, tcgen05 cta_group::2) ------------------------
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
