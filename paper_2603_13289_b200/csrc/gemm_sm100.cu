@@ -371,6 +371,29 @@ __global__ void __launch_bounds__(kThreads, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // The producer starts streaming the weights (B) of its first STAGES k-blocks
+  // before the dependency wait -- they do not depend on the previous kernel --
+  // so with programmatic dependent launch the weight stream overlaps the
+  // previous kernel's tail; A (activations) follows after the wait.
+  int pre = 0;
+  if (warp == 0 && !p.rows_dev && !p.streamk && !CSK && !(p.dbg & 1)) {
+    const Units Up = units_of<PAIR, MT>(p);
+    Work w0;
+    if (elect_one() && get_work<PAIR>(Up, false, 0, w0)) {
+      pre = min(C::STAGES, w0.kb1 - w0.kb0);
+      for (int i = 0; i < pre; ++i) {
+        uint8_t* sa = smem + i * C::STAGE_BYTES;
+        const int kx = (w0.kb0 + i) * kBK;
+        if constexpr (PAIR == 2) {
+          if (rank == 0) mbar_arrive_expect_tx(&full[i], 2 * C::STAGE_BYTES);
+          tma_load_2d_pair(sa + C::A_BYTES, &tmB, &full[i], kx, w0.nt * BN + rank * (BN / 2));
+        } else {
+          mbar_arrive_expect_tx(&full[i], C::STAGE_BYTES);
+          tma_load_2d(sa + C::A_BYTES, &tmB, &full[i], kx, w0.nt * BN);
+        }
+      }
+    }
+  }
   pdl_wait();  // the prologue above overlapped the previous kernel; its outputs are visible from here
   const Units U = units_of<PAIR, MT>(p);
 
@@ -387,21 +410,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = kb0; kb < kb0 + pf && kb < kb1; ++kb) tma_prefetch_2d(&tmB, kb * kBK, bcol);
         for (int kb = kb0; kb < kb1; ++kb) {
           if (pf && kb + pf < kb1) tma_prefetch_2d(&tmB, (kb + pf) * kBK, bcol);
-          mbar_wait(&empty[stage], phase ^ 1);
+          const bool early = it == 0 && kb - kb0 < pre;  // stage armed, its B already in flight
+          if (!early) mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
           const bool same = p.dbg & 1;
           const int kx = same ? 0 : kb * kBK, am = same ? 0 : mt, bn_ = same ? 0 : nt;
           if constexpr (PAIR == 2) {
             // the leader's barrier counts both CTAs' bytes
-            if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+            if (rank == 0 && !early) mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
             tma_load_2d_pair(sa, &tmA, &full[stage], kx, (am * 2 + rank) * kBM);
-            tma_load_2d_pair(sa + C::A_BYTES, &tmB, &full[stage], kx, bn_ * BN + rank * (BN / 2));
+            if (!early) tma_load_2d_pair(sa + C::A_BYTES, &tmB, &full[stage], kx, bn_ * BN + rank * (BN / 2));
           } else {
-            mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+            if (!early) mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
 #pragma unroll
             for (int mi = 0; mi < MT; ++mi)
               tma_load_2d(sa + mi * kBM * kBK * 2, &tmA, &full[stage], kx, (am * MT + mi) * kBM);
-            tma_load_2d(sa + C::A_BYTES, &tmB, &full[stage], kx, bn_ * BN);
+            if (!early) tma_load_2d(sa + C::A_BYTES, &tmB, &full[stage], kx, bn_ * BN);
           }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
