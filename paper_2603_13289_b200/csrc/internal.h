@@ -215,6 +215,8 @@ struct Rows {
   int g1 = 0, g2 = 0;
 };
 
+bool pdl_enabled();  // programmatic dependent launch (RK_PDL, default on), gemm_sm100.cu
+
 // ---- kernel launchers (kernels_*.cu) -------------------------------------
 namespace k {
 // weights

@@ -11,9 +11,27 @@
 #include <algorithm>
 
 #include "internal.h"
+#include "sm100.cuh"
 
 namespace rk {
 namespace {
+// Launch with programmatic stream serialization (see sm100.cuh pdl_*): every
+// kernel launched through here starts with pdl_trigger(); pdl_wait().
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  RK_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
+}
+
 
 constexpr int kThreads = 256;
 
@@ -127,6 +145,8 @@ __global__ void bf16_to_f32_kernel(float* dst, const __nv_bfloat16* src, size_t 
 // ---------------------------------------------------------------------------
 __global__ void embed_kernel(float* hidden, const void* emb, size_t elem, const int32_t* tokens,
                              int n, int d) {
+  sm100::pdl_trigger();
+  sm100::pdl_wait();
   const size_t total = (size_t)n * d;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
        i += (size_t)gridDim.x * blockDim.x) {
@@ -164,11 +184,15 @@ __global__ void positions_from_sel_kernel(int* pos, const int* sel, const int* c
     pos[r] = base + sel[r];
 }
 __global__ void iota_kernel(int* pos, int n, int base) {
+  sm100::pdl_trigger();
+  sm100::pdl_wait();
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
     pos[r] = base + r;
 }
 __global__ void mark_rows_kernel(uint8_t* origin, int len, int lo, int hi, const int* sel,
                                  const int* count, int rows_max) {
+  sm100::pdl_trigger();
+  sm100::pdl_wait();
   const int rows = count ? *count : rows_max;
   const int layers = hi - lo + 1;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows * layers;
@@ -176,6 +200,8 @@ __global__ void mark_rows_kernel(uint8_t* origin, int len, int lo, int hi, const
     origin[(size_t)(lo + i / rows) * len + sel[i % rows]] = 1;
 }
 __global__ void mark_layers_kernel(uint8_t* origin, int len, int lo, int hi) {
+  sm100::pdl_trigger();
+  sm100::pdl_wait();
   const size_t total = (size_t)(hi - lo + 1) * len;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
        i += (size_t)gridDim.x * blockDim.x)
@@ -184,6 +210,8 @@ __global__ void mark_layers_kernel(uint8_t* origin, int len, int lo, int hi) {
 // Device-side zero fill / copy as kernels (not copy-engine operations, which
 // would queue behind relay-cache uploads streaming on the copy engines).
 __global__ void zero_bytes_kernel(uint8_t* dst, size_t n) {
+  sm100::pdl_trigger();
+  sm100::pdl_wait();
   const size_t i0 = (blockIdx.x * (size_t)blockDim.x + threadIdx.x), stride = (size_t)gridDim.x * blockDim.x;
   if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
     uint4* d4 = reinterpret_cast<uint4*>(dst);
@@ -194,6 +222,8 @@ __global__ void zero_bytes_kernel(uint8_t* dst, size_t n) {
   }
 }
 __global__ void copy_bytes_kernel(uint8_t* dst, const uint8_t* src, size_t n) {
+  sm100::pdl_trigger();
+  sm100::pdl_wait();
   const size_t i0 = (blockIdx.x * (size_t)blockDim.x + threadIdx.x), stride = (size_t)gridDim.x * blockDim.x;
   if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
     uint4* d4 = reinterpret_cast<uint4*>(dst);
@@ -218,12 +248,16 @@ __global__ void zero_rows_kernel(uint8_t* dst, size_t pitch, size_t width, size_
   }
 }
 __global__ void copy_i32_kernel(int* dst, const int* src, int n) {
+  sm100::pdl_trigger();
+  sm100::pdl_wait();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = src[i];
 }
 __global__ void fill_doubles_kernel(double* dst, int n, double v) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[i] = v;
 }
 __global__ void set_depth_kernel(uint64_t* depth, int n, uint64_t v) {
+  sm100::pdl_trigger();
+  sm100::pdl_wait();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) depth[i] = v;
 }
 
@@ -256,6 +290,8 @@ __device__ void block_argmax(float& best, int& bi) {
 }
 __global__ void __launch_bounds__(256) argmax_partial_kernel(const float* __restrict__ x, int n,
                                                              float2* __restrict__ part) {
+  sm100::pdl_trigger();
+  sm100::pdl_wait();
   float best = -__int_as_float(0x7f800000);
   int bi = 0x7fffffff;
   const int n4 = (reinterpret_cast<uintptr_t>(x) & 15) ? 0 : n / 4;
@@ -273,6 +309,8 @@ __global__ void __launch_bounds__(256) argmax_partial_kernel(const float* __rest
   if (threadIdx.x == 0) part[blockIdx.x] = make_float2(best, __int_as_float(bi));
 }
 __global__ void argmax_final_kernel(const float2* __restrict__ part, int parts, int* out) {
+  sm100::pdl_trigger();
+  sm100::pdl_wait();
   float best = -__int_as_float(0x7f800000);
   int bi = 0x7fffffff;
   for (int i = threadIdx.x; i < parts; i += blockDim.x)
@@ -297,6 +335,8 @@ __global__ void __launch_bounds__(256) realign_graft_dh_kernel(
     const T* __restrict__ k_pre, const T* __restrict__ v_src, int n, int kv,
     const double2* __restrict__ rope, int base, T* __restrict__ ctx_k, T* __restrict__ ctx_v,
     size_t ctx_layer_stride, int skip_lo, int skip_hi) {
+  sm100::pdl_trigger();
+  sm100::pdl_wait();
   constexpr int VEC = 16 / sizeof(T);
   int l = blockIdx.y;
   if (skip_hi >= skip_lo && l >= skip_lo) l += skip_hi - skip_lo + 1;
@@ -503,6 +543,8 @@ __global__ void __launch_bounds__(256) score_dh_kernel(const T* __restrict__ ctx
                                                        int n, int heads, const double2* __restrict__ rope,
                                                        int base, double* __restrict__ s_dev,
                                                        double* __restrict__ s_key) {
+  sm100::pdl_trigger();
+  sm100::pdl_wait();
   constexpr int NV = DH * sizeof(T) / 16;  // 16-byte vectors per head slice
   extern __shared__ double cosv[];          // [tokens of this CTA][2][heads]
   const int per_tok = 2 * heads;
@@ -674,6 +716,8 @@ __device__ __forceinline__ void two_sum(double a, double b, double& s, double& e
 __global__ void __launch_bounds__(1024) select_relay_kernel(
     const double* s_dev, const float* influence, const double* infl_mean, int n, double tau_dev,
     double tau_inf, int suffix_k, uint32_t* flags, int* sel_idx, uint32_t* sel_tags, int* info) {
+  sm100::pdl_trigger();
+  sm100::pdl_wait();
   __shared__ double thr[2], margin_abs;
   __shared__ int valid[2], uncertain;
   __shared__ double red_hi[32], red_lo[32];
@@ -857,7 +901,7 @@ void doubles_to_floats(cudaStream_t s, float* dst, const double* src, int n) {
 void embed(cudaStream_t s, float* hidden, const void* emb, size_t elem, const int32_t* tokens,
            int n, int d, int, int*) {
   const size_t total = (size_t)n * d;
-  embed_kernel<<<blocks_for(total) < 4096 ? blocks_for(total) : 4096, kThreads, 0, s>>>(hidden, emb, elem, tokens, n, d);
+  launch_pdl(embed_kernel, dim3(blocks_for(total) < 4096 ? blocks_for(total) : 4096), dim3(kThreads), 0, s, hidden, emb, elem, tokens, n, d);
 }
 void gather_rows(cudaStream_t s, float* dst, const float* src, const int* idx, const int* count,
                  int rows_max, int d) {
@@ -875,22 +919,24 @@ void positions_from_sel(cudaStream_t s, int* pos, const int* sel, const int* cou
   positions_from_sel_kernel<<<blocks_for(rows_max), kThreads, 0, s>>>(pos, sel, count, rows_max, base);
 }
 void iota_positions(cudaStream_t s, int* pos, int n, int base) {
-  iota_kernel<<<blocks_for(n), kThreads, 0, s>>>(pos, n, base);
+  launch_pdl(iota_kernel, dim3(blocks_for(n)), dim3(kThreads), 0, s, pos, n, base);
 }
 void mark_rows(cudaStream_t s, uint8_t* origin, int len, int lo, int hi, const int* sel,
                const int* count, int rows_max) {
   if (hi < lo) return;
-  mark_rows_kernel<<<blocks_for((size_t)rows_max * (hi - lo + 1)), kThreads, 0, s>>>(origin, len, lo, hi, sel, count, rows_max);
+  launch_pdl(mark_rows_kernel, dim3(blocks_for((size_t)rows_max * (hi - lo + 1))), dim3(kThreads), 0, s, origin, len, lo, hi, sel, count, rows_max);
 }
 void mark_layers(cudaStream_t s, uint8_t* origin, int len, int lo, int hi) {
   if (hi < lo) return;
-  mark_layers_kernel<<<blocks_for((size_t)(hi - lo + 1) * len), kThreads, 0, s>>>(origin, len, lo, hi);
+  launch_pdl(mark_layers_kernel, dim3(blocks_for((size_t)(hi - lo + 1) * len)), dim3(kThreads), 0, s, origin, len, lo, hi);
 }
 struct ZeroList {
   uint8_t* p[16];
   size_t n[16];
 };
-__global__ void zero_many_kernel(ZeroList z) {  // blockIdx.y = buffer
+__global__ void zero_many_kernel(ZeroList z) {
+  sm100::pdl_trigger();
+  sm100::pdl_wait();  // (blockIdx.y = buffer)
   uint8_t* dst = z.p[blockIdx.y];
   const size_t n = z.n[blockIdx.y];
   const size_t i0 = blockIdx.x * (size_t)blockDim.x + threadIdx.x, stride = (size_t)gridDim.x * blockDim.x;
@@ -914,18 +960,18 @@ void zero_many(cudaStream_t s, const std::vector<std::pair<void*, size_t>>& bufs
     }
     if (!mx) continue;
     const unsigned blocks = (unsigned)std::min<size_t>(256, (mx / 16 + kThreads - 1) / kThreads + 1);
-    zero_many_kernel<<<dim3(blocks, m), kThreads, 0, s>>>(z);
+    launch_pdl(zero_many_kernel, dim3(dim3(blocks, m)), dim3(kThreads), 0, s, z);
   }
 }
 void zero_dev(cudaStream_t s, void* dst, size_t bytes) {
   if (!bytes) return;
   const size_t blocks = std::min<size_t>(1184, (bytes / 16 + kThreads - 1) / kThreads + 1);
-  zero_bytes_kernel<<<(unsigned)blocks, kThreads, 0, s>>>(static_cast<uint8_t*>(dst), bytes);
+  launch_pdl(zero_bytes_kernel, dim3((unsigned)blocks), dim3(kThreads), 0, s, static_cast<uint8_t*>(dst), bytes);
 }
 void copy_dev(cudaStream_t s, void* dst, const void* src, size_t bytes) {
   if (!bytes) return;
   const size_t blocks = std::min<size_t>(1184, (bytes / 16 + kThreads - 1) / kThreads + 1);
-  copy_bytes_kernel<<<(unsigned)blocks, kThreads, 0, s>>>(static_cast<uint8_t*>(dst),
+  launch_pdl(copy_bytes_kernel, dim3((unsigned)blocks), dim3(kThreads), 0, s, static_cast<uint8_t*>(dst),
                                                           static_cast<const uint8_t*>(src), bytes);
 }
 void zero_rows(cudaStream_t s, void* dst, size_t pitch, size_t width, size_t rows) {
@@ -935,18 +981,18 @@ void zero_rows(cudaStream_t s, void* dst, size_t pitch, size_t width, size_t row
   zero_rows_kernel<<<grid, kThreads, 0, s>>>(static_cast<uint8_t*>(dst), pitch, width, rows);
 }
 void copy_i32(cudaStream_t s, int* dst, const int* src, int n) {
-  if (n > 0) copy_i32_kernel<<<std::min(64, blocks_for(n)), kThreads, 0, s>>>(dst, src, n);
+  if (n > 0) launch_pdl(copy_i32_kernel, dim3(std::min(64, blocks_for(n))), dim3(kThreads), 0, s, dst, src, n);
 }
 void fill_doubles(cudaStream_t s, double* dst, int n, double v) {
   fill_doubles_kernel<<<blocks_for(n), kThreads, 0, s>>>(dst, n, v);
 }
 void set_depth(cudaStream_t s, uint64_t* depth, int n, uint64_t v) {
-  set_depth_kernel<<<blocks_for(n), kThreads, 0, s>>>(depth, n, v);
+  launch_pdl(set_depth_kernel, dim3(blocks_for(n)), dim3(kThreads), 0, s, depth, n, v);
 }
 void argmax(cudaStream_t s, const float* x, int n, int* out, void* ws) {
   const int g = std::min(kArgBlocks, blocks_for((size_t)(n + 3) / 4));
-  argmax_partial_kernel<<<g, kThreads, 0, s>>>(x, n, static_cast<float2*>(ws));
-  argmax_final_kernel<<<1, kThreads, 0, s>>>(static_cast<const float2*>(ws), g, out);
+  launch_pdl(argmax_partial_kernel, dim3(g), dim3(kThreads), 0, s, x, n, static_cast<float2*>(ws));
+  launch_pdl(argmax_final_kernel, dim3(1), dim3(kThreads), 0, s, static_cast<const float2*>(ws), g, out);
 }
 
 void realign_graft(cudaStream_t s, const void* k_pre, const void* v_src, size_t elem, int L, int n,
@@ -958,7 +1004,7 @@ void realign_graft(cudaStream_t s, const void* k_pre, const void* v_src, size_t 
   const size_t vecs = (size_t)n * (kv * elem / 16);
   dim3 grid((unsigned)((vecs + 255) / 256), (unsigned)layers);
 #define RK_REALIGN_DH(T, D)                                                                                  \
-  realign_graft_dh_kernel<T, D><<<grid, 256, 0, s>>>((const T*)k_pre, (const T*)v_src, n, kv, rope, base,     \
+  launch_pdl(realign_graft_dh_kernel<T, D>, dim3(grid), dim3(256), 0, s, (const T*)k_pre, (const T*)v_src, n, kv, rope, base,     \
                                                      (T*)ctx_k, (T*)ctx_v, ctx_layer_stride, skip_lo, skip_hi)
   if (elem == 4 && dh == 64) RK_REALIGN_DH(float, 64);
   else if (elem == 4 && dh == 128) RK_REALIGN_DH(float, 128);
@@ -1049,7 +1095,7 @@ void score_deviation(cudaStream_t s, const void* ctx_v, const void* cache_v, con
     const size_t smem = (size_t)tok * 2 * heads * sizeof(double);
     const int grid = (n + tok - 1) / tok;
 #define RK_SCORE_DH(T, D)                                                                                      \
-  score_dh_kernel<T, D><<<grid, 256, smem, s>>>((const T*)ctx_v, (const T*)cache_v, (const T*)ctx_k,          \
+  launch_pdl(score_dh_kernel<T, D>, dim3(grid), dim3(256), smem, s, (const T*)ctx_v, (const T*)cache_v, (const T*)ctx_k,          \
                                                 (const T*)cache_kpre, n, heads, rope, base, s_dev, s_key)
     if (elem == 4 && dh == 64) RK_SCORE_DH(float, 64);
     else if (elem == 4) RK_SCORE_DH(float, 128);
@@ -1084,7 +1130,7 @@ void select_relay(cudaStream_t s, const double* s_dev, const float* influence,
   } else {
     seq_threshold_report_kernel<<<1, 1024, 0, s>>>(s_dev, n, tau_dev, dinfo);
   }
-  select_relay_kernel<<<1, 1024, 0, s>>>(s_dev, influence, infl_mean, n, tau_dev, tau_inf, suffix_k, sel_tags + n,
+  launch_pdl(select_relay_kernel, dim3(1), dim3(1024), 0, s, s_dev, influence, infl_mean, n, tau_dev, tau_inf, suffix_k, sel_tags + n,
                                          sel_idx, sel_tags, info);
 }
 void blend_scores(cudaStream_t s, const void* ctx_v, const void* cache_v, size_t elem, int n,
@@ -1109,6 +1155,8 @@ void seq_mean(cudaStream_t s, const float* x, int n, double* out) {
 namespace rk {
 namespace {
 __global__ void segment_offsets_kernel(k::SegCounts c, int U, int start, int* offs) {
+  sm100::pdl_trigger();
+  sm100::pdl_wait();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   int o = start;
   for (int u = 0; u < U; ++u) {
@@ -1120,6 +1168,8 @@ __global__ void segment_offsets_kernel(k::SegCounts c, int U, int start, int* of
 // H[off + r] = src[idx[r]]; pos[off + r] = base + idx[r]
 __global__ void gather_rows_to_kernel(float* H, const int* off, const float* src, const int* idx, const int* count,
                                       int d, int* pos, int base) {
+  sm100::pdl_trigger();
+  sm100::pdl_wait();
   const int rows = *count, o = *off;
   const size_t total = (size_t)rows * d;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
@@ -1131,6 +1181,8 @@ __global__ void gather_rows_to_kernel(float* H, const int* off, const float* src
 // dst[idx[r]] = H[off + r]; depth[idx[r]] = value
 __global__ void scatter_rows_from_kernel(float* dst, const float* H, const int* off, const int* idx, const int* count,
                                          int d, uint64_t* depth, uint64_t value) {
+  sm100::pdl_trigger();
+  sm100::pdl_wait();
   const int rows = *count, o = *off;
   const size_t total = (size_t)rows * d;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
@@ -1143,17 +1195,17 @@ __global__ void scatter_rows_from_kernel(float* dst, const float* H, const int* 
 
 namespace k {
 void segment_offsets(cudaStream_t s, const SegCounts& c, int U, int start, int* offs) {
-  segment_offsets_kernel<<<1, 32, 0, s>>>(c, U, start, offs);
+  launch_pdl(segment_offsets_kernel, dim3(1), dim3(32), 0, s, c, U, start, offs);
 }
 void gather_rows_to(cudaStream_t s, float* H, const int* off, const float* src, const int* idx, const int* count,
                     int rows_max, int d, int* pos, int base) {
   const size_t total = (size_t)rows_max * d;
-  gather_rows_to_kernel<<<blocks_for(total) < 4096 ? blocks_for(total) : 4096, kThreads, 0, s>>>(H, off, src, idx, count, d, pos, base);
+  launch_pdl(gather_rows_to_kernel, dim3(blocks_for(total) < 4096 ? blocks_for(total) : 4096), dim3(kThreads), 0, s, H, off, src, idx, count, d, pos, base);
 }
 void scatter_rows_from(cudaStream_t s, float* dst, const float* H, const int* off, const int* idx, const int* count,
                        int rows_max, int d, uint64_t* depth, uint64_t value) {
   const size_t total = (size_t)rows_max * d;
-  scatter_rows_from_kernel<<<blocks_for(total) < 4096 ? blocks_for(total) : 4096, kThreads, 0, s>>>(dst, H, off, idx, count, d, depth, value);
+  launch_pdl(scatter_rows_from_kernel, dim3(blocks_for(total) < 4096 ? blocks_for(total) : 4096), dim3(kThreads), 0, s, dst, H, off, idx, count, d, depth, value);
 }
 }  // namespace k
 }  // namespace rk
