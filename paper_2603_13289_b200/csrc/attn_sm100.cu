@@ -541,6 +541,8 @@ __device__ __forceinline__ void attn_combine_one(const AttnArgs& a, int row, int
 // far below rows_max in sparse passes)
 template <int DH>
 __global__ void attn_combine_kernel(const AttnArgs a) {
+  pdl_trigger();
+  pdl_wait();
   const int M = a.rows_dev ? *a.rows_dev : a.rows_max;
   const int lane = threadIdx.x % 32;
   const long long n = (long long)M * a.H;
@@ -597,7 +599,16 @@ void launch_attn(rk_engine* e, const CUtensorMap& tq, const CUtensorMap& tk, con
   else go(attn_kernel<DH, false>);
   if (a.splits > 1) {
     const int warps = a.rows_max * a.H;
-    attn_combine_kernel<DH><<<std::min((warps + 7) / 8, 4 * e->sm_count), 256, 0, e->stream>>>(a);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(std::min((warps + 7) / 8, 4 * e->sm_count));
+    cfg.blockDim = dim3(256);
+    cfg.stream = e->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    RK_CUDA(cudaLaunchKernelEx(&cfg, attn_combine_kernel<DH>, a));
     e->launches += 1;
   }
 }

@@ -7,15 +7,33 @@
 
 #include "layer.h"
 #include "layer_bf16.h"
+#include "sm100.cuh"
 
 namespace rk {
 namespace {
+// 256-thread launch with programmatic stream serialization (sm100.cuh pdl_*).
+template <typename... KArgs, typename... Args>
+void launch_pdl1(void (*kern)(KArgs...), dim3 grid, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  RK_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
+}
+
 
 __device__ __forceinline__ int live(const Rows& r) { return r.rows_dev ? *r.rows_dev : r.rows_max; }
 
 // rms_norm (tensor.cpp:109-119) in fp32, output bf16 (GEMM operand). One warp per row.
 __global__ void rmsnorm_bf16_kernel(const float* __restrict__ x, const float* __restrict__ gain, float eps,
                                     __nv_bfloat16* __restrict__ out, Rows rows, int d) {
+  sm100::pdl_trigger();
+  sm100::pdl_wait();
   const int M = live(rows);
   const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -43,6 +61,8 @@ __global__ void rmsnorm_bf16_kernel(const float* __restrict__ x, const float* __
 // into the weights) and 1/rms per row, applied in the consumer's epilogue.
 __global__ void norm_prep_kernel(const float* __restrict__ x, float eps, __nv_bfloat16* __restrict__ out,
                                  float* __restrict__ inv, Rows rows, int d) {
+  sm100::pdl_trigger();
+  sm100::pdl_wait();
   const int M = live(rows);
   const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -92,7 +112,7 @@ static int* split_flags(rk_engine* e) {
 void rmsnorm_bf16(cudaStream_t st, const float* x, const float* gain, float eps, __nv_bfloat16* out, Rows rows,
                   int d) {
   if (rows.rows_max <= 0) return;
-  rmsnorm_bf16_kernel<<<(rows.rows_max + 7) / 8, 256, 0, st>>>(x, gain, eps, out, rows, d);
+  launch_pdl1(rmsnorm_bf16_kernel, dim3((rows.rows_max + 7) / 8), st, x, gain, eps, out, rows, d);
 }
 
 // Fused-RMSNorm buffers (scratch): per-row 1/rms, partial sums, m-tile counters.
@@ -141,7 +161,7 @@ void run_layer_bf16(rk_engine* e, rk_weights* w, rk_context* ctx, int l, float* 
 
   const NormBufs nb = norm_bufs(e, (size_t)rows.rows_max);
   if (!prepared) {  // else the previous layer's down GEMM left bf16 rows + 1/rms
-    norm_prep_kernel<<<(rows.rows_max + 7) / 8, 256, 0, st>>>(hidden, s.norm_eps, normed, nb.inv, rows, d);
+    launch_pdl1(norm_prep_kernel, dim3((rows.rows_max + 7) / 8), st, hidden, s.norm_eps, normed, nb.inv, rows, d);
     e->launches += 1;
   }
   GemmArgs g;
