@@ -386,14 +386,18 @@ def run_ours(args, world, rank, local, dist):
     for _ in range(e2e_K):
         e2e_step()
     e2e_ms = reduce_max(dist, (time.perf_counter() - h0) * 1e3, local) / e2e_K  # one session per rank
-    # the upload alone (diagnostic: how much of e2e is PCIe)
-    h0 = time.perf_counter()
-    for _ in range(e2e_K):
+    # the upload alone (diagnostic: how much of e2e is PCIe); median of
+    # per-iteration times (an nvidia-smi sample of the clock sampler can stall
+    # the driver's enqueue for tens of ms)
+    ups_ms = []
+    for _ in range(max(e2e_K, 5)):
+        h0 = time.perf_counter()
         ups = [w.upload_cache(h, asynchronous=True) for h in hosts]
         for c in ups:
             c.wait()
+        ups_ms.append((time.perf_counter() - h0) * 1e3)
         del ups
-    upload_ms = (time.perf_counter() - h0) * 1e3 / e2e_K
+    upload_ms = statistics.median(ups_ms)
     # bytes that cross PCIe: fp32 K/V, unless RK_HOST_CONVERT=1 converts them
     # to bf16 on the host first (rk_cache_upload_async), then half of that
     kv_div = 2 if os.environ.get("RK_HOST_CONVERT", "0") != "0" else 1
