@@ -1,5 +1,5 @@
 #!/bin/bash
-OUT=gpurun_out/cfg4; mkdir -p $OUT
+OUT=gpurun_out/cfg5; mkdir -p $OUT
 timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu > $OUT/bench_c2.json 2> $OUT/bench_c2.err
 for c in c3 c4; do
   timeout 900 python bench.py --config $c --steps 5 --warmup 3 --no-cpu > $OUT/bench_$c.json 2> $OUT/bench_$c.err
