@@ -370,10 +370,16 @@ def run_ours(args, world, rank, local, dist):
     # (rk_cache_upload), tokens staged, logits read back.
     hosts = [pin_host(c.to_host()) for c in caches]
 
+    # layers l_start..l_det-1 of every cache are never read by the relay (the
+    # band recomputes them; l_det is read by the deviation score): they are
+    # held back (rk_cache_upload_async_defer) and never cross PCIe
+    l_start, l_det = WL["profile"][0], WL["profile"][1]
+    defer = (l_start, l_det - 1) if l_det > l_start else None
+
     def e2e_step():
         # layer-streamed uploads: the relay prefill starts while later layers
         # of the caches are still crossing PCIe (rk_cache_upload_async)
-        ups = [w.upload_cache(h, asynchronous=True) for h in hosts]
+        ups = [w.upload_cache(h, asynchronous=True, defer=defer) for h in hosts]
         ctx.reset()
         out = ctx.agent_prefill(mine[0]["prefix"], ups, mine[0]["suffix"], prof, opts, want_logits=True)
         return out["first_token"]
@@ -392,16 +398,17 @@ def run_ours(args, world, rank, local, dist):
     ups_ms = []
     for _ in range(max(e2e_K, 5)):
         h0 = time.perf_counter()
-        ups = [w.upload_cache(h, asynchronous=True) for h in hosts]
+        ups = [w.upload_cache(h, asynchronous=True, defer=defer) for h in hosts]
         for c in ups:
-            c.wait()
+            c.xfer_wait()
         ups_ms.append((time.perf_counter() - h0) * 1e3)
         del ups
     upload_ms = statistics.median(ups_ms)
     # bytes that cross PCIe: fp32 K/V, unless RK_HOST_CONVERT=1 converts them
     # to bf16 on the host first (rk_cache_upload_async), then half of that
     kv_div = 2 if os.environ.get("RK_HOST_CONVERT", "0") != "0" else 1
-    h2d = sum((h.k_pre.nbytes + h.v.nbytes) // kv_div + h.hidden_snapshot.nbytes + h.influence.nbytes +
+    sent = 1.0 - ((defer[1] - defer[0] + 1) / WL["spec"]["num_layers"] if defer else 0.0)
+    h2d = sum(int((h.k_pre.nbytes + h.v.nbytes) * sent) // kv_div + h.hidden_snapshot.nbytes + h.influence.nbytes +
               h.segment_tokens.nbytes for h in hosts) + 4 * (WL["prefix"] + WL["suffix"])
     d2h = 4 * WL["spec"]["vocab_size"] + 4
 

@@ -235,8 +235,17 @@ int rk_cache_capture_prefill(rk_engine* e, rk_weights* w, rk_context* ctx,
  * memory makes the copies truly asynchronous. */
 int rk_cache_upload_async(rk_engine* e, rk_weights* w, const rk_relay_cache_view* view,
                           rk_cache** out);
-/* Block until an asynchronous upload has landed (the host arrays may be freed). */
+/* rk_cache_upload_async with layers [defer_lo, defer_hi] held back: each of
+ * them crosses PCIe only when a later call first reads it (a relay with
+ * profile (l_start, l_det, l_end) never reads layers l_start..l_det-1). */
+int rk_cache_upload_async_defer(rk_engine* e, rk_weights* w, const rk_relay_cache_view* view,
+                                uint64_t defer_lo, uint64_t defer_hi, rk_cache** out);
+/* Block until an asynchronous upload has landed, deferred layers included
+ * (the host arrays may be freed afterwards). */
 int rk_cache_wait(rk_cache* c);
+/* Block until the copies issued so far have landed; deferred layers stay
+ * deferred (the host arrays must stay valid). */
+int rk_cache_sync(rk_cache* c);
 uint64_t rk_cache_segment_len(const rk_cache* c);
 /* Copy a cache back to host (fp32). Any pointer may be NULL. k_pre/v: [L] arrays of [n x kv]. */
 int rk_cache_export(rk_cache* c, int32_t* tokens, float* const* k_pre, float* const* v,

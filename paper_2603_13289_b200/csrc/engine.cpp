@@ -336,6 +336,32 @@ rk_weights* new_weights(rk_engine* e, const rk_model_spec* spec, int precision) 
 // ============================================================================
 // C ABI
 // ============================================================================
+namespace rk {
+// Upload a deferred layer (rk_cache_upload_async_defer) on the cache's copy
+// stream the first time something reads it.
+void ensure_cache_layer(rk_cache* c, uint64_t l) {
+  if (c->deferred.empty() || !c->deferred[l]) return;
+  const size_t n = c->n, kv = c->kv();
+  for (int which = 0; which < 2; ++which) {
+    const float* src = which == 0 ? c->host_k[l] : c->host_v[l];
+    char* dst = static_cast<char*>(which == 0 ? c->k_pre.p : c->v.p) + l * n * kv * c->elem;
+    if (c->elem == 4) {
+      RK_CUDA(cudaMemcpyAsync(dst, src, n * kv * 4, cudaMemcpyHostToDevice, c->xfer));
+    } else {
+      float* stage = c->staging.as<float>() + (size_t)which * n * kv;
+      RK_CUDA(cudaMemcpyAsync(stage, src, n * kv * 4, cudaMemcpyHostToDevice, c->xfer));
+      k::f32_to_bf16(c->xfer, reinterpret_cast<__nv_bfloat16*>(dst), stage, n * kv);
+    }
+  }
+  RK_CUDA(cudaEventCreateWithFlags(&c->ev_layer[l], cudaEventDisableTiming));
+  RK_CUDA(cudaEventRecord(c->ev_layer[l], c->xfer));
+  c->deferred[l] = 0;
+}
+void ensure_cache_all(rk_cache* c) {
+  for (uint64_t l = 0; l < c->deferred.size(); ++l) ensure_cache_layer(c, l);
+}
+}  // namespace rk
+
 extern "C" {
 
 int rk_abi_version(void) { return RK_ABI_VERSION; }
@@ -524,7 +550,8 @@ inline uint32_t* c_flags_of(char* stage, uint64_t R, size_t slot) {
 }
 // RelayCache::validate + upload (relay_cache.cpp:18-41). async: everything on
 // the copy stream with per-layer events, no host synchronization.
-rk_cache* upload_cache(rk_engine* e, rk_weights* w, const rk_relay_cache_view* v, bool async) {
+rk_cache* upload_cache(rk_engine* e, rk_weights* w, const rk_relay_cache_view* v, bool async, uint64_t defer_lo = 1,
+                       uint64_t defer_hi = 0) {
   require(v != nullptr && w != nullptr, RK_ERR_INVALID_ARGUMENT, "null cache view / weights");
   const uint64_t n = v->segment_len;
   require(n > 0, RK_ERR_INVALID_ARGUMENT, "relay cache: empty segment");
@@ -647,8 +674,17 @@ rk_cache* upload_cache(rk_engine* e, rk_weights* w, const rk_relay_cache_view* v
   // device; two staging buffers alternate (stream order keeps them safe, no
   // host round trip), so pinned sources stream at copy-engine speed
   if (c->elem == 2) c->staging.alloc_pooled(pl, 2 * n * kv * 4);
+  if (async && defer_lo <= defer_hi) {  // these layers cross PCIe only if a later call reads them
+    c->deferred.assign(c->L, 0);
+    c->host_k.assign(v->k_pre, v->k_pre + c->L);
+    c->host_v.assign(v->v, v->v + c->L);
+  }
   int flip = 0;
   for (uint64_t l = 0; l < c->L; ++l) {
+    if (!c->deferred.empty() && l >= defer_lo && l <= defer_hi) {
+      c->deferred[l] = 1;
+      continue;
+    }
     for (int which = 0; which < 2; ++which) {
       const float* src = which == 0 ? v->k_pre[l] : v->v[l];
       char* dst = static_cast<char*>(which == 0 ? c->k_pre.p : c->v.p) + l * n * kv * c->elem;
@@ -688,7 +724,28 @@ int rk_cache_upload_async(rk_engine* e, rk_weights* w, const rk_relay_cache_view
   });
 }
 
+int rk_cache_upload_async_defer(rk_engine* e, rk_weights* w, const rk_relay_cache_view* v, uint64_t defer_lo,
+                                uint64_t defer_hi, rk_cache** out) {
+  return guard([&] {
+    DeviceGuard g(e->device);
+    require(v != nullptr && defer_lo <= defer_hi && defer_hi < v->num_layers, RK_ERR_INVALID_ARGUMENT,
+            "deferred layer range out of bounds");
+    *out = upload_cache(e, w, v, true, defer_lo, defer_hi);
+  });
+}
+
+
+
 int rk_cache_wait(rk_cache* c) {
+  return guard([&] {
+    require(c != nullptr, RK_ERR_INVALID_ARGUMENT, "null cache");
+    DeviceGuard g(c->e->device);
+    ensure_cache_all(c);  // the host arrays may be freed after this call
+    if (c->async) RK_CUDA(cudaStreamSynchronize(c->xfer));
+  });
+}
+
+int rk_cache_sync(rk_cache* c) {
   return guard([&] {
     require(c != nullptr, RK_ERR_INVALID_ARGUMENT, "null cache");
     DeviceGuard g(c->e->device);
@@ -702,6 +759,7 @@ namespace {
 void export_cache(rk_cache* c, int32_t* tokens, float* const* k_pre, float* const* v, float* hidden,
                   float* influence) {
   DeviceGuard g(c->e->device);
+  ensure_cache_all(c);
   if (c->async) RK_CUDA(cudaStreamSynchronize(c->xfer));
   cudaStream_t st = c->e->stream;
   const size_t kv = c->kv(), n = c->n;
@@ -1153,6 +1211,8 @@ int rk_token_deviation(rk_cache* reuse, rk_cache* full, double* value_cos, doubl
             "token_deviation: kv width not divisible by head count");
     DeviceGuard g(reuse->e->device);
     rk_engine* e = reuse->e;
+    ensure_cache_all(reuse);
+    ensure_cache_all(full);
     if (reuse->async) RK_CUDA(cudaStreamSynchronize(reuse->xfer));
     if (full->async) RK_CUDA(cudaStreamSynchronize(full->xfer));
     const size_t n = reuse->n, L = reuse->L;

@@ -158,6 +158,10 @@ struct rk_cache {
   cudaStream_t xfer = nullptr;
   cudaEvent_t ev_meta = nullptr;
   std::vector<cudaEvent_t> ev_layer;
+  // deferred layers (rk_cache_upload_async_defer): uploaded from the host view
+  // the first time a call reads them
+  std::vector<uint8_t> deferred;
+  std::vector<const float*> host_k, host_v;
   rk::DevBuf staging;  // fp32 layer staging of the bf16 conversion
   // host-converted upload (bf16 weights, async): the engine's uploader thread
   // converts layer l into a ring of pinned bf16 slots and sets flags[l]; the
@@ -215,6 +219,8 @@ struct Rows {
   int g1 = 0, g2 = 0;
 };
 
+void ensure_cache_layer(rk_cache* c, uint64_t l);  // engine.cpp: upload a deferred layer now
+void ensure_cache_all(rk_cache* c);
 bool pdl_enabled();  // programmatic dependent launch (RK_PDL, default on), gemm_sm100.cu
 
 // ---- kernel launchers (kernels_*.cu) -------------------------------------

@@ -170,13 +170,20 @@ class Weights(_Obj):
         _check(lib().rk_context_create(P(self.engine.ptr), P(self.ptr), C.byref(out)))
         return Context(out.value, self)
 
-    def upload_cache(self, host, asynchronous=False):
+    def upload_cache(self, host, asynchronous=False, defer=None):
         """RelayCache host arrays -> device (rk_cache_upload). asynchronous:
         rk_cache_upload_async -- layers stream in on the copy stream while
-        later calls run; the host arrays stay referenced by the Cache."""
+        later calls run; the host arrays stay referenced by the Cache.
+        defer=(lo, hi) (asynchronous only): those layers cross PCIe only when
+        a later call reads them (rk_cache_upload_async_defer)."""
         out = P()
-        fn = lib().rk_cache_upload_async if asynchronous else lib().rk_cache_upload
-        _check(fn(P(self.engine.ptr), P(self.ptr), C.byref(host.view()), C.byref(out)))
+        if defer is not None:
+            assert asynchronous, "deferred layers need an asynchronous upload"
+            _check(lib().rk_cache_upload_async_defer(P(self.engine.ptr), P(self.ptr), C.byref(host.view()),
+                                                     U64(defer[0]), U64(defer[1]), C.byref(out)))
+        else:
+            fn = lib().rk_cache_upload_async if asynchronous else lib().rk_cache_upload
+            _check(fn(P(self.engine.ptr), P(self.ptr), C.byref(host.view()), C.byref(out)))
         c = Cache(out.value, self)
         if asynchronous:
             c._host = host
@@ -204,8 +211,14 @@ class Cache(_Obj):
         return int(lib().rk_cache_segment_len(P(self.ptr)))
 
     def wait(self):
-        """Block until an asynchronous upload has landed (rk_cache_wait)."""
+        """Block until an asynchronous upload has landed, deferred layers
+        included (rk_cache_wait): the host arrays may be freed afterwards."""
         _check(lib().rk_cache_wait(P(self.ptr)))
+
+    def xfer_wait(self):
+        """Block until the copies issued so far have landed (deferred layers
+        stay deferred) -- a diagnostic for timing the upload alone."""
+        _check(lib().rk_cache_sync(P(self.ptr)))
 
     def save(self, path):
         """save_relay_cache (relay_cache.cpp:238-245): the RKRC file (rk_cache_save)."""

@@ -308,3 +308,25 @@ def test_profile_model_bf16_runs(engine):
     got = profile_model(engine.weights(spec, 9, "bf16"), TwoStageConfig.make(instances=2, segment_len=16))
     assert got["l_start"] <= got["l_det"] <= got["l_end"] < 8
     assert np.isfinite(got["curve_s"]).all()
+
+
+@pytest.mark.parametrize("mode", ["relay", "zero", "blend"])
+def test_deferred_layers_bit_exact(engine, oracle, mode):
+    """rk_cache_upload_async_defer: the held-back layers are uploaded when a
+    call first reads them (ZERO and BLEND read them, RELAY with the band over
+    them does not) -- same bits as the plain upload, and export sees them."""
+    spec = spec_of(6, 64, 4, kv_heads=2)
+    ow = oracle.weights(spec, 31)
+    c1 = oracle.scenario(ow, pattern_tokens(9, 64, 1), 16, 1)
+    c2 = oracle.scenario(ow, pattern_tokens(7, 64, 2), 11, 1)
+    prof = triple(1, 3, 4) if mode == "relay" else LayerProfile()
+    opts = RelayOptions.make(mode=mode, suffix_k=3, blend_alpha=0.5)
+    res = []
+    for defer in (None, (1, 2)):
+        w = engine.weights(spec, 31)
+        ups = [w.upload_cache(c, asynchronous=True, defer=defer) for c in (c1, c2)]
+        out = w.context().agent_prefill(pattern_tokens(5, 64, 3), ups, pattern_tokens(4, 64, 4), prof, opts)
+        res.append(out["logits"])
+        back = ups[0].to_host()
+        assert_bit_equal(back.k_pre, c1.k_pre, f"defer.{mode}.export")
+    assert_bit_equal(res[1], res[0], f"defer.{mode}.logits")
