@@ -130,3 +130,20 @@ def test_fullsize_marks_selection_accounting(full):
         dev = sel[(tags & 1) != 0]
         assert (seg["s_dev"][dev] >= thr).all()
         assert (seg["s_dev"][np.setdiff1d(np.arange(n), dev)] < thr).all()
+
+
+def test_fullsize_streamed_upload_matches_resident(full):
+    """The e2e path at full size: host caches streamed in by layer (with the
+    band layers deferred) while the relay runs -- every kernel launched with
+    programmatic dependent launch behind a per-layer event wait -- gives the
+    same bits as caches already resident on the device."""
+    bench, w, sess, prof, opts = full
+    ref = run(sess, prof, opts)
+    hosts = [bench.pin_host(c.to_host()) for c in sess["caches"]]
+    defer = (prof.l_start, prof.l_det - 1) if prof.l_det > prof.l_start else None
+    for _ in range(2):
+        ups = [w.upload_cache(h, asynchronous=True, defer=defer) for h in hosts]
+        sess["ctx"].reset()
+        got = sess["ctx"].agent_prefill(sess["prefix"], ups, sess["suffix"], prof, opts, want_logits=True)
+        assert got["first_token"] == ref["first_token"]
+        assert np.array_equal(got["logits"].view(np.uint32), ref["logits"].view(np.uint32))
