@@ -1148,7 +1148,11 @@ static void choose_config(GemmArgs& p, int sm_count, int rows_hint) {
   p.streamk = 0;
   const int kb = p.K / kBK;
   auto ceil_div = [](long long a, long long b) { return (int)((a + b - 1) / b); };
-  auto t_kb = [](int a_kb, int b_kb) { return 0.0096 * (a_kb + b_kb); };  // us per k-block of one unit
+  // us per k-block of one unit: the staged bytes at the L2->SM feed rate.
+  // (RK_GEMM_TKB_FLOOR_NS=450 floors it at a k-block round trip -- closer for
+  // narrow tiles, but the extra split-K it then picks measured slower on c2.)
+  static const double t_floor = env("RK_GEMM_TKB_FLOOR_NS", 0) * 1e-3;
+  auto t_kb = [](int a_kb, int b_kb) { return std::max(t_floor, 0.0096 * (a_kb + b_kb)); };
 
   // 1-CTA (or pair) tiles, BN by the fill rule
   const int pslots = pair_env ? pair_slots(sm_count) : 0;
@@ -1172,7 +1176,7 @@ static void choose_config(GemmArgs& p, int sm_count, int rows_hint) {
   if (p.N % bn) raise(RK_ERR_INVALID_ARGUMENT, "bf16 GEMM needs N % 64 == 0");
   p.bn = bn;
   double best = (double)ceil_div((long long)num_m * (p.N / bn), slots) * kb *
-                (p.pair == 2 ? 0.42 * bn / 256.0 : t_kb(16, bn / 8));
+                (p.pair == 2 ? std::max(0.42 * bn / 256.0, t_floor * 0.93) : t_kb(16, bn / 8));
 
   const bool residual_split = p.epi == EPI_ADD && p.split_flags;
   auto part_cost = [&](int s) { return s > 1 ? 3.0 + 2.0 * s * (double)rows_hint * p.N * 4 / 8e6 : 0.0; };
