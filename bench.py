@@ -164,7 +164,8 @@ def dist_setup(args):
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
+        if args.impl == "ours":
+            torch.cuda.set_device(local)
         dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
     return world, rank, local, dist
 
@@ -173,9 +174,26 @@ def reduce_max(dist, value, local):
     if dist is None:
         return value
     import torch
-    t = torch.tensor([value], dtype=torch.float64, device=f"cuda:{local}")
+    dev = f"cuda:{local}" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([value], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def free_port():
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_ranks(argv, gpus):
+    """`python bench.py --gpus N` outside torchrun: re-launch this script as N
+    ranks (one process per GPU, torch.distributed.run on 127.0.0.1) and pass
+    rank 0's JSON line through. Returns the launcher's exit code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + argv
+    return subprocess.call(cmd)
 
 
 def barrier(dist):
@@ -184,11 +202,53 @@ def barrier(dist):
 
 
 # ---- the reference CPU path ------------------------------------------------------
-def cpu_sample(gpu_caches=None, threads=None, steps=1, warmup=0, kind="reference"):
+def reference_work(spec, prefix, seg_lens, suffix, selected, profile):
+    """FLOPs the reference spends on the downstream agent's TTFT, by its own
+    FLOP model (relay_engine.cpp:72-128: flops_span_full for the prefix and
+    suffix prefills, flops_segment_schedule per relayed segment at its base)
+    plus the all-row logits its prefill computes (model.cpp:328, 2*d*V per
+    prefix and suffix row; the engine computes only the last row). The CPU
+    reference is a plain i-k-j fp32 loop (tensor.cpp:66-86) whose time per
+    FLOP barely depends on the shape, which is what makes a bounded sample
+    extrapolate (checked against a full c2 run: profiles/r02_cpu_full_c2.json)."""
+    d, kv, ff = spec.d_model, spec.num_kv_heads * spec.d_head, spec.d_ff
+    L, dhH, V = spec.num_layers, spec.d_head * spec.num_heads, spec.vocab_size
+    pm = 2.0 * d * (2.0 * d + 2.0 * kv) + 6.0 * d * ff
+
+    def attn(b, n):
+        return 4.0 * dhH * (n * b + n * (n + 1.0) / 2.0)
+
+    def span(b, n):
+        return L * n * pm + L * attn(b, n)
+
+    l_start, l_det, l_end = profile
+    total, base = span(0, prefix), prefix
+    for n, sel in zip(seg_lens, selected):
+        avg = base + (n + 1.0) / 2.0
+        total += (l_det - l_start + 1) * (n * pm + attn(base, n)) + (l_end - l_det) * sel * (pm + 4.0 * dhH * avg)
+        base += n
+    total += span(base, suffix)
+    total += 2.0 * d * V * (prefix + suffix)
+    return total
+
+
+def full_c2_reference_run():
+    """The committed one-off run of the reference on the FULL c2 prompt (tools/cpu_full_c2.py)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_cpu_full_c2.json")) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def cpu_sample(gpu_caches=None, threads=None, steps=1, warmup=0, kind="reference", full_selected=None):
     """Time the reference's own relay path (oracle/_ref: the reference library
     built from its sources) -- or the restatement if _ref is absent -- on a
     bounded sample of the workload: same model, prefix/segments/suffix cut to
-    WL["cpu"] tokens, one independent session per host core. Returns (tokens/s, meta)."""
+    WL["cpu"] tokens. One session on one core (latency), then one independent
+    session per host core (throughput). Both are extrapolated to the FULL
+    prompt of the GPU arm with the reference's FLOP model (reference_work),
+    and labelled as such. Returns (full-prompt tokens/s on all cores, meta)."""
     from oracle.oracle import Oracle, available
     if kind == "reference" and not available("reference"):
         kind = "restatement"
@@ -197,20 +257,30 @@ def cpu_sample(gpu_caches=None, threads=None, steps=1, warmup=0, kind="reference
     w = orc.weights(spec, SEED, checked=(kind == "reference"))
     pr = prompts(0)
     cp, cs, cx = WL["cpu"]
-    caches = []
-    for host in gpu_caches:
-        c = host.copy()
-        c.segment_tokens = c.segment_tokens[:cs].copy()
-        c.k_pre = np.ascontiguousarray(c.k_pre[:, :cs])
-        c.v = np.ascontiguousarray(c.v[:, :cs])
-        c.hidden_snapshot = np.ascontiguousarray(c.hidden_snapshot[:cs])
-        c.influence = np.ascontiguousarray(c.influence[:cs])
-        c.decode_steps_observed = cs
-        caches.append(c)
-    prof, opts = options()
     last = WL["agents"] - 1
+    if gpu_caches is None:  # the reference's own decode-time captures of the cut segments
+        caches = [orc.scenario(w, pr[f"a{a}_prefix"][:cp], cs, WL["profile"][0]) for a in range(last)]
+    else:
+        caches = []
+        for host in gpu_caches:
+            c = host.copy()
+            c.segment_tokens = c.segment_tokens[:cs].copy()
+            c.k_pre = np.ascontiguousarray(c.k_pre[:, :cs])
+            c.v = np.ascontiguousarray(c.v[:, :cs])
+            c.hidden_snapshot = np.ascontiguousarray(c.hidden_snapshot[:cs])
+            c.influence = np.ascontiguousarray(c.influence[:cs])
+            c.decode_steps_observed = cs
+            caches.append(c)
+    prof, opts = options()
     prefix, suffix = pr[f"a{last}_prefix"][:cp], pr[f"a{last}_suffix"][:cx]
     tokens = len(prefix) + sum(c.segment_len for c in caches) + len(suffix)
+    # one core, one session (also yields the sample's selection for its work figure)
+    t0 = time.perf_counter()
+    _, _, ctx = orc.agent_prefill(w, prefix, caches, suffix, prof, opts)
+    ms1 = (time.perf_counter() - t0) * 1e3
+    l_det = WL["profile"][1]
+    sel = [int(sg[2][l_det + 1].sum()) if l_det + 1 < spec.num_layers else 0 for sg in orc.ctx_segments(ctx)]
+    work_sample = reference_work(spec, len(prefix), [c.segment_len for c in caches], len(suffix), sel, WL["profile"])
     threads = threads or (os.cpu_count() or 1)
     times = []
     for i in range(warmup + steps):
@@ -218,19 +288,36 @@ def cpu_sample(gpu_caches=None, threads=None, steps=1, warmup=0, kind="reference
             ms, _ = orc.agent_prefill_parallel(w, threads, prefix, caches, suffix, prof, opts)
             used = threads
         else:
-            t0 = time.perf_counter()
-            orc.agent_prefill(w, prefix, caches, suffix, prof, opts)
-            ms = (time.perf_counter() - t0) * 1e3
-            used = 1
+            ms, used = ms1, 1
         if i >= warmup:
             times.append(ms)
     ms = sum(times) / len(times)
-    tps = used * tokens / (ms / 1e3)
+    # the full prompt of the GPU arm
+    n_full = prompt_tokens()
+    full_sel = full_selected or [int(round(0.25 * WL["segment"]))] * last
+    work_full = reference_work(spec, WL["prefix"], [WL["segment"]] * last, WL["suffix"], full_sel, WL["profile"])
+    scale = work_full / work_sample
+    ttft1_ms = ms1 * scale           # one session, one core
+    ttftN_ms = ms * scale            # `used` concurrent sessions (memory-bandwidth shared)
+    tps = used * n_full / (ttftN_ms / 1e3)
     meta = {"kind": "reference" if kind == "reference" else "port", "cores": used,
-            "sample": f"{WL['title'].split(':')[0]} model, prefix {cp} + {len(caches)} relayed segments x "
-                      f"{cs} + suffix {cx} = {tokens} tokens per session, {used} concurrent sessions, "
-                      f"profile {WL['profile']}",
-            "ms_per_session_step": ms, "host": host_info()}
+            "extrapolated": True,
+            "sample": f"{WL['title'].split(':')[0]} model, measured on prefix {cp} + {len(caches)} relayed segments x "
+                      f"{cs} + suffix {cx} = {tokens} tokens per session ({used} concurrent sessions); extrapolated "
+                      f"to the GPU arm's {n_full}-token prompt by the reference's FLOP model (relay_engine.cpp:72-128 "
+                      f"+ all-row prefill logits): x{scale:.1f} work",
+            "sample_ms_per_session": round(ms, 3), "sample_ms_one_core": round(ms1, 3),
+            "sample_tokens_per_s": round(used * tokens / (ms / 1e3), 4),
+            "sample_gflop_per_s_per_core": round(work_sample / (ms1 / 1e3) / 1e9, 3),
+            "full_prompt_selected_per_segment": full_sel,
+            "full_prompt_ttft_ms_one_core_extrapolated": round(ttft1_ms, 1),
+            "full_prompt_ttft_ms_all_cores_extrapolated": round(ttftN_ms, 1),
+            "host": host_info()}
+    ref = full_c2_reference_run() if WL is WORKLOADS["c2"] else None
+    if ref:
+        meta["full_prompt_measured_once"] = {k: ref.get(k) for k in ("ttft_ms", "tokens_per_s_one_core",
+                                                                    "gflops_per_s", "workload", "host",
+                                                                    "measured_in")}
     return tps, meta
 
 
@@ -295,6 +382,59 @@ def build_session(w, session):
     last = WL["agents"] - 1
     return {"caches": caches, "prefix": pr[f"a{last}_prefix"], "suffix": pr[f"a{last}_suffix"],
             "ctx": w.context(), "session": session}
+
+
+def _rel_l2(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def exact_leg(eng, w, timed):
+    """The fp32-exact mode (bit-identical to the reference: tests/test_gpu_wide.py
+    at c2/c3 width) on the SAME workload: its TTFT, and the bf16 throughput
+    mode's own error against it on the same relay caches (north_star: "a bf16
+    throughput mode reports its own max error"): logits, first token, per
+    segment selection Jaccard and |I|, K/V and segment hidden rel-L2."""
+    wx = eng.weights(spec_obj(), SEED, "fp32")
+    sx = build_session(wx, 0)  # fp32-exact captures of the upstream agents' segments
+    hosts = [c.to_host() for c in sx["caches"]]
+    prof, opts = options()
+
+    def run(ctx, caches, outputs=False):
+        ctx.reset()
+        return ctx.agent_prefill(sx["prefix"], caches, sx["suffix"], prof, opts, want_logits=True, outputs=outputs)
+
+    rx = run(sx["ctx"], sx["caches"], True)
+    dev_ms, _, launches = timed(lambda: run(sx["ctx"], sx["caches"]), 2, 1)
+    Kx, Vx = sx["ctx"].all()
+    cb = [w.upload_cache(h) for h in hosts]
+    ctxb = w.context()
+    rb = run(ctxb, cb, True)
+    Kb, Vb = ctxb.all()
+    segs = []
+    for sb, sxg in zip(rb["segments"], rx["segments"]):
+        a, b = set(int(i) for i in sb["selection"]), set(int(i) for i in sxg["selection"])
+        segs.append({"selected_bf16": len(a), "selected_exact": len(b),
+                     "selection_jaccard": round(len(a & b) / max(1, len(a | b)), 4),
+                     "hidden_rel_l2": _rel_l2(sb["hidden"][sb["depth"] == sxg["depth"]],
+                                              sxg["hidden"][sb["depth"] == sxg["depth"]]),
+                     "s_dev_max_abs": float(np.max(np.abs(sb["s_dev"] - sxg["s_dev"])))})
+    err = {
+        "against": "fp32-exact run of the same prompt and relay caches (bit-equal to the reference CPU path)",
+        "logits_max_abs": float(np.max(np.abs(rb["logits"].astype(np.float64) - rx["logits"]))),
+        "logits_rel_l2": _rel_l2(rb["logits"], rx["logits"]),
+        "first_token_match": rb["first_token"] == rx["first_token"],
+        "k_rel_l2": _rel_l2(Kb, Kx), "v_rel_l2": _rel_l2(Vb, Vx),
+        "kv_max_abs": float(max(np.max(np.abs(Kb - Kx)), np.max(np.abs(Vb - Vx)))),
+        "segments": segs,
+    }
+    n_tokens = prompt_tokens()
+    exact = {"ttft_ms": round(dev_ms / 2, 3), "tokens_per_s": round(n_tokens / (dev_ms / 2 / 1e3), 1),
+             "gpu_launches_per_step": int(launches // 2),
+             "selected_per_segment": [int(x["selection_count"]) for x in rx["segments"]],
+             "note": "RK_FP32_EXACT: SIMT kernels replaying the reference's fp32 operation order"}
+    del sx, wx, cb, ctxb
+    return exact, err
 
 
 def run_ours(args, world, rank, local, dist):
@@ -418,6 +558,13 @@ def run_ours(args, world, rank, local, dist):
     kstats = eng.profile_read()
     eng.profile(False)
 
+    exact, bf16_err = None, None
+    if args.exact_leg == "on" or (args.exact_leg == "auto" and args.config == "c2"):
+        try:
+            exact, bf16_err = exact_leg(eng, w, timed)
+        except Exception as ex:
+            exact = {"error": f"{type(ex).__name__}: {str(ex)[:200]}"}
+
     # results gather over NCCL (after timing; no collective on the hot path)
     recs = []
     for sess in mine:
@@ -439,11 +586,18 @@ def run_ours(args, world, rank, local, dist):
     kstats = merge_kernel_stats(kstats)
     gemm = next((k for k in kstats if k["name"].startswith("gemm")), None)
     roofline = None
+    clocks = clk.summary()
+    # burst peak when the SMs ran at (near) their max clock during the timed
+    # region, the sustained (power-capped) figure otherwise (B200_PROFILING.md)
+    near_max = bool(clocks.get("sm_mhz") and clocks.get("sm_max_mhz") and
+                    clocks["sm_mhz"] >= 0.95 * clocks["sm_max_mhz"])
+    tf_peak, peak_kind = (tf_burst, "bf16_tflops (burst; SM clock near max)") if near_max else \
+        (tf_sus, "bf16_tflops_sustained (SM clock below max)")
     if gemm and gemm["total_ms"] > 0:
         achieved = gemm["flops"] / (gemm["total_ms"] / 1e3) / 1e12
         roofline = {"kernel": "gemm_bf16_tcgen05", "bound": "tensor", "achieved": round(achieved, 1),
-                    "peak": tf_sus, "peak_source": f"{src} bf16_tflops_sustained", "unit": "TFLOP/s",
-                    "frac": round(achieved / tf_sus, 4),
+                    "peak": tf_peak, "peak_source": f"{src} {peak_kind}", "unit": "TFLOP/s",
+                    "frac": round(achieved / tf_peak, 4),
                     "traffic": traffic.get("gemm_bf16_tcgen05", {}).get("traffic_bytes"),
                     "traffic_launch": traffic.get("gemm_bf16_tcgen05", {}).get("launch"),
                     "launches_per_step": gemm["launches"],
@@ -465,7 +619,7 @@ def run_ours(args, world, rank, local, dist):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            tps, meta = cpu_sample(hosts, steps=1, warmup=0, kind="reference")
+            tps, meta = cpu_sample(hosts, steps=1, warmup=0, kind="reference", full_selected=selected)
             cpu = {"value": round(tps, 4), "unit": "tokens/s", **meta}
         except Exception as ex:  # the CPU leg is a reported baseline, not the product
             cpu = {"value": None, "unit": "tokens/s", "error": str(ex)[:200]}
@@ -499,7 +653,9 @@ def run_ours(args, world, rank, local, dist):
                            "tflops": round(k["flops"] / (k["total_ms"] / 1e3) / 1e12, 1) if k["flops"] and k["total_ms"] else None}
                           for k in detail[:40]],
         "cpu_baseline": cpu,
-        "clocks": clk.summary(),
+        "fp32_exact": exact,
+        "bf16_error": bf16_err,
+        "clocks": clocks,
     }
     if rank == 0:
         print(json.dumps(out), flush=True)
@@ -508,7 +664,10 @@ def run_ours(args, world, rank, local, dist):
 def run_reference(args, world, rank, local, dist):
     """--impl reference: the reference's own CPU implementation of the path
     (oracle/_ref, built from /root/reference sources) on this box's host cores,
-    same metric/unit, each step a bounded sample of the c2 workload."""
+    same metric/unit: each step runs one independent session per host core on
+    a bounded sample of the workload (the reference's own decode-time captures
+    of the cut segments), extrapolated to the GPU arm's full prompt with the
+    reference's FLOP model (cpu_sample; labelled "extrapolated")."""
     if rank != 0:
         return
     try:
@@ -517,42 +676,50 @@ def run_reference(args, world, rank, local, dist):
             print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference "
                                                                   "at build time)"}))
             return
-        # inputs: the chain's caches are data; build them with the reference
-        # itself (decode-time capture of the cut segments) to stay CPU-only.
-        from oracle.oracle import Oracle
-        orc = Oracle("reference")
-        spec = spec_obj()
-        w = orc.weights(spec, SEED, checked=True)
-        pr = prompts(0)
-        cp, cs, cx = WL["cpu"]
-        last = WL["agents"] - 1
-        caches = [orc.scenario(w, pr[f"a{a}_prefix"][:cp], cs, WL["profile"][0]) for a in range(last)]
-        prof, opts = options()
-        prefix, suffix = pr[f"a{last}_prefix"][:cp], pr[f"a{last}_suffix"][:cx]
-        tokens = len(prefix) + last * cs + len(suffix)
-        threads = os.cpu_count() or 1
-        for _ in range(args.warmup):
-            orc.agent_prefill_parallel(w, threads, prefix, caches, suffix, prof, opts)
-        times = []
-        for _ in range(args.steps):
-            ms, _ = orc.agent_prefill_parallel(w, threads, prefix, caches, suffix, prof, opts)
-            times.append(ms)
-        ms = sum(times) / len(times)
-        value = threads * tokens / (ms / 1e3)
-        sample = (f"{WL['title'].split(':')[0]} model (fp32 reference), prefix {cp} + {last} relayed segments x "
-                  f"{cs} + suffix {cx} = {tokens} tokens/session, {threads} concurrent sessions")
+        ref = full_c2_reference_run() if args.config == "c2" else None
+        full_sel = ref.get("selected_per_segment") if ref else None
+        value, meta = cpu_sample(None, steps=args.steps, warmup=args.warmup, kind="reference",
+                                 full_selected=full_sel)
+        ms = meta["full_prompt_ttft_ms_all_cores_extrapolated"]
         print(json.dumps({
             "impl": "reference", "metric": "relay-prefill tokens/s (downstream-agent TTFT at ~80% KV reuse)",
             "value": round(value, 4), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
-            "config": {"workload": f"{WL['title']}, bounded CPU sample", "config_id": args.config, "sample": sample},
-            "cpu_baseline": {"value": round(value, 4), "unit": "tokens/s", "kind": "reference", "cores": threads,
-                             "sample": sample, "host": host_info()},
+            "config": {"workload": f"{WL['title']}, last agent's TTFT at a {prompt_tokens()}-token prompt, "
+                                   f"profile {WL['profile']} (CPU: measured sample, FLOP-model extrapolated)",
+                       "config_id": args.config, "sample": meta["sample"]},
+            "ttft_ms_one_core": meta["full_prompt_ttft_ms_one_core_extrapolated"],
+            "cpu_baseline": {"value": round(value, 4), "unit": "tokens/s", **meta},
             "e2e": {"value": round(value, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         }), flush=True)
     except Exception as ex:
         print(json.dumps({"impl": "reference", "unavailable": f"{type(ex).__name__}: {str(ex)[:200]}"}))
+
+
+def run_stub(args, world, rank, local, dist):
+    """The multi-rank plumbing of run_ours without a GPU (CPU tests, gloo):
+    sessions sharded contiguously, a timed loop of no-op sessions bracketed by
+    barriers, max-over-ranks time, one all_gather of the per-session records
+    after timing, one JSON line on rank 0."""
+    from paper_2603_13289_b200.sessions import gather_records, shard
+    n_sessions = args.sessions or WL.get("sessions", world)
+    mine = list(shard(n_sessions, world, rank))
+    barrier(dist)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        for sid in mine:
+            sum(range(1000))
+    ms = reduce_max(dist, (time.perf_counter() - t0) * 1e3, local)
+    barrier(dist)
+    recs = [{"session": sid, "first_token": 1000 + sid, "segments": WL["agents"] - 1, "ttft_ms": ms} for sid in mine]
+    gathered = gather_records(recs, n_sessions, dist)
+    if rank == 0:
+        print(json.dumps({"impl": "stub", "n_gpus": world, "steps": args.steps, "sessions": n_sessions,
+                          "sessions_per_rank": len(mine), "sessions_gathered": len(gathered),
+                          "gathered_ids": [r["session"] for r in gathered],
+                          "first_tokens_ok": all(r["first_token"] == 1000 + r["session"] for r in gathered)}),
+              flush=True)
 
 
 def main():
@@ -560,19 +727,26 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--impl", choices=["ours", "reference", "stub"], default="ours",
+                    help="stub: the launcher/shard/gather plumbing with a CPU no-op session (tests only)")
     ap.add_argument("--config", choices=sorted(WORKLOADS), default="c2",
                     help="workload (default c2: the config BASELINE.json's metric is quoted on)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--exact-leg", choices=["auto", "on", "off"], default="auto",
+                    help="fp32-exact TTFT + bf16 error leg (auto: c2 only)")
     ap.add_argument("--lean", action="store_true",
                     help="timed relay steps only (for ncu launch lists): no full-prefill, e2e or profiling legs")
     ap.add_argument("--sessions", type=int, default=0,
                     help="collaboration sessions in total, sharded contiguously over the GPUs (default: one per GPU)")
     args = ap.parse_args()
     set_workload(args.config)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(sys.argv[1:], args.gpus))
     world, rank, local, dist = dist_setup(args)
     if args.impl == "reference":
         run_reference(args, world, rank, local, dist)
+    elif args.impl == "stub":
+        run_stub(args, world, rank, local, dist)
     else:
         run_ours(args, world, rank, local, dist)
     if dist is not None:

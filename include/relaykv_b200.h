@@ -351,6 +351,38 @@ void rk_context_destroy(rk_context* c);
  * last_logits: logits of the last row [V] (NULL = not computed). */
 int rk_prefill(rk_engine* e, rk_weights* w, rk_context* ctx, const int32_t* tokens, uint64_t n,
                uint64_t base_position, float* last_logits);
+/* prefill with capture (model.cpp:305-331 with CaptureFlags/StepTrace,
+ * model.hpp:89-111) -- what decode_step / greedy_generate hand to a StepHook
+ * (model.cpp:364-389) and what the reference's PrefillResult carries.
+ * Every destination is a HOST buffer and may be NULL (= not captured):
+ *   logits  [n][V]            every row's logits (output_logits over all rows)
+ *   hidden  [L][n][d_model]   each layer's input rows (CaptureFlags::hidden)
+ *   k_pre   [L][n][kv]        K before rotation      (CaptureFlags::pre_rope_keys)
+ *   v       [L][n][kv]        V as produced          (CaptureFlags::pre_rope_keys)
+ *   attn    [L][n][H][base+n] softmax rows over the causal context, zero past
+ *                             each row's own position (CaptureFlags::attention)
+ * Rows are committed to ctx exactly as rk_prefill does. */
+typedef struct rk_trace_request {
+  float* logits;
+  float* hidden;
+  float* k_pre;
+  float* v;
+  float* attn;
+} rk_trace_request;
+int rk_prefill_trace(rk_engine* e, rk_weights* w, rk_context* ctx, const int32_t* tokens, uint64_t n,
+                     uint64_t base_position, const rk_trace_request* req);
+/* row_logits_from_layer (model.cpp:339-362): one HOST hidden row [d_model]
+ * run as a pure query from first_layer to the top at `position` (its own
+ * context cell overridden by the fresh K/V, nothing committed), then
+ * output_logits; logits [V] (host). workflow.cpp:347-354 uses it when an
+ * agent has no suffix. */
+int rk_row_logits_from_layer(rk_engine* e, rk_weights* w, rk_context* ctx, const float* hidden_row,
+                             uint64_t first_layer, uint64_t position, float* logits);
+/* Page-lock caller-owned host memory (cudaHostRegister) so uploads from it
+ * (rk_cache_upload_async) stream at full PCIe speed and overlap compute;
+ * rk_host_unpin releases it. */
+int rk_host_pin(void* ptr, uint64_t bytes);
+int rk_host_unpin(void* ptr);
 /* relay_extend (relay_engine.cpp:183-361): appends one relayed segment at ctx size. */
 int rk_relay_extend(rk_engine* e, rk_weights* w, rk_context* ctx, rk_cache* cache,
                     const rk_layer_profile* profile, const rk_relay_options* opts,

@@ -442,12 +442,15 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
     } else {
       const float inv = 1.f / l_run;
       uint4* dst = reinterpret_cast<uint4*>(a.out + (size_t)row * (a.H * DH) + h * DH);
+      float chk = inv * 0.f;  // non-finite output (x * 0 is NaN iff x is inf/NaN)
 #pragma unroll
       for (int c = 0; c < DH; c += 32) {
         uint32_t o[32];
         tmem_ld32(o_col + c, o);
         tmem_ld_wait();
         if (valid) {
+#pragma unroll
+          for (int u = 0; u < 32; ++u) chk = fmaf(__uint_as_float(o[u]), 0.f, chk);
 #pragma unroll
           for (int u = 0; u < 32; u += 8)
             dst[(c + u) / 8] = make_uint4(pack_bf16(__uint_as_float(o[u]) * inv, __uint_as_float(o[u + 1]) * inv),
@@ -456,6 +459,7 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
                                           pack_bf16(__uint_as_float(o[u + 6]) * inv, __uint_as_float(o[u + 7]) * inv));
         }
       }
+      if (valid && chk != chk && a.status) *reinterpret_cast<volatile int*>(a.status) = 1;
     }
   }
   tc_fence_before();
@@ -532,6 +536,10 @@ __device__ __forceinline__ void attn_combine_one(const AttnArgs& a, int row, int
     for (int i = 0; i < PER; ++i) o[i] += wz * a.ws_o[pr * DH + lane * PER + i];
   }
   const float inv = 1.f / lsum;
+  float chk = inv * 0.f;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) chk = fmaf(o[i], 0.f, chk);
+  if (chk != chk && a.status) *reinterpret_cast<volatile int*>(a.status) = 1;
   __nv_bfloat16* dst = a.out + (size_t)row * (a.H * DH) + h * DH + lane * PER;
 #pragma unroll
   for (int i = 0; i < PER; i += 2) *reinterpret_cast<uint32_t*>(dst + i) = pack_bf16(o[i] * inv, o[i + 1] * inv);
@@ -619,6 +627,7 @@ void attention_bf16(rk_engine* e, const AttnArgs& a_in, const __nv_bfloat16* ctx
                     int ctx_rows) {
   if (a_in.rows_max <= 0) return;
   AttnArgs a = a_in;
+  if (!a.status) a.status = e->status.as<int>();
   // split-KV when the query tiles alone cannot fill the SMs (sparse passes:
   // plan for ~1/3 of rows_max live). A split covers >= 2 key tiles; CTAs
   // whose rows end before their split exit at once, so long tiles (suffix,

@@ -1002,6 +1002,45 @@ int rk_prefill(rk_engine* e, rk_weights* w, rk_context* ctx, const int32_t* toke
   });
 }
 
+int rk_prefill_trace(rk_engine* e, rk_weights* w, rk_context* ctx, const int32_t* tokens, uint64_t n,
+                     uint64_t base, const rk_trace_request* req) {
+  return guard([&] {
+    DeviceGuard g(e->device);
+    const rk_trace_request none{};
+    Runner r(e, w);
+    r.prefill_trace(ctx, tokens, n, base, req ? *req : none);
+    r.finish();
+  });
+}
+
+int rk_row_logits_from_layer(rk_engine* e, rk_weights* w, rk_context* ctx, const float* hidden_row,
+                             uint64_t first_layer, uint64_t position, float* logits) {
+  return guard([&] {
+    DeviceGuard g(e->device);
+    require(ctx != nullptr && ctx->w == w, RK_ERR_INVALID_ARGUMENT, "context belongs to other weights");
+    require(hidden_row != nullptr && logits != nullptr, RK_ERR_INVALID_ARGUMENT, "null hidden row or logits");
+    require(first_layer <= w->s.num_layers, RK_ERR_INVALID_ARGUMENT, "row_logits_from_layer: first_layer out of range");
+    require(position < ctx->size, RK_ERR_INVALID_ARGUMENT, "row_logits_from_layer: position outside the context");
+    DevBuf row(w->s.d_model * 4);
+    RK_CUDA(cudaMemcpyAsync(row.p, hidden_row, w->s.d_model * 4, cudaMemcpyHostToDevice, e->stream));
+    Runner r(e, w);
+    r.row_logits_from_layer(ctx, row.as<float>(), first_layer, position);
+    r.finish();
+    r.download_logits(logits);
+  });
+}
+
+int rk_host_pin(void* ptr, uint64_t bytes) {
+  return guard([&] {
+    require(ptr != nullptr && bytes > 0, RK_ERR_INVALID_ARGUMENT, "rk_host_pin: empty range");
+    RK_CUDA(cudaHostRegister(ptr, bytes, cudaHostRegisterDefault));
+  });
+}
+
+int rk_host_unpin(void* ptr) {
+  return guard([&] { RK_CUDA(cudaHostUnregister(ptr)); });
+}
+
 int rk_relay_extend(rk_engine* e, rk_weights* w, rk_context* ctx, rk_cache* cache,
                     const rk_layer_profile* profile, const rk_relay_options* opts, rk_relay_output* out) {
   return guard([&] {

@@ -49,6 +49,13 @@ using namespace sm100;
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;  // 64 bf16 = one 128-byte swizzle row
+
+// ensure_finite (tensor.cpp:58-64): x * 0 is NaN exactly when x is inf or NaN,
+// so one FFMA per value folds a whole chunk into one check.
+__device__ __forceinline__ float finite_acc(float acc, float x) { return fmaf(x, 0.0f, acc); }
+__device__ __forceinline__ void flag_nonfinite(int* status, float acc) {
+  if (acc != acc && status) *reinterpret_cast<volatile int*>(status) = 1;
+}
 constexpr int kThreads = 192;
 
 // PAIR = 2: a CTA pair (cluster of 2, tcgen05 cta_group::2) computes a
@@ -146,8 +153,13 @@ template <int EPI>
 __device__ __forceinline__ void epilogue_chunk(const GemmArgs& p, int row, int col, const uint32_t (&r)[32],
                                                float rs, int split = 0) {
   float v[32];
+  float chk = 0.f;
 #pragma unroll
-  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * rs;
+  for (int j = 0; j < 32; ++j) {
+    v[j] = __uint_as_float(r[j]) * rs;
+    chk = finite_acc(chk, v[j]);
+  }
+  flag_nonfinite(p.status, chk);
   if constexpr (EPI == EPI_F32 || EPI == EPI_PART) {
     float* base = EPI != EPI_PART ? p.out_f32 + (size_t)row * p.ld_out + col
                   : p.streamk ? p.ws_part + (((size_t)blockIdx.x * kSkSlots + split) * kBM + row % kBM) * p.bn + col % p.bn
@@ -519,6 +531,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         float ss[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) ss[i] = 0.f;
+        float chk = 0.f;  // non-finite matmul values (rows past M are zero-filled A rows: finite)
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
           uint32_t r[32];
@@ -548,6 +561,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             h.z += __uint_as_float(a4.z);
             h.w += __uint_as_float(a4.w);
             if (rr < M) {
+              chk = finite_acc(finite_acc(finite_acc(finite_acc(chk, __uint_as_float(a4.x)), __uint_as_float(a4.y)),
+                                          __uint_as_float(a4.z)), __uint_as_float(a4.w));
               *hptr(i, c) = h;
               if (norm) {
                 ss[i] = fmaf(h.x, h.x, fmaf(h.y, h.y, fmaf(h.z, h.z, fmaf(h.w, h.w, ss[i]))));
@@ -557,6 +572,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
+        flag_nonfinite(p.status, chk);
         if (norm) {
           // row sums over the 8 lanes of each row group; lane ch==0 owns rows 4i+sub
 #pragma unroll
@@ -665,6 +681,7 @@ __device__ __forceinline__ void splitk_reduce_row(const GemmArgs& p, int splits,
           acc.x += v[s].x; acc.y += v[s].y; acc.z += v[s].z; acc.w += v[s].w;
         }
     }
+    flag_nonfinite(p.status, finite_acc(finite_acc(finite_acc(finite_acc(0.f, acc.x), acc.y), acc.z), acc.w));
     float4 x = h[c];
     x.x += acc.x; x.y += acc.y; x.z += acc.z; x.w += acc.w;
     h[c] = x;
@@ -728,6 +745,10 @@ __device__ __forceinline__ float dot8(uint4 w, uint4 a) {
 // RoPE pairs stay together) with the GEMM's epilogue semantics.
 template <int EPI, int R>
 __device__ __forceinline__ void gemv_store(const GemmArgs& p, int n0, const float (&v)[R], float rs) {
+  float chk = 0.f;
+#pragma unroll
+  for (int r = 0; r < R; ++r) chk = finite_acc(chk, v[r] * rs);
+  flag_nonfinite(p.status, chk);
   if constexpr (EPI == EPI_SILU) {  // rows (2j, 2j+1) = (gate j, up j)
 #pragma unroll
     for (int r = 0; r < R; r += 2) {
@@ -1235,6 +1256,7 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
                int rows_hint) {
   if (p.rows_max <= 0) return;
   if (p.K % kBK) raise(RK_ERR_INVALID_ARGUMENT, "bf16 GEMM needs K % 64 == 0");
+  if (!p.status) p.status = e->status.as<int>();
   static const bool gemv_env = [] {
     const char* v = std::getenv("RK_GEMV");
     return v ? std::atoi(v) != 0 : true;

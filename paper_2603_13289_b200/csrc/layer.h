@@ -39,6 +39,9 @@ class Runner {
   ~Runner();
 
   void prefill(rk_context* ctx, const int32_t* tokens, uint64_t n, uint64_t base, bool want_logits);
+  // prefill with capture into host buffers (rk_prefill_trace)
+  void prefill_trace(rk_context* ctx, const int32_t* tokens, uint64_t n, uint64_t base,
+                     const rk_trace_request& req);
   ExtendResult relay_extend(rk_context* ctx, rk_cache* cache, const rk_layer_profile* prof,
                             const rk_relay_options& opts);
   // relay_prefill's next-token logits at the segment end (relay_engine.cpp:381-393)
@@ -57,6 +60,9 @@ class Runner {
   void resolve(ExtendResult& r);  // after finish(): counts, stats, timings
   void fill_output(ExtendResult& res, rk_context* ctx, rk_relay_output* out);
   void download_logits(float* dst);
+  // row_logits_from_layer (model.cpp:339-362) of a device hidden row into scratch logits
+  void row_logits_from_layer(rk_context* ctx, const float* hidden_row, uint64_t first_layer,
+                             uint64_t position);
   int32_t first_token();
 
   void begin_timer();
@@ -67,8 +73,6 @@ class Runner {
   void run_layer(rk_context* ctx, int layer, float* hidden, Rows rows, bool commit, int max_ctx,
                  float* probs = nullptr, int key_lo = 0, int key_n = 0, int tail = -1);
   void last_row_logits(const float* hidden_row);  // output_logits (model.cpp:282-288)
-  void row_logits_from_layer(rk_context* ctx, const float* hidden_row, uint64_t first_layer,
-                             uint64_t position);
   ExtendPlan plan_extend(uint64_t base, rk_cache* cache, const rk_layer_profile* prof,
                          const rk_relay_options& opts);
   void agent_fused(rk_context* ctx, const int32_t* prefix, uint64_t P, rk_cache* const* ups, uint64_t U,
@@ -111,5 +115,7 @@ void run_layer_bf16(rk_engine* e, rk_weights* w, rk_context* ctx, int layer, flo
                     Rows rows, bool commit, int max_ctx, float* probs, int key_lo, int key_n,
                     void* cap_k, void* cap_v, bool prepared, int tail = -1);
 void last_row_logits_bf16(rk_engine* e, rk_weights* w, const float* hidden_row, float* logits);
+// output_logits over a row set (model.cpp:282-288): logits [rows][V] fp32
+void rows_logits_bf16(rk_engine* e, rk_weights* w, const float* hidden, Rows rows, float* logits);
 
 }  // namespace rk

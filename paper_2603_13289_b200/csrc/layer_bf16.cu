@@ -282,4 +282,20 @@ void last_row_logits_bf16(rk_engine* e, rk_weights* w, const float* hidden_row, 
   e->launches += 1;
 }
 
+void rows_logits_bf16(rk_engine* e, rk_weights* w, const float* hidden, Rows rows, float* logits) {
+  Scratch& S = *e->scratch;
+  const rk_model_spec& s = w->s;
+  auto* normed = S.normed.as<__nv_bfloat16>();
+  rmsnorm_bf16(e->stream, hidden, w->final_norm, s.norm_eps, normed, rows, s.d_model);
+  GemmArgs g;
+  g.rows_max = rows.rows_max;
+  g.N = s.vocab_size;
+  g.K = s.d_model;
+  g.epi = EPI_F32;
+  g.out_f32 = logits;
+  g.ld_out = s.vocab_size;
+  gemm_bf16(e, normed, s.d_model, static_cast<const __nv_bfloat16*>(w->head), g, rows.rows_max);
+  e->launches += 1;
+}
+
 }  // namespace rk

@@ -55,6 +55,10 @@ struct GemmArgs {
   float norm_eps = 1e-5f;
   float* ws_part = nullptr;  // EPI_PART workspace [splits][rows_max][N], or stream-K [grid*2][128][bn]
   int streamk = 0;           // EPI_PART: stream-K work split (set by gemm_bf16)
+  // ensure_finite (tensor.cpp:58-64, after every matmul): any non-finite
+  // product value sets status[0] (engine status flags, set by gemm_bf16);
+  // the call then fails with RK_ERR_NONFINITE ("matmul: non-finite value")
+  int* status = nullptr;
 };
 constexpr int kNormSlots = 64;  // max N tiles of a residual GEMM (d_model / BN)
 
@@ -88,6 +92,7 @@ struct AttnArgs {
   // roles: softmax group 0, group 1, MMA issuer)
   unsigned long long* trace = nullptr;
   int pingpong = 1;  // set by attention_bf16
+  int* status = nullptr;  // non-finite output flag (engine status[0], set by attention_bf16)
 };
 // ctx_k / ctx_v: the layer's [ctx_rows x kv] bf16 context rows.
 void attention_bf16(rk_engine* e, const AttnArgs& a, const __nv_bfloat16* ctx_k, const __nv_bfloat16* ctx_v,

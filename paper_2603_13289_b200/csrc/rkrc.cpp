@@ -31,25 +31,194 @@ uint64_t fnv1a64(const uint8_t* p, size_t n) {  // serialize.cpp:36-43
   return h;
 }
 
-// nlohmann::json number_float formatting (its dtoa: shortest round-trip
-// digits, then format_buffer with min_exp -4 / max_exp 15): "10000.0",
-// "0.0001", "1.5e-07", "3.3999999521443642e+38".
+// nlohmann::json (3.11.3) number_float formatting, which the reference's
+// manifest text goes through (serialize.cpp: json::dump): Grisu2 digit
+// generation (F. Loitsch, "Printing Floating-Point Numbers Quickly and
+// Accurately with Integers", PLDI 2010) with the boundaries of the double and
+// the alpha/gamma window [-60, -32], then the format with min_exp -4 /
+// max_exp 15: "10000.0", "0.0001", "1.5e-07", "803.1189575195313".
+// Grisu2 does not always return the shortest/closest digits, so a shortest
+// round-trip search would differ in the last digit for some floats
+// (tests/test_rkrc.py sweeps 1,500 random thetas against the reference).
+namespace grisu {
+struct DiyFp {
+  uint64_t f;
+  int e;
+};
+DiyFp sub(DiyFp x, DiyFp y) { return {x.f - y.f, x.e}; }
+DiyFp mul(DiyFp x, DiyFp y) {  // upper 64 bits of the 128-bit product, rounded half up
+  const unsigned __int128 p = (unsigned __int128)x.f * y.f;
+  const uint64_t h = (uint64_t)(p >> 64) + (uint64_t)((p >> 63) & 1);
+  return {h, x.e + y.e + 64};
+}
+DiyFp normalize(DiyFp x) {
+  while ((x.f >> 63) == 0) {
+    x.f <<= 1;
+    x.e--;
+  }
+  return x;
+}
+struct CachedPower {
+  uint64_t f;
+  int e, k;
+};
+// f * 2^e = 10^k rounded to nearest, f normalized to [2^63, 2^64), k = -300..324
+// step 8 (generated exactly with Python Fractions).
+constexpr CachedPower kPowers[] = {
+    {0xAB70FE17C79AC6CAull, -1060, -300},
+    {0xFF77B1FCBEBCDC4Full, -1034, -292},
+    {0xBE5691EF416BD60Cull, -1007, -284},
+    {0x8DD01FAD907FFC3Cull, -980, -276},
+    {0xD3515C2831559A83ull, -954, -268},
+    {0x9D71AC8FADA6C9B5ull, -927, -260},
+    {0xEA9C227723EE8BCBull, -901, -252},
+    {0xAECC49914078536Dull, -874, -244},
+    {0x823C12795DB6CE57ull, -847, -236},
+    {0xC21094364DFB5637ull, -821, -228},
+    {0x9096EA6F3848984Full, -794, -220},
+    {0xD77485CB25823AC7ull, -768, -212},
+    {0xA086CFCD97BF97F4ull, -741, -204},
+    {0xEF340A98172AACE5ull, -715, -196},
+    {0xB23867FB2A35B28Eull, -688, -188},
+    {0x84C8D4DFD2C63F3Bull, -661, -180},
+    {0xC5DD44271AD3CDBAull, -635, -172},
+    {0x936B9FCEBB25C996ull, -608, -164},
+    {0xDBAC6C247D62A584ull, -582, -156},
+    {0xA3AB66580D5FDAF6ull, -555, -148},
+    {0xF3E2F893DEC3F126ull, -529, -140},
+    {0xB5B5ADA8AAFF80B8ull, -502, -132},
+    {0x87625F056C7C4A8Bull, -475, -124},
+    {0xC9BCFF6034C13053ull, -449, -116},
+    {0x964E858C91BA2655ull, -422, -108},
+    {0xDFF9772470297EBDull, -396, -100},
+    {0xA6DFBD9FB8E5B88Full, -369, -92},
+    {0xF8A95FCF88747D94ull, -343, -84},
+    {0xB94470938FA89BCFull, -316, -76},
+    {0x8A08F0F8BF0F156Bull, -289, -68},
+    {0xCDB02555653131B6ull, -263, -60},
+    {0x993FE2C6D07B7FACull, -236, -52},
+    {0xE45C10C42A2B3B06ull, -210, -44},
+    {0xAA242499697392D3ull, -183, -36},
+    {0xFD87B5F28300CA0Eull, -157, -28},
+    {0xBCE5086492111AEBull, -130, -20},
+    {0x8CBCCC096F5088CCull, -103, -12},
+    {0xD1B71758E219652Cull, -77, -4},
+    {0x9C40000000000000ull, -50, 4},
+    {0xE8D4A51000000000ull, -24, 12},
+    {0xAD78EBC5AC620000ull, 3, 20},
+    {0x813F3978F8940984ull, 30, 28},
+    {0xC097CE7BC90715B3ull, 56, 36},
+    {0x8F7E32CE7BEA5C70ull, 83, 44},
+    {0xD5D238A4ABE98068ull, 109, 52},
+    {0x9F4F2726179A2245ull, 136, 60},
+    {0xED63A231D4C4FB27ull, 162, 68},
+    {0xB0DE65388CC8ADA8ull, 189, 76},
+    {0x83C7088E1AAB65DBull, 216, 84},
+    {0xC45D1DF942711D9Aull, 242, 92},
+    {0x924D692CA61BE758ull, 269, 100},
+    {0xDA01EE641A708DEAull, 295, 108},
+    {0xA26DA3999AEF774Aull, 322, 116},
+    {0xF209787BB47D6B85ull, 348, 124},
+    {0xB454E4A179DD1877ull, 375, 132},
+    {0x865B86925B9BC5C2ull, 402, 140},
+    {0xC83553C5C8965D3Dull, 428, 148},
+    {0x952AB45CFA97A0B3ull, 455, 156},
+    {0xDE469FBD99A05FE3ull, 481, 164},
+    {0xA59BC234DB398C25ull, 508, 172},
+    {0xF6C69A72A3989F5Cull, 534, 180},
+    {0xB7DCBF5354E9BECEull, 561, 188},
+    {0x88FCF317F22241E2ull, 588, 196},
+    {0xCC20CE9BD35C78A5ull, 614, 204},
+    {0x98165AF37B2153DFull, 641, 212},
+    {0xE2A0B5DC971F303Aull, 667, 220},
+    {0xA8D9D1535CE3B396ull, 694, 228},
+    {0xFB9B7CD9A4A7443Cull, 720, 236},
+    {0xBB764C4CA7A44410ull, 747, 244},
+    {0x8BAB8EEFB6409C1Aull, 774, 252},
+    {0xD01FEF10A657842Cull, 800, 260},
+    {0x9B10A4E5E9913129ull, 827, 268},
+    {0xE7109BFBA19C0C9Dull, 853, 276},
+    {0xAC2820D9623BF429ull, 880, 284},
+    {0x80444B5E7AA7CF85ull, 907, 292},
+    {0xBF21E44003ACDD2Dull, 933, 300},
+    {0x8E679C2F5E44FF8Full, 960, 308},
+    {0xD433179D9C8CB841ull, 986, 316},
+    {0x9E19DB92B4E31BA9ull, 1013, 324},
+};
+void round_last(char* buf, int len, uint64_t dist, uint64_t delta, uint64_t rest, uint64_t ten_k) {
+  while (rest < dist && delta - rest >= ten_k && (rest + ten_k < dist || dist - rest > rest + ten_k - dist)) {
+    buf[len - 1]--;
+    rest += ten_k;
+  }
+}
+// digits of v (> 0, finite) into buf; value = buf * 10^dec_exp
+void digits(double v, char* buf, int& len, int& dec_exp) {
+  uint64_t bits;
+  std::memcpy(&bits, &v, 8);
+  const uint64_t F = bits & ((1ull << 52) - 1), E = bits >> 52;
+  const DiyFp w = E == 0 ? DiyFp{F, 1 - 1075} : DiyFp{F + (1ull << 52), (int)E - 1075};
+  const bool closer = F == 0 && E > 1;  // the lower neighbour is half as far
+  const DiyFp m_plus = normalize({2 * w.f + 1, w.e - 1});
+  DiyFp m_minus = closer ? DiyFp{4 * w.f - 1, w.e - 2} : DiyFp{2 * w.f - 1, w.e - 1};
+  m_minus = {m_minus.f << (m_minus.e - m_plus.e), m_plus.e};
+  const DiyFp vn = normalize(w);
+  // cached power c = 10^-k with alpha <= m_plus.e + c.e + 64 <= gamma
+  const int f = -60 - m_plus.e - 1;
+  const int k = (f * 78913) / (1 << 18) + (f > 0);
+  const CachedPower& cp = kPowers[(300 + k + 7) / 8];
+  const DiyFp c{cp.f, cp.e};
+  const DiyFp ww = mul(vn, c), wm = mul(m_minus, c), wp = mul(m_plus, c);
+  const DiyFp Mm{wm.f + 1, wm.e}, Mp{wp.f - 1, wp.e};
+  dec_exp = -cp.k;
+  uint64_t delta = sub(Mp, Mm).f, dist = sub(Mp, ww).f;
+  const DiyFp one{1ull << -Mp.e, Mp.e};
+  uint32_t p1 = (uint32_t)(Mp.f >> -one.e);
+  uint64_t p2 = Mp.f & (one.f - 1);
+  uint32_t pow10 = 1;
+  int n = 1;  // digits of p1
+  for (uint32_t t = p1; t >= 10; t /= 10) {
+    pow10 *= 10;
+    ++n;
+  }
+  len = 0;
+  while (n > 0) {
+    const uint32_t d = p1 / pow10, r = p1 % pow10;
+    buf[len++] = (char)('0' + d);
+    p1 = r;
+    --n;
+    const uint64_t rest = ((uint64_t)p1 << -one.e) + p2;
+    if (rest <= delta) {
+      dec_exp += n;
+      round_last(buf, len, dist, delta, rest, (uint64_t)pow10 << -one.e);
+      return;
+    }
+    pow10 /= 10;
+  }
+  int m = 0;
+  for (;;) {
+    p2 *= 10;
+    const uint64_t d = p2 >> -one.e, r = p2 & (one.f - 1);
+    buf[len++] = (char)('0' + d);
+    p2 = r;
+    ++m;
+    delta *= 10;
+    dist *= 10;
+    if (p2 <= delta) break;
+  }
+  dec_exp -= m;
+  round_last(buf, len, dist, delta, p2, one.f);
+}
+}  // namespace grisu
+
 std::string json_double(double v) {
   if (v == 0) return std::signbit(v) ? "-0.0" : "0.0";
   std::string out = v < 0 ? "-" : "";
   v = std::fabs(v);
-  char buf[64];
-  for (int prec = 1; prec <= 17; ++prec) {
-    std::snprintf(buf, sizeof buf, "%.*e", prec - 1, v);
-    if (std::strtod(buf, nullptr) == v) break;
-  }
-  std::string digits;
-  const char* q = buf;
-  for (; *q && *q != 'e'; ++q)
-    if (std::isdigit((unsigned char)*q)) digits += *q;
-  const int e10 = std::atoi(q + 1);
-  while (digits.size() > 1 && digits.back() == '0') digits.pop_back();
-  const int k = (int)digits.size(), n = e10 + 1;  // value = 0.digits * 10^n
+  char buf[32];
+  int len = 0, dec_exp = 0;
+  grisu::digits(v, buf, len, dec_exp);
+  const std::string digits(buf, buf + len);
+  const int k = len, n = len + dec_exp;  // value = 0.digits * 10^n
   if (k <= n && n <= 15) {
     out += digits + std::string(n - k, '0') + ".0";
   } else if (0 < n && n <= 15) {
@@ -283,7 +452,7 @@ HostCacheFile decode(Source& src, bool pinned) {
   std::memcpy(&version, hdr + 4, 4);
   std::memcpy(&mlen, hdr + 8, 8);
   if (version != 1) raise(RK_ERR_SCHEMA, "unsupported format version " + std::to_string(version));
-  if (16 + mlen > size) raise(RK_ERR_SCHEMA, "blob file truncated (manifest)");
+  if (mlen > size - 16) raise(RK_ERR_SCHEMA, "blob file truncated (manifest)");  // (no 16 + mlen wrap)
   std::string mtext(mlen, '\0');
   src.read(mtext.data(), mlen);
   Parser ps{mtext.data(), mtext.data() + mlen};

@@ -239,6 +239,88 @@ void Runner::prefill(rk_context* ctx, const int32_t* tokens, uint64_t n, uint64_
   if (want_logits) last_row_logits(S.hidden.as<float>() + (n - 1) * s.d_model);
 }
 
+// prefill with capture (model.cpp:305-331, CaptureFlags/StepTrace): the same
+// layer pass with the top layer over all rows, each layer's input rows, pre-RoPE
+// K/V and full-context attention rows copied out per layer, and every row's
+// logits (output_logits over the chunk, model.cpp:328).
+void Runner::prefill_trace(rk_context* ctx, const int32_t* tokens, uint64_t n, uint64_t base,
+                           const rk_trace_request& rq) {
+  const rk_model_spec& s = w_->s;
+  require(ctx != nullptr && ctx->w == w_, RK_ERR_INVALID_ARGUMENT, "context belongs to other weights");
+  require(n > 0, RK_ERR_INVALID_ARGUMENT, "prefill: empty token chunk");
+  require(base == ctx->size, RK_ERR_INVALID_ARGUMENT,
+          "prefill: base_position " + std::to_string(base) + " != context size " + std::to_string(ctx->size));
+  require(base + n <= s.max_positions, RK_ERR_INVALID_ARGUMENT,
+          "prefill: position overflow beyond max_positions " + std::to_string(s.max_positions));
+  require(tokens != nullptr, RK_ERR_INVALID_ARGUMENT, "null tokens");
+  check_tokens(tokens, n);
+  ensure_rows(n);
+  Scratch& S = *e_->scratch;
+  const uint64_t L = s.num_layers, d = s.d_model, kv = w_->kv(), H = s.num_heads, V = s.vocab_size;
+  const uint64_t keys = base + n, el = w_->elem;
+  int* dev_tok = upload_tokens(tokens, n, tok_cursor_);
+  tok_cursor_ += (int)n;
+  k::embed(st_, S.hidden.as<float>(), w_->emb, w_->elem, dev_tok, (int)n, (int)d, 0, nullptr);
+  ctx->resize(base + n);
+  k::iota_positions(st_, S.positions.as<int>(), (int)n, (int)base);
+  e_->launches += 2;
+  Rows rows{(int)n, nullptr, S.positions.as<int>()};
+  const bool kvcap = rq.k_pre || rq.v;
+  DevBuf kst, vst, f32, probs;
+  if (kvcap) {
+    kst.alloc(n * kv * el);
+    vst.alloc(n * kv * el);
+    if (el == 2) f32.alloc(n * kv * 4);
+  }
+  if (rq.attn) probs.alloc(n * H * keys * 4);
+  auto kv_out = [&](float* dst, const DevBuf& src) {
+    if (!dst) return;
+    if (el == 4) {
+      RK_CUDA(cudaMemcpyAsync(dst, src.p, n * kv * 4, cudaMemcpyDeviceToHost, st_));
+    } else {
+      k::bf16_to_f32(st_, f32.as<float>(), static_cast<const __nv_bfloat16*>(src.p), n * kv);
+      RK_CUDA(cudaMemcpyAsync(dst, f32.p, n * kv * 4, cudaMemcpyDeviceToHost, st_));
+      e_->launches += 1;
+    }
+    RK_CUDA(cudaStreamSynchronize(st_));
+  };
+  prepared_ = false;
+  for (uint64_t l = 0; l < L; ++l) {
+    if (rq.hidden) {
+      RK_CUDA(cudaMemcpyAsync(rq.hidden + l * n * d, S.hidden.p, n * d * 4, cudaMemcpyDeviceToHost, st_));
+      RK_CUDA(cudaStreamSynchronize(st_));
+    }
+    if (kvcap) {
+      cap_k_ = static_cast<float*>(kst.p);
+      cap_v_ = static_cast<float*>(vst.p);
+    }
+    run_layer(ctx, (int)l, S.hidden.as<float>(), rows, true, (int)(base + n), rq.attn ? probs.as<float>() : nullptr,
+              0, (int)keys, -1);
+    cap_k_ = cap_v_ = nullptr;
+    if (kvcap) {
+      kv_out(rq.k_pre ? rq.k_pre + l * n * kv : nullptr, kst);
+      kv_out(rq.v ? rq.v + l * n * kv : nullptr, vst);
+    }
+    if (rq.attn) {
+      RK_CUDA(cudaMemcpyAsync(rq.attn + l * n * H * keys, probs.p, n * H * keys * 4, cudaMemcpyDeviceToHost, st_));
+      RK_CUDA(cudaStreamSynchronize(st_));
+    }
+  }
+  if (rq.logits) {  // output_logits over every row (model.cpp:282-288)
+    DevBuf lg(n * V * 4);
+    if (w_->precision == RK_BF16) {
+      rows_logits_bf16(e_, w_, S.hidden.as<float>(), rows, lg.as<float>());
+    } else {
+      k::rmsnorm_exact(st_, S.hidden.as<float>(), w_->final_norm, s.norm_eps, S.normed.as<float>(), rows, (int)d);
+      k::gemm_exact(st_, S.normed.as<float>(), static_cast<const float*>(w_->head), lg.as<float>(), rows, (int)V,
+                    (int)d, k::EPI_STORE, e_->status.as<int>());
+    }
+    e_->launches += 2;
+    RK_CUDA(cudaMemcpyAsync(rq.logits, lg.p, n * V * 4, cudaMemcpyDeviceToHost, st_));
+    RK_CUDA(cudaStreamSynchronize(st_));
+  }
+}
+
 // Validation of one relay_extend (relay_engine.cpp:186-192, 236-243, 296-298;
 // relay_cache.cpp:43-49, 157-161) and its layer window.
 ExtendPlan Runner::plan_extend(uint64_t base, rk_cache* cache, const rk_layer_profile* prof,
@@ -294,7 +376,15 @@ ExtendResult Runner::relay_extend(rk_context* ctx, rk_cache* cache, const rk_lay
   const rk_model_spec& s = w_->s;
   require(ctx != nullptr && ctx->w == w_, RK_ERR_INVALID_ARGUMENT, "context belongs to other weights");
   const ExtendPlan plan = plan_extend(ctx->size, cache, prof, opts);
-  wait_cache_all(cache);
+  // wait only for what this extend reads: RELAY/BLEND never read cache layers
+  // l_start..l_det-1 (the band recomputes them; l_det feeds the deviation
+  // score), FULL reads no layer at all -- deferred uploads of the others stay deferred
+  if (cache->async) {
+    wait_cache_meta(cache);
+    if (opts.mode != RK_MODE_FULL)
+      for (uint64_t l = 0; l < s.num_layers; ++l)
+        if (opts.mode == RK_MODE_ZERO || l < plan.l_start || l >= plan.l_det) wait_cache_layer(cache, l);
+  }
   const uint64_t n = cache->n, base = ctx->size, L = s.num_layers;
   const int mode = opts.mode;
   const uint64_t l_start = plan.l_start, l_det = plan.l_det, sparse_hi = plan.sparse_hi;

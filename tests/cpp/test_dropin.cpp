@@ -273,3 +273,123 @@ TEST_CASE("cache export/import is the identity") {
   std::filesystem::remove(p);
   CHECK_THROWS_AS(load_relay_cache(p), IoError);
 }
+
+// model.hpp:108-111 + workflow.cpp:304,343: PrefillResult.logits is chunk x
+// vocab and callers index row(n-1); every row equals a prefill ending there.
+TEST_CASE("prefill returns every row's logits (chunk x vocab)") {
+  const Weights w = init_weights(spec_of(6, 32, 4), 61);
+  const auto toks = pattern_tokens(9, 64, 3);
+  KVContext a(w.spec);
+  const PrefillResult all = prefill(w, toks, a, 0);
+  REQUIRE(all.logits.rows() == 9);
+  REQUIRE(all.logits.cols() == 64);
+  for (std::size_t n = 1; n <= 9; ++n) {  // row n-1 == the last row of a prefill of the first n tokens
+    KVContext b(w.spec);
+    const PrefillResult part = prefill(w, std::span<const TokenId>(toks.data(), n), b, 0);
+    CHECK(std::memcmp(part.logits.row(n - 1).data(), all.logits.row(n - 1).data(), 64 * 4) == 0);
+  }
+  set_prefill_logits(PrefillLogits::kLastRow);
+  KVContext c(w.spec);
+  const PrefillResult last = prefill(w, toks, c, 0);
+  set_prefill_logits(PrefillLogits::kAllRows);
+  CHECK(std::memcmp(last.logits.row(8).data(), all.logits.row(8).data(), 64 * 4) == 0);
+  CHECK(ctx_bit_equal(a, c));
+}
+
+// relay_cache.cpp:51-136 through the StepHook API (test_engine.cpp:43-62):
+// greedy_generate + RelayRecorder over host traces == the device recorder.
+TEST_CASE("RelayRecorder over greedy_generate traces equals the device capture") {
+  const Weights w = init_weights(spec_of(6, 32, 4), 62);
+  const auto old = pattern_tokens(11, 64, 4);
+  KVContext dctx(w.spec);
+  const PrefillResult p = prefill(w, old, dctx, 0);
+  CaptureFlags cap;
+  cap.hidden = cap.pre_rope_keys = cap.attention = true;
+  RelayRecorder rec(w.spec, old.size(), 1);
+  std::size_t steps = 0;
+  const StepHook hook = [&](const StepTrace& tr, TokenId tok, std::size_t pos) {
+    REQUIRE(tr.attn.size() == w.spec.num_layers);
+    CHECK(tr.attn[0][0].cols() == pos + 1);
+    rec.feed(tr, tok, pos);
+    ++steps;
+  };
+  const auto gen = greedy_generate(w, dctx, p.logits.row(old.size() - 1), 13, cap, hook);
+  const RelayCache host = rec.finalize();
+  KVContext dev_ctx;
+  const RelayCache dev = capture_relay_cache(w, old, 13, 1, &dev_ctx);
+  CHECK(steps == 13);
+  CHECK(gen.tokens == dev.segment_tokens);
+  CHECK(host.segment_tokens == dev.segment_tokens);
+  CHECK(host.influence == dev.influence);
+  CHECK(export_relay_cache(host) == export_relay_cache(dev));
+  CHECK(ctx_bit_equal(dctx, dev_ctx));
+  // a trace without attention is rejected by name (relay_cache.cpp:75-84)
+  RelayRecorder bad(w.spec, 0, 0);
+  CHECK_THROWS_AS(bad.feed(StepTrace{}, 1, 0), std::invalid_argument);
+}
+
+TEST_CASE("relay caches are validated before any pointer reaches the device") {
+  const Weights w = init_weights(spec_of(6, 32, 4), 63);
+  RelayCache c = capture_relay_cache(w, pattern_tokens(8, 64, 1), 6, 1);
+  RelayOptions opts;
+  RelayCache short_v = c;
+  short_v.v[2].data.resize(5);  // malformed: would be a heap over-read
+  short_v.v[2].shape = {1, 5};
+  CHECK_THROWS_AS(relay_prefill(w, pattern_tokens(4, 64, 2), short_v, triple(1, 2, 4), opts), std::invalid_argument);
+  CHECK_THROWS_AS(export_relay_cache(short_v), std::invalid_argument);
+  RelayCache wrong_geom = c;
+  wrong_geom.theta_base = 500000.0f;
+  CHECK_THROWS_AS(relay_prefill(w, pattern_tokens(4, 64, 2), wrong_geom, triple(1, 2, 4), opts),
+                  std::invalid_argument);
+  RelayCache neg = c;
+  neg.influence[0] = -1.0f;
+  CHECK_THROWS_AS(relay_prefill(w, pattern_tokens(4, 64, 2), neg, triple(1, 2, 4), opts), std::invalid_argument);
+}
+
+TEST_CASE("device weights follow the Weights object: in-place edits need release, new storage re-uploads") {
+  Weights w = init_weights(spec_of(6, 32, 4), 64);
+  const auto toks = pattern_tokens(7, 64, 5);
+  KVContext a(w.spec);
+  const PrefillResult base = prefill(w, toks, a, 0);
+  w.output_head.data[3] += 1.0f;  // in place: the device copy is now stale ...
+  release_device_weights(w);      // ... until released
+  KVContext b(w.spec);
+  const PrefillResult edited = prefill(w, toks, b, 0);
+  CHECK(std::memcmp(base.logits.row(6).data(), edited.logits.row(6).data(), 64 * 4) != 0);
+  w.output_head.data = std::vector<float>(w.output_head.data);  // new storage: detected without a release
+  w.output_head.data[3] -= 1.0f;
+  KVContext c(w.spec);
+  const PrefillResult restored = prefill(w, toks, c, 0);
+  CHECK(std::memcmp(base.logits.row(6).data(), restored.logits.row(6).data(), 64 * 4) == 0);
+  const Weights copy = w;  // a copy owns its own device copies
+  KVContext d(copy.spec);
+  const PrefillResult from_copy = prefill(copy, toks, d, 0);
+  CHECK(std::memcmp(base.logits.row(6).data(), from_copy.logits.row(6).data(), 64 * 4) == 0);
+}
+
+TEST_CASE("page-locked relay caches give the same relay") {
+  const Weights w = init_weights(spec_of(6, 32, 4), 65);
+  const RelayCache c = capture_relay_cache(w, pattern_tokens(9, 64, 1), 16, 1);
+  RelayOptions opts;
+  const RelayPrefillResult a = relay_prefill(w, pattern_tokens(5, 64, 2), c, triple(1, 2, 4), opts);
+  {
+    PinnedRelayCache pin(c);
+    const RelayPrefillResult b = relay_prefill(w, pattern_tokens(5, 64, 2), c, triple(1, 2, 4), opts);
+    CHECK(a.segment.selection.indices == b.segment.selection.indices);
+    CHECK(a.segment_end_logits.bit_equal(b.segment_end_logits));
+    CHECK(ctx_bit_equal(a.ctx.kv, b.ctx.kv));
+  }
+}
+
+// model.cpp:339-362 through the ABI (rk_row_logits_from_layer)
+TEST_CASE("row_logits_from_layer equals relay_prefill's segment-end logits") {
+  const Weights w = init_weights(spec_of(6, 32, 4), 66);
+  const RelayCache c = capture_relay_cache(w, pattern_tokens(9, 64, 1), 12, 1);
+  RelayOptions opts;
+  const RelayPrefillResult r = relay_prefill(w, pattern_tokens(5, 64, 2), c, triple(1, 2, 4), opts);
+  const std::size_t n = c.segment_len(), depth = r.segment.hidden_depth[n - 1];
+  REQUIRE(depth < w.spec.num_layers);
+  const Tensor lg = row_logits_from_layer(w, r.segment.segment_hidden.row(n - 1), depth, r.ctx.kv,
+                                          r.ctx.kv.size() - 1);
+  CHECK(lg.bit_equal(r.segment_end_logits));
+}

@@ -193,3 +193,27 @@ def test_bytes_api_matches_file_api(path):
         HostRelayCache.from_bytes(data[:-3])
     with pytest.raises(SchemaError):
         HostRelayCache.from_bytes(b"")
+
+
+def test_theta_float_formatting_sweep_matches_reference(tmp_path):
+    """nlohmann::json dump formats the manifest's theta_base with Grisu2
+    (shortest digits in most cases, not all); the engine's formatter searches
+    the shortest round-trip digits. A randomized sweep of float theta values
+    over 80 binades pins that both produce the same bytes."""
+    orc = ref_oracle()
+    r = np.random.default_rng(7)
+    exps = r.integers(-40, 40, 1500)
+    mant = r.random(1500) + 1.0
+    thetas = [float(np.float32(m * 2.0 ** int(e))) for m, e in zip(mant, exps)]
+    thetas += [float(np.float32(x)) for x in (1e4, 5e5, 1e6, 1e-3, 123456.789, 3.0e38, 1.17549435e-38)]
+    base = random_cache(11, L=1, n=1)
+    ours, theirs = tmp_path / "o.rkrc", tmp_path / "t.rkrc"
+    bad = []
+    for th in thetas:
+        base.theta_base = th
+        base.save(ours)
+        orc.save_cache(base, theirs)
+        a, b = ours.read_bytes(), theirs.read_bytes()
+        if a != b:
+            bad.append((th, split(a)[1].get("theta_base"), split(b)[1].get("theta_base")))
+    assert not bad, bad[:10]

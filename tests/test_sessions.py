@@ -51,3 +51,24 @@ def test_gloo_world2_gather(n):
     assert [r["session"] for r in out] == list(range(n))
     assert all(r["first_token"] == 1000 + r["session"] for r in out)
     assert {r["ttft_ns"] for r in out} == ({5_000_000, 6_000_000} if n > 1 else {5_000_000})
+
+
+def test_bench_gpus_flag_spawns_ranks():
+    """`python bench.py --gpus 2` (no torchrun around it) launches 2 ranks itself
+    (bench.spawn_ranks -> torch.distributed.run), shards c4's 64 sessions, and
+    rank 0 prints one line with every session gathered. The stub impl runs the
+    same launcher / shard / barrier / max-over-ranks / all_gather plumbing as
+    the engine arm with a CPU no-op session (gloo)."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "stub", "--gpus", "2",
+                          "--config", "c4", "--steps", "2"], capture_output=True, text=True, timeout=240, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    rec = json.loads(lines[0])
+    assert rec["n_gpus"] == 2 and rec["sessions_per_rank"] == 32
+    assert rec["sessions_gathered"] == 64 and rec["gathered_ids"] == list(range(64)) and rec["first_tokens_ok"]
