@@ -43,8 +43,19 @@ class HostRelayCache:
         return int(self.k_pre.shape[0])
 
     def view(self):
-        """rk_relay_cache_view pointing into this object's arrays (kept alive by self)."""
-        L = self.num_layers
+        """rk_relay_cache_view pointing into this object's arrays (kept alive by self).
+        Array shapes are checked first (the C ABI reads L x n x kv_dim floats per
+        K/V table, n x d_model hidden floats and n influence scores); the
+        reference's semantic checks (relay_cache.cpp:18-49) run in the ABI."""
+        from paper_2603_13289_b200.abi import RK_ERR_INVALID_ARGUMENT, exception_for
+        L, n, kv = self.num_layers, self.segment_len, self.num_kv_heads * self.d_head
+        if self.k_pre.ndim != 3 or self.k_pre.shape[1:] != (n, kv) or self.v.shape != self.k_pre.shape:
+            raise exception_for(RK_ERR_INVALID_ARGUMENT, "relay cache: K/V tables must be [L, n, kv_dim] "
+                                f"({L}, {n}, {kv}); got {self.k_pre.shape} / {self.v.shape}")
+        if self.hidden_snapshot.shape != (n, self.d_model):
+            raise exception_for(RK_ERR_INVALID_ARGUMENT, "relay cache: hidden snapshot shape mismatch")
+        if self.influence.shape != (n,):
+            raise exception_for(RK_ERR_INVALID_ARGUMENT, "relay cache: influence length mismatch")
         kp = (C.POINTER(C.c_float) * max(L, 1))()
         vp = (C.POINTER(C.c_float) * max(L, 1))()
         for l in range(L):

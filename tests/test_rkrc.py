@@ -217,3 +217,17 @@ def test_theta_float_formatting_sweep_matches_reference(tmp_path):
         if a != b:
             bad.append((th, split(a)[1].get("theta_base"), split(b)[1].get("theta_base")))
     assert not bad, bad[:10]
+
+
+def test_view_rejects_malformed_arrays():
+    """HostRelayCache.view() checks array shapes before handing pointers to
+    the C ABI (which reads L x n x kv_dim floats per table): a short V table,
+    a wrong hidden snapshot or influence length is InvalidArgument, not a
+    heap over-read."""
+    for mutate in (lambda c: setattr(c, "v", np.ascontiguousarray(c.v[:, :2])),
+                   lambda c: setattr(c, "hidden_snapshot", np.ascontiguousarray(c.hidden_snapshot[:, :3])),
+                   lambda c: setattr(c, "influence", np.ascontiguousarray(c.influence[:1]))):
+        c = random_cache(5, L=2, n=4)
+        mutate(c)
+        with pytest.raises(InvalidArgument):
+            c.view()
