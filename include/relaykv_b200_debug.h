@@ -32,6 +32,9 @@ int rk_debug_bench_gemm(rk_engine* e, int M, int N, int K, int epi, int iters, f
 int rk_debug_select_relay(rk_engine* e, const double* s_dev, const float* influence, double infl_mean, int n,
                           double tau_dev, double tau_inf, int suffix_k, int32_t* sel_idx, uint32_t* sel_tags,
                           int32_t* count, double* dinfo);
+/* top_k_by_score (selector.cpp:90-105) on the device (radix select):
+   the `count` largest scores, ties by ascending index, as an ascending list */
+int rk_debug_select_topk(rk_engine* e, const double* score, int n, int count, int32_t* sel_idx, int32_t* out_count);
 /* y[i] = device glibc_expf(x[i]) */
 int rk_debug_expf(rk_engine* e, const float* x, float* y, uint64_t n);
 /* Host only: the upload path's fp32 -> bf16 conversion on a `threads`-worker pool. */

@@ -1,6 +1,8 @@
 // debug_hooks.cu -- kernel-level test entry points (relaykv_b200_debug.h).
 #include <string>
 #include <vector>
+#include <algorithm>
+#include <cstdlib>
 #include <cmath>
 
 #include "glibc_expf.h"
@@ -165,12 +167,18 @@ int rk_debug_trace_attention(rk_engine* e, int M, int T, int H, int Hkv, int dh,
 int rk_debug_bench_gemm(rk_engine* e, int M, int N, int K, int epi, int iters, float* ms) {
   return guard([&] {
     cudaStream_t st = e->stream;
-    DevBuf f((size_t)(M > N ? M : N) * K * 4), a((size_t)M * K * 2), b((size_t)N * K * 2), c((size_t)M * N * 4),
+    // the weights rotate over enough copies (>= 256 MB) that every iteration
+    // streams them from HBM, as each layer's weights are in a relay step
+    const size_t wbytes = (size_t)N * K * 2;
+    int copies = (int)std::min<size_t>(16, std::max<size_t>(1, ((size_t)256 << 20) / wbytes + 1));
+    if (const char* c = std::getenv("RK_BENCH_COPIES")) copies = std::max(1, std::atoi(c));  // 1: L2-resident weights
+    DevBuf f((size_t)(M > N ? M : N) * K * 4), a((size_t)M * K * 2), b(wbytes * copies), c((size_t)M * N * 4),
         flags(1 << 18);
     k::init_uniform(st, f.as<float>(), (size_t)M * K, 21, 1.0f);
     k::f32_to_bf16(st, a.as<__nv_bfloat16>(), f.as<float>(), (size_t)M * K);
     k::init_uniform(st, f.as<float>(), (size_t)N * K, 22, 0.02f);
-    k::f32_to_bf16(st, b.as<__nv_bfloat16>(), f.as<float>(), (size_t)N * K);
+    for (int i = 0; i < copies; ++i)
+      k::f32_to_bf16(st, b.as<__nv_bfloat16>() + (size_t)i * N * K, f.as<float>(), (size_t)N * K);
     RK_CUDA(cudaMemsetAsync(c.p, 0, c.bytes, st));
     RK_CUDA(cudaMemsetAsync(flags.p, 0, flags.bytes, st));
     GemmArgs g;
@@ -188,7 +196,8 @@ int rk_debug_bench_gemm(rk_engine* e, int M, int N, int K, int epi, int iters, f
     RK_CUDA(cudaEventCreate(&e0));
     RK_CUDA(cudaEventCreate(&e1));
     RK_CUDA(cudaEventRecord(e0, st));
-    for (int i = 0; i < iters; ++i) gemm_bf16(e, a.as<__nv_bfloat16>(), K, b.as<__nv_bfloat16>(), g, M);
+    for (int i = 0; i < iters; ++i)
+      gemm_bf16(e, a.as<__nv_bfloat16>(), K, b.as<__nv_bfloat16>() + (size_t)(i % copies) * N * K, g, M);
     RK_CUDA(cudaEventRecord(e1, st));
     RK_CUDA(cudaEventSynchronize(e1));
     RK_CUDA(cudaEventElapsedTime(ms, e0, e1));
@@ -196,6 +205,20 @@ int rk_debug_bench_gemm(rk_engine* e, int M, int N, int K, int epi, int iters, f
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     RK_CUDA(cudaGetLastError());
+  });
+}
+
+int rk_debug_select_topk(rk_engine* e, const double* score, int n, int count, int32_t* sel_idx, int32_t* out_count) {
+  return guard([&] {
+    cudaStream_t st = e->stream;
+    DevBuf sc((size_t)n * 8 + 8), idx((size_t)n * 4 + 4), tags((size_t)2 * n * 4 + 8), info(64);
+    RK_CUDA(cudaMemcpy(sc.p, score, (size_t)n * 8, cudaMemcpyHostToDevice));
+    RK_CUDA(cudaMemset(info.p, 0, 64));
+    k::select_topk(st, sc.as<double>(), n, count, idx.as<int>(), tags.as<uint32_t>(), info.as<int>());
+    RK_CUDA(cudaStreamSynchronize(st));
+    RK_CUDA(cudaGetLastError());
+    RK_CUDA(cudaMemcpy(out_count, info.p, 4, cudaMemcpyDeviceToHost));
+    RK_CUDA(cudaMemcpy(sel_idx, idx.p, (size_t)*out_count * 4, cudaMemcpyDeviceToHost));
   });
 }
 

@@ -180,8 +180,8 @@ __device__ __forceinline__ void epilogue_chunk(const GemmArgs& p, int row, int c
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const float g0 = v[4 * j], u0 = v[4 * j + 1], g1 = v[4 * j + 2], u1 = v[4 * j + 3];
-      const float a0 = g0 / (1.0f + __expf(-g0)) * u0;
-      const float a1 = g1 / (1.0f + __expf(-g1)) * u1;
+      const float a0 = __fdividef(g0, 1.0f + __expf(-g0)) * u0;  // (no IEEE-division slow path; bf16 output)
+      const float a1 = __fdividef(g1, 1.0f + __expf(-g1)) * u1;
       packed[j] = pack_bf16(a0, a1);
     }
     uint4* dst = reinterpret_cast<uint4*>(p.out_bf16 + (size_t)row * p.ld_bf16 + col / 2);
@@ -339,6 +339,96 @@ __device__ __forceinline__ void csk_epilogue(const GemmArgs& p, const Units& U, 
         p.norm_inv[grow] = rsqrtf(tot / (float)p.N + p.norm_eps);
       }
       if (threadIdx.x == 64) p.norm_cnt[(size_t)mt * 8 + me] = 0;
+    }
+  }
+}
+
+// In-kernel split-K fixup (EPI_PART with p.fixup): after storing its fp32
+// partial of a 32-row group of tile (mt, nt), a warp takes a ticket; the last
+// of the p.splits warps sums the partials in split order (the order of
+// splitk_reduce_add_kernel, so the same bits), adds them to the residual and
+// runs the fused RMSNorm producer side -- no reduce launch, partials read from
+// L2 right after they were written. Lanes: 8 per row (16-byte chunks), 4 rows
+// per pass; all loads of a pass are in flight before the adds.
+template <int BN>
+__device__ __noinline__ void splitk_fixup(const GemmArgs& p, int splits, int num_n, int num_m128, int mt, int nt,
+                                          int quarter, int lane, int M) {
+  const int row0 = mt * kBM + quarter * 32;
+  if (row0 >= M) return;  // (every split skips these rows alike)
+  int* cnt = p.split_flags + ((size_t)(nt * num_m128 + mt) * 4 + quarter);
+  __threadfence();
+  __syncwarp();
+  int prev = 0;
+  if (lane == 0) prev = atomicAdd(cnt, 1);
+  prev = __shfl_sync(0xffffffffu, prev, 0);
+  if (prev != splits - 1) return;
+  __threadfence();  // the other splits' partials are visible from here
+  const bool norm = p.norm_part != nullptr;
+  const int sub = lane >> 3, ch = lane & 7;
+  constexpr int NC = BN / 32;  // 32-column passes
+  float chk = 0.f;
+#pragma unroll 1
+  for (int rg = 0; rg < 8; ++rg) {
+    const int row = row0 + rg * 4 + sub;
+    const bool ok = row < M;
+    const size_t rr = ok ? (size_t)row : (size_t)row0;
+    float4 acc[NC], h[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int col = nt * BN + c * 32 + ch * 4;
+      acc[c] = __ldcg(reinterpret_cast<const float4*>(p.ws_part + rr * p.N + col));
+      h[c] = __ldcg(reinterpret_cast<const float4*>(p.out_f32 + rr * p.ld_out + col));
+    }
+    for (int sp = 1; sp < splits; ++sp) {
+      float4 v[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+        v[c] = __ldcg(reinterpret_cast<const float4*>(p.ws_part + ((size_t)sp * p.rows_max + rr) * p.N + nt * BN +
+                                                      c * 32 + ch * 4));
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        acc[c].x += v[c].x; acc[c].y += v[c].y; acc[c].z += v[c].z; acc[c].w += v[c].w;
+      }
+    }
+    float ss = 0.f;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int col = nt * BN + c * 32 + ch * 4;
+      chk = finite_acc(finite_acc(finite_acc(finite_acc(chk, acc[c].x), acc[c].y), acc[c].z), acc[c].w);
+      float4 x = h[c];
+      x.x += acc[c].x; x.y += acc[c].y; x.z += acc[c].z; x.w += acc[c].w;
+      if (ok) {
+        *reinterpret_cast<float4*>(p.out_f32 + rr * p.ld_out + col) = x;
+        if (norm) {
+          ss = fmaf(x.x, x.x, fmaf(x.y, x.y, fmaf(x.z, x.z, fmaf(x.w, x.w, ss))));
+          *reinterpret_cast<uint2*>(p.norm_bf16 + rr * p.N + col) = make_uint2(pack_bf16(x.x, x.y), pack_bf16(x.z, x.w));
+        }
+      }
+    }
+    if (norm) {
+      ss += __shfl_xor_sync(0xffffffffu, ss, 1);
+      ss += __shfl_xor_sync(0xffffffffu, ss, 2);
+      ss += __shfl_xor_sync(0xffffffffu, ss, 4);
+      if (ok && ch == 0) p.norm_part[rr * kNormSlots + nt] = ss;
+    }
+  }
+  flag_nonfinite(p.status, chk);
+  if (lane == 0) *cnt = 0;  // self-resetting for the next GEMM
+  if (norm) {  // the last of the num_n tiles of these 32 rows turns the partials into 1/rms
+    __threadfence();
+    __syncwarp();
+    int done = 0;
+    if (lane == 0) done = atomicAdd(p.norm_cnt + (size_t)mt * 4 + quarter, 1) + 1;
+    done = __shfl_sync(0xffffffffu, done, 0);
+    if (done == num_n) {
+      __threadfence();
+      const int row = row0 + lane;
+      if (row < M) {
+        float tot = 0.f;
+        for (int t = 0; t < num_n; ++t) tot += __ldcg(p.norm_part + (size_t)row * kNormSlots + t);
+        p.norm_inv[row] = rsqrtf(tot / (float)p.N + p.norm_eps);
+      }
+      if (lane == 0) p.norm_cnt[(size_t)mt * 4 + quarter] = 0;
     }
   }
 }
@@ -503,7 +593,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row = mt * kBM + quarter * 32 + lane;
       int* flag = nullptr;
       if (EPI == EPI_ADD && U.splits > 1) {  // ordered split-K: wait for split s-1 on these rows
-        flag = p.split_flags + ((size_t)(nt * U.num_m + mt) * 4 + quarter);
+        flag = p.split_flags + ((size_t)(nt * U.num_m * PAIR * MT + mt) * 4 + quarter);  // mt: this CTA's 128-row tile
         if (lane == 0)
           while (atomicAdd(flag, 0) != s) __nanosleep(64);
         __syncwarp();
@@ -623,6 +713,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (PAIR == 2) mbar_arrive_cluster(&tempty[acc], 0);
         else mbar_arrive(&tempty[acc]);
       }
+      if constexpr (EPI == EPI_PART && MT == 1) {  // (the accumulator is released first: the fixup reads no TMEM)
+        if (p.fixup && !p.streamk)
+          splitk_fixup<BN>(p, U.splits, U.num_n, U.num_m * PAIR, (w.mt * PAIR + rank), w.nt, quarter, lane, M);
+      }
     }
   }
   if constexpr (CSK) {
@@ -637,6 +731,223 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     if (warp == 1) tmem_dealloc(tmem, C::TMEM_COLS);
   }
+}
+
+// ---------------------------------------------------------------------------
+// Swap-AB CTA pair for short static M (the prefix/suffix-only layers, M <= 512):
+// D^T[N x M] = W[N x K] . X[M x K]^T. The weights take the MMA's M side -- 256
+// rows per pair, each CTA staging its own 128 -- and the M tokens its N side,
+// nc chunks of tc columns (each CTA staging half of every chunk). The 1-CTA
+// 128 x 256 tile stages 48 KB per k-block for 4.2 MFLOP and, at M = 320, reads
+// every weight tile three times in two rounds; here a CTA stages 16 + M/16 KB
+// for 2*128*M*64 FLOP (M = 320: 36 KB for 5.2 MFLOP) and each weight tile is
+// read by exactly one pair in one round. TMEM lane = output feature, column =
+// token, so the epilogue walks 32 tokens per tcgen05.ld; residual GEMMs store
+// split-K partials (EPI_PART) for splitk_reduce_add_kernel.
+// ---------------------------------------------------------------------------
+constexpr int kSwStages = 4;
+constexpr int kSwA = kBM * kBK * 2;     // 16 KB: this CTA's 128 weight rows
+constexpr int kSwBMax = 256 * kBK * 2;  // 32 KB: half of up to 512 tokens
+constexpr int kSwStage = kSwA + kSwBMax;
+constexpr int kSwRs = 544;  // row scales of up to 512 tokens (+ one chunk of padding)
+constexpr int kSwSmem = kSwStages * kSwStage + 1024 + 256 + kSwRs * 4;
+constexpr uint32_t kSwTmemCols = 512;
+constexpr int kSwThreads = 320;  // producer, MMA issuer, 8 epilogue warps (two per TMEM lane quarter)
+
+// Epilogue of one CTA's 128 features (thread = feature n) over the M tokens.
+// rs_sm: the M row scales (1.0 without a fused RMSNorm), staged in shared
+// memory; warp half `hw` of a lane quarter takes token chunks hw, hw+2, ...
+template <int EPI>
+__device__ __forceinline__ void swap_epilogue(const GemmArgs& p, uint32_t tbase, int n, int M, int split,
+                                              int lane, int hw, const float* rs_sm) {
+  const bool odd = lane & 1;  // == n & 1: RoPE pairs and (gate, up) pairs are adjacent lanes
+  float chk = 0.f;
+#pragma unroll 1
+  for (int t0 = 32 * hw; t0 < M; t0 += 64) {
+    uint32_t r[32];
+    tmem_ld32(tbase + (uint32_t)t0, r);
+    tmem_ld_wait();
+    float v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      v[j] = __uint_as_float(r[j]) * rs_sm[t0 + j];
+      if (t0 + j < M) chk = finite_acc(chk, v[j]);  // (columns past the token tile hold no data)
+    }
+    if constexpr (EPI == EPI_F32 || EPI == EPI_PART) {
+      float* base = EPI == EPI_PART ? p.ws_part + (size_t)split * p.rows_max * p.N + n : p.out_f32 + n;
+      const size_t ld = EPI == EPI_PART ? (size_t)p.N : (size_t)p.ld_out;
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (t0 + j < M) base[(size_t)(t0 + j) * ld] = v[j];
+    } else if constexpr (EPI == EPI_SILU) {
+      // even lane (gate) takes tokens t0..t0+15, odd lane (up) t0+16..t0+31
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const float recv = __shfl_xor_sync(0xffffffffu, odd ? v[j] : v[16 + j], 1);
+        const int t = odd ? t0 + 16 + j : t0 + j;
+        const float g = odd ? recv : v[j], u = odd ? v[16 + j] : recv;
+        if (t < M) p.out_bf16[(size_t)t * p.ld_bf16 + n / 2] = __float2bfloat16_rn(__fdividef(g, 1.0f + __expf(-g)) * u);
+      }
+    } else {  // EPI_QKV
+      const int q = p.q, kv = p.kv, dh = p.dh;
+      if (n >= q + kv) {  // V rows into the context (warp-uniform region: q, kv are multiples of 32)
+        const int c = n - q - kv;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int t = t0 + j;
+          if (t >= M) break;
+          const __nv_bfloat16 b = __float2bfloat16_rn(v[j]);
+          if (p.cap_v) p.cap_v[(size_t)t * kv + c] = b;
+          (p.commit ? p.ctx_v + (size_t)p.pos[t] * kv : p.self_v + (size_t)t * kv)[c] = b;
+        }
+      } else {
+        const bool is_k = n >= q;
+        const int c = is_k ? n - q : n, pi = (c % dh) / 2;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float partner = __shfl_xor_sync(0xffffffffu, v[j], 1);
+          const int t = t0 + j;
+          if (t < M) {
+            if (is_k && p.cap_k) p.cap_k[(size_t)t * kv + c] = __float2bfloat16_rn(v[j]);
+            const int pos = p.pos[t];
+            const float2 cs = p.rope[(size_t)pos * (dh / 2) + pi];
+            const float x0 = odd ? partner : v[j], x1 = odd ? v[j] : partner;
+            const float o = odd ? x0 * cs.y + x1 * cs.x : x0 * cs.x - x1 * cs.y;
+            __nv_bfloat16* base = !is_k ? p.out_bf16 + (size_t)t * p.ld_bf16
+                                        : (p.commit ? p.ctx_k + (size_t)pos * kv : p.self_k + (size_t)t * kv);
+            base[c] = __float2bfloat16_rn(o);
+          }
+        }
+      }
+    }
+  }
+  flag_nonfinite(p.status, chk);
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(kSwThreads, 1)
+    gemm_swap_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+                     const GemmArgs p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSwStages * kSwStage);
+  uint64_t* empty = full + kSwStages;
+  uint64_t* tfull = empty + kSwStages;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  float* rs_sm = reinterpret_cast<float*>(smem + kSwStages * kSwStage + 256);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_ctarank();  // 0 = leader (issues the MMAs)
+  pdl_trigger();
+  const int tc = p.tc, nc = p.nc, half = tc / 2;
+  const uint32_t stage_tx = 2u * (uint32_t)(kSwA + nc * half * kBK * 2);  // both CTAs' bytes, on the leader
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmW);
+    tma_prefetch(&tmX);
+    for (int i = 0; i < kSwStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 16);  // the 8 epilogue warps of both CTAs
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_pair(tmem_slot, kSwTmemCols);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int kb_total = p.K / kBK, splits = p.splits, kb_per = (kb_total + splits - 1) / splits;
+  const int units = (p.N / 256) * splits;
+  // unit -> (weight tile, split), split fastest; both CTAs of a pair walk the same units
+  auto unit_of = [&](int k, int& wt, int& s, int& kb0, int& kb1) {
+    const int u = (int)blockIdx.x / 2 + k * ((int)gridDim.x / 2);
+    if (u >= units) return false;
+    s = u % splits;
+    wt = u / splits;
+    kb0 = s * kb_per;
+    kb1 = min(kb_total, kb0 + kb_per);
+    return true;
+  };
+  // the first stages' weights do not depend on the previous kernel: in flight before the wait
+  int pre = 0;
+  if (warp == 0) {
+    int wt, s, kb0, kb1;
+    if (elect_one() && unit_of(0, wt, s, kb0, kb1)) {
+      pre = min(kSwStages, kb1 - kb0);
+      for (int i = 0; i < pre; ++i) {
+        if (rank == 0) mbar_arrive_expect_tx(&full[i], stage_tx);
+        tma_load_2d_pair(smem + i * kSwStage, &tmW, &full[i], (kb0 + i) * kBK, wt * 256 + (int)rank * kBM);
+      }
+    }
+  }
+  pdl_wait();
+
+  if (warp == 0) {
+    if (elect_one()) {  // ---------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      int wt, s, kb0, kb1;
+      for (int it = 0; unit_of(it, wt, s, kb0, kb1); ++it) {
+        for (int kb = kb0; kb < kb1; ++kb) {
+          const bool early = it == 0 && kb - kb0 < pre;
+          uint8_t* sa = smem + stage * kSwStage;
+          if (!early) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            if (rank == 0) mbar_arrive_expect_tx(&full[stage], stage_tx);
+            tma_load_2d_pair(sa, &tmW, &full[stage], kb * kBK, wt * 256 + (int)rank * kBM);
+          }
+          for (int c = 0; c < nc; ++c)
+            tma_load_2d_pair(sa + kSwA + c * half * (kBK * 2), &tmX, &full[stage], kb * kBK, c * tc + (int)rank * half);
+          if (++stage == kSwStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0 && elect_one()) {  // ---------------- MMA issuer (the pair's leader)
+      const uint32_t idesc = idesc_bf16(2 * kBM, tc);
+      int stage = 0;
+      uint32_t phase = 0;
+      int wt, s, kb0, kb1;
+      for (int it = 0; unit_of(it, wt, s, kb0, kb1); ++it) {
+        mbar_wait(tempty, (it & 1) ^ 1);
+        tc_fence_after();
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(smem + stage * kSwStage), b0 = a0 + kSwA;
+          for (int c = 0; c < nc; ++c) {
+#pragma unroll
+            for (int k = 0; k < kBK / 16; ++k)
+              mma_bf16_ss_pair(tmem + (uint32_t)(c * tc), sdesc_sw128(a0 + k * 32, 16, 1024),
+                               sdesc_sw128(b0 + c * half * (kBK * 2) + k * 32, 16, 1024), idesc,
+                               (kb > kb0 || k > 0) ? 1u : 0u);
+          }
+          tc_commit_pair(&empty[stage]);
+          if (++stage == kSwStages) { stage = 0; phase ^= 1; }
+        }
+        tc_commit_pair(tfull);
+      }
+    }
+  } else {  // ------------------------------- epilogue warps 2..9
+    const int quarter = warp & 3, hw = (warp - 2) >> 2;
+    for (int i = threadIdx.x - 64; i < kSwRs; i += 256)
+      rs_sm[i] = i < p.rows_max ? (p.row_scale ? p.row_scale[i] : 1.0f) : 0.0f;
+    named_bar_sync(1, 256);
+    int wt, s, kb0, kb1;
+    for (int it = 0; unit_of(it, wt, s, kb0, kb1); ++it) {
+      mbar_wait(tfull, it & 1);
+      tc_fence_after();
+      const int n = wt * 256 + (int)rank * kBM + quarter * 32 + lane;
+      swap_epilogue<EPI>(p, tmem + ((uint32_t)(quarter * 32) << 16), n, p.rows_max, s, lane, hw, rs_sm);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty, 0);
+    }
+  }
+  tc_fence_before();
+  cluster_sync();  // neither CTA leaves while its peer may still signal its barriers
+  if (warp == 1) tmem_dealloc_pair(tmem, kSwTmemCols);
 }
 
 // Split-K reduction + residual epilogue (EPI_PART partials): one CTA per row,
@@ -1150,7 +1461,7 @@ void make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t c
 //    1-CTA shapes: EPI_PART partials reduced in split order by
 //    splitk_reduce_add_kernel (+ ~3 us and 2*s*M*N*4 B at ~8 TB/s), or the
 //    opt-in cluster (DSMEM) reduction / stream-K.
-static void choose_config(GemmArgs& p, int sm_count, int rows_hint) {
+static double choose_config(GemmArgs& p, int sm_count, int rows_hint) {
   auto env = [](const char* name, int dflt) {
     const char* v = std::getenv(name);
     return v ? std::atoi(v) : dflt;
@@ -1250,6 +1561,55 @@ static void choose_config(GemmArgs& p, int sm_count, int rows_hint) {
     p.streamk = pick.streamk;
     if (pick.streamk || (pick.splits > 1 && !pick.csk)) p.epi = EPI_PART;
   }
+  return best;
+}
+
+// Swap-AB pair (gemm_swap_kernel) for a short static M. Measured (r02g,
+// weights streamed from HBM): it wins for the wide SiLU GEMMs of the
+// prefix/suffix-only layers -- c2 gate/up M=320 N=16384 30.1 -> 25.2 us, c3
+// N=28672 84.6 -> 77.0 us -- where the 1-CTA kernel needs two rounds of
+// 128 x 256 tiles and re-reads every weight tile per m tile; it loses on the
+// narrow QKV / W_o / down GEMMs (too few 256-row weight tiles to fill the
+// SMs, and its single-unit epilogue is exposed). RK_GEMM_SWAP: 0 never,
+// 1 (default) wide SiLU GEMMs with 128 < M <= 512, 2 every eligible GEMM
+// (tests; residual GEMMs then write split-K partials).
+static bool choose_swap(GemmArgs& p, int sm_count, double other_us) {
+  static const int swap_env = [] {
+    const char* v = std::getenv("RK_GEMM_SWAP");
+    return v ? std::atoi(v) : 1;
+  }();
+  const int M = p.rows_max;
+  if (!swap_env || p.rows_dev || M < 2 || M > 512 || p.N % 256 || p.K % kBK) return false;
+  if (!(p.epi == EPI_QKV || p.epi == EPI_SILU || p.epi == EPI_F32 || p.epi == EPI_ADD)) return false;
+  if (p.epi == EPI_QKV && (p.q % 32 || p.kv % 32)) return false;
+  const int pslots = pair_slots(sm_count);
+  if (pslots <= 0) return false;
+  const int nc = M <= 256 ? 1 : 2;
+  const int tc = ((M + nc - 1) / nc + 15) / 16 * 16;
+  const int kb = p.K / kBK, tiles = p.N / 256;
+  if (swap_env != 2 && !(p.epi == EPI_SILU && M > kBM && 2 * tiles >= pslots)) return false;
+  (void)other_us;
+  const double t_kb = std::max(0.0096 * (16.0 + nc * tc / 16.0), 2.0 * nc * tc / 1900.0);
+  double best = 1e30;
+  int best_s = 1;
+  for (int s = 1; s <= (p.epi == EPI_ADD ? 8 : 1); ++s) {  // (splitk_reduce_add_kernel: <= 8 partials)
+    if (s > 1 && (kb / s < 2 || (s - 1) * ((kb + s - 1) / s) >= kb)) continue;
+    const int units = tiles * s;
+    double c = (double)((units + pslots - 1) / pslots) * ((kb + s - 1) / s) * t_kb + 1.0;
+    if (p.epi == EPI_ADD) c += 3.0 + 2.0 * s * (double)M * p.N * 4 / 8e6;  // partials + reduce kernel
+    if (c < best) { best = c; best_s = s; }
+  }
+  p.swap = 1;
+  p.nc = nc;
+  p.tc = tc;
+  p.pair = 2;
+  p.mt_group = 1;
+  p.csk = 0;
+  p.streamk = 0;
+  p.splits = best_s;
+  p.bn = 256;
+  if (p.epi == EPI_ADD) p.epi = EPI_PART;
+  return true;
 }
 
 void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat16* B, GemmArgs p,
@@ -1302,8 +1662,72 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
     }
     return;
   }
-  choose_config(p, e->sm_count, rows_hint > 0 ? rows_hint : p.rows_max);
+  {
+    GemmArgs alt = p;
+    const double other = choose_config(alt, e->sm_count, rows_hint > 0 ? rows_hint : p.rows_max);
+    if (!choose_swap(p, e->sm_count, other)) p = alt;
+  }
   static const bool log = std::getenv("RK_GEMM_LOG") != nullptr;
+  if (p.swap) {
+    if (log)
+      std::fprintf(stderr, "[gemm] M=%d N=%d K=%d epi=%d -> swap nc=%d tc=%d splits=%d\n", p.rows_max, p.N, p.K, p.epi,
+                   p.nc, p.tc, p.splits);
+    CUtensorMap tw, tx;
+    make_tmap_bf16(&tw, B, (uint64_t)p.N, (uint64_t)p.K, kBM, (uint64_t)p.K);
+    make_tmap_bf16(&tx, A, (uint64_t)p.rows_max, (uint64_t)p.K, (uint32_t)(p.tc / 2), (uint64_t)lda);
+    const int units = (p.N / 256) * p.splits;
+    const int grid = 2 * std::min(units, pair_slots(e->sm_count));
+    if (p.epi == EPI_PART) {
+      e->scratch->gemm_ws.ensure((size_t)p.splits * p.rows_max * p.N * 4);
+      p.ws_part = e->scratch->gemm_ws.as<float>();
+    }
+    static const char* kEpiS[] = {"qkv", "add", "silu", "f32", "addsplit"};
+    ProfScope ps(e, (e->prof && e->prof->on)
+                        ? intern(std::string("gemm_") + kEpiS[p.epi] + "_m" + std::to_string(p.rows_max) + "_n" +
+                                 std::to_string(p.N) + "_k" + std::to_string(p.K) + "_swap_s" + std::to_string(p.splits))
+                        : "gemm",
+                 0, 0);
+    ps.rec.kind = 1;
+    ps.rec.rows_dev = nullptr;
+    ps.rec.rows_max = p.rows_max;
+    ps.rec.N = p.N;
+    ps.rec.K = p.K;
+    static bool attr_done[5] = {false, false, false, false, false};
+    auto go = [&](auto kern) {
+      if (!attr_done[p.epi]) {
+        RK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSwSmem));
+        attr_done[p.epi] = true;
+      }
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(grid);
+      cfg.blockDim = dim3(kSwThreads);
+      cfg.dynamicSmemBytes = kSwSmem;
+      cfg.stream = e->stream;
+      cudaLaunchAttribute at[2];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[1].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = pdl_enabled() ? 2 : 1;
+      RK_CUDA(cudaLaunchKernelEx(&cfg, kern, tw, tx, p));
+    };
+    switch (p.epi) {
+      case EPI_QKV: go(gemm_swap_kernel<EPI_QKV>); break;
+      case EPI_SILU: go(gemm_swap_kernel<EPI_SILU>); break;
+      case EPI_PART:
+        go(gemm_swap_kernel<EPI_PART>);
+        launch_pdl(splitk_reduce_add_kernel, dim3(std::min(p.rows_max, 8 * e->sm_count)), dim3(256), 0, e->stream, p,
+                   (int)p.splits, grid);
+        e->launches += 1;
+        break;
+      default: go(gemm_swap_kernel<EPI_F32>); break;
+    }
+    e->launches += 1;
+    return;
+  }
   if (log)
     std::fprintf(stderr, "[gemm] M=%d%s N=%d K=%d epi=%d -> bn=%d pair=%d mt=%d splits=%d csk=%d streamk=%d\n",
                  p.rows_max, p.rows_dev ? "(dyn)" : "", p.N, p.K, p.epi, p.bn, p.pair, p.mt_group, p.splits, p.csk,
@@ -1340,12 +1764,22 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
     case EPI_QKV: launch_bn<EPI_QKV>(e->stream, ta, tb, p, grid); break;
     case EPI_ADD: launch_bn<EPI_ADD>(e->stream, ta, tb, p, grid); break;
     case EPI_SILU: launch_bn<EPI_SILU>(e->stream, ta, tb, p, grid); break;
-    case EPI_PART:
+    case EPI_PART: {
+      // split-K reduced inside the GEMM by the last split of each row group
+      // (RK_GEMM_FIXUP=0: a separate splitk_reduce_add_kernel launch instead)
+      static const bool fixup_env = [] {
+        const char* v = std::getenv("RK_GEMM_FIXUP");
+        return v ? std::atoi(v) != 0 : true;
+      }();
+      p.fixup = fixup_env && !p.streamk && p.split_flags && p.mt_group == 1 && p.pair == 1;
       launch_bn<EPI_PART>(e->stream, ta, tb, p, grid);
-      launch_pdl(splitk_reduce_add_kernel, dim3(std::min(p.rows_max, 8 * e->sm_count)), dim3(256), 0, e->stream, p,
-                 (int)p.splits, grid);
-      e->launches += 1;
+      if (!p.fixup) {
+        launch_pdl(splitk_reduce_add_kernel, dim3(std::min(p.rows_max, 8 * e->sm_count)), dim3(256), 0, e->stream, p,
+                   (int)p.splits, grid);
+        e->launches += 1;
+      }
       break;
+    }
     default: launch_bn<EPI_F32>(e->stream, ta, tb, p, grid); break;
   }
   e->launches += 1;

@@ -253,6 +253,11 @@ void mark_layers(cudaStream_t s, uint8_t* origin, int len, int layer_lo, int lay
 void zero_dev(cudaStream_t s, void* dst, size_t bytes);
 void zero_many(cudaStream_t s, const std::vector<std::pair<void*, size_t>>& bufs);  // one launch
 void copy_dev(cudaStream_t s, void* dst, const void* src, size_t bytes);
+// decode capture (graph-replayed steps; see Runner::capture_decode)
+void decode_step_begin(cudaStream_t s, const int* step, int src, const int* tokens, int* cur_tok, int* pos);
+void decode_step_end(cudaStream_t s, int* step, int n, int L, size_t row_bytes, const void* stage_k,
+                     const void* stage_v, void* k_pre, void* v, size_t hid_bytes, const void* stage_h, void* hidden,
+                     const int* next_tok, int* tokens);
 void zero_rows(cudaStream_t s, void* dst, size_t pitch, size_t width, size_t rows);
 void copy_i32(cudaStream_t s, int* dst, const int* src, int n);  // src may be mapped host memory
 void fill_doubles(cudaStream_t s, double* dst, int n, double v);
@@ -264,6 +269,22 @@ void argmax(cudaStream_t s, const float* x, int n, int* out, void* ws);
 void realign_graft(cudaStream_t s, const void* k_pre, const void* v_src, size_t elem, int L,
                    int n, int kv, int dh, const double2* rope, int base, void* ctx_k, void* ctx_v,
                    size_t ctx_layer_stride, int skip_lo, int skip_hi);
+// several segments (caches k_pre/v [L][n][kv] grafted at ctx rows base..) in one launch
+struct RealignJob {
+  const void* k_pre;
+  const void* v;
+  int n, base;
+};
+constexpr int kMaxRealignJobs = 8;
+struct RealignJobs {
+  const void* k_pre[kMaxRealignJobs];
+  const void* v[kMaxRealignJobs];
+  int n[kMaxRealignJobs], base[kMaxRealignJobs], blk0[kMaxRealignJobs + 1];
+  int count;
+};
+void realign_graft_batch(cudaStream_t s, const RealignJob* jobs, int count, size_t elem, int L, int kv, int dh,
+                         const double2* rope, void* ctx_k, void* ctx_v, size_t ctx_layer_stride, int skip_lo,
+                         int skip_hi);
 void score_deviation(cudaStream_t s, const void* ctx_v, const void* cache_v, const void* ctx_k,
                      const void* cache_kpre, size_t elem, int n, int kv, int heads, int dh,
                      const double2* rope, int base, double* s_dev, double* s_key);

@@ -328,57 +328,109 @@ __global__ void argmax_final_kernel(const float2* __restrict__ part, int parts, 
 // rounded (tensor.cpp:140-141); V is a bit copy. Layers [skip_lo, skip_hi]
 // are skipped (the band recompute overwrites them; relay_engine.cpp:261-264).
 // ---------------------------------------------------------------------------
-// Fast path for d_head 64/128: every index is a shift or mask except one
-// division per thread (the segment position, for the cos/sin row).
+// Fast path for d_head 64/128, staged through shared memory by TMA bulk
+// copies: a CTA owns P consecutive segment positions of one grafted layer.
+// One thread issues two cp.async.bulk loads (the P x kv block of K_pre and of
+// V, contiguous in the cache's [L][n][kv] layout) on an mbarrier while the CTA
+// stages the P rows of the double cos/sin table; V goes straight back out with
+// a bulk store into the context rows [base+p0, base+p0+P) (contiguous in the
+// context's [L][cap][kv] layout), K is rotated in shared memory (double, no
+// FMA) and follows with a second bulk store. Registers stay low, so many CTAs
+// per SM keep their bulk copies in flight.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(sm100::smem_u32(dst)), "l"(src), "r"(bytes), "r"(sm100::smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(sm100::smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit_wait_read() {
+  asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 template <typename T, int DH>
-__global__ void __launch_bounds__(256) realign_graft_dh_kernel(
-    const T* __restrict__ k_pre, const T* __restrict__ v_src, int n, int kv,
-    const double2* __restrict__ rope, int base, T* __restrict__ ctx_k, T* __restrict__ ctx_v,
-    size_t ctx_layer_stride, int skip_lo, int skip_hi) {
-  sm100::pdl_trigger();
-  sm100::pdl_wait();
-  constexpr int VEC = 16 / sizeof(T);
+__global__ void __launch_bounds__(128) realign_graft_dh_kernel(const __grid_constant__ k::RealignJobs J, int kv,
+                                                               const double2* __restrict__ rope, T* __restrict__ ctx_k,
+                                                               T* __restrict__ ctx_v, size_t ctx_layer_stride,
+                                                               int skip_lo, int skip_hi, int P) {
+  extern __shared__ __align__(128) uint8_t sm_raw[];
+  constexpr int VEC = 16 / sizeof(T), HALF = DH / 2, CH = DH / VEC;  // CH: 16-byte chunks per head slice
+  int u = 0;  // the segment (job) of this CTA
+  while (u + 1 < J.count && (int)blockIdx.x >= J.blk0[u + 1]) ++u;
+  const int n = J.n[u], base = J.base[u];
+  const int p0 = ((int)blockIdx.x - J.blk0[u]) * P, np = min(P, n - p0);
+  const uint32_t bytes = (uint32_t)np * kv * sizeof(T);
+  T* sk = reinterpret_cast<T*>(sm_raw);
+  T* sv = reinterpret_cast<T*>(sm_raw + (size_t)P * kv * sizeof(T));
+  double2* cs_sm = reinterpret_cast<double2*>(sm_raw + (size_t)2 * P * kv * sizeof(T));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(cs_sm + (size_t)P * HALF);
   int l = blockIdx.y;
   if (skip_hi >= skip_lo && l >= skip_lo) l += skip_hi - skip_lo + 1;
-  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const size_t e0 = t * VEC;  // element offset within the layer's [n x kv] block
-  if (e0 >= (size_t)n * kv) return;
-  const int p = (int)(e0 / (unsigned)kv);
-  const int pair0 = (int)(e0 & (DH - 1)) / 2;
-  const size_t src = (size_t)l * n * kv + e0;
-  const uint4 kraw = __ldcs(reinterpret_cast<const uint4*>(k_pre + src));
-  const uint4 vraw = __ldcs(reinterpret_cast<const uint4*>(v_src + src));
-  const size_t dst = (size_t)l * ctx_layer_stride + (size_t)base * kv + e0;
-  *reinterpret_cast<uint4*>(ctx_v + dst) = vraw;
-  const double2* cs = rope + (size_t)(base + p) * (DH / 2) + pair0;
-  double2 c_s[VEC / 2];
+  sm100::pdl_trigger();
+  if (threadIdx.x == 0) {
+    sm100::mbar_init(bar, 1);
+    sm100::fence_barrier_init();
+  }
+  // the table is host-built and constant: staged before the dependency wait
+  for (int i = threadIdx.x; i < np * HALF; i += blockDim.x) cs_sm[i] = rope[(size_t)(base + p0) * HALF + i];
+  __syncthreads();
+  sm100::pdl_wait();
+  const size_t src = ((size_t)l * n + p0) * kv;
+  const size_t dst = (size_t)l * ctx_layer_stride + (size_t)(base + p0) * kv;
+  if (threadIdx.x == 0) {
+    sm100::mbar_arrive_expect_tx(bar, 2 * bytes);
+    bulk_g2s(sk, static_cast<const T*>(J.k_pre[u]) + src, bytes, bar);
+    bulk_g2s(sv, static_cast<const T*>(J.v[u]) + src, bytes, bar);
+  }
+  sm100::mbar_wait(bar, 0);
+  if (threadIdx.x == 0) bulk_s2g(ctx_v + dst, sv, bytes);  // V: a bit copy
+  // thread = (position, 16-byte chunk of the head slice): its cos/sin pairs
+  // live in registers across every head
+  const int heads = kv / DH;
+  for (int it = threadIdx.x; it < np * CH; it += blockDim.x) {
+    const int pl = it / CH, ch = it - pl * CH;
+    double2 c_s[VEC / 2];
 #pragma unroll
-  for (int i = 0; i < VEC / 2; ++i) c_s[i] = cs[i];
-  const T* kin = reinterpret_cast<const T*>(&kraw);
-  uint4 kout_raw;
-  T* kout = reinterpret_cast<T*>(&kout_raw);
+    for (int i = 0; i < VEC / 2; ++i) c_s[i] = cs_sm[pl * HALF + ch * (VEC / 2) + i];
+    uint4* row = reinterpret_cast<uint4*>(sk + (size_t)pl * kv) + ch;
+    for (int h = 0; h < heads; ++h) {
+      uint4 raw = row[h * CH];
+      const T* kin = reinterpret_cast<const T*>(&raw);
+      uint4 out_raw;
+      T* kout = reinterpret_cast<T*>(&out_raw);
 #pragma unroll
-  for (int e = 0; e < VEC; e += 2) {
-    double x0, x1;
-    if constexpr (sizeof(T) == 4) {
-      x0 = (double)kin[e];
-      x1 = (double)kin[e + 1];
-    } else {
-      x0 = (double)__bfloat162float(kin[e]);
-      x1 = (double)__bfloat162float(kin[e + 1]);
-    }
-    const double2 c = c_s[e / 2];
-    const double r0 = __dsub_rn(__dmul_rn(c.x, x0), __dmul_rn(c.y, x1));
-    const double r1 = __dadd_rn(__dmul_rn(c.y, x0), __dmul_rn(c.x, x1));
-    if constexpr (sizeof(T) == 4) {
-      kout[e] = __double2float_rn(r0);
-      kout[e + 1] = __double2float_rn(r1);
-    } else {
-      kout[e] = __float2bfloat16_rn(__double2float_rn(r0));
-      kout[e + 1] = __float2bfloat16_rn(__double2float_rn(r1));
+      for (int e = 0; e < VEC; e += 2) {
+        double x0, x1;
+        if constexpr (sizeof(T) == 4) {
+          x0 = (double)kin[e];
+          x1 = (double)kin[e + 1];
+        } else {
+          x0 = (double)__bfloat162float(kin[e]);
+          x1 = (double)__bfloat162float(kin[e + 1]);
+        }
+        const double2 c = c_s[e / 2];
+        const double r0 = __dsub_rn(__dmul_rn(c.x, x0), __dmul_rn(c.y, x1));
+        const double r1 = __dadd_rn(__dmul_rn(c.y, x0), __dmul_rn(c.x, x1));
+        if constexpr (sizeof(T) == 4) {
+          kout[e] = __double2float_rn(r0);
+          kout[e + 1] = __double2float_rn(r1);
+        } else {
+          kout[e] = __float2bfloat16_rn(__double2float_rn(r0));
+          kout[e + 1] = __float2bfloat16_rn(__double2float_rn(r1));
+        }
+      }
+      row[h * CH] = out_raw;
     }
   }
-  *reinterpret_cast<uint4*>(ctx_k + dst) = kout_raw;
+  sm100::fence_proxy_async();  // generic-proxy smem writes -> visible to the bulk copy
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    bulk_s2g(ctx_k + dst, sk, bytes);
+    bulk_commit_wait_read();  // both stores complete (and have read shared memory) before the CTA exits
+  }
 }
 
 template <typename T>
@@ -544,14 +596,24 @@ __global__ void __launch_bounds__(256) score_dh_kernel(const T* __restrict__ ctx
                                                        int base, double* __restrict__ s_dev,
                                                        double* __restrict__ s_key) {
   sm100::pdl_trigger();
-  sm100::pdl_wait();
   constexpr int NV = DH * sizeof(T) / 16;  // 16-byte vectors per head slice
-  extern __shared__ double cosv[];          // [tokens of this CTA][2][heads]
+  extern __shared__ double cosv[];          // [tokens of this CTA][2][heads], then the cos/sin rows
   const int per_tok = 2 * heads;
   const int tok = blockDim.x / per_tok;
   const int t = threadIdx.x / per_tok, which = (threadIdx.x / heads) % 2, h = threadIdx.x % heads;
   const int j = blockIdx.x * tok + t;
   const int kv = heads * DH;
+  // the CTA's rows of the (constant, host-built) double cos/sin table, staged
+  // before the dependency wait: the K rotation reads them from shared memory
+  // instead of 32 dependent L2 loads inside its sequential loop
+  double2* cs_sm = reinterpret_cast<double2*>(cosv + (size_t)tok * per_tok);
+  {
+    const int nt = min(tok, n - (int)blockIdx.x * tok);
+    for (int i = threadIdx.x; i < nt * (DH / 2); i += blockDim.x)
+      cs_sm[i] = rope[(size_t)(base + blockIdx.x * tok) * (DH / 2) + i];
+  }
+  __syncthreads();
+  sm100::pdl_wait();
   if (t < tok && j < n) {
     const size_t off = (size_t)j * kv + (size_t)h * DH;
     const T* a = which == 0 ? ctx_v : ctx_k;
@@ -562,7 +624,7 @@ __global__ void __launch_bounds__(256) score_dh_kernel(const T* __restrict__ ctx
       x[i] = __ldcs(reinterpret_cast<const uint4*>(a + off) + i);
       y[i] = __ldcs(reinterpret_cast<const uint4*>(b + off) + i);
     }
-    const double2* cs = rope + (size_t)(base + j) * (DH / 2);
+    const double2* cs = cs_sm + t * (DH / 2);
     double dot = 0.0, na = 0.0, nb = 0.0;
     bool same = true;
 #pragma unroll  // fully: the slices stay in registers (compile-time indices)
@@ -828,35 +890,134 @@ __global__ void blend_score_kernel(const void* ctx_v, const void* cache_v, size_
   score[j] = __dsqrt_rn(acc);
 }
 
-// top_k_by_score (selector.cpp:90-105): rank by (score desc, index asc).
-__global__ void topk_flags_kernel(const double* score, int n, int count, uint32_t* flags) {
-  extern __shared__ double tile[];
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  const double sj = j < n ? score[j] : 0.0;
-  int rank = 0;
-  for (int t0 = 0; t0 < n; t0 += blockDim.x) {
-    if (t0 + (int)threadIdx.x < n) tile[threadIdx.x] = score[t0 + threadIdx.x];
+// top_k_by_score (selector.cpp:90-105): the `count` largest scores, ties by
+// ascending index (the reference's stable sort by score desc), as a radix
+// select in one CTA. Scores are non-negative doubles (L2 norms), so their bit
+// patterns order like the values: eight MSB-first passes of an 8-bit digit
+// histogram pin the exact key T of the count-th largest score and how many of
+// the keys equal to T are still needed; a final pass in index order flags
+// every key > T and the first `need` keys == T, then the block compaction
+// writes the ascending index list. O(8n) reads instead of O(n^2) rank counting.
+__global__ void __launch_bounds__(1024) topk_radix_kernel(const double* __restrict__ score, int n, int count,
+                                                          uint32_t* flags, int* sel_idx, uint32_t* sel_tags,
+                                                          int* info) {
+  __shared__ int hist[256];
+  __shared__ unsigned long long s_prefix;
+  __shared__ int s_need;
+  __shared__ int warp_sums[32];
+  __shared__ int running;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int k = count < n ? count : n;
+  if (threadIdx.x == 0) { s_prefix = 0ull; s_need = k; running = 0; }
+  __syncthreads();
+  unsigned long long mask = 0ull;
+  if (k > 0 && k < n) {
+    for (int shift = 56; shift >= 0; shift -= 8) {
+      for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+      __syncthreads();
+      const unsigned long long prefix = s_prefix;
+      for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        const unsigned long long key = (unsigned long long)__double_as_longlong(score[j]);
+        if ((key & mask) == prefix) atomicAdd(&hist[(int)((key >> shift) & 255ull)], 1);
+      }
+      __syncthreads();
+      if (wid == 0) {  // lane l covers digits 255-8l .. 248-8l, scanned from the top
+        int c[8], sum = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) { c[i] = hist[255 - 8 * lane - i]; sum += c[i]; }
+        int incl = sum;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int u = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += u;
+        }
+        const int want = s_need, excl = incl - sum;
+        if (excl < want && want <= incl) {
+          int cum = excl;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            if (cum + c[i] >= want) {
+              s_prefix = prefix | ((unsigned long long)(255 - 8 * lane - i) << shift);
+              s_need = want - cum;
+              break;
+            }
+            cum += c[i];
+          }
+        }
+      }
+      mask |= 255ull << shift;
+      __syncthreads();
+    }
+  }
+  const unsigned long long T = s_prefix;
+  const int need = s_need;  // keys == T to take, lowest indices first
+  for (int chunk = 0; chunk < n; chunk += blockDim.x) {
+    const int j = chunk + threadIdx.x;
+    const unsigned long long key = j < n ? (unsigned long long)__double_as_longlong(score[j]) : 0ull;
+    const bool eq = j < n && k > 0 && k < n && key == T;
+    const unsigned ballot = __ballot_sync(0xffffffffu, eq);
+    if (lane == 0) warp_sums[wid] = __popc(ballot);
     __syncthreads();
-    const int lim = min((int)blockDim.x, n - t0);
-    for (int i = 0; i < lim; ++i) {
-      const double si = tile[i];
-      const int ii = t0 + i;
-      rank += (si > sj) || (si == sj && ii < j);
+    if (wid == 0) {
+      int v = lane < nw ? warp_sums[lane] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
+      }
+      if (lane < nw) warp_sums[lane] = v;  // inclusive
     }
     __syncthreads();
+    const int rank_eq = running + (wid == 0 ? 0 : warp_sums[wid - 1]) + __popc(ballot & ((1u << lane) - 1u));
+    if (j < n) {
+      const bool take = k >= n || (k > 0 && (key > T || (eq && rank_eq < need)));
+      flags[j] = take ? RK_SEL_BLEND_TOPK : 0u;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) running += warp_sums[nw - 1];
+    __syncthreads();
   }
-  if (j < n) flags[j] = rank < count ? RK_SEL_BLEND_TOPK : 0u;
-}
-
-__global__ void __launch_bounds__(1024) compact_kernel(int n, const uint32_t* flags, int* sel_idx,
-                                                       uint32_t* sel_tags, int* info) {
+  __syncthreads();  // flags (global) written by this CTA are visible to it after the barrier
   block_compact(nullptr, n, flags, sel_idx, sel_tags, info);
 }
+
 
 __global__ void seq_mean_kernel(const float* x, int n, double* out) {
   double m = 0.0;
   for (int j = 0; j < n; ++j) m = __dadd_rn(m, (double)x[j]);
   *out = __ddiv_rn(m, (double)n);
+}
+
+// Decode-capture step bookkeeping: a graph-replayed decode step reads its
+// index from device memory (step_begin: the row's position and token), and
+// step_end moves the step's captured rows from fixed staging buffers to their
+// slots in the relay cache, stores the next token and advances the index.
+__global__ void decode_step_begin_kernel(const int* step, int src, const int* tokens, int* cur_tok, int* pos) {
+  sm100::pdl_trigger();
+  sm100::pdl_wait();
+  if (threadIdx.x == 0) {
+    const int t = *step;
+    pos[0] = src + t;
+    cur_tok[0] = tokens[t];
+  }
+}
+__global__ void decode_step_end_kernel(int* step, int n, int L, int row_words, const uint32_t* stage_k,
+                                       const uint32_t* stage_v, uint32_t* k_pre, uint32_t* v, int hid_words,
+                                       const uint32_t* stage_h, uint32_t* hidden, const int* next_tok, int* tokens) {
+  sm100::pdl_trigger();
+  sm100::pdl_wait();
+  const int t = *step;
+  for (int i = threadIdx.x; i < L * row_words; i += blockDim.x) {
+    const int l = i / row_words, w = i - l * row_words;
+    const size_t dst = ((size_t)l * n + t) * row_words + w;
+    k_pre[dst] = stage_k[i];
+    v[dst] = stage_v[i];
+  }
+  if (hidden)
+    for (int i = threadIdx.x; i < hid_words; i += blockDim.x) hidden[(size_t)t * hid_words + i] = stage_h[i];
+  __syncthreads();  // every thread has read *step
+  if (threadIdx.x == 0) {
+    if (next_tok) tokens[t + 1] = *next_tok;
+    *step = t + 1;
+  }
 }
 
 }  // namespace
@@ -968,6 +1129,17 @@ void zero_dev(cudaStream_t s, void* dst, size_t bytes) {
   const size_t blocks = std::min<size_t>(1184, (bytes / 16 + kThreads - 1) / kThreads + 1);
   launch_pdl(zero_bytes_kernel, dim3((unsigned)blocks), dim3(kThreads), 0, s, static_cast<uint8_t*>(dst), bytes);
 }
+void decode_step_begin(cudaStream_t s, const int* step, int src, const int* tokens, int* cur_tok, int* pos) {
+  launch_pdl(decode_step_begin_kernel, dim3(1), dim3(32), 0, s, step, src, tokens, cur_tok, pos);
+}
+void decode_step_end(cudaStream_t s, int* step, int n, int L, size_t row_bytes, const void* stage_k,
+                     const void* stage_v, void* k_pre, void* v, size_t hid_bytes, const void* stage_h, void* hidden,
+                     const int* next_tok, int* tokens) {
+  launch_pdl(decode_step_end_kernel, dim3(1), dim3(1024), 0, s, step, n, L, (int)(row_bytes / 4),
+             static_cast<const uint32_t*>(stage_k), static_cast<const uint32_t*>(stage_v), static_cast<uint32_t*>(k_pre),
+             static_cast<uint32_t*>(v), (int)(hid_bytes / 4), static_cast<const uint32_t*>(stage_h),
+             static_cast<uint32_t*>(hidden), next_tok, tokens);
+}
 void copy_dev(cudaStream_t s, void* dst, const void* src, size_t bytes) {
   if (!bytes) return;
   const size_t blocks = std::min<size_t>(1184, (bytes / 16 + kThreads - 1) / kThreads + 1);
@@ -998,27 +1170,72 @@ void argmax(cudaStream_t s, const float* x, int n, int* out, void* ws) {
 void realign_graft(cudaStream_t s, const void* k_pre, const void* v_src, size_t elem, int L, int n,
                    int kv, int dh, const double2* rope, int base, void* ctx_k, void* ctx_v,
                    size_t ctx_layer_stride, int skip_lo, int skip_hi) {
+  const RealignJob job{k_pre, v_src, n, base};
+  realign_graft_batch(s, &job, 1, elem, L, kv, dh, rope, ctx_k, ctx_v, ctx_layer_stride, skip_lo, skip_hi);
+}
+
+void realign_graft_batch(cudaStream_t s, const RealignJob* jobs, int count, size_t elem, int L, int kv, int dh,
+                         const double2* rope, void* ctx_k, void* ctx_v, size_t ctx_layer_stride, int skip_lo,
+                         int skip_hi) {
   const int skipped = skip_hi >= skip_lo ? skip_hi - skip_lo + 1 : 0;
   const int layers = L - skipped;
-  if (layers <= 0 || n <= 0) return;
-  const size_t vecs = (size_t)n * (kv * elem / 16);
-  dim3 grid((unsigned)((vecs + 255) / 256), (unsigned)layers);
+  if (layers <= 0 || count <= 0) return;
+  bool bulk_ok = (dh == 64 || dh == 128) && ((reinterpret_cast<uintptr_t>(ctx_k) | reinterpret_cast<uintptr_t>(ctx_v) |
+                                              (kv * elem)) & 15) == 0;
+  for (int u = 0; u < count; ++u)
+    bulk_ok = bulk_ok && ((reinterpret_cast<uintptr_t>(jobs[u].k_pre) | reinterpret_cast<uintptr_t>(jobs[u].v)) & 15) == 0;
+  if (!bulk_ok) {  // generic d_head / alignment: one thread per 16-byte vector
+    for (int u = 0; u < count; ++u) {
+      const int n = jobs[u].n;
+      if (n <= 0) continue;
+      const size_t vecs = (size_t)n * (kv * elem / 16);
+      dim3 grid((unsigned)((vecs + 255) / 256), (unsigned)layers);
+      if (elem == 4)
+        realign_graft_kernel<float><<<grid, 256, 0, s>>>(
+            (const float*)jobs[u].k_pre, (const float*)jobs[u].v, n, kv, dh, rope, jobs[u].base, (float*)ctx_k,
+            (float*)ctx_v, ctx_layer_stride, skip_lo, skip_hi);
+      else
+        realign_graft_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(
+            (const __nv_bfloat16*)jobs[u].k_pre, (const __nv_bfloat16*)jobs[u].v, n, kv, dh, rope, jobs[u].base,
+            (__nv_bfloat16*)ctx_k, (__nv_bfloat16*)ctx_v, ctx_layer_stride, skip_lo, skip_hi);
+    }
+    return;
+  }
+  // fast path: P positions (~16 KB of K and of V) of one segment and one
+  // grafted layer per CTA, every segment of the call in one launch
+  const int P = (int)std::max<size_t>(1, 16384 / (kv * elem));
+  const size_t smem = (size_t)2 * P * kv * elem + (size_t)P * (dh / 2) * 16 + 16;
+  for (int u0 = 0; u0 < count; u0 += kMaxRealignJobs) {
+    RealignJobs J{};
+    J.count = std::min(kMaxRealignJobs, count - u0);
+    int blocks = 0;
+    for (int i = 0; i < J.count; ++i) {
+      const RealignJob& jb = jobs[u0 + i];
+      J.k_pre[i] = jb.k_pre;
+      J.v[i] = jb.v;
+      J.n[i] = jb.n;
+      J.base[i] = jb.base;
+      J.blk0[i] = blocks;
+      blocks += (jb.n + P - 1) / P;
+    }
+    J.blk0[J.count] = blocks;
+    if (blocks == 0) continue;
 #define RK_REALIGN_DH(T, D)                                                                                  \
-  launch_pdl(realign_graft_dh_kernel<T, D>, dim3(grid), dim3(256), 0, s, (const T*)k_pre, (const T*)v_src, n, kv, rope, base,     \
-                                                     (T*)ctx_k, (T*)ctx_v, ctx_layer_stride, skip_lo, skip_hi)
-  if (elem == 4 && dh == 64) RK_REALIGN_DH(float, 64);
-  else if (elem == 4 && dh == 128) RK_REALIGN_DH(float, 128);
-  else if (elem == 2 && dh == 64) RK_REALIGN_DH(__nv_bfloat16, 64);
-  else if (elem == 2 && dh == 128) RK_REALIGN_DH(__nv_bfloat16, 128);
-  else if (elem == 4)
-    realign_graft_kernel<float><<<grid, 256, 0, s>>>(
-        (const float*)k_pre, (const float*)v_src, n, kv, dh, rope, base, (float*)ctx_k,
-        (float*)ctx_v, ctx_layer_stride, skip_lo, skip_hi);
-  else
-    realign_graft_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(
-        (const __nv_bfloat16*)k_pre, (const __nv_bfloat16*)v_src, n, kv, dh, rope, base,
-        (__nv_bfloat16*)ctx_k, (__nv_bfloat16*)ctx_v, ctx_layer_stride, skip_lo, skip_hi);
+  do {                                                                                                       \
+    static bool attr = false;                                                                                \
+    if (!attr) {                                                                                             \
+      RK_CUDA(cudaFuncSetAttribute(realign_graft_dh_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)); \
+      attr = true;                                                                                           \
+    }                                                                                                        \
+    launch_pdl(realign_graft_dh_kernel<T, D>, dim3(blocks, layers), dim3(128), smem, s, J, kv, rope, (T*)ctx_k, \
+               (T*)ctx_v, ctx_layer_stride, skip_lo, skip_hi, P);                                            \
+  } while (0)
+    if (elem == 4 && dh == 64) RK_REALIGN_DH(float, 64);
+    else if (elem == 4) RK_REALIGN_DH(float, 128);
+    else if (dh == 64) RK_REALIGN_DH(__nv_bfloat16, 64);
+    else RK_REALIGN_DH(__nv_bfloat16, 128);
 #undef RK_REALIGN_DH
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1091,11 +1308,18 @@ void score_deviation(cudaStream_t s, const void* ctx_v, const void* cache_v, con
   const bool aligned = ((reinterpret_cast<uintptr_t>(ctx_v) | reinterpret_cast<uintptr_t>(cache_v) |
                          reinterpret_cast<uintptr_t>(ctx_k) | reinterpret_cast<uintptr_t>(cache_kpre)) & 15) == 0;
   if (aligned && (dh == 64 || dh == 128) && 2 * heads <= 256) {
-    const int tok = 256 / (2 * heads);
-    const size_t smem = (size_t)tok * 2 * heads * sizeof(double);
+    // tokens per CTA: at most 256 threads, and few enough that the grid covers
+    // every SM about twice (the per-thread double loops are latency-bound)
+    static const int sms = [] {
+      int dev = 0, v = 148;
+      if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+      return v;
+    }();
+    const int tok = std::max(1, std::min(256 / (2 * heads), (n + 2 * sms - 1) / (2 * sms)));
+    const size_t smem = (size_t)tok * 2 * heads * sizeof(double) + (size_t)tok * (dh / 2) * 16;
     const int grid = (n + tok - 1) / tok;
 #define RK_SCORE_DH(T, D)                                                                                      \
-  launch_pdl(score_dh_kernel<T, D>, dim3(grid), dim3(256), smem, s, (const T*)ctx_v, (const T*)cache_v, (const T*)ctx_k,          \
+  launch_pdl(score_dh_kernel<T, D>, dim3(grid), dim3(tok * 2 * heads), smem, s, (const T*)ctx_v, (const T*)cache_v, (const T*)ctx_k,          \
                                                 (const T*)cache_kpre, n, heads, rope, base, s_dev, s_key)
     if (elem == 4 && dh == 64) RK_SCORE_DH(float, 64);
     else if (elem == 4) RK_SCORE_DH(float, 128);
@@ -1139,8 +1363,7 @@ void blend_scores(cudaStream_t s, const void* ctx_v, const void* cache_v, size_t
 }
 void select_topk(cudaStream_t s, const double* score, int n, int count, int* sel_idx,
                  uint32_t* sel_tags, int* info) {
-  topk_flags_kernel<<<blocks_for(n), kThreads, kThreads * sizeof(double), s>>>(score, n, count, sel_tags + n);
-  compact_kernel<<<1, 1024, 0, s>>>(n, sel_tags + n, sel_idx, sel_tags, info);
+  topk_radix_kernel<<<1, 1024, 0, s>>>(score, n, count, sel_tags + n, sel_idx, sel_tags, info);
 }
 void seq_mean(cudaStream_t s, const float* x, int n, double* out) {
   seq_mean_kernel<<<1, 1, 0, s>>>(x, n, out);

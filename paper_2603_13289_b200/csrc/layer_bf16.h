@@ -23,6 +23,9 @@ struct GemmArgs {
   int prefetch = 0;             // k-blocks of B (weights) prefetched into L2 ahead of the smem ring
   int mt_group = 1;             // 2/3: one CTA computes all m tiles of an N tile (M <= 128*mt_group)
   int pair = 1;                 // 2: CTA-pair kernel (256-row tiles, cta_group::2), chosen by gemm_bf16
+  // swap-AB (short static M): the weights are the MMA's M side (256 rows per
+  // CTA pair), the M tokens its N side in nc chunks of tc (<= 256) columns
+  int swap = 0, tc = 0, nc = 1;
   int* split_flags = nullptr;   // ordered split-K flags (EPI_ADD), zero-initialised
   // outputs
   float* out_f32 = nullptr;     // EPI_ADD / EPI_F32, row stride ld_out
@@ -55,6 +58,7 @@ struct GemmArgs {
   float norm_eps = 1e-5f;
   float* ws_part = nullptr;  // EPI_PART workspace [splits][rows_max][N], or stream-K [grid*2][128][bn]
   int streamk = 0;           // EPI_PART: stream-K work split (set by gemm_bf16)
+  int fixup = 0;             // EPI_PART: the last split of each row group reduces in the GEMM (no reduce kernel)
   // ensure_finite (tensor.cpp:58-64, after every matmul): any non-finite
   // product value sets status[0] (engine status flags, set by gemm_bf16);
   // the call then fails with RK_ERR_NONFINITE ("matmul: non-finite value")

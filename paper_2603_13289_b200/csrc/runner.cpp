@@ -755,28 +755,31 @@ void Runner::agent_fused(rk_context* ctx, const int32_t* prefix, uint64_t P, rk_
     wait_cache_meta(ups[u]);
   }
   const size_t el = w_->elem, kvd = w_->kv();
-  auto graft_layer = [&](uint64_t l) {  // realign + graft of layer l of every segment
+  uint64_t n_all = 0;
+  for (uint64_t u = 0; u < U; ++u) n_all += n[u];
+  auto graft_layer = [&](uint64_t l) {  // realign + graft of layer l of every segment, one launch
     if ((int)l >= skip_lo && (int)l <= skip_hi) return;
+    std::vector<k::RealignJob> jobs(U);
     for (uint64_t u = 0; u < U; ++u) {
       rk_cache* c = ups[u];
       wait_cache_layer(c, l);
-      ProfScope ps(e_, "realign_graft", 3.0 * kvd * n[u], 4.0 * n[u] * kvd * el);
-      k::realign_graft(st_, static_cast<char*>(c->k_pre.p) + l * n[u] * kvd * el,
-                       static_cast<char*>(c->v.p) + l * n[u] * kvd * el, el, 1, (int)n[u], (int)kvd, (int)s.d_head,
-                       rope, (int)base[u], static_cast<char*>(ctx->k.p) + l * layer_stride * el,
-                       static_cast<char*>(ctx->v.p) + l * layer_stride * el, layer_stride, 1, 0);
-      e_->launches += 1;
+      jobs[u] = {static_cast<char*>(c->k_pre.p) + l * n[u] * kvd * el, static_cast<char*>(c->v.p) + l * n[u] * kvd * el,
+                 (int)n[u], (int)base[u]};
     }
+    ProfScope ps(e_, "realign_graft", 3.0 * kvd * n_all, 4.0 * n_all * kvd * el);
+    k::realign_graft_batch(st_, jobs.data(), (int)U, el, 1, (int)kvd, (int)s.d_head, rope,
+                           static_cast<char*>(ctx->k.p) + l * layer_stride * el,
+                           static_cast<char*>(ctx->v.p) + l * layer_stride * el, layer_stride, 1, 0);
+    e_->launches += 1;
   };
-  if (!streamed) {
-    for (uint64_t u = 0; u < U; ++u) {  // one launch per segment over all grafted layers
-      rk_cache* c = ups[u];
-      const int grafted = (int)L - (skip_hi >= skip_lo ? skip_hi - skip_lo + 1 : 0);
-      ProfScope ps(e_, "realign_graft", 3.0 * kvd * n[u] * grafted, 4.0 * grafted * n[u] * kvd * el);
-      k::realign_graft(st_, c->k_pre.p, c->v.p, el, (int)L, (int)n[u], (int)kvd, (int)s.d_head, rope,
-                       (int)base[u], ctx->k.p, ctx->v.p, layer_stride, skip_lo, skip_hi);
-      e_->launches += 1;
-    }
+  if (!streamed) {  // one launch: every segment, every grafted layer
+    std::vector<k::RealignJob> jobs(U);
+    for (uint64_t u = 0; u < U; ++u) jobs[u] = {ups[u]->k_pre.p, ups[u]->v.p, (int)n[u], (int)base[u]};
+    const int grafted = (int)L - (skip_hi >= skip_lo ? skip_hi - skip_lo + 1 : 0);
+    ProfScope ps(e_, "realign_graft", 3.0 * kvd * n_all * grafted, 4.0 * grafted * n_all * kvd * el);
+    k::realign_graft_batch(st_, jobs.data(), (int)U, el, (int)L, (int)kvd, (int)s.d_head, rope, ctx->k.p, ctx->v.p,
+                           layer_stride, skip_lo, skip_hi);
+    e_->launches += 1;
   }
   const int ev_realign = event();
   // pass inputs: prefix / suffix embeddings, segment snapshots (or embeddings for BLEND)
@@ -978,6 +981,15 @@ rk_cache* Runner::capture_prefill(rk_context* ctx, const int32_t* tokens, uint64
   return c.release();
 }
 
+// Greedy decode with capture, one row per step (greedy_generate,
+// model.cpp:372-389, feeding RelayRecorder, relay_cache.cpp:68-127). A step's
+// ~10 kernels per layer are launch-bound on the host, so the step is recorded
+// once as a CUDA graph and replayed: its position, token and capture slots come
+// from a device step counter (decode_step_begin/end), the context is sized for
+// all n steps up front (keys past a step's position are masked by causality),
+// and the captured K_pre / V / snapshot rows go through fixed staging buffers.
+// Step 0 runs eagerly (it sizes every buffer the graph then reuses); the last
+// step, which needs no next-token logits, too. RK_DECODE_GRAPH=0: all eager.
 rk_cache* Runner::capture_decode(rk_context* ctx, const float* first_logits, uint64_t n, uint64_t snapshot,
                                  bool include_self) {
   const rk_model_spec& s = w_->s;
@@ -988,37 +1000,87 @@ rk_cache* Runner::capture_decode(rk_context* ctx, const float* first_logits, uin
   std::unique_ptr<rk_cache> c(new_cache(e_, w_, n, src, snapshot));
   ensure_rows(1);
   Scratch& S = *e_->scratch;
-  const size_t d = s.d_model, kv = w_->kv(), H = s.num_heads, V = s.vocab_size;
+  const size_t d = s.d_model, kv = w_->kv(), H = s.num_heads, V = s.vocab_size, L = s.num_layers, el = c->elem;
   if (first_logits) RK_CUDA(cudaMemcpyAsync(S.logits.p, first_logits, V * 4, cudaMemcpyHostToDevice, st_));
   DevBuf acc(n * 8), probs(H * n * 4);
+  const size_t row_bytes = kv * el;
+  DevBuf stage(2 * L * row_bytes + d * 4 + 64);  // [K_pre rows | V rows | snapshot row | step, token, next token]
+  char* sk = static_cast<char*>(stage.p);
+  char* sv = sk + L * row_bytes;
+  char* sh = sv + L * row_bytes;
+  int* ints = reinterpret_cast<int*>(sh + d * 4);
+  int *step = ints, *cur_tok = ints + 1, *next_tok = ints + 2;
   k::zero_dev(st_, acc.p, n * 8);
+  k::zero_dev(st_, ints, 16);
   int* tok = c->tokens.as<int>();
   // greedy_generate (model.cpp:372-389): next = argmax(prompt-end logits)
   k::argmax(st_, S.logits.as<float>(), (int)V, tok, S.argmax.as<char>() + 64);
-  e_->launches += 2;
-  for (uint64_t t = 0; t < n; ++t) {
-    const uint64_t pos = src + t;
-    ctx->resize(pos + 1);
-    k::embed(st_, S.hidden.as<float>(), w_->emb, w_->elem, tok + t, 1, (int)d, 0, nullptr);
-    k::iota_positions(st_, S.positions.as<int>(), 1, (int)pos);
+  e_->launches += 4;
+  ctx->resize(src + n);
+  auto one_step = [&](bool logits) {
+    k::decode_step_begin(st_, step, (int)src, tok, cur_tok, S.positions.as<int>());
+    k::embed(st_, S.hidden.as<float>(), w_->emb, w_->elem, cur_tok, 1, (int)d, 0, nullptr);
     e_->launches += 2;
     Rows rows{1, nullptr, S.positions.as<int>()};
     prepared_ = false;
-    for (uint64_t l = 0; l < s.num_layers; ++l) {
-      if (l == snapshot)
-        k::copy_dev(st_, c->hidden.as<float>() + t * d, S.hidden.p, d * 4);
-      cap_k_ = static_cast<float*>(static_cast<void*>(static_cast<char*>(c->k_pre.p) + (l * n + t) * kv * c->elem));
-      cap_v_ = static_cast<float*>(static_cast<void*>(static_cast<char*>(c->v.p) + (l * n + t) * kv * c->elem));
-      run_layer(ctx, (int)l, S.hidden.as<float>(), rows, true, (int)(pos + 1), probs.as<float>(), (int)src, (int)n);
+    for (uint64_t l = 0; l < L; ++l) {
+      if (l == snapshot) {
+        k::copy_dev(st_, sh, S.hidden.p, d * 4);
+        e_->launches += 1;
+      }
+      cap_k_ = reinterpret_cast<float*>(sk + l * row_bytes);
+      cap_v_ = reinterpret_cast<float*>(sv + l * row_bytes);
+      run_layer(ctx, (int)l, S.hidden.as<float>(), rows, true, (int)(src + n), probs.as<float>(), (int)src, (int)n);
       cap_k_ = cap_v_ = nullptr;
       k::influence_accum(st_, acc.as<double>(), probs.as<float>(), rows, (int)H, (int)src, (int)n, include_self);
       e_->launches += 1;
     }
-    if (t + 1 < n) {
+    if (logits) {
       last_row_logits(S.hidden.as<float>());
-      k::argmax(st_, S.logits.as<float>(), (int)V, tok + t + 1, S.argmax.as<char>() + 64);
+      k::argmax(st_, S.logits.as<float>(), (int)V, next_tok, S.argmax.as<char>() + 64);
       e_->launches += 2;
     }
+    k::decode_step_end(st_, step, (int)n, (int)L, row_bytes, sk, sv, c->k_pre.p, c->v.p, d * 4, sh, c->hidden.p,
+                       logits ? next_tok : nullptr, tok);
+    e_->launches += 1;
+  };
+  static const bool graph_env = [] {
+    const char* v = std::getenv("RK_DECODE_GRAPH");
+    return v ? std::atoi(v) != 0 : true;
+  }();
+  const bool graph = graph_env && n >= 4 && !(e_->prof && e_->prof->on);
+  if (!graph) {
+    for (uint64_t t = 0; t < n; ++t) one_step(t + 1 < n);
+  } else {
+    one_step(true);  // step 0, eagerly: every buffer and kernel attribute the graph reuses is set up here
+    const uint64_t l0 = e_->launches;
+    cudaGraph_t g = nullptr;
+    RK_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeRelaxed));
+    try {
+      one_step(true);
+    } catch (...) {
+      cudaGraph_t tmp = nullptr;
+      cudaStreamEndCapture(st_, &tmp);
+      if (tmp) cudaGraphDestroy(tmp);
+      throw;
+    }
+    RK_CUDA(cudaStreamEndCapture(st_, &g));
+    const uint64_t per_step = e_->launches - l0;
+    cudaGraphExec_t ge = nullptr;
+    const cudaError_t ierr = cudaGraphInstantiate(&ge, g, 0);
+    cudaGraphDestroy(g);
+    RK_CUDA(ierr);
+    for (uint64_t t = 1; t + 1 < n; ++t) {
+      const cudaError_t lerr = cudaGraphLaunch(ge, st_);
+      if (lerr != cudaSuccess) {
+        cudaGraphExecDestroy(ge);
+        RK_CUDA(lerr);
+      }
+    }
+    e_->launches += per_step * (n - 3);  // (the captured step's launches were counted once already)
+    one_step(false);                     // the last step: no next-token logits
+    RK_CUDA(cudaStreamSynchronize(st_));
+    RK_CUDA(cudaGraphExecDestroy(ge));
   }
   k::doubles_to_floats(st_, c->influence.as<float>(), acc.as<double>(), (int)n);
   k::seq_mean(st_, c->influence.as<float>(), (int)n, c->infl_mean.as<double>());

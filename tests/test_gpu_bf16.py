@@ -174,3 +174,53 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, RK_HOST_CONVERT="1"), capture_output=True,
                        text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_bf16_with_swap_ab_forced():
+    """The same end-to-end bars with every eligible GEMM (static M <= 512) on
+    the swap-AB CTA-pair kernel (RK_GEMM_SWAP=2): its QKV (RoPE + K/V scatter),
+    SiLU and split-K residual epilogues inside real layers. Subprocess."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, RK_GEMM_SWAP="2")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", __file__,
+                        "-k", "relay_prefill_vs_exact or agent_chain or nonunit"],
+                       env=env, capture_output=True, text=True, timeout=900, cwd=os.path.dirname(os.path.dirname(__file__)))
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
+
+
+def test_bf16_capture_decode_graph_equals_eager(engine, tmp_path):
+    """The graph-replayed decode capture (default) and the eager step-by-step
+    one (RK_DECODE_GRAPH=0, subprocess) launch the same kernels on the same
+    buffers: the captured caches are bit-identical."""
+    import os
+    import subprocess
+    import sys
+    spec = SPECS[1][1]
+
+    def run(path, env_extra):
+        code = f"""
+import sys, numpy as np
+sys.path.insert(0, {os.getcwd()!r})
+from paper_2603_13289_b200.abi import ModelSpec
+from paper_2603_13289_b200.engine import Engine
+from tests.scenarios import pattern_tokens
+from tests.test_gpu_bf16 import SPECS
+e = Engine(0)
+spec = SPECS[1][1]
+w = e.weights(spec, 21, "bf16")
+ctx = w.context()
+logits = ctx.prefill(pattern_tokens(33, spec.vocab_size, 3))
+h = ctx.capture_decode(logits, 40, 1).to_host()
+np.savez({path!r}, tok=h.segment_tokens, k=h.k_pre, v=h.v, hid=h.hidden_snapshot, inf=h.influence)
+"""
+        r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env_extra), capture_output=True,
+                           text=True, timeout=300)
+        assert r.returncode == 0, r.stdout + r.stderr
+        return np.load(path)
+
+    g = run(str(tmp_path / "graph.npz"), {})
+    e = run(str(tmp_path / "eager.npz"), {"RK_DECODE_GRAPH": "0"})
+    for f in ("tok", "k", "v", "hid", "inf"):
+        assert np.array_equal(np.asarray(g[f]).view(np.uint8), np.asarray(e[f]).view(np.uint8)), f

@@ -306,3 +306,102 @@ def test_gemv_residual(engine, shape):
     got = run_gemm(engine, A, B, H, M, 1)
     ref = H + bf16_round(A).astype(np.float64) @ bf16_round(B).astype(np.float64).T
     assert np.abs(got - ref).max() / np.abs(ref).max() < 2e-5
+
+
+SWAP_SHAPES = [(7, 256, 128), (200, 512, 512), (320, 16384, 2048), (333, 1024, 2048), (320, 2048, 8192),
+               (64, 3072, 2048), (256, 2048, 8192), (129, 256, 64), (512, 768, 1024), (2, 256, 256)]
+
+
+def test_gemm_swap_ab_pair():
+    """The swap-AB CTA-pair kernel (weights on the MMA's M side, tokens on N;
+    forced with RK_GEMM_SWAP=2 for every M <= 512, N % 256 == 0) on store and
+    residual (split-K partials) GEMMs, in a subprocess: fp64 agreement and
+    deterministic residuals."""
+    import os
+    import subprocess
+    import sys
+    code = f"""
+import numpy as np, sys
+sys.path.insert(0, {os.getcwd()!r})
+from paper_2603_13289_b200.engine import Engine
+from tests.test_gpu_kernels import run_gemm, bf16_round, SWAP_SHAPES
+e = Engine(0)
+for (M, N, K) in SWAP_SHAPES:
+    rng = np.random.default_rng(M + N + K)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    B = (rng.standard_normal((N, K)) / np.sqrt(K)).astype(np.float32)
+    H = rng.standard_normal((M, N)).astype(np.float32)
+    for epi, C0 in ((3, np.zeros((M, N))), (1, H)):
+        got = run_gemm(e, A, B, C0, M, epi)
+        ref = C0 + bf16_round(A).astype(np.float64) @ bf16_round(B).astype(np.float64).T
+        err = np.abs(got - ref).max() / np.abs(ref).max()
+        assert err < 2e-5, (M, N, K, epi, err)
+        if epi == 1:
+            again = run_gemm(e, A, B, C0, M, epi)
+            assert np.array_equal(got.view(np.uint32), again.view(np.uint32)), (M, N, K)
+print("ok")
+"""
+    env = dict(os.environ, RK_GEMM_SWAP="2", RK_GEMM_LOG="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+    assert "swap" in r.stderr, "the swap kernel was not selected"
+
+
+
+@pytest.mark.parametrize("case", ["random", "ties", "zeros", "big", "none", "all", "over"])
+def test_select_topk_radix(engine, case):
+    """BLEND's top_k_by_score (selector.cpp:90-105) as a device radix select:
+    the count largest scores, ties broken by ascending index (the reference's
+    stable sort), returned ascending -- including heavy ties and k = 0 / n / > n."""
+    rng = np.random.default_rng(13)
+    n, k = {"random": (1856, 371), "ties": (1000, 333), "zeros": (300, 100), "big": (40000, 2000),
+            "none": (500, 0), "all": (500, 500), "over": (64, 99)}[case]
+    s = rng.random(n) * 3.0
+    if case == "ties":
+        s = np.round(s * 4) / 4  # a dozen distinct values
+    if case == "zeros":
+        s[:] = 0.0
+    if case == "big":
+        s[::7] = s[3]  # a large tie class straddling the cut
+    order = sorted(range(n), key=lambda j: (-s[j], j))[:min(k, n)]
+    want = np.array(sorted(order), np.int32)
+    idx = np.zeros(n + 1, np.int32)
+    cnt = C.c_int32(-1)
+    _check(lib().rk_debug_select_topk(P(engine.ptr), np.ascontiguousarray(s).ctypes.data_as(C.POINTER(C.c_double)), n, k,
+                                      idx.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(cnt)))
+    assert cnt.value == len(want)
+    assert np.array_equal(idx[:cnt.value], want)
+
+
+@pytest.mark.parametrize("shape", [(1360, 2048, 8192), (320, 2048, 8192), (40, 512, 4096)])
+def test_gemm_split_k_fixup_equals_reduce_kernel(engine, shape, tmp_path):
+    """Split-K residual GEMMs reduce inside the GEMM (the last split of each
+    row group sums the partials in split order); the separate reduce kernel
+    (RK_GEMM_FIXUP=0, subprocess) sums the same partials in the same order, so
+    the residual rows are bit-identical; both match fp64."""
+    import os
+    import subprocess
+    import sys
+    M, N, K = shape
+    rng = np.random.default_rng(17)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    B = (rng.standard_normal((N, K)) / np.sqrt(K)).astype(np.float32)
+    H = rng.standard_normal((M, N)).astype(np.float32)
+    np.savez(tmp_path / "in.npz", A=A, B=B, H=H)
+    got = run_gemm(engine, A, B, H, M, 1)
+    code = f"""
+import numpy as np, sys
+sys.path.insert(0, {os.getcwd()!r})
+from paper_2603_13289_b200.engine import Engine
+from tests.test_gpu_kernels import run_gemm
+e = Engine(0)
+d = np.load({str(tmp_path / "in.npz")!r})
+np.save({str(tmp_path / "out.npy")!r}, run_gemm(e, d["A"], d["B"], d["H"], {M}, 1))
+"""
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, RK_GEMM_FIXUP="0"), capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    want = np.load(tmp_path / "out.npy")
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), "in-GEMM fixup != reduce kernel"
+    ref = H + bf16_round(A).astype(np.float64) @ bf16_round(B).astype(np.float64).T
+    assert np.abs(got - ref).max() / np.abs(ref).max() < 2e-5
