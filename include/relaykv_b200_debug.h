@@ -23,6 +23,10 @@ int rk_debug_attention_bf16(rk_engine* e, const float* q, const float* k, const 
 /* Device-resident timing (random operands, CUDA events): avg ms per call.
  * attention: band rows at positions T-M..T-1 over T context rows. */
 int rk_debug_bench_attention(rk_engine* e, int M, int T, int H, int Hkv, int dh, int iters, float* ms);
+/* Same, on a given row layout (positions, live count, row groups as in
+ * rk_debug_attention_bf16): the c2 sparse / prefix+suffix passes. */
+int rk_debug_bench_attention_rows(rk_engine* e, const int32_t* pos, int M, int live, int g1, int g2, int T, int H,
+                                  int Hkv, int dh, int iters, float* ms);
 /* clock64 timeline of one attention CTA (the last query tiles of head 0) on
  * the band case: out[3 roles][64 steps][8 events] (see attn_sm100.cu). */
 int rk_debug_trace_attention(rk_engine* e, int M, int T, int H, int Hkv, int dh, unsigned long long* out);

@@ -124,13 +124,14 @@ struct ACfg {
 __device__ __forceinline__ void tile_rows(const AttnArgs& a, int M, int tile, int& r0, int& r1) {
   const int g1 = min(a.g1, M), g2 = min(max(a.g2, g1), M);
   const int lo[3] = {0, g2, g1}, hi[3] = {g1, M, g2};  // prefix | segment rows | suffix
+  const int rq = a.rq;
 #pragma unroll
   for (int g = 0; g < 3; ++g) {
     const int b0 = lo[g], b1 = hi[g];
-    const int nt = (b1 - b0 + kQ - 1) / kQ;
+    const int nt = (b1 - b0 + rq - 1) / rq;
     if (tile < nt) {
-      r0 = b0 + tile * kQ;
-      r1 = min(r0 + kQ, b1);
+      r0 = b0 + tile * rq;
+      r1 = min(r0 + rq, b1);
       return;
     }
     tile -= nt;
@@ -152,6 +153,44 @@ __device__ __forceinline__ void exp2_pair(float x0, float x1, bool poly, float& 
     e0 = fast_exp2(x0);
     e1 = fast_exp2(x1);
   }
+}
+
+// Split-KV merge, streaming part: NP >= ts parts, Q float4 per thread per
+// round (NP * Q loads in flight); returns the non-finite check value.
+template <int DH, int NP>
+__device__ __forceinline__ float attn_merge_stream(const AttnArgs& a, const float4* src, const float* wsm, int rl, int ts,
+                                                   int r0, int r1, int rq, int G, int h0) {
+  constexpr int F4 = DH / 4;  // float4 per lane row
+  constexpr int Q = NP <= 4 ? 8 : (NP <= 8 ? 4 : 2);
+  float chk = 0.f;
+#pragma unroll 1
+  for (int i0 = 0; i0 < F4; i0 += Q) {
+    float4 v[NP][Q];
+#pragma unroll
+    for (int z = 0; z < NP; ++z)
+#pragma unroll
+      for (int q = 0; q < Q; ++q) v[z][q] = __ldcg(src + (size_t)min(z, ts - 1) * kQ * F4 + rl + 128 * (i0 + q));
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int f = rl + 128 * (i0 + q), ln = f / F4;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int z = 0; z < NP; ++z) {
+        const float wz = wsm[ln * 16 + z];
+        acc.x += wz * v[z][q].x;
+        acc.y += wz * v[z][q].y;
+        acc.z += wz * v[z][q].z;
+        acc.w += wz * v[z][q].w;
+      }
+      const int hl = ln / rq, row = r0 + ln % rq;
+      if (hl < G && row < r1) {
+        chk = fmaf(acc.x + acc.y + acc.z + acc.w, 0.f, chk);
+        *reinterpret_cast<uint2*>(a.out + (size_t)row * (a.H * DH) + (h0 + hl) * DH + 4 * (f % F4)) =
+            make_uint2(pack_bf16(acc.x, acc.y), pack_bf16(acc.z, acc.w));
+      }
+    }
+  }
+  return chk;
 }
 
 // POLY: bit c set -> the 4 pairs of 16-byte chunk c (of 8 per 64-key block)
@@ -191,9 +230,15 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
   __syncthreads();
   for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) atomicMax(s_kmax, a.pos[i]);
   __syncthreads();
-  const int h = blockIdx.y;
+  // GQA packing: the CTA's 128 TMEM lanes hold rq rows x `group` q heads of
+  // one kv head (lane = head_local * rq + row), so every K/V tile is staged
+  // once for all heads of its group and a tile spans only rq positions
+  // (tighter causal bound for gathered sparse rows). group 1: rq = 128 rows
+  // of head blockIdx.y.
+  const int G = a.group, rq = a.rq;
   const int part = blockIdx.x;  // split-KV part (fastest grid dim: a tile's parts dispatch together)
-  const int kvh = h / (a.H / a.Hkv);
+  const int kvh = G > 1 ? (int)blockIdx.y : (int)blockIdx.y / (a.H / a.Hkv);
+  const int h0 = G > 1 ? kvh * G : (int)blockIdx.y;  // first q head of the CTA
   // Adaptive split-KV: a tile whose key range exceeds tiles_per_split key
   // tiles is cut into ts = ceil(nk_tile / tiles_per_split) (<= gridDim.x)
   // equal parts; CTA z covers part z. Tiles that fit in one part write their
@@ -202,14 +247,15 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
   const int nk_tile = *s_kmax / KEYS + 1;
   const int ts = min((int)gridDim.x, (nk_tile + a.tiles_per_split - 1) / a.tiles_per_split);
   const int tps = (nk_tile + ts - 1) / ts;
+  const int ts_eff = (nk_tile + tps - 1) / tps;  // parts that own key tiles
   const int j0 = part * tps;
   const int nk = min(nk_tile - j0, tps);
-  const bool partial = ts > 1;
+  const bool partial = ts_eff > 1;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const bool trace_cta = TRACE && a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
-  if (a.row_splits && part == 0 && h == 0)
-    for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) a.row_splits[i] = ts;
-  if (part >= ts || nk <= 0) return;  // this tile has no such part
+  if (a.row_splits && part == 0 && blockIdx.y == 0)
+    for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) a.row_splits[i] = ts_eff;
+  if (part >= ts_eff || nk <= 0) return;  // this tile has no such part
 
   if (warp == 4 && lane == 0) {
     tma_prefetch(&tmQ);
@@ -250,9 +296,10 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
       }
     } else if (warp == 6) {
       if (elect_one()) {  // ------------------------------------- TMA Q, V
-        mbar_arrive_expect_tx(q_full, C::Q_TILE);
-        for (int b = 0; b < DB; ++b)
-          tma_load_2d(smem + C::OFF_Q + b * kQ * 128, &tmQ, q_full, h * DH + b * 64, r0);
+        mbar_arrive_expect_tx(q_full, G * rq * DH * 2);
+        for (int hl = 0; hl < G; ++hl)
+          for (int b = 0; b < DB; ++b)
+            tma_load_2d(smem + C::OFF_Q + b * kQ * 128 + hl * rq * 128, &tmQ, q_full, (h0 + hl) * DH + b * 64, r0);
         for (int j = 0; j < nk; ++j) {
           const int st = j & 1;
           mbar_wait(&v_empty[st], ((j >> 1) & 1) ^ 1);
@@ -315,9 +362,11 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
   } else {  // ------------------------------------------------ softmax warpgroup
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(C::REG_SM) : "memory");
     const bool tracing = trace_cta && warp == 0 && lane == 0;
-    const int rl = warp * 32 + lane;  // row within the tile == TMEM lane
-    const int row = r0 + rl;
-    const bool valid = row < r1;
+    const int rl = warp * 32 + lane;  // TMEM lane
+    const int hl = rl / rq;           // head within the group
+    const int h = h0 + hl;
+    const int row = r0 + rl % rq;
+    const bool valid = hl < G && row < r1;
     const int pos = valid ? a.pos[row] : *s_kmax;
     const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
     const uint32_t s_col = tmem + lane_base + C::S_COL;
@@ -420,7 +469,68 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
     }
     mbar_wait(o_done, (nk - 1) & 1);
     tc_fence_after();
-    if (partial) {
+    if (partial && a.tile_cnt) {
+      // in-kernel merge: partials in a tile-contiguous block [tile][part][lane][DH]
+      // (one 128 x DH fp32 block per part); the last part of this (tile, kv
+      // group) to finish merges them with coalesced streaming reads -- no
+      // combine launch
+      const size_t tid = (size_t)blockIdx.z * gridDim.y + blockIdx.y;
+      const size_t blk = (tid * gridDim.x + part) * kQ;  // lanes of this part's block
+#pragma unroll
+      for (int c = 0; c < DH; c += 32) {
+        uint32_t o[32];
+        tmem_ld32(o_col + c, o);
+        tmem_ld_wait();
+        float4* dst = reinterpret_cast<float4*>(a.ws_o + (blk + rl) * DH + c);
+#pragma unroll
+        for (int u = 0; u < 32; u += 4)
+          dst[u / 4] = make_float4(__uint_as_float(o[u]), __uint_as_float(o[u + 1]), __uint_as_float(o[u + 2]),
+                                   __uint_as_float(o[u + 3]));
+      }
+      reinterpret_cast<float2*>(a.ws_ml)[blk + rl] = make_float2(valid ? m_run : -INFINITY, l_run);
+      int* s_last = reinterpret_cast<int*>(bar + 15);
+      __threadfence();
+      named_bar_sync(1, 128);
+      int* cnt = a.tile_cnt + tid;
+      if (rl == 0) *s_last = atomicAdd(cnt, 1) == ts_eff - 1;
+      named_bar_sync(1, 128);
+      if (*s_last) {
+        __threadfence();
+        if (rl == 0) *cnt = 0;  // self-resetting for the next launch
+        // per-lane part weights 2^(m_z - m) / l into smem (the K ring is idle now)
+        float* wsm = reinterpret_cast<float*>(smem + C::OFF_K);  // [lane][16]
+        const size_t blk0 = tid * gridDim.x * kQ;
+        float mz[16], lz[16];
+#pragma unroll
+        for (int z = 0; z < 16; ++z) {
+          const float2 v = __ldcg(reinterpret_cast<const float2*>(a.ws_ml) + blk0 + (size_t)min(z, ts_eff - 1) * kQ + rl);
+          mz[z] = z < ts_eff ? v.x : -INFINITY;
+          lz[z] = v.y;
+        }
+        float m = -INFINITY;
+#pragma unroll
+        for (int z = 0; z < 16; ++z) m = fmaxf(m, mz[z]);
+        float lsum = 0.f;
+#pragma unroll
+        for (int z = 0; z < 16; ++z) {
+          mz[z] = mz[z] == -INFINITY ? 0.f : fast_exp2(mz[z] - m);
+          lsum += mz[z] * lz[z];
+        }
+        const float inv = 1.f / lsum;
+#pragma unroll
+        for (int z = 0; z < 16; ++z) wsm[rl * 16 + z] = mz[z] * inv;
+        named_bar_sync(1, 128);
+        // stream: thread t takes float4 f = t + 128 i of every part block
+        // (lane f / (DH/4), columns 4 (f % (DH/4)) ..), all parts' loads in
+        // flight at once (branch-free: part index clamped, weight 0 past ts)
+        const float4* src = reinterpret_cast<const float4*>(a.ws_o) + blk0 * (DH / 4);
+        float chk = 0.f;
+        if (ts_eff <= 4) chk = attn_merge_stream<DH, 4>(a, src, wsm, rl, ts_eff, r0, r1, rq, G, h0);
+        else if (ts_eff <= 8) chk = attn_merge_stream<DH, 8>(a, src, wsm, rl, ts_eff, r0, r1, rq, G, h0);
+        else chk = attn_merge_stream<DH, 16>(a, src, wsm, rl, ts_eff, r0, r1, rq, G, h0);
+        if (chk != chk && a.status) *reinterpret_cast<volatile int*>(a.status) = 1;
+      }
+    } else if (partial) {
       const size_t pr = ((size_t)part * a.rows_max + row) * a.H + h;
 #pragma unroll
       for (int c = 0; c < DH; c += 32) {
@@ -561,8 +671,8 @@ __global__ void attn_combine_kernel(const AttnArgs a) {
 
 // Upper bound on query tiles of a launch (row groups split at their bounds).
 int max_tiles(const AttnArgs& a) {
-  const int M = a.rows_max, g1 = std::min(a.g1, M), g2 = std::min(std::max(a.g2, g1), M);
-  return (g1 + kQ - 1) / kQ + (g2 - g1 + kQ - 1) / kQ + (M - g2 + kQ - 1) / kQ;
+  const int M = a.rows_max, g1 = std::min(a.g1, M), g2 = std::min(std::max(a.g2, g1), M), rq = a.rq;
+  return (g1 + rq - 1) / rq + (g2 - g1 + rq - 1) / rq + (M - g2 + rq - 1) / rq;
 }
 
 template <int DH>
@@ -586,7 +696,7 @@ void launch_attn(rk_engine* e, const CUtensorMap& tq, const CUtensorMap& tk, con
                                  ACfg<DH>::SMEM));
     attr = true;
   }
-  dim3 grid(a.splits, a.H, max_tiles(a));
+  dim3 grid(a.splits, a.group > 1 ? a.Hkv : a.H, max_tiles(a));
   auto go = [&](auto kern) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
@@ -605,7 +715,7 @@ void launch_attn(rk_engine* e, const CUtensorMap& tq, const CUtensorMap& tk, con
   else if (poly == 0x92) go(attn_kernel<DH, false, 0x92>);
   else if (poly == 0) go(attn_kernel<DH, false, 0x00>);
   else go(attn_kernel<DH, false>);
-  if (a.splits > 1) {
+  if (a.splits > 1 && !a.tile_cnt) {
     const int warps = a.rows_max * a.H;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(std::min((warps + 7) / 8, 4 * e->sm_count));
@@ -628,6 +738,20 @@ void attention_bf16(rk_engine* e, const AttnArgs& a_in, const __nv_bfloat16* ctx
   if (a_in.rows_max <= 0) return;
   AttnArgs a = a_in;
   if (!a.status) a.status = e->status.as<int>();
+
+  // GQA packing (RK_ATTN_PACK=0: off): G = H / H_kv q heads share a CTA, rq =
+  // the largest power of two rows with G * rq <= 128 (>= 8, so G <= 16)
+  static const bool pack_env = [] {
+    const char* v = std::getenv("RK_ATTN_PACK");
+    return v ? std::atoi(v) != 0 : true;
+  }();
+  a.group = 1;
+  a.rq = kQ;
+  if (pack_env && a.Hkv > 0 && a.H % a.Hkv == 0 && a.H / a.Hkv > 1 && a.H / a.Hkv <= 16) {
+    a.group = a.H / a.Hkv;
+    a.rq = 8;
+    while (a.rq * 2 * a.group <= kQ) a.rq *= 2;
+  }
   // split-KV when the query tiles alone cannot fill the SMs (sparse passes:
   // plan for ~1/3 of rows_max live). A split covers >= 2 key tiles; CTAs
   // whose rows end before their split exit at once, so long tiles (suffix,
@@ -635,7 +759,7 @@ void attention_bf16(rk_engine* e, const AttnArgs& a_in, const __nv_bfloat16* ctx
   AttnArgs hint = a;
   if (a.rows_dev) hint.rows_max = std::max(a.g2 + 1, a.rows_max / 3);
   const int ctas_per_sm = a.dh == 64 ? ACfg<64>::CTAS : ACfg<128>::CTAS;
-  const int base = max_tiles(hint) * a.H;          // CTAs without splitting
+  const int base = max_tiles(hint) * (a.group > 1 ? a.Hkv : a.H);  // CTAs without splitting
   const int slots = ctas_per_sm * e->sm_count;     // CTAs resident at once
   const int keys = a.dh == 64 ? ACfg<64>::KEYS : ACfg<128>::KEYS;
   const int nk_max = (ctx_rows + keys - 1) / keys;
@@ -669,15 +793,30 @@ void attention_bf16(rk_engine* e, const AttnArgs& a_in, const __nv_bfloat16* ctx
   }
   if (a.splits > 1) {
     Scratch& S = *e->scratch;
-    const size_t per = (size_t)a.splits * a.rows_max * a.H;
+    // partials: in-kernel merge (default) -> per (tile, kv group, part) one
+    // 128-lane block; RK_ATTN_MERGE=0 -> row-major [part][row][head] for the
+    // separate attn_combine_kernel
+    static const bool merge_env = [] {
+      const char* v = std::getenv("RK_ATTN_MERGE");
+      return v ? std::atoi(v) != 0 : true;
+    }();
+    const size_t tiles = (size_t)max_tiles(a) * (a.group > 1 ? a.Hkv : a.H);
+    const size_t per = merge_env ? tiles * a.splits * kQ : (size_t)a.splits * a.rows_max * a.H;
     S.attn_ws.ensure(per * (a.dh + 2) * 4 + (size_t)a.rows_max * 4 + 256);
     a.ws_o = S.attn_ws.as<float>();
     a.ws_ml = a.ws_o + per * a.dh;
     a.row_splits = reinterpret_cast<int*>(a.ws_ml + per * 2);
+    if (merge_env) {  // per-(tile, kv group) arrival counters, zeroed once, self-resetting
+      if (S.attn_cnt.bytes < tiles * 4) {
+        S.attn_cnt.ensure(tiles * 4);
+        RK_CUDA(cudaMemsetAsync(S.attn_cnt.p, 0, S.attn_cnt.bytes, e->stream));
+      }
+      a.tile_cnt = S.attn_cnt.as<int>();
+    }
   }
   const int q = a.H * a.dh, kv = a.Hkv * a.dh;
   CUtensorMap tq, tk, tv;
-  make_tmap_bf16(&tq, a.q, (uint64_t)a.rows_max, (uint64_t)q, kQ, (uint64_t)q);
+  make_tmap_bf16(&tq, a.q, (uint64_t)a.rows_max, (uint64_t)q, (uint32_t)a.rq, (uint64_t)q);
   make_tmap_bf16(&tk, ctx_k, (uint64_t)ctx_rows, (uint64_t)kv, keys, (uint64_t)kv);
   make_tmap_bf16(&tv, ctx_v, (uint64_t)ctx_rows, (uint64_t)kv, keys, (uint64_t)kv);
   ProfScope ps(e, (e->prof && e->prof->on)

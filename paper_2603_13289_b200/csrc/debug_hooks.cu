@@ -133,6 +133,48 @@ int rk_debug_bench_attention(rk_engine* e, int M, int T, int H, int Hkv, int dh,
   });
 }
 
+int rk_debug_bench_attention_rows(rk_engine* e, const int32_t* pos, int M, int live, int g1, int g2, int T, int H,
+                                  int Hkv, int dh, int iters, float* ms) {
+  return guard([&] {
+    cudaStream_t st = e->stream;
+    const size_t nq = (size_t)M * H * dh, nk = (size_t)T * Hkv * dh;
+    DevBuf f((nq > nk ? nq : nk) * 4), qb(nq * 2), kb(nk * 2), vb(nk * 2), o(nq * 2), p(M * 4 + 16);
+    k::init_uniform(st, f.as<float>(), nq, 11, 1.0f);
+    k::f32_to_bf16(st, qb.as<__nv_bfloat16>(), f.as<float>(), nq);
+    k::init_uniform(st, f.as<float>(), nk, 12, 1.0f);
+    k::f32_to_bf16(st, kb.as<__nv_bfloat16>(), f.as<float>(), nk);
+    k::init_uniform(st, f.as<float>(), nk, 13, 1.0f);
+    k::f32_to_bf16(st, vb.as<__nv_bfloat16>(), f.as<float>(), nk);
+    RK_CUDA(cudaMemcpy(p.p, pos, M * 4, cudaMemcpyHostToDevice));
+    RK_CUDA(cudaMemcpy(p.as<int>() + M, &live, 4, cudaMemcpyHostToDevice));
+    AttnArgs a;
+    a.q = qb.as<__nv_bfloat16>();
+    a.out = o.as<__nv_bfloat16>();
+    a.pos = p.as<int>();
+    a.rows_max = M;
+    a.rows_dev = live < M ? p.as<int>() + M : nullptr;
+    a.g1 = g1;
+    a.g2 = g2;
+    a.H = H;
+    a.Hkv = Hkv;
+    a.dh = dh;
+    a.scale_log2 = 1.4426950408889634f / std::sqrt((float)dh);
+    attention_bf16(e, a, kb.as<__nv_bfloat16>(), vb.as<__nv_bfloat16>(), T);
+    cudaEvent_t e0, e1;
+    RK_CUDA(cudaEventCreate(&e0));
+    RK_CUDA(cudaEventCreate(&e1));
+    RK_CUDA(cudaEventRecord(e0, st));
+    for (int i = 0; i < iters; ++i) attention_bf16(e, a, kb.as<__nv_bfloat16>(), vb.as<__nv_bfloat16>(), T);
+    RK_CUDA(cudaEventRecord(e1, st));
+    RK_CUDA(cudaEventSynchronize(e1));
+    RK_CUDA(cudaEventElapsedTime(ms, e0, e1));
+    *ms /= iters;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    RK_CUDA(cudaGetLastError());
+  });
+}
+
 int rk_debug_trace_attention(rk_engine* e, int M, int T, int H, int Hkv, int dh, unsigned long long* out) {
   return guard([&] {
     cudaStream_t st = e->stream;

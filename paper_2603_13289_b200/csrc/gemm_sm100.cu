@@ -1765,11 +1765,13 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
     case EPI_ADD: launch_bn<EPI_ADD>(e->stream, ta, tb, p, grid); break;
     case EPI_SILU: launch_bn<EPI_SILU>(e->stream, ta, tb, p, grid); break;
     case EPI_PART: {
-      // split-K reduced inside the GEMM by the last split of each row group
-      // (RK_GEMM_FIXUP=0: a separate splitk_reduce_add_kernel launch instead)
+      // partials reduced by splitk_reduce_add_kernel (RK_GEMM_FIXUP=1: by the
+      // last split of each row group inside the GEMM -- measured slower, r02k:
+      // c2 sparse W_down 113 us vs 66 us with the reduce launch, because the
+      // fixup warps hold up the next tile's epilogue)
       static const bool fixup_env = [] {
         const char* v = std::getenv("RK_GEMM_FIXUP");
-        return v ? std::atoi(v) != 0 : true;
+        return v ? std::atoi(v) != 0 : false;
       }();
       p.fixup = fixup_env && !p.streamk && p.split_flags && p.mt_group == 1 && p.pair == 1;
       launch_bn<EPI_PART>(e->stream, ta, tb, p, grid);

@@ -201,7 +201,7 @@ namespace rk {
 struct Scratch {
   DevBuf hidden, sub_hidden, normed, qkv, attn, act, logits, tokens, positions, sub_positions;
   DevBuf s_dev, s_key, sel_idx, sel_tags, sel_info, depth, argmax, seg_hidden_out;
-  DevBuf gemm_tmp, attn_ws, gemm_ws;
+  DevBuf gemm_tmp, attn_ws, attn_cnt, gemm_ws;
   DevBuf norm_inv, norm_part, norm_cnt;  // fused RMSNorm (layer_bf16.cu)
 };
 

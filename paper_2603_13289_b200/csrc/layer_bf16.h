@@ -92,10 +92,12 @@ struct AttnArgs {
   float* ws_o = nullptr;
   float* ws_ml = nullptr;
   int* row_splits = nullptr;  // [rows_max] parts of each row's tile (1 = output written directly)
+  int* tile_cnt = nullptr;    // [tiles x grid.y] zeroed, self-resetting: in-kernel split-KV merge
   // debug: clock64 timeline of the last CTA of head 0 ([role 0..2][step < 64][event < 8];
   // roles: softmax group 0, group 1, MMA issuer)
   unsigned long long* trace = nullptr;
   int pingpong = 1;  // set by attention_bf16
+  int group = 1, rq = 128;  // GQA packing (set by attention_bf16): q heads per CTA, rows per head
   int* status = nullptr;  // non-finite output flag (engine status[0], set by attention_bf16)
 };
 // ctx_k / ctx_v: the layer's [ctx_rows x kv] bf16 context rows.

@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT; OUT=gpurun_out/r02p; mkdir -p $OUT
+timeout 900 python -m pytest tests/test_gpu_kernels.py -x -q -k "attention" > $OUT/pytest_attn.log 2>&1; echo "exit $?" >> $OUT/pytest_attn.log
+for cfg in "X=0" "RK_ATTN_MERGE=0" "RK_ATTN_SPLITWAVES=100" "RK_ATTN_MINPART=2" "RK_ATTN_MINPART=8"; do
+  echo "== $cfg" >> $OUT/mb.txt
+  env $(echo $cfg | tr ',' ' ') timeout 120 python tools/microbench.py rows >> $OUT/mb.txt 2>&1
+done
