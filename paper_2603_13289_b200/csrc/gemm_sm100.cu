@@ -32,6 +32,9 @@
 //   EPI_SILU  interleaved (gate, up) columns -> bf16 silu(g)*u (model.cpp:226)
 //   EPI_F32   plain fp32 store (logits)
 #include <cuda.h>
+#include <cstdio>
+#include <cstring>
+#include <vector>
 
 #include <algorithm>
 #include <cstdio>
@@ -151,7 +154,7 @@ __device__ __forceinline__ bool get_work(const Units& U, bool streamk, int k, Wo
 
 template <int EPI>
 __device__ __forceinline__ void epilogue_chunk(const GemmArgs& p, int row, int col, const uint32_t (&r)[32],
-                                               float rs, int split = 0) {
+                                               float rs, int split = 0, const float2* csv = nullptr, int pos_in = -1) {
   float v[32];
   float chk = 0.f;
 #pragma unroll
@@ -189,7 +192,7 @@ __device__ __forceinline__ void epilogue_chunk(const GemmArgs& p, int row, int c
     dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
   } else {  // EPI_QKV
     const int q = p.q, kv = p.kv, dh = p.dh;
-    const int pos = p.pos[row];
+    const int pos = pos_in >= 0 ? pos_in : p.pos[row];
     const int region = col < q ? 0 : (col < q + kv ? 1 : 2);
     if (region == 2) {
       const int c = col - q - kv;
@@ -221,7 +224,7 @@ __device__ __forceinline__ void epilogue_chunk(const GemmArgs& p, int row, int c
     uint32_t pk[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-      const float2 t = cs[j];
+      const float2 t = csv ? csv[j] : cs[j];
       const float x0 = v[2 * j], x1 = v[2 * j + 1];
       pk[j] = pack_bf16(x0 * t.x - x1 * t.y, x0 * t.y + x1 * t.x);
     }
@@ -693,12 +696,36 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&tfull[acc], use & 1);
         tc_fence_after();
         const float rs = (p.row_scale && row < M) ? p.row_scale[row] : 1.0f;
+        if constexpr (EPI == EPI_QKV) {
+          // RoPE {cos, sin} of this row's position for the next chunk are
+          // loaded while the current chunk computes (one exposed L2 latency
+          // per tile instead of one per 32 columns)
+          const int pos = row < M ? p.pos[row] : 0;
+          const float2* csrow = p.rope + (size_t)pos * (p.dh / 2);
+          float2 cur[16], nxt[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) cur[j] = csrow[((nt * BN) % p.dh) / 2 + j];
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
-          uint32_t r[32];
-          tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + acol + c, r);
-          tmem_ld_wait();
-          if (row < M) epilogue_chunk<EPI>(p, row, nt * BN + c, r, rs, s);
+          for (int c = 0; c < BN; c += 32) {
+            if (c + 32 < BN) {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) nxt[j] = csrow[((nt * BN + c + 32) % p.dh) / 2 + j];
+            }
+            uint32_t r[32];
+            tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + acol + c, r);
+            tmem_ld_wait();
+            if (row < M) epilogue_chunk<EPI>(p, row, nt * BN + c, r, rs, s, cur, pos);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) cur[j] = nxt[j];
+          }
+        } else {
+#pragma unroll 1
+          for (int c = 0; c < BN; c += 32) {
+            uint32_t r[32];
+            tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + acol + c, r);
+            tmem_ld_wait();
+            if (row < M) epilogue_chunk<EPI>(p, row, nt * BN + c, r, rs, s);
+          }
         }
       }
       if (flag) {
@@ -1484,7 +1511,11 @@ static double choose_config(GemmArgs& p, int sm_count, int rows_hint) {
   // (RK_GEMM_TKB_FLOOR_NS=450 floors it at a k-block round trip -- closer for
   // narrow tiles, but the extra split-K it then picks measured slower on c2.)
   static const double t_floor = env("RK_GEMM_TKB_FLOOR_NS", 0) * 1e-3;
-  auto t_kb = [](int a_kb, int b_kb) { return std::max(t_floor, 0.0096 * (a_kb + b_kb)); };
+  // (r02s recalibration on the c2 step: 1-CTA 128x256 ~0.50 us per k-block,
+  // CTA pair 256x256 ~0.39 us -- the pair also wins the dynamic-row sparse
+  // gate/up and W_down GEMMs, where the old 0.46 / 0.425 picked 1-CTA tiles)
+  auto t_kb = [](int a_kb, int b_kb) { return std::max(t_floor, 0.0104 * (a_kb + b_kb)); };
+  constexpr double kPairKb = 0.39;  // us per k-block of a 256 x 256 pair unit
 
   // 1-CTA (or pair) tiles, BN by the fill rule
   const int pslots = pair_env ? pair_slots(sm_count) : 0;
@@ -1496,19 +1527,33 @@ static double choose_config(GemmArgs& p, int sm_count, int rows_hint) {
           best = std::min(best, ceil_div((long long)ceil_div(rows_hint, tm) * (p.N / cand), slots_) * (cand / 128));
       return best;
     };
-    const double single = rounds(kBM, sm_count) * 0.46, pair = rounds(2 * kBM, pslots) * 0.425;
+    const double single = rounds(kBM, sm_count) * t_kb(16, 32), pair = rounds(2 * kBM, pslots) * kPairKb;
     if (pair_env == 2 || (rows_hint >= 640 && pair <= single)) p.pair = 2;
   }
   const int slots = p.pair == 2 ? pslots : sm_count;
   const int num_m = ceil_div(rows_hint, kBM * p.pair);
   int bn = 64;
-  for (int cand : {256, 128}) {
-    if (p.N % cand == 0 && num_m * (p.N / cand) >= slots) { bn = cand; break; }
+  if (p.pair == 2) {
+    // pair tiles: the BN with the fewest unit-rounds x width; on a tie the
+    // wider tile (fewer, longer units), except the QKV epilogue (RoPE + K/V
+    // scatter) of the sparse passes, whose exposed last epilogue favours two
+    // narrower rounds (measured r02s: sparse W_o 256 wins, sparse QKV 128)
+    double bc = 1e30;
+    for (int cand : {256, 128, 64}) {
+      if (p.N % cand) continue;
+      const double c = (double)ceil_div((long long)num_m * (p.N / cand), slots) *
+                       std::max(kPairKb * cand / 256.0, t_kb(16, cand / 16));
+      if (c < bc || (c == bc && p.epi == EPI_QKV && p.rows_dev && cand >= 128)) { bc = c; bn = cand; }
+    }
+  } else {
+    for (int cand : {256, 128}) {
+      if (p.N % cand == 0 && num_m * (p.N / cand) >= slots) { bn = cand; break; }
+    }
   }
   if (p.N % bn) raise(RK_ERR_INVALID_ARGUMENT, "bf16 GEMM needs N % 64 == 0");
   p.bn = bn;
   double best = (double)ceil_div((long long)num_m * (p.N / bn), slots) * kb *
-                (p.pair == 2 ? std::max(0.42 * bn / 256.0, t_floor * 0.93) : t_kb(16, bn / 8));
+                (p.pair == 2 ? std::max(kPairKb * bn / 256.0, t_kb(16, bn / 16)) : t_kb(16, bn / 8));
 
   const bool residual_split = p.epi == EPI_ADD && p.split_flags;
   auto part_cost = [&](int s) { return s > 1 ? 3.0 + 2.0 * s * (double)rows_hint * p.N * 4 / 8e6 : 0.0; };
@@ -1663,9 +1708,47 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
     return;
   }
   {
+    const int epi0 = p.epi;
     GemmArgs alt = p;
     const double other = choose_config(alt, e->sm_count, rows_hint > 0 ? rows_hint : p.rows_max);
     if (!choose_swap(p, e->sm_count, other)) p = alt;
+    // sweep hook: RK_GEMM_OVERRIDE="M[d]:N:K=bn/pair/splits;..." (d: live rows
+    // on the device) forces one shape's tile config (tools/gemm_override_sweep.py)
+    struct Ovr {
+      int M, dyn, N, K, bn, pair, splits;
+    };
+    static const std::vector<Ovr> ovr = [] {
+      std::vector<Ovr> v;
+      const char* s = std::getenv("RK_GEMM_OVERRIDE");
+      while (s && *s) {
+        Ovr o{};
+        char d = 0;
+        int n = 0;
+        if (std::sscanf(s, "%d%c", &o.M, &d) == 2 && d == 'd') {
+          o.dyn = 1;
+          std::sscanf(s, "%*dd:%d:%d=%d/%d/%d%n", &o.N, &o.K, &o.bn, &o.pair, &o.splits, &n);
+        } else {
+          std::sscanf(s, "%*d:%d:%d=%d/%d/%d%n", &o.N, &o.K, &o.bn, &o.pair, &o.splits, &n);
+        }
+        if (n > 0) v.push_back(o);
+        s = std::strchr(s, ';');
+        if (s) ++s;
+      }
+      return v;
+    }();
+    for (const Ovr& o : ovr) {
+      if (o.M == p.rows_max && o.dyn == (p.rows_dev != nullptr) && o.N == p.N && o.K == p.K) {
+        p = alt;
+        p.swap = 0;
+        p.bn = o.bn;
+        p.pair = o.pair;
+        p.splits = (epi0 == EPI_ADD || epi0 == EPI_PART) ? o.splits : 1;
+        p.mt_group = 1;
+        p.csk = 0;
+        p.streamk = 0;
+        p.epi = (o.splits > 1 && (epi0 == EPI_ADD || epi0 == EPI_PART)) ? EPI_PART : epi0;
+      }
+    }
   }
   static const bool log = std::getenv("RK_GEMM_LOG") != nullptr;
   if (p.swap) {
