@@ -429,11 +429,58 @@ def exact_leg(eng, w, timed):
         "segments": segs,
     }
     n_tokens = prompt_tokens()
+    eng.profile(True)  # where the exact step's time goes (CUDA events per launch)
+    run(sx["ctx"], sx["caches"])
+    kst = eng.profile_read()
+    eng.profile(False)
+    split = {}
+    for k in kst:
+        key = "attention" if k["name"].startswith("attn_exact") else (
+            "gemm" if k["name"].startswith("gemm_exact") else k["name"])
+        split[key] = split.get(key, 0.0) + k["total_ms"]
     exact = {"ttft_ms": round(dev_ms / 2, 3), "tokens_per_s": round(n_tokens / (dev_ms / 2 / 1e3), 1),
+             "ms_by_kind": {k: round(v, 3) for k, v in split.items()},
              "gpu_launches_per_step": int(launches // 2),
              "selected_per_segment": [int(x["selection_count"]) for x in rx["segments"]],
              "note": "RK_FP32_EXACT: SIMT kernels replaying the reference's fp32 operation order"}
-    del sx, wx, cb, ctxb
+    del cb, ctxb
+    # fp32-accurate tensor-core mode (RK_FP32_TC: 3xTF32 tcgen05 GEMMs + fp32
+    # flash attention) on the same relay caches: TTFT and error vs the exact run
+    tc = None
+    try:
+        wt = eng.weights(spec_obj(), SEED, "fp32tc")
+        ct = [wt.upload_cache(h) for h in hosts]
+        ctxt = wt.context()
+        rt = run(ctxt, ct, True)
+        Kt, Vt = ctxt.all()
+        tc_ms, _, tc_launches = timed(lambda: run(ctxt, ct), 3, 1)
+        eng.profile(True)
+        run(ctxt, ct)
+        kst = eng.profile_read()
+        eng.profile(False)
+        tsplit = {}
+        for k in kst:
+            key = "attention" if k["name"].startswith("attn") else (
+                "gemm" if k["name"].startswith("tc_split_gemm") else (
+                    "inner_gemm" if k["name"].startswith("gemm") else k["name"]))
+            tsplit[key] = tsplit.get(key, 0.0) + k["total_ms"]
+        same_sel = all(np.array_equal(a["selection"], b["selection"]) for a, b in zip(rt["segments"], rx["segments"]))
+        tc = {"ttft_ms": round(tc_ms / 3, 3), "tokens_per_s": round(n_tokens / (tc_ms / 3 / 1e3), 1),
+              "ms_by_kind": {k: round(v, 3) for k, v in tsplit.items()},
+              "gpu_launches_per_step": int(tc_launches // 3),
+              "error_vs_exact": {"logits_rel_l2": _rel_l2(rt["logits"], rx["logits"]),
+                                 "logits_max_abs": float(np.max(np.abs(rt["logits"].astype(np.float64) - rx["logits"]))),
+                                 "kv_rel_l2": max(_rel_l2(Kt, Kx), _rel_l2(Vt, Vx)) if same_sel else None,
+                                 "first_token_match": rt["first_token"] == rx["first_token"],
+                                 "selection_equal": same_sel,
+                                 "selected_per_segment": [int(x["selection_count"]) for x in rt["segments"]]},
+              "note": "RK_FP32_TC: 3xTF32 tcgen05 GEMMs (hi/lo split, K chunked into <=1536-element TMEM "
+                      "accumulations summed in fp32) + fp32 flash attention; exact-path storage and relay kernels"}
+        del ct, ctxt, wt
+    except Exception as ex:
+        tc = {"error": f"{type(ex).__name__}: {str(ex)[:200]}"}
+    exact["fp32_tc"] = tc
+    del sx, wx
     return exact, err
 
 

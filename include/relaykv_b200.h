@@ -49,8 +49,12 @@ typedef enum rk_status {
  *    double RoPE from a host cos/sin table) so results are bit-identical to
  *    the reference CPU path.
  *  RK_BF16: bf16 weights and KV context, tcgen05 tensor-core GEMMs with fp32
- *    accumulation, flash attention; throughput mode, reports its own error. */
-typedef enum rk_precision { RK_FP32_EXACT = 0, RK_BF16 = 1 } rk_precision;
+ *    accumulation, flash attention; throughput mode, reports its own error.
+ *  RK_FP32_TC: fp32-accurate tensor-core mode: RK_FP32_EXACT's storage and
+ *    relay kernels, matmuls as 3xTF32 on tcgen05 (hi/lo split, fp32
+ *    accumulation) and an fp32 flash attention; not bit-identical, relative
+ *    error ~1e-6 (north_star's "fp32-accumulate mode <= 1e-4 relative"). */
+typedef enum rk_precision { RK_FP32_EXACT = 0, RK_BF16 = 1, RK_FP32_TC = 2 } rk_precision;
 
 /* RelayMode (relay_engine.hpp:17-22). */
 typedef enum rk_relay_mode {

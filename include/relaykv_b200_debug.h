@@ -12,6 +12,9 @@ extern "C" {
 /* C[M x N] (+)= A[M x K] . B[N x K]^T with bf16-rounded operands; epi 1 adds
  * into C (residual epilogue, deterministic split-K), 3 stores. live_rows <=
  * rows_max is passed through device memory like a sparse pass. */
+/* RK_FP32_TC matmul: C (+)= A[M x K] . B[K x N] (reference layouts, fp32)
+ * as 3xTF32 on tcgen05 (layer_tc.cu). */
+int rk_debug_gemm_tc(rk_engine* e, const float* A, const float* B, float* C, int M, int N, int K, int add);
 int rk_debug_gemm_bf16(rk_engine* e, const float* A, const float* B, float* C, int rows_max, int live_rows,
                        int N, int K, int epi);
 /* out[M x H*dh] = causal attention of q rows at positions pos over ctx rows

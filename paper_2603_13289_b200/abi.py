@@ -15,6 +15,7 @@ RK_ERR_IO = 6
 
 RK_FP32_EXACT = 0
 RK_BF16 = 1
+RK_FP32_TC = 2
 
 RK_MODE_FULL = 0
 RK_MODE_ZERO = 1

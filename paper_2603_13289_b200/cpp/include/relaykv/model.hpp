@@ -31,7 +31,7 @@ struct rk_weights;
 
 namespace relaykv {
 
-enum class Precision { kFp32Exact = 0, kBf16 = 1 };
+enum class Precision { kFp32Exact = 0, kBf16 = 1, kFp32Tc = 2 };  // = rk_precision
 enum class PrefillLogits { kAllRows = 0, kLastRow = 1 };
 // Device and numerics of subsequent calls (process-wide; default 0, exact, all rows).
 void set_device(int device);

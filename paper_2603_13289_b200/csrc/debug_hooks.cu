@@ -7,6 +7,7 @@
 
 #include "glibc_expf.h"
 #include "layer_bf16.h"
+#include "layer_tc.h"
 #include "relaykv_b200_debug.h"
 
 using namespace rk;
@@ -39,6 +40,22 @@ DevBuf to_bf16(cudaStream_t st, const float* h, size_t n) {
 }  // namespace
 
 extern "C" {
+
+int rk_debug_gemm_tc(rk_engine* e, const float* A, const float* B, float* C, int M, int N, int K, int add) {
+  return guard([&] {
+    cudaStream_t st = e->stream;
+    DevBuf a((size_t)M * K * 4), b((size_t)K * N * 4), bt((size_t)3 * K * N * 4), c((size_t)M * N * 4);
+    RK_CUDA(cudaMemcpy(a.p, A, (size_t)M * K * 4, cudaMemcpyHostToDevice));
+    RK_CUDA(cudaMemcpy(b.p, B, (size_t)K * N * 4, cudaMemcpyHostToDevice));
+    RK_CUDA(cudaMemcpy(c.p, C, (size_t)M * N * 4, cudaMemcpyHostToDevice));
+    tc::pack_weight(st, bt.as<float>(), b.as<float>(), N, 0, 1, K, N);
+    Rows rows{M, nullptr, nullptr};
+    tc::gemm(e, a.as<float>(), K, rows, bt.as<float>(), N, K, c.as<float>(), N, add != 0);
+    RK_CUDA(cudaStreamSynchronize(st));
+    RK_CUDA(cudaGetLastError());
+    RK_CUDA(cudaMemcpy(C, c.p, (size_t)M * N * 4, cudaMemcpyDeviceToHost));
+  });
+}
 
 int rk_debug_gemm_bf16(rk_engine* e, const float* A, const float* B, float* C, int rows_max, int live_rows, int N,
                        int K, int epi) {

@@ -16,6 +16,7 @@
 #include <thread>
 
 #include "internal.h"
+#include "layer_tc.h"
 #include "layer.h"
 #include "prof.h"
 #include "profiler.h"
@@ -299,6 +300,28 @@ void pack_tensor(rk_weights* w, size_t idx, const float* src) {
   else RK_CUDA(cudaMemcpyAsync(w->head, src, d * V * 4, cudaMemcpyDeviceToDevice, st));
 }
 
+// RK_FP32_TC: the 3xTF32 packings [N x 3K] of the four layer matmuls, built
+// from the fp32 reference-layout tensors (layer_tc.cu).
+void build_tc_weights(rk_weights* w) {
+  const rk_model_spec& s = w->s;
+  const size_t d = s.d_model, q = w->q(), kv = w->kv(), ff = s.d_ff;
+  const size_t per = 3 * (d * (q + 2 * kv) + q * d + d * 2 * ff + ff * d);
+  w->tc_blob.alloc(per * s.num_layers * 4);
+  float* p = w->tc_blob.as<float>();
+  cudaStream_t st = w->e->stream;
+  for (auto& ly : w->layers) {
+    ly.tc_qkv = p, p += 3 * d * (q + 2 * kv);
+    ly.tc_o = p, p += 3 * q * d;
+    ly.tc_gu = p, p += 3 * d * 2 * ff;
+    ly.tc_down = p, p += 3 * ff * d;
+    tc::pack_weight(st, ly.tc_qkv, static_cast<const float*>(ly.w_qkv), (int)(q + 2 * kv), 0, 1, (int)d,
+                    (int)(q + 2 * kv));
+    tc::pack_weight(st, ly.tc_o, static_cast<const float*>(ly.w_o), (int)d, 0, 1, (int)q, (int)d);
+    tc::pack_weight(st, ly.tc_gu, static_cast<const float*>(ly.w_gu), (int)(2 * ff), 0, 1, (int)d, (int)(2 * ff));
+    tc::pack_weight(st, ly.tc_down, static_cast<const float*>(ly.w_down), (int)d, 0, 1, (int)ff, (int)d);
+  }
+}
+
 void check_spec(const rk_model_spec& s) {
   require(s.num_layers >= 1 && s.d_model > 0 && s.num_heads > 0 && s.num_kv_heads > 0 &&
               s.d_head > 0 && s.d_ff > 0 && s.vocab_size > 0 && s.max_positions > 0,
@@ -313,12 +336,20 @@ void check_spec(const rk_model_spec& s) {
 rk_weights* new_weights(rk_engine* e, const rk_model_spec* spec, int precision) {
   require(spec != nullptr, RK_ERR_INVALID_ARGUMENT, "null spec");
   check_spec(*spec);
-  require(precision == RK_FP32_EXACT || precision == RK_BF16, RK_ERR_INVALID_ARGUMENT, "bad precision");
+  require(precision == RK_FP32_EXACT || precision == RK_BF16 || precision == RK_FP32_TC, RK_ERR_INVALID_ARGUMENT,
+          "bad precision");
   auto w = std::make_unique<rk_weights>();
   w->e = e;
   w->s = *spec;
   w->precision = precision;
   w->elem = precision == RK_BF16 ? 2 : 4;
+  if (precision == RK_FP32_TC) {
+    require(spec->d_model % 64 == 0 && (spec->num_heads * spec->d_head) % 64 == 0 && spec->d_ff % 64 == 0 &&
+                (spec->num_heads * spec->d_head + 2 * spec->num_kv_heads * spec->d_head) % 64 == 0,
+            RK_ERR_INVALID_ARGUMENT, "fp32-tc mode requires d_model, q_dim, qkv width and d_ff to be multiples of 64");
+    require(spec->d_head == 64 || spec->d_head == 128, RK_ERR_INVALID_ARGUMENT,
+            "fp32-tc mode supports d_head 64 or 128");
+  }
   if (precision == RK_BF16) {
     require(spec->d_model % 64 == 0 && (spec->num_heads * spec->d_head) % 64 == 0 && spec->d_ff % 64 == 0 &&
                 spec->vocab_size % 64 == 0,
@@ -478,6 +509,7 @@ int rk_weights_init(rk_engine* e, const rk_model_spec* spec, uint64_t seed, int 
     }
     ones(1 + 9 * s.num_layers);
     gen(2 + 9 * s.num_layers, d_in);
+    if (precision == RK_FP32_TC) build_tc_weights(w.get());
     RK_CUDA(cudaStreamSynchronize(st));
     *out = w.release();
   });
@@ -502,6 +534,7 @@ int rk_weights_upload(rk_engine* e, const rk_model_spec* spec, const float* cons
       RK_CUDA(cudaMemcpyAsync(tmp.p, tensors[i], td.rows * td.cols * 4, cudaMemcpyHostToDevice, e->stream));
       pack_tensor(w.get(), i, tmp.as<float>());
     }
+    if (precision == RK_FP32_TC) build_tc_weights(w.get());
     RK_CUDA(cudaStreamSynchronize(e->stream));
     *out = w.release();
   });

@@ -436,7 +436,7 @@ __device__ __noinline__ void splitk_fixup(const GemmArgs& p, int splits, int num
   }
 }
 
-template <int BN, int EPI, int PAIR, bool CSK = false, int MT = 1>
+template <int BN, int EPI, int PAIR, bool CSK = false, int MT = 1, bool TF32 = false>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const GemmArgs p) {
@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     if (rank == 0 && elect_one()) {  // ---------------- MMA issuer (the pair's leader)
-      constexpr uint32_t idesc = idesc_bf16(kBM * PAIR, BN);
+      constexpr uint32_t idesc = TF32 ? idesc_tf32(kBM * PAIR, BN) : idesc_bf16(kBM * PAIR, BN);
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
@@ -560,9 +560,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int k = 0; k < kBK / 16; ++k) {
               if (p.dbg & 2) break;
               const uint32_t am = a0 + mi * kBM * kBK * 2 + k * 32;
-              if constexpr (PAIR == 2)
+              if constexpr (PAIR == 2 && TF32)
+                mma_tf32_ss_pair(d, sdesc_sw128(am, 16, 1024), sdesc_sw128(b0 + k * 32, 16, 1024), idesc,
+                                 (kb > kb0 || k > 0) ? 1u : 0u);
+              else if constexpr (PAIR == 2)
                 mma_bf16_ss_pair(d, sdesc_sw128(am, 16, 1024), sdesc_sw128(b0 + k * 32, 16, 1024), idesc,
                                  (kb > kb0 || k > 0) ? 1u : 0u);
+              else if constexpr (TF32)
+                mma_tf32_ss(d + mi * BN, sdesc_sw128(am, 16, 1024), sdesc_sw128(b0 + k * 32, 16, 1024), idesc,
+                            (kb > kb0 || k > 0) ? 1u : 0u);
               else
                 mma_bf16_ss(d + mi * BN, sdesc_sw128(am, 16, 1024), sdesc_sw128(b0 + k * 32, 16, 1024), idesc,
                             (kb > kb0 || k > 0) ? 1u : 0u);
@@ -1006,18 +1012,22 @@ __device__ __forceinline__ void splitk_reduce_row(const GemmArgs& p, int splits,
         acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
       }
     } else {
-      // all partials in flight at once, then summed in split order
-      float4 v[8];
+      // up to 8 partials in flight at once, summed in split order
+      acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int s0 = 0; s0 < splits; s0 += 8) {
+        float4 v[8];
 #pragma unroll
-      for (int s = 0; s < 8; ++s)
-        if (s < splits)
-          v[s] = __ldcg(reinterpret_cast<const float4*>(p.ws_part + ((size_t)s * p.rows_max + row) * p.N) + c);
-      acc = v[0];
+        for (int s = 0; s < 8; ++s)
+          if (s0 + s < splits)
+            v[s] = __ldcg(reinterpret_cast<const float4*>(p.ws_part + ((size_t)(s0 + s) * p.rows_max + row) * p.N) + c);
+        if (s0 == 0) acc = v[0];
+        else { acc.x += v[0].x; acc.y += v[0].y; acc.z += v[0].z; acc.w += v[0].w; }
 #pragma unroll
-      for (int s = 1; s < 8; ++s)
-        if (s < splits) {
-          acc.x += v[s].x; acc.y += v[s].y; acc.z += v[s].z; acc.w += v[s].w;
-        }
+        for (int s = 1; s < 8; ++s)
+          if (s0 + s < splits) {
+            acc.x += v[s].x; acc.y += v[s].y; acc.z += v[s].z; acc.w += v[s].w;
+          }
+      }
     }
     flag_nonfinite(p.status, finite_acc(finite_acc(finite_acc(finite_acc(0.f, acc.x), acc.y), acc.z), acc.w));
     float4 x = h[c];
@@ -1315,13 +1325,13 @@ void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cuda
   RK_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
 }
 
-template <int BN, int EPI, int PAIR, bool CSK = false, int MT = 1>
+template <int BN, int EPI, int PAIR, bool CSK = false, int MT = 1, bool TF32 = false>
 void launch(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& p, int grid) {
   using C = Cfg<BN, PAIR, MT>;
   static bool attr = false;
   if (!attr) {
-    RK_CUDA(cudaFuncSetAttribute(gemm_bf16_kernel<BN, EPI, PAIR, CSK, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 C::SMEM));
+    RK_CUDA(cudaFuncSetAttribute(gemm_bf16_kernel<BN, EPI, PAIR, CSK, MT, TF32>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr = true;
   }
   if constexpr (CSK) {
@@ -1339,7 +1349,7 @@ void launch(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const G
     cfg.numAttrs = 1;
     RK_CUDA(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<BN, EPI, 1, true>, a, b, p));
   } else if constexpr (PAIR == 1) {
-    launch_pdl(gemm_bf16_kernel<BN, EPI, 1, false, MT>, dim3(grid), dim3(kThreads), C::SMEM, st, a, b, p);
+    launch_pdl(gemm_bf16_kernel<BN, EPI, 1, false, MT, TF32>, dim3(grid), dim3(kThreads), C::SMEM, st, a, b, p);
   } else {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
@@ -1355,12 +1365,26 @@ void launch(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const G
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
-    RK_CUDA(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<BN, EPI, 2>, a, b, p));
+    RK_CUDA(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<BN, EPI, 2, false, 1, TF32>, a, b, p));
   }
 }
 
 template <int EPI>
 void launch_bn(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& p, int grid) {
+  if constexpr (EPI == EPI_ADD || EPI == EPI_F32 || EPI == EPI_PART) {
+    if (p.tf32) {  // 3xTF32 mode: 1-CTA or pair tiles only
+      if (p.pair == 2) {
+        if (p.bn == 256) launch<256, EPI, 2, false, 1, true>(st, a, b, p, grid);
+        else if (p.bn == 128) launch<128, EPI, 2, false, 1, true>(st, a, b, p, grid);
+        else launch<64, EPI, 2, false, 1, true>(st, a, b, p, grid);
+      } else {
+        if (p.bn == 256) launch<256, EPI, 1, false, 1, true>(st, a, b, p, grid);
+        else if (p.bn == 128) launch<128, EPI, 1, false, 1, true>(st, a, b, p, grid);
+        else launch<64, EPI, 1, false, 1, true>(st, a, b, p, grid);
+      }
+      return;
+    }
+  }
   if constexpr (EPI == EPI_ADD) {
     if (p.csk) {
       if (p.bn == 256) launch<256, EPI_ADD, 1, true>(st, a, b, p, grid);
@@ -1666,7 +1690,8 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
     const char* v = std::getenv("RK_GEMV");
     return v ? std::atoi(v) != 0 : true;
   }();
-  if (gemv_env && p.rows_max == 1 && !p.rows_dev &&
+  if (p.tf32 && p.epi != EPI_ADD && p.epi != EPI_F32) raise(RK_ERR_INVALID_ARGUMENT, "tf32 GEMM: ADD / F32 epilogues");
+  if (gemv_env && !p.tf32 && p.rows_max == 1 && !p.rows_dev &&
       (p.epi == EPI_ADD || p.epi == EPI_SILU || p.epi == EPI_F32 || p.epi == EPI_QKV) && p.N % 4 == 0) {
     const size_t smem = (size_t)p.K * 2;
     const bool narrow = p.N / (kGvWarps * 4) < 2 * e->sm_count;
@@ -1711,7 +1736,31 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
     const int epi0 = p.epi;
     GemmArgs alt = p;
     const double other = choose_config(alt, e->sm_count, rows_hint > 0 ? rows_hint : p.rows_max);
-    if (!choose_swap(p, e->sm_count, other)) p = alt;
+    if (p.tf32 || !choose_swap(p, e->sm_count, other)) p = alt;
+    if (p.tf32) {
+      // The tensor core's fp32 accumulation loses ~3.6e-9 (relative, measured)
+      // per accumulated element of K, linearly in K (r02v: rel-L2 6e-6 at a
+      // 3K of 1536, 8.7e-5 at 24576). So the 3K-long dot products are cut into
+      // chunks of <= 48 k-blocks (1536 fp32) accumulated in TMEM, written as
+      // split-K partials and summed on the CUDA cores (RN, split order).
+      p.mt_group = 1;
+      p.csk = 0;
+      p.streamk = 0;
+      p.epi = epi0;
+      const int kb = p.K / kBK;
+      int sp = std::min(16, (kb + 47) / 48);
+      while (sp > 1 && (sp - 1) * ((kb + sp - 1) / sp) >= kb) --sp;
+      p.splits = sp;
+      if (sp > 1) {
+        p.pair = 1;
+        if (p.N % p.bn) p.bn = 64;
+        if (epi0 == EPI_F32)  // the reduce adds into the output: start from zero
+          RK_CUDA(cudaMemset2DAsync(p.out_f32, (size_t)p.ld_out * 4, 0, (size_t)p.N * 4, p.rows_max, e->stream));
+        p.epi = EPI_PART;
+      } else {
+        p.splits = 1;
+      }
+    }
     // sweep hook: RK_GEMM_OVERRIDE="M[d]:N:K=bn/pair/splits;..." (d: live rows
     // on the device) forces one shape's tile config (tools/gemm_override_sweep.py)
     struct Ovr {

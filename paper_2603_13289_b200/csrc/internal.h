@@ -122,6 +122,11 @@ struct rk_layer_dev {
   void* w_o = nullptr;         // [q x d]
   void* w_gu = nullptr;        // [d x 2ff] interleaved
   void* w_down = nullptr;      // [ff x d]
+  // RK_FP32_TC: 3xTF32 packings [N x 3K] = [hi | lo | hi] of the transposed weights
+  float* tc_qkv = nullptr;
+  float* tc_o = nullptr;
+  float* tc_gu = nullptr;
+  float* tc_down = nullptr;
 };
 
 struct rk_weights {
@@ -130,6 +135,7 @@ struct rk_weights {
   int precision = RK_FP32_EXACT;
   size_t elem = 4;             // bytes per stored weight element
   rk::DevBuf blob;             // all tensors
+  rk::DevBuf tc_blob;          // RK_FP32_TC packed weights (layer_tc.cu)
   void* emb = nullptr;         // [V x d] (fp32 exact; bf16 in BF16)
   float* final_norm = nullptr; // [d]
   void* head = nullptr;        // exact: [d x V]; bf16: [V x d]
@@ -202,6 +208,7 @@ struct Scratch {
   DevBuf hidden, sub_hidden, normed, qkv, attn, act, logits, tokens, positions, sub_positions;
   DevBuf s_dev, s_key, sel_idx, sel_tags, sel_info, depth, argmax, seg_hidden_out;
   DevBuf gemm_tmp, attn_ws, attn_cnt, gemm_ws;
+  DevBuf tc_split, tc_gu;  // RK_FP32_TC: [hi|hi|lo] GEMM operand, gate/up output
   DevBuf norm_inv, norm_part, norm_cnt;  // fused RMSNorm (layer_bf16.cu)
 };
 

@@ -17,22 +17,43 @@ __device__ __forceinline__ int live_rows(const Rows& r) { return r.rows_dev ? *r
 
 // rms_norm (tensor.cpp:109-119): ms sequential over the row, then
 // inv = 1/sqrt(ms/n + eps), out = x * inv * gain.
-__global__ void rmsnorm_exact_kernel(const float* __restrict__ x, const float* __restrict__ gain,
-                                     float eps, float* __restrict__ out, Rows rows, int d) {
-  __shared__ float inv_s[128];
+// CTA = 32 rows, 256 threads: the 8 warps stage 64-column chunks of the rows
+// into shared memory with coalesced loads (double-buffered), and lane r of
+// warp 0 adds its row's squares in column order -- the reference's sequential
+// sum, bit for bit, without a strided global load per element.
+constexpr int kNormRows = 32, kNormCols = 64;
+__global__ void __launch_bounds__(256) rmsnorm_exact_kernel(const float* __restrict__ x, const float* __restrict__ gain,
+                                                            float eps, float* __restrict__ out, Rows rows, int d) {
+  __shared__ float tile[2][kNormRows][kNormCols + 1];
+  __shared__ float inv_s[kNormRows];
   const int M = live_rows(rows);
-  const int r0 = blockIdx.x * 128;
+  const int r0 = blockIdx.x * kNormRows;
   if (r0 >= M) return;
-  const int r = r0 + threadIdx.x;
-  if (r < M) {
-    const float* xr = x + (size_t)r * d;
-    float ms = 0.0f;
-    for (int i = 0; i < d; ++i) ms = __fadd_rn(ms, __fmul_rn(xr[i], xr[i]));
+  const int nr = min(kNormRows, M - r0);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  auto stage = [&](int buf, int c0) {
+    for (int rr = warp; rr < nr; rr += 8)
+      for (int c = lane; c < kNormCols; c += 32)
+        tile[buf][rr][c] = c0 + c < d ? x[(size_t)(r0 + rr) * d + c0 + c] : 0.0f;
+  };
+  float ms = 0.0f;
+  const int nch = (d + kNormCols - 1) / kNormCols;
+  stage(0, 0);
+  __syncthreads();
+  for (int ch = 0; ch < nch; ++ch) {
+    if (ch + 1 < nch) stage((ch + 1) & 1, (ch + 1) * kNormCols);  // next chunk lands while warp 0 sums
+    if (warp == 0 && lane < nr) {
+      const int n = min(kNormCols, d - ch * kNormCols);
+      const float* t = tile[ch & 1][lane];
+      for (int c = 0; c < n; ++c) ms = __fadd_rn(ms, __fmul_rn(t[c], t[c]));
+    }
+    __syncthreads();
+  }
+  if (warp == 0 && lane < nr) {
     ms = __fdiv_rn(ms, (float)d);
-    inv_s[threadIdx.x] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(ms, eps)));
+    inv_s[lane] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(ms, eps)));
   }
   __syncthreads();
-  const int nr = min(128, M - r0);
   for (int i = threadIdx.x; i < nr * d; i += blockDim.x) {
     const int rr = i / d, c = i % d;
     const size_t idx = (size_t)(r0 + rr) * d + c;
@@ -263,7 +284,7 @@ namespace k {
 void rmsnorm_exact(cudaStream_t s, const float* x, const float* gain, float eps, float* out,
                    Rows rows, int d) {
   if (rows.rows_max <= 0) return;
-  rmsnorm_exact_kernel<<<(rows.rows_max + 127) / 128, 128, 0, s>>>(x, gain, eps, out, rows, d);
+  rmsnorm_exact_kernel<<<(rows.rows_max + kNormRows - 1) / kNormRows, 256, 0, s>>>(x, gain, eps, out, rows, d);
 }
 
 void gemm_exact(cudaStream_t s, const float* A, const float* B, float* C, Rows rows, int N, int K,

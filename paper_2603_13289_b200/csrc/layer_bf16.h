@@ -26,6 +26,10 @@ struct GemmArgs {
   // swap-AB (short static M): the weights are the MMA's M side (256 rows per
   // CTA pair), the M tokens its N side in nc chunks of tc (<= 256) columns
   int swap = 0, tc = 0, nc = 1;
+  // tf32: operands are fp32 viewed as bf16 pairs (K, lda in bf16 units = 2x
+  // the fp32 count), kind::tf32 MMAs (the 3xTF32 mode's K-concatenated
+  // [hi|lo|hi] x [hi|hi|lo] operands); EPI_ADD / EPI_F32 only
+  int tf32 = 0;
   int* split_flags = nullptr;   // ordered split-K flags (EPI_ADD), zero-initialised
   // outputs
   float* out_f32 = nullptr;     // EPI_ADD / EPI_F32, row stride ld_out

@@ -11,6 +11,7 @@
 #include <cstdlib>
 
 #include "layer.h"
+#include "layer_tc.h"
 #include "prof.h"
 
 namespace rk {
@@ -144,15 +145,27 @@ void Runner::run_layer(rk_context* ctx, int l, float* hidden, Rows rows, bool co
   float* ck = static_cast<float*>(ctx->k_layer(l));
   float* cv = static_cast<float*>(ctx->v_layer(l));
   const double2* rope = w_->rope->cs.as<double2>();
-  k::rmsnorm_exact(st_, hidden, ly.attn_norm, s.norm_eps, S.normed.as<float>(), rows, d);
-  k::gemm_exact(st_, S.normed.as<float>(), static_cast<const float*>(ly.w_qkv), S.qkv.as<float>(), rows,
-                q + 2 * kv, d, k::EPI_STORE, status);
+  const bool tcm = w_->precision == RK_FP32_TC;  // 3xTF32 matmuls + fp32 flash attention (layer_tc.cu)
+  {
+    ProfScope ps(e_, "norm_exact", 0, 0);
+    k::rmsnorm_exact(st_, hidden, ly.attn_norm, s.norm_eps, S.normed.as<float>(), rows, d);
+  }
+  if (tcm) {
+    tc::gemm(e_, S.normed.as<float>(), d, rows, ly.tc_qkv, q + 2 * kv, d, S.qkv.as<float>(), q + 2 * kv, false);
+  } else {
+    ProfScope ps(e_, "gemm_exact_qkv", 0, 0);
+    k::gemm_exact(st_, S.normed.as<float>(), static_cast<const float*>(ly.w_qkv), S.qkv.as<float>(), rows,
+                  q + 2 * kv, d, k::EPI_STORE, status);
+  }
   if (cap_k_) {  // decode-time capture of pre-rotation K and V (model.cpp:254-257)
     k::copy2d_f32(st_, cap_k_, kv, 1, S.qkv.as<float>() + q, q + 2 * kv, 1, rows.rows_max, kv);
     k::copy2d_f32(st_, cap_v_, kv, 1, S.qkv.as<float>() + q + kv, q + 2 * kv, 1, rows.rows_max, kv);
     e_->launches += 2;
   }
-  k::rope_commit_exact(st_, S.qkv.as<float>(), rows, H, Hkv, dh, rope, ck, cv, commit ? 1 : 0);
+  {
+    ProfScope ps(e_, "rope_commit_exact", 0, 0);
+    k::rope_commit_exact(st_, S.qkv.as<float>(), rows, H, Hkv, dh, rope, ck, cv, commit ? 1 : 0);
+  }
   const float* qkv = S.qkv.as<float>();
   if (tail >= 0 && commit && !rows.rows_dev && tail < rows.rows_max) {
     // only the last `tail` rows continue (see run_layer_bf16)
@@ -165,15 +178,36 @@ void Runner::run_layer(rk_context* ctx, int l, float* hidden, Rows rows, bool co
     qkv += (size_t)off * (q + 2 * kv);
     rows = Rows{tail, nullptr, rows.pos + off};
   }
-  k::attn_exact(st_, qkv, rows, H, Hkv, dh, ck, cv, S.attn.as<float>(), commit ? 0 : 1,
-                max_ctx, probs, key_lo, key_n);
-  k::gemm_exact(st_, S.attn.as<float>(), static_cast<const float*>(ly.w_o), hidden, rows, d, q,
-                k::EPI_ADD, status);
+  if (tcm && commit && !probs) {  // (the pure-query pass and the capture keep the exact kernel)
+    tc::attention(e_, qkv, q + 2 * kv, rows, H, Hkv, dh, ck, cv, S.attn.as<float>());
+  } else {
+    ProfScope ps(e_, "attn_exact", 0, 0);
+    k::attn_exact(st_, qkv, rows, H, Hkv, dh, ck, cv, S.attn.as<float>(), commit ? 0 : 1,
+                  max_ctx, probs, key_lo, key_n);
+  }
+  if (tcm) {
+    tc::gemm(e_, S.attn.as<float>(), q, rows, ly.tc_o, d, q, hidden, d, true);
+    k::rmsnorm_exact(st_, hidden, ly.mlp_norm, s.norm_eps, S.normed.as<float>(), rows, d);
+    S.tc_gu.ensure((size_t)rows.rows_max * 2 * ff * 4);
+    tc::gemm(e_, S.normed.as<float>(), d, rows, ly.tc_gu, 2 * ff, d, S.tc_gu.as<float>(), 2 * ff, false);
+    tc::silu(e_, S.tc_gu.as<float>(), S.act.as<float>(), rows, ff);
+    tc::gemm(e_, S.act.as<float>(), ff, rows, ly.tc_down, d, ff, hidden, d, true);
+    e_->launches += 3;
+    return;
+  }
+  {
+    ProfScope ps(e_, "gemm_exact_o", 0, 0);
+    k::gemm_exact(st_, S.attn.as<float>(), static_cast<const float*>(ly.w_o), hidden, rows, d, q,
+                  k::EPI_ADD, status);
+  }
   k::rmsnorm_exact(st_, hidden, ly.mlp_norm, s.norm_eps, S.normed.as<float>(), rows, d);
-  k::gemm_exact(st_, S.normed.as<float>(), static_cast<const float*>(ly.w_gu), S.act.as<float>(), rows,
-                2 * ff, d, k::EPI_SILU_PAIR, status);
-  k::gemm_exact(st_, S.act.as<float>(), static_cast<const float*>(ly.w_down), hidden, rows, d, ff,
-                k::EPI_ADD, status);
+  {
+    ProfScope ps(e_, "gemm_exact_mlp", 0, 0);
+    k::gemm_exact(st_, S.normed.as<float>(), static_cast<const float*>(ly.w_gu), S.act.as<float>(), rows,
+                  2 * ff, d, k::EPI_SILU_PAIR, status);
+    k::gemm_exact(st_, S.act.as<float>(), static_cast<const float*>(ly.w_down), hidden, rows, d, ff,
+                  k::EPI_ADD, status);
+  }
   e_->launches += 8;
 }
 

@@ -7,11 +7,12 @@ library raises at import of this module.
 """
 import ctypes as C
 import os
+import sys
 
 import numpy as np
 
 from .abi import (LayerProfile, ModelSpec, RelayCacheView, RelayOptions, RelayOutput, RK_BF16,
-                  RK_FP32_EXACT, exception_for, stats_dict)
+                  RK_FP32_EXACT, RK_FP32_TC, exception_for, stats_dict)
 from .hostcache import HostRelayCache
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "librelaykv_b200.so")
@@ -77,6 +78,11 @@ class _Obj:
             self.ptr = None
 
     def __del__(self):
+        # (at interpreter shutdown the engine may already be gone -- objects
+        # kept alive by a traceback must not free into a destroyed engine;
+        # the process exit releases the device memory)
+        if sys.is_finalizing():
+            return
         try:
             self.close()
         except Exception:
@@ -136,13 +142,13 @@ class Engine(_Obj):
     # ---- factories ------------------------------------------------------------
     def weights(self, spec, seed, precision="fp32"):
         """init_weights(spec, seed) on the device (model.cpp:81-114)."""
-        prec = {"fp32": RK_FP32_EXACT, "bf16": RK_BF16}[precision]
+        prec = {"fp32": RK_FP32_EXACT, "bf16": RK_BF16, "fp32tc": RK_FP32_TC}[precision]
         out = P()
         _check(lib().rk_weights_init(P(self.ptr), C.byref(spec), U64(seed), prec, C.byref(out)))
         return Weights(out.value, self, spec, precision)
 
     def weights_from_tensors(self, spec, tensors, precision="fp32"):
-        prec = {"fp32": RK_FP32_EXACT, "bf16": RK_BF16}[precision]
+        prec = {"fp32": RK_FP32_EXACT, "bf16": RK_BF16, "fp32tc": RK_FP32_TC}[precision]
         arrs = [np.ascontiguousarray(t, np.float32) for t in tensors]
         ptrs = (F32P * len(arrs))(*[a.ctypes.data_as(F32P) for a in arrs])
         out = P()
