@@ -625,7 +625,7 @@ def run_ours(args, world, rank, local, dist):
     hbm, tf_burst, tf_sus, src = peaks()
     traffic = {}  # ncu DRAM bytes per launch, from the committed capture of this workload
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r02_traffic.json")) as f:
             traffic = json.load(f)["kernels"] if args.config == "c2" else {}
     except Exception:
         traffic = {}

@@ -30,12 +30,13 @@ if has launches; then
     $LEAN > $OUT/launches_bench.log 2>&1
 fi
 if has ncu; then
-  # kernel regex : launches to skip inside the step (c2: attention launch 1 = band layer 1,
-  # launch 3 = first sparse layer; GEMM launch 6 = band gate/up)
-  for spec in "gemm_bf16_kernel:6" "attn_kernel:1" "attn_kernel:3" "realign_graft:0" "score_dh_kernel:0" \
-              "select_relay_kernel:0"; do
-    pat=${spec%%:*}; skip=${spec##*:}
-    timeout 600 ncu $NV --set full --import-source on --clock-control none -k regex:$pat -s $skip -c 1 \
+  # c2 step order: gemm_bf16_kernel #5 = band gate/up (layer 1), #11-#14 = first
+  # sparse layer's QKV / W_o / gate/up / W_down; attn_kernel #0 prefix+suffix
+  # layer, #1 band, #3 sparse; gemm_swap_kernel #0 = prefix+suffix gate/up
+  for spec in "gemm_bf16_kernel:5:1" "gemm_bf16_kernel:11:4" "attn_kernel:0:1" "attn_kernel:1:1" "attn_kernel:3:1" \
+              "gemm_swap_kernel:0:1" "realign_graft:0:1" "score_dh_kernel:0:1" "select_relay_kernel:0:1"; do
+    pat=${spec%%:*}; rest=${spec#*:}; skip=${rest%%:*}; cnt=${rest##*:}
+    timeout 900 ncu $NV --set full --import-source on --clock-control none -k regex:$pat -s $skip -c $cnt \
       -o $OUT/full_${pat}_$skip $LEAN > $OUT/ncu_${pat}_$skip.log 2>&1
   done
 fi

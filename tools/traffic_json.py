@@ -1,7 +1,7 @@
 """Per-kernel DRAM traffic of one launch each (ncu --set full captures of a
-tools/gpu_round.sh run) -> profiles/r01_traffic.json (bench.py roofline.traffic).
+tools/gpu_round.sh run) -> profiles/r02_traffic.json (bench.py roofline.traffic).
 
-  python tools/traffic_json.py gpurun_out/<tag> > profiles/r01_traffic.json
+  python tools/traffic_json.py gpurun_out/<tag> > profiles/r02_traffic.json
 """
 import csv
 import io
@@ -10,13 +10,17 @@ import os
 import subprocess
 import sys
 
-CAPTURES = {  # capture file -> (bench kernel family, launch description)
-    "full_gemm_bf16_kernel_6": ("gemm_bf16_tcgen05", "band gate/up GEMM, layer 1: M=4032 N=16384 K=2048, CTA pair "
+CAPTURES = {  # capture file -> (bench kernel family, launch description); r02 capture order (tools/gpu_round.sh)
+    "full_gemm_bf16_kernel_5": ("gemm_bf16_tcgen05", "band gate/up GEMM, layer 1: M=4032 N=16384 K=2048, CTA pair "
                                                      "(256x256 pair tile, SiLU epilogue)"),
-    "full_attn_kernel_1": ("attention_bf16_tcgen05", "band layer 1: 4032 query rows x 4032 keys, 32 heads, d_head 64"),
+    "full_attn_kernel_1": ("attention_bf16_tcgen05", "band layer 1: 4032 query rows x 4032 keys, 32 heads, d_head 64, "
+                                                     "GQA-packed (32 rows x 4 heads per CTA)"),
     "full_attn_kernel_3": ("attention_bf16_tcgen05_sparse", "sparse layer 3: live rows (prefix|suffix|selected) x "
                                                             "4032 keys"),
-    "full_realign_graft_0": ("realign_graft", "segment 1: 1856 tokens x 14 grafted layers x kv 512, bf16"),
+    "full_attn_kernel_0": ("attention_bf16_tcgen05_presuf", "prefix+suffix layer 0: 320 rows x 4032 keys, split-KV "
+                                                            "with in-kernel merge"),
+    "full_gemm_swap_kernel_0": ("gemm_swap_bf16_tcgen05", "prefix+suffix gate/up: M=320 N=16384 K=2048, swap-AB pair"),
+    "full_realign_graft_0": ("realign_graft", "both segments: 2 x 1856 tokens x 14 grafted layers x kv 512, bf16"),
     "full_score_dh_kernel_0": ("score_deviation", "segment 1: 1856 tokens, V and K at l_det"),
     "full_select_relay_kernel_0": ("select_relay", "segment 1: 1856 scores"),
 }
