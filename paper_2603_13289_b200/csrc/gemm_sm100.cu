@@ -16,8 +16,8 @@
 //   CTA pair   cluster of 2, tcgen05 cta_group::2, 256 x BN tiles; each CTA
 //              stages half of B, halving the L2->SM feed per MMA
 //   split-K    residual GEMMs that cannot fill the GPU: fp32 partials reduced
-//              in split order (splitk_reduce_add_kernel) or, opt-in, over DSMEM
-//   m-grouped  (opt-in) all m tiles of a short M in one CTA
+//              in split order (splitk_reduce_add_kernel)
+//   swap-AB    (gemm_swap_kernel) wide short-M SiLU GEMMs: weights on the MMA's M side
 //   GEMV       M = 1 (top-layer last row, logits head, decode steps): CUDA
 //              cores at HBM speed with the same epilogues
 //
@@ -66,20 +66,18 @@ constexpr int kThreads = 192;
 // of B, so a CTA's shared-memory fill per k-block drops from 48 KB to 32 KB
 // (BN=256) -- the L2->SM feed, not the tensor pipe, bounds the 1-CTA kernel.
 //
-// MT > 1 (short M, <= MT*128 rows): one CTA computes all MT m-tiles of its N
-// tile, so each weight (B) tile is staged by exactly one SM instead of MT --
-// for the prefix/suffix-only layers the weight stream, not the tiny A, is the
-// traffic. MT accumulators of BN columns each (single-buffered when 2 do not fit).
+// (Variants measured slower on the c2 shapes in round 1-2 and removed: cluster
+// split-K over DSMEM, m-grouped short-M tiles, stream-K, L2 weight prefetch,
+// in-GEMM split-K fixup -- see DESIGN.md section 11.)
 constexpr int pow2_cols(int c) { return c <= 32 ? 32 : (c <= 64 ? 64 : (c <= 128 ? 128 : (c <= 256 ? 256 : 512))); }
-template <int BN, int PAIR = 1, int MT = 1>
+template <int BN, int PAIR = 1>
 struct Cfg {
-  static constexpr int A_BYTES = MT * kBM * kBK * 2;
+  static constexpr int A_BYTES = kBM * kBK * 2;
   static constexpr int B_BYTES = BN / PAIR * kBK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = MT > 1 ? (192 * 1024) / STAGE_BYTES
-                                       : PAIR == 1 ? ((BN == 256) ? 4 : (BN == 128 ? 6 : 8)) : (BN == 256 ? 6 : 8);
-  static constexpr int NACC = 2 * MT * BN <= 512 ? 2 : 1;  // TMEM accumulator buffers
-  static constexpr int TMEM_COLS = pow2_cols(NACC * MT * BN);
+  static constexpr int STAGES = PAIR == 1 ? ((BN == 256) ? 4 : (BN == 128 ? 6 : 8)) : (BN == 256 ? 6 : 8);
+  static constexpr int NACC = 2;  // TMEM accumulator buffers
+  static constexpr int TMEM_COLS = pow2_cols(NACC * BN);
   // per epilogue warp: a 32x32 fp32 staging tile for the coalesced residual epilogue
   static constexpr int EPI_STAGE = 4 * 32 * 32 * 4;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + EPI_STAGE;
@@ -90,12 +88,12 @@ struct Units {
   int total;
 };
 
-template <int PAIR = 1, int MT = 1>
+template <int PAIR = 1>
 __device__ __forceinline__ Units units_of(const GemmArgs& p) {
   Units u;
   const int M = p.rows_dev ? *p.rows_dev : p.rows_max;
-  // m tiles of 128 (or 256-row pair tiles); one group of MT tiles when MT > 1
-  u.num_m = MT > 1 ? (M > 0 ? 1 : 0) : (M + kBM * PAIR - 1) / (kBM * PAIR);
+  // m tiles of 128 (or 256-row pair tiles)
+  u.num_m = (M + kBM * PAIR - 1) / (kBM * PAIR);
   u.num_n = p.N / p.bn;
   // live row count known only on the device: pick split-K here (grid = all SMs)
   u.splits = p.splits;
@@ -114,41 +112,20 @@ __device__ __forceinline__ void decode_unit(const Units& u, int unit, int& mt, i
   nt = tile / u.num_m;
 }
 
-// One accumulator's worth of work: tile (mt, nt), k-blocks [kb0, kb1); s is
-// the split index (split-K) or the CTA-local slot (stream-K).
+// One accumulator's worth of work: tile (mt, nt), k-blocks [kb0, kb1) of split s.
 struct Work {
   int mt, nt, s, kb0, kb1;
 };
 
-// Stream-K: the tile-major k-block space (tile t = mt + nt*num_m) is cut into
-// gridDim.x equal contiguous ranges; CTA g takes range g, touching at most
-// kSkSlots tiles (the host uses it only with at most 2 tiles per CTA, counting
-// the largest live row count).
-constexpr int kSkSlots = 4;
-__device__ __forceinline__ long long sk_lo(const Units& u, int g, int G) {
-  return (long long)u.num_m * u.num_n * u.kb_total * g / G;
-}
-
 // k-th work item of this CTA (both CTAs of a pair walk the same units);
 // false when the CTA is done.
 template <int PAIR = 1>
-__device__ __forceinline__ bool get_work(const Units& U, bool streamk, int k, Work& w) {
-  if (PAIR == 2 || !streamk) {
-    const int unit = blockIdx.x / PAIR + k * (gridDim.x / PAIR);
-    if (unit >= U.total) return false;
-    decode_unit(U, unit, w.mt, w.nt, w.s);
-    w.kb0 = w.s * U.kb_per;
-    w.kb1 = min(U.kb_total, w.kb0 + U.kb_per);
-    return true;
-  }
-  const long long lo = sk_lo(U, blockIdx.x, gridDim.x), hi = sk_lo(U, blockIdx.x + 1, gridDim.x);
-  const long long t = lo / U.kb_total + k, tlo = t * U.kb_total;
-  if (tlo >= hi || lo >= hi) return false;
-  w.kb0 = (int)((lo > tlo ? lo : tlo) - tlo);
-  w.kb1 = (int)((hi < tlo + U.kb_total ? hi : tlo + U.kb_total) - tlo);
-  w.mt = (int)(t % U.num_m);
-  w.nt = (int)(t / U.num_m);
-  w.s = k;
+__device__ __forceinline__ bool get_work(const Units& U, int k, Work& w) {
+  const int unit = blockIdx.x / PAIR + k * (gridDim.x / PAIR);
+  if (unit >= U.total) return false;
+  decode_unit(U, unit, w.mt, w.nt, w.s);
+  w.kb0 = w.s * U.kb_per;
+  w.kb1 = min(U.kb_total, w.kb0 + U.kb_per);
   return true;
 }
 
@@ -165,8 +142,7 @@ __device__ __forceinline__ void epilogue_chunk(const GemmArgs& p, int row, int c
   flag_nonfinite(p.status, chk);
   if constexpr (EPI == EPI_F32 || EPI == EPI_PART) {
     float* base = EPI != EPI_PART ? p.out_f32 + (size_t)row * p.ld_out + col
-                  : p.streamk ? p.ws_part + (((size_t)blockIdx.x * kSkSlots + split) * kBM + row % kBM) * p.bn + col % p.bn
-                              : p.ws_part + ((size_t)split * p.rows_max + row) * p.N + col;
+                                  : p.ws_part + ((size_t)split * p.rows_max + row) * p.N + col;
     float4* dst = reinterpret_cast<float4*>(base);
 #pragma unroll
     for (int j = 0; j < 8; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
@@ -237,210 +213,11 @@ __device__ __forceinline__ void epilogue_chunk(const GemmArgs& p, int row, int c
   }
 }
 
-// Cluster split-K epilogue (CSK): the p.splits CTAs of a cluster computed the
-// K slices of one 128 x BN tile; row group o (g = ceil(128/s) rows) is owned
-// by CTA o. Each CTA stores its slice of group o into CTA o's (now idle)
-// pipeline shared memory over DSMEM, then every owner adds the s slices in
-// split order -- the same order as splitk_reduce_add_kernel, so the result is
-// bit-identical to the EPI_PART path without the global partial round trip
-// and the second launch -- to the residual, with the fused RMSNorm statistics.
-template <int BN>
-__device__ __forceinline__ void csk_epilogue(const GemmArgs& p, const Units& U, uint8_t* smem, uint32_t tmem,
-                                             int warp, int lane) {
-  const int s = p.splits, g = (kBM + s - 1) / s;
-  const uint32_t me = cluster_ctarank();
-  Work w;
-  if (!get_work<1>(U, false, 0, w)) return;  // the whole cluster is past the live rows
-  const int mt = w.mt, nt = w.nt;
-  const int M = p.rows_dev ? *p.rows_dev : p.rows_max;
-  float* red = reinterpret_cast<float*>(smem);  // [src split][g rows][BN], 16-B units XOR-swizzled by row
-  cluster_sync();  // every CTA's MMAs are done: all pipeline memory in the cluster is free
-  if (warp >= 2) {
-    const int quarter = warp & 3, row = quarter * 32 + lane;
-    const int o = row / g, lr = row - o * g;
-    const float rs = (p.row_scale && mt * kBM + row < M) ? p.row_scale[mt * kBM + row] : 1.0f;
-    const uint32_t dst = mapa_u32(smem_u32(red + ((size_t)me * g + lr) * BN), (p.dbg & 4) ? me : (uint32_t)o);
-#pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
-      uint32_t r[32];
-      tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + c, r);
-      tmem_ld_wait();
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int u = c / 4 + (j ^ (lr & 7));
-        st_cluster_v4(dst + u * 16, __float_as_uint(__uint_as_float(r[4 * j]) * rs),
-                      __float_as_uint(__uint_as_float(r[4 * j + 1]) * rs),
-                      __float_as_uint(__uint_as_float(r[4 * j + 2]) * rs),
-                      __float_as_uint(__uint_as_float(r[4 * j + 3]) * rs));
-      }
-    }
-  }
-  cluster_sync();  // all slices landed
-  if (warp < 2 || (p.dbg & 8)) return;
-  const bool norm = p.norm_part != nullptr;
-  const int r0 = (int)me * g, r1 = min(kBM, r0 + g), nrows = r1 - r0;
-  // warp w takes rows w, w+4, ...; RB rows at a time with their residuals
-  // loaded up front (the global-load latency is paid once per batch)
-  constexpr int NP = BN >= 128 ? BN / 128 : 1, RB = 8;
-  for (int base = warp - 2; base < nrows; base += 4 * RB) {
-    float4 hv[RB][NP];
-#pragma unroll
-    for (int i = 0; i < RB; ++i) {
-      const int lr = base + 4 * i, grow = mt * kBM + r0 + lr;
-#pragma unroll
-      for (int k = 0; k < NP; ++k) {
-        const int cc = lane * 4 + 128 * k;
-        hv[i][k] = (lr < nrows && grow < M && cc < BN)
-                       ? __ldcg(reinterpret_cast<const float4*>(p.out_f32 + (size_t)grow * p.ld_out + nt * BN + cc))
-                       : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < RB; ++i) {
-      const int lr = base + 4 * i, grow = mt * kBM + r0 + lr;
-      if (lr >= nrows || grow >= M) break;
-      float ss = 0.f;
-#pragma unroll
-      for (int k = 0; k < NP; ++k) {
-        const int cc = lane * 4 + 128 * k;
-        if (cc >= BN) break;
-        const int unit = cc / 4, phys = (unit & ~7) | ((unit & 7) ^ (lr & 7));
-        float4 acc = *reinterpret_cast<const float4*>(red + (size_t)lr * BN + phys * 4);
-        for (int src = 1; src < s; ++src) {
-          const float4 v = *reinterpret_cast<const float4*>(red + ((size_t)src * g + lr) * BN + phys * 4);
-          acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-        }
-        float4 h = hv[i][k];
-        h.x += acc.x; h.y += acc.y; h.z += acc.z; h.w += acc.w;
-        *reinterpret_cast<float4*>(p.out_f32 + (size_t)grow * p.ld_out + nt * BN + cc) = h;
-        if (norm) {
-          ss = fmaf(h.x, h.x, fmaf(h.y, h.y, fmaf(h.z, h.z, fmaf(h.w, h.w, ss))));
-          *reinterpret_cast<uint2*>(p.norm_bf16 + (size_t)grow * p.N + nt * BN + cc) =
-              make_uint2(pack_bf16(h.x, h.y), pack_bf16(h.z, h.w));
-        }
-      }
-      if (norm) {
-        for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-        if (lane == 0) p.norm_part[(size_t)grow * kNormSlots + nt] = ss;
-      }
-    }
-  }
-  if (norm) {
-    // the last of the num_n tiles of this row group turns the partials into 1/rms
-    __shared__ int done_sh;
-    __threadfence();
-    named_bar_sync(1, 128);
-    if (threadIdx.x == 64) done_sh = atomicAdd(p.norm_cnt + (size_t)mt * 8 + me, 1) + 1;
-    named_bar_sync(1, 128);
-    if (done_sh == U.num_n) {
-      __threadfence();
-      for (int lr = threadIdx.x - 64; lr < r1 - r0; lr += 128) {
-        const int grow = mt * kBM + r0 + lr;
-        if (grow >= M) break;
-        float tot = 0.f;
-        for (int t = 0; t < U.num_n; ++t) tot += __ldcg(p.norm_part + (size_t)grow * kNormSlots + t);
-        p.norm_inv[grow] = rsqrtf(tot / (float)p.N + p.norm_eps);
-      }
-      if (threadIdx.x == 64) p.norm_cnt[(size_t)mt * 8 + me] = 0;
-    }
-  }
-}
-
-// In-kernel split-K fixup (EPI_PART with p.fixup): after storing its fp32
-// partial of a 32-row group of tile (mt, nt), a warp takes a ticket; the last
-// of the p.splits warps sums the partials in split order (the order of
-// splitk_reduce_add_kernel, so the same bits), adds them to the residual and
-// runs the fused RMSNorm producer side -- no reduce launch, partials read from
-// L2 right after they were written. Lanes: 8 per row (16-byte chunks), 4 rows
-// per pass; all loads of a pass are in flight before the adds.
-template <int BN>
-__device__ __noinline__ void splitk_fixup(const GemmArgs& p, int splits, int num_n, int num_m128, int mt, int nt,
-                                          int quarter, int lane, int M) {
-  const int row0 = mt * kBM + quarter * 32;
-  if (row0 >= M) return;  // (every split skips these rows alike)
-  int* cnt = p.split_flags + ((size_t)(nt * num_m128 + mt) * 4 + quarter);
-  __threadfence();
-  __syncwarp();
-  int prev = 0;
-  if (lane == 0) prev = atomicAdd(cnt, 1);
-  prev = __shfl_sync(0xffffffffu, prev, 0);
-  if (prev != splits - 1) return;
-  __threadfence();  // the other splits' partials are visible from here
-  const bool norm = p.norm_part != nullptr;
-  const int sub = lane >> 3, ch = lane & 7;
-  constexpr int NC = BN / 32;  // 32-column passes
-  float chk = 0.f;
-#pragma unroll 1
-  for (int rg = 0; rg < 8; ++rg) {
-    const int row = row0 + rg * 4 + sub;
-    const bool ok = row < M;
-    const size_t rr = ok ? (size_t)row : (size_t)row0;
-    float4 acc[NC], h[NC];
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const int col = nt * BN + c * 32 + ch * 4;
-      acc[c] = __ldcg(reinterpret_cast<const float4*>(p.ws_part + rr * p.N + col));
-      h[c] = __ldcg(reinterpret_cast<const float4*>(p.out_f32 + rr * p.ld_out + col));
-    }
-    for (int sp = 1; sp < splits; ++sp) {
-      float4 v[NC];
-#pragma unroll
-      for (int c = 0; c < NC; ++c)
-        v[c] = __ldcg(reinterpret_cast<const float4*>(p.ws_part + ((size_t)sp * p.rows_max + rr) * p.N + nt * BN +
-                                                      c * 32 + ch * 4));
-#pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        acc[c].x += v[c].x; acc[c].y += v[c].y; acc[c].z += v[c].z; acc[c].w += v[c].w;
-      }
-    }
-    float ss = 0.f;
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const int col = nt * BN + c * 32 + ch * 4;
-      chk = finite_acc(finite_acc(finite_acc(finite_acc(chk, acc[c].x), acc[c].y), acc[c].z), acc[c].w);
-      float4 x = h[c];
-      x.x += acc[c].x; x.y += acc[c].y; x.z += acc[c].z; x.w += acc[c].w;
-      if (ok) {
-        *reinterpret_cast<float4*>(p.out_f32 + rr * p.ld_out + col) = x;
-        if (norm) {
-          ss = fmaf(x.x, x.x, fmaf(x.y, x.y, fmaf(x.z, x.z, fmaf(x.w, x.w, ss))));
-          *reinterpret_cast<uint2*>(p.norm_bf16 + rr * p.N + col) = make_uint2(pack_bf16(x.x, x.y), pack_bf16(x.z, x.w));
-        }
-      }
-    }
-    if (norm) {
-      ss += __shfl_xor_sync(0xffffffffu, ss, 1);
-      ss += __shfl_xor_sync(0xffffffffu, ss, 2);
-      ss += __shfl_xor_sync(0xffffffffu, ss, 4);
-      if (ok && ch == 0) p.norm_part[rr * kNormSlots + nt] = ss;
-    }
-  }
-  flag_nonfinite(p.status, chk);
-  if (lane == 0) *cnt = 0;  // self-resetting for the next GEMM
-  if (norm) {  // the last of the num_n tiles of these 32 rows turns the partials into 1/rms
-    __threadfence();
-    __syncwarp();
-    int done = 0;
-    if (lane == 0) done = atomicAdd(p.norm_cnt + (size_t)mt * 4 + quarter, 1) + 1;
-    done = __shfl_sync(0xffffffffu, done, 0);
-    if (done == num_n) {
-      __threadfence();
-      const int row = row0 + lane;
-      if (row < M) {
-        float tot = 0.f;
-        for (int t = 0; t < num_n; ++t) tot += __ldcg(p.norm_part + (size_t)row * kNormSlots + t);
-        p.norm_inv[row] = rsqrtf(tot / (float)p.N + p.norm_eps);
-      }
-      if (lane == 0) p.norm_cnt[(size_t)mt * 4 + quarter] = 0;
-    }
-  }
-}
-
-template <int BN, int EPI, int PAIR, bool CSK = false, int MT = 1, bool TF32 = false>
+template <int BN, int EPI, int PAIR, bool TF32 = false>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const GemmArgs p) {
-  using C = Cfg<BN, PAIR, MT>;
+  using C = Cfg<BN, PAIR>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
@@ -481,10 +258,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   // so with programmatic dependent launch the weight stream overlaps the
   // previous kernel's tail; A (activations) follows after the wait.
   int pre = 0;
-  if (warp == 0 && !p.rows_dev && !p.streamk && !CSK && !(p.dbg & 1)) {
-    const Units Up = units_of<PAIR, MT>(p);
+  if (warp == 0 && !p.rows_dev && !(p.dbg & 1)) {
+    const Units Up = units_of<PAIR>(p);
     Work w0;
-    if (elect_one() && get_work<PAIR>(Up, false, 0, w0)) {
+    if (elect_one() && get_work<PAIR>(Up, 0, w0)) {
       pre = min(C::STAGES, w0.kb1 - w0.kb0);
       for (int i = 0; i < pre; ++i) {
         uint8_t* sa = smem + i * C::STAGE_BYTES;
@@ -500,21 +277,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   pdl_wait();  // the prologue above overlapped the previous kernel; its outputs are visible from here
-  const Units U = units_of<PAIR, MT>(p);
+  const Units U = units_of<PAIR>(p);
 
   if (warp == 0) {
     if (elect_one()) {  // ---------------- TMA producer
       int stage = 0;
       uint32_t phase = 0;
       Work w;
-      for (int it = 0; get_work<PAIR>(U, p.streamk, it, w); ++it) {
+      for (int it = 0; get_work<PAIR>(U, it, w); ++it) {
         const int mt = w.mt, nt = w.nt, kb0 = w.kb0, kb1 = w.kb1;
-        const int bcol = nt * BN + rank * (BN / PAIR);
-        // one CTA per weight tile (m tile 0) prefetches it into L2 ahead of the ring
-        const int pf = mt == 0 ? p.prefetch : 0;
-        for (int kb = kb0; kb < kb0 + pf && kb < kb1; ++kb) tma_prefetch_2d(&tmB, kb * kBK, bcol);
         for (int kb = kb0; kb < kb1; ++kb) {
-          if (pf && kb + pf < kb1) tma_prefetch_2d(&tmB, (kb + pf) * kBK, bcol);
           const bool early = it == 0 && kb - kb0 < pre;  // stage armed, its B already in flight
           if (!early) mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
@@ -527,9 +299,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (!early) tma_load_2d_pair(sa + C::A_BYTES, &tmB, &full[stage], kx, bn_ * BN + rank * (BN / 2));
           } else {
             if (!early) mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-#pragma unroll
-            for (int mi = 0; mi < MT; ++mi)
-              tma_load_2d(sa + mi * kBM * kBK * 2, &tmA, &full[stage], kx, (am * MT + mi) * kBM);
+            tma_load_2d(sa, &tmA, &full[stage], kx, am * kBM);
             if (!early) tma_load_2d(sa + C::A_BYTES, &tmB, &full[stage], kx, bn_ * BN);
           }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
@@ -543,23 +313,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int local = 0;
       Work w;
-      for (int it = 0; get_work<PAIR>(U, p.streamk, it, w); ++it, ++local) {
+      for (int it = 0; get_work<PAIR>(U, it, w); ++it, ++local) {
         const int kb0 = w.kb0, kb1 = w.kb1;
         const int acc = local % C::NACC;
         mbar_wait(&tempty[acc], ((local / C::NACC) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d = tmem + acc * MT * BN;
+        const uint32_t d = tmem + acc * BN;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a0 = smem_u32(smem + stage * C::STAGE_BYTES);
           const uint32_t b0 = a0 + C::A_BYTES;
-#pragma unroll
-          for (int mi = 0; mi < MT; ++mi) {
+          {
 #pragma unroll
             for (int k = 0; k < kBK / 16; ++k) {
               if (p.dbg & 2) break;
-              const uint32_t am = a0 + mi * kBM * kBK * 2 + k * 32;
+              const uint32_t am = a0 + k * 32;
               if constexpr (PAIR == 2 && TF32)
                 mma_tf32_ss_pair(d, sdesc_sw128(am, 16, 1024), sdesc_sw128(b0 + k * 32, 16, 1024), idesc,
                                  (kb > kb0 || k > 0) ? 1u : 0u);
@@ -567,10 +336,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mma_bf16_ss_pair(d, sdesc_sw128(am, 16, 1024), sdesc_sw128(b0 + k * 32, 16, 1024), idesc,
                                  (kb > kb0 || k > 0) ? 1u : 0u);
               else if constexpr (TF32)
-                mma_tf32_ss(d + mi * BN, sdesc_sw128(am, 16, 1024), sdesc_sw128(b0 + k * 32, 16, 1024), idesc,
+                mma_tf32_ss(d, sdesc_sw128(am, 16, 1024), sdesc_sw128(b0 + k * 32, 16, 1024), idesc,
                             (kb > kb0 || k > 0) ? 1u : 0u);
               else
-                mma_bf16_ss(d + mi * BN, sdesc_sw128(am, 16, 1024), sdesc_sw128(b0 + k * 32, 16, 1024), idesc,
+                mma_bf16_ss(d, sdesc_sw128(am, 16, 1024), sdesc_sw128(b0 + k * 32, 16, 1024), idesc,
                             (kb > kb0 || k > 0) ? 1u : 0u);
             }
           }
@@ -582,27 +351,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         else tc_commit(&tfull[acc]);
       }
     }
-  } else if constexpr (CSK) {  // epilogue warps: wait for this CTA's K slice, then the cluster epilogue
-    Work w0;
-    if (get_work<1>(U, false, 0, w0)) {  // (a cluster past the live rows has no tile)
-      mbar_wait(&tfull[0], 0);
-      tc_fence_after();
-    }
   } else {  // ------------------------------- epilogue warps 2..5
     const int quarter = warp & 3;
     const int M = p.rows_dev ? *p.rows_dev : p.rows_max;
     int local = 0;
     Work w;
-    for (int it = 0; get_work<PAIR>(U, p.streamk, it, w); ++it, ++local) {
+    for (int it = 0; get_work<PAIR>(U, it, w); ++it, ++local) {
       const int acc = local % C::NACC, use = local / C::NACC;
-#pragma unroll 1
-      for (int mi = 0; mi < MT; ++mi) {
-      const int mt = (w.mt * PAIR + rank) * MT + mi, nt = w.nt, s = w.s;  // this CTA's 128-row tile
-      const uint32_t acol = (uint32_t)((acc * MT + mi) * BN);  // its accumulator's first TMEM column
+      {
+      const int mt = w.mt * PAIR + rank, nt = w.nt, s = w.s;  // this CTA's 128-row tile
+      const uint32_t acol = (uint32_t)(acc * BN);  // its accumulator's first TMEM column
       const int row = mt * kBM + quarter * 32 + lane;
       int* flag = nullptr;
       if (EPI == EPI_ADD && U.splits > 1) {  // ordered split-K: wait for split s-1 on these rows
-        flag = p.split_flags + ((size_t)(nt * U.num_m * PAIR * MT + mt) * 4 + quarter);  // mt: this CTA's 128-row tile
+        flag = p.split_flags + ((size_t)(nt * U.num_m * PAIR + mt) * 4 + quarter);  // mt: this CTA's 128-row tile
         if (lane == 0)
           while (atomicAdd(flag, 0) != s) __nanosleep(64);
         __syncwarp();
@@ -739,22 +501,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) atomicExch(flag, s + 1 == U.splits ? 0 : s + 1);
       }
-      }  // m tiles of the group
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
         if constexpr (PAIR == 2) mbar_arrive_cluster(&tempty[acc], 0);
         else mbar_arrive(&tempty[acc]);
       }
-      if constexpr (EPI == EPI_PART && MT == 1) {  // (the accumulator is released first: the fixup reads no TMEM)
-        if (p.fixup && !p.streamk)
-          splitk_fixup<BN>(p, U.splits, U.num_n, U.num_m * PAIR, (w.mt * PAIR + rank), w.nt, quarter, lane, M);
-      }
     }
-  }
-  if constexpr (CSK) {
-    __syncwarp();
-    csk_epilogue<BN>(p, U, smem, tmem, warp, lane);
   }
   tc_fence_before();
   if constexpr (PAIR == 2) {
@@ -987,31 +741,13 @@ __global__ void __launch_bounds__(kSwThreads, 1)
 // h[row] += sum_s part[s][row] in split order (deterministic); with the fused
 // RMSNorm the bf16 row copy and 1/rms come out of the same pass.
 // one row of splitk_reduce_add_kernel
-__device__ __forceinline__ void splitk_reduce_row(const GemmArgs& p, int splits, int row, const Units& U,
-                                                  int G, const int* sk_tab) {
+__device__ __forceinline__ void splitk_reduce_row(const GemmArgs& p, int splits, int row) {
   const int n4 = p.N / 4;
   float ss = 0.f;
   float4* h = reinterpret_cast<float4*>(p.out_f32 + (size_t)row * p.ld_out);
   for (int c = threadIdx.x; c < n4; c += blockDim.x) {
     float4 acc;
-    if (p.streamk) {  // partials of the CTAs whose k-block ranges cover this tile, in CTA order
-      const int mt = row / kBM, nt = (4 * c) / p.bn;
-      const int t = mt + nt * U.num_m, tlo = t * U.kb_total, thi = tlo + U.kb_total;
-      int lo = 0, hi = G - 1;  // last CTA whose range starts at or before tlo (binary search)
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) / 2;
-        if (sk_tab[mid] <= tlo) lo = mid;
-        else hi = mid - 1;
-      }
-      acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int g = lo; g < G && sk_tab[g] < thi; ++g) {
-        if (sk_tab[g + 1] == sk_tab[g]) continue;  // empty range: no partial
-        const int slot = t - sk_tab[g] / U.kb_total;
-        const float4 v = __ldcg(reinterpret_cast<const float4*>(
-            p.ws_part + (((size_t)g * kSkSlots + slot) * kBM + row % kBM) * p.bn + (4 * c) % p.bn));
-        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-      }
-    } else {
+    {
       // up to 8 partials in flight at once, summed in split order
       acc = make_float4(0.f, 0.f, 0.f, 0.f);
       for (int s0 = 0; s0 < splits; s0 += 8) {
@@ -1052,18 +788,11 @@ __device__ __forceinline__ void splitk_reduce_row(const GemmArgs& p, int splits,
   }
 }
 
-__global__ void __launch_bounds__(256) splitk_reduce_add_kernel(const GemmArgs p, int splits, int G) {
+__global__ void __launch_bounds__(256) splitk_reduce_add_kernel(const GemmArgs p, int splits) {
   pdl_trigger();
   pdl_wait();
   const int M = p.rows_dev ? *p.rows_dev : p.rows_max;
-  const Units U = units_of<1>(p);
-  __shared__ int sk_tab[1025];  // stream-K range starts of the G CTAs (+ end)
-  if (p.streamk) {
-    for (int g = threadIdx.x; g <= G; g += blockDim.x) sk_tab[g] = (int)sk_lo(U, g, G);
-    __syncthreads();
-  }
-  for (int row = blockIdx.x; row < M; row += gridDim.x)
-    splitk_reduce_row(p, splits, row, U, G, sk_tab);
+  for (int row = blockIdx.x; row < M; row += gridDim.x) splitk_reduce_row(p, splits, row);
 }
 
 // ---------------------------------------------------------------------------
@@ -1325,31 +1054,17 @@ void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cuda
   RK_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
 }
 
-template <int BN, int EPI, int PAIR, bool CSK = false, int MT = 1, bool TF32 = false>
+template <int BN, int EPI, int PAIR, bool TF32 = false>
 void launch(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& p, int grid) {
-  using C = Cfg<BN, PAIR, MT>;
+  using C = Cfg<BN, PAIR>;
   static bool attr = false;
   if (!attr) {
-    RK_CUDA(cudaFuncSetAttribute(gemm_bf16_kernel<BN, EPI, PAIR, CSK, MT, TF32>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    RK_CUDA(cudaFuncSetAttribute(gemm_bf16_kernel<BN, EPI, PAIR, TF32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 C::SMEM));
     attr = true;
   }
-  if constexpr (CSK) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = C::SMEM;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = p.splits;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    RK_CUDA(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<BN, EPI, 1, true>, a, b, p));
-  } else if constexpr (PAIR == 1) {
-    launch_pdl(gemm_bf16_kernel<BN, EPI, 1, false, MT, TF32>, dim3(grid), dim3(kThreads), C::SMEM, st, a, b, p);
+  if constexpr (PAIR == 1) {
+    launch_pdl(gemm_bf16_kernel<BN, EPI, 1, TF32>, dim3(grid), dim3(kThreads), C::SMEM, st, a, b, p);
   } else {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
@@ -1365,79 +1080,32 @@ void launch(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const G
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
-    RK_CUDA(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<BN, EPI, 2, false, 1, TF32>, a, b, p));
+    RK_CUDA(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<BN, EPI, 2, TF32>, a, b, p));
+  }
+}
+
+template <int EPI, bool TF32>
+void launch_tiles(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& p, int grid) {
+  if (p.pair == 2) {
+    if (p.bn == 256) launch<256, EPI, 2, TF32>(st, a, b, p, grid);
+    else if (p.bn == 128) launch<128, EPI, 2, TF32>(st, a, b, p, grid);
+    else launch<64, EPI, 2, TF32>(st, a, b, p, grid);
+  } else {
+    if (p.bn == 256) launch<256, EPI, 1, TF32>(st, a, b, p, grid);
+    else if (p.bn == 128) launch<128, EPI, 1, TF32>(st, a, b, p, grid);
+    else launch<64, EPI, 1, TF32>(st, a, b, p, grid);
   }
 }
 
 template <int EPI>
 void launch_bn(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& p, int grid) {
   if constexpr (EPI == EPI_ADD || EPI == EPI_F32 || EPI == EPI_PART) {
-    if (p.tf32) {  // 3xTF32 mode: 1-CTA or pair tiles only
-      if (p.pair == 2) {
-        if (p.bn == 256) launch<256, EPI, 2, false, 1, true>(st, a, b, p, grid);
-        else if (p.bn == 128) launch<128, EPI, 2, false, 1, true>(st, a, b, p, grid);
-        else launch<64, EPI, 2, false, 1, true>(st, a, b, p, grid);
-      } else {
-        if (p.bn == 256) launch<256, EPI, 1, false, 1, true>(st, a, b, p, grid);
-        else if (p.bn == 128) launch<128, EPI, 1, false, 1, true>(st, a, b, p, grid);
-        else launch<64, EPI, 1, false, 1, true>(st, a, b, p, grid);
-      }
+    if (p.tf32) {  // 3xTF32 mode (kind::tf32)
+      launch_tiles<EPI, true>(st, a, b, p, grid);
       return;
     }
   }
-  if constexpr (EPI == EPI_ADD) {
-    if (p.csk) {
-      if (p.bn == 256) launch<256, EPI_ADD, 1, true>(st, a, b, p, grid);
-      else if (p.bn == 128) launch<128, EPI_ADD, 1, true>(st, a, b, p, grid);
-      else launch<64, EPI_ADD, 1, true>(st, a, b, p, grid);
-      return;
-    }
-  }
-  if (p.mt_group == 3) {
-    launch<128, EPI, 1, false, 3>(st, a, b, p, grid);
-    return;
-  }
-  if (p.mt_group == 2) {
-    launch<128, EPI, 1, false, 2>(st, a, b, p, grid);
-    return;
-  }
-  if (p.pair == 2) {
-    if (p.bn == 256) launch<256, EPI, 2>(st, a, b, p, grid);
-    else if (p.bn == 128) launch<128, EPI, 2>(st, a, b, p, grid);
-    else launch<64, EPI, 2>(st, a, b, p, grid);
-  } else {
-    if (p.bn == 256) launch<256, EPI, 1>(st, a, b, p, grid);
-    else if (p.bn == 128) launch<128, EPI, 1>(st, a, b, p, grid);
-    else launch<64, EPI, 1>(st, a, b, p, grid);
-  }
-}
-
-// Clusters of s CSK CTAs the GPU can hold at once.
-int csk_slots(int s) {
-  static int slots[9] = {-1, -1, -1, -1, -1, -1, -1, -1, -1};
-  if (s < 2 || s > 8) return 0;
-  if (slots[s] < 0) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(s * 64);
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = Cfg<256, 1>::SMEM;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = s;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    RK_CUDA(cudaFuncSetAttribute(gemm_bf16_kernel<256, EPI_ADD, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 Cfg<256, 1>::SMEM));
-    int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, gemm_bf16_kernel<256, EPI_ADD, 1, true>, &cfg) != cudaSuccess || n <= 0) {
-      cudaGetLastError();
-      n = 0;
-    }
-    slots[s] = n;
-  }
-  return slots[s];
+  launch_tiles<EPI, false>(st, a, b, p, grid);
 }
 
 // CTA pairs the GPU can hold at once (a GPC's odd SM cannot host a pair).
@@ -1517,18 +1185,11 @@ static double choose_config(GemmArgs& p, int sm_count, int rows_hint) {
     const char* v = std::getenv(name);
     return v ? std::atoi(v) : dflt;
   };
-  static const int pf_env = env("RK_GEMM_PREFETCH", 0);  // opt-in
-  p.prefetch = 0;
-  static const int pair_env = env("RK_GEMM_PAIR", 1), dbg_env = env("RK_GEMM_DBG", 0),
-                   csk_env = env("RK_GEMM_CSK", 0), mm_env = env("RK_GEMM_MM", 0),
-                   sk_env = env("RK_GEMM_STREAMK", 0);
+  static const int pair_env = env("RK_GEMM_PAIR", 1), dbg_env = env("RK_GEMM_DBG", 0);
   p.dbg = dbg_env;
   p.sms = sm_count;
   p.splits = 1;
   p.pair = 1;
-  p.mt_group = 1;
-  p.csk = 0;
-  p.streamk = 0;
   const int kb = p.K / kBK;
   auto ceil_div = [](long long a, long long b) { return (int)((a + b - 1) / b); };
   // us per k-block of one unit: the staged bytes at the L2->SM feed rate.
@@ -1582,20 +1243,7 @@ static double choose_config(GemmArgs& p, int sm_count, int rows_hint) {
   const bool residual_split = p.epi == EPI_ADD && p.split_flags;
   auto part_cost = [&](int s) { return s > 1 ? 3.0 + 2.0 * s * (double)rows_hint * p.N * 4 / 8e6 : 0.0; };
   auto split_ok = [&](int s) { return kb / s >= 4 && (s - 1) * ((kb + s - 1) / s) < kb; };
-  struct Choice {
-    int bn, splits, mt, csk, streamk;
-  } pick{-1, 1, 1, 0, 0};
-
-  // m-grouped tiles (short M): all ceil(M/128) m tiles in one CTA, BN = 128
-  const int mtc = ceil_div(p.rows_max, kBM);
-  if (mm_env && (mtc == 2 || mtc == 3) && p.N % 128 == 0 && p.epi != EPI_PART) {
-    const double t = t_kb(16 * mtc, 16);
-    for (int sp = 1; sp <= (residual_split ? 8 : 1); ++sp) {
-      if (sp > 1 && !split_ok(sp)) continue;
-      const double c = (double)ceil_div((long long)(p.N / 128) * sp, sm_count) * ((kb + sp - 1) / sp) * t + part_cost(sp);
-      if (c < best) { best = c; pick = {128, sp, mtc, 0, 0}; }
-    }
-  }
+  int pick_bn = -1, pick_splits = 1;
   // split-K over 1-CTA 128 x wide tiles
   if (residual_split) {
     const int wide = p.N % 256 == 0 ? 256 : (p.N % 128 == 0 ? 128 : 64);
@@ -1604,31 +1252,14 @@ static double choose_config(GemmArgs& p, int sm_count, int rows_hint) {
     for (int sp = 2; sp <= 8; ++sp) {
       if (!split_ok(sp)) continue;
       const double c = (double)ceil_div((long long)tiles1 * sp, sm_count) * ((kb + sp - 1) / sp) * t1 + part_cost(sp);
-      if (c < best) { best = c; pick = {wide, sp, 1, 0, 0}; }
-      const int cs = csk_env ? csk_slots(sp) : 0;
-      if (cs > 0) {
-        const double cc = (double)ceil_div(tiles1, cs) * ((kb + sp - 1) / sp) * t1 + 1.0;
-        if (cc < best) { best = cc; pick = {wide, sp, 1, 1, 0}; }
-      }
-    }
-    const int tiles_max = ceil_div(p.rows_max, kBM) * (p.N / wide);
-    if (sk_env && kb >= 2 && tiles_max <= 2 * sm_count) {  // stream-K (opt-in; slower at c2 shapes)
-      const double c = ((double)tiles1 * kb + sm_count - 1) / sm_count * t1 + 1.0 +
-                       2.0 * (tiles1 + sm_count) * (double)kBM * wide * 4 / 8e6;
-      if (c < best) { best = c; pick = {wide, 1, 1, 0, 1}; }
+      if (c < best) { best = c; pick_bn = wide; pick_splits = sp; }
     }
   }
-  // short M: each weight tile is read by few CTAs, straight from HBM, and the
-  // smem ring alone cannot cover the DRAM latency -> prefetch ahead into L2
-  if (pf_env > 0 && rows_hint <= 512) p.prefetch = pf_env;
-  if (pick.bn > 0) {
+  if (pick_bn > 0) {
     p.pair = 1;
-    p.bn = pick.bn;
-    p.splits = pick.splits;
-    p.mt_group = pick.mt;
-    p.csk = pick.csk;
-    p.streamk = pick.streamk;
-    if (pick.streamk || (pick.splits > 1 && !pick.csk)) p.epi = EPI_PART;
+    p.bn = pick_bn;
+    p.splits = pick_splits;
+    p.epi = EPI_PART;
   }
   return best;
 }
@@ -1672,9 +1303,6 @@ static bool choose_swap(GemmArgs& p, int sm_count, double other_us) {
   p.nc = nc;
   p.tc = tc;
   p.pair = 2;
-  p.mt_group = 1;
-  p.csk = 0;
-  p.streamk = 0;
   p.splits = best_s;
   p.bn = 256;
   if (p.epi == EPI_ADD) p.epi = EPI_PART;
@@ -1743,9 +1371,6 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
       // 3K of 1536, 8.7e-5 at 24576). So the 3K-long dot products are cut into
       // chunks of <= 48 k-blocks (1536 fp32) accumulated in TMEM, written as
       // split-K partials and summed on the CUDA cores (RN, split order).
-      p.mt_group = 1;
-      p.csk = 0;
-      p.streamk = 0;
       p.epi = epi0;
       const int kb = p.K / kBK;
       int sp = std::min(16, (kb + 47) / 48);
@@ -1792,9 +1417,6 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
         p.bn = o.bn;
         p.pair = o.pair;
         p.splits = (epi0 == EPI_ADD || epi0 == EPI_PART) ? o.splits : 1;
-        p.mt_group = 1;
-        p.csk = 0;
-        p.streamk = 0;
         p.epi = (o.splits > 1 && (epi0 == EPI_ADD || epi0 == EPI_PART)) ? EPI_PART : epi0;
       }
     }
@@ -1852,7 +1474,7 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
       case EPI_PART:
         go(gemm_swap_kernel<EPI_PART>);
         launch_pdl(splitk_reduce_add_kernel, dim3(std::min(p.rows_max, 8 * e->sm_count)), dim3(256), 0, e->stream, p,
-                   (int)p.splits, grid);
+                   (int)p.splits);
         e->launches += 1;
         break;
       default: go(gemm_swap_kernel<EPI_F32>); break;
@@ -1861,30 +1483,26 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
     return;
   }
   if (log)
-    std::fprintf(stderr, "[gemm] M=%d%s N=%d K=%d epi=%d -> bn=%d pair=%d mt=%d splits=%d csk=%d streamk=%d\n",
-                 p.rows_max, p.rows_dev ? "(dyn)" : "", p.N, p.K, p.epi, p.bn, p.pair, p.mt_group, p.splits, p.csk,
-                 p.streamk);
+    std::fprintf(stderr, "[gemm] M=%d%s N=%d K=%d epi=%d -> bn=%d pair=%d splits=%d tf32=%d\n", p.rows_max,
+                 p.rows_dev ? "(dyn)" : "", p.N, p.K, p.epi, p.bn, p.pair, p.splits, p.tf32);
   if (p.norm_part && p.N / p.bn > kNormSlots) raise(RK_ERR_INVALID_ARGUMENT, "fused RMSNorm: too many N tiles");
   CUtensorMap ta, tb;
   make_tmap_bf16(&ta, A, (uint64_t)p.rows_max, (uint64_t)p.K, kBM, (uint64_t)lda);
   make_tmap_bf16(&tb, B, (uint64_t)p.N, (uint64_t)p.K, (uint32_t)(p.bn / p.pair), (uint64_t)p.K);
-  const int num_m = p.mt_group > 1 ? 1 : (p.rows_max + kBM * p.pair - 1) / (kBM * p.pair);
+  const int num_m = (p.rows_max + kBM * p.pair - 1) / (kBM * p.pair);
   const int total = num_m * (p.N / p.bn) * p.splits;  // units (pair units for the pair kernel)
   const int slots = p.pair == 2 ? pair_slots(e->sm_count) : e->sm_count;
-  const int grid = p.csk ? total  // one tile per cluster of p.splits CTAs
-                   : p.streamk ? e->sm_count : p.pair * (total < slots ? total : slots);
+  const int grid = p.pair * (total < slots ? total : slots);
   if (p.epi == EPI_PART) {
-    e->scratch->gemm_ws.ensure(p.streamk ? (size_t)grid * kSkSlots * kBM * p.bn * 4
-                                         : (size_t)p.splits * p.rows_max * p.N * 4);
+    e->scratch->gemm_ws.ensure((size_t)p.splits * p.rows_max * p.N * 4);
     p.ws_part = e->scratch->gemm_ws.as<float>();
   }
   static const char* kEpi[] = {"qkv", "add", "silu", "f32", "addsplit"};
   ProfScope ps(e, (e->prof && e->prof->on)
                       ? intern(std::string("gemm_") + kEpi[p.epi] + "_m" + std::to_string(p.rows_max) +
                                (p.rows_dev ? "dyn" : "") + "_n" + std::to_string(p.N) + "_k" + std::to_string(p.K) +
-                               "_bn" + std::to_string(p.bn) + (p.streamk ? std::string("_sk") : "_s" + std::to_string(p.splits)) +
-                               (p.pair == 2 ? "_pair" : "") + (p.csk ? "_csk" : "") +
-                               (p.mt_group > 1 ? "_mt" + std::to_string(p.mt_group) : ""))
+                               "_bn" + std::to_string(p.bn) + "_s" + std::to_string(p.splits) +
+                               (p.pair == 2 ? "_pair" : "") + (p.tf32 ? "_tf32" : ""))
                       : "gemm",
                0, 0);
   ps.rec.kind = 1;
@@ -1896,24 +1514,12 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
     case EPI_QKV: launch_bn<EPI_QKV>(e->stream, ta, tb, p, grid); break;
     case EPI_ADD: launch_bn<EPI_ADD>(e->stream, ta, tb, p, grid); break;
     case EPI_SILU: launch_bn<EPI_SILU>(e->stream, ta, tb, p, grid); break;
-    case EPI_PART: {
-      // partials reduced by splitk_reduce_add_kernel (RK_GEMM_FIXUP=1: by the
-      // last split of each row group inside the GEMM -- measured slower, r02k:
-      // c2 sparse W_down 113 us vs 66 us with the reduce launch, because the
-      // fixup warps hold up the next tile's epilogue)
-      static const bool fixup_env = [] {
-        const char* v = std::getenv("RK_GEMM_FIXUP");
-        return v ? std::atoi(v) != 0 : false;
-      }();
-      p.fixup = fixup_env && !p.streamk && p.split_flags && p.mt_group == 1 && p.pair == 1;
+    case EPI_PART:  // partials, then splitk_reduce_add_kernel sums them in split order
       launch_bn<EPI_PART>(e->stream, ta, tb, p, grid);
-      if (!p.fixup) {
-        launch_pdl(splitk_reduce_add_kernel, dim3(std::min(p.rows_max, 8 * e->sm_count)), dim3(256), 0, e->stream, p,
-                   (int)p.splits, grid);
-        e->launches += 1;
-      }
+      launch_pdl(splitk_reduce_add_kernel, dim3(std::min(p.rows_max, 8 * e->sm_count)), dim3(256), 0, e->stream, p,
+                 (int)p.splits);
+      e->launches += 1;
       break;
-    }
     default: launch_bn<EPI_F32>(e->stream, ta, tb, p, grid); break;
   }
   e->launches += 1;

@@ -19,9 +19,6 @@ struct GemmArgs {
   int bn = 128, splits = 1;     // chosen by gemm_bf16 (splits re-chosen on the device for live rows)
   int sms = 148;
   int dbg = 0;                  // experiments (RK_GEMM_DBG): 1 = every k-block loads tile (0,0), 2 = no MMAs
-  int csk = 0;                  // 1: split-K inside a cluster of `splits` CTAs, reduced over DSMEM
-  int prefetch = 0;             // k-blocks of B (weights) prefetched into L2 ahead of the smem ring
-  int mt_group = 1;             // 2/3: one CTA computes all m tiles of an N tile (M <= 128*mt_group)
   int pair = 1;                 // 2: CTA-pair kernel (256-row tiles, cta_group::2), chosen by gemm_bf16
   // swap-AB (short static M): the weights are the MMA's M side (256 rows per
   // CTA pair), the M tokens its N side in nc chunks of tc (<= 256) columns
@@ -60,9 +57,7 @@ struct GemmArgs {
   float* norm_inv = nullptr;    // [rows_max]
   int* norm_cnt = nullptr;      // [m tiles * 4], zero-initialised, self-resetting
   float norm_eps = 1e-5f;
-  float* ws_part = nullptr;  // EPI_PART workspace [splits][rows_max][N], or stream-K [grid*2][128][bn]
-  int streamk = 0;           // EPI_PART: stream-K work split (set by gemm_bf16)
-  int fixup = 0;             // EPI_PART: the last split of each row group reduces in the GEMM (no reduce kernel)
+  float* ws_part = nullptr;  // EPI_PART workspace [splits][rows_max][N]
   // ensure_finite (tensor.cpp:58-64, after every matmul): any non-finite
   // product value sets status[0] (engine status flags, set by gemm_bf16);
   // the call then fails with RK_ERR_NONFINITE ("matmul: non-finite value")

@@ -206,37 +206,6 @@ def test_select_certified_threshold(engine, case):
         assert dinfo[0] == thr, (dinfo[0], thr)
 
 
-@pytest.mark.parametrize("shape", [(40, 512, 4096), (320, 2048, 8192), (1356, 2048, 2048)])
-def test_gemm_residual_streamk(engine, shape):
-    """The opt-in stream-K residual path (RK_GEMM_STREAMK=1) in a subprocess:
-    deterministic and equal to the reference within bf16-operand tolerance."""
-    import os
-    import subprocess
-    import sys
-    code = f"""
-import numpy as np, sys
-sys.path.insert(0, {os.getcwd()!r})
-from paper_2603_13289_b200.engine import Engine
-from tests.test_gpu_kernels import run_gemm, bf16_round
-e = Engine(0)
-M, N, K = {shape}
-rng = np.random.default_rng(4)
-A = rng.standard_normal((M, K)).astype(np.float32)
-B = (rng.standard_normal((N, K)) / np.sqrt(K)).astype(np.float32)
-H = rng.standard_normal((M, N)).astype(np.float32)
-got = run_gemm(e, A, B, H, M, 1)
-again = run_gemm(e, A, B, H, M, 1)
-assert np.array_equal(got.view(np.uint32), again.view(np.uint32))
-ref = H + bf16_round(A).astype(np.float64) @ bf16_round(B).astype(np.float64).T
-err = np.abs(got - ref).max() / np.abs(ref).max()
-assert err < 2e-5, err
-print("ok")
-"""
-    env = dict(os.environ, RK_GEMM_STREAMK="1", RK_GEMM_PAIR="0")  # stream-K is a 1-CTA-kernel mode
-    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
-    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
-
-
 def test_gemm_single_cta_kernel():
     """The 1-CTA GEMM kernel (RK_GEMM_PAIR=0; the default uses CTA pairs for
     M > 128) on the store / residual / live-row shapes, in a subprocess."""
@@ -264,42 +233,6 @@ print("ok")
     env = dict(os.environ, RK_GEMM_PAIR="0")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
-
-
-@pytest.mark.parametrize("shape", [(320, 2048, 8192), (1356, 2048, 2048), (40, 512, 4096), (320, 4096, 14336)])
-def test_gemm_cluster_split_k_matches_global_split_k(engine, shape, tmp_path):
-    """Split-K reduced inside a cluster over DSMEM (opt-in RK_GEMM_CSK=1,
-    subprocess) and the global-partials split-K path (default) both match the
-    fp64 reference; each is deterministic. (Their split counts may differ, so
-    their bits may too; with equal splits the summation order is the same.)"""
-    import os
-    import subprocess
-    import sys
-    M, N, K = shape
-    rng = np.random.default_rng(11)
-    A = rng.standard_normal((M, K)).astype(np.float32)
-    B = (rng.standard_normal((N, K)) / np.sqrt(K)).astype(np.float32)
-    H = rng.standard_normal((M, N)).astype(np.float32)
-    np.savez(tmp_path / "in.npz", A=A, B=B, H=H)
-    got = run_gemm(engine, A, B, H, M, 1)
-    code = f"""
-import numpy as np, sys
-sys.path.insert(0, {os.getcwd()!r})
-from paper_2603_13289_b200.engine import Engine
-from tests.test_gpu_kernels import run_gemm
-e = Engine(0)
-d = np.load({str(tmp_path / "in.npz")!r})
-np.save({str(tmp_path / "out.npy")!r}, run_gemm(e, d["A"], d["B"], d["H"], {M}, 1))
-"""
-    env = dict(os.environ, RK_GEMM_CSK="1")
-    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
-    assert r.returncode == 0, r.stdout + r.stderr
-    want = np.load(tmp_path / "out.npy")
-    again = run_gemm(engine, A, B, H, M, 1)
-    assert np.array_equal(got.view(np.uint32), again.view(np.uint32)), "split-K not deterministic"
-    ref = H + bf16_round(A).astype(np.float64) @ bf16_round(B).astype(np.float64).T
-    assert np.abs(got - ref).max() / np.abs(ref).max() < 2e-5
-    assert np.abs(want - ref).max() / np.abs(ref).max() < 2e-5
 
 
 @pytest.mark.parametrize("shape", [(1, 2048, 8192), (1, 4096, 14336), (1, 64, 64)])
@@ -378,37 +311,3 @@ def test_select_topk_radix(engine, case):
                                       idx.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(cnt)))
     assert cnt.value == len(want)
     assert np.array_equal(idx[:cnt.value], want)
-
-
-@pytest.mark.parametrize("shape", [(1360, 2048, 8192), (320, 2048, 8192), (40, 512, 4096)])
-def test_gemm_split_k_fixup_equals_reduce_kernel(engine, shape, tmp_path):
-    """Split-K residual GEMMs: the separate reduce kernel (default) and the
-    opt-in in-GEMM fixup (RK_GEMM_FIXUP=1, subprocess: the last split of each
-    row group sums the partials) add the same partials in the same split
-    order, so the residual rows are bit-identical; both match fp64."""
-    import os
-    import subprocess
-    import sys
-    M, N, K = shape
-    rng = np.random.default_rng(17)
-    A = rng.standard_normal((M, K)).astype(np.float32)
-    B = (rng.standard_normal((N, K)) / np.sqrt(K)).astype(np.float32)
-    H = rng.standard_normal((M, N)).astype(np.float32)
-    np.savez(tmp_path / "in.npz", A=A, B=B, H=H)
-    got = run_gemm(engine, A, B, H, M, 1)
-    code = f"""
-import numpy as np, sys
-sys.path.insert(0, {os.getcwd()!r})
-from paper_2603_13289_b200.engine import Engine
-from tests.test_gpu_kernels import run_gemm
-e = Engine(0)
-d = np.load({str(tmp_path / "in.npz")!r})
-np.save({str(tmp_path / "out.npy")!r}, run_gemm(e, d["A"], d["B"], d["H"], {M}, 1))
-"""
-    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, RK_GEMM_FIXUP="1"), capture_output=True,
-                       text=True, timeout=300)
-    assert r.returncode == 0, r.stdout + r.stderr
-    want = np.load(tmp_path / "out.npy")
-    assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), "reduce kernel != in-GEMM fixup"
-    ref = H + bf16_round(A).astype(np.float64) @ bf16_round(B).astype(np.float64).T
-    assert np.abs(got - ref).max() / np.abs(ref).max() < 2e-5
