@@ -139,6 +139,12 @@ __device__ __forceinline__ void tile_rows(const AttnArgs& a, int M, int tile, in
   r0 = r1 = 0;
 }
 
+// Query tiles of the live rows (tile_rows numbering).
+__device__ __forceinline__ int live_tiles(const AttnArgs& a, int M) {
+  const int g1 = min(a.g1, M), g2 = min(max(a.g2, g1), M), rq = a.rq;
+  return (g1 + rq - 1) / rq + (M - g2 + rq - 1) / rq + (g2 - g1 + rq - 1) / rq;
+}
+
 // 3-input max (FMNMX3 on sm_100): two new values per instruction
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float d;
@@ -217,12 +223,16 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
   pdl_trigger();
   pdl_wait();  // rows_dev / positions / Q of the previous kernel
   const int M = a.rows_dev ? *a.rows_dev : a.rows_max;
-  // grid (split part, head, tile) with tiles in reverse order: the CTAs of the
-  // latest (longest) query tiles of every head dispatch first, all parts of a
-  // tile together
+  // grid (split part, head, tile) with the LIVE tiles in reverse order: the
+  // CTAs of the latest (longest) query tiles of every head dispatch first, all
+  // parts of a tile together; grid slots past the live tile count (sparse
+  // passes size the grid for rows_max) come last and exit at once instead of
+  // occupying the first waves
+  const int nlive = live_tiles(a, M);
+  if ((int)blockIdx.z >= nlive) return;
   int r0, r1;
-  tile_rows(a, M, (int)gridDim.z - 1 - (int)blockIdx.z, r0, r1);
-  if (r1 <= r0) return;  // no rows (tiles past the live count)
+  tile_rows(a, M, nlive - 1 - (int)blockIdx.z, r0, r1);
+  if (r1 <= r0) return;
   if (threadIdx.x == 0) {
     if (smem_u32(smem) & 1023) __trap();  // SW128 tiles need a 1 KB aligned base
     *s_kmax = -1;
