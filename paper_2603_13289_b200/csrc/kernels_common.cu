@@ -1394,6 +1394,15 @@ __global__ void gather_rows_to_kernel(float* H, const int* off, const float* src
   sm100::pdl_trigger();
   sm100::pdl_wait();
   const int rows = *count, o = *off;
+  if ((d & 3) == 0) {  // 16-byte vectors, 32-bit index math
+    const int d4 = d / 4, total = rows * d4;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+      const int r = i / d4, c = i - r * d4, j = idx[r];
+      reinterpret_cast<float4*>(H + (size_t)(o + r) * d)[c] = reinterpret_cast<const float4*>(src + (size_t)j * d)[c];
+      if (c == 0) pos[o + r] = base + j;
+    }
+    return;
+  }
   const size_t total = (size_t)rows * d;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
     const size_t r = i / d, c = i % d;
@@ -1407,6 +1416,15 @@ __global__ void scatter_rows_from_kernel(float* dst, const float* H, const int* 
   sm100::pdl_trigger();
   sm100::pdl_wait();
   const int rows = *count, o = *off;
+  if ((d & 3) == 0) {
+    const int d4 = d / 4, total = rows * d4;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+      const int r = i / d4, c = i - r * d4, j = idx[r];
+      reinterpret_cast<float4*>(dst + (size_t)j * d)[c] = reinterpret_cast<const float4*>(H + (size_t)(o + r) * d)[c];
+      if (c == 0) depth[j] = value;
+    }
+    return;
+  }
   const size_t total = (size_t)rows * d;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
     const size_t r = i / d, c = i % d;
@@ -1422,12 +1440,12 @@ void segment_offsets(cudaStream_t s, const SegCounts& c, int U, int start, int* 
 }
 void gather_rows_to(cudaStream_t s, float* H, const int* off, const float* src, const int* idx, const int* count,
                     int rows_max, int d, int* pos, int base) {
-  const size_t total = (size_t)rows_max * d;
+  const size_t total = (size_t)rows_max * d / (d % 4 ? 1 : 4);
   launch_pdl(gather_rows_to_kernel, dim3(blocks_for(total) < 4096 ? blocks_for(total) : 4096), dim3(kThreads), 0, s, H, off, src, idx, count, d, pos, base);
 }
 void scatter_rows_from(cudaStream_t s, float* dst, const float* H, const int* off, const int* idx, const int* count,
                        int rows_max, int d, uint64_t* depth, uint64_t value) {
-  const size_t total = (size_t)rows_max * d;
+  const size_t total = (size_t)rows_max * d / (d % 4 ? 1 : 4);
   launch_pdl(scatter_rows_from_kernel, dim3(blocks_for(total) < 4096 ? blocks_for(total) : 4096), dim3(kThreads), 0, s, dst, H, off, idx, count, d, depth, value);
 }
 }  // namespace k
