@@ -34,6 +34,10 @@ int rk_debug_bench_attention_rows(rk_engine* e, const int32_t* pos, int M, int l
  * the band case: out[3 roles][64 steps][8 events] (see attn_sm100.cu). */
 int rk_debug_trace_attention(rk_engine* e, int M, int T, int H, int Hkv, int dh, unsigned long long* out);
 int rk_debug_bench_gemm(rk_engine* e, int M, int N, int K, int epi, int iters, float* ms);
+/* clock64 timeline of CTA 0 of one GEMM: out[3][512] (role 0: producer, per
+ * k-block slot acquired; 1: MMA issuer, per k-block stage full; 2: epilogue,
+ * per unit accumulator ready / drained). */
+int rk_debug_trace_gemm(rk_engine* e, int M, int N, int K, int epi, unsigned long long* out);
 /* K2b selection (select_relay) on host-given scores: sorted indices + tags,
  * count, dinfo = {exact threshold, min relative margin}. */
 int rk_debug_select_relay(rk_engine* e, const double* s_dev, const float* influence, double infl_mean, int n,

@@ -250,6 +250,28 @@ int rk_debug_bench_gemm(rk_engine* e, int M, int N, int K, int epi, int iters, f
     g.out_bf16 = reinterpret_cast<__nv_bfloat16*>(c.p);
     g.ld_bf16 = N / 2;
     g.split_flags = flags.as<int>();
+    // epi 0: the real QKV epilogue (c2-like heads: d_head 64, kv 512): 1/rms row
+    // scale, RoPE on Q/K, Q as bf16, K/V scattered into a context at positions 0..M-1
+    DevBuf pos, ctxk, ctxv, rs;
+    if (epi == EPI_QKV) {
+      const int dh = 64, kv = 512;
+      pos.alloc((size_t)M * 4);
+      k::iota_positions(st, pos.as<int>(), M, 0);
+      ctxk.alloc((size_t)M * kv * 2);
+      ctxv.alloc((size_t)M * kv * 2);
+      rs.alloc((size_t)M * 4);
+      k::fill(st, rs.as<float>(), M, 1.0f);
+      g.pos = pos.as<int>();
+      g.rope = rope_table(e, 10000.0f, dh, (uint64_t)M)->csf.as<float2>();
+      g.dh = dh;
+      g.kv = kv;
+      g.q = N - 2 * kv;
+      g.ctx_k = ctxk.as<__nv_bfloat16>();
+      g.ctx_v = ctxv.as<__nv_bfloat16>();
+      g.commit = 1;
+      g.row_scale = rs.as<float>();
+      g.ld_bf16 = g.q;
+    }
     gemm_bf16(e, a.as<__nv_bfloat16>(), K, b.as<__nv_bfloat16>(), g, M);
     cudaEvent_t e0, e1;
     RK_CUDA(cudaEventCreate(&e0));
@@ -264,6 +286,37 @@ int rk_debug_bench_gemm(rk_engine* e, int M, int N, int K, int epi, int iters, f
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     RK_CUDA(cudaGetLastError());
+  });
+}
+
+int rk_debug_trace_gemm(rk_engine* e, int M, int N, int K, int epi, unsigned long long* out) {
+  return guard([&] {
+    cudaStream_t st = e->stream;
+    DevBuf f((size_t)(M > N ? M : N) * K * 4), a((size_t)M * K * 2), b((size_t)N * K * 2), c((size_t)M * N * 4),
+        flags(1 << 18), tr(3 * 512 * 8);
+    k::init_uniform(st, f.as<float>(), (size_t)M * K, 21, 1.0f);
+    k::f32_to_bf16(st, a.as<__nv_bfloat16>(), f.as<float>(), (size_t)M * K);
+    k::init_uniform(st, f.as<float>(), (size_t)N * K, 22, 0.02f);
+    k::f32_to_bf16(st, b.as<__nv_bfloat16>(), f.as<float>(), (size_t)N * K);
+    RK_CUDA(cudaMemsetAsync(c.p, 0, c.bytes, st));
+    RK_CUDA(cudaMemsetAsync(flags.p, 0, flags.bytes, st));
+    RK_CUDA(cudaMemsetAsync(tr.p, 0, tr.bytes, st));
+    GemmArgs g;
+    g.rows_max = M;
+    g.N = N;
+    g.K = K;
+    g.epi = epi;
+    g.out_f32 = c.as<float>();
+    g.ld_out = N;
+    g.out_bf16 = reinterpret_cast<__nv_bfloat16*>(c.p);
+    g.ld_bf16 = N / 2;
+    g.split_flags = flags.as<int>();
+    gemm_bf16(e, a.as<__nv_bfloat16>(), K, b.as<__nv_bfloat16>(), g, M);  // warm
+    g.trace = tr.as<unsigned long long>();
+    gemm_bf16(e, a.as<__nv_bfloat16>(), K, b.as<__nv_bfloat16>(), g, M);
+    RK_CUDA(cudaStreamSynchronize(st));
+    RK_CUDA(cudaGetLastError());
+    RK_CUDA(cudaMemcpy(out, tr.p, tr.bytes, cudaMemcpyDeviceToHost));
   });
 }
 

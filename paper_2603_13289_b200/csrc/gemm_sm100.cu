@@ -60,6 +60,14 @@ __device__ __forceinline__ void flag_nonfinite(int* status, float acc) {
   if (acc != acc && status) *reinterpret_cast<volatile int*>(status) = 1;
 }
 constexpr int kThreads = 192;
+// debug timeline (GemmArgs::trace, rk_debug_trace_gemm): CTA 0 only;
+// role 0 producer (per k-block: empty slot acquired), role 1 MMA issuer (per
+// k-block: stage full), role 2 epilogue warp 2 (per unit: 2u accumulator
+// ready, 2u+1 drained)
+#define GTRACE(role, i, cond)                                                                  \
+  do {                                                                                         \
+    if (p.trace && blockIdx.x == 0 && (cond) && (i) < 512) p.trace[(role) * 512 + (i)] = clock64(); \
+  } while (0)
 
 // PAIR = 2: a CTA pair (cluster of 2, tcgen05 cta_group::2) computes a
 // 256 x BN tile; each CTA stages its own 128 rows of A and HALF of the BN rows
@@ -213,6 +221,33 @@ __device__ __forceinline__ void epilogue_chunk(const GemmArgs& p, int row, int c
   }
 }
 
+// Coalesced epilogue stores: a warp's 32 rows (thread = row, the TMEM lane
+// layout) are transposed through a per-warp 4 KB shared tile so that each
+// store instruction covers whole row segments -- 8 lanes per 128-byte fp32
+// segment -- instead of 32 rows x 16 B (r02af trace: the per-row stores made
+// the fp32 epilogue of a 256-column pair tile take ~16k cycles and stalled
+// the next tile's mainloop; F32 band-shape GEMM 49 -> 42 us). (For the bf16
+// QKV / SiLU outputs the extra shared-memory traffic competes with the next
+// tile's MMAs and measured slower -- r02ag -- so they store per row.)
+// dst(rl) returns the destination of local row rl's segment (nullptr: skip).
+template <class Dst>
+__device__ __forceinline__ void stage_store128(uint8_t* T, int lane, const float (&v)[32], Dst dst) {
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    *reinterpret_cast<uint4*>(T + lane * 128 + ((j ^ (lane & 7)) * 16)) =
+        make_uint4(__float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]), __float_as_uint(v[4 * j + 2]),
+                   __float_as_uint(v[4 * j + 3]));
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int rl = 4 * i + (lane >> 3), ch = lane & 7;
+    const uint4 x = *reinterpret_cast<const uint4*>(T + rl * 128 + ((ch ^ (rl & 7)) * 16));
+    uint4* d = dst(rl);
+    if (d) d[ch] = x;
+  }
+}
+
 template <int BN, int EPI, int PAIR, bool TF32 = false>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -284,11 +319,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       Work w;
+      int kbn = 0;  // (trace index)
       for (int it = 0; get_work<PAIR>(U, it, w); ++it) {
         const int mt = w.mt, nt = w.nt, kb0 = w.kb0, kb1 = w.kb1;
-        for (int kb = kb0; kb < kb1; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb, ++kbn) {
           const bool early = it == 0 && kb - kb0 < pre;  // stage armed, its B already in flight
           if (!early) mbar_wait(&empty[stage], phase ^ 1);
+          GTRACE(0, kbn, true);
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
           const bool same = p.dbg & 1;
           const int kx = same ? 0 : kb * kBK, am = same ? 0 : mt, bn_ = same ? 0 : nt;
@@ -311,7 +348,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t idesc = TF32 ? idesc_tf32(kBM * PAIR, BN) : idesc_bf16(kBM * PAIR, BN);
       int stage = 0;
       uint32_t phase = 0;
-      int local = 0;
+      int local = 0, kbm = 0;
       Work w;
       for (int it = 0; get_work<PAIR>(U, it, w); ++it, ++local) {
         const int kb0 = w.kb0, kb1 = w.kb1;
@@ -319,8 +356,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&tempty[acc], ((local / C::NACC) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * BN;
-        for (int kb = kb0; kb < kb1; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb, ++kbm) {
           mbar_wait(&full[stage], phase);
+          GTRACE(1, kbm, true);
           tc_fence_after();
           const uint32_t a0 = smem_u32(smem + stage * C::STAGE_BYTES);
           const uint32_t b0 = a0 + C::A_BYTES;
@@ -388,6 +426,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int i = 0; i < 8; ++i) hb[i] = (row0 + 4 * i + sub < M) ? __ldcg(hptr(i, 0)) : make_float4(0.f, 0.f, 0.f, 0.f);
         mbar_wait(&tfull[acc], use & 1);
+        GTRACE(2, 2 * local, warp == 2 && lane == 0);
         tc_fence_after();
         float ss[8];
 #pragma unroll
@@ -462,37 +501,84 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       } else {
         mbar_wait(&tfull[acc], use & 1);
+        GTRACE(2, 2 * local, warp == 2 && lane == 0);
         tc_fence_after();
         const float rs = (p.row_scale && row < M) ? p.row_scale[row] : 1.0f;
+        uint8_t* T = epi_stage + quarter * 4096;
+        const int row0 = mt * kBM + quarter * 32;  // the warp's first row
         if constexpr (EPI == EPI_QKV) {
-          // RoPE {cos, sin} of this row's position for the next chunk are
-          // loaded while the current chunk computes (one exposed L2 latency
-          // per tile instead of one per 32 columns)
           const int pos = row < M ? p.pos[row] : 0;
           const float2* csrow = p.rope + (size_t)pos * (p.dh / 2);
-          float2 cur[16], nxt[16];
+          if (p.dh == 64) {
+            // the row's whole RoPE {cos, sin} row (32 pairs, 256 B) once per
+            // tile as 16-byte loads; every head of the tile reuses it (chunks
+            // c and c+32 of a head take its two halves)
+            float2 cs[32];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) cur[j] = csrow[((nt * BN) % p.dh) / 2 + j];
-#pragma unroll 1
-          for (int c = 0; c < BN; c += 32) {
-            if (c + 32 < BN) {
-#pragma unroll
-              for (int j = 0; j < 16; ++j) nxt[j] = csrow[((nt * BN + c + 32) % p.dh) / 2 + j];
+            for (int j = 0; j < 16; ++j) {
+              const float4 t = reinterpret_cast<const float4*>(csrow)[j];
+              cs[2 * j] = make_float2(t.x, t.y);
+              cs[2 * j + 1] = make_float2(t.z, t.w);
             }
-            uint32_t r[32];
-            tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + acol + c, r);
-            tmem_ld_wait();
-            if (row < M) epilogue_chunk<EPI>(p, row, nt * BN + c, r, rs, s, cur, pos);
+#pragma unroll 1
+            for (int c = 0; c < BN; c += 64) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) cur[j] = nxt[j];
+              for (int hh = 0; hh < 2; ++hh) {
+                uint32_t r[32];
+                tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + acol + c + 32 * hh, r);
+                tmem_ld_wait();
+                if (row < M) epilogue_chunk<EPI>(p, row, nt * BN + c + 32 * hh, r, rs, s, cs + 16 * hh, pos);
+              }
+            }
+          } else {
+            // RoPE {cos, sin} of the next chunk load while the current one computes
+            float2 cur[16], nxt[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) cur[j] = csrow[((nt * BN) % p.dh) / 2 + j];
+#pragma unroll 1
+            for (int c = 0; c < BN; c += 32) {
+              if (c + 32 < BN) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) nxt[j] = csrow[((nt * BN + c + 32) % p.dh) / 2 + j];
+              }
+              uint32_t r[32];
+              tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + acol + c, r);
+              tmem_ld_wait();
+              if (row < M) epilogue_chunk<EPI>(p, row, nt * BN + c, r, rs, s, cur, pos);
+#pragma unroll
+              for (int j = 0; j < 16; ++j) cur[j] = nxt[j];
+            }
           }
-        } else {
+        } else if constexpr (EPI == EPI_SILU) {
 #pragma unroll 1
           for (int c = 0; c < BN; c += 32) {
             uint32_t r[32];
             tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + acol + c, r);
             tmem_ld_wait();
             if (row < M) epilogue_chunk<EPI>(p, row, nt * BN + c, r, rs, s);
+          }
+        } else {  // EPI_F32 / EPI_PART: 128-byte fp32 segments
+#pragma unroll 1
+          for (int c = 0; c < BN; c += 32) {
+            uint32_t r[32];
+            tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + acol + c, r);
+            tmem_ld_wait();
+            float v[32];
+            float chk = 0.f;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              v[j] = __uint_as_float(r[j]) * rs;
+              chk = finite_acc(chk, v[j]);
+            }
+            if (row < M) flag_nonfinite(p.status, chk);
+            const int col = nt * BN + c;
+            stage_store128(T, lane, v, [&](int rl) -> uint4* {
+              const int rr = row0 + rl;
+              if (rr >= M) return nullptr;
+              float* base = EPI != EPI_PART ? p.out_f32 + (size_t)rr * p.ld_out + col
+                                            : p.ws_part + ((size_t)s * p.rows_max + rr) * p.N + col;
+              return reinterpret_cast<uint4*>(base);
+            });
           }
         }
       }
@@ -504,6 +590,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
+      GTRACE(2, 2 * local + 1, warp == 2 && lane == 0);
       if (lane == 0) {
         if constexpr (PAIR == 2) mbar_arrive_cluster(&tempty[acc], 0);
         else mbar_arrive(&tempty[acc]);

@@ -19,6 +19,7 @@ struct GemmArgs {
   int bn = 128, splits = 1;     // chosen by gemm_bf16 (splits re-chosen on the device for live rows)
   int sms = 148;
   int dbg = 0;                  // experiments (RK_GEMM_DBG): 1 = every k-block loads tile (0,0), 2 = no MMAs
+  unsigned long long* trace = nullptr;  // debug: clock64 timeline of CTA 0 ([role 0..2][event < 512])
   int pair = 1;                 // 2: CTA-pair kernel (256-row tiles, cta_group::2), chosen by gemm_bf16
   // swap-AB (short static M): the weights are the MMA's M side (256 rows per
   // CTA pair), the M tokens its N side in nc chunks of tc (<= 256) columns
