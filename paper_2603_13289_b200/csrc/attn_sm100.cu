@@ -499,13 +499,13 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
       }
       reinterpret_cast<float2*>(a.ws_ml)[blk + rl] = make_float2(valid ? m_run : -INFINITY, l_run);
       int* s_last = reinterpret_cast<int*>(bar + 15);
-      __threadfence();
+      fence_acq_rel_gpu();  // (release: this part's partials)
       named_bar_sync(1, 128);
       int* cnt = a.tile_cnt + tid;
       if (rl == 0) *s_last = atomicAdd(cnt, 1) == ts_eff - 1;
       named_bar_sync(1, 128);
       if (*s_last) {
-        __threadfence();
+        fence_acq_rel_gpu();  // (acquire: every part's partials)
         if (rl == 0) *cnt = 0;  // self-resetting for the next launch
         // per-lane part weights 2^(m_z - m) / l into smem (the K ring is idle now)
         float* wsm = reinterpret_cast<float*>(smem + C::OFF_K);  // [lane][16]

@@ -250,6 +250,20 @@ int rk_debug_bench_gemm(rk_engine* e, int M, int N, int K, int epi, int iters, f
     g.out_bf16 = reinterpret_cast<__nv_bfloat16*>(c.p);
     g.ld_bf16 = N / 2;
     g.split_flags = flags.as<int>();
+    // RK_BENCH_NORM=1 (residual epi): the fused RMSNorm producer of the layer
+    // pass (bf16 row copy, per-tile sums of squares, last tile writes 1/rms)
+    DevBuf nbf, npart, ninv, ncnt;
+    if (epi == EPI_ADD && std::getenv("RK_BENCH_NORM")) {
+      nbf.alloc((size_t)M * N * 2);
+      npart.alloc((size_t)M * kNormSlots * 4 + 256);
+      ninv.alloc((size_t)M * 4 + 256);
+      ncnt.alloc(((size_t)(M + 127) / 128 * 8 + 64) * 4);
+      RK_CUDA(cudaMemsetAsync(ncnt.p, 0, ncnt.bytes, st));
+      g.norm_bf16 = nbf.as<__nv_bfloat16>();
+      g.norm_part = npart.as<float>();
+      g.norm_inv = ninv.as<float>();
+      g.norm_cnt = ncnt.as<int>();
+    }
     // epi 0: the real QKV epilogue (c2-like heads: d_head 64, kv 512): 1/rms row
     // scale, RoPE on Q/K, Q as bf16, K/V scattered into a context at positions 0..M-1
     DevBuf pos, ctxk, ctxv, rs;

@@ -275,6 +275,10 @@ __device__ __forceinline__ bool elect_one() {
   return pred != 0;
 }
 
+// GPU-scope acquire/release fence: with a relaxed atomic it forms the
+// release (writer) / acquire (last arriver) halves of a ticket handoff --
+// lighter than __threadfence()'s sequentially consistent fence.
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }

@@ -28,7 +28,8 @@ if __name__ == "__main__":
             ms, tf = attn(e, *case)
             print(f"attn M={case[0]} T={case[1]} H={case[2]} Hkv={case[3]} dh={case[4]}: {ms * 1e3:.1f} us  {tf:.1f} TFLOP/s", flush=True)
     if which in ("all", "gemm"):
-        for case in [(4032, 3072, 2048, 0), (320, 3072, 2048, 0), (1356, 3072, 2048, 0),
+        for case in [(4032, 2048, 2048, 1), (1356, 2048, 2048, 1), (320, 2048, 2048, 1), (1356, 2048, 8192, 1),
+                     (4032, 3072, 2048, 0), (320, 3072, 2048, 0), (1356, 3072, 2048, 0),
                      (4032, 16384, 2048, 2), (4032, 2048, 8192, 1), (4032, 3072, 2048, 3), (320, 16384, 2048, 2),
                      (320, 2048, 8192, 1), (320, 3072, 2048, 3), (1356, 2048, 2048, 1), (8192, 8192, 8192, 3)]:
             ms, tf = gemm(e, *case)
