@@ -849,8 +849,18 @@ __device__ __forceinline__ void splitk_reduce_row(const GemmArgs& p, int splits,
   float4* h = reinterpret_cast<float4*>(p.out_f32 + (size_t)row * p.ld_out);
   for (int c = threadIdx.x; c < n4; c += blockDim.x) {
     float4 acc;
-    {
-      // up to 8 partials in flight at once, summed in split order
+    if (splits <= 8) {  // all partials in flight at once, then summed in split order
+      float4 v[8];
+#pragma unroll
+      for (int s = 0; s < 8; ++s)
+        if (s < splits) v[s] = __ldcg(reinterpret_cast<const float4*>(p.ws_part + ((size_t)s * p.rows_max + row) * p.N) + c);
+      acc = v[0];
+#pragma unroll
+      for (int s = 1; s < 8; ++s)
+        if (s < splits) {
+          acc.x += v[s].x; acc.y += v[s].y; acc.z += v[s].z; acc.w += v[s].w;
+        }
+    } else {  // (the fp32-TC mode's up to 16 K chunks) 8 at a time, in split order
       acc = make_float4(0.f, 0.f, 0.f, 0.f);
       for (int s0 = 0; s0 < splits; s0 += 8) {
         float4 v[8];
