@@ -316,8 +316,17 @@ def cpu_sample(gpu_caches=None, threads=None, steps=1, warmup=0, kind="reference
     ref = full_c2_reference_run() if WL is WORKLOADS["c2"] else None
     if ref:
         meta["full_prompt_measured_once"] = {k: ref.get(k) for k in ("ttft_ms", "tokens_per_s_one_core",
-                                                                    "gflops_per_s", "workload", "host",
-                                                                    "measured_in")}
+                                                                    "gflops_per_s", "first_token", "workload",
+                                                                    "host", "measured_in")}
+        if ref.get("sample_gflop_per_s_same_host"):
+            # the sample runs less efficiently per FLOP than the full prompt (small
+            # matrices): scale the extrapolated time by the ratio both measured
+            # on one host (profiles/r02_cpu_full_c2.json)
+            f = ref["sample_gflop_per_s_same_host"] / ref["gflops_per_s"]
+            tps /= f
+            meta["calibrated_by_full_run"] = round(f, 4)
+            meta["full_prompt_ttft_ms_one_core_extrapolated"] = round(ttft1_ms * f, 1)
+            meta["full_prompt_ttft_ms_all_cores_extrapolated"] = round(ttftN_ms * f, 1)
     return tps, meta
 
 
