@@ -639,9 +639,66 @@ constexpr int kSwA = kBM * kBK * 2;     // 16 KB: this CTA's 128 weight rows
 constexpr int kSwBMax = 256 * kBK * 2;  // 32 KB: half of up to 512 tokens
 constexpr int kSwStage = kSwA + kSwBMax;
 constexpr int kSwRs = 544;  // row scales of up to 512 tokens (+ one chunk of padding)
-constexpr int kSwSmem = kSwStages * kSwStage + 1024 + 256 + kSwRs * 4;
+constexpr int kSwEpi = 8 * 1024;  // per epilogue warp: 32 tokens x 16 bf16 outputs (SiLU transpose)
+constexpr int kSwSmem = kSwStages * kSwStage + 1024 + 256 + kSwRs * 4 + kSwEpi;
 constexpr uint32_t kSwTmemCols = 512;
 constexpr int kSwThreads = 320;  // producer, MMA issuer, 8 epilogue warps (two per TMEM lane quarter)
+
+// SiLU epilogue of the swap kernel: thread = feature n (gate on even lanes,
+// up on odd), 32 tokens per TMEM load. The 16 outputs x 32 tokens of a warp go
+// through a 1 KB shared tile so each store is a 16-byte piece of a token's
+// 32-byte output segment (2 instructions per chunk instead of 16 2-byte
+// scattered stores); row scales come as 16-byte shared loads; full chunks run
+// without per-element bounds checks. (r02al trace: the scalar version took
+// ~3.5k cycles per 32-token chunk, as long as the whole mainloop.)
+__device__ __forceinline__ void swap_silu_epilogue(const GemmArgs& p, uint32_t tbase, int n, int M, int lane, int hw,
+                                                   const float* rs_sm, uint8_t* S) {
+  const bool odd = lane & 1;
+  const int i = lane >> 1;            // output column within the warp's 16
+  const int col0 = (n - lane) / 2;    // the warp's first output column
+  const uint32_t rs_s = smem_u32(rs_sm), S_s = smem_u32(S);
+  float chk = 0.f;
+#pragma unroll 1
+  for (int t0 = 32 * hw; t0 < M; t0 += 64) {
+    uint32_t r[32];
+    tmem_ld32(tbase + (uint32_t)t0, r);
+    float rs[32];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                   : "=f"(rs[4 * q]), "=f"(rs[4 * q + 1]), "=f"(rs[4 * q + 2]), "=f"(rs[4 * q + 3])
+                   : "r"(rs_s + (uint32_t)(t0 + 4 * q) * 4u));
+    tmem_ld_wait();
+    const int lim = M - t0;  // valid tokens in this chunk (>= 32 except the last)
+    float v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      v[j] = __uint_as_float(r[j]) * rs[j];
+      chk = finite_acc(chk, j < lim ? v[j] : 0.f);
+    }
+    // even lane (gate) takes tokens t0..t0+15, odd lane (up) t0+16..t0+31
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float recv = __shfl_xor_sync(0xffffffffu, odd ? v[j] : v[16 + j], 1);
+      const float g = odd ? recv : v[j], u = odd ? v[16 + j] : recv;
+      const float a = __fdividef(g, 1.0f + __expf(-g)) * u;
+      const int tl = (odd ? 16 : 0) + j;
+      asm volatile("st.shared.b16 [%0], %1;" ::"r"(S_s + (uint32_t)(tl * 32 + i * 2)),
+                   "h"(__bfloat16_as_ushort(__float2bfloat16_rn(a))));
+    }
+    __syncwarp();
+#pragma unroll
+    for (int rep = 0; rep < 2; ++rep) {
+      const int piece = lane + 32 * rep, tok = piece >> 1, h = piece & 1;
+      uint4 x;
+      asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w)
+                   : "r"(S_s + (uint32_t)(tok * 32 + h * 16)));
+      if (tok < lim) *reinterpret_cast<uint4*>(p.out_bf16 + (size_t)(t0 + tok) * p.ld_bf16 + col0 + 8 * h) = x;
+    }
+    __syncwarp();
+  }
+  flag_nonfinite(p.status, chk);
+}
 
 // Epilogue of one CTA's 128 features (thread = feature n) over the M tokens.
 // rs_sm: the M row scales (1.0 without a fused RMSNorm), staged in shared
@@ -776,13 +833,14 @@ __global__ void __launch_bounds__(kSwThreads, 1)
     if (elect_one()) {  // ---------------- TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      int wt, s, kb0, kb1;
+      int wt, s, kb0, kb1, kbn = 0;
       for (int it = 0; unit_of(it, wt, s, kb0, kb1); ++it) {
-        for (int kb = kb0; kb < kb1; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb, ++kbn) {
           const bool early = it == 0 && kb - kb0 < pre;
           uint8_t* sa = smem + stage * kSwStage;
           if (!early) {
             mbar_wait(&empty[stage], phase ^ 1);
+            GTRACE(0, kbn, true);
             if (rank == 0) mbar_arrive_expect_tx(&full[stage], stage_tx);
             tma_load_2d_pair(sa, &tmW, &full[stage], kb * kBK, wt * 256 + (int)rank * kBM);
           }
@@ -797,12 +855,13 @@ __global__ void __launch_bounds__(kSwThreads, 1)
       const uint32_t idesc = idesc_bf16(2 * kBM, tc);
       int stage = 0;
       uint32_t phase = 0;
-      int wt, s, kb0, kb1;
+      int wt, s, kb0, kb1, kbm = 0;
       for (int it = 0; unit_of(it, wt, s, kb0, kb1); ++it) {
         mbar_wait(tempty, (it & 1) ^ 1);
         tc_fence_after();
-        for (int kb = kb0; kb < kb1; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb, ++kbm) {
           mbar_wait(&full[stage], phase);
+          GTRACE(1, kbm, true);
           tc_fence_after();
           const uint32_t a0 = smem_u32(smem + stage * kSwStage), b0 = a0 + kSwA;
           for (int c = 0; c < nc; ++c) {
@@ -826,9 +885,15 @@ __global__ void __launch_bounds__(kSwThreads, 1)
     int wt, s, kb0, kb1;
     for (int it = 0; unit_of(it, wt, s, kb0, kb1); ++it) {
       mbar_wait(tfull, it & 1);
+      GTRACE(2, 2 * it, warp == 2 && lane == 0);
       tc_fence_after();
       const int n = wt * 256 + (int)rank * kBM + quarter * 32 + lane;
-      swap_epilogue<EPI>(p, tmem + ((uint32_t)(quarter * 32) << 16), n, p.rows_max, s, lane, hw, rs_sm);
+      if constexpr (EPI == EPI_SILU)
+        swap_silu_epilogue(p, tmem + ((uint32_t)(quarter * 32) << 16), n, p.rows_max, lane, hw, rs_sm,
+                           reinterpret_cast<uint8_t*>(rs_sm + kSwRs) + (warp - 2) * 1024);
+      else
+        swap_epilogue<EPI>(p, tmem + ((uint32_t)(quarter * 32) << 16), n, p.rows_max, s, lane, hw, rs_sm);
+      GTRACE(2, 2 * it + 1, warp == 2 && lane == 0);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty, 0);
@@ -1477,6 +1542,7 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
     GemmArgs alt = p;
     const double other = choose_config(alt, e->sm_count, rows_hint > 0 ? rows_hint : p.rows_max);
     if (p.tf32 || !choose_swap(p, e->sm_count, other)) p = alt;
+    p.dbg = alt.dbg;
     if (p.tf32) {
       // The tensor core's fp32 accumulation loses ~3.6e-9 (relative, measured)
       // per accumulated element of K, linearly in K (r02v: rel-L2 6e-6 at a
