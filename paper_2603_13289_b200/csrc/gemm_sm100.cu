@@ -634,7 +634,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 // token, so the epilogue walks 32 tokens per tcgen05.ld; residual GEMMs store
 // split-K partials (EPI_PART) for splitk_reduce_add_kernel.
 // ---------------------------------------------------------------------------
-constexpr int kSwStages = 4;
+constexpr int kSwStages = 4;      // ring bytes = kSwStages * kSwStage; the ring is cut into
+constexpr int kSwMaxStages = 6;   // as many stages of the launch's real size as fit (<= 6)
 constexpr int kSwA = kBM * kBK * 2;     // 16 KB: this CTA's 128 weight rows
 constexpr int kSwBMax = 256 * kBK * 2;  // 32 KB: half of up to 512 tokens
 constexpr int kSwStage = kSwA + kSwBMax;
@@ -777,8 +778,8 @@ __global__ void __launch_bounds__(kSwThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSwStages * kSwStage);
-  uint64_t* empty = full + kSwStages;
-  uint64_t* tfull = empty + kSwStages;
+  uint64_t* empty = full + kSwMaxStages;
+  uint64_t* tfull = empty + kSwMaxStages;
   uint64_t* tempty = tfull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
   float* rs_sm = reinterpret_cast<float*>(smem + kSwStages * kSwStage + 256);
@@ -786,11 +787,13 @@ __global__ void __launch_bounds__(kSwThreads, 1)
   const uint32_t rank = cluster_ctarank();  // 0 = leader (issues the MMAs)
   pdl_trigger();
   const int tc = p.tc, nc = p.nc, half = tc / 2;
-  const uint32_t stage_tx = 2u * (uint32_t)(kSwA + nc * half * kBK * 2);  // both CTAs' bytes, on the leader
+  const int sst = kSwA + nc * half * kBK * 2;  // this launch's stage bytes (M = 320: 36 KB of the 48 KB maximum)
+  const int nst = min(kSwMaxStages, kSwStages * kSwStage / sst);  // 5 stages at M = 320 instead of 4
+  const uint32_t stage_tx = 2u * (uint32_t)sst;  // both CTAs' bytes, on the leader
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmW);
     tma_prefetch(&tmX);
-    for (int i = 0; i < kSwStages; ++i) {
+    for (int i = 0; i < nst; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
@@ -820,10 +823,10 @@ __global__ void __launch_bounds__(kSwThreads, 1)
   if (warp == 0) {
     int wt, s, kb0, kb1;
     if (elect_one() && unit_of(0, wt, s, kb0, kb1)) {
-      pre = min(kSwStages, kb1 - kb0);
+      pre = min(nst, kb1 - kb0);
       for (int i = 0; i < pre; ++i) {
         if (rank == 0) mbar_arrive_expect_tx(&full[i], stage_tx);
-        tma_load_2d_pair(smem + i * kSwStage, &tmW, &full[i], (kb0 + i) * kBK, wt * 256 + (int)rank * kBM);
+        tma_load_2d_pair(smem + i * sst, &tmW, &full[i], (kb0 + i) * kBK, wt * 256 + (int)rank * kBM);
       }
     }
   }
@@ -837,7 +840,7 @@ __global__ void __launch_bounds__(kSwThreads, 1)
       for (int it = 0; unit_of(it, wt, s, kb0, kb1); ++it) {
         for (int kb = kb0; kb < kb1; ++kb, ++kbn) {
           const bool early = it == 0 && kb - kb0 < pre;
-          uint8_t* sa = smem + stage * kSwStage;
+          uint8_t* sa = smem + stage * sst;
           if (!early) {
             mbar_wait(&empty[stage], phase ^ 1);
             GTRACE(0, kbn, true);
@@ -846,7 +849,7 @@ __global__ void __launch_bounds__(kSwThreads, 1)
           }
           for (int c = 0; c < nc; ++c)
             tma_load_2d_pair(sa + kSwA + c * half * (kBK * 2), &tmX, &full[stage], kb * kBK, c * tc + (int)rank * half);
-          if (++stage == kSwStages) { stage = 0; phase ^= 1; }
+          if (++stage == nst) { stage = 0; phase ^= 1; }
         }
       }
     }
@@ -863,7 +866,7 @@ __global__ void __launch_bounds__(kSwThreads, 1)
           mbar_wait(&full[stage], phase);
           GTRACE(1, kbm, true);
           tc_fence_after();
-          const uint32_t a0 = smem_u32(smem + stage * kSwStage), b0 = a0 + kSwA;
+          const uint32_t a0 = smem_u32(smem + stage * sst), b0 = a0 + kSwA;
           for (int c = 0; c < nc; ++c) {
 #pragma unroll
             for (int k = 0; k < kBK / 16; ++k)
@@ -872,7 +875,7 @@ __global__ void __launch_bounds__(kSwThreads, 1)
                                (kb > kb0 || k > 0) ? 1u : 0u);
           }
           tc_commit_pair(&empty[stage]);
-          if (++stage == kSwStages) { stage = 0; phase ^= 1; }
+          if (++stage == nst) { stage = 0; phase ^= 1; }
         }
         tc_commit_pair(tfull);
       }

@@ -23,6 +23,9 @@ if __name__ == "__main__":
     for i in range(n):
         print(f"  kb {i:3d}: slot {prod[i] - t0 if prod[i] else -1:7d}  full {mma[i] - t0:7d}"
               + (f"  (+{mma[i] - mma[i - 1]})" if i else ""))
-    for u in range(256):
+    extra = [(i, int(epi_t[i] - t0)) for i in range(100, 130) if epi_t[i]]
+    if extra:
+        print("  epilogue warp 2 marks:", extra)
+    for u in range(50):
         if epi_t[2 * u]:
             print(f"  unit {u}: acc ready {epi_t[2 * u] - t0:7d}  drained {epi_t[2 * u + 1] - t0:7d}")
