@@ -325,6 +325,18 @@ int rk_debug_trace_gemm(rk_engine* e, int M, int N, int K, int epi, unsigned lon
     g.out_bf16 = reinterpret_cast<__nv_bfloat16*>(c.p);
     g.ld_bf16 = N / 2;
     g.split_flags = flags.as<int>();
+    DevBuf nbf, npart, ninv, ncnt;
+    if (epi == EPI_ADD && std::getenv("RK_BENCH_NORM")) {  // the layer pass's fused RMSNorm producer
+      nbf.alloc((size_t)M * N * 2);
+      npart.alloc((size_t)M * kNormSlots * 4 + 256);
+      ninv.alloc((size_t)M * 4 + 256);
+      ncnt.alloc(((size_t)(M + 127) / 128 * 8 + 64) * 4);
+      RK_CUDA(cudaMemsetAsync(ncnt.p, 0, ncnt.bytes, st));
+      g.norm_bf16 = nbf.as<__nv_bfloat16>();
+      g.norm_part = npart.as<float>();
+      g.norm_inv = ninv.as<float>();
+      g.norm_cnt = ncnt.as<int>();
+    }
     gemm_bf16(e, a.as<__nv_bfloat16>(), K, b.as<__nv_bfloat16>(), g, M);  // warm
     g.trace = tr.as<unsigned long long>();
     gemm_bf16(e, a.as<__nv_bfloat16>(), K, b.as<__nv_bfloat16>(), g, M);
