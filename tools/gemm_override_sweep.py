@@ -22,6 +22,12 @@ SETS = {
         ("320:2048:2048", "gemm_add", ["64/1/1", "128/1/1", "64/2/1", "128/2/1", "64/1/2", "128/1/2", "256/1/4"]),
         ("320:2048:8192", "gemm_add", ["256/1/6", "256/1/4", "256/1/8", "128/1/4", "128/1/6", "64/1/2", "64/1/4"]),
     ],
+    "m320pair": [
+        ("320:2048:8192", "gemm_add", ["256/1/6", "256/2/2", "256/2/4", "256/2/6", "128/2/4", "128/2/8"]),
+        ("320:2048:2048", "gemm_add", ["64/1/1", "256/2/2", "128/2/2", "256/2/4", "64/2/2"]),
+        ("4032d:2048:8192", "gemm_add", ["256/2/1", "256/2/2", "128/2/2", "256/2/3"]),
+        ("4032d:2048:2048", "gemm_add", ["256/2/1", "256/2/2", "128/2/2"]),
+    ],
     "band": [
         ("4032:3072:2048", "gemm_qkv_m4032_", ["256/2/1", "128/2/1", "256/1/1"]),
         ("4032:2048:2048", "gemm_add", ["256/2/1", "128/2/1", "128/1/1", "256/1/1"]),
