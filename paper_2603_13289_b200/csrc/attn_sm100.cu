@@ -767,7 +767,7 @@ void attention_bf16(rk_engine* e, const AttnArgs& a_in, const __nv_bfloat16* ctx
   // whose rows end before their split exit at once, so long tiles (suffix,
   // late segment rows) spread over many CTAs while short ones stay whole.
   AttnArgs hint = a;
-  if (a.rows_dev) hint.rows_max = std::max(a.g2 + 1, a.rows_max / 3);
+  if (a.rows_dev) hint.rows_max = a.rows_hint > 0 ? std::max(a.g2 + 1, a.rows_hint) : std::max(a.g2 + 1, a.rows_max / 3);
   const int ctas_per_sm = a.dh == 64 ? ACfg<64>::CTAS : ACfg<128>::CTAS;
   const int base = max_tiles(hint) * (a.group > 1 ? a.Hkv : a.H);  // CTAs without splitting
   const int slots = ctas_per_sm * e->sm_count;     // CTAs resident at once

@@ -95,6 +95,11 @@ struct rk_engine {
   rk::PinnedPool pinned_pool;
   uint64_t launches = 0;
   int use_graphs = 0;
+  // fraction of a relayed segment's rows the last RELAY/BLEND selection kept
+  // (-1: none yet). The live row count of a sparse pass exists only on the
+  // device; the host plans its GEMM tiles / attention split from this
+  // (Rows::hint) instead of a fixed guess.
+  double sel_frac = -1.0;
   int fused = 1;  // layer-major fused agent schedule (runner.cpp agent_fused)
   std::vector<std::unique_ptr<rk::RopeTable>> rope;
   std::unique_ptr<rk::Scratch> scratch;
@@ -224,6 +229,7 @@ struct Rows {
   // rows [0, g1), [g1, g2), [g2, live). Attention tiles never straddle a
   // group boundary, so a tile's key range follows its own rows' positions.
   int g1 = 0, g2 = 0;
+  int hint = 0;  // expected live rows when rows_dev is set (0: unknown -> rows_max / 3)
 };
 
 void ensure_cache_layer(rk_cache* c, uint64_t l);  // engine.cpp: upload a deferred layer now

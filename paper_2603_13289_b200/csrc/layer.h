@@ -58,6 +58,15 @@ class Runner {
   // Synchronize, raise on device-side errors, resolve pending ExtendResults.
   void finish();
   void resolve(ExtendResult& r);  // after finish(): counts, stats, timings
+  // expected live rows of a sparse pass over `head` fixed rows plus the
+  // selected ones of `seg` segment rows: the last observed selection fraction,
+  // 0 when none was observed yet (the grids cover rows_max regardless; the
+  // hint only picks tile shapes and the split-KV plan)
+  int live_hint(uint64_t head, uint64_t seg) const {
+    if (e_->sel_frac < 0) return 0;
+    const double sel = e_->sel_frac * static_cast<double>(seg) + 0.5;
+    return static_cast<int>(std::min<double>(static_cast<double>(head + seg), static_cast<double>(head) + sel));
+  }
   void fill_output(ExtendResult& res, rk_context* ctx, rk_relay_output* out);
   void download_logits(float* dst);
   // row_logits_from_layer (model.cpp:339-362) of a device hidden row into scratch logits

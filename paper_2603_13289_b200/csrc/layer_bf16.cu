@@ -149,7 +149,7 @@ void run_layer_bf16(rk_engine* e, rk_weights* w, rk_context* ctx, int l, float* 
   auto* ck = static_cast<__nv_bfloat16*>(ctx->k_layer(l));
   auto* cv = static_cast<__nv_bfloat16*>(ctx->v_layer(l));
   // live rows of a sparse pass are known only on the device: plan tiles for ~1/3
-  int hint = rows.rows_dev ? std::max(1, rows.rows_max / 3) : rows.rows_max;
+  int hint = rows.rows_dev ? (rows.hint > 0 ? rows.hint : std::max(1, rows.rows_max / 3)) : rows.rows_max;
   int* flags = split_flags(e);
   __nv_bfloat16* save = reinterpret_cast<__nv_bfloat16*>(S.seg_hidden_out.as<char>() + 0);
   if (!commit) {
@@ -207,6 +207,7 @@ void run_layer_bf16(rk_engine* e, rk_weights* w, rk_context* ctx, int l, float* 
   a.rows_dev = rows.rows_dev;
   a.g1 = rows.g1;
   a.g2 = rows.g2;
+  a.rows_hint = rows.rows_dev ? rows.hint : 0;
   a.H = s.num_heads;
   a.Hkv = s.num_kv_heads;
   a.dh = s.d_head;

@@ -98,6 +98,7 @@ struct AttnArgs {
   unsigned long long* trace = nullptr;
   int pingpong = 1;  // set by attention_bf16
   int group = 1, rq = 128;  // GQA packing (set by attention_bf16): q heads per CTA, rows per head
+  int rows_hint = 0;        // expected live rows (Rows::hint) for the split-KV plan
   int* status = nullptr;  // non-finite output flag (engine status[0], set by attention_bf16)
 };
 // ctx_k / ctx_v: the layer's [ctx_rows x kv] bf16 context rows.

@@ -294,7 +294,7 @@ void gemm(rk_engine* e, const float* A, int lda, Rows rows, const float* Wtc, in
   g.ld_out = ldo;
   g.tf32 = 1;
   gemm_bf16(e, reinterpret_cast<const __nv_bfloat16*>(a3), 2 * 3 * K, reinterpret_cast<const __nv_bfloat16*>(Wtc), g,
-            rows.rows_dev ? std::max(1, rows.rows_max / 3) : 0);
+            rows.rows_dev ? (rows.hint > 0 ? rows.hint : std::max(1, rows.rows_max / 3)) : 0);
 }
 
 void silu(rk_engine* e, const float* gu, float* act, Rows rows, int ff) {

@@ -562,6 +562,7 @@ ExtendResult Runner::relay_extend(rk_context* ctx, rk_cache* cache, const rk_lay
         k::positions_from_sel(st_, X.sub_pos.as<int>(), X.sel_idx.as<int>(), count, (int)n, (int)base);
         e_->launches += 2;
         Rows sparse_rows{(int)n, count, X.sub_pos.as<int>()};
+        sparse_rows.hint = live_hint(0, n);
         prepared_ = false;
         for (uint64_t l = l_det + 1; l <= sparse_hi; ++l)
           run_layer(ctx, (int)l, X.sub_hidden.as<float>(), sparse_rows, true, max_ctx);
@@ -596,6 +597,8 @@ void Runner::resolve(ExtendResult& r) {
                                         : 1.0 - static_cast<double>(st.recomputed_entries) /
                                                     static_cast<double>(st.total_entries);
   st.selected_count = count;
+  if ((r.mode == RK_MODE_RELAY || r.mode == RK_MODE_BLEND) && r.n > 0)
+    e_->sel_frac = static_cast<double>(count) / static_cast<double>(r.n);
   st.selected_deviation = count ? (uint64_t)r.info[1] : 0;
   st.selected_influence_score = count ? (uint64_t)r.info[2] : 0;
   st.selected_influence_suffix = count ? (uint64_t)r.info[3] : 0;
@@ -840,7 +843,10 @@ void Runner::agent_fused(rk_context* ctx, const int32_t* prefix, uint64_t P, rk_
   for (uint64_t l = 0; l < L; ++l) {
     Rows rows{(int)head, nullptr, pos};
     if (segs && l >= l_start && l <= l_det) rows = Rows{(int)(head + segrows), nullptr, pos};
-    else if (segs && l > l_det && l <= sparse_hi) rows = Rows{(int)(head + segrows), offs + U, pos};
+    else if (segs && l > l_det && l <= sparse_hi) {
+      rows = Rows{(int)(head + segrows), offs + U, pos};
+      rows.hint = live_hint(head, segrows);
+    }
     rows.g1 = (int)P;
     rows.g2 = (int)head;
     // the row set grows at l = 0, at the band start and after the selected
