@@ -251,8 +251,8 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
   const int h0 = G > 1 ? kvh * G : (int)blockIdx.y;  // first q head of the CTA
   // Adaptive split-KV: a tile whose key range exceeds tiles_per_split key
   // tiles is cut into ts = ceil(nk_tile / tiles_per_split) (<= gridDim.x)
-  // equal parts; CTA z covers part z. Tiles that fit in one part write their
-  // output directly (no partials, no combine); row_splits tells the combine.
+  // equal parts; CTA x covers part x, and the last part to finish merges them
+  // (in-kernel, below). Tiles that fit in one part write their output directly.
   constexpr int KEYS = C::KEYS;
   const int nk_tile = *s_kmax / KEYS + 1;
   const int ts = min((int)gridDim.x, (nk_tile + a.tiles_per_split - 1) / a.tiles_per_split);
@@ -263,8 +263,6 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
   const bool partial = ts_eff > 1;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const bool trace_cta = TRACE && a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
-  if (a.row_splits && part == 0 && blockIdx.y == 0)
-    for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) a.row_splits[i] = ts_eff;
   if (part >= ts_eff || nk <= 0) return;  // this tile has no such part
 
   if (warp == 4 && lane == 0) {
@@ -479,7 +477,7 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
     }
     mbar_wait(o_done, (nk - 1) & 1);
     tc_fence_after();
-    if (partial && a.tile_cnt) {
+    if (partial) {
       // in-kernel merge: partials in a tile-contiguous block [tile][part][lane][DH]
       // (one 128 x DH fp32 block per part); the last part of this (tile, kv
       // group) to finish merges them with coalesced streaming reads -- no
@@ -539,25 +537,6 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
         else if (ts_eff <= 8) chk = attn_merge_stream<DH, 8>(a, src, wsm, rl, ts_eff, r0, r1, rq, G, h0);
         else chk = attn_merge_stream<DH, 16>(a, src, wsm, rl, ts_eff, r0, r1, rq, G, h0);
         if (chk != chk && a.status) *reinterpret_cast<volatile int*>(a.status) = 1;
-      }
-    } else if (partial) {
-      const size_t pr = ((size_t)part * a.rows_max + row) * a.H + h;
-#pragma unroll
-      for (int c = 0; c < DH; c += 32) {
-        uint32_t o[32];
-        tmem_ld32(o_col + c, o);
-        tmem_ld_wait();
-        if (valid) {
-          float4* dst = reinterpret_cast<float4*>(a.ws_o + pr * DH + c);
-#pragma unroll
-          for (int u = 0; u < 32; u += 4)
-            dst[u / 4] = make_float4(__uint_as_float(o[u]), __uint_as_float(o[u + 1]), __uint_as_float(o[u + 2]),
-                                     __uint_as_float(o[u + 3]));
-        }
-      }
-      if (valid) {
-        a.ws_ml[pr * 2] = m_run;
-        a.ws_ml[pr * 2 + 1] = l_run;
       }
     } else {
       const float inv = 1.f / l_run;
@@ -632,53 +611,6 @@ __global__ void attn_probs_kernel(const __nv_bfloat16* __restrict__ q, const __n
   }
 }
 
-// Merge split-KV partials: out = sum_z 2^(m_z - m) acc_z / sum_z 2^(m_z - m) l_z.
-// One warp per (row, head).
-template <int DH>
-__device__ __forceinline__ void attn_combine_one(const AttnArgs& a, int row, int h, int lane) {
-  const int ts = a.row_splits[row];  // parts of this row's tile (1: written directly)
-  if (ts <= 1) return;
-  float m = -INFINITY;
-  for (int z = 0; z < ts; ++z)
-    m = fmaxf(m, a.ws_ml[(((size_t)z * a.rows_max + row) * a.H + h) * 2]);
-  constexpr int PER = DH / 32;
-  float o[PER];
-#pragma unroll
-  for (int i = 0; i < PER; ++i) o[i] = 0.f;
-  float lsum = 0.f;
-  for (int z = 0; z < ts; ++z) {
-    const size_t pr = ((size_t)z * a.rows_max + row) * a.H + h;
-    const float mz = a.ws_ml[pr * 2];
-    if (mz == -INFINITY) continue;
-    const float wz = fast_exp2(mz - m);
-    lsum += wz * a.ws_ml[pr * 2 + 1];
-#pragma unroll
-    for (int i = 0; i < PER; ++i) o[i] += wz * a.ws_o[pr * DH + lane * PER + i];
-  }
-  const float inv = 1.f / lsum;
-  float chk = inv * 0.f;
-#pragma unroll
-  for (int i = 0; i < PER; ++i) chk = fmaf(o[i], 0.f, chk);
-  if (chk != chk && a.status) *reinterpret_cast<volatile int*>(a.status) = 1;
-  __nv_bfloat16* dst = a.out + (size_t)row * (a.H * DH) + h * DH + lane * PER;
-#pragma unroll
-  for (int i = 0; i < PER; i += 2) *reinterpret_cast<uint32_t*>(dst + i) = pack_bf16(o[i] * inv, o[i + 1] * inv);
-}
-
-// grid-strided over the live (row, head) pairs (the live row count may be
-// far below rows_max in sparse passes)
-template <int DH>
-__global__ void attn_combine_kernel(const AttnArgs a) {
-  pdl_trigger();
-  pdl_wait();
-  const int M = a.rows_dev ? *a.rows_dev : a.rows_max;
-  const int lane = threadIdx.x % 32;
-  const long long n = (long long)M * a.H;
-  for (long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / 32; gw < n;
-       gw += (long long)gridDim.x * blockDim.x / 32)
-    attn_combine_one<DH>(a, (int)(gw / a.H), (int)(gw % a.H), lane);
-}
-
 // Upper bound on query tiles of a launch (row groups split at their bounds).
 int max_tiles(const AttnArgs& a) {
   const int M = a.rows_max, g1 = std::min(a.g1, M), g2 = std::min(std::max(a.g2, g1), M), rq = a.rq;
@@ -725,20 +657,6 @@ void launch_attn(rk_engine* e, const CUtensorMap& tq, const CUtensorMap& tk, con
   else if (poly == 0x92) go(attn_kernel<DH, false, 0x92>);
   else if (poly == 0) go(attn_kernel<DH, false, 0x00>);
   else go(attn_kernel<DH, false>);
-  if (a.splits > 1 && !a.tile_cnt) {
-    const int warps = a.rows_max * a.H;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(std::min((warps + 7) / 8, 4 * e->sm_count));
-    cfg.blockDim = dim3(256);
-    cfg.stream = e->stream;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = pdl_enabled() ? 1 : 0;
-    RK_CUDA(cudaLaunchKernelEx(&cfg, attn_combine_kernel<DH>, a));
-    e->launches += 1;
-  }
 }
 
 }  // namespace
@@ -803,26 +721,19 @@ void attention_bf16(rk_engine* e, const AttnArgs& a_in, const __nv_bfloat16* ctx
   }
   if (a.splits > 1) {
     Scratch& S = *e->scratch;
-    // partials: in-kernel merge (default) -> per (tile, kv group, part) one
-    // 128-lane block; RK_ATTN_MERGE=0 -> row-major [part][row][head] for the
-    // separate attn_combine_kernel
-    static const bool merge_env = [] {
-      const char* v = std::getenv("RK_ATTN_MERGE");
-      return v ? std::atoi(v) != 0 : true;
-    }();
+    // partials: per (tile, kv group, part) one 128-lane fp32 block + (m, l)
+    // per lane, merged in-kernel by the tile's last part (r02r: faster than a
+    // separate combine launch, 19.8 vs 20.5 us on the c2 prefix+suffix layer)
     const size_t tiles = (size_t)max_tiles(a) * (a.group > 1 ? a.Hkv : a.H);
-    const size_t per = merge_env ? tiles * a.splits * kQ : (size_t)a.splits * a.rows_max * a.H;
-    S.attn_ws.ensure(per * (a.dh + 2) * 4 + (size_t)a.rows_max * 4 + 256);
+    const size_t per = tiles * a.splits * kQ;
+    S.attn_ws.ensure(per * (a.dh + 2) * 4 + 256);
     a.ws_o = S.attn_ws.as<float>();
     a.ws_ml = a.ws_o + per * a.dh;
-    a.row_splits = reinterpret_cast<int*>(a.ws_ml + per * 2);
-    if (merge_env) {  // per-(tile, kv group) arrival counters, zeroed once, self-resetting
-      if (S.attn_cnt.bytes < tiles * 4) {
-        S.attn_cnt.ensure(tiles * 4);
-        RK_CUDA(cudaMemsetAsync(S.attn_cnt.p, 0, S.attn_cnt.bytes, e->stream));
-      }
-      a.tile_cnt = S.attn_cnt.as<int>();
+    if (S.attn_cnt.bytes < tiles * 4) {  // arrival counters, zeroed once, self-resetting
+      S.attn_cnt.ensure(tiles * 4);
+      RK_CUDA(cudaMemsetAsync(S.attn_cnt.p, 0, S.attn_cnt.bytes, e->stream));
     }
+    a.tile_cnt = S.attn_cnt.as<int>();
   }
   const int q = a.H * a.dh, kv = a.Hkv * a.dh;
   CUtensorMap tq, tk, tv;

@@ -91,7 +91,6 @@ struct AttnArgs {
   int splits = 1, tiles_per_split = 1 << 20;
   float* ws_o = nullptr;
   float* ws_ml = nullptr;
-  int* row_splits = nullptr;  // [rows_max] parts of each row's tile (1 = output written directly)
   int* tile_cnt = nullptr;    // [tiles x grid.y] zeroed, self-resetting: in-kernel split-KV merge
   // debug: clock64 timeline of the last CTA of head 0 ([role 0..2][step < 64][event < 8];
   // roles: softmax group 0, group 1, MMA issuer)
