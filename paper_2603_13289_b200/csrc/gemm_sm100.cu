@@ -83,7 +83,8 @@ struct Cfg {
   static constexpr int A_BYTES = kBM * kBK * 2;
   static constexpr int B_BYTES = BN / PAIR * kBK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = PAIR == 1 ? ((BN == 256) ? 4 : (BN == 128 ? 6 : 8)) : (BN == 256 ? 6 : 8);
+  static constexpr int STAGES = PAIR == 1 ? ((BN == 256) ? 4 : (BN == 128 ? 6 : 8))
+                                           : (BN == 256 ? 6 : (BN == 192 ? 7 : 8));
   static constexpr int NACC = 2;  // TMEM accumulator buffers
   static constexpr int TMEM_COLS = pow2_cols(NACC * BN);
   // per epilogue warp: a 32x32 fp32 staging tile for the coalesced residual epilogue
@@ -102,7 +103,7 @@ __device__ __forceinline__ Units units_of(const GemmArgs& p) {
   const int M = p.rows_dev ? *p.rows_dev : p.rows_max;
   // m tiles of 128 (or 256-row pair tiles)
   u.num_m = (M + kBM * PAIR - 1) / (kBM * PAIR);
-  u.num_n = p.N / p.bn;
+  u.num_n = (p.N + p.bn - 1) / p.bn;  // (BN 192: the last N tile may be ragged)
   // live row count known only on the device: pick split-K here (grid = all SMs)
   u.splits = p.splits;
   u.kb_total = p.K / kBK;
@@ -418,6 +419,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* T = epi_stage + quarter * 4096;
         const int sub = lane >> 3, ch = lane & 7;  // row-within-4 and 16-byte chunk of the read-back layout
         const int row0 = mt * kBM + quarter * 32;
+        const int bn_live = min(BN, p.N - nt * BN);  // (a ragged last N tile stores its live columns only)
         auto hptr = [&](int i, int c) {  // residual of local row 4i+sub, columns c + 4*ch ..
           const int rr = row0 + 4 * i + sub;
           return reinterpret_cast<float4*>(p.out_f32 + (size_t)(rr < M ? rr : 0) * p.ld_out + nt * BN + c) + ch;
@@ -433,7 +435,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < 8; ++i) ss[i] = 0.f;
         float chk = 0.f;  // non-finite matmul values (rows past M are zero-filled A rows: finite)
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
+        for (int c = 0; c < bn_live; c += 32) {
           uint32_t r[32];
           tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + acol + c, r);
           tmem_ld_wait();
@@ -446,7 +448,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           float4 cur[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) cur[i] = hb[i];
-          if (c + 32 < BN) {
+          if (c + 32 < bn_live) {
 #pragma unroll
             for (int i = 0; i < 8; ++i)
               hb[i] = (row0 + 4 * i + sub < M) ? __ldcg(hptr(i, c + 32)) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -519,6 +521,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         GTRACE(2, 2 * local, warp == 2 && lane == 0);
         tc_fence_after();
         const float rs = (p.row_scale && row < M) ? p.row_scale[row] : 1.0f;
+        const int bn_live = min(BN, p.N - nt * BN);  // (ragged last N tile)
         uint8_t* T = epi_stage + quarter * 4096;
         const int row0 = mt * kBM + quarter * 32;  // the warp's first row
         if constexpr (EPI == EPI_QKV) {
@@ -536,9 +539,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               cs[2 * j + 1] = make_float2(t.z, t.w);
             }
 #pragma unroll 1
-            for (int c = 0; c < BN; c += 64) {
+            for (int c = 0; c < bn_live; c += 64) {
 #pragma unroll
               for (int hh = 0; hh < 2; ++hh) {
+                if (c + 32 * hh >= bn_live) break;
                 uint32_t r[32];
                 tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + acol + c + 32 * hh, r);
                 tmem_ld_wait();
@@ -551,8 +555,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < 16; ++j) cur[j] = csrow[((nt * BN) % p.dh) / 2 + j];
 #pragma unroll 1
-            for (int c = 0; c < BN; c += 32) {
-              if (c + 32 < BN) {
+            for (int c = 0; c < bn_live; c += 32) {
+              if (c + 32 < bn_live) {
 #pragma unroll
                 for (int j = 0; j < 16; ++j) nxt[j] = csrow[((nt * BN + c + 32) % p.dh) / 2 + j];
               }
@@ -566,7 +570,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         } else if constexpr (EPI == EPI_SILU) {
 #pragma unroll 1
-          for (int c = 0; c < BN; c += 32) {
+          for (int c = 0; c < bn_live; c += 32) {
             uint32_t r[32];
             tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + acol + c, r);
             tmem_ld_wait();
@@ -574,7 +578,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         } else {  // EPI_F32 / EPI_PART: 128-byte fp32 segments
 #pragma unroll 1
-          for (int c = 0; c < BN; c += 32) {
+          for (int c = 0; c < bn_live; c += 32) {
             uint32_t r[32];
             tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + acol + c, r);
             tmem_ld_wait();
@@ -1268,6 +1272,7 @@ template <int EPI, bool TF32>
 void launch_tiles(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& p, int grid) {
   if (p.pair == 2) {
     if (p.bn == 256) launch<256, EPI, 2, TF32>(st, a, b, p, grid);
+    else if (p.bn == 192) launch<192, EPI, 2, TF32>(st, a, b, p, grid);
     else if (p.bn == 128) launch<128, EPI, 2, TF32>(st, a, b, p, grid);
     else launch<64, EPI, 2, TF32>(st, a, b, p, grid);
   } else {
@@ -1403,10 +1408,14 @@ static double choose_config(GemmArgs& p, int sm_count, int rows_hint) {
     // wider tile (fewer, longer units), except the QKV epilogue (RoPE + K/V
     // scatter) of the sparse passes, whose exposed last epilogue favours two
     // narrower rounds (measured r02s: sparse W_o 256 wins, sparse QKV 128)
+    // (192: a ragged last N tile, e.g. N = 2048 = 10 x 192 + 128, when whole
+    // 256-column tiles leave a third of the pair slots idle -- c2 sparse W_down:
+    // 48 pair units on 74 slots)
     double bc = 1e30;
-    for (int cand : {256, 128, 64}) {
-      if (p.N % cand) continue;
-      const double c = (double)ceil_div((long long)num_m * (p.N / cand), slots) *
+    for (int cand : {256, 192, 128, 64}) {
+      if (cand != 192 && p.N % cand) continue;
+      if (cand == 192 && (p.N % 32 || p.N <= 192)) continue;
+      const double c = (double)ceil_div((long long)num_m * ceil_div(p.N, cand), slots) *
                        std::max(kPairKb * cand / 256.0, t_kb(16, cand / 16));
       if (c < bc || (c == bc && p.epi == EPI_QKV && p.rows_dev && cand >= 128)) { bc = c; bn = cand; }
     }
@@ -1415,9 +1424,9 @@ static double choose_config(GemmArgs& p, int sm_count, int rows_hint) {
       if (p.N % cand == 0 && num_m * (p.N / cand) >= slots) { bn = cand; break; }
     }
   }
-  if (p.N % bn) raise(RK_ERR_INVALID_ARGUMENT, "bf16 GEMM needs N % 64 == 0");
+  if (p.N % bn && bn != 192) raise(RK_ERR_INVALID_ARGUMENT, "bf16 GEMM needs N % 64 == 0");
   p.bn = bn;
-  double best = (double)ceil_div((long long)num_m * (p.N / bn), slots) * kb *
+  double best = (double)ceil_div((long long)num_m * ceil_div(p.N, bn), slots) * kb *
                 (p.pair == 2 ? std::max(kPairKb * bn / 256.0, t_kb(16, bn / 16)) : t_kb(16, bn / 8));
 
   const bool residual_split = p.epi == EPI_ADD && p.split_flags;
@@ -1671,7 +1680,7 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
   make_tmap_bf16(&ta, A, (uint64_t)p.rows_max, (uint64_t)p.K, kBM, (uint64_t)lda);
   make_tmap_bf16(&tb, B, (uint64_t)p.N, (uint64_t)p.K, (uint32_t)(p.bn / p.pair), (uint64_t)p.K);
   const int num_m = (p.rows_max + kBM * p.pair - 1) / (kBM * p.pair);
-  const int total = num_m * (p.N / p.bn) * p.splits;  // units (pair units for the pair kernel)
+  const int total = num_m * ((p.N + p.bn - 1) / p.bn) * p.splits;  // units (pair units for the pair kernel)
   const int slots = p.pair == 2 ? pair_slots(e->sm_count) : e->sm_count;
   const int grid = p.pair * (total < slots ? total : slots);
   if (p.epi == EPI_PART) {

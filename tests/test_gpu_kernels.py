@@ -311,3 +311,41 @@ def test_select_topk_radix(engine, case):
                                       idx.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(cnt)))
     assert cnt.value == len(want)
     assert np.array_equal(idx[:cnt.value], want)
+
+
+@pytest.mark.parametrize("case", [(1360, 2048, 8192, 1, 1360), (700, 2048, 2048, 3, 700), (1500, 1600, 1024, 1, 1111),
+                                  (900, 16384, 512, 3, 900)])
+def test_gemm_pair_bn192_ragged_n(case, tmp_path):
+    """CTA-pair tiles 192 columns wide with a ragged last N tile (N % 192 != 0:
+    the tile's rows past N are TMA zero fill and are never stored), forced by
+    RK_GEMM_OVERRIDE in a subprocess; residual (EPI_ADD, with live rows on the
+    device) and plain-store epilogues against fp64."""
+    import os
+    import subprocess
+    import sys
+    M, N, K, epi, live = case
+    rng = np.random.default_rng(M + N)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    B = (rng.standard_normal((N, K)) / np.sqrt(K)).astype(np.float32)
+    H = rng.standard_normal((M, N)).astype(np.float32)
+    np.savez(tmp_path / "in.npz", A=A, B=B, H=H)
+    code = f"""
+import numpy as np, sys
+sys.path.insert(0, {os.getcwd()!r})
+from paper_2603_13289_b200.engine import Engine
+from tests.test_gpu_kernels import run_gemm
+e = Engine(0)
+d = np.load({str(tmp_path / "in.npz")!r})
+np.save({str(tmp_path / "out.npy")!r}, run_gemm(e, d["A"], d["B"], d["H"], {live}, {epi}))
+"""
+    key = f"{M}{'d' if live < M else ''}:{N}:{K}=192/2/1"
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, RK_GEMM_OVERRIDE=key, RK_GEMM_LOG="1"),
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "bn=192 pair=2" in r.stderr, r.stderr
+    got = np.load(tmp_path / "out.npy")
+    prod = bf16_round(A[:live]).astype(np.float64) @ bf16_round(B).astype(np.float64).T
+    ref = (H[:live] + prod) if epi == 1 else prod
+    assert np.abs(got[:live] - ref).max() / np.abs(ref).max() < 2e-5
+    if live < M:
+        assert np.array_equal(got[live:], H[live:]), "rows past the live count were written"
