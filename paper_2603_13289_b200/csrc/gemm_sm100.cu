@@ -312,6 +312,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
+  if (warp == 0 && p.rows_dev && p.m_hint > 0 && !(p.dbg & 1)) {
+    // live rows known only on the device: warm L2 with the weight k-blocks of
+    // the first unit the host's row estimate predicts (a wrong guess costs L2
+    // bandwidth only), so the ring's first loads after the wait hit L2
+    Units Uh = units_of<PAIR>(p);
+    Uh.num_m = p.m_hint;
+    Uh.total = Uh.num_m * Uh.num_n * Uh.splits;
+    Work w0;
+    if (elect_one() && get_work<PAIR>(Uh, 0, w0))
+      for (int i = 0; i < C::STAGES && w0.kb0 + i < w0.kb1; ++i)
+        tma_prefetch_2d(&tmB, (w0.kb0 + i) * kBK, w0.nt * BN + (int)rank * (BN / PAIR));
+  }
   pdl_wait();  // the prologue above overlapped the previous kernel; its outputs are visible from here
   const Units U = units_of<PAIR>(p);
 
@@ -1681,6 +1693,7 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
   make_tmap_bf16(&tb, B, (uint64_t)p.N, (uint64_t)p.K, (uint32_t)(p.bn / p.pair), (uint64_t)p.K);
   const int num_m = (p.rows_max + kBM * p.pair - 1) / (kBM * p.pair);
   const int total = num_m * ((p.N + p.bn - 1) / p.bn) * p.splits;  // units (pair units for the pair kernel)
+  p.m_hint = p.rows_dev && rows_hint > 0 ? (rows_hint + kBM * p.pair - 1) / (kBM * p.pair) : 0;
   const int slots = p.pair == 2 ? pair_slots(e->sm_count) : e->sm_count;
   const int grid = p.pair * (total < slots ? total : slots);
   if (p.epi == EPI_PART) {

@@ -24,6 +24,7 @@ struct GemmArgs {
   // swap-AB (short static M): the weights are the MMA's M side (256 rows per
   // CTA pair), the M tokens its N side in nc chunks of tc (<= 256) columns
   int swap = 0, tc = 0, nc = 1;
+  int m_hint = 0;  // live-row launches: m tiles of the host's row estimate (L2 warm-up of the first weight tiles)
   // tf32: operands are fp32 viewed as bf16 pairs (K, lda in bf16 units = 2x
   // the fp32 count), kind::tf32 MMAs (the 3xTF32 mode's K-concatenated
   // [hi|lo|hi] x [hi|hi|lo] operands); EPI_ADD / EPI_F32 only
