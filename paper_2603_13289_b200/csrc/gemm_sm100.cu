@@ -1579,8 +1579,9 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
       while (sp > 1 && (sp - 1) * ((kb + sp - 1) / sp) >= kb) --sp;
       p.splits = sp;
       if (sp > 1) {
-        p.pair = 1;
-        if (p.N % p.bn) p.bn = 64;
+        p.pair = 1;  // (1-CTA tiles are 256 / 128 / 64 wide; a 192 pair pick maps to the widest that divides N)
+        if (p.bn != 256 && p.bn != 128 && p.bn != 64) p.bn = 256;
+        while (p.bn > 64 && p.N % p.bn) p.bn /= 2;
         if (epi0 == EPI_F32)  // the reduce adds into the output: start from zero
           RK_CUDA(cudaMemset2DAsync(p.out_f32, (size_t)p.ld_out * 4, 0, (size_t)p.N * 4, p.rows_max, e->stream));
         p.epi = EPI_PART;
