@@ -33,6 +33,8 @@ int rk_debug_bench_attention_rows(rk_engine* e, const int32_t* pos, int M, int l
 /* clock64 timeline of one attention CTA (the last query tiles of head 0) on
  * the band case: out[3 roles][64 steps][8 events] (see attn_sm100.cu). */
 int rk_debug_trace_attention(rk_engine* e, int M, int T, int H, int Hkv, int dh, unsigned long long* out);
+int rk_debug_trace_attention_rows(rk_engine* e, const int32_t* pos, int M, int live, int g1, int g2, int T, int H,
+                                  int Hkv, int dh, unsigned long long* out, int max_ctas, int* n);
 int rk_debug_bench_gemm(rk_engine* e, int M, int N, int K, int epi, int iters, float* ms);
 /* clock64 timeline of CTA 0 of one GEMM: out[3][512] (role 0: producer, per
  * k-block slot acquired; 1: MMA issuer, per k-block stage full; 2: epilogue,

@@ -221,50 +221,11 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
   int* s_kmax = reinterpret_cast<int*>(bar + 14);
 
   pdl_trigger();
-  pdl_wait();  // rows_dev / positions / Q of the previous kernel
-  const int M = a.rows_dev ? *a.rows_dev : a.rows_max;
-  // grid (split part, head, tile) with the LIVE tiles in reverse order: the
-  // CTAs of the latest (longest) query tiles of every head dispatch first, all
-  // parts of a tile together; grid slots past the live tile count (sparse
-  // passes size the grid for rows_max) come last and exit at once instead of
-  // occupying the first waves
-  const int nlive = live_tiles(a, M);
-  if ((int)blockIdx.z >= nlive) return;
-  int r0, r1;
-  tile_rows(a, M, nlive - 1 - (int)blockIdx.z, r0, r1);
-  if (r1 <= r0) return;
-  if (threadIdx.x == 0) {
-    if (smem_u32(smem) & 1023) __trap();  // SW128 tiles need a 1 KB aligned base
-    *s_kmax = -1;
-  }
-  __syncthreads();
-  for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) atomicMax(s_kmax, a.pos[i]);
-  __syncthreads();
-  // GQA packing: the CTA's 128 TMEM lanes hold rq rows x `group` q heads of
-  // one kv head (lane = head_local * rq + row), so every K/V tile is staged
-  // once for all heads of its group and a tile spans only rq positions
-  // (tighter causal bound for gathered sparse rows). group 1: rq = 128 rows
-  // of head blockIdx.y.
-  const int G = a.group, rq = a.rq;
-  const int part = blockIdx.x;  // split-KV part (fastest grid dim: a tile's parts dispatch together)
-  const int kvh = G > 1 ? (int)blockIdx.y : (int)blockIdx.y / (a.H / a.Hkv);
-  const int h0 = G > 1 ? kvh * G : (int)blockIdx.y;  // first q head of the CTA
-  // Adaptive split-KV: a tile whose key range exceeds tiles_per_split key
-  // tiles is cut into ts = ceil(nk_tile / tiles_per_split) (<= gridDim.x)
-  // equal parts; CTA x covers part x, and the last part to finish merges them
-  // (in-kernel, below). Tiles that fit in one part write their output directly.
-  constexpr int KEYS = C::KEYS;
-  const int nk_tile = *s_kmax / KEYS + 1;
-  const int ts = min((int)gridDim.x, (nk_tile + a.tiles_per_split - 1) / a.tiles_per_split);
-  const int tps = (nk_tile + ts - 1) / ts;
-  const int ts_eff = (nk_tile + tps - 1) / tps;  // parts that own key tiles
-  const int j0 = part * tps;
-  const int nk = min(nk_tile - j0, tps);
-  const bool partial = ts_eff > 1;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const bool trace_cta = TRACE && a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
-  if (part >= ts_eff || nk <= 0) return;  // this tile has no such part
-
+  uint64_t t_entry = 0, t_wait = 0;  // (TRACE: per-CTA global-timer span, after the 1536 event slots)
+  if (TRACE) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_entry));
+  const long long c_entry = TRACE ? clock64() : 0;
+  // shared-memory setup overlaps the previous kernel's tail (before the wait)
   if (warp == 4 && lane == 0) {
     tma_prefetch(&tmQ);
     tma_prefetch(&tmK);
@@ -282,18 +243,82 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
     mbar_init(o_done, 1);
     fence_barrier_init();
   }
+  if (threadIdx.x == 0) {
+    if (smem_u32(smem) & 1023) __trap();  // SW128 tiles need a 1 KB aligned base
+    *s_kmax = -1;
+  }
+  pdl_wait();  // rows_dev / positions / Q of the previous kernel
+  if (TRACE) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_wait));
+  const bool tr_cta = TRACE && a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0;
+  const int M = a.rows_dev ? *a.rows_dev : a.rows_max;
+  // grid (split part, head, tile) with the LIVE tiles in reverse order: the
+  // CTAs of the latest (longest) query tiles of every head dispatch first, all
+  // parts of a tile together; grid slots past the live tile count (sparse
+  // passes size the grid for rows_max) come last and exit at once instead of
+  // occupying the first waves
+  const int nlive = live_tiles(a, M);
+  if ((int)blockIdx.z >= nlive) return;
+  int r0, r1;
+  tile_rows(a, M, nlive - 1 - (int)blockIdx.z, r0, r1);
+  if (r1 <= r0) return;
+  // GQA packing: the CTA's 128 TMEM lanes hold rq rows x `group` q heads of
+  // one kv head (lane = head_local * rq + row), so every K/V tile is staged
+  // once for all heads of its group and a tile spans only rq positions
+  // (tighter causal bound for gathered sparse rows). group 1: rq = 128 rows
+  // of head blockIdx.y.
+  const int G = a.group, rq = a.rq;
+  const int part = blockIdx.x;  // split-KV part (fastest grid dim: a tile's parts dispatch together)
+  const int kvh = G > 1 ? (int)blockIdx.y : (int)blockIdx.y / (a.H / a.Hkv);
+  const int h0 = G > 1 ? kvh * G : (int)blockIdx.y;  // first q head of the CTA
+  constexpr int KEYS = C::KEYS;
+  constexpr int DB = DH / 64;  // 64-wide swizzle blocks along d
+  __syncthreads();  // barriers initialised
+  // Part 0 of a live tile always owns key tile 0, so its Q and first K tile
+  // go out now; their latency overlaps the key-bound scan and TMEM allocation.
+  const bool early = part == 0;
+  if (early && warp == 6 && elect_one()) {
+    mbar_arrive_expect_tx(q_full, G * rq * DH * 2);
+    for (int hl = 0; hl < G; ++hl)
+      for (int b = 0; b < DB; ++b)
+        tma_load_2d(smem + C::OFF_Q + b * kQ * 128 + hl * rq * 128, &tmQ, q_full, (h0 + hl) * DH + b * 64, r0);
+  }
+  if (early && warp == 4 && elect_one()) {
+    mbar_arrive_expect_tx(&k_full[0], C::KV_BYTES);
+    for (int b = 0; b < DB; ++b)
+      tma_load_2d(smem + C::OFF_K + b * KEYS * 128, &tmK, &k_full[0], kvh * DH + b * 64, 0);
+  }
+  for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) atomicMax(s_kmax, a.pos[i]);
+  __syncthreads();
+  if (tr_cta) {  // prologue marks (role 1 slots: one tile per CTA leaves them free)
+    a.trace[(64 + 0) * 8 + 0] = c_entry;
+    a.trace[(64 + 0) * 8 + 1] = clock64();
+  }
+  // Adaptive split-KV: a tile whose key range exceeds tiles_per_split key
+  // tiles is cut into ts = ceil(nk_tile / tiles_per_split) (<= gridDim.x)
+  // equal parts; CTA x covers part x, and the last part to finish merges them
+  // (in-kernel, below). Tiles that fit in one part write their output directly.
+  const int nk_tile = *s_kmax / KEYS + 1;
+  const int ts = min((int)gridDim.x, (nk_tile + a.tiles_per_split - 1) / a.tiles_per_split);
+  const int tps = (nk_tile + ts - 1) / ts;
+  const int ts_eff = (nk_tile + tps - 1) / tps;  // parts that own key tiles
+  const int j0 = part * tps;
+  const int nk = min(nk_tile - j0, tps);
+  const bool partial = ts_eff > 1;
+  const bool trace_cta = TRACE && a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
+  if (part >= ts_eff || nk <= 0) return;  // this tile has no such part (never part 0: no TMA in flight)
+
   if (warp == 5) tmem_alloc(tmem_slot, C::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  constexpr int DB = DH / 64;  // 64-wide swizzle blocks along d
+  if (tr_cta) a.trace[(64 + 0) * 8 + 2] = clock64();
 
   if (warp >= 4) {  // ------------------------------------------ control warpgroup
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(C::REG_CTL) : "memory");
     if (warp == 4) {
       if (elect_one()) {  // ---------------------------------------- TMA K
-        for (int j = 0; j < nk; ++j) {
+        for (int j = early ? 1 : 0; j < nk; ++j) {  // (part 0: K tile 0 already issued)
           const int st = j & 1;
           mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
           uint8_t* sk = smem + C::OFF_K + st * C::KV_BYTES;
@@ -304,10 +329,12 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
       }
     } else if (warp == 6) {
       if (elect_one()) {  // ------------------------------------- TMA Q, V
-        mbar_arrive_expect_tx(q_full, G * rq * DH * 2);
-        for (int hl = 0; hl < G; ++hl)
-          for (int b = 0; b < DB; ++b)
-            tma_load_2d(smem + C::OFF_Q + b * kQ * 128 + hl * rq * 128, &tmQ, q_full, (h0 + hl) * DH + b * 64, r0);
+        if (!early) {
+          mbar_arrive_expect_tx(q_full, G * rq * DH * 2);
+          for (int hl = 0; hl < G; ++hl)
+            for (int b = 0; b < DB; ++b)
+              tma_load_2d(smem + C::OFF_Q + b * kQ * 128 + hl * rq * 128, &tmQ, q_full, (h0 + hl) * DH + b * 64, r0);
+        }
         for (int j = 0; j < nk; ++j) {
           const int st = j & 1;
           mbar_wait(&v_empty[st], ((j >> 1) & 1) ^ 1);
@@ -477,6 +504,7 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
     }
     mbar_wait(o_done, (nk - 1) & 1);
     tc_fence_after();
+    if (tracing) a.trace[(64 + 0) * 8 + 3] = clock64();
     if (partial) {
       // in-kernel merge: partials in a tile-contiguous block [tile][part][lane][DH]
       // (one 128 x DH fp32 block per part); the last part of this (tile, kv
@@ -502,6 +530,7 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
       int* cnt = a.tile_cnt + tid;
       if (rl == 0) *s_last = atomicAdd(cnt, 1) == ts_eff - 1;
       named_bar_sync(1, 128);
+      if (tracing) a.trace[(64 + 0) * 8 + 4] = clock64();
       if (*s_last) {
         fence_acq_rel_gpu();  // (acquire: every part's partials)
         if (rl == 0) *cnt = 0;  // self-resetting for the next launch
@@ -537,6 +566,7 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
         else if (ts_eff <= 8) chk = attn_merge_stream<DH, 8>(a, src, wsm, rl, ts_eff, r0, r1, rq, G, h0);
         else chk = attn_merge_stream<DH, 16>(a, src, wsm, rl, ts_eff, r0, r1, rq, G, h0);
         if (chk != chk && a.status) *reinterpret_cast<volatile int*>(a.status) = 1;
+        if (tracing) a.trace[(64 + 0) * 8 + 5] = clock64();
       }
     } else {
       const float inv = 1.f / l_run;
@@ -559,11 +589,24 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
         }
       }
       if (valid && chk != chk && a.status) *reinterpret_cast<volatile int*>(a.status) = 1;
+      if (tracing) a.trace[(64 + 0) * 8 + 5] = clock64();
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 5) tmem_dealloc(tmem, C::TMEM_COLS);
+  if (tr_cta) a.trace[(64 + 0) * 8 + 6] = clock64();
+  if (TRACE && a.trace && threadIdx.x == 0) {
+    uint64_t t_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    const size_t cid = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    unsigned long long* ct = a.trace + 1536 + 4 * cid;
+    ct[0] = t_entry;
+    ct[1] = t_wait;
+    ct[2] = t_end;
+    ct[3] = (unsigned long long)nk | ((unsigned long long)partial << 8) | ((unsigned long long)ts_eff << 16) |
+            ((unsigned long long)(r1 - r0) << 32);
+  }
 }
 
 // Normalised attention probabilities over a window of segment keys for the

@@ -192,6 +192,50 @@ int rk_debug_bench_attention_rows(rk_engine* e, const int32_t* pos, int M, int l
   });
 }
 
+// Per-CTA global-timer spans of one attention launch over a rows layout (as
+// rk_debug_bench_attention_rows): out[4 * cta] = {entry, after the dependency
+// wait, end, nk | partial << 8 | parts << 16 | rows << 32}; CTAs that exit
+// early (dead tiles / parts) stay 0; out[0, 1536) holds CTA (0,0,0)'s event slots
+// (rk_debug_trace_attention layout) first. out must hold 1536 + 4 * max_ctas.
+int rk_debug_trace_attention_rows(rk_engine* e, const int32_t* pos, int M, int live, int g1, int g2, int T, int H,
+                                  int Hkv, int dh, unsigned long long* out, int max_ctas, int* n) {
+  return guard([&] {
+    cudaStream_t st = e->stream;
+    const size_t nq = (size_t)M * H * dh, nk = (size_t)T * Hkv * dh;
+    DevBuf f((nq > nk ? nq : nk) * 4), qb(nq * 2), kb(nk * 2), vb(nk * 2), o(nq * 2), p(M * 4 + 16),
+        tr((1536 + 4 * (size_t)max_ctas) * 8);
+    k::init_uniform(st, f.as<float>(), nq, 11, 1.0f);
+    k::f32_to_bf16(st, qb.as<__nv_bfloat16>(), f.as<float>(), nq);
+    k::init_uniform(st, f.as<float>(), nk, 12, 1.0f);
+    k::f32_to_bf16(st, kb.as<__nv_bfloat16>(), f.as<float>(), nk);
+    k::init_uniform(st, f.as<float>(), nk, 13, 1.0f);
+    k::f32_to_bf16(st, vb.as<__nv_bfloat16>(), f.as<float>(), nk);
+    RK_CUDA(cudaMemcpy(p.p, pos, M * 4, cudaMemcpyHostToDevice));
+    RK_CUDA(cudaMemcpy(p.as<int>() + M, &live, 4, cudaMemcpyHostToDevice));
+    AttnArgs a;
+    a.q = qb.as<__nv_bfloat16>();
+    a.out = o.as<__nv_bfloat16>();
+    a.pos = p.as<int>();
+    a.rows_max = M;
+    a.rows_dev = live < M ? p.as<int>() + M : nullptr;
+    a.g1 = g1;
+    a.g2 = g2;
+    a.H = H;
+    a.Hkv = Hkv;
+    a.dh = dh;
+    a.scale_log2 = 1.4426950408889634f / std::sqrt((float)dh);
+    attention_bf16(e, a, kb.as<__nv_bfloat16>(), vb.as<__nv_bfloat16>(), T);  // warm
+    RK_CUDA(cudaMemsetAsync(tr.p, 0, tr.bytes, st));
+    RK_CUDA(cudaStreamSynchronize(st));
+    a.trace = tr.as<unsigned long long>();
+    attention_bf16(e, a, kb.as<__nv_bfloat16>(), vb.as<__nv_bfloat16>(), T);
+    RK_CUDA(cudaStreamSynchronize(st));
+    RK_CUDA(cudaGetLastError());
+    RK_CUDA(cudaMemcpy(out, tr.p, tr.bytes, cudaMemcpyDeviceToHost));  // event slots, then the CTA spans
+    *n = max_ctas;
+  });
+}
+
 int rk_debug_trace_attention(rk_engine* e, int M, int T, int H, int Hkv, int dh, unsigned long long* out) {
   return guard([&] {
     cudaStream_t st = e->stream;
