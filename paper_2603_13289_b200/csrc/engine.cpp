@@ -9,6 +9,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <chrono>
 #include <cstring>
 #include <atomic>
 #include <future>
@@ -154,6 +155,7 @@ rk_engine::~rk_engine() {
   scratch.reset();
   rope.clear();
   if (pinned) cudaFreeHost(pinned);
+  if (results_host) cudaFreeHost(results_host);
   if (side) {
     cudaStreamSynchronize(side);
     cudaStreamDestroy(side);
@@ -1119,15 +1121,26 @@ int rk_agent_prefill(rk_engine* e, rk_weights* w, rk_context* ctx, const int32_t
     DeviceGuard g(e->device);
     require(opts != nullptr && ctx != nullptr, RK_ERR_INVALID_ARGUMENT, "null argument");
     require(ctx->size == 0, RK_ERR_INVALID_ARGUMENT, "agent prefill: context must be empty");
+    static const bool host_timing = std::getenv("RK_HOST_TIMING") != nullptr;  // (diagnostic: stderr)
+    const auto t0 = std::chrono::steady_clock::now();
     Runner r(e, w);
     std::vector<ExtendResult> results;
     r.agent_prefill(ctx, prefix, n_prefix, ups, n_up, suffix, n_suffix, profile, *opts, results);
+    r.stage_results(results, first_token != nullptr);
+    const auto t1 = std::chrono::steady_clock::now();
     r.finish();
+    const auto t2 = std::chrono::steady_clock::now();
     for (auto& res : results) r.resolve(res);
     if (outs)
       for (size_t u = 0; u < results.size(); ++u) r.fill_output(results[u], ctx, &outs[u]);
     if (end_logits) r.download_logits(end_logits);
     if (first_token) *first_token = r.first_token();
+    if (host_timing) {
+      const auto t3 = std::chrono::steady_clock::now();
+      auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+      std::fprintf(stderr, "[host] agent_prefill enqueue %.1f us, wait %.1f us, after %.1f us\n", us(t0, t1),
+                   us(t1, t2), us(t2, t3));
+    }
   });
 }
 

@@ -106,6 +106,10 @@ struct rk_engine {
   // pinned host staging
   void* pinned = nullptr;
   size_t pinned_bytes = 0;
+  // pinned landing area of a call's small results (selection counts, threshold,
+  // first token), copied in stream order before the call's final synchronize
+  void* results_host = nullptr;
+  static constexpr size_t kResultsBytes = 4096;
   rk::DevBuf status;  // int flags: [0] non-finite
   std::vector<cudaEvent_t> events;
   std::vector<std::unique_ptr<rk::ExtendSlot>> slots;
@@ -266,6 +270,15 @@ void mark_layers(cudaStream_t s, uint8_t* origin, int len, int layer_lo, int lay
 void zero_dev(cudaStream_t s, void* dst, size_t bytes);
 void zero_many(cudaStream_t s, const std::vector<std::pair<void*, size_t>>& bufs);  // one launch
 void copy_dev(cudaStream_t s, void* dst, const void* src, size_t bytes);
+// up to 16 small copies (e.g. into mapped pinned host memory) in one launch:
+// no copy engine, so they never queue behind bulk uploads
+struct SmallCopies {
+  const void* src[16];
+  void* dst[16];
+  int bytes[16];
+  int n = 0;
+};
+void small_copies(cudaStream_t s, const SmallCopies& c);
 // decode capture (graph-replayed steps; see Runner::capture_decode)
 void decode_step_begin(cudaStream_t s, const int* step, int src, const int* tokens, int* cur_tok, int* pos);
 void decode_step_end(cudaStream_t s, int* step, int n, int L, size_t row_bytes, const void* stage_k,

@@ -1140,6 +1140,17 @@ void decode_step_end(cudaStream_t s, int* step, int n, int L, size_t row_bytes, 
              static_cast<uint32_t*>(v), (int)(hid_bytes / 4), static_cast<const uint32_t*>(stage_h),
              static_cast<uint32_t*>(hidden), next_tok, tokens);
 }
+__global__ void small_copies_kernel(const SmallCopies c) {
+  sm100::pdl_trigger();
+  sm100::pdl_wait();
+  const int i = blockIdx.x;
+  const uint8_t* src = static_cast<const uint8_t*>(c.src[i]);
+  uint8_t* dst = static_cast<uint8_t*>(c.dst[i]);
+  for (int b = threadIdx.x; b < c.bytes[i]; b += blockDim.x) dst[b] = src[b];
+}
+void small_copies(cudaStream_t s, const SmallCopies& c) {
+  if (c.n > 0) launch_pdl(small_copies_kernel, dim3((unsigned)c.n), dim3(64), 0, s, c);
+}
 void copy_dev(cudaStream_t s, void* dst, const void* src, size_t bytes) {
   if (!bytes) return;
   const size_t blocks = std::min<size_t>(1184, (bytes / 16 + kThreads - 1) / kThreads + 1);

@@ -21,6 +21,7 @@ struct ExtendResult {
   // host copies after finish()
   int info[8] = {0};
   double dinfo[2] = {0, 0};
+  int staged = -1;  // byte offset of info/dinfo in rk_engine::results_host (stage_results), -1: not staged
   rk_reuse_stats stats{};
 };
 
@@ -56,6 +57,10 @@ class Runner {
                            uint64_t snapshot, bool include_self);
 
   // Synchronize, raise on device-side errors, resolve pending ExtendResults.
+  // queue the results' small device values (and the first token) for one
+  // asynchronous copy each into pinned memory ahead of finish(), so resolve()
+  // and first_token() need no further device round trips
+  void stage_results(std::vector<ExtendResult>& rs, bool token);
   void finish();
   void resolve(ExtendResult& r);  // after finish(): counts, stats, timings
   // expected live rows of a sparse pass over `head` fixed rows plus the
@@ -110,6 +115,7 @@ class Runner {
   // bf16 path: the last layer left its rows' fused-RMSNorm inputs (bf16 rows,
   // 1/rms) for the same row set; cleared whenever the rows or hidden change.
   bool prepared_ = false;
+  bool token_staged_ = false, status_staged_ = false;
 };
 
 // weights_export helper: unpack tensor idx of the engine layout to fp32 [rows x cols].

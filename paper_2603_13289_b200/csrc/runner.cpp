@@ -581,12 +581,51 @@ ExtendResult Runner::relay_extend(rk_context* ctx, rk_cache* cache, const rk_lay
   return r;
 }
 
+void Runner::stage_results(std::vector<ExtendResult>& rs, bool token) {
+  if (!e_->results_host) RK_CUDA(cudaMallocHost(&e_->results_host, rk_engine::kResultsBytes));
+  uint8_t* h = nullptr;  // the device's view of the pinned area (a kernel writes it over PCIe)
+  RK_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h), e_->results_host, 0));
+  k::SmallCopies c;
+  auto add = [&](void* dst, const void* src, int bytes) {
+    c.src[c.n] = src;
+    c.dst[c.n] = dst;
+    c.bytes[c.n] = bytes;
+    ++c.n;
+  };
+  size_t off = 64;  // [0, 4): first token, [8, 16): status flags
+  for (auto& r : rs) {
+    if (!(r.mode == RK_MODE_RELAY || r.mode == RK_MODE_BLEND)) continue;
+    if (c.n + 3 > 16 || off + sizeof r.info + sizeof r.dinfo > rk_engine::kResultsBytes) break;  // (rest: resolve copies)
+    ExtendSlot& X = slot(r.slot);
+    add(h + off, X.info.p, (int)sizeof r.info);
+    add(h + off + sizeof r.info, X.dinfo.p, (int)sizeof r.dinfo);
+    r.staged = (int)off;
+    off += sizeof r.info + sizeof r.dinfo;
+  }
+  if (token && e_->scratch->argmax.p) {
+    add(h, e_->scratch->argmax.p, 4);
+    token_staged_ = true;
+  }
+  add(h + 8, e_->status.p, 8);  // the non-finite flags finish() checks
+  status_staged_ = true;
+  // the threshold report (dinfo) runs on the side stream (k::select_relay)
+  if (e_->side_join) RK_CUDA(cudaStreamWaitEvent(st_, e_->side_join, 0));
+  k::small_copies(st_, c);
+  e_->launches += c.n > 0;
+}
+
 void Runner::resolve(ExtendResult& r) {
   const rk_model_spec& s = w_->s;
   ExtendSlot& X = slot(r.slot);
   if (r.mode == RK_MODE_RELAY || r.mode == RK_MODE_BLEND) {
-    RK_CUDA(cudaMemcpy(r.info, X.info.p, sizeof r.info, cudaMemcpyDeviceToHost));
-    RK_CUDA(cudaMemcpy(r.dinfo, X.dinfo.p, sizeof r.dinfo, cudaMemcpyDeviceToHost));
+    if (r.staged >= 0) {  // landed with finish()'s synchronize
+      const uint8_t* h = static_cast<const uint8_t*>(e_->results_host) + r.staged;
+      std::memcpy(r.info, h, sizeof r.info);
+      std::memcpy(r.dinfo, h + sizeof r.info, sizeof r.dinfo);
+    } else {
+      RK_CUDA(cudaMemcpy(r.info, X.info.p, sizeof r.info, cudaMemcpyDeviceToHost));
+      RK_CUDA(cudaMemcpy(r.dinfo, X.dinfo.p, sizeof r.dinfo, cudaMemcpyDeviceToHost));
+    }
   }
   const uint64_t count = (r.mode == RK_MODE_RELAY || r.mode == RK_MODE_BLEND) ? (uint64_t)r.info[0] : 0;
   rk_reuse_stats& st = r.stats;
@@ -1136,7 +1175,8 @@ void Runner::finish() {
   if (e_->side) RK_CUDA(cudaStreamSynchronize(e_->side));
   RK_CUDA(cudaGetLastError());
   int flags[2] = {0, 0};
-  RK_CUDA(cudaMemcpy(flags, e_->status.p, sizeof flags, cudaMemcpyDeviceToHost));
+  if (status_staged_) std::memcpy(flags, static_cast<const uint8_t*>(e_->results_host) + 8, sizeof flags);
+  else RK_CUDA(cudaMemcpy(flags, e_->status.p, sizeof flags, cudaMemcpyDeviceToHost));
   if (flags[0]) raise(RK_ERR_NONFINITE, "matmul: non-finite value");
 }
 
@@ -1179,7 +1219,8 @@ void Runner::download_logits(float* dst) {
 
 int32_t Runner::first_token() {
   int32_t t = 0;
-  RK_CUDA(cudaMemcpy(&t, e_->scratch->argmax.p, 4, cudaMemcpyDeviceToHost));
+  if (token_staged_) std::memcpy(&t, e_->results_host, 4);
+  else RK_CUDA(cudaMemcpy(&t, e_->scratch->argmax.p, 4, cudaMemcpyDeviceToHost));
   return t;
 }
 
