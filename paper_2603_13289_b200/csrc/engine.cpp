@@ -1130,7 +1130,7 @@ int rk_agent_prefill(rk_engine* e, rk_weights* w, rk_context* ctx, const int32_t
     const auto t1 = std::chrono::steady_clock::now();
     r.finish();
     const auto t2 = std::chrono::steady_clock::now();
-    for (auto& res : results) r.resolve(res);
+    for (auto& res : results) r.resolve(res, outs != nullptr);  // (wall timings only reach the caller via outs)
     if (outs)
       for (size_t u = 0; u < results.size(); ++u) r.fill_output(results[u], ctx, &outs[u]);
     if (end_logits) r.download_logits(end_logits);

@@ -62,7 +62,7 @@ class Runner {
   // and first_token() need no further device round trips
   void stage_results(std::vector<ExtendResult>& rs, bool token);
   void finish();
-  void resolve(ExtendResult& r);  // after finish(): counts, stats, timings
+  void resolve(ExtendResult& r, bool timings = true);  // after finish(): counts, stats (+ event timings)
   // expected live rows of a sparse pass over `head` fixed rows plus the
   // selected ones of `seg` segment rows: the last observed selection fraction,
   // 0 when none was observed yet (the grids cover rows_max regardless; the

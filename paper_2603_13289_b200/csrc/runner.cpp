@@ -614,7 +614,7 @@ void Runner::stage_results(std::vector<ExtendResult>& rs, bool token) {
   e_->launches += c.n > 0;
 }
 
-void Runner::resolve(ExtendResult& r) {
+void Runner::resolve(ExtendResult& r, bool timings) {
   const rk_model_spec& s = w_->s;
   ExtendSlot& X = slot(r.slot);
   if (r.mode == RK_MODE_RELAY || r.mode == RK_MODE_BLEND) {
@@ -651,7 +651,7 @@ void Runner::resolve(ExtendResult& r) {
     st.flops_cost = rk_flops_segment_schedule(&s, r.base, r.n, r.l_start, r.l_det, r.sparse_hi, count);
   auto ms = [&](int a, int b) {
     float v = 0.f;
-    if (a >= 0 && b >= 0) RK_CUDA(cudaEventElapsedTime(&v, e_->events[a], e_->events[b]));
+    if (timings && a >= 0 && b >= 0) RK_CUDA(cudaEventElapsedTime(&v, e_->events[a], e_->events[b]));
     return static_cast<double>(v);
   };
   st.wall.realign_ms = ms(r.ev_begin, r.ev_realign);
