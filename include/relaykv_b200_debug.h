@@ -48,6 +48,11 @@ int rk_debug_select_relay(rk_engine* e, const double* s_dev, const float* influe
 /* top_k_by_score (selector.cpp:90-105) on the device (radix select):
    the `count` largest scores, ties by ascending index, as an ascending list */
 int rk_debug_select_topk(rk_engine* e, const double* score, int n, int count, int32_t* sel_idx, int32_t* out_count);
+/* K2 deviation scores at l_det (k::score_deviation) on host rows: elem 2 =
+   bf16 bit patterns, 4 = fp32; rope = [base + n][dh / 2] {cos, sin} doubles */
+int rk_debug_score_deviation(rk_engine* e, const void* ctx_v, const void* cache_v, const void* ctx_k,
+                             const void* cache_kpre, int elem, int n, int heads, int dh, const double* rope, int base,
+                             double* s_dev, double* s_key);
 /* y[i] = device glibc_expf(x[i]) */
 int rk_debug_expf(rk_engine* e, const float* x, float* y, uint64_t n);
 /* Host only: the upload path's fp32 -> bf16 conversion on a `threads`-worker pool. */

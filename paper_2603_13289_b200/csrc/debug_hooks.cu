@@ -390,6 +390,29 @@ int rk_debug_trace_gemm(rk_engine* e, int M, int N, int K, int epi, unsigned lon
   });
 }
 
+// K2 deviation scores (k::score_deviation) on host rows: elem 2 = bf16 rows
+// (uint16 bit patterns), 4 = fp32; rope = [base + n][dh / 2] {cos, sin} doubles.
+int rk_debug_score_deviation(rk_engine* e, const void* ctx_v, const void* cache_v, const void* ctx_k,
+                             const void* cache_kpre, int elem, int n, int heads, int dh, const double* rope, int base,
+                             double* s_dev, double* s_key) {
+  return guard([&] {
+    cudaStream_t st = e->stream;
+    const size_t bytes = (size_t)n * heads * dh * elem, rbytes = (size_t)(base + n) * dh / 2 * 16;
+    DevBuf a(bytes), b(bytes), c(bytes), d(bytes), r(rbytes), sd((size_t)n * 8), sk((size_t)n * 8);
+    RK_CUDA(cudaMemcpy(a.p, ctx_v, bytes, cudaMemcpyHostToDevice));
+    RK_CUDA(cudaMemcpy(b.p, cache_v, bytes, cudaMemcpyHostToDevice));
+    RK_CUDA(cudaMemcpy(c.p, ctx_k, bytes, cudaMemcpyHostToDevice));
+    RK_CUDA(cudaMemcpy(d.p, cache_kpre, bytes, cudaMemcpyHostToDevice));
+    RK_CUDA(cudaMemcpy(r.p, rope, rbytes, cudaMemcpyHostToDevice));
+    k::score_deviation(st, a.p, b.p, c.p, d.p, (size_t)elem, n, heads * dh, heads, dh, r.as<double2>(), base,
+                       sd.as<double>(), sk.as<double>());
+    RK_CUDA(cudaStreamSynchronize(st));
+    RK_CUDA(cudaGetLastError());
+    RK_CUDA(cudaMemcpy(s_dev, sd.p, (size_t)n * 8, cudaMemcpyDeviceToHost));
+    RK_CUDA(cudaMemcpy(s_key, sk.p, (size_t)n * 8, cudaMemcpyDeviceToHost));
+  });
+}
+
 int rk_debug_select_topk(rk_engine* e, const double* score, int n, int count, int32_t* sel_idx, int32_t* out_count) {
   return guard([&] {
     cudaStream_t st = e->stream;

@@ -673,6 +673,85 @@ __global__ void __launch_bounds__(256) score_dh_kernel(const T* __restrict__ ctx
   }
 }
 
+// bf16 storage (the throughput mode, whose K/V already differ from the
+// reference's): one warp per (token, {V,K}) row, EPL = kv/32 elements per lane
+// (one head spans DH/EPL lanes), 16-byte loads, per-lane double partial sums
+// combined across the head's lanes by shuffles, heads summed in order. The
+// key rotation is the double one of realign() (same bf16 rounding), so an
+// unchanged key still scores exactly 1. Not the reference's sequential order
+// (the fp32-exact path keeps score_dh_kernel): ~1e-16 relative on a cosine.
+// The per-thread sequential double loops were latency-bound at ~0.08 of HBM.
+template <int DH, int EPL>
+__global__ void __launch_bounds__(256) score_bf16_warp_kernel(const __nv_bfloat16* __restrict__ ctx_v,
+                                                              const __nv_bfloat16* __restrict__ cache_v,
+                                                              const __nv_bfloat16* __restrict__ ctx_k,
+                                                              const __nv_bfloat16* __restrict__ cache_kpre, int n,
+                                                              int heads, const double2* __restrict__ rope, int base,
+                                                              double* __restrict__ s_dev, double* __restrict__ s_key) {
+  sm100::pdl_trigger();
+  constexpr int LPH = DH / EPL;  // lanes per head
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
+  const int j = gw >> 1, which = gw & 1;  // row j, 0 = V, 1 = K
+  if (j >= n) return;
+  const int e0 = (lane % LPH) * EPL;  // first element within the head
+  // the (constant) cos/sin of the key rotation load before the dependency wait
+  double2 cs[EPL / 2];
+  if (which == 1) {
+    const double2* cr = rope + (size_t)(base + j) * (DH / 2) + e0 / 2;
+#pragma unroll
+    for (int i = 0; i < EPL / 2; ++i) cs[i] = __ldg(cr + i);
+  }
+  sm100::pdl_wait();
+  const int kv = heads * DH;
+  const size_t off = (size_t)j * kv + (size_t)lane * EPL;
+  const __nv_bfloat16* a = (which == 0 ? ctx_v : ctx_k) + off;
+  const __nv_bfloat16* b = (which == 0 ? cache_v : cache_kpre) + off;
+  uint4 x[EPL / 8], y[EPL / 8];
+#pragma unroll
+  for (int i = 0; i < EPL / 8; ++i) {
+    x[i] = __ldcs(reinterpret_cast<const uint4*>(a) + i);
+    y[i] = __ldcs(reinterpret_cast<const uint4*>(b) + i);
+  }
+  double dot = 0.0, na = 0.0, nb = 0.0;
+  bool same = true;
+#pragma unroll
+  for (int i = 0; i < EPL; i += 2) {
+    const __nv_bfloat16* xp = reinterpret_cast<const __nv_bfloat16*>(x);
+    const __nv_bfloat16* yp = reinterpret_cast<const __nv_bfloat16*>(y);
+    const float x0 = __bfloat162float(xp[i]), x1 = __bfloat162float(xp[i + 1]);
+    float y0 = __bfloat162float(yp[i]), y1 = __bfloat162float(yp[i + 1]);
+    if (which == 1) {  // realigned key, bit-identical to realign()
+      const double2 c = cs[i / 2];
+      const double r0 = __dsub_rn(__dmul_rn(c.x, (double)y0), __dmul_rn(c.y, (double)y1));
+      const double r1 = __dadd_rn(__dmul_rn(c.y, (double)y0), __dmul_rn(c.x, (double)y1));
+      y0 = __bfloat162float(__float2bfloat16_rn(__double2float_rn(r0)));
+      y1 = __bfloat162float(__float2bfloat16_rn(__double2float_rn(r1)));
+    }
+    same = same && __float_as_uint(x0) == __float_as_uint(y0) && __float_as_uint(x1) == __float_as_uint(y1);
+    dot = fma((double)x0, (double)y0, fma((double)x1, (double)y1, dot));
+    na = fma((double)x0, (double)x0, fma((double)x1, (double)x1, na));
+    nb = fma((double)y0, (double)y0, fma((double)y1, (double)y1, nb));
+  }
+#pragma unroll
+  for (int o = LPH / 2; o; o >>= 1) {  // within the head's lanes
+    dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    na += __shfl_xor_sync(0xffffffffu, na, o);
+    nb += __shfl_xor_sync(0xffffffffu, nb, o);
+  }
+  // every lane of a head now holds its sums; the head's cosine
+  const unsigned head_mask = (LPH == 32 ? 0xffffffffu : ((1u << LPH) - 1u)) << (lane / LPH * LPH);
+  same = (__ballot_sync(0xffffffffu, !same) & head_mask) == 0;  // every element of the head unchanged
+  const double sa = sqrt(na), sb = sqrt(nb);
+  double c;
+  if (sa < 1e-12 || sb < 1e-12) c = 0.0;
+  else if (same) c = 1.0;
+  else c = fmin(1.0, fmax(-1.0, dot / (sa * sb)));
+  // heads summed in order by lane 0 (head h's value from lane h * LPH)
+  double acc = 0.0;
+  for (int h = 0; h < heads; ++h) acc += __shfl_sync(0xffffffffu, c, h * LPH);
+  if (lane == 0) (which == 0 ? s_dev : s_key)[j] = 1.0 - acc / (double)heads;
+}
+
 // ---------------------------------------------------------------------------
 // K2b selection (selector.cpp:32-88): mean-relative thresholds with the
 // reference's sequential double mean, suffix window, sorted union with tag
@@ -1318,6 +1397,23 @@ void score_deviation(cudaStream_t s, const void* ctx_v, const void* cache_v, con
   const size_t row = (size_t)kv * elem;
   const bool aligned = ((reinterpret_cast<uintptr_t>(ctx_v) | reinterpret_cast<uintptr_t>(cache_v) |
                          reinterpret_cast<uintptr_t>(ctx_k) | reinterpret_cast<uintptr_t>(cache_kpre)) & 15) == 0;
+  if (aligned && elem == 2 && (dh == 64 || dh == 128) && kv % 256 == 0 && kv / 32 <= dh && dh % (kv / 32) == 0 &&
+      kv / 32 <= 32) {
+    const int warps = 2 * n, grid = (warps * 32 + 255) / 256;
+#define RK_SCORE_W(D, E)                                                                                         \
+  launch_pdl(score_bf16_warp_kernel<D, E>, dim3(grid), dim3(256), 0, s, (const __nv_bfloat16*)ctx_v,             \
+             (const __nv_bfloat16*)cache_v, (const __nv_bfloat16*)ctx_k, (const __nv_bfloat16*)cache_kpre, n,    \
+             heads, rope, base, s_dev, s_key)
+    const int epl = kv / 32;
+    if (dh == 64 && epl == 8) RK_SCORE_W(64, 8);
+    else if (dh == 64 && epl == 16) RK_SCORE_W(64, 16);
+    else if (dh == 64 && epl == 32) RK_SCORE_W(64, 32);
+    else if (dh == 128 && epl == 8) RK_SCORE_W(128, 8);
+    else if (dh == 128 && epl == 16) RK_SCORE_W(128, 16);
+    else RK_SCORE_W(128, 32);
+#undef RK_SCORE_W
+    return;
+  }
   if (aligned && (dh == 64 || dh == 128) && 2 * heads <= 256) {
     // tokens per CTA: at most 256 threads, and few enough that the grid covers
     // every SM about twice (the per-thread double loops are latency-bound)
