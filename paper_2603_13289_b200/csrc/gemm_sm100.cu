@@ -27,8 +27,9 @@
 //             buffer, K/V rows scattered into the context at each row's
 //             absolute position (model.cpp:266-269), optional capture of
 //             pre-RoPE K and V (decode-time capture, model.cpp:254-257)
-//   EPI_ADD   hidden += D (residual); split-K partials are added in split
-//             order (deterministic) via per-tile flags
+//   EPI_ADD   hidden += D (residual) + the next RMSNorm's bf16 rows and 1/rms;
+//             split-K residual GEMMs write EPI_PART partials instead, summed
+//             in split order (deterministic) by splitk_reduce_add_kernel
 //   EPI_SILU  interleaved (gate, up) columns -> bf16 silu(g)*u (model.cpp:226)
 //   EPI_F32   plain fp32 store (logits)
 #include <cuda.h>
@@ -413,14 +414,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int mt = w.mt * PAIR + rank, nt = w.nt, s = w.s;  // this CTA's 128-row tile
       const uint32_t acol = (uint32_t)(acc * BN);  // its accumulator's first TMEM column
       const int row = mt * kBM + quarter * 32 + lane;
-      int* flag = nullptr;
-      if (EPI == EPI_ADD && U.splits > 1) {  // ordered split-K: wait for split s-1 on these rows
-        flag = p.split_flags + ((size_t)(nt * U.num_m * PAIR + mt) * 4 + quarter);  // mt: this CTA's 128-row tile
-        if (lane == 0)
-          while (atomicAdd(flag, 0) != s) __nanosleep(64);
-        __syncwarp();
-        __threadfence();
-      }
       if constexpr (EPI == EPI_ADD) {
         // Coalesced residual epilogue: each 32x32 accumulator chunk (thread =
         // row) goes through a swizzled smem tile so that 8 lanes cover one
@@ -612,11 +605,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             });
           }
         }
-      }
-      if (flag) {
-        __threadfence();
-        __syncwarp();
-        if (lane == 0) atomicExch(flag, s + 1 == U.splits ? 0 : s + 1);
       }
       }
       tc_fence_before();
@@ -1716,7 +1704,10 @@ void gemm_bf16(rk_engine* e, const __nv_bfloat16* A, int lda, const __nv_bfloat1
   ps.rec.K = p.K;
   switch (p.epi) {
     case EPI_QKV: launch_bn<EPI_QKV>(e->stream, ta, tb, p, grid); break;
-    case EPI_ADD: launch_bn<EPI_ADD>(e->stream, ta, tb, p, grid); break;
+    case EPI_ADD:  // (unsplit: split-K residual GEMMs run as EPI_PART + splitk_reduce_add_kernel)
+      if (p.splits != 1) raise(RK_ERR_LOGIC, "residual GEMM epilogue with split-K");
+      launch_bn<EPI_ADD>(e->stream, ta, tb, p, grid);
+      break;
     case EPI_SILU: launch_bn<EPI_SILU>(e->stream, ta, tb, p, grid); break;
     case EPI_PART:  // partials, then splitk_reduce_add_kernel sums them in split order
       launch_bn<EPI_PART>(e->stream, ta, tb, p, grid);

@@ -29,7 +29,7 @@ struct GemmArgs {
   // the fp32 count), kind::tf32 MMAs (the 3xTF32 mode's K-concatenated
   // [hi|lo|hi] x [hi|hi|lo] operands); EPI_ADD / EPI_F32 only
   int tf32 = 0;
-  int* split_flags = nullptr;   // ordered split-K flags (EPI_ADD), zero-initialised
+  int* split_flags = nullptr;   // non-null: a residual GEMM may run split-K (EPI_PART partials + reduce)
   // outputs
   float* out_f32 = nullptr;     // EPI_ADD / EPI_F32, row stride ld_out
   int ld_out = 0;

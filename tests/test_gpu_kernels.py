@@ -96,7 +96,7 @@ ATT = [(64, 200, 4, 2, 64, "band"), (300, 700, 8, 2, 64, "sparse"), (130, 1000, 
        # GQA packing shapes: group 7 (Qwen2.5-7B: 28/4, 16 rows x 7 heads, 16 idle lanes), 16 (8 rows), 3, 8
        (500, 1800, 28, 4, 128, "live"), (333, 1200, 28, 4, 128, "mixed"), (260, 900, 32, 2, 64, "mixed"),
        (190, 640, 12, 4, 64, "sparse"), (450, 1500, 16, 2, 128, "live"),
-       # few static rows (<= 4, rows x group <= 16): the CUDA-core split-key kernel (attn_decode_kernel)
+       # few static rows (1-4; the top layer's last row, decode-capture steps)
        (1, 4032, 32, 8, 64, "band"), (4, 3000, 32, 8, 64, "sparse"), (2, 1000, 28, 4, 128, "band"),
        (3, 500, 8, 8, 64, "sparse"), (1, 1, 4, 2, 64, "band"), (1, 129, 16, 16, 128, "band"),
        (4, 129, 16, 2, 128, "sparse")]
