@@ -330,8 +330,9 @@ void select_topk(cudaStream_t s, const double* score, int n, int count, int* sel
 void seq_mean(cudaStream_t s, const float* x, int n, double* out);
 
 // fused agent schedule
+constexpr int kMaxFusedSegments = 32;  // upstream segments of one layer-major fused agent prefill
 struct SegCounts {
-  const int* count[8];
+  const int* count[kMaxFusedSegments];
 };
 void segment_offsets(cudaStream_t s, const SegCounts& c, int U, int start, int* offs);
 void gather_rows_to(cudaStream_t s, float* H, const int* off, const float* src, const int* idx, const int* count,

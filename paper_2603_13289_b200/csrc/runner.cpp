@@ -687,7 +687,7 @@ void Runner::agent_prefill(rk_context* ctx, const int32_t* prefix, uint64_t n_pr
     for (uint64_t u = 0; u < n_up; ++u) full.insert(full.end(), ups[u]->host_tokens.begin(), ups[u]->host_tokens.end());
     if (n_suffix) full.insert(full.end(), suffix, suffix + n_suffix);
     prefill(ctx, full.data(), full.size(), 0, true);
-  } else if (e_->fused && n_up <= 8) {
+  } else if (e_->fused && n_up <= (uint64_t)k::kMaxFusedSegments) {
     agent_fused(ctx, prefix, n_prefix, ups, n_up, suffix, n_suffix, prof, opts, results);
   } else {
     prefill(ctx, prefix, n_prefix, 0, false);

@@ -110,6 +110,30 @@ def test_agent_prefill_bit_exact(engine, oracle, mode, fused):
     engine.set_fused(1)
 
 
+def test_agent_prefill_many_segments_bit_exact(engine, oracle):
+    """Ten relayed segments (a deep agent chain) through the fused schedule:
+    bit-identical to the oracle's sequential order (the fused schedule takes
+    up to 32 segments; relay and blend)."""
+    spec = spec_of(8, 32, 4)
+    ow = oracle.weights(spec, 56)
+    caches = [oracle.scenario(ow, pattern_tokens(5 + i, 64, 10 + i), 6 + (i % 3), 1) for i in range(10)]
+    prof = triple(1, 2, 5)
+    for mode in ("relay", "blend"):
+        opts = RelayOptions.make(mode=mode, suffix_k=2, blend_alpha=0.25)
+        suffix = pattern_tokens(3, 64, 40)
+        logits, tok, octx = oracle.agent_prefill(ow, pattern_tokens(4, 64, 41), caches, suffix, prof, opts)
+        w = engine.weights(spec, 56)
+        ctx = w.context()
+        got = ctx.agent_prefill(pattern_tokens(4, 64, 41), [w.upload_cache(c) for c in caches], suffix, prof, opts)
+        assert_bit_equal(got["logits"], logits, f"many.{mode}.logits")
+        assert got["first_token"] == tok
+        K, V = ctx.all()
+        Ko, Vo = oracle.ctx_all(octx)
+        assert_bit_equal(K, Ko, f"many.{mode}.K")
+        assert_bit_equal(V, Vo, f"many.{mode}.V")
+        assert len(ctx.segments()) == 10
+
+
 def test_zero_mode_round_trip(engine, oracle):
     """ZERO with the unchanged prefix reproduces decode-time KV (test_engine.cpp:124-137)."""
     spec = spec_of(8, 32, 4)
