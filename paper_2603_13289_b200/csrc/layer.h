@@ -99,7 +99,6 @@ class Runner {
   ExtendSlot& slot(int i);
   void wait_cache_meta(rk_cache* c);
   void wait_cache_layer(rk_cache* c, uint64_t layer);
-  void wait_cache_all(rk_cache* c);
 
   rk_engine* e_;
   rk_weights* w_;

@@ -52,14 +52,6 @@ void Runner::wait_cache_layer(rk_cache* c, uint64_t l) {
   ensure_cache_layer(c, l);
   if (c->async) RK_CUDA(cudaStreamWaitEvent(st_, c->ev_layer[l], 0));
 }
-void Runner::wait_cache_all(rk_cache* c) {
-  if (c->async) {
-    ensure_cache_all(c);  // (deferred layers go last on the copy stream)
-    RK_CUDA(cudaStreamWaitEvent(st_, c->ev_meta, 0));
-    for (cudaEvent_t ev : c->ev_layer)
-      if (ev) RK_CUDA(cudaStreamWaitEvent(st_, ev, 0));
-  }
-}
 
 ExtendSlot& Runner::slot(int i) {
   while ((int)e_->slots.size() <= i) e_->slots.emplace_back(new ExtendSlot());
