@@ -199,6 +199,39 @@ __device__ __forceinline__ float attn_merge_stream(const AttnArgs& a, const floa
   return chk;
 }
 
+// Split-KV merge of a lane slice [l0, l1) of the tile (cooperative merge: each
+// part of a cluster-launched tile merges its own slice once all parts have
+// written their partials); weights wsm[lane][16] as above.
+template <int DH, int NP>
+__device__ __forceinline__ float attn_merge_slice(const AttnArgs& a, const float4* src, const float* wsm, int rl,
+                                                  int ts, int l0, int l1, int r0, int r1, int rq, int G, int h0) {
+  constexpr int F4 = DH / 4;
+  float chk = 0.f;
+#pragma unroll 2
+  for (int f = l0 * F4 + rl; f < l1 * F4; f += 128) {
+    float4 v[NP];
+#pragma unroll
+    for (int z = 0; z < NP; ++z) v[z] = __ldcg(src + (size_t)min(z, ts - 1) * kQ * F4 + f);
+    const int ln = f / F4;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int z = 0; z < NP; ++z) {
+      const float wz = wsm[ln * 16 + z];
+      acc.x += wz * v[z].x;
+      acc.y += wz * v[z].y;
+      acc.z += wz * v[z].z;
+      acc.w += wz * v[z].w;
+    }
+    const int hl = ln / rq, row = r0 + ln % rq;
+    if (hl < G && row < r1) {
+      chk = fmaf(acc.x + acc.y + acc.z + acc.w, 0.f, chk);
+      *reinterpret_cast<uint2*>(a.out + (size_t)row * (a.H * DH) + (h0 + hl) * DH + 4 * (f % F4)) =
+          make_uint2(pack_bf16(acc.x, acc.y), pack_bf16(acc.z, acc.w));
+    }
+  }
+  return chk;
+}
+
 // POLY: bit c set -> the 4 pairs of 16-byte chunk c (of 8 per 64-key block)
 // take the FMA-pipe cubic instead of MUFU.EX2 (0x88: a quarter of the exps).
 template <int DH, bool TRACE, int POLY = 0x88>
@@ -528,6 +561,54 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
       fence_acq_rel_gpu();  // (release: this part's partials)
       named_bar_sync(1, 128);
       int* cnt = a.tile_cnt + tid;
+      if (a.coop) {
+        // the tile's parts are one cluster (co-scheduled): wait for all of
+        // them, then each merges its slice of the 128 lanes in one round of
+        // loads -- instead of the last part streaming every lane alone
+        if (rl == 0) {
+          atomicAdd(cnt, 1);
+          uint32_t spins = 0;
+          while (*reinterpret_cast<volatile int*>(cnt) < ts_eff) {
+            __nanosleep(64);
+            if (++spins > (1u << 26)) __trap();  // (a scheduling bug traps instead of hanging)
+          }
+        }
+        named_bar_sync(1, 128);
+        fence_acq_rel_gpu();  // (acquire: every part's partials)
+        const int l0 = part * kQ / ts_eff, l1 = (part + 1) * kQ / ts_eff;
+        float* wsm = reinterpret_cast<float*>(smem + C::OFF_K);  // [lane][16]
+        const size_t blk0 = tid * gridDim.x * kQ;
+        if (rl < l1 - l0) {
+          const int ln = l0 + rl;
+          float mz[16], lz[16];
+#pragma unroll
+          for (int z = 0; z < 16; ++z) {
+            const float2 v = __ldcg(reinterpret_cast<const float2*>(a.ws_ml) + blk0 + (size_t)min(z, ts_eff - 1) * kQ + ln);
+            mz[z] = z < ts_eff ? v.x : -INFINITY;
+            lz[z] = v.y;
+          }
+          float m = -INFINITY;
+#pragma unroll
+          for (int z = 0; z < 16; ++z) m = fmaxf(m, mz[z]);
+          float lsum = 0.f;
+#pragma unroll
+          for (int z = 0; z < 16; ++z) {
+            mz[z] = mz[z] == -INFINITY ? 0.f : fast_exp2(mz[z] - m);
+            lsum += mz[z] * lz[z];
+          }
+          const float inv = 1.f / lsum;
+#pragma unroll
+          for (int z = 0; z < 16; ++z) wsm[ln * 16 + z] = mz[z] * inv;
+        }
+        named_bar_sync(1, 128);
+        const float4* src = reinterpret_cast<const float4*>(a.ws_o) + blk0 * (DH / 4);
+        float chk = 0.f;
+        if (ts_eff <= 4) chk = attn_merge_slice<DH, 4>(a, src, wsm, rl, ts_eff, l0, l1, r0, r1, rq, G, h0);
+        else chk = attn_merge_slice<DH, 8>(a, src, wsm, rl, ts_eff, l0, l1, r0, r1, rq, G, h0);
+        if (chk != chk && a.status) *reinterpret_cast<volatile int*>(a.status) = 1;
+        named_bar_sync(1, 128);
+        if (rl == 0 && atomicAdd(cnt, 1) == 2 * ts_eff - 1) *cnt = 0;  // the last to leave resets it
+      } else {
       if (rl == 0) *s_last = atomicAdd(cnt, 1) == ts_eff - 1;
       named_bar_sync(1, 128);
       if (tracing) a.trace[(64 + 0) * 8 + 4] = clock64();
@@ -568,6 +649,7 @@ __global__ void __launch_bounds__(kThreadsA, ACfg<DH>::CTAS)
         if (chk != chk && a.status) *reinterpret_cast<volatile int*>(a.status) = 1;
         if (tracing) a.trace[(64 + 0) * 8 + 5] = clock64();
       }
+      }  // (last-arriver merge)
     } else {
       const float inv = 1.f / l_run;
       uint4* dst = reinterpret_cast<uint4*>(a.out + (size_t)row * (a.H * DH) + h * DH);
@@ -682,18 +764,37 @@ void launch_attn(rk_engine* e, const CUtensorMap& tq, const CUtensorMap& tk, con
     attr = true;
   }
   dim3 grid(a.splits, a.group > 1 ? a.Hkv : a.H, max_tiles(a));
+  // split launches: a tile's parts form one cluster, so they are co-scheduled
+  // and merge cooperatively (RK_ATTN_COOP=0: the last part merges alone)
+  static const bool coop_env = [] {
+    const char* v = std::getenv("RK_ATTN_COOP");
+    return v ? std::atoi(v) != 0 : true;
+  }();
+  AttnArgs ac = a;
+  ac.coop = coop_env && a.splits > 1 && a.splits <= 8 && !a.trace;
   auto go = [&](auto kern) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = dim3(kThreadsA);
     cfg.dynamicSmemBytes = ACfg<DH>::SMEM;
     cfg.stream = e->stream;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    if (pdl_enabled()) {
+      at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[na].val.programmaticStreamSerializationAllowed = 1;
+      ++na;
+    }
+    if (ac.coop) {
+      at[na].id = cudaLaunchAttributeClusterDimension;
+      at[na].val.clusterDim.x = (unsigned)a.splits;
+      at[na].val.clusterDim.y = 1;
+      at[na].val.clusterDim.z = 1;
+      ++na;
+    }
     cfg.attrs = at;
-    cfg.numAttrs = pdl_enabled() ? 1 : 0;
-    RK_CUDA(cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, a));
+    cfg.numAttrs = na;
+    RK_CUDA(cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, ac));
   };
   if (a.trace) go(attn_kernel<DH, true>);
   else if (poly == 0xAA) go(attn_kernel<DH, false, 0xAA>);

@@ -96,7 +96,7 @@ struct AttnArgs {
   // debug: clock64 timeline of the last CTA of head 0 ([role 0..2][step < 64][event < 8];
   // roles: softmax group 0, group 1, MMA issuer)
   unsigned long long* trace = nullptr;
-  int pingpong = 1;  // set by attention_bf16
+  int coop = 0;  // split parts launched as one cluster: every part merges a slice (set by attention_bf16)
   int group = 1, rq = 128;  // GQA packing (set by attention_bf16): q heads per CTA, rows per head
   int rows_hint = 0;        // expected live rows (Rows::hint) for the split-KV plan
   int* status = nullptr;  // non-finite output flag (engine status[0], set by attention_bf16)
