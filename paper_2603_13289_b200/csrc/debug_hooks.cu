@@ -45,9 +45,9 @@ int rk_debug_gemm_tc(rk_engine* e, const float* A, const float* B, float* C, int
   return guard([&] {
     cudaStream_t st = e->stream;
     DevBuf a((size_t)M * K * 4), b((size_t)K * N * 4), bt((size_t)3 * K * N * 4), c((size_t)M * N * 4);
-    RK_CUDA(cudaMemcpy(a.p, A, (size_t)M * K * 4, cudaMemcpyHostToDevice));
-    RK_CUDA(cudaMemcpy(b.p, B, (size_t)K * N * 4, cudaMemcpyHostToDevice));
-    RK_CUDA(cudaMemcpy(c.p, C, (size_t)M * N * 4, cudaMemcpyHostToDevice));
+    RK_CUDA(cudaMemcpyAsync(a.p, A, (size_t)M * K * 4, cudaMemcpyHostToDevice, e->stream));
+    RK_CUDA(cudaMemcpyAsync(b.p, B, (size_t)K * N * 4, cudaMemcpyHostToDevice, e->stream));
+    RK_CUDA(cudaMemcpyAsync(c.p, C, (size_t)M * N * 4, cudaMemcpyHostToDevice, e->stream));
     tc::pack_weight(st, bt.as<float>(), b.as<float>(), N, 0, 1, K, N);
     Rows rows{M, nullptr, nullptr};
     tc::gemm(e, a.as<float>(), K, rows, bt.as<float>(), N, K, c.as<float>(), N, add != 0);
@@ -63,8 +63,8 @@ int rk_debug_gemm_bf16(rk_engine* e, const float* A, const float* B, float* C, i
     cudaStream_t st = e->stream;
     DevBuf a = to_bf16(st, A, (size_t)rows_max * K), b = to_bf16(st, B, (size_t)N * K);
     DevBuf c((size_t)rows_max * N * 4), live(4), flags(1 << 18);
-    RK_CUDA(cudaMemcpy(c.p, C, (size_t)rows_max * N * 4, cudaMemcpyHostToDevice));
-    RK_CUDA(cudaMemcpy(live.p, &live_rows, 4, cudaMemcpyHostToDevice));
+    RK_CUDA(cudaMemcpyAsync(c.p, C, (size_t)rows_max * N * 4, cudaMemcpyHostToDevice, e->stream));
+    RK_CUDA(cudaMemcpyAsync(live.p, &live_rows, 4, cudaMemcpyHostToDevice, e->stream));
     RK_CUDA(cudaMemset(flags.p, 0, 1 << 18));
     GemmArgs g;
     g.rows_max = rows_max;
@@ -89,8 +89,8 @@ int rk_debug_attention_bf16(rk_engine* e, const float* q, const float* kk, const
     DevBuf qb = to_bf16(st, q, (size_t)M * H * dh), kb = to_bf16(st, kk, (size_t)T * Hkv * dh),
            vb = to_bf16(st, v, (size_t)T * Hkv * dh);
     DevBuf p(M * 4 + 16), o((size_t)M * H * dh * 2), of((size_t)M * H * dh * 4);
-    RK_CUDA(cudaMemcpy(p.p, pos, M * 4, cudaMemcpyHostToDevice));
-    RK_CUDA(cudaMemcpy(p.as<int>() + M, &live, 4, cudaMemcpyHostToDevice));
+    RK_CUDA(cudaMemcpyAsync(p.p, pos, M * 4, cudaMemcpyHostToDevice, e->stream));
+    RK_CUDA(cudaMemcpyAsync(p.as<int>() + M, &live, 4, cudaMemcpyHostToDevice, e->stream));
     RK_CUDA(cudaMemsetAsync(o.p, 0, (size_t)M * H * dh * 2, st));
     AttnArgs a;
     a.q = qb.as<__nv_bfloat16>();
@@ -162,8 +162,8 @@ int rk_debug_bench_attention_rows(rk_engine* e, const int32_t* pos, int M, int l
     k::f32_to_bf16(st, kb.as<__nv_bfloat16>(), f.as<float>(), nk);
     k::init_uniform(st, f.as<float>(), nk, 13, 1.0f);
     k::f32_to_bf16(st, vb.as<__nv_bfloat16>(), f.as<float>(), nk);
-    RK_CUDA(cudaMemcpy(p.p, pos, M * 4, cudaMemcpyHostToDevice));
-    RK_CUDA(cudaMemcpy(p.as<int>() + M, &live, 4, cudaMemcpyHostToDevice));
+    RK_CUDA(cudaMemcpyAsync(p.p, pos, M * 4, cudaMemcpyHostToDevice, e->stream));
+    RK_CUDA(cudaMemcpyAsync(p.as<int>() + M, &live, 4, cudaMemcpyHostToDevice, e->stream));
     AttnArgs a;
     a.q = qb.as<__nv_bfloat16>();
     a.out = o.as<__nv_bfloat16>();
@@ -210,8 +210,8 @@ int rk_debug_trace_attention_rows(rk_engine* e, const int32_t* pos, int M, int l
     k::f32_to_bf16(st, kb.as<__nv_bfloat16>(), f.as<float>(), nk);
     k::init_uniform(st, f.as<float>(), nk, 13, 1.0f);
     k::f32_to_bf16(st, vb.as<__nv_bfloat16>(), f.as<float>(), nk);
-    RK_CUDA(cudaMemcpy(p.p, pos, M * 4, cudaMemcpyHostToDevice));
-    RK_CUDA(cudaMemcpy(p.as<int>() + M, &live, 4, cudaMemcpyHostToDevice));
+    RK_CUDA(cudaMemcpyAsync(p.p, pos, M * 4, cudaMemcpyHostToDevice, e->stream));
+    RK_CUDA(cudaMemcpyAsync(p.as<int>() + M, &live, 4, cudaMemcpyHostToDevice, e->stream));
     AttnArgs a;
     a.q = qb.as<__nv_bfloat16>();
     a.out = o.as<__nv_bfloat16>();
@@ -399,11 +399,11 @@ int rk_debug_score_deviation(rk_engine* e, const void* ctx_v, const void* cache_
     cudaStream_t st = e->stream;
     const size_t bytes = (size_t)n * heads * dh * elem, rbytes = (size_t)(base + n) * dh / 2 * 16;
     DevBuf a(bytes), b(bytes), c(bytes), d(bytes), r(rbytes), sd((size_t)n * 8), sk((size_t)n * 8);
-    RK_CUDA(cudaMemcpy(a.p, ctx_v, bytes, cudaMemcpyHostToDevice));
-    RK_CUDA(cudaMemcpy(b.p, cache_v, bytes, cudaMemcpyHostToDevice));
-    RK_CUDA(cudaMemcpy(c.p, ctx_k, bytes, cudaMemcpyHostToDevice));
-    RK_CUDA(cudaMemcpy(d.p, cache_kpre, bytes, cudaMemcpyHostToDevice));
-    RK_CUDA(cudaMemcpy(r.p, rope, rbytes, cudaMemcpyHostToDevice));
+    RK_CUDA(cudaMemcpyAsync(a.p, ctx_v, bytes, cudaMemcpyHostToDevice, e->stream));
+    RK_CUDA(cudaMemcpyAsync(b.p, cache_v, bytes, cudaMemcpyHostToDevice, e->stream));
+    RK_CUDA(cudaMemcpyAsync(c.p, ctx_k, bytes, cudaMemcpyHostToDevice, e->stream));
+    RK_CUDA(cudaMemcpyAsync(d.p, cache_kpre, bytes, cudaMemcpyHostToDevice, e->stream));
+    RK_CUDA(cudaMemcpyAsync(r.p, rope, rbytes, cudaMemcpyHostToDevice, e->stream));
     k::score_deviation(st, a.p, b.p, c.p, d.p, (size_t)elem, n, heads * dh, heads, dh, r.as<double2>(), base,
                        sd.as<double>(), sk.as<double>());
     RK_CUDA(cudaStreamSynchronize(st));
@@ -417,7 +417,7 @@ int rk_debug_select_topk(rk_engine* e, const double* score, int n, int count, in
   return guard([&] {
     cudaStream_t st = e->stream;
     DevBuf sc((size_t)n * 8 + 8), idx((size_t)n * 4 + 4), tags((size_t)2 * n * 4 + 8), info(64);
-    RK_CUDA(cudaMemcpy(sc.p, score, (size_t)n * 8, cudaMemcpyHostToDevice));
+    RK_CUDA(cudaMemcpyAsync(sc.p, score, (size_t)n * 8, cudaMemcpyHostToDevice, e->stream));
     RK_CUDA(cudaMemset(info.p, 0, 64));
     k::select_topk(st, sc.as<double>(), n, count, idx.as<int>(), tags.as<uint32_t>(), info.as<int>());
     RK_CUDA(cudaStreamSynchronize(st));
@@ -433,9 +433,9 @@ int rk_debug_select_relay(rk_engine* e, const double* s_dev, const float* influe
   return guard([&] {
     cudaStream_t st = e->stream;
     DevBuf sd(n * 8), inf(n * 4), im(8), idx(n * 4), tags(2 * n * 4), info(64), di(64);
-    RK_CUDA(cudaMemcpy(sd.p, s_dev, n * 8, cudaMemcpyHostToDevice));
-    RK_CUDA(cudaMemcpy(inf.p, influence, n * 4, cudaMemcpyHostToDevice));
-    RK_CUDA(cudaMemcpy(im.p, &infl_mean, 8, cudaMemcpyHostToDevice));
+    RK_CUDA(cudaMemcpyAsync(sd.p, s_dev, n * 8, cudaMemcpyHostToDevice, e->stream));
+    RK_CUDA(cudaMemcpyAsync(inf.p, influence, n * 4, cudaMemcpyHostToDevice, e->stream));
+    RK_CUDA(cudaMemcpyAsync(im.p, &infl_mean, 8, cudaMemcpyHostToDevice, e->stream));
     RK_CUDA(cudaMemset(info.p, 0, 64));
     k::select_relay(st, sd.as<double>(), inf.as<float>(), im.as<double>(), n, tau_dev, tau_inf, suffix_k,
                     idx.as<int>(), tags.as<uint32_t>(), info.as<int>(), di.as<double>(), e->side, e->side_fork,
@@ -453,7 +453,7 @@ int rk_debug_select_relay(rk_engine* e, const double* s_dev, const float* influe
 int rk_debug_expf(rk_engine* e, const float* x, float* y, uint64_t n) {
   return guard([&] {
     DevBuf dx(n * 4), dy(n * 4);
-    RK_CUDA(cudaMemcpy(dx.p, x, n * 4, cudaMemcpyHostToDevice));
+    RK_CUDA(cudaMemcpyAsync(dx.p, x, n * 4, cudaMemcpyHostToDevice, e->stream));
     expf_kernel<<<1024, 256, 0, e->stream>>>(dx.as<float>(), dy.as<float>(), n);
     RK_CUDA(cudaStreamSynchronize(e->stream));
     RK_CUDA(cudaMemcpy(y, dy.p, n * 4, cudaMemcpyDeviceToHost));
