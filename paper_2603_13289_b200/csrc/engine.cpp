@@ -137,11 +137,13 @@ RopeTable* rope_table(rk_engine* e, float theta, uint64_t d_head, uint64_t posit
     }
   }
   t->cs.alloc(h.size() * sizeof(double2));
-  RK_CUDA(cudaMemcpy(t->cs.p, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  // (stream-ordered: a pageable cudaMemcpy may return before its DMA lands,
+  // and the kernels reading the table run on the non-blocking engine stream)
+  RK_CUDA(cudaMemcpyAsync(t->cs.p, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice, e->stream));
   std::vector<float2> hf(h.size());
   for (size_t i = 0; i < h.size(); ++i) hf[i] = make_float2((float)h[i].x, (float)h[i].y);
   t->csf.alloc(hf.size() * sizeof(float2));
-  RK_CUDA(cudaMemcpy(t->csf.p, hf.data(), hf.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  RK_CUDA(cudaMemcpyAsync(t->csf.p, hf.data(), hf.size() * sizeof(float2), cudaMemcpyHostToDevice, e->stream));
   e->rope.push_back(std::move(t));
   return e->rope.back().get();
 }
