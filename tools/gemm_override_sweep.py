@@ -28,6 +28,12 @@ SETS = {
         ("4032d:2048:8192", "gemm_add", ["256/2/1", "256/2/2", "128/2/2", "256/2/3"]),
         ("4032d:2048:2048", "gemm_add", ["256/2/1", "256/2/2", "128/2/2"]),
     ],
+    "sparse192": [
+        ("4032d:2048:2048", "gemm_add", ["192/2/1", "256/2/1", "128/2/1", "64/2/1", "128/1/1", "128/1/2", "256/1/2"]),
+        ("4032d:2048:8192", "gemm_add", ["192/2/1", "256/2/1", "128/2/1", "256/1/2", "256/1/3", "128/1/3"]),
+        ("4032d:3072:2048", "gemm_qkv_m4032dyn_n3072", ["256/2/1", "192/2/1", "128/2/1"]),
+        ("4032d:16384:2048", "gemm_silu_m4032dyn", ["192/2/1", "256/2/1", "128/2/1"]),
+    ],
     "band": [
         ("4032:3072:2048", "gemm_qkv_m4032_", ["256/2/1", "128/2/1", "256/1/1"]),
         ("4032:2048:2048", "gemm_add", ["256/2/1", "128/2/1", "128/1/1", "256/1/1"]),
