@@ -839,14 +839,14 @@ void attention_bf16(rk_engine* e, const AttnArgs& a_in, const __nv_bfloat16* ctx
   a.tiles_per_split = nk_max > 0 ? nk_max : 1;
   // Adaptive split-KV when the grid cannot fill ~1.5 waves: the longest
   // tile should not walk more key tiles than the average load of a resident
-  // slot (~ base * nk_max / (2 * slots), causal), and no part below 4 key
+  // slot (~ base * nk_max / (2 * slots), causal), and no part below 6 key
   // tiles (a CTA's fixed cost is a few microseconds). Only tiles longer than
   // that are cut (per tile, on the device); the rest write their output
   // directly. (Measured: a uniform 2-way split of the c2 sparse layers and a
   // column-split softmax with two warpgroups per tile were both slower.)
   static const int min_part = [] {
     const char* v = std::getenv("RK_ATTN_MINPART");
-    return v ? std::max(1, std::atoi(v)) : 4;
+    return v ? std::max(1, std::atoi(v)) : 6;  // (4 before the cooperative merge; 6 measured best with it, r02cd/r02ck)
   }();
   static const double split_div = [] {
     const char* v = std::getenv("RK_ATTN_SPLITDIV");
